@@ -1,0 +1,362 @@
+"""Benchmark of the robust Reference Governor step on B200 (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1]): the bench snapshot of the
+reference's bench_sweep (harness.py:269-271) -- surrogate fuel-cell plant,
+h = 0.01, Y = [-0.9, 0.9], eps = 0.05, x0 = 0, v_prev = 0, r = 0.5, M = 32
+candidates, j* = 256, U(+-0.001) disturbances, 1000 scenarios per GPU, a fresh
+scenario seed every step.  All 32 rows are feasible, so one step is exactly
+32 * n_sim * 256 cell-steps (one cell-step = one RK4 transition of one
+(candidate, scenario) rollout with its fused checks).
+
+  value  device-resident throughput: the fused step kernel (RNG in-kernel, so
+         inputs are the step's scalars), CUDA events on the launching stream,
+         L2 flushed between steps.  cell-steps/s over all ranks.
+  e2e    the same metric through the public API robust_rg_parallel() with
+         host buffers in and the KappaResult (incl. P) back on the host.
+  --impl reference  the reference's CPU path (oracle C port of the numba
+         kernels, kernels.py:47-162, with the reference's fill partition) on
+         every host core, same workload.
+
+Multi-GPU (torchrun): rank r takes scenarios [r*n, (r+1)*n) of one global
+stream (weak scaling); per-row violation counts are summed with one NCCL
+all-reduce per step and every rank extracts the same row.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "robust RG step latency (ms) at N scenarios; scenario-steps/sec vs FP64 roofline"
+UNIT = "cell-steps/s"
+FLOPS_PER_CELL_STEP = 210  # 58 explicit ops + 4 tanh x 38
+J_STAR, M_GRID, N_PER_GPU, R_REF = 256, 32, 1000, 0.5
+BASE_SEED = 7
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="own", choices=["own", "reference"])
+    ap.add_argument("--n-sim", type=int, default=N_PER_GPU, help="scenarios per GPU")
+    ap.add_argument("--j-star", type=int, default=J_STAR)
+    ap.add_argument("--e2e-steps", type=int, default=300)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
+        int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([s.strip() for s in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 7
+                          for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU baseline
+
+def cpu_baseline(n_sim: int, j_star: int, seconds: float, reps_max: int = 20):
+    """The reference's CPU path (oracle port) on this host: multicore on every
+    core, plus one serial rep; presampled scenarios like bench_sweep's
+    kernel-only mode (harness.py:345-354)."""
+    from oracle import oracle as orc
+
+    cores = orc.cpu_count()
+    tlo, thi = orc.tighten(-0.9, 0.9, 0.0, 0.05)
+    dist = orc.sample(BASE_SEED, n_sim, j_star + 1, [(-0.001, 0.001)] * 3)
+    x0 = np.zeros(3)
+    cells = M_GRID * n_sim * j_star
+
+    def one(workers):
+        t0 = time.perf_counter()
+        k, v, feas, _, _, st = orc.grid_step(0.01, x0, 0.0, R_REF, M_GRID, dist, -0.9, 0.9, tlo,
+                                             thi, j_star, workers=workers)
+        dt = time.perf_counter() - t0
+        assert st["early_terms"] == 0 and feas and k == 1.0
+        return dt
+
+    one(cores)  # warm-up: thread creation and page faults stay out of the clock
+    times, t_end = [], time.perf_counter() + seconds
+    while len(times) < reps_max and (not times or time.perf_counter() < t_end):
+        times.append(one(cores))
+    ser_cells = M_GRID * min(n_sim, 250) * j_star
+    d_ser = dist[: min(n_sim, 250)]
+    t0 = time.perf_counter()
+    orc.grid_step(0.01, x0, 0.0, R_REF, M_GRID, d_ser, -0.9, 0.9, tlo, thi, j_star, workers=1)
+    t_ser = time.perf_counter() - t0
+    best = min(times)
+    return {
+        "value": cells / best, "unit": UNIT, "cores": cores, "kind": "port",
+        "sample": f"{len(times)} robust grid steps (M={M_GRID}, n_sim={n_sim}, j*={j_star}, "
+                  f"presampled scenarios) on {cores} threads, best rep",
+        "ms_per_step": best * 1e3, "ms_per_step_mean": statistics.mean(times) * 1e3,
+        "serial_1core": {"value": ser_cells / t_ser, "unit": UNIT,
+                         "sample": f"1 step at n_sim={min(n_sim, 250)}"},
+    }
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    n_sim = args.n_sim * world
+    cb = cpu_baseline(n_sim, args.j_star, args.cpu_seconds)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": cb["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2 bench snapshot: robust grid step", "n_sim": n_sim,
+                   "j_star": args.j_star, "m_grid": M_GRID, "plant": "surrogate-fc",
+                   "disturbance": "U(+-0.001)", "r": R_REF},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "serial_1core": cb["serial_1core"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- own arm
+
+def run_own(args, rank, world, local_rank):
+    import torch
+
+    import paper_2510_08288_b200 as rg
+    from paper_2510_08288_b200 import _capi
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    ctx = _capi.context(local_rank)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr, device=torch.device("cuda", local_rank))
+
+    n_sim, j_star = args.n_sim, args.j_star
+    k0 = rank * n_sim
+    cells_rank = M_GRID * n_sim * j_star
+    plant = rg.make_plant("surrogate-fc")
+    box = rg.ConstraintSet(-0.9, 0.9, anchor=0.0)
+    tight = rg.tighten(box, 0.05)
+    v_lo, v_hi = rg.admissible_setpoints(tight.lower, tight.upper)
+    prob = _capi.Problem(0.01, -0.9, 0.9, v_lo, v_hi, j_star, 0)
+    model = rg.DisturbanceModel.scaled(0.001, 3)
+    x0 = np.zeros(3)
+    lib = ctx.lib
+    res = _capi.GridResult()
+    viol = torch.zeros(M_GRID, dtype=torch.int32, device=f"cuda:{local_rank}")
+    flags = _capi.RG_ASYNC | _capi.RG_NO_TIMING
+    if world > 1:
+        flags |= _capi.RG_DEVICE_PTRS
+    x0_arg = x0.ctypes.data_as(ctypes_vp()) if world == 1 else \
+        torch.zeros(3, dtype=torch.float64, device=f"cuda:{local_rank}")
+    x0_ptr = x0_arg if world == 1 else ctypes_vp()(x0_arg.data_ptr())
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32,
+                        device=f"cuda:{local_rank}")
+    big = torch.tensor(1 << 40, dtype=torch.int64, device=f"cuda:{local_rank}")
+
+    def step(s):
+        scen = _capi.make_scenarios(BASE_SEED + s, k0, n_sim, model.lo, model.span)
+        _capi.check(lib.rg_grid_step(ctx.handle, prob, x0_ptr, 0.0, R_REF, M_GRID, 0, None,
+                                     n_sim, 0, scen,
+                                     ctypes_vp()(viol.data_ptr()) if world > 1 else None,
+                                     None, res, flags))
+        if world > 1:
+            import torch.distributed as dist
+            c = viol.to(torch.int64)
+            c = torch.where(c == -1, big, c)
+            dist.all_reduce(c)
+            full = c == 0
+            idx = torch.arange(M_GRID, device=c.device)
+            best = torch.where(full, idx, torch.full_like(idx, -1)).max()
+            return best
+        return None
+
+    with torch.cuda.stream(stream):
+        for s in range(args.warmup):
+            step(s)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        sampler = ClockSampler(local_rank)
+        sampler.start()
+        time.sleep(0.2)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        w0 = time.perf_counter()
+        for s in range(args.steps):
+            flush.zero_()  # L2 (126 MB) flush between timed steps, outside the events
+            ev[s][0].record(stream)
+            step(args.warmup + s)
+            ev[s][1].record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+        if world > 1:
+            torch.distributed.barrier()
+        clocks = sampler.stop()
+    per = np.array([a.elapsed_time(b) for a, b in ev])  # ms
+    total_ms = float(per.sum())
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local_rank}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    # the step's decision must be the reference's: all 32 rows feasible -> kappa = 1
+    out = _capi.GridResult()
+    _capi.check(lib.rg_grid_fetch(ctx.handle, None, M_GRID, out))
+    if world == 1:
+        assert out.row == M_GRID - 1 and out.early_terms == 0, (out.row, out.early_terms)
+
+    cells_total = cells_rank * world * args.steps
+    value = cells_total / (total_ms * 1e-3)
+    ms_per_step = total_ms / args.steps
+
+    # dominant kernel: k_grid.  Its share of the step is 100% at N=1; its own
+    # duration is the event time (one launch per event pair).
+    kernel_ms = float(np.mean(per)) if world == 1 else None
+    peak = ctx.fp64_peak()
+    roof = None
+    if kernel_ms:
+        achieved = FLOPS_PER_CELL_STEP * cells_rank / (kernel_ms * 1e-3)
+        roof = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
+                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": _ncu_traffic(),
+                "peak_source": "measured in this run: rg_fp64_peak (independent DFMA chains, "
+                               "2 flop per DFMA); MEASURED_PEAKS.json has no FP64 figure",
+                "flops_per_cell_step": FLOPS_PER_CELL_STEP, "cell_steps_per_launch": cells_rank,
+                "kernel_ms": kernel_ms}
+
+    # e2e through the public API with host buffers (rank-local shard)
+    e2e = None
+    if world == 1:
+        cfg = rg.GovernorConfig(j_star=j_star, m_grid=M_GRID, n_sim=n_sim)
+        for s in range(5):
+            rg.robust_rg_parallel(plant, x0, rg.GovernorState(0.0), R_REF, box,
+                                  rg.sample_scenarios(model, n_sim, j_star + 1, seed=s), cfg)
+        t0 = time.perf_counter()
+        for s in range(args.e2e_steps):
+            scen = rg.sample_scenarios(model, n_sim, j_star + 1, seed=BASE_SEED + s)
+            r = rg.robust_rg_parallel(plant, x0, rg.GovernorState(0.0), R_REF, box, scen, cfg)
+        t_e2e = (time.perf_counter() - t0) / args.e2e_steps
+        assert r.kappa_opt == 1.0 and r.matrix.all()
+        h2d = 3 * 8 + 2 * 8 + 9 * 8   # x0, v_prev/r, scenario stream descriptor (kernel params)
+        d2h = (M_GRID * ((n_sim + 31) // 32) * 4) + M_GRID * 4 + 64  # P bits, counts, result
+        e2e = {"value": cells_rank / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e * 1e3,
+               "api": "paper_2510_08288_b200.robust_rg_parallel (keep_matrix=True)"}
+
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        c = cpu_baseline(n_sim, j_star, args.cpu_seconds)
+        cb = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cb["serial_1core"] = c["serial_1core"]
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "C2 bench snapshot: robust grid step (Alg. 3), fused RNG",
+                       "n_sim": n_sim * world, "n_sim_per_gpu": n_sim, "j_star": j_star,
+                       "m_grid": M_GRID, "plant": "surrogate-fc", "disturbance": "U(+-0.001)",
+                       "r": R_REF, "cell_steps_per_step": cells_rank * world,
+                       "l2": "flushed between timed steps (256 MB write, outside the events)",
+                       "parallelism": f"scenario shards x{world}" + (", NCCL all-reduce of "
+                                                                     "row counts" if world > 1
+                                                                     else "")},
+            "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
+            "gpu_launches": args.steps, "clocks": clocks,
+            "wall_ms_per_step": wall * 1e3 / args.steps,
+            "kernel_ms_p50": float(np.median(per)), "kernel_ms_min": float(per.min()),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def ctypes_vp():
+    import ctypes
+    return ctypes.c_void_p
+
+
+def _ncu_traffic():
+    """dram bytes per k_grid launch from the committed ncu --set full summary."""
+    p = ROOT / "profiles" / "k_grid_traffic.json"
+    try:
+        return json.loads(p.read_text())["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        return None
+
+
+def main():
+    args = parse()
+    rank, world, local_rank = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_own(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

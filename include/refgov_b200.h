@@ -1,0 +1,180 @@
+/*
+ * refgov_b200.h -- C ABI of the B200-native robust Reference Governor hot path.
+ *
+ * Drop-in boundary for the reference package `refgov` (arxiv 2510.08288,
+ * pkg/src/refgov).  The reference reaches its device through a subprocess
+ * and temp-file protocol (backend_gpu.fill, backend_gpu.py:50-140) and runs
+ * its CPU hot loop in numba (kernels.py:47-162); this library replaces both
+ * with in-process calls into sm_100a kernels.  Plain C types only: host or
+ * device pointers plus sizes; no torch or CUDA types in any signature.
+ *
+ * Return codes map onto the reference's error taxonomy (errors.py:8-32):
+ *   RG_OK              0
+ *   RG_E_NODEVICE     -1  -> BackendUnavailableError (no CUDA device)
+ *   RG_E_UNSUPPORTED  -2  -> BackendUnavailableError (not sm_100, or a host
+ *                            libm whose tanh neither port reproduces)
+ *   RG_E_ARGS         -3  -> ConfigError (shapes, ranges)
+ *   RG_E_CUDA         -4  -> RefgovError (device failure)
+ * rg_last_error() returns a thread-local message for the last failure.
+ *
+ * Threading: one call at a time per context (the reference's governor is not
+ * re-entrant either).  Calls are synchronous unless RG_ASYNC is
+ * passed; results are on the host when a synchronous call returns.
+ */
+#ifndef REFGOV_B200_H
+#define REFGOV_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define RG_API __attribute__((visibility("default")))
+#else
+#define RG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RG_ABI_VERSION 1
+
+#define RG_OK 0
+#define RG_E_NODEVICE (-1)
+#define RG_E_UNSUPPORTED (-2)
+#define RG_E_ARGS (-3)
+#define RG_E_CUDA (-4)
+
+/* cell status codes: kernels.py:37-39 */
+#define RG_CELL_VIOLATED 0
+#define RG_CELL_OK 1
+#define RG_CELL_OVERFLOW 2
+
+/* which glibc expm1 build the device tanh reproduces */
+#define RG_TANH_AUTO 0    /* probe the host libm once at rg_create */
+#define RG_TANH_FMA 1     /* __expm1_fma (x86-64 hosts with FMA+AVX2) */
+#define RG_TANH_GENERIC 2 /* generic SSE2 __expm1 */
+
+/* flags */
+#define RG_DEVICE_PTRS 0x1  /* array arguments are device pointers */
+#define RG_ASYNC 0x2        /* enqueue only; no host readback, no sync */
+#define RG_ABANDON 0x4      /* grid step: stop rows already known infeasible */
+#define RG_NO_TIMING 0x8    /* skip the CUDA-event kernel timing */
+
+typedef struct rg_ctx rg_ctx;
+
+/* Plant and constraint set for every call.
+ * step_size:        SurrogateFuelCellPlant.step_size (dynamics.py:247-263)
+ * y_lower, y_upper: ConstraintSet.lower/upper on y = x1 (constraints.py:37-70)
+ * ss_v_lower/upper: the setpoints v whose steady state passes the tightened
+ *                   set, tight.contains(np.tanh(v)) (governor.py:302, 401),
+ *                   as an exact interval computed and verified on the host
+ * j_star:           prediction horizon in steps */
+typedef struct {
+    double step_size;
+    double y_lower, y_upper;
+    double ss_v_lower, ss_v_upper;
+    int32_t j_star;
+    int32_t _pad;
+} rg_problem;
+
+/* Counter-RNG scenario set (disturbance.py:179-203): scenario k of the set is
+ * k0 + k of the stream `seed`, entry (k, j, i) = lo[i] + span[i] * u. */
+typedef struct {
+    uint64_t seed;
+    int64_t k0;
+    int64_t n_sim;
+    double lo[3];
+    double span[3];
+} rg_scenarios;
+
+/* Result of rg_grid_step (robust_rg_parallel, governor.py:520-579). */
+typedef struct {
+    int32_t row;            /* 0-based best all-feasible row, -1 when none */
+    int32_t n_active;       /* rows simulated after the steady-state gate and dedup */
+    int32_t ss_pruned_rows; /* governor.py:344 */
+    int32_t dedup_rows;     /* governor.py:345 */
+    int64_t sims_run;       /* n_active * n_sim (governor.py:341) */
+    int64_t early_terms;    /* evaluated cells with steps < j_star (governor.py:342) */
+    int64_t overflows;      /* cells ending in CELL_OVERFLOW (governor.py:343) */
+    int64_t abandoned;      /* cells stopped by RG_ABANDON (0 without it) */
+    float kernel_ms;        /* CUDA-event time of the step kernel */
+    int32_t _pad;
+} rg_grid_result;
+
+/* Result of rg_bisect (robust_rg_sequential / bisection_rg). */
+typedef struct {
+    double kappa;           /* min over scenarios of the bisected kappa */
+    int32_t found;          /* AND over scenarios */
+    int32_t _pad;
+    int64_t cells;          /* sims_run (governor.py:501) */
+    int64_t early;          /* early_terms (governor.py:502) */
+    float kernel_ms;
+    int32_t _pad2;
+} rg_bisect_result;
+
+RG_API int32_t rg_abi_version(void);
+RG_API const char *rg_last_error(void);
+RG_API int32_t rg_device_count(int32_t *n);
+
+/* Create a context on CUDA device `device` (sm_100 required). */
+RG_API int32_t rg_create(int32_t device, int32_t tanh_variant, rg_ctx **out);
+RG_API int32_t rg_destroy(rg_ctx *ctx);
+RG_API int32_t rg_get_tanh_variant(rg_ctx *ctx, int32_t *variant);
+/* The cudaStream_t the context launches on, as an opaque pointer. */
+RG_API int32_t rg_get_stream(rg_ctx *ctx, void **stream);
+RG_API int32_t rg_synchronize(rg_ctx *ctx);
+
+/* y[i] = tanh(x[i]) with the device port of glibc tanh (self-test hook). */
+RG_API int32_t rg_tanh(rg_ctx *ctx, const double *x, double *y, int64_t n, int32_t flags);
+
+/* sample_scenarios / _uniform_grid (disturbance.py:85-92, 179-203):
+ * out[n_sim][horizon][width], width <= 16; scenario k is stream index k0 + k. */
+RG_API int32_t rg_sample_scenarios(rg_ctx *ctx, uint64_t seed, int64_t k0, int64_t n_sim,
+                            int64_t horizon, int32_t width, const double *lo,
+                            const double *span, double *out, int32_t flags);
+
+/* Parity fill: the kernels.run_cells seam (kernels.py:260-300) behind
+ * backend_gpu.fill (backend_gpu.py:50).  For each active row rows[a] the
+ * candidate v_rows[rows[a]] is rolled out against every scenario and
+ * S[rows[a]][k] (RG_CELL_*) and steps[rows[a]][k] are written; other rows are
+ * untouched.  Scenarios come from `dist` ([n_sim][horizon][3], horizon >=
+ * j_star + 1) or, when dist is NULL, from the counter RNG `rng`. */
+RG_API int32_t rg_fill(rg_ctx *ctx, const rg_problem *prob, const double *x0, const double *v_rows,
+                int32_t m_rows, const int32_t *rows, int32_t n_rows, const double *dist,
+                int64_t n_sim, int64_t horizon, const rg_scenarios *rng, uint8_t *S,
+                int32_t *steps, int32_t flags);
+
+/* Fused robust grid step (robust_rg_parallel): candidates kappa_i = i/(m-1),
+ * v_i = update_setpoint(v_prev, r, kappa_i), steady-state gate and dedup on
+ * the device, rollouts with fused RNG (dist NULL) or staged dist, per-row
+ * feasibility reduction and extraction of the best row (prefix_mode as in
+ * extract_kappa_opt, governor.py:351-377).  Optional outputs:
+ *   row_viol[m]       per-row violating-scenario counts (UINT32_MAX = pruned)
+ *   pbits[m][ceil(n_sim/32)]  P as a bitmask, bit k%32 of word k/32
+ * With RG_ASYNC nothing is read back; the result lands in device memory and
+ * rg_grid_fetch copies it out later. */
+RG_API int32_t rg_grid_step(rg_ctx *ctx, const rg_problem *prob, const double *x0, double v_prev,
+                     double r, int32_t m_grid, int32_t prefix_mode, const double *dist,
+                     int64_t n_sim, int64_t horizon, const rg_scenarios *rng,
+                     uint32_t *row_viol, uint32_t *pbits, rg_grid_result *out, int32_t flags);
+RG_API int32_t rg_grid_fetch(rg_ctx *ctx, uint32_t *row_viol, int32_t m_grid, rg_grid_result *out);
+
+/* Exact Alg. 2 (robust_rg_sequential, governor.py:469-517): each scenario runs
+ * _bisect_kappa (governor.py:380-430) on its own disturbance; reductions give
+ * min kappa, AND found and the summed counters.  Scenario source: dist, rng,
+ * or both NULL for the nominal (zero-disturbance) prediction of bisection_rg.
+ * Per-scenario outputs and the tested path ([n_sim][n_kappa+1], unused slots
+ * untouched) are optional. */
+RG_API int32_t rg_bisect(rg_ctx *ctx, const rg_problem *prob, const double *x0, double v_prev,
+                  double r, int32_t n_kappa, const double *dist, int64_t n_sim, int64_t horizon,
+                  const rg_scenarios *rng, double *kappa_k, int32_t *found_k, int32_t *cells_k,
+                  int32_t *early_k, double *path_kappa, uint8_t *path_ok,
+                  rg_bisect_result *out, int32_t flags);
+
+/* FP64 roofline probe: independent DFMA chains; returns achieved FLOP/s. */
+RG_API int32_t rg_fp64_peak(rg_ctx *ctx, double *flops_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* REFGOV_B200_H */

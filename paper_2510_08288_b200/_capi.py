@@ -1,0 +1,250 @@
+"""ctypes binding of the C ABI (include/refgov_b200.h).
+
+The library is built in-tree (``python -m paper_2510_08288_b200.build`` or
+``__graft_entry__.build()``) as ``_lib/librefgov_b200.so``.  There is no
+fallback: if the library or a CUDA device is missing, every device entry point
+raises BackendUnavailableError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+import numpy as np
+
+from .errors import BackendUnavailableError, ConfigError, RefgovError
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "librefgov_b200.so"
+
+RG_OK, RG_E_NODEVICE, RG_E_UNSUPPORTED, RG_E_ARGS, RG_E_CUDA = 0, -1, -2, -3, -4
+RG_TANH_AUTO, RG_TANH_FMA, RG_TANH_GENERIC = 0, 1, 2
+RG_DEVICE_PTRS, RG_ASYNC, RG_ABANDON, RG_NO_TIMING = 0x1, 0x2, 0x4, 0x8
+
+_i32, _i64, _u64, _d, _vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, \
+    ctypes.c_void_p
+
+
+class Problem(ctypes.Structure):
+    _fields_ = [("step_size", _d), ("y_lower", _d), ("y_upper", _d), ("ss_v_lower", _d),
+                ("ss_v_upper", _d), ("j_star", _i32), ("_pad", _i32)]
+
+
+class Scenarios(ctypes.Structure):
+    _fields_ = [("seed", _u64), ("k0", _i64), ("n_sim", _i64), ("lo", _d * 3), ("span", _d * 3)]
+
+
+class GridResult(ctypes.Structure):
+    _fields_ = [("row", _i32), ("n_active", _i32), ("ss_pruned_rows", _i32),
+                ("dedup_rows", _i32), ("sims_run", _i64), ("early_terms", _i64),
+                ("overflows", _i64), ("abandoned", _i64), ("kernel_ms", ctypes.c_float),
+                ("_pad", _i32)]
+
+
+class BisectResult(ctypes.Structure):
+    _fields_ = [("kappa", _d), ("found", _i32), ("_pad", _i32), ("cells", _i64),
+                ("early", _i64), ("kernel_ms", ctypes.c_float), ("_pad2", _i32)]
+
+
+def make_scenarios(seed: int, k0: int, n_sim: int, lo, span) -> "Scenarios":
+    """rg_scenarios for the counter-RNG stream ``seed`` (masked to 64 bits)."""
+    d3 = _d * 3
+    return Scenarios(int(seed) & (2**64 - 1), int(k0), int(n_sim), d3(*map(float, lo)),
+                     d3(*map(float, span)))
+
+
+# name -> (restype, argtypes); the exact export list of include/refgov_b200.h
+SIGNATURES = {
+    "rg_abi_version": (_i32, []),
+    "rg_last_error": (ctypes.c_char_p, []),
+    "rg_device_count": (_i32, [ctypes.POINTER(_i32)]),
+    "rg_create": (_i32, [_i32, _i32, ctypes.POINTER(_vp)]),
+    "rg_destroy": (_i32, [_vp]),
+    "rg_get_tanh_variant": (_i32, [_vp, ctypes.POINTER(_i32)]),
+    "rg_get_stream": (_i32, [_vp, ctypes.POINTER(_vp)]),
+    "rg_synchronize": (_i32, [_vp]),
+    "rg_tanh": (_i32, [_vp, _vp, _vp, _i64, _i32]),
+    "rg_sample_scenarios": (_i32, [_vp, _u64, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _i32]),
+    "rg_fill": (_i32, [_vp, ctypes.POINTER(Problem), _vp, _vp, _i32, _vp, _i32, _vp, _i64,
+                       _i64, ctypes.POINTER(Scenarios), _vp, _vp, _i32]),
+    "rg_grid_step": (_i32, [_vp, ctypes.POINTER(Problem), _vp, _d, _d, _i32, _i32, _vp, _i64,
+                            _i64, ctypes.POINTER(Scenarios), _vp, _vp,
+                            ctypes.POINTER(GridResult), _i32]),
+    "rg_grid_fetch": (_i32, [_vp, _vp, _i32, ctypes.POINTER(GridResult)]),
+    "rg_bisect": (_i32, [_vp, ctypes.POINTER(Problem), _vp, _d, _d, _i32, _vp, _i64, _i64,
+                         ctypes.POINTER(Scenarios), _vp, _vp, _vp, _vp, _vp, _vp,
+                         ctypes.POINTER(BisectResult), _i32]),
+    "rg_fp64_peak": (_i32, [_vp, ctypes.POINTER(_d)]),
+}
+
+_lib = None
+_lock = threading.RLock()
+_contexts: dict = {}
+
+
+def load_library():
+    """Load the in-tree CUDA library; BackendUnavailableError when it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise BackendUnavailableError(
+                f"CUDA library {LIB_PATH} is not built; run __graft_entry__.build() "
+                "(there is no CPU fallback)")
+        lib = ctypes.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.rg_abi_version() != 1:
+            raise BackendUnavailableError("CUDA library ABI version mismatch; rebuild it")
+        _lib = lib
+        return lib
+
+
+def check(code: int) -> None:
+    if code == RG_OK:
+        return
+    msg = (_lib.rg_last_error() or b"").decode(errors="replace")
+    if code in (RG_E_NODEVICE, RG_E_UNSUPPORTED):
+        raise BackendUnavailableError(msg)
+    if code == RG_E_ARGS:
+        raise ConfigError(msg)
+    raise RefgovError(f"CUDA failure: {msg}")
+
+
+def _p(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(_vp)
+
+
+def device_count() -> int:
+    lib = load_library()
+    n = _i32(0)
+    rc = lib.rg_device_count(ctypes.byref(n))
+    return int(n.value) if rc == RG_OK else 0
+
+
+class Context:
+    """One CUDA context per device: stream, scratch buffers, result staging."""
+
+    def __init__(self, device: int = 0, tanh_variant: int = RG_TANH_AUTO):
+        self.lib = load_library()
+        h = _vp()
+        check(self.lib.rg_create(int(device), int(tanh_variant), ctypes.byref(h)))
+        self.handle = h
+        self.device = int(device)
+        v = _i32()
+        check(self.lib.rg_get_tanh_variant(self.handle, ctypes.byref(v)))
+        self.tanh_variant = int(v.value)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.rg_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream_ptr(self) -> int:
+        s = _vp()
+        check(self.lib.rg_get_stream(self.handle, ctypes.byref(s)))
+        return int(s.value or 0)
+
+    def synchronize(self):
+        check(self.lib.rg_synchronize(self.handle))
+
+    # -- entry points ---------------------------------------------------
+    def tanh(self, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty_like(x)
+        check(self.lib.rg_tanh(self.handle, _p(x), _p(y), x.size, 0))
+        return y
+
+    def sample(self, seed: int, k0: int, n_sim: int, horizon: int, lo, span) -> np.ndarray:
+        lo = np.ascontiguousarray(lo, dtype=np.float64)
+        span = np.ascontiguousarray(span, dtype=np.float64)
+        out = np.empty((n_sim, horizon, lo.size), dtype=np.float64)
+        check(self.lib.rg_sample_scenarios(self.handle, seed & (2**64 - 1), k0, n_sim, horizon,
+                                           lo.size, _p(lo), _p(span), _p(out), 0))
+        return out
+
+    def fill(self, prob: Problem, x0, v_rows, rows, dist, n_sim, scen: Scenarios | None,
+             S: np.ndarray, steps: np.ndarray) -> None:
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        v_rows = np.ascontiguousarray(v_rows, dtype=np.float64)
+        rows = np.ascontiguousarray(rows, dtype=np.int32)
+        horizon = 0
+        if dist is not None:
+            dist = np.ascontiguousarray(dist, dtype=np.float64)
+            horizon = dist.shape[1]
+        check(self.lib.rg_fill(self.handle, ctypes.byref(prob), _p(x0), _p(v_rows), v_rows.size,
+                               _p(rows), rows.size, _p(dist), int(n_sim), int(horizon),
+                               ctypes.byref(scen) if scen is not None else None, _p(S),
+                               _p(steps), 0))
+
+    def grid_step(self, prob: Problem, x0, v_prev, r, m_grid, prefix_mode, dist, n_sim,
+                  scen: Scenarios | None, want_pbits: bool, abandon: bool = False):
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        horizon = 0
+        if dist is not None:
+            dist = np.ascontiguousarray(dist, dtype=np.float64)
+            horizon = dist.shape[1]
+        viol = np.zeros(m_grid, dtype=np.uint32)
+        pbits = np.zeros((m_grid, (n_sim + 31) // 32), dtype=np.uint32) if want_pbits else None
+        res = GridResult()
+        flags = RG_ABANDON if abandon else 0
+        check(self.lib.rg_grid_step(self.handle, ctypes.byref(prob), _p(x0), float(v_prev),
+                                    float(r), int(m_grid), int(bool(prefix_mode)), _p(dist),
+                                    int(n_sim), int(horizon),
+                                    ctypes.byref(scen) if scen is not None else None, _p(viol),
+                                    _p(pbits), ctypes.byref(res), flags))
+        return res, viol, pbits
+
+    def bisect(self, prob: Problem, x0, v_prev, r, n_kappa, dist, n_sim,
+               scen: Scenarios | None, per_scenario: bool = False, paths: bool = False):
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        horizon = 0
+        if dist is not None:
+            dist = np.ascontiguousarray(dist, dtype=np.float64)
+            horizon = dist.shape[1]
+        kap = fnd = cel = erl = pk = po = None
+        if per_scenario:
+            kap = np.empty(n_sim, dtype=np.float64)
+            fnd = np.empty(n_sim, dtype=np.int32)
+            cel = np.empty(n_sim, dtype=np.int32)
+            erl = np.empty(n_sim, dtype=np.int32)
+        if paths:
+            pk = np.empty((n_sim, n_kappa + 1), dtype=np.float64)
+            po = np.empty((n_sim, n_kappa + 1), dtype=np.uint8)
+        res = BisectResult()
+        check(self.lib.rg_bisect(self.handle, ctypes.byref(prob), _p(x0), float(v_prev), float(r),
+                                 int(n_kappa), _p(dist), int(n_sim), int(horizon),
+                                 ctypes.byref(scen) if scen is not None else None, _p(kap),
+                                 _p(fnd), _p(cel), _p(erl), _p(pk), _p(po), ctypes.byref(res), 0))
+        per = (kap, fnd, cel, erl) if per_scenario else None
+        return res, per, ((pk, po) if paths else None)
+
+    def fp64_peak(self) -> float:
+        f = _d()
+        check(self.lib.rg_fp64_peak(self.handle, ctypes.byref(f)))
+        return float(f.value)
+
+
+def context(device: int = 0) -> Context:
+    """The process-wide context of ``device`` (created on first use)."""
+    ctx = _contexts.get(device)
+    if ctx is None:
+        with _lock:
+            ctx = _contexts.get(device)
+            if ctx is None:
+                ctx = Context(device)
+                _contexts[device] = ctx
+    return ctx

@@ -1,0 +1,733 @@
+// rg_capi.cu -- extern "C" boundary of the library (include/refgov_b200.h).
+//
+// Owns the per-context CUDA stream, the device scratch (grown on demand and
+// reused across calls, so a steady-state governor loop allocates nothing) and
+// the pinned host staging for results.  Every entry point validates its
+// arguments the way the reference does (governor.py:81-108, 268-282) and maps
+// failures onto the RG_E_* codes.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+
+#include "../../include/refgov_b200.h"
+#include "rg_kernels.h"
+#include "rg_math.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int32_t fail(int32_t code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int32_t fail(int32_t code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define RG_CUDA(call)                                                                      \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(RG_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                               \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t n) {
+        if (n <= bytes && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&p, std::max<size_t>(n, 256));
+        if (e == cudaSuccess) bytes = std::max<size_t>(n, 256);
+        return e;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+struct HostBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t n) {
+        if (n <= bytes && p) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMallocHost(&p, std::max<size_t>(n, 256));
+        if (e == cudaSuccess) bytes = std::max<size_t>(n, 256);
+        return e;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+// Inputs where glibc's two expm1 builds give different tanh bits.
+const uint64_t kProbeBits[16] = {
+    0xbfc3bab49ff59a00ull, 0xbfbf607d2a367f40ull, 0xbff1e04607439275ull, 0xbfc87c559853f610ull,
+    0x3fc1bd2970c05a80ull, 0xbfc4df513e0c5a90ull, 0x3fc813eee33158a0ull, 0x3fc351feaea207e0ull,
+    0xbfbf0d9c6d2f7d40ull, 0xbfc324032814df90ull, 0xbffe08c8d2bc0699ull, 0x3fc00ecbb330a320ull,
+    0x3ff319e0623618f8ull, 0xbff949e37cad90c4ull, 0xbfb3d362eb61dac0ull, 0x3fc779d23c26eb20ull};
+
+bool same_bits(double a, double b) { return memcmp(&a, &b, 8) == 0; }
+
+// Which glibc expm1 build does this process's libm tanh use?  0 when neither.
+int probe_host_tanh() {
+    int fma_ok = 0, gen_ok = 0;
+    for (uint64_t b : kProbeBits) {
+        double x;
+        memcpy(&x, &b, 8);
+        const double ref = ::tanh(x);
+        fma_ok += same_bits(ref, rg::tanh_glibc<true>(x));
+        gen_ok += same_bits(ref, rg::tanh_glibc<false>(x));
+    }
+    int v = 0;
+    if (fma_ok == 16 && gen_ok < 16) v = rg::kTanhFma;
+    if (gen_ok == 16 && fma_ok < 16) v = rg::kTanhGeneric;
+    if (!v) return 0;
+    // confirm on a deterministic sweep of the branches the rollout uses
+    uint64_t s = 0x243F6A8885A308D3ull;
+    for (int i = 0; i < 8192; ++i) {
+        s = s * 6364136223846793005ull + 1442695040888963407ull;
+        const double x = ((double)(s >> 11) * 0x1p-53 - 0.5) * (i & 1 ? 8.0 : 50.0);
+        if (!same_bits(::tanh(x), rg::tanh_variant(x, v))) return 0;
+    }
+    return v;
+}
+
+}  // namespace
+
+struct rg_ctx {
+    int device = 0;
+    int variant = rg::kTanhFma;
+    int sm_count = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // grid-step accumulators and outputs
+    int grid_cap = 0;
+    DevBuf g_viol, g_early, g_ovf, g_aband, g_src, g_ticket, g_violout, g_out;
+    // bisection accumulators and outputs
+    DevBuf b_acc, b_out;
+    // scratch
+    DevBuf dist_raw, soa, S, steps, pbits, rows, vrows, tmp_a, tmp_b, kap_k, fnd_k, cel_k,
+        erl_k, path_k, path_o;
+    HostBuf h_stage;
+};
+
+namespace {
+
+int32_t enter(rg_ctx* ctx) {
+    if (!ctx) return fail(RG_E_ARGS, "null context");
+    RG_CUDA(cudaSetDevice(ctx->device));
+    return RG_OK;
+}
+
+int32_t make_problem(const rg_problem* p, rg::ProblemDev* out) {
+    if (!p) return fail(RG_E_ARGS, "null problem");
+    if (!(p->step_size > 0.0) || !isfinite(p->step_size))
+        return fail(RG_E_ARGS, "step_size must be positive, got %g", p->step_size);
+    if (p->j_star < 1) return fail(RG_E_ARGS, "j_star must be >= 1, got %d", p->j_star);
+    if (isnan(p->y_lower) || isnan(p->y_upper) || !(p->y_lower < p->y_upper))
+        return fail(RG_E_ARGS, "constraint requires lower < upper, got [%g, %g]", p->y_lower,
+                    p->y_upper);
+    out->h = p->step_size;
+    out->hh = 0.5 * p->step_size;  // kernels.py:59 evaluates 0.5 * h first
+    out->c = p->step_size / 6.0;   // kernels.py:54
+    out->ylo = p->y_lower;
+    out->yhi = p->y_upper;
+    out->vlo = p->ss_v_lower;
+    out->vhi = p->ss_v_upper;
+    out->j_star = p->j_star;
+    return RG_OK;
+}
+
+rg::ScenarioStream make_stream(const rg_scenarios* s) {
+    rg::ScenarioStream st{};
+    st.hs = rg::splitmix64(s->seed);
+    for (int i = 0; i < 3; ++i) {
+        st.lo[i] = s->lo[i];
+        st.span[i] = s->span[i];
+    }
+    return st;
+}
+
+cudaMemcpyKind kind_h2d(int32_t flags) {
+    return (flags & RG_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+}
+cudaMemcpyKind kind_d2h(int32_t flags) {
+    return (flags & RG_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+}
+
+// Stage a [n_sim][horizon][3] tensor as SoA d[(j*3+i)*ld + k] (rows j < j_star).
+int32_t stage_dist(rg_ctx* ctx, const double* dist, int64_t n_sim, int64_t horizon,
+                   int32_t j_star, int32_t flags, const double** soa, int64_t* ld) {
+    const size_t raw_bytes = (size_t)n_sim * horizon * 3 * sizeof(double);
+    const double* dsrc = dist;
+    if (!(flags & RG_DEVICE_PTRS)) {
+        RG_CUDA(ctx->dist_raw.ensure(raw_bytes));
+        RG_CUDA(cudaMemcpyAsync(ctx->dist_raw.p, dist, raw_bytes, cudaMemcpyHostToDevice,
+                                ctx->stream));
+        dsrc = ctx->dist_raw.as<double>();
+    }
+    *ld = (n_sim + 31) / 32 * 32;
+    RG_CUDA(ctx->soa.ensure((size_t)j_star * 3 * (*ld) * sizeof(double)));
+    RG_CUDA(rg::launch_to_soa(dsrc, ctx->soa.as<double>(), n_sim, horizon, j_star, *ld,
+                              ctx->stream));
+    *soa = ctx->soa.as<double>();
+    return RG_OK;
+}
+
+int32_t grow_grid(rg_ctx* ctx, int m) {
+    if (m <= ctx->grid_cap) return RG_OK;
+    const int cap = std::max(m, 64);
+    RG_CUDA(ctx->g_viol.ensure(cap * sizeof(unsigned)));
+    RG_CUDA(ctx->g_early.ensure(cap * sizeof(unsigned long long)));
+    RG_CUDA(ctx->g_ovf.ensure(cap * sizeof(unsigned long long)));
+    RG_CUDA(ctx->g_aband.ensure(cap * sizeof(unsigned long long)));
+    RG_CUDA(ctx->g_src.ensure(cap * sizeof(int)));
+    RG_CUDA(ctx->g_violout.ensure(cap * sizeof(unsigned)));
+    RG_CUDA(ctx->g_ticket.ensure(sizeof(unsigned)));
+    RG_CUDA(ctx->g_out.ensure(sizeof(rg::GridOut)));
+    RG_CUDA(cudaMemsetAsync(ctx->g_viol.p, 0, ctx->g_viol.bytes, ctx->stream));
+    RG_CUDA(cudaMemsetAsync(ctx->g_early.p, 0, ctx->g_early.bytes, ctx->stream));
+    RG_CUDA(cudaMemsetAsync(ctx->g_ovf.p, 0, ctx->g_ovf.bytes, ctx->stream));
+    RG_CUDA(cudaMemsetAsync(ctx->g_aband.p, 0, ctx->g_aband.bytes, ctx->stream));
+    RG_CUDA(cudaMemsetAsync(ctx->g_ticket.p, 0, ctx->g_ticket.bytes, ctx->stream));
+    RG_CUDA(cudaMemsetAsync(ctx->g_out.p, 0, ctx->g_out.bytes, ctx->stream));
+    ctx->grid_cap = cap;
+    return RG_OK;
+}
+
+int tpb_for(const rg_ctx* ctx, int64_t n_sim, int64_t rows) {
+    // Small problems: small blocks spread the warps over more SMs.
+    const int64_t warps = (n_sim + 31) / 32 * std::max<int64_t>(rows, 1);
+    if (warps < (int64_t)ctx->sm_count * 8) return 32;
+    if (warps < (int64_t)ctx->sm_count * 16) return 64;
+    return 128;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t rg_abi_version(void) { return RG_ABI_VERSION; }
+
+const char* rg_last_error(void) { return g_err.c_str(); }
+
+int32_t rg_device_count(int32_t* n) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        if (n) *n = 0;
+        return fail(RG_E_NODEVICE, "no CUDA device: %s", cudaGetErrorString(e));
+    }
+    if (n) *n = c;
+    return RG_OK;
+}
+
+int32_t rg_create(int32_t device, int32_t tanh_variant, rg_ctx** out) {
+    if (!out) return fail(RG_E_ARGS, "null output pointer");
+    *out = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(RG_E_NODEVICE, "no CUDA device available (%s)",
+                    e == cudaSuccess ? "count 0" : cudaGetErrorString(e));
+    }
+    if (device < 0 || device >= n) return fail(RG_E_ARGS, "device %d out of range [0, %d)", device, n);
+    cudaDeviceProp prop;
+    RG_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (!(prop.major == 10 && prop.minor == 0))
+        return fail(RG_E_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a",
+                    device, prop.major, prop.minor);
+    int variant = tanh_variant;
+    if (variant == RG_TANH_AUTO) {
+        variant = probe_host_tanh();
+        if (!variant)
+            return fail(RG_E_UNSUPPORTED,
+                        "host libm tanh matches neither glibc expm1 build; device results "
+                        "would not be bit-identical to the reference");
+    } else if (variant != RG_TANH_FMA && variant != RG_TANH_GENERIC) {
+        return fail(RG_E_ARGS, "unknown tanh variant %d", variant);
+    }
+    rg_ctx* ctx = new rg_ctx();
+    ctx->device = device;
+    ctx->variant = variant;
+    ctx->sm_count = prop.multiProcessorCount;
+    int32_t rc = enter(ctx);
+    if (rc) { delete ctx; return rc; }
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) {
+        delete ctx;
+        return fail(RG_E_CUDA, "stream/event creation failed: %s",
+                    cudaGetErrorString(cudaGetLastError()));
+    }
+    rc = grow_grid(ctx, 64);
+    if (!rc) {
+        if (ctx->b_acc.ensure(sizeof(rg::BisectAcc)) != cudaSuccess ||
+            ctx->b_out.ensure(sizeof(rg::BisectOut)) != cudaSuccess ||
+            ctx->h_stage.ensure(1 << 16) != cudaSuccess)
+            rc = fail(RG_E_CUDA, "allocation failed");
+    }
+    if (!rc) {
+        rg::BisectAcc acc{0x3ff0000000000000ull, 1, 0ull, 0ull, 0u};
+        if (cudaMemcpy(ctx->b_acc.p, &acc, sizeof acc, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemset(ctx->b_out.p, 0, sizeof(rg::BisectOut)) != cudaSuccess ||
+            cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+            rc = fail(RG_E_CUDA, "context init failed");
+    }
+    if (rc) {
+        rg_destroy(ctx);
+        return rc;
+    }
+    *out = ctx;
+    return RG_OK;
+}
+
+int32_t rg_destroy(rg_ctx* ctx) {
+    if (!ctx) return RG_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    DevBuf* bufs[] = {&ctx->g_viol, &ctx->g_early, &ctx->g_ovf, &ctx->g_aband, &ctx->g_src,
+                      &ctx->g_ticket, &ctx->g_violout, &ctx->g_out, &ctx->b_acc, &ctx->b_out,
+                      &ctx->dist_raw, &ctx->soa, &ctx->S, &ctx->steps, &ctx->pbits, &ctx->rows,
+                      &ctx->vrows, &ctx->tmp_a, &ctx->tmp_b, &ctx->kap_k, &ctx->fnd_k,
+                      &ctx->cel_k, &ctx->erl_k, &ctx->path_k, &ctx->path_o};
+    for (DevBuf* b : bufs) b->release();
+    ctx->h_stage.release();
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return RG_OK;
+}
+
+int32_t rg_get_tanh_variant(rg_ctx* ctx, int32_t* variant) {
+    if (!ctx || !variant) return fail(RG_E_ARGS, "null argument");
+    *variant = ctx->variant;
+    return RG_OK;
+}
+
+int32_t rg_get_stream(rg_ctx* ctx, void** stream) {
+    if (!ctx || !stream) return fail(RG_E_ARGS, "null argument");
+    *stream = (void*)ctx->stream;
+    return RG_OK;
+}
+
+int32_t rg_synchronize(rg_ctx* ctx) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RG_OK;
+}
+
+int32_t rg_tanh(rg_ctx* ctx, const double* x, double* y, int64_t n, int32_t flags) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    if (n < 0 || (n > 0 && (!x || !y))) return fail(RG_E_ARGS, "bad tanh arguments");
+    if (n == 0) return RG_OK;
+    const size_t bytes = (size_t)n * sizeof(double);
+    const double* dx = x;
+    double* dy = y;
+    if (!(flags & RG_DEVICE_PTRS)) {
+        RG_CUDA(ctx->tmp_a.ensure(bytes));
+        RG_CUDA(ctx->tmp_b.ensure(bytes));
+        RG_CUDA(cudaMemcpyAsync(ctx->tmp_a.p, x, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        dx = ctx->tmp_a.as<double>();
+        dy = ctx->tmp_b.as<double>();
+    }
+    RG_CUDA(rg::launch_tanh(dx, dy, n, ctx->variant == rg::kTanhFma, ctx->stream));
+    if (!(flags & RG_DEVICE_PTRS))
+        RG_CUDA(cudaMemcpyAsync(y, dy, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RG_OK;
+}
+
+int32_t rg_sample_scenarios(rg_ctx* ctx, uint64_t seed, int64_t k0, int64_t n_sim,
+                            int64_t horizon, int32_t width, const double* lo,
+                            const double* span, double* out, int32_t flags) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    if (n_sim < 1 || horizon < 1)
+        return fail(RG_E_ARGS, "n_sim and horizon must be >= 1, got %lld, %lld",
+                    (long long)n_sim, (long long)horizon);
+    if (width < 1 || width > 16) return fail(RG_E_ARGS, "width must be in [1, 16], got %d", width);
+    if (k0 < 0) return fail(RG_E_ARGS, "k0 must be >= 0");
+    if (!lo || !span || !out) return fail(RG_E_ARGS, "null buffer");
+    rg::SampleArgs a{};
+    a.hs = rg::splitmix64(seed);
+    a.k0 = k0;
+    a.n_sim = n_sim;
+    a.horizon = horizon;
+    a.width = width;
+    for (int i = 0; i < width; ++i) {
+        a.lo[i] = lo[i];
+        a.span[i] = span[i];
+    }
+    const size_t bytes = (size_t)n_sim * horizon * width * sizeof(double);
+    if (flags & RG_DEVICE_PTRS) {
+        a.out = out;
+    } else {
+        RG_CUDA(ctx->dist_raw.ensure(bytes));
+        a.out = ctx->dist_raw.as<double>();
+    }
+    RG_CUDA(rg::launch_sample(a, ctx->stream));
+    if (!(flags & RG_DEVICE_PTRS))
+        RG_CUDA(cudaMemcpyAsync(out, a.out, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    if (!(flags & RG_ASYNC)) RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RG_OK;
+}
+
+int32_t rg_fill(rg_ctx* ctx, const rg_problem* prob, const double* x0, const double* v_rows,
+                int32_t m_rows, const int32_t* rows, int32_t n_rows, const double* dist,
+                int64_t n_sim, int64_t horizon, const rg_scenarios* rng, uint8_t* S,
+                int32_t* steps, int32_t flags) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    rg::FillArgs a{};
+    if ((rc = make_problem(prob, &a.p))) return rc;
+    if (!x0 || !v_rows || (n_rows > 0 && !rows) || !S || !steps)
+        return fail(RG_E_ARGS, "null buffer");
+    if (m_rows < 1 || n_rows < 0 || n_rows > m_rows)
+        return fail(RG_E_ARGS, "bad row counts m=%d n=%d", m_rows, n_rows);
+    if (n_sim < 1) return fail(RG_E_ARGS, "n_sim must be >= 1");
+    if (!dist && !rng) return fail(RG_E_ARGS, "need a scenario tensor or an RNG stream");
+    if (dist && horizon < (int64_t)prob->j_star + 1)
+        return fail(RG_E_ARGS, "scenario horizon %lld too short: need >= j_star+1 = %d",
+                    (long long)horizon, prob->j_star + 1);
+    if (!(flags & RG_DEVICE_PTRS)) {
+        for (int32_t q = 0; q < n_rows; ++q)
+            if (rows[q] < 0 || rows[q] >= m_rows)
+                return fail(RG_E_ARGS, "row index %d out of range", rows[q]);
+        for (int i = 0; i < 3; ++i) a.x0[i] = x0[i];
+    } else {
+        RG_CUDA(cudaMemcpy(a.x0, x0, 3 * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    if (n_rows == 0) return RG_OK;
+    RG_CUDA(ctx->vrows.ensure(m_rows * sizeof(double)));
+    RG_CUDA(ctx->rows.ensure(n_rows * sizeof(int32_t)));
+    RG_CUDA(cudaMemcpyAsync(ctx->vrows.p, v_rows, m_rows * sizeof(double), kind_h2d(flags),
+                            ctx->stream));
+    RG_CUDA(cudaMemcpyAsync(ctx->rows.p, rows, n_rows * sizeof(int32_t), kind_h2d(flags),
+                            ctx->stream));
+    a.v_rows = ctx->vrows.as<double>();
+    a.rows = ctx->rows.as<int32_t>();
+    a.n_rows = n_rows;
+    a.n_sim = n_sim;
+    a.tpb = tpb_for(ctx, n_sim, n_rows);
+    const bool use_rng = dist == nullptr;
+    if (use_rng) {
+        a.stream = make_stream(rng);
+        a.k0 = rng->k0;
+    } else {
+        if ((rc = stage_dist(ctx, dist, n_sim, horizon, prob->j_star, flags, &a.soa, &a.ld)))
+            return rc;
+    }
+    const size_t cells = (size_t)m_rows * n_sim;
+    if (flags & RG_DEVICE_PTRS) {
+        a.S = S;
+        a.steps = steps;
+    } else {
+        RG_CUDA(ctx->S.ensure(cells));
+        RG_CUDA(ctx->steps.ensure(cells * sizeof(int32_t)));
+        a.S = ctx->S.as<uint8_t>();
+        a.steps = ctx->steps.as<int32_t>();
+    }
+    RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+    RG_CUDA(rg::launch_fill(a, ctx->variant == rg::kTanhFma, use_rng, ctx->stream));
+    RG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+    if (!(flags & RG_DEVICE_PTRS)) {
+        // copy back only the active rows: the caller's other rows stay untouched
+        for (int32_t q = 0; q < n_rows; ++q) {
+            const int64_t off = (int64_t)rows[q] * n_sim;
+            RG_CUDA(cudaMemcpyAsync(S + off, a.S + off, n_sim, cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+            RG_CUDA(cudaMemcpyAsync(steps + off, a.steps + off, n_sim * sizeof(int32_t),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+        }
+    }
+    if (!(flags & RG_ASYNC)) RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RG_OK;
+}
+
+static int32_t read_grid(rg_ctx* ctx, uint32_t* row_viol, int32_t m_grid, rg_grid_result* out,
+                         bool viol_is_device, bool timed) {
+    RG_CUDA(ctx->h_stage.ensure(sizeof(rg::GridOut) + (size_t)m_grid * sizeof(unsigned)));
+    rg::GridOut* ho = ctx->h_stage.as<rg::GridOut>();
+    unsigned* hv = reinterpret_cast<unsigned*>(ho + 1);
+    RG_CUDA(cudaMemcpyAsync(ho, ctx->g_out.p, sizeof(rg::GridOut), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    if (row_viol) {
+        if (viol_is_device)
+            RG_CUDA(cudaMemcpyAsync(row_viol, ctx->g_violout.p, m_grid * sizeof(unsigned),
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
+        else
+            RG_CUDA(cudaMemcpyAsync(hv, ctx->g_violout.p, m_grid * sizeof(unsigned),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (row_viol && !viol_is_device) memcpy(row_viol, hv, m_grid * sizeof(unsigned));
+    if (out) {
+        out->row = ho->row;
+        out->n_active = ho->n_active;
+        out->ss_pruned_rows = ho->ss_pruned_rows;
+        out->dedup_rows = ho->dedup_rows;
+        out->sims_run = ho->sims_run;
+        out->early_terms = ho->early_terms;
+        out->overflows = ho->overflows;
+        out->abandoned = ho->abandoned;
+        out->kernel_ms = 0.f;
+        if (timed) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) == cudaSuccess) out->kernel_ms = ms;
+            cudaGetLastError();
+        }
+    }
+    return RG_OK;
+}
+
+int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, double v_prev,
+                     double r, int32_t m_grid, int32_t prefix_mode, const double* dist,
+                     int64_t n_sim, int64_t horizon, const rg_scenarios* rng,
+                     uint32_t* row_viol, uint32_t* pbits, rg_grid_result* out, int32_t flags) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    rg::GridArgs a{};
+    if ((rc = make_problem(prob, &a.p))) return rc;
+    if (!x0) return fail(RG_E_ARGS, "null x0");
+    if (m_grid < 2) return fail(RG_E_ARGS, "m_grid must be >= 2, got %d", m_grid);
+    if (m_grid > 65535) return fail(RG_E_ARGS, "m_grid must be <= 65535, got %d", m_grid);
+    if (n_sim < 1) return fail(RG_E_ARGS, "n_sim must be >= 1");
+    if (!dist && !rng) return fail(RG_E_ARGS, "need a scenario tensor or an RNG stream");
+    if (dist && horizon < (int64_t)prob->j_star + 1)
+        return fail(RG_E_ARGS, "scenario horizon %lld too short: need >= j_star+1 = %d",
+                    (long long)horizon, prob->j_star + 1);
+    if (!isfinite(v_prev) || !isfinite(r)) return fail(RG_E_ARGS, "v_prev and r must be finite");
+    if (flags & RG_DEVICE_PTRS)
+        RG_CUDA(cudaMemcpy(a.x0, x0, 3 * sizeof(double), cudaMemcpyDeviceToHost));
+    else
+        for (int i = 0; i < 3; ++i) a.x0[i] = x0[i];
+    if (!(isfinite(a.x0[0]) && isfinite(a.x0[1]) && isfinite(a.x0[2])))
+        return fail(RG_E_ARGS, "state entries must be finite");
+    if ((rc = grow_grid(ctx, m_grid))) return rc;
+    a.v_prev = v_prev;
+    a.r = r;
+    a.m_grid = m_grid;
+    a.prefix_mode = prefix_mode ? 1 : 0;
+    a.n_sim = n_sim;
+    const bool use_rng = dist == nullptr;
+    if (use_rng) {
+        a.stream = make_stream(rng);
+        a.k0 = rng->k0;
+    } else if ((rc = stage_dist(ctx, dist, n_sim, horizon, prob->j_star, flags, &a.soa, &a.ld))) {
+        return rc;
+    }
+    a.viol = ctx->g_viol.as<unsigned>();
+    a.early = ctx->g_early.as<unsigned long long>();
+    a.ovf = ctx->g_ovf.as<unsigned long long>();
+    a.abandoned = ctx->g_aband.as<unsigned long long>();
+    a.row_src = ctx->g_src.as<int>();
+    a.ticket = ctx->g_ticket.as<unsigned>();
+    a.viol_out = ctx->g_violout.as<unsigned>();
+    a.out = ctx->g_out.as<rg::GridOut>();
+    a.pwords = (n_sim + 31) / 32;
+    const bool abandon = (flags & RG_ABANDON) && !pbits;
+    if (pbits) {
+        if (flags & RG_DEVICE_PTRS) {
+            a.pbits = pbits;
+        } else {
+            RG_CUDA(ctx->pbits.ensure((size_t)m_grid * a.pwords * sizeof(unsigned)));
+            a.pbits = ctx->pbits.as<unsigned>();
+        }
+        // rows that are pruned or duplicated are not written by the kernel
+        RG_CUDA(cudaMemsetAsync(a.pbits, 0, (size_t)m_grid * a.pwords * sizeof(unsigned),
+                                ctx->stream));
+    }
+    a.tpb = tpb_for(ctx, n_sim, m_grid);
+    const bool timed = !(flags & RG_NO_TIMING);
+    if (timed) RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+    RG_CUDA(rg::launch_grid(a, ctx->variant == rg::kTanhFma, use_rng, abandon, ctx->stream));
+    if (timed) RG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+    if (pbits && !(flags & RG_DEVICE_PTRS))
+        RG_CUDA(cudaMemcpyAsync(pbits, a.pbits, (size_t)m_grid * a.pwords * sizeof(unsigned),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+    if (flags & RG_ASYNC) {
+        if (row_viol && (flags & RG_DEVICE_PTRS))
+            RG_CUDA(cudaMemcpyAsync(row_viol, ctx->g_violout.p, m_grid * sizeof(unsigned),
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
+        return RG_OK;
+    }
+    return read_grid(ctx, row_viol, m_grid, out, (flags & RG_DEVICE_PTRS) != 0, timed);
+}
+
+int32_t rg_grid_fetch(rg_ctx* ctx, uint32_t* row_viol, int32_t m_grid, rg_grid_result* out) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    if (m_grid < 1 || m_grid > ctx->grid_cap) return fail(RG_E_ARGS, "bad m_grid %d", m_grid);
+    return read_grid(ctx, row_viol, m_grid, out, false, false);
+}
+
+int32_t rg_bisect(rg_ctx* ctx, const rg_problem* prob, const double* x0, double v_prev,
+                  double r, int32_t n_kappa, const double* dist, int64_t n_sim, int64_t horizon,
+                  const rg_scenarios* rng, double* kappa_k, int32_t* found_k, int32_t* cells_k,
+                  int32_t* early_k, double* path_kappa, uint8_t* path_ok,
+                  rg_bisect_result* out, int32_t flags) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    rg::BisectArgs a{};
+    if ((rc = make_problem(prob, &a.p))) return rc;
+    if (!x0) return fail(RG_E_ARGS, "null x0");
+    if (n_kappa < 1) return fail(RG_E_ARGS, "n_kappa must be >= 1, got %d", n_kappa);
+    if (n_sim < 1) return fail(RG_E_ARGS, "n_sim must be >= 1");
+    if (dist && horizon < (int64_t)prob->j_star + 1)
+        return fail(RG_E_ARGS, "scenario horizon %lld too short: need >= j_star+1 = %d",
+                    (long long)horizon, prob->j_star + 1);
+    if (!isfinite(v_prev) || !isfinite(r)) return fail(RG_E_ARGS, "v_prev and r must be finite");
+    if ((kappa_k || found_k || cells_k || early_k) && !(kappa_k && found_k && cells_k && early_k))
+        return fail(RG_E_ARGS, "per-scenario outputs come as a set of four");
+    if ((path_kappa != nullptr) != (path_ok != nullptr))
+        return fail(RG_E_ARGS, "path outputs come as a pair");
+    if (flags & RG_DEVICE_PTRS)
+        RG_CUDA(cudaMemcpy(a.x0, x0, 3 * sizeof(double), cudaMemcpyDeviceToHost));
+    else
+        for (int i = 0; i < 3; ++i) a.x0[i] = x0[i];
+    a.v_prev = v_prev;
+    a.r = r;
+    a.n_kappa = n_kappa;
+    a.n_sim = n_sim;
+    int src = 0;
+    if (dist) {
+        src = 2;
+        if ((rc = stage_dist(ctx, dist, n_sim, horizon, prob->j_star, flags, &a.soa, &a.ld)))
+            return rc;
+    } else if (rng) {
+        src = 1;
+        a.stream = make_stream(rng);
+        a.k0 = rng->k0;
+    }
+    const bool dev = (flags & RG_DEVICE_PTRS) != 0;
+    if (kappa_k) {
+        if (dev) {
+            a.kappa_k = kappa_k;
+            a.found_k = found_k;
+            a.cells_k = cells_k;
+            a.early_k = early_k;
+        } else {
+            RG_CUDA(ctx->kap_k.ensure(n_sim * sizeof(double)));
+            RG_CUDA(ctx->fnd_k.ensure(n_sim * sizeof(int32_t)));
+            RG_CUDA(ctx->cel_k.ensure(n_sim * sizeof(int32_t)));
+            RG_CUDA(ctx->erl_k.ensure(n_sim * sizeof(int32_t)));
+            a.kappa_k = ctx->kap_k.as<double>();
+            a.found_k = ctx->fnd_k.as<int32_t>();
+            a.cells_k = ctx->cel_k.as<int32_t>();
+            a.early_k = ctx->erl_k.as<int32_t>();
+        }
+    }
+    const size_t npath = (size_t)n_sim * (n_kappa + 1);
+    if (path_kappa) {
+        if (dev) {
+            a.path_kappa = path_kappa;
+            a.path_ok = path_ok;
+        } else {
+            RG_CUDA(ctx->path_k.ensure(npath * sizeof(double)));
+            RG_CUDA(ctx->path_o.ensure(npath));
+            a.path_kappa = ctx->path_k.as<double>();
+            a.path_ok = ctx->path_o.as<uint8_t>();
+            // unused slots read back as NaN / 255
+            RG_CUDA(cudaMemsetAsync(a.path_kappa, 0xff, npath * sizeof(double), ctx->stream));
+            RG_CUDA(cudaMemsetAsync(a.path_ok, 0xff, npath, ctx->stream));
+        }
+    }
+    a.acc = ctx->b_acc.as<rg::BisectAcc>();
+    a.out = ctx->b_out.as<rg::BisectOut>();
+    a.tpb = tpb_for(ctx, n_sim, 1);
+    const bool timed = !(flags & RG_NO_TIMING);
+    if (timed) RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+    RG_CUDA(rg::launch_bisect(a, ctx->variant == rg::kTanhFma, src, ctx->stream));
+    if (timed) RG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+    if (!dev) {
+        if (kappa_k) {
+            RG_CUDA(cudaMemcpyAsync(kappa_k, a.kappa_k, n_sim * sizeof(double),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+            RG_CUDA(cudaMemcpyAsync(found_k, a.found_k, n_sim * sizeof(int32_t),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+            RG_CUDA(cudaMemcpyAsync(cells_k, a.cells_k, n_sim * sizeof(int32_t),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+            RG_CUDA(cudaMemcpyAsync(early_k, a.early_k, n_sim * sizeof(int32_t),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        if (path_kappa) {
+            RG_CUDA(cudaMemcpyAsync(path_kappa, a.path_kappa, npath * sizeof(double),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+            RG_CUDA(cudaMemcpyAsync(path_ok, a.path_ok, npath, cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+        }
+    }
+    if (flags & RG_ASYNC) return RG_OK;
+    RG_CUDA(ctx->h_stage.ensure(sizeof(rg::BisectOut)));
+    rg::BisectOut* ho = ctx->h_stage.as<rg::BisectOut>();
+    RG_CUDA(cudaMemcpyAsync(ho, ctx->b_out.p, sizeof(rg::BisectOut), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (out) {
+        out->kappa = ho->kappa;
+        out->found = ho->found;
+        out->cells = ho->cells;
+        out->early = ho->early;
+        out->kernel_ms = 0.f;
+        if (timed) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) == cudaSuccess) out->kernel_ms = ms;
+            cudaGetLastError();
+        }
+    }
+    return RG_OK;
+}
+
+int32_t rg_fp64_peak(rg_ctx* ctx, double* flops_per_s) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    if (!flops_per_s) return fail(RG_E_ARGS, "null output");
+    RG_CUDA(ctx->tmp_a.ensure(64));
+    const int blocks = ctx->sm_count * 8, threads = 256, iters = 1 << 14;
+    // warm-up, then the best of three
+    RG_CUDA(rg::launch_dfma_peak(ctx->tmp_a.as<double>(), blocks, threads, 256, ctx->stream));
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+        RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+        RG_CUDA(rg::launch_dfma_peak(ctx->tmp_a.as<double>(), blocks, threads, iters,
+                                     ctx->stream));
+        RG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+        RG_CUDA(cudaEventSynchronize(ctx->ev1));
+        float ms = 0.f;
+        RG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        best = std::min(best, ms);
+    }
+    *flops_per_s = (double)blocks * threads * iters * 8.0 * 2.0 / (best * 1e-3);
+    return RG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,447 @@
+// rg_kernels.cu -- sm_100a kernels of the robust Reference Governor hot path.
+//
+//   k_sample      scenario tensor from the counter RNG (disturbance.py:179-203)
+//   k_to_soa      [k][j][i] host-layout tensor -> SoA d[(j*3+i)*ld + k]
+//   k_fill        parity fill: status/steps per (active row, scenario) cell
+//                 (kernels.py:121-162 / backend_gpu.fill seam)
+//   k_grid        fused robust grid step (governor.py:245-377, 520-579):
+//                 ss gate + dedup per row, rollout with fused RNG or staged
+//                 SoA, warp-ballot feasibility reduction into per-row counters,
+//                 optional P bitmask, last-block extraction of the best row
+//   k_bisect      exact Alg. 2 (governor.py:380-430, 469-517): one thread per
+//                 scenario runs its own bisection; min/AND/sum reductions
+//   k_tanh        device tanh for the bit-parity self-test
+//
+// Layout: one thread per (row, scenario) cell, scenarios on the fast axis so a
+// warp is 32 consecutive scenarios of one candidate setpoint: their
+// trajectories stay close, so the data-dependent branches of tanh/expm1 and
+// the early exits mostly agree across the warp.
+#include "rg_kernels.h"
+
+#include <cuda_runtime.h>
+
+#include "rg_cell.cuh"
+
+namespace rg {
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+// warp-aggregated add of a per-lane predicate count into a 64-bit counter
+__device__ __forceinline__ void warp_count_add(bool pred, unsigned long long* ctr) {
+    const unsigned m = __ballot_sync(0xffffffffu, pred);
+    if (lane_id() == 0 && m) atomicAdd(ctr, (unsigned long long)__popc(m));
+}
+
+__device__ __forceinline__ CellConst make_cell(const ProblemDev& p) {
+    CellConst c;
+    c.h = p.h;
+    c.hh = p.hh;
+    c.c = p.c;
+    c.ylo = p.ylo;
+    c.yhi = p.yhi;
+    c.j_star = p.j_star;
+    return c;
+}
+
+__device__ __forceinline__ bool ss_gate(double v, const ProblemDev& p) {
+    return p.vlo <= v && v <= p.vhi;  // NaN -> false, like ConstraintSet.contains
+}
+
+// ---------------------------------------------------------------------------
+// scenario generation
+// ---------------------------------------------------------------------------
+
+__global__ void k_sample(SampleArgs a) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (k, j)
+    const int64_t total = a.n_sim * a.horizon;
+    if (idx >= total) return;
+    const int64_t k = idx / a.horizon;
+    const int64_t j = idx - k * a.horizon;
+    const uint64_t K = splitmix64(a.hs ^ (uint64_t)(a.k0 + k));
+    const uint64_t J = splitmix64(K ^ (uint64_t)j);
+    double* o = a.out + idx * a.width;
+    for (int i = 0; i < a.width; ++i) {
+        const double u = unit_double(splitmix64(J ^ (uint64_t)i));
+        o[i] = add(a.lo[i], mul(a.span[i], u));
+    }
+}
+
+// tile transpose of [n_sim][horizon][3] (rows j < j_star) into d[(j*3+i)*ld + k]
+__global__ void k_to_soa(const double* __restrict__ src, double* __restrict__ dst,
+                         int64_t n_sim, int64_t horizon, int32_t j_star, int64_t ld) {
+    __shared__ double tile[32][32 * 3 + 1];
+    const int64_t k0 = (int64_t)blockIdx.x * 32;
+    const int32_t j0 = blockIdx.y * 32;
+    // load: warp w reads scenario k0+w, 32 steps x 3 comps (96 contiguous doubles)
+    for (int w = threadIdx.y; w < 32; w += blockDim.y) {
+        const int64_t k = k0 + w;
+        for (int e = threadIdx.x; e < 96; e += 32) {
+            const int32_t j = j0 + e / 3;
+            double v = 0.0;
+            if (k < n_sim && j < j_star) v = src[(k * horizon + j) * 3 + (e % 3)];
+            tile[w][e] = v;
+        }
+    }
+    __syncthreads();
+    // store: lanes run over k (coalesced), rows over (j, i)
+    for (int r = threadIdx.y; r < 96; r += blockDim.y) {
+        const int32_t j = j0 + r / 3;
+        const int i = r % 3;
+        const int64_t k = k0 + threadIdx.x;
+        if (j < j_star && k < ld) dst[((int64_t)j * 3 + i) * ld + k] = tile[threadIdx.x][r];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// parity fill: status/steps for every (active row, scenario)
+// ---------------------------------------------------------------------------
+
+template <bool FMA, bool RNG>
+__global__ void __launch_bounds__(128) k_fill(FillArgs a) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= a.n_sim) return;
+    const int32_t row = a.rows[blockIdx.y];
+    const double v = a.v_rows[row];
+    const CellConst c = make_cell(a.p);
+    int32_t steps = 0;
+    int st;
+    if (RNG) {
+        RngSource src{a.stream, scenario_key(a.stream, (uint64_t)(a.k0 + k))};
+        st = rollout<FMA, false>(c, a.x0[0], a.x0[1], a.x0[2], v, src, steps, nullptr);
+    } else {
+        SoaSource src{a.soa + k, a.ld};
+        st = rollout<FMA, false>(c, a.x0[0], a.x0[1], a.x0[2], v, src, steps, nullptr);
+    }
+    a.S[(int64_t)row * a.n_sim + k] = (uint8_t)st;
+    a.steps[(int64_t)row * a.n_sim + k] = steps;
+}
+
+// ---------------------------------------------------------------------------
+// fused robust grid step
+// ---------------------------------------------------------------------------
+
+// Row status for the grid: -2 pruned by the steady-state gate, -1 simulated,
+// >= 0 duplicate of that (earlier, simulated) row.  governor.py:302-317.
+__device__ int row_source(const GridArgs& a, int i, double* v_out) {
+    const double kap_i = dvd((double)i, (double)(a.m_grid - 1));
+    const double v = update_setpoint(a.v_prev, a.r, kap_i);
+    *v_out = v;
+    if (!ss_gate(v, a.p)) return -2;
+    for (int q = 0; q < i; ++q) {
+        const double vq = update_setpoint(a.v_prev, a.r, dvd((double)q, (double)(a.m_grid - 1)));
+        if (ss_gate(vq, a.p) && vq == v) return q;
+    }
+    return -1;
+}
+
+template <bool FMA, bool RNG, bool POLL>
+__global__ void __launch_bounds__(128) k_grid(GridArgs a) {
+    __shared__ int s_src;
+    __shared__ double s_v;
+    const int i = blockIdx.y;
+    if (threadIdx.x == 0) {
+        double v;
+        s_src = row_source(a, i, &v);
+        s_v = v;
+        if (blockIdx.x == 0) a.row_src[i] = s_src;
+    }
+    __syncthreads();
+    const int src_i = s_src;
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (src_i == -1) {
+        const bool live = k < a.n_sim;
+        int st = kOk;
+        int32_t steps = a.p.j_star;
+        if (live) {
+            const CellConst c = make_cell(a.p);
+            if (RNG) {
+                RngSource src{a.stream, scenario_key(a.stream, (uint64_t)(a.k0 + k))};
+                st = rollout<FMA, POLL>(c, a.x0[0], a.x0[1], a.x0[2], s_v, src, steps,
+                                        a.viol + i);
+            } else {
+                SoaSource src{a.soa + k, a.ld};
+                st = rollout<FMA, POLL>(c, a.x0[0], a.x0[1], a.x0[2], s_v, src, steps,
+                                        a.viol + i);
+            }
+        }
+        const bool bad = live && st != kOk && st != kAbandoned;
+        const unsigned bad_mask = __ballot_sync(0xffffffffu, bad);
+        if (lane_id() == 0 && bad_mask) atomicAdd(a.viol + i, (unsigned)__popc(bad_mask));
+        warp_count_add(live && st != kAbandoned && steps < a.p.j_star, a.early + i);
+        warp_count_add(live && st == kOverflow, a.ovf + i);
+        warp_count_add(live && st == kAbandoned, a.abandoned + i);
+        if (a.pbits) {
+            const unsigned ok_mask = __ballot_sync(0xffffffffu, live && st == kOk);
+            if (lane_id() == 0 && (k - lane_id()) < a.n_sim)
+                a.pbits[(int64_t)i * a.pwords + (k >> 5)] = ok_mask;
+        }
+    }
+    // last block out extracts the row and resets the accumulators
+    __shared__ bool s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned total = gridDim.x * gridDim.y;
+        s_last = atomicAdd(a.ticket, 1u) == total - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x == 0) {
+        int best = -1;
+        int n_active = 0, pruned = 0, dup = 0;
+        unsigned long long early = 0, ovf = 0, aband = 0;
+        for (int q = 0; q < a.m_grid; ++q) {
+            const int s = ((volatile int*)a.row_src)[q];
+            bool full;
+            if (s == -2) {
+                full = false;
+                ++pruned;
+            } else if (s == -1) {
+                ++n_active;
+                full = ((volatile unsigned*)a.viol)[q] == 0u &&
+                       ((volatile unsigned long long*)a.abandoned)[q] == 0ull;
+                early += ((volatile unsigned long long*)a.early)[q];
+                ovf += ((volatile unsigned long long*)a.ovf)[q];
+                aband += ((volatile unsigned long long*)a.abandoned)[q];
+            } else {
+                ++dup;
+                full = ((volatile unsigned*)a.viol)[s] == 0u &&
+                       ((volatile unsigned long long*)a.abandoned)[s] == 0ull;
+            }
+            a.viol_out[q] = s == -2 ? 0xffffffffu
+                                    : ((volatile unsigned*)a.viol)[s < 0 ? q : s];
+            if (a.prefix_mode) {
+                if (best == q - 1 && full) best = q;
+            } else if (full) {
+                best = q;
+            }
+        }
+        a.out->row = best;
+        a.out->n_active = n_active;
+        a.out->ss_pruned_rows = pruned;
+        a.out->dedup_rows = dup;
+        a.out->early_terms = (long long)early;
+        a.out->overflows = (long long)ovf;
+        a.out->abandoned = (long long)aband;
+        a.out->sims_run = (long long)n_active * a.n_sim;
+        a.out->seq += 1;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < a.m_grid; q += blockDim.x) {
+        a.viol[q] = 0u;
+        a.early[q] = 0ull;
+        a.ovf[q] = 0ull;
+        a.abandoned[q] = 0ull;
+    }
+    if (threadIdx.x == 0) *a.ticket = 0u;
+}
+
+// ---------------------------------------------------------------------------
+// exact Alg. 2: per-scenario bisection
+// ---------------------------------------------------------------------------
+
+template <bool FMA, int SRC>  // SRC: 0 zero (nominal), 1 rng, 2 soa
+__global__ void __launch_bounds__(128) k_bisect(BisectArgs a) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = k < a.n_sim;
+    double kopt = 1.0;
+    int found = 1, cells = 0, early = 0;
+    if (live) {
+        const CellConst c = make_cell(a.p);
+        RngSource rsrc{};
+        SoaSource ssrc{};
+        if (SRC == 1) rsrc = RngSource{a.stream, scenario_key(a.stream, (uint64_t)(a.k0 + k))};
+        if (SRC == 2) ssrc = SoaSource{a.soa + k, a.ld};
+        double klo = 0.0, khi = 1.0;
+        kopt = 0.0;
+        found = 0;
+        for (int it = -1; it < a.n_kappa; ++it) {
+            const double kappa = it < 0 ? 1.0 : mul(0.5, add(klo, khi));
+            const double v = update_setpoint(a.v_prev, a.r, kappa);
+            bool ok = false;
+            int32_t sr = 0;
+            if (ss_gate(v, a.p)) {
+                int st;
+                if (SRC == 1)
+                    st = rollout<FMA, false>(c, a.x0[0], a.x0[1], a.x0[2], v, rsrc, sr, nullptr);
+                else if (SRC == 2)
+                    st = rollout<FMA, false>(c, a.x0[0], a.x0[1], a.x0[2], v, ssrc, sr, nullptr);
+                else
+                    st = rollout<FMA, false>(c, a.x0[0], a.x0[1], a.x0[2], v, ZeroSource{}, sr,
+                                             nullptr);
+                ok = st == kOk;
+            }
+            if (a.path_kappa) {
+                a.path_kappa[k * (a.n_kappa + 1) + cells] = kappa;
+                a.path_ok[k * (a.n_kappa + 1) + cells] = ok ? 1 : 0;
+            }
+            cells += 1;
+            if (sr < a.p.j_star && !ok) early += 1;
+            if (it < 0) {
+                if (ok) {
+                    kopt = 1.0;
+                    found = 1;
+                    break;
+                }
+                continue;
+            }
+            if (ok) {
+                kopt = kappa;
+                found = 1;
+                klo = kappa;
+            } else {
+                khi = kappa;
+            }
+        }
+        if (a.kappa_k) {
+            a.kappa_k[k] = kopt;
+            a.found_k[k] = found;
+            a.cells_k[k] = cells;
+            a.early_k[k] = early;
+        }
+    }
+    // reductions: min kappa (non-negative doubles order like their bits), AND found,
+    // sums of cells and early terminations
+    unsigned long long kb = (unsigned long long)__double_as_longlong(kopt);
+    int all_found = found;
+    long long sc = cells, se = early;
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long ob = __shfl_down_sync(0xffffffffu, kb, off);
+        kb = ob < kb ? ob : kb;
+        all_found &= __shfl_down_sync(0xffffffffu, all_found, off);
+        sc += __shfl_down_sync(0xffffffffu, sc, off);
+        se += __shfl_down_sync(0xffffffffu, se, off);
+    }
+    if (lane_id() == 0) {
+        atomicMin(&a.acc->kappa_bits, kb);
+        if (!all_found) atomicAnd(&a.acc->found, 0);
+        atomicAdd(&a.acc->cells, (unsigned long long)sc);
+        atomicAdd(&a.acc->early, (unsigned long long)se);
+    }
+    __shared__ bool s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&a.acc->ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    __threadfence();
+    volatile BisectAcc* acc = a.acc;
+    a.out->kappa = __longlong_as_double((long long)acc->kappa_bits);
+    a.out->found = acc->found;
+    a.out->cells = (long long)acc->cells;
+    a.out->early = (long long)acc->early;
+    a.out->seq += 1;
+    acc->kappa_bits = 0x3ff0000000000000ull;  // 1.0
+    acc->found = 1;
+    acc->cells = 0ull;
+    acc->early = 0ull;
+    acc->ticket = 0u;
+}
+
+// ---------------------------------------------------------------------------
+// tanh self-test
+// ---------------------------------------------------------------------------
+
+template <bool FMA>
+__global__ void k_tanh(const double* __restrict__ x, double* __restrict__ y, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) y[i] = tanh_glibc<FMA>(x[i]);
+}
+
+// FP64 issue-rate probe: independent DFMA chains (the roofline denominator)
+__global__ void k_dfma_peak(double* out, int iters, double a, double b) {
+    double x0 = threadIdx.x * 1e-9, x1 = x0 + 1.0, x2 = x0 + 2.0, x3 = x0 + 3.0;
+    double x4 = x0 + 4.0, x5 = x0 + 5.0, x6 = x0 + 6.0, x7 = x0 + 7.0;
+    for (int i = 0; i < iters; ++i) {
+        x0 = __fma_rn(x0, a, b);
+        x1 = __fma_rn(x1, a, b);
+        x2 = __fma_rn(x2, a, b);
+        x3 = __fma_rn(x3, a, b);
+        x4 = __fma_rn(x4, a, b);
+        x5 = __fma_rn(x5, a, b);
+        x6 = __fma_rn(x6, a, b);
+        x7 = __fma_rn(x7, a, b);
+    }
+    const double s = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
+    if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+
+static inline unsigned blocks_for(int64_t n, int tpb) { return (unsigned)((n + tpb - 1) / tpb); }
+
+cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s) {
+    const int64_t total = a.n_sim * a.horizon;
+    if (total == 0) return cudaSuccess;
+    k_sample<<<blocks_for(total, 256), 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_to_soa(const double* src, double* dst, int64_t n_sim, int64_t horizon,
+                          int32_t j_star, int64_t ld, cudaStream_t s) {
+    dim3 grid((unsigned)((ld + 31) / 32), (unsigned)((j_star + 31) / 32));
+    k_to_soa<<<grid, dim3(32, 8), 0, s>>>(src, dst, n_sim, horizon, j_star, ld);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill(const FillArgs& a, bool fma, bool rng, cudaStream_t s) {
+    if (a.n_rows == 0 || a.n_sim == 0) return cudaSuccess;
+    dim3 grid(blocks_for(a.n_sim, a.tpb), (unsigned)a.n_rows);
+    if (fma) {
+        if (rng) k_fill<true, true><<<grid, a.tpb, 0, s>>>(a);
+        else     k_fill<true, false><<<grid, a.tpb, 0, s>>>(a);
+    } else {
+        if (rng) k_fill<false, true><<<grid, a.tpb, 0, s>>>(a);
+        else     k_fill<false, false><<<grid, a.tpb, 0, s>>>(a);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, cudaStream_t s) {
+    dim3 grid(blocks_for(a.n_sim, a.tpb), (unsigned)a.m_grid);
+#define RG_GRID(F, R, P) k_grid<F, R, P><<<grid, a.tpb, 0, s>>>(a)
+    if (fma) {
+        if (rng) { if (poll) RG_GRID(true, true, true); else RG_GRID(true, true, false); }
+        else     { if (poll) RG_GRID(true, false, true); else RG_GRID(true, false, false); }
+    } else {
+        if (rng) { if (poll) RG_GRID(false, true, true); else RG_GRID(false, true, false); }
+        else     { if (poll) RG_GRID(false, false, true); else RG_GRID(false, false, false); }
+    }
+#undef RG_GRID
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bisect(const BisectArgs& a, bool fma, int src, cudaStream_t s) {
+    const unsigned g = blocks_for(a.n_sim, a.tpb);
+#define RG_BIS(F, S) k_bisect<F, S><<<g, a.tpb, 0, s>>>(a)
+    if (fma) {
+        if (src == 0) RG_BIS(true, 0); else if (src == 1) RG_BIS(true, 1); else RG_BIS(true, 2);
+    } else {
+        if (src == 0) RG_BIS(false, 0); else if (src == 1) RG_BIS(false, 1); else RG_BIS(false, 2);
+    }
+#undef RG_BIS
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tanh(const double* x, double* y, int64_t n, bool fma, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    if (fma) k_tanh<true><<<blocks_for(n, 256), 256, 0, s>>>(x, y, n);
+    else     k_tanh<false><<<blocks_for(n, 256), 256, 0, s>>>(x, y, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dfma_peak(double* out, int blocks, int threads, int iters, cudaStream_t s) {
+    k_dfma_peak<<<blocks, threads, 0, s>>>(out, iters, 0.999999, 1e-7);
+    return cudaGetLastError();
+}
+
+}  // namespace rg

@@ -1,0 +1,116 @@
+// rg_kernels.h -- argument blocks and launchers shared by rg_kernels.cu and
+// the C-ABI layer (rg_capi.cu).  Internal to the library.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rg_rng.cuh"
+
+namespace rg {
+
+// Plant + constraints, pre-digested for the device.
+struct ProblemDev {
+    double h, hh, c;   // step size, 0.5*h, h/6
+    double ylo, yhi;   // output bounds (cset.lower/upper)
+    double vlo, vhi;   // admissible setpoints of the steady-state gate
+    int32_t j_star;
+};
+
+struct SampleArgs {
+    uint64_t hs;       // splitmix64(seed)
+    int64_t k0, n_sim, horizon;
+    int32_t width;
+    double lo[16], span[16];
+    double* out;       // [n_sim][horizon][width]
+};
+
+struct FillArgs {
+    ProblemDev p;
+    double x0[3];
+    const double* v_rows;  // device [m_rows]
+    const int32_t* rows;   // device [n_rows]
+    int32_t n_rows;
+    int64_t n_sim, k0;
+    ScenarioStream stream;  // RNG source
+    const double* soa;      // staged source, d[(j*3+i)*ld + k]
+    int64_t ld;
+    uint8_t* S;             // device [m_rows][n_sim]
+    int32_t* steps;         // device [m_rows][n_sim]
+    int tpb;
+};
+
+struct GridOut {
+    int32_t row;            // best all-feasible row (0-based), -1 none
+    int32_t n_active, ss_pruned_rows, dedup_rows;
+    long long sims_run, early_terms, overflows, abandoned;
+    unsigned long long seq;
+};
+
+struct GridArgs {
+    ProblemDev p;
+    double x0[3];
+    double v_prev, r;
+    int32_t m_grid, prefix_mode;
+    int64_t n_sim, k0;
+    ScenarioStream stream;
+    const double* soa;
+    int64_t ld;
+    // accumulators (zero between launches; the last block resets them)
+    unsigned* viol;                 // [m]
+    unsigned long long* early;      // [m]
+    unsigned long long* ovf;        // [m]
+    unsigned long long* abandoned;  // [m]
+    int* row_src;                   // [m]
+    unsigned* ticket;
+    unsigned* viol_out;             // [m] per-row violation count (0xffffffff = pruned)
+    GridOut* out;
+    unsigned* pbits;                // optional [m][pwords] feasibility bitmask
+    int64_t pwords;
+    int tpb;
+};
+
+struct BisectAcc {
+    unsigned long long kappa_bits;  // min over scenarios (as bits; kappa >= 0)
+    int found;                      // AND
+    unsigned long long cells, early;
+    unsigned ticket;
+};
+
+struct BisectOut {
+    double kappa;
+    int found;
+    long long cells, early;
+    unsigned long long seq;
+};
+
+struct BisectArgs {
+    ProblemDev p;
+    double x0[3];
+    double v_prev, r;
+    int32_t n_kappa;
+    int64_t n_sim, k0;
+    ScenarioStream stream;
+    const double* soa;
+    int64_t ld;
+    double* kappa_k;   // optional per-scenario results
+    int32_t* found_k;
+    int32_t* cells_k;
+    int32_t* early_k;
+    double* path_kappa;  // optional [n_sim][n_kappa+1]
+    uint8_t* path_ok;
+    BisectAcc* acc;
+    BisectOut* out;
+    int tpb;
+};
+
+cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s);
+cudaError_t launch_to_soa(const double* src, double* dst, int64_t n_sim, int64_t horizon,
+                          int32_t j_star, int64_t ld, cudaStream_t s);
+cudaError_t launch_fill(const FillArgs& a, bool fma, bool rng, cudaStream_t s);
+cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, cudaStream_t s);
+cudaError_t launch_bisect(const BisectArgs& a, bool fma, int src, cudaStream_t s);
+cudaError_t launch_tanh(const double* x, double* y, int64_t n, bool fma, cudaStream_t s);
+cudaError_t launch_dfma_peak(double* out, int blocks, int threads, int iters, cudaStream_t s);
+
+}  // namespace rg

@@ -1,0 +1,458 @@
+"""Setpoint governors on the B200 (reference governor.py:1-579, drop-in names).
+
+Same entry points, arguments, results and errors as the reference:
+
+* ``robust_rg_parallel``   Alg. 3 grid search -> one fused kernel
+  (csrc/rg_kernels.cu:k_grid): per-row steady-state gate and dedup, rollouts
+  with the counter RNG fused in (or a staged tensor), warp-ballot feasibility
+  reduction, extraction of the best row on the device.
+* ``robust_rg_sequential`` Alg. 2 -> one kernel (k_bisect): every scenario runs
+  its own bisection, then min / AND / sum reductions on the device.
+* ``bisection_rg``         Alg. 1 -> the same kernel on the nominal prediction.
+* ``fill_feasibility``     the full (candidate, scenario) matrix via the parity
+  fill kernel (k_fill), with the reference's host-side gate, dedup and stats.
+
+The numpy-tanh steady-state gate stays exactly the reference's: on the host
+where the reference evaluates it per row (fill_feasibility), and on the device
+as the verified setpoint interval of ssgate.py where the decision is made on
+the device.  There is no CPU fallback: without the CUDA library or a device
+every call raises BackendUnavailableError.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from .constraints import ConstraintSet, tighten, tighten_margin, validate_epsilon
+from .disturbance import ScenarioSet
+from .errors import BackendUnavailableError, ConfigError, DomainError, InfeasibleError, \
+    RefgovError
+from .ssgate import admissible_setpoints
+
+__all__ = ["BACKENDS", "GovernorConfig", "GovernorState", "KappaResult", "CellProbe",
+           "update_setpoint", "grid_kappas", "fill_feasibility", "extract_kappa_opt",
+           "bisection_rg", "robust_rg_sequential", "robust_rg_parallel", "probe_candidate",
+           "check_candidate", "DIAG_CSV_HEADER", "CELL_OK", "CELL_VIOLATED", "CELL_OVERFLOW"]
+
+# "gpu" is the reference's name for its device backend (governor.py:53); both
+# names select the CUDA device here.  CPU backends do not exist in this build.
+BACKENDS = ("cuda", "gpu")
+_POLICIES = ("hold", "error")
+CELL_OK, CELL_VIOLATED, CELL_OVERFLOW = 1, 0, 2  # kernels.py:37-39
+
+DIAG_CSV_HEADER = "t,kappa_opt,v,feasible,sims_run,early_terms,wall_us"
+
+
+@dataclass
+class GovernorConfig:
+    """Governor knobs (governor.py:57-108) plus the device ones.
+
+    device: CUDA ordinal.  keep_matrix: return the feasibility matrix P from
+    robust_rg_parallel (the reference always does); False returns only the
+    decision and lets rows already known infeasible stop early.
+    ``workers`` is accepted for signature compatibility and ignored.
+    """
+
+    j_star: int = 256
+    epsilon: float = 0.05
+    n_kappa: int = 8
+    m_grid: int = 32
+    n_sim: int = 64
+    backend: str = "cuda"
+    infeasible_policy: str = "hold"
+    prefix_mode: bool = False
+    workers: int | None = None
+    tighten_mode: str = "scale"
+    device: int = 0
+    keep_matrix: bool = True
+
+    def __post_init__(self):
+        if self.j_star < 1:
+            raise ConfigError(f"j_star must be >= 1, got {self.j_star}")
+        if self.tighten_mode == "scale":
+            validate_epsilon(self.epsilon)
+        elif self.tighten_mode == "margin":
+            if not (np.isfinite(self.epsilon) and self.epsilon > 0):
+                raise ConfigError(f"margin tightening needs epsilon > 0, got {self.epsilon}")
+        else:
+            raise ConfigError(f"tighten_mode must be scale or margin, got {self.tighten_mode!r}")
+        if self.n_kappa < 1:
+            raise ConfigError(f"n_kappa must be >= 1, got {self.n_kappa}")
+        if self.m_grid < 2:
+            raise ConfigError(f"m_grid must be >= 2, got {self.m_grid}")
+        if self.n_sim < 1:
+            raise ConfigError(f"n_sim must be >= 1, got {self.n_sim}")
+        if self.backend not in BACKENDS:
+            raise ConfigError(f"backend must be one of {BACKENDS}, got {self.backend!r}")
+        if self.infeasible_policy not in _POLICIES:
+            raise ConfigError(f"infeasible_policy must be one of {_POLICIES}, "
+                              f"got {self.infeasible_policy!r}")
+        if self.workers is not None and self.workers < 1:
+            raise ConfigError(f"workers must be >= 1 or None, got {self.workers}")
+
+
+@dataclass
+class GovernorState:
+    """The last applied setpoint, carried between timesteps."""
+
+    v_prev: float = 0.0
+
+    def __post_init__(self):
+        if not np.isfinite(self.v_prev):
+            raise ConfigError(f"v_prev must be finite, got {self.v_prev}")
+
+
+@dataclass
+class KappaResult:
+    """Outcome of one governor call (governor.py:122-137)."""
+
+    kappa_opt: float
+    v_applied: float
+    feasible: bool
+    diagnostics: dict = field(default_factory=dict)
+    matrix: np.ndarray | None = None
+
+    def diagnostics_csv_row(self, t: int) -> str:
+        d = self.diagnostics
+        return (f"{t},{self.kappa_opt!r},{self.v_applied!r},{int(self.feasible)},"
+                f"{d.get('sims_run', 0)},{d.get('early_terms', 0)},{d.get('wall_us', 0)}")
+
+
+@dataclass(frozen=True)
+class CellProbe:
+    ok: bool
+    steady_state_ok: bool
+    status: int
+    steps_run: int
+    violation_step: int | None
+
+
+def update_setpoint(v_prev: float, r: float, kappa: float) -> float:
+    """v_prev + kappa (r - v_prev), exact at kappa = 0 and 1 (governor.py:151-159)."""
+    if not 0.0 <= kappa <= 1.0:
+        raise DomainError(f"kappa must lie in [0, 1], got {kappa}")
+    if kappa == 0.0:
+        return float(v_prev)
+    if kappa == 1.0:
+        return float(r)
+    return float(v_prev + kappa * (r - v_prev))
+
+
+def grid_kappas(m_grid: int) -> np.ndarray:
+    """{i/(M-1)} ascending, endpoints exact (governor.py:162-166)."""
+    if m_grid < 2:
+        raise ConfigError(f"m_grid must be >= 2, got {m_grid}")
+    return np.arange(m_grid, dtype=np.float64) / (m_grid - 1)
+
+
+def extract_kappa_opt(P, prefix_mode: bool = False):
+    """Best all-feasible row (1-based) and its kappa (governor.py:351-377)."""
+    P = np.asarray(P)
+    if P.ndim != 2 or P.size == 0:
+        raise ConfigError(f"P must be a nonempty 2-D matrix, got shape {P.shape}")
+    m = P.shape[0]
+    full = P.all(axis=1)
+    if prefix_mode:
+        bad = np.flatnonzero(~full)
+        idx = (int(bad[0]) if bad.size else m) - 1
+    else:
+        ok = np.flatnonzero(full)
+        idx = int(ok[-1]) if ok.size else -1
+    if idx < 0:
+        return None, None
+    if m == 1:
+        return 1, 1.0
+    return idx + 1, idx / (m - 1)
+
+
+# ---------------------------------------------------------------------------
+# host-side preparation shared by the entry points
+# ---------------------------------------------------------------------------
+
+def _tightened(cset, eps: float, mode: str) -> ConstraintSet:
+    if mode == "scale":
+        return tighten(cset, eps)
+    if mode == "margin":
+        return tighten_margin(cset, eps)
+    raise ConfigError(f"tighten_mode must be scale or margin, got {mode!r}")
+
+
+def _require_device_plant(plant) -> None:
+    if getattr(plant, "kernel_kind", None) != "surrogate-fc":
+        raise BackendUnavailableError(
+            "the device kernels are specialised to the surrogate fuel-cell plant; "
+            f"got plant kernel kind {getattr(plant, 'kernel_kind', None)!r}")
+
+
+def _validate_state(plant, x) -> np.ndarray:
+    if hasattr(plant, "validate_state"):
+        return plant.validate_state(x)
+    x = np.asarray(x, dtype=np.float64)
+    if x.shape != (3,) or not np.all(np.isfinite(x)):
+        raise ConfigError("state must be a finite vector of shape (3,)")
+    return x
+
+
+def _problem(plant, cset, tight, j_star: int) -> _capi.Problem:
+    v_lo, v_hi = admissible_setpoints(float(tight.lower), float(tight.upper))
+    return _capi.Problem(float(plant.step_size), float(cset.lower), float(cset.upper), v_lo,
+                         v_hi, int(j_star), 0)
+
+
+def _source(scenarios, j_star: int):
+    """(dense tensor | None, n_sim, RNG stream | None) for the kernels.
+
+    Mirrors _scenario_tensor (governor.py:169-179) for the shape checks.
+    """
+    if isinstance(scenarios, ScenarioSet) and scenarios.is_generated:
+        if scenarios.state_dim != 3:
+            raise ConfigError(f"scenarios must be (n_sim, horizon, 3), got state dim "
+                              f"{scenarios.state_dim}")
+        if scenarios.horizon < j_star + 1:
+            raise ConfigError(f"scenario horizon {scenarios.horizon} too short: need >= "
+                              f"j_star+1 = {j_star + 1}")
+        return None, scenarios.n_sim, _capi.make_scenarios(
+            scenarios.seed, scenarios.k0, scenarios.n_sim, scenarios.model.lo,
+            scenarios.model.span)
+    data = scenarios.data if hasattr(scenarios, "data") else np.asarray(scenarios)
+    data = np.asarray(data)
+    if data.ndim != 3 or data.shape[2] != 3:
+        raise ConfigError(f"scenarios must be (n_sim, horizon, 3), got {data.shape}")
+    if data.shape[1] < j_star + 1:
+        raise ConfigError(f"scenario horizon {data.shape[1]} too short: need >= "
+                          f"j_star+1 = {j_star + 1}")
+    if data.shape[0] < 1:
+        raise ConfigError("need at least one scenario")
+    return np.ascontiguousarray(data, dtype=np.float64), data.shape[0], None
+
+
+def _host_rows(v_prev: float, r: float, grid: np.ndarray, plant, tight):
+    """v per row, the numpy-tanh gate and the dedup map (governor.py:286, 302-317)."""
+    v_rows = np.array([update_setpoint(v_prev, r, float(k)) for k in grid])
+    ss_ok = np.array([tight.contains(plant.steady_state_output(v)) for v in v_rows], dtype=bool)
+    first: dict = {}
+    reps = []
+    dup_src = np.full(grid.size, -1, dtype=np.int64)
+    for i in range(grid.size):
+        if not ss_ok[i]:
+            continue
+        v = float(v_rows[i])
+        if v in first:
+            dup_src[i] = first[v]
+        else:
+            first[v] = i
+            reps.append(i)
+    return v_rows, ss_ok, dup_src, np.array(reps, dtype=np.int32)
+
+
+def _backend_check(backend: str) -> None:
+    if backend not in BACKENDS:
+        raise ConfigError(f"backend must be one of {BACKENDS}, got {backend!r}")
+
+
+# ---------------------------------------------------------------------------
+# fill_feasibility: the parity matrix
+# ---------------------------------------------------------------------------
+
+def fill_feasibility(backend, plant, x0, v_prev, r_t, grid, scenarios, cset, eps, j_star,
+                     workers=None, stats=None, tighten_mode="scale", device: int = 0):
+    """The (len(grid), n_sim) feasibility matrix P (governor.py:245-348).
+
+    Every active (candidate, scenario) cell is one device thread; the
+    steady-state gate, dedup and P assembly follow the reference line for line.
+    """
+    _backend_check(backend)
+    grid = np.asarray(grid, dtype=np.float64)
+    if grid.ndim != 1 or grid.size < 1:
+        raise ConfigError(f"grid must be a nonempty 1-D array, got shape {grid.shape}")
+    if np.any(np.diff(grid) < 0):
+        raise ConfigError("grid must be sorted ascending")
+    if np.any((grid < 0.0) | (grid > 1.0)) or not np.all(np.isfinite(grid)):
+        raise ConfigError("grid entries must lie in [0, 1]")
+    x0 = _validate_state(plant, x0)
+    if tighten_mode == "scale":
+        validate_epsilon(eps)
+    if j_star < 1:
+        raise ConfigError(f"j_star must be >= 1, got {j_star}")
+    _require_device_plant(plant)
+    dist, n_sim, stream = _source(scenarios, j_star)
+    tight = _tightened(cset, eps, tighten_mode)
+
+    t0 = time.perf_counter()
+    v_rows, ss_ok, dup_src, rows = _host_rows(v_prev, r_t, grid, plant, tight)
+    m = grid.size
+    S = np.zeros((m, n_sim), dtype=np.uint8)
+    steps = np.zeros((m, n_sim), dtype=np.int32)
+    ctx = _capi.context(device)
+    prob = _problem(plant, cset, tight, j_star)
+    ctx.fill(prob, x0, v_rows, rows, dist, n_sim, stream, S, steps)
+    for i in np.flatnonzero(dup_src >= 0):
+        S[i] = S[dup_src[i]]
+        steps[i] = steps[dup_src[i]]
+    P = (S == CELL_OK) & ss_ok[:, None]
+    if stats is not None:
+        ev = steps[rows] if rows.size else steps[:0]
+        stats.update(
+            backend="cuda", workers=1, device=ctx.device,
+            sims_run=int(rows.size * n_sim),
+            early_terms=int(np.count_nonzero(ev < j_star)),
+            overflows=int(np.count_nonzero(S[rows] == CELL_OVERFLOW)) if rows.size else 0,
+            ss_pruned_rows=int(np.count_nonzero(~ss_ok)),
+            dedup_rows=int(np.count_nonzero(dup_src >= 0)),
+            wall_us=int((time.perf_counter() - t0) * 1e6),
+        )
+    return P
+
+
+# ---------------------------------------------------------------------------
+# Alg. 3: robust grid step
+# ---------------------------------------------------------------------------
+
+def robust_rg_parallel(plant, x_t, state, r_t, cset, scenarios, config, backend=None):
+    """Scenario-robust governor step by grid search (governor.py:520-579)."""
+    x_t = _validate_state(plant, x_t)
+    backend = backend or config.backend
+    _backend_check(backend)
+    _require_device_plant(plant)
+    grid = grid_kappas(config.m_grid)
+    if config.tighten_mode == "scale":
+        validate_epsilon(config.epsilon)
+    tight = _tightened(cset, config.epsilon, config.tighten_mode)
+    dist, n_sim, stream = _source(scenarios, config.j_star)
+    device = getattr(config, "device", 0)
+    keep = getattr(config, "keep_matrix", True)
+
+    t0 = time.perf_counter()
+    v_rows, ss_ok, dup_src, rows = _host_rows(state.v_prev, r_t, grid, plant, tight)
+    ctx = _capi.context(device)
+    prob = _problem(plant, cset, tight, config.j_star)
+    res, viol, pbits = ctx.grid_step(prob, x_t, state.v_prev, r_t, config.m_grid,
+                                     config.prefix_mode, dist, n_sim, stream, want_pbits=keep,
+                                     abandon=not keep)
+    # the device gate (verified interval) and dedup must agree with numpy's
+    if res.ss_pruned_rows != int(np.count_nonzero(~ss_ok)) or \
+            res.dedup_rows != int(np.count_nonzero(dup_src >= 0)):
+        raise RefgovError("device steady-state gate disagrees with numpy tanh")
+    P = None
+    if keep:
+        bits = np.unpackbits(pbits.view(np.uint8), axis=1, bitorder="little")[:, :n_sim]
+        P = bits.astype(bool)
+        P[~ss_ok] = False
+        for i in np.flatnonzero(dup_src >= 0):
+            P[i] = P[dup_src[i]]
+    row = None if res.row < 0 else res.row + 1
+    stats = dict(
+        backend="cuda", workers=1, device=ctx.device, sims_run=int(res.sims_run),
+        early_terms=int(res.early_terms), overflows=int(res.overflows),
+        ss_pruned_rows=int(res.ss_pruned_rows), dedup_rows=int(res.dedup_rows),
+        abandoned=int(res.abandoned), kernel_us=int(res.kernel_ms * 1e3),
+        wall_us=int((time.perf_counter() - t0) * 1e6), method="parallel-grid",
+    )
+    if row is None:
+        if config.infeasible_policy == "error":
+            raise InfeasibleError("no candidate feasible, including kappa=0 (hold current "
+                                  "setpoint)")
+        return KappaResult(kappa_opt=0.0, v_applied=state.v_prev, feasible=False,
+                           diagnostics=stats, matrix=P)
+    kappa = float(grid[row - 1])
+    v = update_setpoint(state.v_prev, r_t, kappa)
+    state.v_prev = v
+    return KappaResult(kappa_opt=kappa, v_applied=v, feasible=True, diagnostics=stats, matrix=P)
+
+
+# ---------------------------------------------------------------------------
+# Alg. 1 / Alg. 2: bisection
+# ---------------------------------------------------------------------------
+
+def _bisect_call(plant, x_t, state, r_t, cset, config, dist, n_sim, stream):
+    tight = _tightened(cset, config.epsilon, config.tighten_mode)
+    ctx = _capi.context(getattr(config, "device", 0))
+    prob = _problem(plant, cset, tight, config.j_star)
+    res, _, _ = ctx.bisect(prob, x_t, state.v_prev, r_t, config.n_kappa, dist, n_sim, stream)
+    return res
+
+
+def bisection_rg(plant, x_t, state, r_t, cset, config):
+    """Disturbance-free governor step by bisection (governor.py:433-466)."""
+    x_t = _validate_state(plant, x_t)
+    _require_device_plant(plant)
+    t0 = time.perf_counter()
+    res = _bisect_call(plant, x_t, state, r_t, cset, config, None, 1, None)
+    kappa = float(res.kappa)
+    v = update_setpoint(state.v_prev, r_t, kappa)
+    state.v_prev = v
+    return KappaResult(kappa_opt=kappa, v_applied=v, feasible=bool(res.found), diagnostics={
+        "method": "bisection", "sims_run": int(res.cells), "early_terms": int(res.early),
+        "kernel_us": int(res.kernel_ms * 1e3),
+        "wall_us": int((time.perf_counter() - t0) * 1e6)})
+
+
+def robust_rg_sequential(plant, x_t, state, r_t, cset, scenarios, config):
+    """Worst case over per-scenario bisections (governor.py:469-517)."""
+    x_t = _validate_state(plant, x_t)
+    if scenarios.n_sim != config.n_sim:
+        raise ConfigError(f"scenario count {scenarios.n_sim} does not match config.n_sim "
+                          f"{config.n_sim}")
+    _require_device_plant(plant)
+    dist, n_sim, stream = _source(scenarios, config.j_star)
+    t0 = time.perf_counter()
+    res = _bisect_call(plant, x_t, state, r_t, cset, config, dist, n_sim, stream)
+    kappa = float(res.kappa)
+    v = update_setpoint(state.v_prev, r_t, kappa)
+    state.v_prev = v
+    return KappaResult(kappa_opt=kappa, v_applied=v, feasible=bool(res.found), diagnostics={
+        "method": "sequential", "sims_run": int(res.cells), "early_terms": int(res.early),
+        "kernel_us": int(res.kernel_ms * 1e3),
+        "wall_us": int((time.perf_counter() - t0) * 1e6)})
+
+
+def bisect_paths(plant, x_t, v_prev, r_t, cset, scenarios, config):
+    """Per-scenario bisection results and tested paths (parity diagnostics).
+
+    Returns (kappa_k, found_k, cells_k, early_k, path_kappa, path_ok); unused
+    path slots are NaN / 255.
+    """
+    x_t = _validate_state(plant, x_t)
+    _require_device_plant(plant)
+    dist, n_sim, stream = _source(scenarios, config.j_star)
+    tight = _tightened(cset, config.epsilon, config.tighten_mode)
+    ctx = _capi.context(getattr(config, "device", 0))
+    prob = _problem(plant, cset, tight, config.j_star)
+    _, per, paths = ctx.bisect(prob, x_t, v_prev, r_t, config.n_kappa, dist, n_sim, stream,
+                               per_scenario=True, paths=True)
+    return (*per, *paths)
+
+
+# ---------------------------------------------------------------------------
+# single-candidate diagnostics (governor.py:193-238)
+# ---------------------------------------------------------------------------
+
+def probe_candidate(plant, x0, v, scenario, cset, eps, j_star, tighten_mode="scale",
+                    device: int = 0) -> CellProbe:
+    x0 = _validate_state(plant, x0)
+    scenario = np.asarray(scenario, dtype=np.float64)
+    if scenario.ndim != 2 or scenario.shape[1] != 3:
+        raise ConfigError(f"scenario must be 2-D with 3 columns, got {scenario.shape}")
+    if scenario.shape[0] < j_star + 1:
+        raise ConfigError(f"scenario length {scenario.shape[0]} too short: need >= "
+                          f"{j_star + 1}")
+    _require_device_plant(plant)
+    tight = _tightened(cset, eps, tighten_mode)
+    if not tight.contains(plant.steady_state_output(v)):
+        return CellProbe(False, False, CELL_VIOLATED, 0, None)
+    S = np.zeros((1, 1), dtype=np.uint8)
+    steps = np.zeros((1, 1), dtype=np.int32)
+    ctx = _capi.context(device)
+    ctx.fill(_problem(plant, cset, tight, j_star), x0, np.array([float(v)]),
+             np.array([0], np.int32), scenario[None], 1, None, S, steps)
+    st, sr = int(S[0, 0]), int(steps[0, 0])
+    ok = st == CELL_OK
+    return CellProbe(ok, True, st, sr, None if ok else sr)
+
+
+def check_candidate(plant, x0, v, scenario, cset, eps, j_star, tighten_mode="scale") -> bool:
+    return probe_candidate(plant, x0, v, scenario, cset, eps, j_star, tighten_mode).ok

@@ -1,0 +1,141 @@
+"""Closed-loop drivers (reference harness.py:52-224), governor on the B200.
+
+``run_closed_loop`` is the reference's driver with the device grid governor:
+every step the scenario set is the counter stream ``derive_seed(seed,
+"scenarios") + t`` (generated inside the kernel, never materialised), the
+governor picks v_t, and the true plant advances on the host with numpy's tanh
+plus its own disturbance stream ``derive_seed(seed, "plant")`` -- exactly the
+reference's arithmetic, so the v_t sequence is bit-identical.
+
+``run_closed_loop_bisection`` substitutes the nominal ``bisection_rg`` at
+harness.py:200 (configuration C1 of BASELINE.md; the reference ships no such
+driver).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .disturbance import DisturbanceModel, ScenarioSet, derive_seed, sample_scenarios
+from .errors import ConfigError, IntegrationOverflowError
+from .governor import GovernorState, bisection_rg, robust_rg_parallel
+
+__all__ = ["ReferenceProfile", "RunRecord", "run_closed_loop", "run_closed_loop_bisection",
+           "RUN_CSV_HEADER", "STATE_LIMIT"]
+
+RUN_CSV_HEADER = "t,r_t,v_t,y_t,kappa_opt,feasible,wall_us"
+STATE_LIMIT = 1e6
+
+
+@dataclass(frozen=True)
+class ReferenceProfile:
+    """Piecewise-constant reference r(t) from (t_start, r) points (harness.py:52-89)."""
+
+    points: tuple
+
+    def __post_init__(self):
+        try:
+            pts = tuple((int(t), float(r)) for t, r in self.points)
+        except (TypeError, ValueError) as e:
+            raise ConfigError(f"profile points must be (t_start, r) pairs: {e}") from None
+        if not pts:
+            raise ConfigError("profile needs at least one (t_start, r) point")
+        if pts[0][0] != 0:
+            raise ConfigError(f"first profile point must start at t=0, got {pts[0][0]}")
+        if any(b[0] <= a[0] for a, b in zip(pts, pts[1:])):
+            raise ConfigError("profile t_start values must be strictly increasing")
+        object.__setattr__(self, "points", pts)
+
+    def schedule(self, steps: int) -> np.ndarray:
+        starts = np.array([t for t, _ in self.points])
+        vals = np.array([r for _, r in self.points])
+        idx = np.searchsorted(starts, np.arange(steps), side="right") - 1
+        return vals[idx]
+
+
+@dataclass
+class RunRecord:
+    rows: list
+    config: dict
+    seed: int
+    aborted: bool = False
+    abort_reason: str | None = None
+    diag_rows: list = field(default_factory=list)
+
+    def violations(self, cset) -> int:
+        return sum(1 for row in self.rows if not cset.contains(row[3]))
+
+
+def _true_disturbance(model: DisturbanceModel, steps: int, seed: int, device: int) -> np.ndarray:
+    # lo + span * u at (plant_seed, 0, t, i): harness.py:172-174
+    return sample_scenarios(model, 1, steps, derive_seed(seed, "plant"), device=device).data[0]
+
+
+def _schedule(profile, steps):
+    if isinstance(profile, ReferenceProfile):
+        return profile.schedule(steps)
+    return np.asarray(profile, dtype=np.float64)[:steps]
+
+
+def run_closed_loop(plant, cset, model, config, profile, steps, seed, governor_on=True,
+                    x0=None, v0=0.0) -> RunRecord:
+    """The governed closed loop of harness.py:138-224 with the device governor."""
+    if steps < 1:
+        raise ConfigError(f"steps must be >= 1, got {steps}")
+    if model.state_dim != plant.state_dim:
+        raise ConfigError(f"disturbance model has {model.state_dim} states, plant has "
+                          f"{plant.state_dim}")
+    device = getattr(config, "device", 0)
+    x = plant.validate_state(np.zeros(plant.state_dim) if x0 is None else x0)
+    state = GovernorState(v_prev=float(v0))
+    scen_seed = derive_seed(seed, "scenarios")
+    d_true = _true_disturbance(model, steps, seed, device)
+    r_sched = _schedule(profile, steps)
+    rec = RunRecord(rows=[], config={"governor_on": governor_on, "j_star": config.j_star,
+                                     "n_sim": config.n_sim, "m_grid": config.m_grid,
+                                     "steps": steps, "backend": "cuda"}, seed=seed)
+    for t in range(steps):
+        r_t = float(r_sched[t])
+        if governor_on:
+            scen = sample_scenarios(model, config.n_sim, config.j_star + 1, seed=scen_seed + t,
+                                    device=device)
+            t0 = time.perf_counter()
+            res = robust_rg_parallel(plant, x, state, r_t, cset, scen, config)
+            wall_us = int((time.perf_counter() - t0) * 1e6)
+            v_t, kappa, feas = res.v_applied, res.kappa_opt, res.feasible
+            rec.diag_rows.append(res.diagnostics_csv_row(t))
+        else:
+            v_t, kappa, feas, wall_us = r_t, 1.0, True, 0
+            state.v_prev = v_t
+        rec.rows.append((t, r_t, v_t, float(plant.output(x, v_t)), float(kappa), bool(feas),
+                         wall_us))
+        try:
+            x = plant.step(x, v_t) + d_true[t]
+        except IntegrationOverflowError as e:
+            rec.aborted, rec.abort_reason = True, f"step {t}: {e}"
+            return rec
+        if not np.all(np.isfinite(x)) or np.any(np.abs(x) > STATE_LIMIT):
+            rec.aborted, rec.abort_reason = True, f"step {t}: state left the operating box"
+            return rec
+    return rec
+
+
+def run_closed_loop_bisection(plant, cset, model, config, profile, steps, seed, x0=None,
+                              v0=0.0):
+    """C1: the same loop with the nominal bisection governor; returns
+    [(KappaResult, y_t)] per step."""
+    device = getattr(config, "device", 0)
+    x = plant.validate_state(np.zeros(plant.state_dim) if x0 is None else x0)
+    state = GovernorState(v_prev=float(v0))
+    d_true = _true_disturbance(model, steps, seed, device)
+    r_sched = _schedule(profile, steps)
+    out = []
+    for t in range(steps):
+        y_t = float(plant.output(x, state.v_prev))
+        res = bisection_rg(plant, x, state, float(r_sched[t]), cset, config)
+        out.append((res, y_t))
+        x = plant.step(x, res.v_applied) + d_true[t]
+    return out

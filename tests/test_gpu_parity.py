@@ -1,0 +1,281 @@
+"""Parity of the CUDA path with the reference (golden fixtures) and the CPU oracle.
+
+Everything here runs through the C ABI on a B200 (``-m gpu``).  The bar is
+bit-exact: identical cell statuses and step counts, identical feasibility
+matrices, identical bisection paths, identical kappa and v_t doubles.
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_2510_08288_b200 as rg
+from paper_2510_08288_b200 import _capi
+from paper_2510_08288_b200.governor import bisect_paths
+from conftest import GOLDEN, bis_case, fill_case
+
+pytestmark = pytest.mark.gpu
+
+with np.load(GOLDEN) as _z:
+    N_FILL = len(_z["fill_names"])
+    N_BIS = len(_z["bis_names"])
+
+MASK = (1 << 64) - 1
+PLANT = rg.make_plant("surrogate-fc")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return _capi.context(0)
+
+
+def _cset(c):
+    return rg.ConstraintSet(c["lower"], c["upper"], c["anchor"])
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.uint64)
+
+
+# ----------------------------------------------------------------- tanh
+
+def test_device_tanh_matches_host_libm_golden(ctx, golden, orc):
+    x = golden["tanh_x"]
+    y = ctx.tanh(x)
+    assert np.array_equal(_bits(y), _bits(orc.libm_tanh(x)))
+    # the fixture was written on the build container's libm (FMA build)
+    if ctx.tanh_variant == _capi.RG_TANH_FMA:
+        assert np.array_equal(_bits(y), _bits(golden["tanh_libm"]))
+
+
+def test_device_tanh_bit_exact_sweep(ctx, orc):
+    rng = np.random.default_rng(5)
+    x = np.concatenate([
+        rng.uniform(-3, 3, 2_000_000), rng.uniform(-25, 25, 500_000),
+        np.ldexp(rng.uniform(0.5, 1.0, 200_000), rng.integers(-64, 6, 200_000)),
+        -np.ldexp(rng.uniform(0.5, 1.0, 200_000), rng.integers(-64, 6, 200_000)),
+        np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 22.0, -22.0, 5e-324, 1.0, -1.0]),
+    ])
+    y = ctx.tanh(x)
+    ref = orc.libm_tanh(x)
+    mism = np.flatnonzero(_bits(y) != _bits(ref))
+    assert mism.size == 0, f"{mism.size} mismatches, first x={x[mism[:5]]}"
+
+
+# ----------------------------------------------------------------- RNG
+
+def test_sample_scenarios_bit_exact(golden):
+    model = rg.DisturbanceModel(ranges=((-0.003, 0.001), (0.0, 0.002), (-1e-4, 1e-4)))
+    s = rg.sample_scenarios(model, 5, 9, seed=2**63 + 5)
+    assert np.array_equal(s.data, golden["scen_small"])
+    big = rg.sample_scenarios(rg.DisturbanceModel.scaled(0.001, 3), 1000, 257, seed=7)
+    assert hashlib.sha256(big.data.tobytes()).digest() == golden["scen_big_sha"].tobytes()
+    wrap = rg.sample_scenarios(rg.DisturbanceModel.scaled(0.001, 3), 3, 5,
+                               seed=((MASK - 1) + 5) & MASK)
+    assert np.array_equal(wrap.data, golden["scen_wrap"])
+    unit = rg.DisturbanceModel(ranges=((0.0, 1.0),) * 3)
+    k0set = rg.ScenarioSet.generated(unit, 4, 6, 2**64 - 3, k0=1_000_000)
+    assert np.array_equal(k0set.data, golden["scen_small_k0"])
+
+
+def test_sample_prefix_and_shards(orc):
+    model = rg.DisturbanceModel.scaled(1.0, 3)
+    big = rg.sample_scenarios(model, 300, 17, seed=42)
+    assert np.array_equal(big.prefix(16).data, big.data[:16])
+    parts = np.concatenate([big.shard(r, 3).data for r in range(3)])
+    assert np.array_equal(parts, big.data)
+    assert np.array_equal(big.data, orc.sample(42, 300, 17, model.ranges))
+
+
+# ----------------------------------------------------------------- cells
+
+def _problem(c, tight=None):
+    cset = _cset(c)
+    tight = tight or rg.tighten(cset, c["eps"])
+    lo, hi = rg.admissible_setpoints(tight.lower, tight.upper)
+    return _capi.Problem(0.01, cset.lower, cset.upper, lo, hi, c["j_star"], 0)
+
+
+@pytest.mark.parametrize("source", ["staged", "rng"])
+@pytest.mark.parametrize("idx", range(N_FILL))
+def test_fill_cells_bit_exact(ctx, golden, idx, source):
+    c = fill_case(golden, idx)
+    grid = rg.grid_kappas(c["m_grid"])
+    v_rows = np.array([rg.update_setpoint(c["v_prev"], c["r"], float(k)) for k in grid])
+    S = np.full((c["m_grid"], c["n_sim"]), 7, np.uint8)
+    steps = np.full((c["m_grid"], c["n_sim"]), -1, np.int32)
+    rows = np.arange(c["m_grid"], dtype=np.int32)
+    if source == "staged":
+        dist = rg.sample_scenarios(rg.DisturbanceModel(c["ranges"]), c["n_sim"],
+                                   c["j_star"] + 1, c["seed"]).data
+        ctx.fill(_problem(c), c["x0"], v_rows, rows, dist, c["n_sim"], None, S, steps)
+    else:
+        m = rg.DisturbanceModel(c["ranges"])
+        scen = _capi.make_scenarios(c["seed"], 0, c["n_sim"], m.lo, m.span)
+        ctx.fill(_problem(c), c["x0"], v_rows, rows, None, c["n_sim"], scen, S, steps)
+    assert np.array_equal(S, c["S_all"]), c["name"]
+    assert np.array_equal(steps, c["steps_all"]), c["name"]
+
+
+@pytest.mark.parametrize("idx", range(N_FILL))
+def test_fill_feasibility_matches_reference(golden, idx):
+    c = fill_case(golden, idx)
+    scen = rg.sample_scenarios(rg.DisturbanceModel(c["ranges"]), c["n_sim"], c["j_star"] + 1,
+                               c["seed"])
+    for s in (scen, rg.ScenarioSet(scen.data)):   # generated and dense inputs
+        stats = {}
+        P = rg.fill_feasibility("cuda", PLANT, c["x0"], c["v_prev"], c["r"],
+                                rg.grid_kappas(c["m_grid"]), s, _cset(c), c["eps"],
+                                c["j_star"], stats=stats)
+        assert np.array_equal(P, c["P"]), c["name"]
+        got = [stats[k] for k in ("sims_run", "early_terms", "overflows", "ss_pruned_rows",
+                                  "dedup_rows")]
+        assert got == [int(v) for v in c["stats"]], c["name"]
+
+
+@pytest.mark.parametrize("keep", [True, False])
+@pytest.mark.parametrize("idx", range(N_FILL))
+def test_robust_rg_parallel_matches_reference(golden, idx, keep):
+    c = fill_case(golden, idx)
+    cfg = rg.GovernorConfig(j_star=c["j_star"], epsilon=c["eps"], m_grid=c["m_grid"],
+                            n_sim=c["n_sim"], prefix_mode=c["prefix"], keep_matrix=keep)
+    scen = rg.sample_scenarios(rg.DisturbanceModel(c["ranges"]), c["n_sim"], c["j_star"] + 1,
+                               c["seed"])
+    for s in (scen, rg.ScenarioSet(scen.data)):
+        state = rg.GovernorState(c["v_prev"])
+        res = rg.robust_rg_parallel(PLANT, c["x0"], state, c["r"], _cset(c), s, cfg)
+        assert (res.kappa_opt, res.v_applied, float(res.feasible)) == \
+            tuple(float(v) for v in c["result"]), c["name"]
+        if keep:
+            assert np.array_equal(res.matrix, c["P"]), c["name"]
+            d = res.diagnostics
+            got = [d[k] for k in ("sims_run", "early_terms", "overflows", "ss_pruned_rows",
+                                  "dedup_rows")]
+            assert got == [int(v) for v in c["stats"]], c["name"]
+
+
+# ----------------------------------------------------------------- bisection
+
+@pytest.mark.parametrize("idx", range(N_BIS))
+def test_robust_rg_sequential_matches_reference(golden, idx):
+    c = bis_case(golden, idx)
+    cfg = rg.GovernorConfig(j_star=c["j_star"], epsilon=c["eps"], n_kappa=c["n_kappa"],
+                            n_sim=c["n_sim"])
+    scen = rg.sample_scenarios(rg.DisturbanceModel(c["ranges"]), c["n_sim"], c["j_star"] + 1,
+                               c["seed"])
+    for s in (scen, rg.ScenarioSet(scen.data)):
+        res = rg.robust_rg_sequential(PLANT, c["x0"], rg.GovernorState(c["v_prev"]), c["r"],
+                                      _cset(c), s, cfg)
+        d = res.diagnostics
+        assert (res.kappa_opt, res.v_applied, float(res.feasible), d["sims_run"],
+                d["early_terms"]) == tuple(float(v) for v in c["result"]), c["name"]
+    kap, fnd, cel, erl, pk, po = bisect_paths(PLANT, c["x0"], c["v_prev"], c["r"], _cset(c),
+                                              scen, cfg)
+    per = np.stack([kap, fnd, cel, erl], axis=1).astype(np.float64)
+    assert np.array_equal(per, c["per"]), c["name"]
+    ref_k, ref_ok = c["paths"][..., 0], c["paths"][..., 1]
+    used = ~np.isnan(ref_k)
+    assert np.array_equal(np.isnan(pk), ~used)
+    assert np.array_equal(pk[used], ref_k[used])
+    assert np.array_equal(po[used], ref_ok[used].astype(np.uint8))
+
+
+def test_nominal_bisection_anchor(golden):
+    res = rg.bisection_rg(PLANT, np.zeros(3), rg.GovernorState(0.0), 2.5,
+                          rg.ConstraintSet(-0.9, 0.9), rg.GovernorConfig())
+    d = res.diagnostics
+    assert (res.kappa_opt, res.v_applied, float(res.feasible), d["sims_run"],
+            d["early_terms"]) == tuple(float(v) for v in golden["nominal_anchor"])
+    assert res.kappa_opt == 0.5078125
+
+
+def test_closed_loop_c1_bisection_trace(golden):
+    """Config 1: desk-scale nominal bisection governor, 2000 steps, v_t bit-exact."""
+    from paper_2510_08288_b200.harness import run_closed_loop_bisection
+
+    prof = golden["desk_profile"]
+    rows = run_closed_loop_bisection(PLANT, rg.ConstraintSet(-0.9, 0.9),
+                                     rg.DisturbanceModel.scaled(0.001, 3), rg.GovernorConfig(),
+                                     prof, 2000, 2024)
+    ref = golden["c1_trace"]
+    got = np.array([[r.kappa_opt, r.v_applied, float(r.feasible), y, r.diagnostics["sims_run"],
+                     r.diagnostics["early_terms"]] for r, y in rows])
+    assert np.array_equal(got, ref)
+
+
+def test_closed_loop_desk_grid_trace(golden):
+    from paper_2510_08288_b200.harness import ReferenceProfile, run_closed_loop
+
+    prof = ReferenceProfile(((0, 0.4), (400, 2.5), (1000, -2.5), (1600, 0.2)))
+    rec = run_closed_loop(PLANT, rg.ConstraintSet(-0.9, 0.9),
+                          rg.DisturbanceModel.scaled(0.001, 3),
+                          rg.GovernorConfig(n_sim=64), prof, 2000, 2024)
+    assert not rec.aborted
+    got = np.array([[row[2], row[3], row[4], float(row[5])] for row in rec.rows])
+    assert np.array_equal(got, golden["desk_grid_trace"])
+
+
+def test_closed_loop_c3_truncated(golden):
+    from paper_2510_08288_b200.harness import ReferenceProfile, run_closed_loop
+
+    prof = ReferenceProfile(((0, 0.4), (400, 2.5), (1000, -2.5), (1600, 0.2)))
+    rec = run_closed_loop(PLANT, rg.ConstraintSet(-0.9, 0.9),
+                          rg.DisturbanceModel.scaled(0.001, 3),
+                          rg.GovernorConfig(n_sim=1000), prof, 40, 2024)
+    got = np.array([[row[2], row[3], row[4], float(row[5])] for row in rec.rows])
+    assert np.array_equal(got, golden["c3_trace40"])
+
+
+# ----------------------------------------------------------------- edges & errors
+
+def test_errors_map_to_reference_types():
+    box = rg.ConstraintSet(-0.9, 0.9)
+    cfg = rg.GovernorConfig(j_star=64, n_sim=1)
+    with pytest.raises(rg.ConfigError):   # short horizon (governor.py:175-178)
+        rg.robust_rg_parallel(PLANT, np.zeros(3), rg.GovernorState(), 1.0, box,
+                              rg.zero_scenarios(3, 64), cfg)
+    with pytest.raises(rg.ConfigError):   # non-finite state
+        rg.robust_rg_parallel(PLANT, np.array([np.nan, 0, 0]), rg.GovernorState(), 1.0, box,
+                              rg.zero_scenarios(3, 65), cfg)
+    lin = rg.LinearOraclePlant([[0.5]], [0.5], [1.0])
+    with pytest.raises(rg.BackendUnavailableError):  # backend_gpu.py:66-71
+        rg.fill_feasibility("cuda", lin, np.zeros(1), 0.0, 1.0, rg.grid_kappas(4),
+                            rg.ScenarioSet(np.zeros((1, 33, 1))), box, 0.05, 32)
+    with pytest.raises(rg.ConfigError):
+        rg.fill_feasibility("serial", PLANT, np.zeros(3), 0.0, 1.0, rg.grid_kappas(4),
+                            rg.zero_scenarios(3, 33), box, 0.05, 32)
+    with pytest.raises(rg.ConfigError):
+        rg.robust_rg_sequential(PLANT, np.zeros(3), rg.GovernorState(), 1.0, box,
+                                rg.zero_scenarios(3, 33), rg.GovernorConfig(j_star=32, n_sim=4))
+
+
+def test_infeasible_policies():
+    box = rg.ConstraintSet(-0.9, 0.9)
+    x_bad = np.array([2.0, 0.0, 0.0])
+    cfg = rg.GovernorConfig(j_star=32, n_sim=1, m_grid=8)
+    state = rg.GovernorState(0.7)
+    res = rg.robust_rg_parallel(PLANT, x_bad, state, 1.0, box, rg.zero_scenarios(3, 33), cfg)
+    assert (res.kappa_opt, res.v_applied, res.feasible, state.v_prev) == (0.0, 0.7, False, 0.7)
+    with pytest.raises(rg.InfeasibleError):
+        rg.robust_rg_parallel(PLANT, x_bad, rg.GovernorState(0.7), 1.0, box,
+                              rg.zero_scenarios(3, 33),
+                              rg.GovernorConfig(j_star=32, n_sim=1, m_grid=8,
+                                                infeasible_policy="error"))
+
+
+def test_repeated_steps_reset_device_accumulators():
+    """The last-block reset must leave the counters clean for the next launch."""
+    box = rg.ConstraintSet(-0.9, 0.9)
+    cfg = rg.GovernorConfig(j_star=128, n_sim=500, m_grid=32)
+    model = rg.DisturbanceModel.scaled(0.02, 3)
+    outs = []
+    for rep in range(3):
+        for r in (2.5, 0.3):
+            scen = rg.sample_scenarios(model, 500, 129, seed=11)
+            res = rg.robust_rg_parallel(PLANT, np.zeros(3), rg.GovernorState(0.0), r, box,
+                                        scen, cfg)
+            outs.append((r, res.kappa_opt, res.diagnostics["early_terms"]))
+    assert outs[0:2] == outs[2:4] == outs[4:6]
