@@ -59,6 +59,11 @@ extern "C" {
 #define RG_ASYNC 0x2        /* enqueue only; no host readback, no sync */
 #define RG_ABANDON 0x4      /* grid step: stop rows already known infeasible */
 #define RG_NO_TIMING 0x8    /* skip the CUDA-event kernel timing */
+#define RG_TANH_LOCKSTEP 0x10 /* rg_tanh: use the rollout's lockstep form */
+#define RG_FUSED_RNG 0x20   /* RNG source: hash inside the rollout loop */
+#define RG_STAGE_RNG 0x40   /* RNG source: generate the SoA tensor first */
+/* With neither RG_FUSED_RNG nor RG_STAGE_RNG an RNG source is staged when
+ * n_sim * j_star <= 4M scenario-steps (it then stays in L2) and fused above. */
 
 typedef struct rg_ctx rg_ctx;
 

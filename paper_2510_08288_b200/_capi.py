@@ -9,6 +9,7 @@ raises BackendUnavailableError.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -16,11 +17,14 @@ import numpy as np
 
 from .errors import BackendUnavailableError, ConfigError, RefgovError
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "librefgov_b200.so"
+LIB_PATH = Path(os.environ.get("RG_LIB_PATH") or
+                Path(__file__).resolve().parent / "_lib" / "librefgov_b200.so")
 
 RG_OK, RG_E_NODEVICE, RG_E_UNSUPPORTED, RG_E_ARGS, RG_E_CUDA = 0, -1, -2, -3, -4
 RG_TANH_AUTO, RG_TANH_FMA, RG_TANH_GENERIC = 0, 1, 2
 RG_DEVICE_PTRS, RG_ASYNC, RG_ABANDON, RG_NO_TIMING = 0x1, 0x2, 0x4, 0x8
+RG_TANH_LOCKSTEP, RG_FUSED_RNG, RG_STAGE_RNG = 0x10, 0x20, 0x40
+_RNG_FLAGS = {None: 0, "fused": RG_FUSED_RNG, "staged": RG_STAGE_RNG}
 
 _i32, _i64, _u64, _d, _vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, \
     ctypes.c_void_p
@@ -162,10 +166,11 @@ class Context:
         check(self.lib.rg_synchronize(self.handle))
 
     # -- entry points ---------------------------------------------------
-    def tanh(self, x: np.ndarray) -> np.ndarray:
+    def tanh(self, x: np.ndarray, lockstep: bool = False) -> np.ndarray:
         x = np.ascontiguousarray(x, dtype=np.float64)
         y = np.empty_like(x)
-        check(self.lib.rg_tanh(self.handle, _p(x), _p(y), x.size, 0))
+        check(self.lib.rg_tanh(self.handle, _p(x), _p(y), x.size,
+                               RG_TANH_LOCKSTEP if lockstep else 0))
         return y
 
     def sample(self, seed: int, k0: int, n_sim: int, horizon: int, lo, span) -> np.ndarray:
@@ -177,7 +182,7 @@ class Context:
         return out
 
     def fill(self, prob: Problem, x0, v_rows, rows, dist, n_sim, scen: Scenarios | None,
-             S: np.ndarray, steps: np.ndarray) -> None:
+             S: np.ndarray, steps: np.ndarray, rng_mode: str | None = None) -> None:
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
         v_rows = np.ascontiguousarray(v_rows, dtype=np.float64)
         rows = np.ascontiguousarray(rows, dtype=np.int32)
@@ -188,10 +193,11 @@ class Context:
         check(self.lib.rg_fill(self.handle, ctypes.byref(prob), _p(x0), _p(v_rows), v_rows.size,
                                _p(rows), rows.size, _p(dist), int(n_sim), int(horizon),
                                ctypes.byref(scen) if scen is not None else None, _p(S),
-                               _p(steps), 0))
+                               _p(steps), _RNG_FLAGS[rng_mode]))
 
     def grid_step(self, prob: Problem, x0, v_prev, r, m_grid, prefix_mode, dist, n_sim,
-                  scen: Scenarios | None, want_pbits: bool, abandon: bool = False):
+                  scen: Scenarios | None, want_pbits: bool, abandon: bool = False,
+                  rng_mode: str | None = None):
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
         horizon = 0
         if dist is not None:
@@ -200,7 +206,7 @@ class Context:
         viol = np.zeros(m_grid, dtype=np.uint32)
         pbits = np.zeros((m_grid, (n_sim + 31) // 32), dtype=np.uint32) if want_pbits else None
         res = GridResult()
-        flags = RG_ABANDON if abandon else 0
+        flags = (RG_ABANDON if abandon else 0) | _RNG_FLAGS[rng_mode]
         check(self.lib.rg_grid_step(self.handle, ctypes.byref(prob), _p(x0), float(v_prev),
                                     float(r), int(m_grid), int(bool(prefix_mode)), _p(dist),
                                     int(n_sim), int(horizon),
@@ -209,7 +215,8 @@ class Context:
         return res, viol, pbits
 
     def bisect(self, prob: Problem, x0, v_prev, r, n_kappa, dist, n_sim,
-               scen: Scenarios | None, per_scenario: bool = False, paths: bool = False):
+               scen: Scenarios | None, per_scenario: bool = False, paths: bool = False,
+               rng_mode: str | None = None):
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
         horizon = 0
         if dist is not None:
@@ -228,7 +235,8 @@ class Context:
         check(self.lib.rg_bisect(self.handle, ctypes.byref(prob), _p(x0), float(v_prev), float(r),
                                  int(n_kappa), _p(dist), int(n_sim), int(horizon),
                                  ctypes.byref(scen) if scen is not None else None, _p(kap),
-                                 _p(fnd), _p(cel), _p(erl), _p(pk), _p(po), ctypes.byref(res), 0))
+                                 _p(fnd), _p(cel), _p(erl), _p(pk), _p(po), ctypes.byref(res),
+                                 _RNG_FLAGS[rng_mode]))
         per = (kap, fnd, cel, erl) if per_scenario else None
         return res, per, ((pk, po) if paths else None)
 

@@ -198,6 +198,27 @@ int32_t stage_dist(rg_ctx* ctx, const double* dist, int64_t n_sim, int64_t horiz
     return RG_OK;
 }
 
+// Small scenario sets: generate the RNG stream once into SoA scratch (L2
+// resident) so the per-cell loop loads three doubles per step instead of
+// re-hashing them for every candidate row.  Large sets keep the fused RNG.
+constexpr int64_t kStageMaxScenarioSteps = 4ll << 20;  // 96 MB of SoA
+
+int32_t stage_rng(rg_ctx* ctx, const rg_scenarios* rng, int64_t n_sim, int32_t j_star,
+                  const double** soa, int64_t* ld) {
+    *ld = (n_sim + 31) / 32 * 32;
+    RG_CUDA(ctx->soa.ensure((size_t)j_star * 3 * (*ld) * sizeof(double)));
+    RG_CUDA(rg::launch_gen_soa(make_stream(rng), rng->k0, n_sim, j_star, *ld,
+                               ctx->soa.as<double>(), ctx->stream));
+    *soa = ctx->soa.as<double>();
+    return RG_OK;
+}
+
+bool want_stage(int64_t n_sim, int32_t j_star, int32_t flags) {
+    if (flags & RG_FUSED_RNG) return false;
+    if (flags & RG_STAGE_RNG) return true;
+    return n_sim * (int64_t)j_star <= kStageMaxScenarioSteps;
+}
+
 int32_t grow_grid(rg_ctx* ctx, int m) {
     if (m <= ctx->grid_cap) return RG_OK;
     const int cap = std::max(m, 64);
@@ -359,7 +380,8 @@ int32_t rg_tanh(rg_ctx* ctx, const double* x, double* y, int64_t n, int32_t flag
         dx = ctx->tmp_a.as<double>();
         dy = ctx->tmp_b.as<double>();
     }
-    RG_CUDA(rg::launch_tanh(dx, dy, n, ctx->variant == rg::kTanhFma, ctx->stream));
+    RG_CUDA(rg::launch_tanh(dx, dy, n, ctx->variant == rg::kTanhFma,
+                            (flags & RG_TANH_LOCKSTEP) != 0, ctx->stream));
     if (!(flags & RG_DEVICE_PTRS))
         RG_CUDA(cudaMemcpyAsync(y, dy, bytes, cudaMemcpyDeviceToHost, ctx->stream));
     RG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -438,8 +460,11 @@ int32_t rg_fill(rg_ctx* ctx, const rg_problem* prob, const double* x0, const dou
     a.n_rows = n_rows;
     a.n_sim = n_sim;
     a.tpb = tpb_for(ctx, n_sim, n_rows);
-    const bool use_rng = dist == nullptr;
-    if (use_rng) {
+    bool use_rng = dist == nullptr;
+    if (use_rng && want_stage(n_sim, prob->j_star, flags)) {
+        if ((rc = stage_rng(ctx, rng, n_sim, prob->j_star, &a.soa, &a.ld))) return rc;
+        use_rng = false;
+    } else if (use_rng) {
         a.stream = make_stream(rng);
         a.k0 = rng->k0;
     } else {
@@ -538,8 +563,11 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
     a.m_grid = m_grid;
     a.prefix_mode = prefix_mode ? 1 : 0;
     a.n_sim = n_sim;
-    const bool use_rng = dist == nullptr;
-    if (use_rng) {
+    bool use_rng = dist == nullptr;
+    if (use_rng && want_stage(n_sim, prob->j_star, flags)) {
+        if ((rc = stage_rng(ctx, rng, n_sim, prob->j_star, &a.soa, &a.ld))) return rc;
+        use_rng = false;
+    } else if (use_rng) {
         a.stream = make_stream(rng);
         a.k0 = rng->k0;
     } else if ((rc = stage_dist(ctx, dist, n_sim, horizon, prob->j_star, flags, &a.soa, &a.ld))) {
@@ -623,6 +651,9 @@ int32_t rg_bisect(rg_ctx* ctx, const rg_problem* prob, const double* x0, double 
         src = 2;
         if ((rc = stage_dist(ctx, dist, n_sim, horizon, prob->j_star, flags, &a.soa, &a.ld)))
             return rc;
+    } else if (rng && want_stage(n_sim, prob->j_star, flags)) {
+        src = 2;
+        if ((rc = stage_rng(ctx, rng, n_sim, prob->j_star, &a.soa, &a.ld))) return rc;
     } else if (rng) {
         src = 1;
         a.stream = make_stream(rng);

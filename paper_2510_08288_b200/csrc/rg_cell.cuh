@@ -17,6 +17,8 @@
 #include "rg_math.cuh"
 #include "rg_rng.cuh"
 
+#include <type_traits>
+
 namespace rg {
 
 enum CellStatus : int { kViolated = 0, kOk = 1, kOverflow = 2, kAbandoned = 3 };
@@ -35,11 +37,12 @@ struct CellConst {
 RG_HD bool in_bounds(double y, double lo, double hi) { return lo <= y && y <= hi; }
 
 // x_{j+1} = RK4(x_j, v) + d_j with Python's operation order (kernels.py:56-79).
+// Reference form: used by the host self-test and as the specification of the
+// pipelined rollout below.
 template <bool FMA>
 RG_HD void sfc_step(double& x1, double& x2, double& x3, double v, const CellConst& p,
                     double d0, double d1, double d2) {
     const double h = p.h, hh = p.hh;
-    // x2 chain (no tanh): k12, a2, k22, b2, k32, c2, k42
     const double k12 = add(-x2, v);
     const double a2 = add(x2, mul(hh, k12));
     const double k22 = add(-a2, v);
@@ -47,12 +50,8 @@ RG_HD void sfc_step(double& x1, double& x2, double& x3, double v, const CellCons
     const double k32 = add(-b2, v);
     const double c2 = add(x2, mul(h, k32));
     const double k42 = add(-c2, v);
-    // four independent tanh evaluations
-    const double t1 = tanh_glibc<FMA>(x2);
-    const double t2 = tanh_glibc<FMA>(a2);
-    const double t3 = tanh_glibc<FMA>(b2);
-    const double t4 = tanh_glibc<FMA>(c2);
-    // x1 / x3 chains
+    double t1, t2, t3, t4;
+    tanh4<FMA>(x2, a2, b2, c2, t1, t2, t3, t4);
     const double k11 = add(-x1, t1);
     const double k13 = add(mul(-2.0, x3), x1);
     const double a1 = add(x1, mul(hh, k11));
@@ -67,7 +66,6 @@ RG_HD void sfc_step(double& x1, double& x2, double& x3, double v, const CellCons
     const double c3 = add(x3, mul(h, k33));
     const double k41 = add(-c1, t4);
     const double k43 = add(mul(-2.0, c3), c1);
-    // x + c*(((k1 + 2 k2) + 2 k3) + k4) + d
     const double s1 = add(add(add(k11, mul(2.0, k21)), mul(2.0, k31)), k41);
     const double s2 = add(add(add(k12, mul(2.0, k22)), mul(2.0, k32)), k42);
     const double s3 = add(add(add(k13, mul(2.0, k23)), mul(2.0, k33)), k43);
@@ -76,36 +74,117 @@ RG_HD void sfc_step(double& x1, double& x2, double& x3, double v, const CellCons
     x3 = add(add(x3, mul(p.c, s3)), d2);
 }
 
+// The x2 sub-chain of one step: dx2/dt = -x2 + v does not involve x1 or x3,
+// so the stage values a2, b2, c2 (the tanh arguments) and the increment s2
+// depend on x2 alone.
+struct X2Stage {
+    double a2, b2, c2, s2;
+};
+
+template <bool FMA>
+RG_HD X2Stage x2_stage(double x2, double v, const CellConst& p) {
+    X2Stage r;
+    const double k12 = add(-x2, v);
+    r.a2 = add(x2, mul(p.hh, k12));
+    const double k22 = add(-r.a2, v);
+    r.b2 = add(x2, mul(p.hh, k22));
+    const double k32 = add(-r.b2, v);
+    r.c2 = add(x2, mul(p.h, k32));
+    const double k42 = add(-r.c2, v);
+    r.s2 = add(add(add(k12, mul(2.0, k22)), mul(2.0, k32)), k42);
+    return r;
+}
+
+// The x1/x3 part of one step given the step's four tanh values.
+template <bool FMA>
+RG_HD void x13_update(double& x1, double& x3, double t1, double t2, double t3, double t4,
+                      const CellConst& p, double d0, double d2) {
+    const double h = p.h, hh = p.hh;
+    const double k11 = add(-x1, t1);
+    const double k13 = add(mul(-2.0, x3), x1);
+    const double a1 = add(x1, mul(hh, k11));
+    const double a3 = add(x3, mul(hh, k13));
+    const double k21 = add(-a1, t2);
+    const double k23 = add(mul(-2.0, a3), a1);
+    const double b1 = add(x1, mul(hh, k21));
+    const double b3 = add(x3, mul(hh, k23));
+    const double k31 = add(-b1, t3);
+    const double k33 = add(mul(-2.0, b3), b1);
+    const double c1 = add(x1, mul(h, k31));
+    const double c3 = add(x3, mul(h, k33));
+    const double k41 = add(-c1, t4);
+    const double k43 = add(mul(-2.0, c3), c1);
+    const double s1 = add(add(add(k11, mul(2.0, k21)), mul(2.0, k31)), k41);
+    const double s3 = add(add(add(k13, mul(2.0, k23)), mul(2.0, k33)), k43);
+    x1 = add(add(x1, mul(p.c, s1)), d0);
+    x3 = add(add(x3, mul(p.c, s3)), d2);
+}
+
 // ---- disturbance sources ---------------------------------------------------
+
+struct D3 {
+    double d0, d1, d2;
+};
+
+constexpr int kRingStride = 128;  // max threads per block of the rollout kernels
 
 // Fused counter RNG: the scenario tensor never exists in memory.
 struct RngSource {
     ScenarioStream s;
     uint64_t K;  // sm(sm(seed) ^ k)
-    RG_HD void get(int32_t j, double& d0, double& d1, double& d2) const {
-        disturbance_at(s, K, (uint64_t)j, d0, d1, d2);
+    RG_HD D3 load(int32_t j) const {
+        D3 r;
+        disturbance_at(s, K, (uint64_t)j, r.d0, r.d1, r.d2);
+        return r;
     }
 };
 
 // Staged structure-of-arrays tensor d[(j*3 + i) * ld + k] (coalesced across k).
+// The rollout streams it through a two-slot per-thread ring in shared memory
+// filled with cp.async two steps ahead of use, so no register ever waits on
+// an in-flight L2 load (ring layout [slot][comp][thread]: conflict-free).
 struct SoaSource {
     const double* d;  // already offset by k
     int64_t ld;       // padded scenario count
-    __device__ __forceinline__ void get(int32_t j, double& d0, double& d1, double& d2) const {
+    double* ring;     // &ring[0][0][threadIdx.x] of a [2][3][RING_STRIDE] array
+    __device__ __forceinline__ D3 load(int32_t j) const {
         const double* p = d + (int64_t)j * 3 * ld;
-        d0 = __ldg(p);
-        d1 = __ldg(p + ld);
-        d2 = __ldg(p + 2 * ld);
+        return D3{__ldg(p), __ldg(p + ld), __ldg(p + 2 * ld)};
+    }
+    __device__ __forceinline__ void issue(int32_t j, int slot) const {
+        const double* p = d + (int64_t)j * 3 * ld;
+        double* r = ring + slot * 3 * kRingStride;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(r + i * kRingStride);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(p + i * ld));
+        }
+    }
+    __device__ __forceinline__ D3 read(int slot) const {
+        const double* r = ring + slot * 3 * kRingStride;
+        return D3{r[0], r[kRingStride], r[2 * kRingStride]};
     }
 };
 
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
 // Nominal prediction (bisection_rg: zero disturbance, governor.py:448).
 struct ZeroSource {
-    RG_HD void get(int32_t, double& d0, double& d1, double& d2) const { d0 = d1 = d2 = 0.0; }
+    RG_HD D3 load(int32_t) const { return D3{0.0, 0.0, 0.0}; }
 };
 
 // One cell.  POLL: every 32 steps check a row-level "already infeasible"
 // flag and abandon (used only when the caller wants verdicts, not P).
+//
+// Software-pipelined by one step: iteration j finishes x1/x3 of step j with
+// the tanh values computed in iteration j-1, while it already runs the x2
+// chain and the four tanh of step j+1 (they need x2_{j+1} only).  The two
+// halves are independent, so their instruction streams interleave; every
+// value is still produced by the reference's operations on the reference's
+// operands, so the bits are those of sfc_step.  A step j+1 that is never
+// reached (early exit) only wastes its speculative tanh work.
 template <bool FMA, bool POLL, class Src>
 __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2, double x3,
                                        double v, const Src& src, int32_t& steps,
@@ -114,26 +193,69 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
         steps = 0;
         return kViolated;
     }
-    for (int32_t j = 0; j < p.j_star; ++j) {
-        double d0, d1, d2;
-        src.get(j, d0, d1, d2);
-        sfc_step<FMA>(x1, x2, x3, v, p, d0, d1, d2);
-        if (!(fabs(x1) <= kStateLimit && fabs(x2) <= kStateLimit && fabs(x3) <= kStateLimit)) {
+    const int32_t J = p.j_star;
+    constexpr bool kRing = std::is_same<Src, SoaSource>::value;
+    // prologue: tanh values of step 0 and x2 after step 0
+    D3 d;
+    if constexpr (kRing) {
+        src.issue(0, 0);
+        cp_async_commit();
+        src.issue(J > 1 ? 1 : 0, 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        d = src.read(0);
+    } else {
+        d = src.load(0);
+    }
+    X2Stage st = x2_stage<FMA>(x2, v, p);
+    double t1, t2, t3, t4;
+    tanh4<FMA>(x2, st.a2, st.b2, st.c2, t1, t2, t3, t4);
+    double x2n = add(add(x2, mul(p.c, st.s2)), d.d1);
+    for (int32_t j = 0; j < J; ++j) {
+        // step j's slot was drained into `d` last iteration: refill it with step j+2
+        if constexpr (kRing) {
+            if (j + 2 < J) src.issue(j + 2, j & 1);
+            cp_async_commit();
+        }
+        // step j+1's x2 chain and tanh values (speculative past an exit)
+        const X2Stage sn = x2_stage<FMA>(x2n, v, p);
+        double u1, u2, u3, u4;
+        tanh4<FMA>(x2n, sn.a2, sn.b2, sn.c2, u1, u2, u3, u4);
+        D3 dn;
+        if constexpr (kRing) {
+            cp_async_wait<1>();  // step j+1 landed (issued one iteration ago)
+            dn = src.read((j + 1) & 1);
+        } else {
+            dn = src.load(j + 1 < J ? j + 1 : j);
+        }
+        const double x2nn = add(add(x2n, mul(p.c, sn.s2)), dn.d1);
+        // step j's x1/x3
+        x13_update<FMA>(x1, x3, t1, t2, t3, t4, p, d.d0, d.d2);
+        if (!(fabs(x1) <= kStateLimit && fabs(x2n) <= kStateLimit && fabs(x3) <= kStateLimit)) {
             steps = j + 1;
+            if constexpr (kRing) cp_async_wait<0>();  // no copy may land after we leave
             return kOverflow;
         }
         if (!in_bounds(x1, p.ylo, p.yhi)) {
             steps = j + 1;
+            if constexpr (kRing) cp_async_wait<0>();
             return kViolated;
         }
         if (POLL && (j & 31) == 31) {
             if (*(volatile const unsigned int*)dead != 0u) {
                 steps = j + 1;
+                if constexpr (kRing) cp_async_wait<0>();
                 return kAbandoned;
             }
         }
+        t1 = u1;
+        t2 = u2;
+        t3 = u3;
+        t4 = u4;
+        x2n = x2nn;
+        d = dn;
     }
-    steps = p.j_star;
+    steps = J;
     return kOk;
 }
 

@@ -22,6 +22,10 @@
 
 #include "rg_cell.cuh"
 
+#ifndef RG_GRID_MINB
+#define RG_GRID_MINB 1
+#endif
+
 namespace rg {
 
 // ---------------------------------------------------------------------------
@@ -70,6 +74,22 @@ __global__ void k_sample(SampleArgs a) {
     }
 }
 
+// counter RNG straight into the SoA layout d[(j*3+i)*ld + k], rows j < j_star:
+// one thread per (scenario, step); lanes run over scenarios, so stores coalesce.
+__global__ void k_gen_soa(ScenarioStream st, int64_t k0, int64_t n_sim, int32_t j_star,
+                          int64_t ld, double* __restrict__ dst) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int32_t j = blockIdx.y;
+    if (k >= n_sim || j >= j_star) return;
+    const uint64_t K = scenario_key(st, (uint64_t)(k0 + k));
+    double d0, d1, d2;
+    disturbance_at(st, K, (uint64_t)j, d0, d1, d2);
+    double* o = dst + (int64_t)j * 3 * ld + k;
+    o[0] = d0;
+    o[ld] = d1;
+    o[2 * ld] = d2;
+}
+
 // tile transpose of [n_sim][horizon][3] (rows j < j_star) into d[(j*3+i)*ld + k]
 __global__ void k_to_soa(const double* __restrict__ src, double* __restrict__ dst,
                          int64_t n_sim, int64_t horizon, int32_t j_star, int64_t ld) {
@@ -101,7 +121,7 @@ __global__ void k_to_soa(const double* __restrict__ src, double* __restrict__ ds
 // ---------------------------------------------------------------------------
 
 template <bool FMA, bool RNG>
-__global__ void __launch_bounds__(128) k_fill(FillArgs a) {
+__global__ void __launch_bounds__(128, RG_GRID_MINB) k_fill(FillArgs a) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= a.n_sim) return;
     const int32_t row = a.rows[blockIdx.y];
@@ -113,7 +133,8 @@ __global__ void __launch_bounds__(128) k_fill(FillArgs a) {
         RngSource src{a.stream, scenario_key(a.stream, (uint64_t)(a.k0 + k))};
         st = rollout<FMA, false>(c, a.x0[0], a.x0[1], a.x0[2], v, src, steps, nullptr);
     } else {
-        SoaSource src{a.soa + k, a.ld};
+        __shared__ double ring[2 * 3 * kRingStride];
+        SoaSource src{a.soa + k, a.ld, ring + threadIdx.x};
         st = rollout<FMA, false>(c, a.x0[0], a.x0[1], a.x0[2], v, src, steps, nullptr);
     }
     a.S[(int64_t)row * a.n_sim + k] = (uint8_t)st;
@@ -139,7 +160,7 @@ __device__ int row_source(const GridArgs& a, int i, double* v_out) {
 }
 
 template <bool FMA, bool RNG, bool POLL>
-__global__ void __launch_bounds__(128) k_grid(GridArgs a) {
+__global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid(GridArgs a) {
     __shared__ int s_src;
     __shared__ double s_v;
     const int i = blockIdx.y;
@@ -163,7 +184,8 @@ __global__ void __launch_bounds__(128) k_grid(GridArgs a) {
                 st = rollout<FMA, POLL>(c, a.x0[0], a.x0[1], a.x0[2], s_v, src, steps,
                                         a.viol + i);
             } else {
-                SoaSource src{a.soa + k, a.ld};
+                __shared__ double ring[2 * 3 * kRingStride];
+                SoaSource src{a.soa + k, a.ld, ring + threadIdx.x};
                 st = rollout<FMA, POLL>(c, a.x0[0], a.x0[1], a.x0[2], s_v, src, steps,
                                         a.viol + i);
             }
@@ -246,7 +268,7 @@ __global__ void __launch_bounds__(128) k_grid(GridArgs a) {
 // ---------------------------------------------------------------------------
 
 template <bool FMA, int SRC>  // SRC: 0 zero (nominal), 1 rng, 2 soa
-__global__ void __launch_bounds__(128) k_bisect(BisectArgs a) {
+__global__ void __launch_bounds__(128, RG_GRID_MINB) k_bisect(BisectArgs a) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool live = k < a.n_sim;
     double kopt = 1.0;
@@ -256,7 +278,8 @@ __global__ void __launch_bounds__(128) k_bisect(BisectArgs a) {
         RngSource rsrc{};
         SoaSource ssrc{};
         if (SRC == 1) rsrc = RngSource{a.stream, scenario_key(a.stream, (uint64_t)(a.k0 + k))};
-        if (SRC == 2) ssrc = SoaSource{a.soa + k, a.ld};
+        __shared__ double ring[2 * 3 * kRingStride];
+        if (SRC == 2) ssrc = SoaSource{a.soa + k, a.ld, ring + threadIdx.x};
         double klo = 0.0, khi = 1.0;
         kopt = 0.0;
         found = 0;
@@ -355,6 +378,18 @@ __global__ void k_tanh(const double* __restrict__ x, double* __restrict__ y, int
     if (i < n) y[i] = tanh_glibc<FMA>(x[i]);
 }
 
+// the rollout's lockstep form (tanh4 / tanh_core), four arguments per thread
+template <bool FMA>
+__global__ void k_tanh4(const double* __restrict__ x, double* __restrict__ y, int64_t n) {
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (i >= n) return;
+    double a[4], z[4];
+    for (int q = 0; q < 4; ++q) a[q] = i + q < n ? x[i + q] : 0.0;
+    tanh4<FMA>(a[0], a[1], a[2], a[3], z[0], z[1], z[2], z[3]);
+    for (int q = 0; q < 4; ++q)
+        if (i + q < n) y[i + q] = z[q];
+}
+
 // FP64 issue-rate probe: independent DFMA chains (the roofline denominator)
 __global__ void k_dfma_peak(double* out, int iters, double a, double b) {
     double x0 = threadIdx.x * 1e-9, x1 = x0 + 1.0, x2 = x0 + 2.0, x3 = x0 + 3.0;
@@ -432,10 +467,24 @@ cudaError_t launch_bisect(const BisectArgs& a, bool fma, int src, cudaStream_t s
     return cudaGetLastError();
 }
 
-cudaError_t launch_tanh(const double* x, double* y, int64_t n, bool fma, cudaStream_t s) {
+cudaError_t launch_tanh(const double* x, double* y, int64_t n, bool fma, bool lockstep,
+                        cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    if (fma) k_tanh<true><<<blocks_for(n, 256), 256, 0, s>>>(x, y, n);
-    else     k_tanh<false><<<blocks_for(n, 256), 256, 0, s>>>(x, y, n);
+    if (lockstep) {
+        const unsigned g = blocks_for((n + 3) / 4, 256);
+        if (fma) k_tanh4<true><<<g, 256, 0, s>>>(x, y, n);
+        else     k_tanh4<false><<<g, 256, 0, s>>>(x, y, n);
+    } else {
+        if (fma) k_tanh<true><<<blocks_for(n, 256), 256, 0, s>>>(x, y, n);
+        else     k_tanh<false><<<blocks_for(n, 256), 256, 0, s>>>(x, y, n);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gen_soa(const ScenarioStream& st, int64_t k0, int64_t n_sim, int32_t j_star,
+                           int64_t ld, double* dst, cudaStream_t s) {
+    dim3 grid(blocks_for(n_sim, 128), (unsigned)j_star);
+    k_gen_soa<<<grid, 128, 0, s>>>(st, k0, n_sim, j_star, ld, dst);
     return cudaGetLastError();
 }
 

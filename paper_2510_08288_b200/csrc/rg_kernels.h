@@ -110,7 +110,10 @@ cudaError_t launch_to_soa(const double* src, double* dst, int64_t n_sim, int64_t
 cudaError_t launch_fill(const FillArgs& a, bool fma, bool rng, cudaStream_t s);
 cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, cudaStream_t s);
 cudaError_t launch_bisect(const BisectArgs& a, bool fma, int src, cudaStream_t s);
-cudaError_t launch_tanh(const double* x, double* y, int64_t n, bool fma, cudaStream_t s);
+cudaError_t launch_tanh(const double* x, double* y, int64_t n, bool fma, bool lockstep,
+                        cudaStream_t s);
+cudaError_t launch_gen_soa(const ScenarioStream& st, int64_t k0, int64_t n_sim, int32_t j_star,
+                           int64_t ld, double* dst, cudaStream_t s);
 cudaError_t launch_dfma_peak(double* out, int blocks, int threads, int iters, cudaStream_t s);
 
 }  // namespace rg

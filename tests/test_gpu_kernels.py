@@ -1,0 +1,131 @@
+"""Kernel-level parity on the B200: the lockstep tanh, both RNG paths (fused and
+staged), and full-size properties checked against the CPU oracle."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2510_08288_b200 as rg
+from paper_2510_08288_b200 import _capi
+from conftest import GOLDEN, bis_case, fill_case
+
+pytestmark = pytest.mark.gpu
+
+with np.load(GOLDEN) as _z:
+    N_FILL = len(_z["fill_names"])
+    N_BIS = len(_z["bis_names"])
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return _capi.context(0)
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.uint64)
+
+
+def _problem(lower, upper, anchor, eps, j_star):
+    tight = rg.tighten(rg.ConstraintSet(lower, upper, anchor), eps)
+    lo, hi = rg.admissible_setpoints(tight.lower, tight.upper)
+    return _capi.Problem(0.01, lower, upper, lo, hi, j_star, 0)
+
+
+def test_lockstep_tanh_bit_exact(ctx, orc):
+    rng = np.random.default_rng(17)
+    x = np.concatenate([
+        rng.uniform(-1.2, 1.2, 2_000_000), rng.uniform(-7, 7, 1_000_000),
+        rng.uniform(-30, 30, 100_000),
+        np.ldexp(rng.uniform(0.5, 1.0, 200_000), rng.integers(-64, 6, 200_000)),
+        -np.ldexp(rng.uniform(0.5, 1.0, 200_000), rng.integers(-64, 6, 200_000)),
+        np.array([0.0, -0.0, np.inf, -np.inf, 22.0, -22.0, 6.5, -6.5, 5e-324, 1.0, -1.0,
+                  0.17328679513998632, 0.5198603854199589]),
+    ])
+    ref = orc.libm_tanh(x)
+    y = ctx.tanh(x, lockstep=True)
+    mism = np.flatnonzero(_bits(y) != _bits(ref))
+    assert mism.size == 0, f"{mism.size} mismatches, first x={x[mism[:5]]}"
+
+
+@pytest.mark.parametrize("mode", ["fused", "staged"])
+@pytest.mark.parametrize("idx", range(N_FILL))
+def test_grid_step_both_rng_paths(ctx, golden, idx, mode):
+    c = fill_case(golden, idx)
+    m = rg.DisturbanceModel(c["ranges"])
+    scen = _capi.make_scenarios(c["seed"], 0, c["n_sim"], m.lo, m.span)
+    prob = _problem(c["lower"], c["upper"], c["anchor"], c["eps"], c["j_star"])
+    res, viol, pbits = ctx.grid_step(prob, c["x0"], c["v_prev"], c["r"], c["m_grid"],
+                                     c["prefix"], None, c["n_sim"], scen, True, rng_mode=mode)
+    P = np.unpackbits(pbits.view(np.uint8), axis=1, bitorder="little")[:, :c["n_sim"]]
+    ss = c["ss_ok"]
+    # simulated rows carry their own bits; the reference's P has the same rows
+    sim = np.array([i for i in range(c["m_grid"]) if ss[i] and
+                    rg.update_setpoint(c["v_prev"], c["r"], i / (c["m_grid"] - 1)) not in
+                    [rg.update_setpoint(c["v_prev"], c["r"], q / (c["m_grid"] - 1))
+                     for q in range(i) if ss[q]]], dtype=int)
+    assert np.array_equal(P[sim].astype(bool), c["P"][sim]), c["name"]
+    assert int(res.sims_run) == int(c["stats"][0]) and int(res.early_terms) == int(c["stats"][1])
+    kappa = 0.0 if res.row < 0 else res.row / (c["m_grid"] - 1)
+    assert kappa == c["result"][0]
+
+
+@pytest.mark.parametrize("mode", ["fused", "staged"])
+@pytest.mark.parametrize("idx", range(N_BIS))
+def test_bisect_both_rng_paths(ctx, golden, idx, mode):
+    c = bis_case(golden, idx)
+    m = rg.DisturbanceModel(c["ranges"])
+    scen = _capi.make_scenarios(c["seed"], 0, c["n_sim"], m.lo, m.span)
+    prob = _problem(c["lower"], c["upper"], c["anchor"], c["eps"], c["j_star"])
+    res, per, _ = ctx.bisect(prob, c["x0"], c["v_prev"], c["r"], c["n_kappa"], None,
+                             c["n_sim"], scen, per_scenario=True, rng_mode=mode)
+    assert np.array_equal(np.stack(per, axis=1).astype(np.float64), c["per"]), c["name"]
+    assert (res.kappa, float(res.found), res.cells, res.early) == \
+        (c["result"][0], c["result"][2], c["result"][3], c["result"][4])
+
+
+def test_million_scenarios_shard_invariance_and_spot_checks(ctx, orc):
+    """C4 shape at reduced horizon: 2^20 scenarios, fused RNG.  Per-row violation
+    counts of the whole set equal the sum over four k0-shards (the multi-GPU
+    partition), and random cells match the oracle's on-the-fly rollout."""
+    n, j_star, M = 1 << 20, 64, 16
+    ranges = [(-0.02, 0.02)] * 3
+    m = rg.DisturbanceModel(ranges)
+    x0 = np.array([np.tanh(0.2), 0.2, np.tanh(0.2) / 2]) + 0.03
+    prob = _problem(-0.9, 0.9, 0.0, 0.05, j_star)
+    full = _capi.make_scenarios(99, 0, n, m.lo, m.span)
+    res, viol, _ = ctx.grid_step(prob, x0, 0.2, 2.4, M, False, None, n, full, False,
+                                 rng_mode="fused")
+    parts = np.zeros(M, dtype=np.int64)
+    for r in range(4):
+        sh = _capi.make_scenarios(99, r * n // 4, n // 4, m.lo, m.span)
+        _, v, _ = ctx.grid_step(prob, x0, 0.2, 2.4, M, False, None, n // 4, sh, False,
+                                rng_mode="fused")
+        parts += np.where(v == 0xFFFFFFFF, 0, v)
+    assert np.array_equal(np.where(viol == 0xFFFFFFFF, 0, viol).astype(np.int64), parts)
+    assert 0 < np.count_nonzero(viol == 0) < M   # the case binds: some rows fail
+    # spot-check cells of the failing and passing rows against the oracle
+    rng = np.random.default_rng(0)
+    ks = rng.choice(n, size=48, replace=False)
+    v_rows = np.array([rg.update_setpoint(0.2, 2.4, i / (M - 1)) for i in range(M)])
+    rows = np.arange(M, dtype=np.int32)
+    for k in ks:
+        sc = _capi.make_scenarios(99, int(k), 1, m.lo, m.span)
+        S = np.zeros((M, 1), np.uint8)
+        st = np.zeros((M, 1), np.int32)
+        ctx.fill(prob, x0, v_rows, rows, None, 1, sc, S, st, rng_mode="fused")
+        for i in range(0, M, 5):
+            assert (int(S[i, 0]), int(st[i, 0])) == orc.cell_sfc_rng(
+                0.01, x0, v_rows[i], 99, int(k), ranges, j_star, -0.9, 0.9)
+
+
+def test_staged_and_fused_agree_at_scale(ctx):
+    n, j_star, M = 20_000, 256, 32
+    m = rg.DisturbanceModel.scaled(0.02, 3)
+    x0 = np.array([np.tanh(-0.4), -0.4, np.tanh(-0.4) / 2])
+    prob = _problem(-0.9, 0.9, 0.0, 0.05, j_star)
+    sc = _capi.make_scenarios(5, 0, n, m.lo, m.span)
+    a = ctx.grid_step(prob, x0, -0.4, -2.5, M, False, None, n, sc, True, rng_mode="fused")
+    b = ctx.grid_step(prob, x0, -0.4, -2.5, M, False, None, n, sc, True, rng_mode="staged")
+    assert a[0].row == b[0].row and a[0].early_terms == b[0].early_terms
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
