@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=300)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-sweep", action="store_true",
+                    help="skip the larger-N points (10k staged, 2^20 fused RNG)")
     return ap.parse_args()
 
 
@@ -307,6 +309,29 @@ def run_own(args, rank, world, local_rank):
                "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e * 1e3,
                "api": "paper_2510_08288_b200.robust_rg_parallel (keep_matrix=True)"}
 
+    # larger scenario counts (BASELINE C3 size and the C4 shard size), same step
+    sweep = []
+    if world == 1 and not args.no_sweep:
+        for n_big, reps in ((10_000, 20), (1 << 20, 3)):
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(reps + 1)]
+            with torch.cuda.stream(stream):
+                for s_i, (a, b) in enumerate(evs):
+                    flush.zero_()
+                    a.record(stream)
+                    sc = _capi.make_scenarios(BASE_SEED + 1000 + s_i, 0, n_big, model.lo,
+                                              model.span)
+                    _capi.check(lib.rg_grid_step(ctx.handle, prob, x0_ptr, 0.0, R_REF, M_GRID, 0,
+                                                 None, n_big, 0, sc, None, None, res, flags))
+                    b.record(stream)
+                torch.cuda.synchronize()
+            t = np.array([a.elapsed_time(b) for a, b in evs[1:]])
+            cells = M_GRID * n_big * j_star
+            rate = cells / (t.mean() * 1e-3)
+            sweep.append({"n_sim": n_big, "ms_per_step": float(t.mean()), "value": rate,
+                          "unit": UNIT, "roofline_frac": FLOPS_PER_CELL_STEP * rate / peak,
+                          "rng": "staged" if n_big * j_star <= (4 << 20) else "fused"})
+
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         c = cpu_baseline(n_sim, j_star, args.cpu_seconds)
@@ -327,7 +352,7 @@ def run_own(args, rank, world, local_rank):
                        "parallelism": f"scenario shards x{world}" + (", NCCL all-reduce of "
                                                                      "row counts" if world > 1
                                                                      else "")},
-            "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
+            "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "sweep": sweep,
             "gpu_launches": args.steps * launches_per_step, "clocks": clocks,
             "wall_ms_per_step": wall * 1e3 / args.steps,
             "kernel_ms_p50": float(np.median(per)), "kernel_ms_min": float(per.min()),

@@ -590,9 +590,6 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
             RG_CUDA(ctx->pbits.ensure((size_t)m_grid * a.pwords * sizeof(unsigned)));
             a.pbits = ctx->pbits.as<unsigned>();
         }
-        // rows that are pruned or duplicated are not written by the kernel
-        RG_CUDA(cudaMemsetAsync(a.pbits, 0, (size_t)m_grid * a.pwords * sizeof(unsigned),
-                                ctx->stream));
     }
     a.tpb = tpb_for(ctx, n_sim, m_grid);
     const bool timed = !(flags & RG_NO_TIMING);

@@ -201,6 +201,9 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid(GridArgs a) {
             if (lane_id() == 0 && (k - lane_id()) < a.n_sim)
                 a.pbits[(int64_t)i * a.pwords + (k >> 5)] = ok_mask;
         }
+    } else if (a.pbits && lane_id() == 0 && (k - lane_id()) < a.n_sim) {
+        // pruned or duplicate row: no simulated bits (the host expands duplicates)
+        a.pbits[(int64_t)i * a.pwords + (k >> 5)] = 0u;
     }
     // last block out extracts the row and resets the accumulators
     __shared__ bool s_last;

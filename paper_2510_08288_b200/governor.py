@@ -21,6 +21,7 @@ every call raises BackendUnavailableError.
 
 from __future__ import annotations
 
+import functools
 import time
 from dataclasses import dataclass, field
 
@@ -230,23 +231,54 @@ def _source(scenarios, j_star: int):
     return np.ascontiguousarray(data, dtype=np.float64), data.shape[0], None
 
 
-def _host_rows(v_prev: float, r: float, grid: np.ndarray, plant, tight):
-    """v per row, the numpy-tanh gate and the dedup map (governor.py:286, 302-317)."""
-    v_rows = np.array([update_setpoint(v_prev, r, float(k)) for k in grid])
-    ss_ok = np.array([tight.contains(plant.steady_state_output(v)) for v in v_rows], dtype=bool)
-    first: dict = {}
+def _host_rows(v_prev: float, r: float, grid: np.ndarray, interval):
+    """v per row, the steady-state gate and the dedup map (governor.py:286, 302-317).
+
+    Vectorised: numpy evaluates v_prev + kappa*(r - v_prev) with the same three
+    roundings as update_setpoint (the endpoints are set exactly as it does),
+    the gate is the verified setpoint interval of ssgate.py (identical to
+    tight.contains(np.tanh(v)) for every double), and rows with equal v map
+    to the first such row like the reference's dict.  For an ascending grid v
+    is monotone, so equal values are adjacent; the general dict walk is kept
+    for the (rounding-induced) non-monotone corner.
+    """
+    v_rows = v_prev + grid * (r - v_prev)
+    v_rows[grid == 0.0] = v_prev
+    v_rows[grid == 1.0] = r
+    ss_ok = (v_rows >= interval[0]) & (v_rows <= interval[1])
+    m = grid.size
+    dv = np.diff(v_rows)
+    if (dv >= 0).all() or (dv <= 0).all():
+        same = np.zeros(m, dtype=bool)
+        same[1:] = (dv == 0) & ss_ok[1:] & ss_ok[:-1]
+        pos = np.arange(m)
+        first = np.maximum.accumulate(np.where(same, 0, pos))
+        dup_src = np.where(same, first, -1)
+        reps = np.flatnonzero(ss_ok & ~same)
+        return v_rows, ss_ok, dup_src, reps.astype(np.int32)
+    first_of: dict = {}
+    dup_src = np.full(m, -1, dtype=np.int64)
     reps = []
-    dup_src = np.full(grid.size, -1, dtype=np.int64)
-    for i in range(grid.size):
-        if not ss_ok[i]:
-            continue
+    for i in np.flatnonzero(ss_ok):
         v = float(v_rows[i])
-        if v in first:
-            dup_src[i] = first[v]
+        if v in first_of:
+            dup_src[i] = first_of[v]
         else:
-            first[v] = i
+            first_of[v] = i
             reps.append(i)
     return v_rows, ss_ok, dup_src, np.array(reps, dtype=np.int32)
+
+
+@functools.lru_cache(maxsize=256)
+def _prepared(step_size, lower, upper, anchor, eps, mode, j_star, m_grid):
+    """Per-configuration constants: the Problem block, the gate interval, the grid."""
+    cset = ConstraintSet(lower, upper, anchor)
+    tight = _tightened(cset, eps, mode)
+    interval = admissible_setpoints(float(tight.lower), float(tight.upper))
+    prob = _capi.Problem(float(step_size), float(lower), float(upper), interval[0],
+                         interval[1], int(j_star), 0)
+    grid = grid_kappas(m_grid) if m_grid else None
+    return prob, interval, grid
 
 
 def _backend_check(backend: str) -> None:
@@ -283,12 +315,13 @@ def fill_feasibility(backend, plant, x0, v_prev, r_t, grid, scenarios, cset, eps
     tight = _tightened(cset, eps, tighten_mode)
 
     t0 = time.perf_counter()
-    v_rows, ss_ok, dup_src, rows = _host_rows(v_prev, r_t, grid, plant, tight)
+    prob, interval, _ = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor, eps,
+                                  tighten_mode, j_star, 0)
+    v_rows, ss_ok, dup_src, rows = _host_rows(float(v_prev), float(r_t), grid, interval)
     m = grid.size
     S = np.zeros((m, n_sim), dtype=np.uint8)
     steps = np.zeros((m, n_sim), dtype=np.int32)
     ctx = _capi.context(device)
-    prob = _problem(plant, cset, tight, j_star)
     ctx.fill(prob, x0, v_rows, rows, dist, n_sim, stream, S, steps)
     for i in np.flatnonzero(dup_src >= 0):
         S[i] = S[dup_src[i]]
@@ -318,18 +351,18 @@ def robust_rg_parallel(plant, x_t, state, r_t, cset, scenarios, config, backend=
     backend = backend or config.backend
     _backend_check(backend)
     _require_device_plant(plant)
-    grid = grid_kappas(config.m_grid)
     if config.tighten_mode == "scale":
         validate_epsilon(config.epsilon)
-    tight = _tightened(cset, config.epsilon, config.tighten_mode)
+    prob, interval, grid = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor,
+                                     config.epsilon, config.tighten_mode, config.j_star,
+                                     config.m_grid)
     dist, n_sim, stream = _source(scenarios, config.j_star)
     device = getattr(config, "device", 0)
     keep = getattr(config, "keep_matrix", True)
 
     t0 = time.perf_counter()
-    v_rows, ss_ok, dup_src, rows = _host_rows(state.v_prev, r_t, grid, plant, tight)
+    v_rows, ss_ok, dup_src, rows = _host_rows(float(state.v_prev), float(r_t), grid, interval)
     ctx = _capi.context(device)
-    prob = _problem(plant, cset, tight, config.j_star)
     res, viol, pbits = ctx.grid_step(prob, x_t, state.v_prev, r_t, config.m_grid,
                                      config.prefix_mode, dist, n_sim, stream, want_pbits=keep,
                                      abandon=not keep)
@@ -369,9 +402,9 @@ def robust_rg_parallel(plant, x_t, state, r_t, cset, scenarios, config, backend=
 # ---------------------------------------------------------------------------
 
 def _bisect_call(plant, x_t, state, r_t, cset, config, dist, n_sim, stream):
-    tight = _tightened(cset, config.epsilon, config.tighten_mode)
+    prob, _, _ = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor, config.epsilon,
+                           config.tighten_mode, config.j_star, 0)
     ctx = _capi.context(getattr(config, "device", 0))
-    prob = _problem(plant, cset, tight, config.j_star)
     res, _, _ = ctx.bisect(prob, x_t, state.v_prev, r_t, config.n_kappa, dist, n_sim, stream)
     return res
 

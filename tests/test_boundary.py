@@ -120,3 +120,31 @@ def test_first_context_in_fresh_process_does_not_hang():
     r = subprocess.run([sys.executable, "-c", code], timeout=120,
                        cwd=str(Path(__file__).resolve().parents[1]))
     assert r.returncode == 0
+
+
+def test_host_rows_match_reference_gate_and_dedup():
+    """governor._host_rows (vectorised v_rows, interval gate, dedup) equals the
+    reference's per-row loop with numpy tanh and a dict (governor.py:286-317)."""
+    from paper_2510_08288_b200.governor import _host_rows, _prepared
+
+    plant = rg.make_plant("surrogate-fc")
+    tight = rg.tighten(rg.ConstraintSet(-0.9, 0.9), 0.05)
+    _, iv, g = _prepared(0.01, -0.9, 0.9, 0.0, 0.05, "scale", 256, 32)
+    rng = np.random.default_rng(1)
+    for trial in range(1500):
+        vp = float(rng.choice([rng.uniform(-2, 2), 0.3, -0.0, 1.2744531163104806]))
+        r = float(rng.choice([rng.uniform(-3, 3), vp, 2.5, np.nextafter(vp, 9)]))
+        grid = g if trial % 2 else np.sort(rng.uniform(0, 1, 17))
+        v, ok, dup, reps = _host_rows(vp, r, grid, iv)
+        v_ref = [rg.update_setpoint(vp, r, float(k)) for k in grid]
+        ok_ref = [tight.contains(plant.steady_state_output(x)) for x in v_ref]
+        first, dup_ref, reps_ref = {}, [-1] * len(grid), []
+        for i in range(len(grid)):
+            if ok_ref[i]:
+                if v_ref[i] in first:
+                    dup_ref[i] = first[v_ref[i]]
+                else:
+                    first[v_ref[i]] = i
+                    reps_ref.append(i)
+        assert np.array_equal(np.array(v_ref).view(np.uint64), v.view(np.uint64))
+        assert list(ok) == ok_ref and list(dup) == dup_ref and list(reps) == reps_ref
