@@ -186,10 +186,18 @@ def run_own(args, rank, world, local_rank):
     import paper_2510_08288_b200 as rg
     from paper_2510_08288_b200 import _capi
 
+    # RG_BENCH_DIST_BACKEND=gloo + RG_BENCH_DEVICE=0 smoke-test the N>1 code path on one GPU
+    # (the collectives then run on the host; timings of such a run mean nothing)
+    backend = os.environ.get("RG_BENCH_DIST_BACKEND", "nccl")
+    if "RG_BENCH_DEVICE" in os.environ:
+        local_rank = int(os.environ["RG_BENCH_DEVICE"])
     torch.cuda.set_device(local_rank)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     ctx = _capi.context(local_rank)
     stream = torch.cuda.ExternalStream(ctx.stream_ptr, device=torch.device("cuda", local_rank))
 
@@ -209,9 +217,7 @@ def run_own(args, rank, world, local_rank):
     flags = _capi.RG_ASYNC | _capi.RG_NO_TIMING
     if world > 1:
         flags |= _capi.RG_DEVICE_PTRS
-    x0_arg = x0.ctypes.data_as(ctypes_vp()) if world == 1 else \
-        torch.zeros(3, dtype=torch.float64, device=f"cuda:{local_rank}")
-    x0_ptr = x0_arg if world == 1 else ctypes_vp()(x0_arg.data_ptr())
+    x0_ptr = x0.ctypes.data_as(ctypes_vp())  # kernel parameter: host memory
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32,
                         device=f"cuda:{local_rank}")
     big = torch.tensor(1 << 40, dtype=torch.int64, device=f"cuda:{local_rank}")
@@ -331,6 +337,31 @@ def run_own(args, rank, world, local_rank):
             sweep.append({"n_sim": n_big, "ms_per_step": float(t.mean()), "value": rate,
                           "unit": UNIT, "roofline_frac": FLOPS_PER_CELL_STEP * rate / peak,
                           "rng": "staged" if n_big * j_star <= (4 << 20) else "fused"})
+
+    if world > 1:
+        from paper_2510_08288_b200.sharded import robust_rg_parallel_sharded
+        cfg = rg.GovernorConfig(j_star=j_star, m_grid=M_GRID, n_sim=n_sim * world,
+                                device=local_rank)
+        for s in range(3):
+            robust_rg_parallel_sharded(plant, x0, rg.GovernorState(0.0), R_REF, box,
+                                       rg.sample_scenarios(model, n_sim * world, j_star + 1,
+                                                           seed=s, device=local_rank), cfg)
+        torch.distributed.barrier()
+        t0 = time.perf_counter()
+        for s in range(args.e2e_steps):
+            scen = rg.sample_scenarios(model, n_sim * world, j_star + 1, seed=BASE_SEED + s,
+                                       device=local_rank)
+            r = robust_rg_parallel_sharded(plant, x0, rg.GovernorState(0.0), R_REF, box, scen,
+                                           cfg)
+        t = torch.tensor([(time.perf_counter() - t0) / args.e2e_steps], dtype=torch.float64,
+                         device=f"cuda:{local_rank}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_e2e = float(t.item())
+        assert r.kappa_opt == 1.0
+        e2e = {"value": cells_rank * world / t_e2e, "unit": UNIT,
+               "h2d_bytes_per_step": 112, "d2h_bytes_per_step": M_GRID * 4 + 64,
+               "ms_per_step": t_e2e * 1e3,
+               "api": "paper_2510_08288_b200.sharded.robust_rg_parallel_sharded"}
 
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -55,7 +55,7 @@ extern "C" {
 #define RG_TANH_GENERIC 2 /* generic SSE2 __expm1 */
 
 /* flags */
-#define RG_DEVICE_PTRS 0x1  /* array arguments are device pointers */
+#define RG_DEVICE_PTRS 0x1  /* array arguments are device pointers (x0[3] is always host) */
 #define RG_ASYNC 0x2        /* enqueue only; no host readback, no sync */
 #define RG_ABANDON 0x4      /* grid step: stop rows already known infeasible */
 #define RG_NO_TIMING 0x8    /* skip the CUDA-event kernel timing */

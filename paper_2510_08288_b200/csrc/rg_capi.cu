@@ -444,10 +444,8 @@ int32_t rg_fill(rg_ctx* ctx, const rg_problem* prob, const double* x0, const dou
         for (int32_t q = 0; q < n_rows; ++q)
             if (rows[q] < 0 || rows[q] >= m_rows)
                 return fail(RG_E_ARGS, "row index %d out of range", rows[q]);
-        for (int i = 0; i < 3; ++i) a.x0[i] = x0[i];
-    } else {
-        RG_CUDA(cudaMemcpy(a.x0, x0, 3 * sizeof(double), cudaMemcpyDeviceToHost));
     }
+    for (int i = 0; i < 3; ++i) a.x0[i] = x0[i];  // x0 is a kernel parameter: host memory
     if (n_rows == 0) return RG_OK;
     RG_CUDA(ctx->vrows.ensure(m_rows * sizeof(double)));
     RG_CUDA(ctx->rows.ensure(n_rows * sizeof(int32_t)));
@@ -551,10 +549,7 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
         return fail(RG_E_ARGS, "scenario horizon %lld too short: need >= j_star+1 = %d",
                     (long long)horizon, prob->j_star + 1);
     if (!isfinite(v_prev) || !isfinite(r)) return fail(RG_E_ARGS, "v_prev and r must be finite");
-    if (flags & RG_DEVICE_PTRS)
-        RG_CUDA(cudaMemcpy(a.x0, x0, 3 * sizeof(double), cudaMemcpyDeviceToHost));
-    else
-        for (int i = 0; i < 3; ++i) a.x0[i] = x0[i];
+    for (int i = 0; i < 3; ++i) a.x0[i] = x0[i];  // x0 is a kernel parameter: host memory
     if (!(isfinite(a.x0[0]) && isfinite(a.x0[1]) && isfinite(a.x0[2])))
         return fail(RG_E_ARGS, "state entries must be finite");
     if ((rc = grow_grid(ctx, m_grid))) return rc;
@@ -635,10 +630,7 @@ int32_t rg_bisect(rg_ctx* ctx, const rg_problem* prob, const double* x0, double 
         return fail(RG_E_ARGS, "per-scenario outputs come as a set of four");
     if ((path_kappa != nullptr) != (path_ok != nullptr))
         return fail(RG_E_ARGS, "path outputs come as a pair");
-    if (flags & RG_DEVICE_PTRS)
-        RG_CUDA(cudaMemcpy(a.x0, x0, 3 * sizeof(double), cudaMemcpyDeviceToHost));
-    else
-        for (int i = 0; i < 3; ++i) a.x0[i] = x0[i];
+    for (int i = 0; i < 3; ++i) a.x0[i] = x0[i];  // x0 is a kernel parameter: host memory
     a.v_prev = v_prev;
     a.r = r;
     a.n_kappa = n_kappa;

@@ -1,0 +1,161 @@
+"""Scenario-sharded governor steps across GPUs.
+
+One process per GPU (torchrun).  A generated ScenarioSet is split into
+contiguous counter ranges, rank r simulating scenarios [k0 + r*n/W,
+k0 + (r+1)*n/W) -- the counter RNG makes that free of scenario traffic
+(disturbance.py:85-92).  The only exchange is per step:
+
+* grid step (Alg. 3): one all-reduce (SUM) of the per-row violating-scenario
+  counts, int64[M]; a row is all-feasible iff its global count is 0, and every
+  rank extracts the same row (extract_kappa_opt, governor.py:351-377);
+* exact Alg. 2: one all-reduce each of MIN kappa, MIN found (= AND) and SUM of
+  the cell / early counters (governor.py:496-506).
+
+The collectives run through torch.distributed (NCCL on GPUs, gloo on CPU for
+the host-logic tests); the local step is the device kernel.
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+
+from . import _capi
+from .errors import InfeasibleError
+from .governor import (KappaResult, _prepared, _source, _validate_state, _require_device_plant,
+                       _host_rows, update_setpoint)
+
+__all__ = ["PRUNED", "global_row_counts", "extract_row", "robust_rg_parallel_sharded",
+           "robust_rg_sequential_sharded", "combine_bisection"]
+
+PRUNED = np.uint32(0xFFFFFFFF)  # rg_grid_step's marker for a gated-out row
+_BIG = 1 << 40                  # > any scenario count; marks pruned rows in the sum
+
+
+def _dist():
+    import torch.distributed as dist
+
+    return dist
+
+
+def global_row_counts(local_viol: np.ndarray, group=None, device=None) -> np.ndarray:
+    """Sum per-row violation counts over ranks; pruned rows stay >= _BIG."""
+    import torch
+
+    c = np.where(local_viol == PRUNED, _BIG, local_viol.astype(np.int64))
+    t = torch.as_tensor(c, dtype=torch.int64)
+    if device is not None:
+        t = t.to(device)
+    _dist().all_reduce(t, op=_dist().ReduceOp.SUM, group=group)
+    return t.cpu().numpy()
+
+
+def extract_row(counts: np.ndarray, dup_src: np.ndarray, prefix_mode: bool) -> int | None:
+    """0-based best all-feasible row from global counts (governor.py:351-377).
+
+    Duplicate rows share their representative's verdict (governor.py:329-333).
+    """
+    src = np.where(dup_src >= 0, dup_src, np.arange(counts.size))
+    full = counts[src] == 0
+    if prefix_mode:
+        bad = np.flatnonzero(~full)
+        idx = (int(bad[0]) if bad.size else full.size) - 1
+    else:
+        ok = np.flatnonzero(full)
+        idx = int(ok[-1]) if ok.size else -1
+    return None if idx < 0 else idx
+
+
+def robust_rg_parallel_sharded(plant, x_t, state, r_t, cset, scenarios, config, group=None,
+                               local_step=None):
+    """robust_rg_parallel over the ranks of `group`; every rank returns the same result.
+
+    ``local_step(shard) -> uint32[M]`` computes this rank's per-row counts; the
+    default is the device kernel (rg_grid_step).  matrix is None (P is sharded).
+    """
+    dist = _dist()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    x_t = _validate_state(plant, x_t)
+    _require_device_plant(plant)
+    prob, interval, grid = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor,
+                                     config.epsilon, config.tighten_mode, config.j_star,
+                                     config.m_grid)
+    shard = scenarios.shard(rank, world)
+    t0 = time.perf_counter()
+    v_rows, ss_ok, dup_src, rows = _host_rows(float(state.v_prev), float(r_t), grid, interval)
+    if local_step is None:
+        ctx = _capi.context(getattr(config, "device", 0))
+        dist_t, n_sim, stream = _source(shard, config.j_star)
+        res, viol, _ = ctx.grid_step(prob, x_t, state.v_prev, r_t, config.m_grid,
+                                     config.prefix_mode, dist_t, n_sim, stream, False,
+                                     abandon=True)
+        dev = f"cuda:{ctx.device}" if dist.get_backend(group) == "nccl" else None
+    else:
+        viol, dev = np.asarray(local_step(shard), dtype=np.uint32), None
+    counts = global_row_counts(viol, group, dev)
+    row = extract_row(counts, dup_src, config.prefix_mode)
+    diag = {"method": "parallel-grid-sharded", "ranks": world, "backend": "cuda",
+            "sims_run": int(rows.size) * scenarios.n_sim,
+            "ss_pruned_rows": int(np.count_nonzero(~ss_ok)),
+            "dedup_rows": int(np.count_nonzero(dup_src >= 0)),
+            "wall_us": int((time.perf_counter() - t0) * 1e6)}
+    if row is None:
+        if config.infeasible_policy == "error":
+            raise InfeasibleError("no candidate feasible, including kappa=0 (hold current "
+                                  "setpoint)")
+        return KappaResult(0.0, state.v_prev, False, diag, None)
+    kappa = float(grid[row])
+    v = update_setpoint(state.v_prev, r_t, kappa)
+    state.v_prev = v
+    return KappaResult(kappa, v, True, diag, None)
+
+
+def combine_bisection(kappa: float, found: int, cells: int, early: int, group=None,
+                      device=None):
+    """MIN kappa, AND found, SUM cells/early over ranks (governor.py:496-506)."""
+    import torch
+
+    dist = _dist()
+    k = torch.tensor([kappa], dtype=torch.float64)
+    f = torch.tensor([int(found)], dtype=torch.int64)
+    ce = torch.tensor([int(cells), int(early)], dtype=torch.int64)
+    if device is not None:
+        k, f, ce = k.to(device), f.to(device), ce.to(device)
+    dist.all_reduce(k, op=dist.ReduceOp.MIN, group=group)
+    dist.all_reduce(f, op=dist.ReduceOp.MIN, group=group)
+    dist.all_reduce(ce, op=dist.ReduceOp.SUM, group=group)
+    ce = ce.cpu().numpy()
+    return float(k.item()), bool(f.item()), int(ce[0]), int(ce[1])
+
+
+def robust_rg_sequential_sharded(plant, x_t, state, r_t, cset, scenarios, config, group=None,
+                                 local_step=None):
+    """robust_rg_sequential (exact Alg. 2) over the ranks of `group`.
+
+    ``local_step(shard) -> (kappa, found, cells, early)`` defaults to rg_bisect.
+    """
+    dist = _dist()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    x_t = _validate_state(plant, x_t)
+    _require_device_plant(plant)
+    shard = scenarios.shard(rank, world)
+    t0 = time.perf_counter()
+    dev = None
+    if local_step is None:
+        prob, _, _ = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor,
+                               config.epsilon, config.tighten_mode, config.j_star, 0)
+        ctx = _capi.context(getattr(config, "device", 0))
+        dist_t, n_sim, stream = _source(shard, config.j_star)
+        res, _, _ = ctx.bisect(prob, x_t, state.v_prev, r_t, config.n_kappa, dist_t, n_sim,
+                               stream)
+        local = (res.kappa, res.found, res.cells, res.early)
+        dev = f"cuda:{ctx.device}" if dist.get_backend(group) == "nccl" else None
+    else:
+        local = local_step(shard)
+    kappa, found, cells, early = combine_bisection(*local, group=group, device=dev)
+    v = update_setpoint(state.v_prev, r_t, kappa)
+    state.v_prev = v
+    return KappaResult(kappa, v, found, {"method": "sequential-sharded", "ranks": world,
+                                         "sims_run": cells, "early_terms": early,
+                                         "wall_us": int((time.perf_counter() - t0) * 1e6)})
