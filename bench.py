@@ -363,6 +363,34 @@ def run_own(args, rank, world, local_rank):
                "ms_per_step": t_e2e * 1e3,
                "api": "paper_2510_08288_b200.sharded.robust_rg_parallel_sharded"}
 
+    # C5 shape: a batch of independent episodes in one launch (64 x 10k scenarios,
+    # bench snapshot so every row runs the full horizon), and C3: the desk-scale
+    # closed loop at 10k scenarios (first 400 steps of the 2000-step trace)
+    if world == 1 and not args.no_sweep:
+        E, n_b = 64, 10_000
+        cfg_b = rg.GovernorConfig(j_star=j_star, m_grid=M_GRID, n_sim=n_b)
+        seeds = [BASE_SEED + 5000 + e for e in range(E)]
+        rg.robust_rg_parallel_batch(plant, np.zeros((E, 3)), np.zeros(E), np.full(E, R_REF),
+                                    box, model, n_b, seeds, cfg_b)
+        t0 = time.perf_counter()
+        kap_b, _, _, _ = rg.robust_rg_parallel_batch(plant, np.zeros((E, 3)), np.zeros(E),
+                                                     np.full(E, R_REF), box, model, n_b, seeds,
+                                                     cfg_b)
+        t_b = time.perf_counter() - t0
+        assert np.all(kap_b == 1.0)
+        sweep.append({"workload": f"C5 shape: batch of {E} episodes x {n_b} scenarios, one launch",
+                      "ms_per_step": t_b * 1e3, "value": E * M_GRID * n_b * j_star / t_b,
+                      "unit": UNIT, "timing": "wall clock around the synchronous API call"})
+        from paper_2510_08288_b200.harness import ReferenceProfile, run_closed_loop
+        prof = ReferenceProfile(((0, 0.4), (400, 2.5), (1000, -2.5), (1600, 0.2)))
+        t0 = time.perf_counter()
+        rec = run_closed_loop(plant, box, model, rg.GovernorConfig(n_sim=10_000), prof, 400, 2024)
+        t_c3 = time.perf_counter() - t0
+        sweep.append({"workload": "C3: desk-scale closed loop, n_sim=10000, first 400 of 2000 steps",
+                      "ms_per_step": t_c3 * 1e3 / 400, "violations": rec.violations(box),
+                      "timing": "wall clock, host true-plant step included (reference: "
+                                "~650 ms/step on 8 CPU cores, SURVEY.md §6)"})
+
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         c = cpu_baseline(n_sim, j_star, args.cpu_seconds)

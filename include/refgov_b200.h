@@ -176,6 +176,22 @@ RG_API int32_t rg_bisect(rg_ctx *ctx, const rg_problem *prob, const double *x0, 
                   int32_t *early_k, double *path_kappa, uint8_t *path_ok,
                   rg_bisect_result *out, int32_t flags);
 
+/* Batched robust grid step: n_episodes independent governor instances
+ * (BASELINE configs C3/C5) in one launch, each with its own state x0[e][3],
+ * v_prev[e], request r[e] and scenario stream seeds[e] (scenarios k0..k0+n_sim-1
+ * of that stream, uniform lo/span shared).  Per episode: the best row (-1
+ * none), kappa = row/(m_grid-1) (0 when none), v = update_setpoint(v_prev, r,
+ * kappa) (v_prev when none), early terminations, and optionally the per-row
+ * violation counts row_viol[e][m].  All arrays are host memory; the call is
+ * synchronous.  RG_ABANDON lets rows already known infeasible stop early. */
+RG_API int32_t rg_grid_step_batch(rg_ctx *ctx, const rg_problem *prob, int32_t n_episodes,
+                                  const double *x0, const double *v_prev, const double *r,
+                                  const uint64_t *seeds, int64_t k0, int64_t n_sim,
+                                  const double *lo, const double *span, int32_t m_grid,
+                                  int32_t prefix_mode, int32_t *row_out, double *kappa_out,
+                                  double *v_out, int64_t *early_out, uint32_t *row_viol,
+                                  int32_t flags);
+
 /* FP64 roofline probe: independent DFMA chains; returns achieved FLOP/s. */
 RG_API int32_t rg_fp64_peak(rg_ctx *ctx, double *flops_per_s);
 

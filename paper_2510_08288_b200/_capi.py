@@ -79,6 +79,8 @@ SIGNATURES = {
     "rg_bisect": (_i32, [_vp, ctypes.POINTER(Problem), _vp, _d, _d, _i32, _vp, _i64, _i64,
                          ctypes.POINTER(Scenarios), _vp, _vp, _vp, _vp, _vp, _vp,
                          ctypes.POINTER(BisectResult), _i32]),
+    "rg_grid_step_batch": (_i32, [_vp, ctypes.POINTER(Problem), _i32, _vp, _vp, _vp, _vp, _i64,
+                                  _i64, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i32]),
     "rg_fp64_peak": (_i32, [_vp, ctypes.POINTER(_d)]),
 }
 
@@ -239,6 +241,28 @@ class Context:
                                  _RNG_FLAGS[rng_mode]))
         per = (kap, fnd, cel, erl) if per_scenario else None
         return res, per, ((pk, po) if paths else None)
+
+    def grid_step_batch(self, prob: Problem, x0, v_prev, r, seeds, k0, n_sim, lo, span,
+                        m_grid, prefix_mode=False, abandon=True, want_viol=False):
+        """Batched robust grid step; returns (row, kappa, v, early[, viol])."""
+        x0 = np.ascontiguousarray(x0, dtype=np.float64).reshape(-1, 3)
+        E = x0.shape[0]
+        v_prev = np.ascontiguousarray(v_prev, dtype=np.float64).reshape(E)
+        r = np.ascontiguousarray(r, dtype=np.float64).reshape(E)
+        seeds = np.asarray([int(s_) & (2**64 - 1) for s_ in seeds], dtype=np.uint64)
+        lo = np.ascontiguousarray(lo, dtype=np.float64)
+        span = np.ascontiguousarray(span, dtype=np.float64)
+        row = np.empty(E, np.int32)
+        kap = np.empty(E, np.float64)
+        v = np.empty(E, np.float64)
+        early = np.empty(E, np.int64)
+        viol = np.empty((E, m_grid), np.uint32) if want_viol else None
+        check(self.lib.rg_grid_step_batch(self.handle, ctypes.byref(prob), E, _p(x0), _p(v_prev),
+                                          _p(r), _p(seeds), int(k0), int(n_sim), _p(lo),
+                                          _p(span), int(m_grid), int(bool(prefix_mode)),
+                                          _p(row), _p(kap), _p(v), _p(early), _p(viol),
+                                          RG_ABANDON if abandon else 0))
+        return (row, kap, v, early, viol) if want_viol else (row, kap, v, early)
 
     def fp64_peak(self) -> float:
         f = _d()

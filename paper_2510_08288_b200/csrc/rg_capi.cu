@@ -129,6 +129,9 @@ struct rg_ctx {
     DevBuf g_viol, g_early, g_ovf, g_aband, g_src, g_ticket, g_violout, g_out;
     // bisection accumulators and outputs
     DevBuf b_acc, b_out;
+    // batched grid step: inputs, accumulators (zeroed on growth, reset by the kernel), outputs
+    int batch_cap = 0;
+    DevBuf e_in, e_viol, e_early, e_src, e_ticket, e_out, e_violout;
     // scratch
     DevBuf dist_raw, soa, S, steps, pbits, rows, vrows, tmp_a, tmp_b, kap_k, fnd_k, cel_k,
         erl_k, path_k, path_o;
@@ -336,7 +339,9 @@ int32_t rg_destroy(rg_ctx* ctx) {
                       &ctx->g_ticket, &ctx->g_violout, &ctx->g_out, &ctx->b_acc, &ctx->b_out,
                       &ctx->dist_raw, &ctx->soa, &ctx->S, &ctx->steps, &ctx->pbits, &ctx->rows,
                       &ctx->vrows, &ctx->tmp_a, &ctx->tmp_b, &ctx->kap_k, &ctx->fnd_k,
-                      &ctx->cel_k, &ctx->erl_k, &ctx->path_k, &ctx->path_o};
+                      &ctx->cel_k, &ctx->erl_k, &ctx->path_k, &ctx->path_o, &ctx->e_in,
+                      &ctx->e_viol, &ctx->e_early, &ctx->e_src, &ctx->e_ticket, &ctx->e_out,
+                      &ctx->e_violout};
     for (DevBuf* b : bufs) b->release();
     ctx->h_stage.release();
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -724,6 +729,99 @@ int32_t rg_bisect(rg_ctx* ctx, const rg_problem* prob, const double* x0, double 
             cudaGetLastError();
         }
     }
+    return RG_OK;
+}
+
+int32_t rg_grid_step_batch(rg_ctx* ctx, const rg_problem* prob, int32_t n_episodes,
+                           const double* x0, const double* v_prev, const double* r,
+                           const uint64_t* seeds, int64_t k0, int64_t n_sim, const double* lo,
+                           const double* span, int32_t m_grid, int32_t prefix_mode,
+                           int32_t* row_out, double* kappa_out, double* v_out,
+                           int64_t* early_out, uint32_t* row_viol, int32_t flags) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    rg::BatchArgs a{};
+    if ((rc = make_problem(prob, &a.p))) return rc;
+    if (n_episodes < 1 || n_episodes > 65535)
+        return fail(RG_E_ARGS, "n_episodes must be in [1, 65535], got %d", n_episodes);
+    if (m_grid < 2 || m_grid > 65535) return fail(RG_E_ARGS, "m_grid must be in [2, 65535]");
+    if (n_sim < 1 || k0 < 0) return fail(RG_E_ARGS, "bad scenario range");
+    if (!x0 || !v_prev || !r || !seeds || !lo || !span || !row_out || !kappa_out || !v_out)
+        return fail(RG_E_ARGS, "null buffer");
+    const int64_t E = n_episodes, M = m_grid;
+    for (int64_t e = 0; e < E; ++e) {
+        if (!(isfinite(x0[3 * e]) && isfinite(x0[3 * e + 1]) && isfinite(x0[3 * e + 2]) &&
+              isfinite(v_prev[e]) && isfinite(r[e])))
+            return fail(RG_E_ARGS, "episode %lld: state, v_prev and r must be finite",
+                        (long long)e);
+    }
+    if (E > ctx->batch_cap || M * E > (int64_t)(ctx->e_viol.bytes / sizeof(unsigned))) {
+        const int64_t cap = std::max<int64_t>(E, 64);
+        const int64_t capm = std::max<int64_t>(E * M, 64 * 32);
+        RG_CUDA(ctx->e_in.ensure(cap * 6 * sizeof(double)));
+        RG_CUDA(ctx->e_viol.ensure(capm * sizeof(unsigned)));
+        RG_CUDA(ctx->e_src.ensure(capm * sizeof(int)));
+        RG_CUDA(ctx->e_violout.ensure(capm * sizeof(unsigned)));
+        RG_CUDA(ctx->e_early.ensure(cap * sizeof(unsigned long long)));
+        RG_CUDA(ctx->e_ticket.ensure(cap * sizeof(unsigned)));
+        RG_CUDA(ctx->e_out.ensure(cap * (sizeof(int) + 3 * sizeof(double))));
+        RG_CUDA(cudaMemsetAsync(ctx->e_viol.p, 0, ctx->e_viol.bytes, ctx->stream));
+        RG_CUDA(cudaMemsetAsync(ctx->e_early.p, 0, ctx->e_early.bytes, ctx->stream));
+        RG_CUDA(cudaMemsetAsync(ctx->e_ticket.p, 0, ctx->e_ticket.bytes, ctx->stream));
+        ctx->batch_cap = (int)cap;
+    }
+    // stage inputs: [x0 (3E) | v_prev (E) | r (E) | hs (E)] through pinned memory
+    const size_t in_bytes = (size_t)E * 6 * sizeof(double);
+    RG_CUDA(ctx->h_stage.ensure(in_bytes + (size_t)E * (sizeof(int) + 3 * sizeof(double)) +
+                                (size_t)E * M * sizeof(unsigned)));
+    double* hin = ctx->h_stage.as<double>();
+    memcpy(hin, x0, (size_t)E * 3 * sizeof(double));
+    memcpy(hin + 3 * E, v_prev, (size_t)E * sizeof(double));
+    memcpy(hin + 4 * E, r, (size_t)E * sizeof(double));
+    uint64_t* hhs = reinterpret_cast<uint64_t*>(hin + 5 * E);
+    for (int64_t e = 0; e < E; ++e) hhs[e] = rg::splitmix64(seeds[e]);
+    RG_CUDA(cudaMemcpyAsync(ctx->e_in.p, hin, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    double* din = ctx->e_in.as<double>();
+    a.x0 = din;
+    a.v_prev = din + 3 * E;
+    a.r = din + 4 * E;
+    a.hs = reinterpret_cast<const uint64_t*>(din + 5 * E);
+    a.n_ep = n_episodes;
+    a.m_grid = m_grid;
+    a.prefix_mode = prefix_mode ? 1 : 0;
+    a.n_sim = n_sim;
+    a.k0 = k0;
+    for (int c = 0; c < 3; ++c) {
+        a.lo[c] = lo[c];
+        a.span[c] = span[c];
+    }
+    a.viol = ctx->e_viol.as<unsigned>();
+    a.early = ctx->e_early.as<unsigned long long>();
+    a.row_src = ctx->e_src.as<int>();
+    a.ticket = ctx->e_ticket.as<unsigned>();
+    char* dout = ctx->e_out.as<char>();
+    a.kappa_out = reinterpret_cast<double*>(dout);
+    a.v_out = a.kappa_out + E;
+    a.early_out = reinterpret_cast<long long*>(a.v_out + E);
+    a.row_out = reinterpret_cast<int*>(a.early_out + E);
+    a.viol_out = row_viol ? ctx->e_violout.as<unsigned>() : nullptr;
+    a.tpb = tpb_for(ctx, n_sim * E, m_grid);
+    RG_CUDA(rg::launch_grid_batch(a, ctx->variant == rg::kTanhFma, (flags & RG_ABANDON) != 0,
+                                  ctx->stream));
+    char* hout = reinterpret_cast<char*>(hin + 6 * E);
+    const size_t out_bytes = (size_t)E * (3 * sizeof(double) + sizeof(int));
+    RG_CUDA(cudaMemcpyAsync(hout, dout, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    unsigned* hviol = reinterpret_cast<unsigned*>(hout + out_bytes);
+    if (row_viol)
+        RG_CUDA(cudaMemcpyAsync(hviol, a.viol_out, (size_t)E * M * sizeof(unsigned),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+    RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    const double* hk = reinterpret_cast<const double*>(hout);
+    memcpy(kappa_out, hk, E * sizeof(double));
+    memcpy(v_out, hk + E, E * sizeof(double));
+    if (early_out) memcpy(early_out, hk + 2 * E, E * sizeof(int64_t));
+    memcpy(row_out, hk + 3 * E, E * sizeof(int32_t));
+    if (row_viol) memcpy(row_viol, hviol, (size_t)E * M * sizeof(unsigned));
     return RG_OK;
 }
 

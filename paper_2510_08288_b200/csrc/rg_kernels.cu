@@ -267,6 +267,90 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid(GridArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// batched grid step: E independent governor instances in one launch
+// ---------------------------------------------------------------------------
+
+template <bool FMA, bool POLL>
+__global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid_batch(BatchArgs a) {
+    __shared__ int s_src;
+    __shared__ double s_v;
+    __shared__ bool s_last;
+    const int e = blockIdx.z;
+    const int i = blockIdx.y;
+    const int M = a.m_grid;
+    const double vp = a.v_prev[e], rr = a.r[e];
+    if (threadIdx.x == 0) {
+        const double v = update_setpoint(vp, rr, dvd((double)i, (double)(M - 1)));
+        int src = ss_gate(v, a.p) ? -1 : -2;
+        for (int q = 0; src == -1 && q < i; ++q) {
+            const double vq = update_setpoint(vp, rr, dvd((double)q, (double)(M - 1)));
+            if (ss_gate(vq, a.p) && vq == v) src = q;
+        }
+        s_src = src;
+        s_v = v;
+        if (blockIdx.x == 0) a.row_src[(int64_t)e * M + i] = src;
+    }
+    __syncthreads();
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned* viol = a.viol + (int64_t)e * M;
+    if (s_src == -1) {
+        const bool live = k < a.n_sim;
+        int st = kOk;
+        int32_t steps = a.p.j_star;
+        if (live) {
+            ScenarioStream ss;
+            ss.hs = a.hs[e];
+            for (int c = 0; c < 3; ++c) {
+                ss.lo[c] = a.lo[c];
+                ss.span[c] = a.span[c];
+            }
+            RngSource src{ss, scenario_key(ss, (uint64_t)(a.k0 + k))};
+            const double* x0 = a.x0 + 3 * (int64_t)e;
+            st = rollout<FMA, POLL>(make_cell(a.p), x0[0], x0[1], x0[2], s_v, src, steps,
+                                    viol + i);
+        }
+        const unsigned bad = __ballot_sync(0xffffffffu, live && st != kOk && st != kAbandoned);
+        if (lane_id() == 0 && bad) atomicAdd(viol + i, (unsigned)__popc(bad));
+        warp_count_add(live && st != kAbandoned && steps < a.p.j_star, a.early + e);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(a.ticket + e, 1u) == gridDim.x * gridDim.y - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x == 0) {
+        const int* rs = a.row_src + (int64_t)e * M;
+        int best = -1;
+        for (int q = 0; q < M; ++q) {
+            const int s = ((volatile const int*)rs)[q];
+            const bool full = s != -2 && ((volatile unsigned*)viol)[s < 0 ? q : s] == 0u;
+            if (a.viol_out)
+                a.viol_out[(int64_t)e * M + q] =
+                    s == -2 ? 0xffffffffu : ((volatile unsigned*)viol)[s < 0 ? q : s];
+            if (a.prefix_mode) {
+                if (best == q - 1 && full) best = q;
+            } else if (full) {
+                best = q;
+            }
+        }
+        a.row_out[e] = best;
+        const double kap = best < 0 ? 0.0 : dvd((double)best, (double)(M - 1));
+        a.kappa_out[e] = kap;
+        a.v_out[e] = best < 0 ? vp : update_setpoint(vp, rr, kap);
+        a.early_out[e] = (long long)((volatile unsigned long long*)a.early)[e];
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < M; q += blockDim.x) viol[q] = 0u;
+    if (threadIdx.x == 0) {
+        a.early[e] = 0ull;
+        a.ticket[e] = 0u;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // exact Alg. 2: per-scenario bisection
 // ---------------------------------------------------------------------------
 
@@ -455,6 +539,18 @@ cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, cudaSt
         else     { if (poll) RG_GRID(false, false, true); else RG_GRID(false, false, false); }
     }
 #undef RG_GRID
+    return cudaGetLastError();
+}
+
+cudaError_t launch_grid_batch(const BatchArgs& a, bool fma, bool poll, cudaStream_t s) {
+    dim3 grid(blocks_for(a.n_sim, a.tpb), (unsigned)a.m_grid, (unsigned)a.n_ep);
+    if (fma) {
+        if (poll) k_grid_batch<true, true><<<grid, a.tpb, 0, s>>>(a);
+        else      k_grid_batch<true, false><<<grid, a.tpb, 0, s>>>(a);
+    } else {
+        if (poll) k_grid_batch<false, true><<<grid, a.tpb, 0, s>>>(a);
+        else      k_grid_batch<false, false><<<grid, a.tpb, 0, s>>>(a);
+    }
     return cudaGetLastError();
 }
 

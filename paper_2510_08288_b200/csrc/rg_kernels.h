@@ -70,6 +70,29 @@ struct GridArgs {
     int tpb;
 };
 
+// Batch of independent governor instances (episodes): one launch covers
+// E episodes x M rows x n_sim scenarios; per-episode arrays are indexed by e.
+struct BatchArgs {
+    ProblemDev p;
+    int32_t n_ep, m_grid, prefix_mode;
+    int64_t n_sim, k0;
+    double lo[3], span[3];
+    const double* x0;       // [E][3]
+    const double* v_prev;   // [E]
+    const double* r;        // [E]
+    const uint64_t* hs;     // [E] splitmix64(seed_e)
+    unsigned* viol;         // [E][M] accumulators (reset by the last block of e)
+    unsigned long long* early;  // [E]
+    int* row_src;           // [E][M]
+    unsigned* ticket;       // [E]
+    int* row_out;           // [E]
+    double* kappa_out;      // [E]
+    double* v_out;          // [E]
+    long long* early_out;   // [E]
+    unsigned* viol_out;     // [E][M] or null
+    int tpb;
+};
+
 struct BisectAcc {
     unsigned long long kappa_bits;  // min over scenarios (as bits; kappa >= 0)
     int found;                      // AND
@@ -109,6 +132,7 @@ cudaError_t launch_to_soa(const double* src, double* dst, int64_t n_sim, int64_t
                           int32_t j_star, int64_t ld, cudaStream_t s);
 cudaError_t launch_fill(const FillArgs& a, bool fma, bool rng, cudaStream_t s);
 cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, cudaStream_t s);
+cudaError_t launch_grid_batch(const BatchArgs& a, bool fma, bool poll, cudaStream_t s);
 cudaError_t launch_bisect(const BisectArgs& a, bool fma, int src, cudaStream_t s);
 cudaError_t launch_tanh(const double* x, double* y, int64_t n, bool fma, bool lockstep,
                         cudaStream_t s);

@@ -37,7 +37,8 @@ from .ssgate import admissible_setpoints
 __all__ = ["BACKENDS", "GovernorConfig", "GovernorState", "KappaResult", "CellProbe",
            "update_setpoint", "grid_kappas", "fill_feasibility", "extract_kappa_opt",
            "bisection_rg", "robust_rg_sequential", "robust_rg_parallel", "probe_candidate",
-           "check_candidate", "DIAG_CSV_HEADER", "CELL_OK", "CELL_VIOLATED", "CELL_OVERFLOW"]
+           "check_candidate", "DIAG_CSV_HEADER", "CELL_OK", "CELL_VIOLATED", "CELL_OVERFLOW",
+           "robust_rg_parallel_batch"]
 
 # "gpu" is the reference's name for its device backend (governor.py:53); both
 # names select the CUDA device here.  CPU backends do not exist in this build.
@@ -395,6 +396,31 @@ def robust_rg_parallel(plant, x_t, state, r_t, cset, scenarios, config, backend=
     v = update_setpoint(state.v_prev, r_t, kappa)
     state.v_prev = v
     return KappaResult(kappa_opt=kappa, v_applied=v, feasible=True, diagnostics=stats, matrix=P)
+
+
+def robust_rg_parallel_batch(plant, X, v_prev, r, cset, model, n_sim, seeds, config, k0=0):
+    """E independent robust grid steps in one device launch (BASELINE C3/C5).
+
+    Episode e is robust_rg_parallel(plant, X[e], GovernorState(v_prev[e]), r[e],
+    cset, sample_scenarios(model, n_sim, j_star+1, seeds[e]), config) with the
+    "hold" policy: returns (kappa[E], v_applied[E], feasible[E], early[E]),
+    each equal to the single-episode call's result.  Rows already known to be
+    infeasible stop early (verdicts are unaffected).
+    """
+    _require_device_plant(plant)
+    if config.tighten_mode == "scale":
+        validate_epsilon(config.epsilon)
+    X = np.ascontiguousarray(X, dtype=np.float64).reshape(-1, 3)
+    if not np.all(np.isfinite(X)):
+        raise ConfigError("state entries must be finite")
+    if model.state_dim != 3 or model.kind != "uniform":
+        raise ConfigError("the batched step needs a 3-state uniform disturbance model")
+    prob, _, _ = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor, config.epsilon,
+                           config.tighten_mode, config.j_star, 0)
+    ctx = _capi.context(getattr(config, "device", 0))
+    row, kappa, v, early = ctx.grid_step_batch(prob, X, v_prev, r, seeds, k0, n_sim, model.lo,
+                                               model.span, config.m_grid, config.prefix_mode)
+    return kappa, v, row >= 0, early
 
 
 # ---------------------------------------------------------------------------

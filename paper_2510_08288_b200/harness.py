@@ -21,10 +21,11 @@ import numpy as np
 
 from .disturbance import DisturbanceModel, ScenarioSet, derive_seed, sample_scenarios
 from .errors import ConfigError, IntegrationOverflowError
-from .governor import GovernorState, bisection_rg, robust_rg_parallel
+from .governor import GovernorState, bisection_rg, robust_rg_parallel, \
+    robust_rg_parallel_batch
 
 __all__ = ["ReferenceProfile", "RunRecord", "run_closed_loop", "run_closed_loop_bisection",
-           "RUN_CSV_HEADER", "STATE_LIMIT"]
+           "run_closed_loop_batch", "RUN_CSV_HEADER", "STATE_LIMIT"]
 
 RUN_CSV_HEADER = "t,r_t,v_t,y_t,kappa_opt,feasible,wall_us"
 STATE_LIMIT = 1e6
@@ -139,3 +140,75 @@ def run_closed_loop_bisection(plant, cset, model, config, profile, steps, seed, 
         out.append((res, y_t))
         x = plant.step(x, res.v_applied) + d_true[t]
     return out
+
+
+def _rk4_batch(h: float, X: np.ndarray, V: np.ndarray) -> np.ndarray:
+    """The surrogate's rk4_step on E states at once (dynamics.py:110-139).
+
+    Elementwise the same IEEE operations as the scalar step; numpy's vector
+    and scalar tanh agree bit for bit (tests/test_harness_batch.py).
+    """
+    def f(Y):
+        out = np.empty_like(Y)
+        out[:, 0] = -Y[:, 0] + np.tanh(Y[:, 1])
+        out[:, 1] = -Y[:, 1] + V
+        out[:, 2] = -2.0 * Y[:, 2] + Y[:, 0]
+        return out
+
+    k1 = f(X)
+    k2 = f(X + 0.5 * h * k1)
+    k3 = f(X + 0.5 * h * k2)
+    k4 = f(X + h * k3)
+    return X + (h / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
+
+
+def run_closed_loop_batch(plant, cset, model, config, profile, steps, seeds, x0=None, v0=0.0):
+    """E independent governed closed loops (BASELINE C5), one device launch per step.
+
+    Episode e is run_closed_loop(plant, cset, model, config, profile, steps,
+    seeds[e]) -- same scenario and plant streams, same arithmetic -- with all
+    live episodes' governor steps batched into rg_grid_step_batch and the true
+    plants advanced together with numpy.  `profile` is one profile for all
+    episodes or an (E, steps) array of requests.  Returns one RunRecord per
+    episode (rows: t, r_t, v_t, y_t, kappa, feasible, wall_us=0).
+    """
+    seeds = [int(s_) for s_ in seeds]
+    E = len(seeds)
+    if steps < 1 or E < 1:
+        raise ConfigError("steps and the number of episodes must be >= 1")
+    device = getattr(config, "device", 0)
+    X = np.tile(np.zeros(3) if x0 is None else np.asarray(x0, dtype=np.float64), (E, 1))
+    Vp = np.full(E, float(v0))
+    if isinstance(profile, ReferenceProfile):
+        R = np.tile(profile.schedule(steps), (E, 1))
+    else:
+        R = np.asarray(profile, dtype=np.float64).reshape(E, -1)[:, :steps]
+    scen_seeds = np.array([derive_seed(s_, "scenarios") for s_ in seeds], dtype=object)
+    D = np.stack([_true_disturbance(model, steps, s_, device) for s_ in seeds])
+    recs = [RunRecord(rows=[], config={"j_star": config.j_star, "n_sim": config.n_sim,
+                                       "m_grid": config.m_grid, "steps": steps,
+                                       "backend": "cuda", "batched": E}, seed=s_)
+            for s_ in seeds]
+    live = np.arange(E)
+    for t in range(steps):
+        if live.size == 0:
+            break
+        kap, v, feas, _ = robust_rg_parallel_batch(
+            plant, X[live], Vp[live], R[live, t], cset, model, config.n_sim,
+            [(int(scen_seeds[e]) + t) for e in live], config)
+        for j, e in enumerate(live):
+            recs[e].rows.append((t, float(R[e, t]), float(v[j]), float(X[e, 0]),
+                                 float(kap[j]), bool(feas[j]), 0))
+        Vp[live] = v
+        Xn = _rk4_batch(plant.step_size, X[live], v)
+        bad = np.any(~np.isfinite(Xn) | (np.abs(Xn) > STATE_LIMIT), axis=1)
+        Xn = Xn + D[live, t]
+        bad2 = np.any(~np.isfinite(Xn) | (np.abs(Xn) > STATE_LIMIT), axis=1)
+        X[live] = Xn
+        for j in np.flatnonzero(bad | bad2):
+            e = live[j]
+            recs[e].aborted = True
+            recs[e].abort_reason = (f"step {t}: integration overflow" if bad[j] else
+                                    f"step {t}: state left the operating box")
+        live = live[~(bad | bad2)]
+    return recs

@@ -1,0 +1,66 @@
+"""Batched episodes (BASELINE C5): the batched device step and closed loop must
+equal the single-episode paths, and the vectorised true-plant step must equal
+the reference's scalar rk4_step (numpy's vector and scalar tanh agree)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2510_08288_b200 as rg
+from paper_2510_08288_b200.harness import (ReferenceProfile, _rk4_batch, run_closed_loop,
+                                           run_closed_loop_batch)
+
+PLANT = rg.make_plant("surrogate-fc")
+BOX = rg.ConstraintSet(-0.9, 0.9)
+PROFILE = ReferenceProfile(((0, 0.4), (400, 2.5), (1000, -2.5), (1600, 0.2)))
+
+
+def test_rk4_batch_equals_scalar_step():
+    rng = np.random.default_rng(0)
+    X = np.concatenate([rng.uniform(-1, 1, (3000, 3)), rng.uniform(-30, 30, (1000, 3))])
+    V = rng.uniform(-3, 3, X.shape[0])
+    got = _rk4_batch(0.01, X, V)
+    ref = np.stack([PLANT.step(X[i], float(V[i])) for i in range(X.shape[0])])
+    assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
+
+
+def test_numpy_tanh_vector_equals_scalar():
+    rng = np.random.default_rng(1)
+    x = np.concatenate([rng.uniform(-3, 3, 200_000), rng.uniform(-25, 25, 50_000)])
+    sc = np.array([np.tanh(np.float64(v)) for v in x])
+    assert np.array_equal(np.tanh(x).view(np.uint64), sc.view(np.uint64))
+
+
+@pytest.mark.gpu
+def test_batch_step_equals_single_steps():
+    rng = np.random.default_rng(7)
+    E, n = 24, 300
+    model = rg.DisturbanceModel.scaled(0.02, 3)
+    cfg = rg.GovernorConfig(j_star=128, m_grid=32, n_sim=n)
+    vp = rng.uniform(-1, 1, E)
+    r = rng.uniform(-2.5, 2.5, E)
+    X = np.stack([[np.tanh(v), v, np.tanh(v) / 2] for v in vp]) + rng.uniform(-0.05, 0.05, (E, 3))
+    X[3] = [2.0, 0.0, 0.0]          # infeasible episode (holds)
+    r[5] = vp[5]                    # all rows duplicate
+    seeds = [int(s) for s in rng.integers(0, 2**63, E)] + []
+    seeds[2] = 2**64 - 3
+    kap, v, feas, _ = rg.robust_rg_parallel_batch(PLANT, X, vp, r, BOX, model, n, seeds, cfg)
+    for e in range(E):
+        scen = rg.sample_scenarios(model, n, cfg.j_star + 1, seed=seeds[e])
+        res = rg.robust_rg_parallel(PLANT, X[e], rg.GovernorState(float(vp[e])), float(r[e]),
+                                    BOX, scen, cfg)
+        assert (kap[e], v[e], bool(feas[e])) == (res.kappa_opt, res.v_applied, res.feasible), e
+
+
+@pytest.mark.gpu
+def test_closed_loop_batch_equals_single_episode_loops(golden):
+    model = rg.DisturbanceModel.scaled(0.001, 3)
+    cfg = rg.GovernorConfig(n_sim=64)
+    seeds = [2024, 3001, 3002, 77]
+    recs = run_closed_loop_batch(PLANT, BOX, model, cfg, PROFILE, 2000, seeds)
+    got = np.array([[row[2], row[3], row[4], float(row[5])] for row in recs[0].rows])
+    assert np.array_equal(got, golden["desk_grid_trace"])   # the reference's own trace
+    for e in (1, 3):
+        single = run_closed_loop(PLANT, BOX, model, cfg, PROFILE, 600, seeds[e])
+        assert [row[:6] for row in recs[e].rows[:600]] == [row[:6] for row in single.rows]
