@@ -64,6 +64,10 @@ extern "C" {
 #define RG_STAGE_RNG 0x40   /* RNG source: generate the SoA tensor first */
 /* With neither RG_FUSED_RNG nor RG_STAGE_RNG an RNG source is staged when
  * n_sim * j_star <= 4M scenario-steps (it then stays in L2) and fused above. */
+#define RG_LPC1 0x80        /* force 1 lane per (row, scenario) cell */
+#define RG_LPC2 0x100       /* force 2 lanes per cell (each evaluates 2 of the 4 tanh) */
+#define RG_LPC4 0x200       /* force 4 lanes per cell (1 tanh each) */
+/* Default: 1 lane per cell (fastest measured).  Results are identical for every choice. */
 
 typedef struct rg_ctx rg_ctx;
 

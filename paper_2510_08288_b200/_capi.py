@@ -25,6 +25,8 @@ RG_TANH_AUTO, RG_TANH_FMA, RG_TANH_GENERIC = 0, 1, 2
 RG_DEVICE_PTRS, RG_ASYNC, RG_ABANDON, RG_NO_TIMING = 0x1, 0x2, 0x4, 0x8
 RG_TANH_LOCKSTEP, RG_FUSED_RNG, RG_STAGE_RNG = 0x10, 0x20, 0x40
 _RNG_FLAGS = {None: 0, "fused": RG_FUSED_RNG, "staged": RG_STAGE_RNG}
+RG_LPC1, RG_LPC2, RG_LPC4 = 0x80, 0x100, 0x200
+_LPC_FLAGS = {None: 0, 1: RG_LPC1, 2: RG_LPC2, 4: RG_LPC4}
 
 _i32, _i64, _u64, _d, _vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, \
     ctypes.c_void_p
@@ -184,7 +186,8 @@ class Context:
         return out
 
     def fill(self, prob: Problem, x0, v_rows, rows, dist, n_sim, scen: Scenarios | None,
-             S: np.ndarray, steps: np.ndarray, rng_mode: str | None = None) -> None:
+             S: np.ndarray, steps: np.ndarray, rng_mode: str | None = None,
+             lpc: int | None = None) -> None:
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
         v_rows = np.ascontiguousarray(v_rows, dtype=np.float64)
         rows = np.ascontiguousarray(rows, dtype=np.int32)
@@ -195,11 +198,11 @@ class Context:
         check(self.lib.rg_fill(self.handle, ctypes.byref(prob), _p(x0), _p(v_rows), v_rows.size,
                                _p(rows), rows.size, _p(dist), int(n_sim), int(horizon),
                                ctypes.byref(scen) if scen is not None else None, _p(S),
-                               _p(steps), _RNG_FLAGS[rng_mode]))
+                               _p(steps), _RNG_FLAGS[rng_mode] | _LPC_FLAGS[lpc]))
 
     def grid_step(self, prob: Problem, x0, v_prev, r, m_grid, prefix_mode, dist, n_sim,
                   scen: Scenarios | None, want_pbits: bool, abandon: bool = False,
-                  rng_mode: str | None = None):
+                  rng_mode: str | None = None, lpc: int | None = None):
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
         horizon = 0
         if dist is not None:
@@ -208,7 +211,7 @@ class Context:
         viol = np.zeros(m_grid, dtype=np.uint32)
         pbits = np.zeros((m_grid, (n_sim + 31) // 32), dtype=np.uint32) if want_pbits else None
         res = GridResult()
-        flags = (RG_ABANDON if abandon else 0) | _RNG_FLAGS[rng_mode]
+        flags = (RG_ABANDON if abandon else 0) | _RNG_FLAGS[rng_mode] | _LPC_FLAGS[lpc]
         check(self.lib.rg_grid_step(self.handle, ctypes.byref(prob), _p(x0), float(v_prev),
                                     float(r), int(m_grid), int(bool(prefix_mode)), _p(dist),
                                     int(n_sim), int(horizon),
@@ -218,7 +221,7 @@ class Context:
 
     def bisect(self, prob: Problem, x0, v_prev, r, n_kappa, dist, n_sim,
                scen: Scenarios | None, per_scenario: bool = False, paths: bool = False,
-               rng_mode: str | None = None):
+               rng_mode: str | None = None, lpc: int | None = None):
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
         horizon = 0
         if dist is not None:
@@ -238,12 +241,12 @@ class Context:
                                  int(n_kappa), _p(dist), int(n_sim), int(horizon),
                                  ctypes.byref(scen) if scen is not None else None, _p(kap),
                                  _p(fnd), _p(cel), _p(erl), _p(pk), _p(po), ctypes.byref(res),
-                                 _RNG_FLAGS[rng_mode]))
+                                 _RNG_FLAGS[rng_mode] | _LPC_FLAGS[lpc]))
         per = (kap, fnd, cel, erl) if per_scenario else None
         return res, per, ((pk, po) if paths else None)
 
     def grid_step_batch(self, prob: Problem, x0, v_prev, r, seeds, k0, n_sim, lo, span,
-                        m_grid, prefix_mode=False, abandon=True, want_viol=False):
+                        m_grid, prefix_mode=False, abandon=True, want_viol=False, lpc=None):
         """Batched robust grid step; returns (row, kappa, v, early[, viol])."""
         x0 = np.ascontiguousarray(x0, dtype=np.float64).reshape(-1, 3)
         E = x0.shape[0]
@@ -261,7 +264,7 @@ class Context:
                                           _p(r), _p(seeds), int(k0), int(n_sim), _p(lo),
                                           _p(span), int(m_grid), int(bool(prefix_mode)),
                                           _p(row), _p(kap), _p(v), _p(early), _p(viol),
-                                          RG_ABANDON if abandon else 0))
+                                          (RG_ABANDON if abandon else 0) | _LPC_FLAGS[lpc]))
         return (row, kap, v, early, viol) if want_viol else (row, kap, v, early)
 
     def fp64_peak(self) -> float:

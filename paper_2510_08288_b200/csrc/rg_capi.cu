@@ -9,6 +9,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -241,6 +242,24 @@ int32_t grow_grid(rg_ctx* ctx, int m) {
     RG_CUDA(cudaMemsetAsync(ctx->g_out.p, 0, ctx->g_out.bytes, ctx->stream));
     ctx->grid_cap = cap;
     return RG_OK;
+}
+
+// Lanes per cell.  LPC = 2 / 4 spread a cell's four tanh chains over lanes
+// (rg_cell.cuh: step_tanh).  Measured on B200 (round 1) the redundant x1/x2/x3
+// work costs more than the extra parallelism buys at every size tried
+// (1k-10k scenarios: 0.255 / 0.322 / 0.417 ms at 1k for LPC 1 / 2 / 4), so the
+// default is one lane per cell; RG_LPC2 / RG_LPC4 remain for experiments and
+// are covered by the parity tests.
+int lpc_for(const rg_ctx* ctx, int64_t cells, int32_t flags) {
+    (void)ctx;
+    (void)cells;
+    if (flags & RG_LPC2) return 2;
+    if (flags & RG_LPC4) return 4;
+    if (const char* env = getenv("RG_FORCE_LPC")) {  // tuning experiments only
+        const int v = atoi(env);
+        if (v == 1 || v == 2 || v == 4) return v;
+    }
+    return 1;
 }
 
 int tpb_for(const rg_ctx* ctx, int64_t n_sim, int64_t rows) {
@@ -485,7 +504,9 @@ int32_t rg_fill(rg_ctx* ctx, const rg_problem* prob, const double* x0, const dou
         a.steps = ctx->steps.as<int32_t>();
     }
     RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-    RG_CUDA(rg::launch_fill(a, ctx->variant == rg::kTanhFma, use_rng, ctx->stream));
+    const int lpc = lpc_for(ctx, (int64_t)n_rows * n_sim, flags);
+    a.tpb = tpb_for(ctx, n_sim * lpc, n_rows);
+    RG_CUDA(rg::launch_fill(a, ctx->variant == rg::kTanhFma, use_rng, lpc, ctx->stream));
     RG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     if (!(flags & RG_DEVICE_PTRS)) {
         // copy back only the active rows: the caller's other rows stay untouched
@@ -591,10 +612,15 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
             a.pbits = ctx->pbits.as<unsigned>();
         }
     }
-    a.tpb = tpb_for(ctx, n_sim, m_grid);
+    const int lpc = lpc_for(ctx, (int64_t)m_grid * n_sim, flags);
+    a.tpb = tpb_for(ctx, n_sim * lpc, m_grid);
+    if (pbits && lpc > 1)  // lanes OR their bits in
+        RG_CUDA(cudaMemsetAsync(a.pbits, 0, (size_t)m_grid * a.pwords * sizeof(unsigned),
+                                ctx->stream));
     const bool timed = !(flags & RG_NO_TIMING);
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-    RG_CUDA(rg::launch_grid(a, ctx->variant == rg::kTanhFma, use_rng, abandon, ctx->stream));
+    RG_CUDA(rg::launch_grid(a, ctx->variant == rg::kTanhFma, use_rng, abandon, lpc,
+                            ctx->stream));
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     if (pbits && !(flags & RG_DEVICE_PTRS))
         RG_CUDA(cudaMemcpyAsync(pbits, a.pbits, (size_t)m_grid * a.pwords * sizeof(unsigned),
@@ -688,10 +714,11 @@ int32_t rg_bisect(rg_ctx* ctx, const rg_problem* prob, const double* x0, double 
     }
     a.acc = ctx->b_acc.as<rg::BisectAcc>();
     a.out = ctx->b_out.as<rg::BisectOut>();
-    a.tpb = tpb_for(ctx, n_sim, 1);
+    const int lpc = lpc_for(ctx, n_sim, flags);
+    a.tpb = tpb_for(ctx, n_sim * lpc, 1);
     const bool timed = !(flags & RG_NO_TIMING);
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-    RG_CUDA(rg::launch_bisect(a, ctx->variant == rg::kTanhFma, src, ctx->stream));
+    RG_CUDA(rg::launch_bisect(a, ctx->variant == rg::kTanhFma, src, lpc, ctx->stream));
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     if (!dev) {
         if (kappa_k) {
@@ -805,9 +832,10 @@ int32_t rg_grid_step_batch(rg_ctx* ctx, const rg_problem* prob, int32_t n_episod
     a.early_out = reinterpret_cast<long long*>(a.v_out + E);
     a.row_out = reinterpret_cast<int*>(a.early_out + E);
     a.viol_out = row_viol ? ctx->e_violout.as<unsigned>() : nullptr;
-    a.tpb = tpb_for(ctx, n_sim * E, m_grid);
+    const int lpc = lpc_for(ctx, n_sim * E * M, flags);
+    a.tpb = tpb_for(ctx, n_sim * E * lpc, m_grid);
     RG_CUDA(rg::launch_grid_batch(a, ctx->variant == rg::kTanhFma, (flags & RG_ABANDON) != 0,
-                                  ctx->stream));
+                                  lpc, ctx->stream));
     char* hout = reinterpret_cast<char*>(hin + 6 * E);
     const size_t out_bytes = (size_t)E * (3 * sizeof(double) + sizeof(int));
     RG_CUDA(cudaMemcpyAsync(hout, dout, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));

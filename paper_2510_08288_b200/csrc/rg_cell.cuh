@@ -175,6 +175,41 @@ struct ZeroSource {
     RG_HD D3 load(int32_t) const { return D3{0.0, 0.0, 0.0}; }
 };
 
+// The four tanh values of one step.  LPC lanes cooperate on a cell: with
+// LPC = 2 each lane of a pair evaluates two of the four (in lockstep) and the
+// pair swaps results with one shuffle per value; with LPC = 4 each lane
+// evaluates one.  ptxas serialises independent tanh chains inside a thread,
+// so spreading them over lanes turns ILP the compiler will not schedule into
+// TLP the warp schedulers do.  Every lane ends with all four values.
+template <bool FMA, int LPC>
+__device__ __forceinline__ void step_tanh(double x2, double a2, double b2, double c2,
+                                          double& u1, double& u2, double& u3, double& u4) {
+    if constexpr (LPC == 1) {
+        tanh4<FMA>(x2, a2, b2, c2, u1, u2, u3, u4);
+    } else if constexpr (LPC == 2) {
+        const bool q = (threadIdx.x & 1u) != 0;
+        const double in[2] = {q ? a2 : x2, q ? c2 : b2};
+        double out[2];
+        tanh_lockstep<FMA, 2>(in, out);
+        const double o0 = __shfl_xor_sync(0xffffffffu, out[0], 1);
+        const double o1 = __shfl_xor_sync(0xffffffffu, out[1], 1);
+        u1 = q ? o0 : out[0];
+        u2 = q ? out[0] : o0;
+        u3 = q ? o1 : out[1];
+        u4 = q ? out[1] : o1;
+    } else {
+        const unsigned q = threadIdx.x & 3u;
+        const double in[1] = {q == 0 ? x2 : (q == 1 ? a2 : (q == 2 ? b2 : c2))};
+        double out[1];
+        tanh_lockstep<FMA, 1>(in, out);
+        const int base = (int)(threadIdx.x & 31u) & ~3;
+        u1 = __shfl_sync(0xffffffffu, out[0], base + 0);
+        u2 = __shfl_sync(0xffffffffu, out[0], base + 1);
+        u3 = __shfl_sync(0xffffffffu, out[0], base + 2);
+        u4 = __shfl_sync(0xffffffffu, out[0], base + 3);
+    }
+}
+
 // One cell.  POLL: every 32 steps check a row-level "already infeasible"
 // flag and abandon (used only when the caller wants verdicts, not P).
 //
@@ -185,16 +220,30 @@ struct ZeroSource {
 // value is still produced by the reference's operations on the reference's
 // operands, so the bits are those of sfc_step.  A step j+1 that is never
 // reached (early exit) only wastes its speculative tanh work.
-template <bool FMA, bool POLL, class Src>
+//
+// LPC > 1: all 32 lanes of the warp run the loop until every cell of the warp
+// is done (lanes of finished or out-of-range cells keep computing throwaway
+// values), so the shuffles in step_tanh always see full warps.  `live` marks
+// lanes whose cell exists.
+template <bool FMA, bool POLL, int LPC, class Src>
 __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2, double x3,
                                        double v, const Src& src, int32_t& steps,
-                                       const unsigned int* dead) {
-    if (!in_bounds(x1, p.ylo, p.yhi)) {
-        steps = 0;
-        return kViolated;
-    }
+                                       const unsigned int* dead, bool live = true) {
     const int32_t J = p.j_star;
     constexpr bool kRing = std::is_same<Src, SoaSource>::value;
+    int status = kOk;
+    steps = J;
+    bool done = !live;
+    if (live && !in_bounds(x1, p.ylo, p.yhi)) {
+        steps = 0;
+        status = kViolated;
+        done = true;
+    }
+    if constexpr (LPC == 1) {
+        if (done) return status;
+    } else {
+        if (__all_sync(0xffffffffu, done)) return status;
+    }
     // prologue: tanh values of step 0 and x2 after step 0
     D3 d;
     if constexpr (kRing) {
@@ -209,7 +258,7 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
     }
     X2Stage st = x2_stage<FMA>(x2, v, p);
     double t1, t2, t3, t4;
-    tanh4<FMA>(x2, st.a2, st.b2, st.c2, t1, t2, t3, t4);
+    step_tanh<FMA, LPC>(x2, st.a2, st.b2, st.c2, t1, t2, t3, t4);
     double x2n = add(add(x2, mul(p.c, st.s2)), d.d1);
     for (int32_t j = 0; j < J; ++j) {
         // step j's slot was drained into `d` last iteration: refill it with step j+2
@@ -220,7 +269,7 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
         // step j+1's x2 chain and tanh values (speculative past an exit)
         const X2Stage sn = x2_stage<FMA>(x2n, v, p);
         double u1, u2, u3, u4;
-        tanh4<FMA>(x2n, sn.a2, sn.b2, sn.c2, u1, u2, u3, u4);
+        step_tanh<FMA, LPC>(x2n, sn.a2, sn.b2, sn.c2, u1, u2, u3, u4);
         D3 dn;
         if constexpr (kRing) {
             cp_async_wait<1>();  // step j+1 landed (issued one iteration ago)
@@ -231,22 +280,27 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
         const double x2nn = add(add(x2n, mul(p.c, sn.s2)), dn.d1);
         // step j's x1/x3
         x13_update<FMA>(x1, x3, t1, t2, t3, t4, p, d.d0, d.d2);
-        if (!(fabs(x1) <= kStateLimit && fabs(x2n) <= kStateLimit && fabs(x3) <= kStateLimit)) {
-            steps = j + 1;
-            if constexpr (kRing) cp_async_wait<0>();  // no copy may land after we leave
-            return kOverflow;
-        }
-        if (!in_bounds(x1, p.ylo, p.yhi)) {
-            steps = j + 1;
-            if constexpr (kRing) cp_async_wait<0>();
-            return kViolated;
-        }
-        if (POLL && (j & 31) == 31) {
-            if (*(volatile const unsigned int*)dead != 0u) {
+        if (!done) {
+            if (!(fabs(x1) <= kStateLimit && fabs(x2n) <= kStateLimit &&
+                  fabs(x3) <= kStateLimit)) {
                 steps = j + 1;
-                if constexpr (kRing) cp_async_wait<0>();
-                return kAbandoned;
+                status = kOverflow;
+                done = true;
+            } else if (!in_bounds(x1, p.ylo, p.yhi)) {
+                steps = j + 1;
+                status = kViolated;
+                done = true;
+            } else if (POLL && (j & 31) == 31 &&
+                       *(volatile const unsigned int*)dead != 0u) {
+                steps = j + 1;
+                status = kAbandoned;
+                done = true;
             }
+        }
+        if constexpr (LPC == 1) {
+            if (done) break;
+        } else {
+            if (__all_sync(0xffffffffu, done)) break;
         }
         t1 = u1;
         t2 = u2;
@@ -255,8 +309,8 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
         x2n = x2nn;
         d = dn;
     }
-    steps = J;
-    return kOk;
+    if constexpr (kRing) cp_async_wait<0>();  // no copy may land after we leave
+    return status;
 }
 
 // governor.py:151-159: exact at both endpoints, three roundings otherwise.

@@ -120,25 +120,29 @@ __global__ void k_to_soa(const double* __restrict__ src, double* __restrict__ ds
 // parity fill: status/steps for every (active row, scenario)
 // ---------------------------------------------------------------------------
 
-template <bool FMA, bool RNG>
+template <bool FMA, bool RNG, int LPC>
 __global__ void __launch_bounds__(128, RG_GRID_MINB) k_fill(FillArgs a) {
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= a.n_sim) return;
+    const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPC;
+    const bool live = k < a.n_sim;
+    if (LPC == 1 && !live) return;
     const int32_t row = a.rows[blockIdx.y];
     const double v = a.v_rows[row];
     const CellConst c = make_cell(a.p);
+    const int64_t kk = live ? k : 0;  // out-of-range lanes replay scenario 0
     int32_t steps = 0;
     int st;
     if (RNG) {
-        RngSource src{a.stream, scenario_key(a.stream, (uint64_t)(a.k0 + k))};
-        st = rollout<FMA, false>(c, a.x0[0], a.x0[1], a.x0[2], v, src, steps, nullptr);
+        RngSource src{a.stream, scenario_key(a.stream, (uint64_t)(a.k0 + kk))};
+        st = rollout<FMA, false, LPC>(c, a.x0[0], a.x0[1], a.x0[2], v, src, steps, nullptr, live);
     } else {
         __shared__ double ring[2 * 3 * kRingStride];
-        SoaSource src{a.soa + k, a.ld, ring + threadIdx.x};
-        st = rollout<FMA, false>(c, a.x0[0], a.x0[1], a.x0[2], v, src, steps, nullptr);
+        SoaSource src{a.soa + kk, a.ld, ring + threadIdx.x};
+        st = rollout<FMA, false, LPC>(c, a.x0[0], a.x0[1], a.x0[2], v, src, steps, nullptr, live);
     }
-    a.S[(int64_t)row * a.n_sim + k] = (uint8_t)st;
-    a.steps[(int64_t)row * a.n_sim + k] = steps;
+    if (live && threadIdx.x % LPC == 0) {
+        a.S[(int64_t)row * a.n_sim + k] = (uint8_t)st;
+        a.steps[(int64_t)row * a.n_sim + k] = steps;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -159,7 +163,7 @@ __device__ int row_source(const GridArgs& a, int i, double* v_out) {
     return -1;
 }
 
-template <bool FMA, bool RNG, bool POLL>
+template <bool FMA, bool RNG, bool POLL, int LPC>
 __global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid(GridArgs a) {
     __shared__ int s_src;
     __shared__ double s_v;
@@ -172,36 +176,43 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid(GridArgs a) {
     }
     __syncthreads();
     const int src_i = s_src;
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPC;
+    const bool lead = threadIdx.x % LPC == 0;
     if (src_i == -1) {
         const bool live = k < a.n_sim;
+        const int64_t kk = live ? k : 0;
         int st = kOk;
         int32_t steps = a.p.j_star;
-        if (live) {
+        if (live || LPC > 1) {
             const CellConst c = make_cell(a.p);
             if (RNG) {
-                RngSource src{a.stream, scenario_key(a.stream, (uint64_t)(a.k0 + k))};
-                st = rollout<FMA, POLL>(c, a.x0[0], a.x0[1], a.x0[2], s_v, src, steps,
-                                        a.viol + i);
+                RngSource src{a.stream, scenario_key(a.stream, (uint64_t)(a.k0 + kk))};
+                st = rollout<FMA, POLL, LPC>(c, a.x0[0], a.x0[1], a.x0[2], s_v, src, steps,
+                                             a.viol + i, live);
             } else {
                 __shared__ double ring[2 * 3 * kRingStride];
-                SoaSource src{a.soa + k, a.ld, ring + threadIdx.x};
-                st = rollout<FMA, POLL>(c, a.x0[0], a.x0[1], a.x0[2], s_v, src, steps,
-                                        a.viol + i);
+                SoaSource src{a.soa + kk, a.ld, ring + threadIdx.x};
+                st = rollout<FMA, POLL, LPC>(c, a.x0[0], a.x0[1], a.x0[2], s_v, src, steps,
+                                             a.viol + i, live);
             }
         }
-        const bool bad = live && st != kOk && st != kAbandoned;
+        const bool cnt = live && lead;
+        const bool bad = cnt && st != kOk && st != kAbandoned;
         const unsigned bad_mask = __ballot_sync(0xffffffffu, bad);
         if (lane_id() == 0 && bad_mask) atomicAdd(a.viol + i, (unsigned)__popc(bad_mask));
-        warp_count_add(live && st != kAbandoned && steps < a.p.j_star, a.early + i);
-        warp_count_add(live && st == kOverflow, a.ovf + i);
-        warp_count_add(live && st == kAbandoned, a.abandoned + i);
+        warp_count_add(cnt && st != kAbandoned && steps < a.p.j_star, a.early + i);
+        warp_count_add(cnt && st == kOverflow, a.ovf + i);
+        warp_count_add(cnt && st == kAbandoned, a.abandoned + i);
         if (a.pbits) {
-            const unsigned ok_mask = __ballot_sync(0xffffffffu, live && st == kOk);
-            if (lane_id() == 0 && (k - lane_id()) < a.n_sim)
-                a.pbits[(int64_t)i * a.pwords + (k >> 5)] = ok_mask;
+            if (LPC == 1) {
+                const unsigned ok_mask = __ballot_sync(0xffffffffu, live && st == kOk);
+                if (lane_id() == 0 && (k - lane_id()) < a.n_sim)
+                    a.pbits[(int64_t)i * a.pwords + (k >> 5)] = ok_mask;
+            } else if (cnt && st == kOk) {  // words pre-zeroed by the host
+                atomicOr(a.pbits + (int64_t)i * a.pwords + (k >> 5), 1u << (k & 31));
+            }
         }
-    } else if (a.pbits && lane_id() == 0 && (k - lane_id()) < a.n_sim) {
+    } else if (LPC == 1 && a.pbits && lane_id() == 0 && (k - lane_id()) < a.n_sim) {
         // pruned or duplicate row: no simulated bits (the host expands duplicates)
         a.pbits[(int64_t)i * a.pwords + (k >> 5)] = 0u;
     }
@@ -270,7 +281,7 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid(GridArgs a) {
 // batched grid step: E independent governor instances in one launch
 // ---------------------------------------------------------------------------
 
-template <bool FMA, bool POLL>
+template <bool FMA, bool POLL, int LPC>
 __global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid_batch(BatchArgs a) {
     __shared__ int s_src;
     __shared__ double s_v;
@@ -291,27 +302,29 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid_batch(BatchArgs a) {
         if (blockIdx.x == 0) a.row_src[(int64_t)e * M + i] = src;
     }
     __syncthreads();
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPC;
+    const bool lead = threadIdx.x % LPC == 0;
     unsigned* viol = a.viol + (int64_t)e * M;
     if (s_src == -1) {
         const bool live = k < a.n_sim;
         int st = kOk;
         int32_t steps = a.p.j_star;
-        if (live) {
+        if (live || LPC > 1) {
             ScenarioStream ss;
             ss.hs = a.hs[e];
             for (int c = 0; c < 3; ++c) {
                 ss.lo[c] = a.lo[c];
                 ss.span[c] = a.span[c];
             }
-            RngSource src{ss, scenario_key(ss, (uint64_t)(a.k0 + k))};
+            RngSource src{ss, scenario_key(ss, (uint64_t)(a.k0 + (live ? k : 0)))};
             const double* x0 = a.x0 + 3 * (int64_t)e;
-            st = rollout<FMA, POLL>(make_cell(a.p), x0[0], x0[1], x0[2], s_v, src, steps,
-                                    viol + i);
+            st = rollout<FMA, POLL, LPC>(make_cell(a.p), x0[0], x0[1], x0[2], s_v, src, steps,
+                                         viol + i, live);
         }
-        const unsigned bad = __ballot_sync(0xffffffffu, live && st != kOk && st != kAbandoned);
+        const bool cnt = live && lead;
+        const unsigned bad = __ballot_sync(0xffffffffu, cnt && st != kOk && st != kAbandoned);
         if (lane_id() == 0 && bad) atomicAdd(viol + i, (unsigned)__popc(bad));
-        warp_count_add(live && st != kAbandoned && steps < a.p.j_star, a.early + e);
+        warp_count_add(cnt && st != kAbandoned && steps < a.p.j_star, a.early + e);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -354,39 +367,55 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid_batch(BatchArgs a) {
 // exact Alg. 2: per-scenario bisection
 // ---------------------------------------------------------------------------
 
-template <bool FMA, int SRC>  // SRC: 0 zero (nominal), 1 rng, 2 soa
+template <bool FMA, int SRC, int LPC>  // SRC: 0 zero (nominal), 1 rng, 2 soa
 __global__ void __launch_bounds__(128, RG_GRID_MINB) k_bisect(BisectArgs a) {
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPC;
     const bool live = k < a.n_sim;
+    const bool lead = threadIdx.x % LPC == 0;
     double kopt = 1.0;
     int found = 1, cells = 0, early = 0;
-    if (live) {
+    if (live || LPC > 1) {
+        const int64_t kk = live ? k : 0;
         const CellConst c = make_cell(a.p);
         RngSource rsrc{};
         SoaSource ssrc{};
-        if (SRC == 1) rsrc = RngSource{a.stream, scenario_key(a.stream, (uint64_t)(a.k0 + k))};
         __shared__ double ring[2 * 3 * kRingStride];
-        if (SRC == 2) ssrc = SoaSource{a.soa + k, a.ld, ring + threadIdx.x};
+        if (SRC == 1) rsrc = RngSource{a.stream, scenario_key(a.stream, (uint64_t)(a.k0 + kk))};
+        if (SRC == 2) ssrc = SoaSource{a.soa + kk, a.ld, ring + threadIdx.x};
         double klo = 0.0, khi = 1.0;
         kopt = 0.0;
         found = 0;
+        // With LPC > 1 the rollouts shuffle across the whole warp, so every
+        // lane walks every candidate; finished or gated-out cells pass
+        // live = false and only keep the warp company.
+        bool fin = !live;
         for (int it = -1; it < a.n_kappa; ++it) {
+            if (LPC == 1) {
+                if (fin) break;
+            } else if (__all_sync(0xffffffffu, fin)) {
+                break;
+            }
             const double kappa = it < 0 ? 1.0 : mul(0.5, add(klo, khi));
             const double v = update_setpoint(a.v_prev, a.r, kappa);
+            const bool run = !fin && ss_gate(v, a.p);
             bool ok = false;
             int32_t sr = 0;
-            if (ss_gate(v, a.p)) {
+            if (run || LPC > 1) {
                 int st;
                 if (SRC == 1)
-                    st = rollout<FMA, false>(c, a.x0[0], a.x0[1], a.x0[2], v, rsrc, sr, nullptr);
+                    st = rollout<FMA, false, LPC>(c, a.x0[0], a.x0[1], a.x0[2], v, rsrc, sr,
+                                                  nullptr, run);
                 else if (SRC == 2)
-                    st = rollout<FMA, false>(c, a.x0[0], a.x0[1], a.x0[2], v, ssrc, sr, nullptr);
+                    st = rollout<FMA, false, LPC>(c, a.x0[0], a.x0[1], a.x0[2], v, ssrc, sr,
+                                                  nullptr, run);
                 else
-                    st = rollout<FMA, false>(c, a.x0[0], a.x0[1], a.x0[2], v, ZeroSource{}, sr,
-                                             nullptr);
-                ok = st == kOk;
+                    st = rollout<FMA, false, LPC>(c, a.x0[0], a.x0[1], a.x0[2], v,
+                                                  ZeroSource{}, sr, nullptr, run);
+                ok = run && st == kOk;
+                if (!run) sr = 0;
             }
-            if (a.path_kappa) {
+            if (fin) continue;
+            if (a.path_kappa && lead) {
                 a.path_kappa[k * (a.n_kappa + 1) + cells] = kappa;
                 a.path_ok[k * (a.n_kappa + 1) + cells] = ok ? 1 : 0;
             }
@@ -396,7 +425,7 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_bisect(BisectArgs a) {
                 if (ok) {
                     kopt = 1.0;
                     found = 1;
-                    break;
+                    fin = true;
                 }
                 continue;
             }
@@ -408,11 +437,17 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_bisect(BisectArgs a) {
                 khi = kappa;
             }
         }
-        if (a.kappa_k) {
+        if (a.kappa_k && live && lead) {
             a.kappa_k[k] = kopt;
             a.found_k[k] = found;
             a.cells_k[k] = cells;
             a.early_k[k] = early;
+        }
+        if (!(live && lead)) {  // neutral elements of the reductions
+            kopt = 1.0;
+            found = 1;
+            cells = 0;
+            early = 0;
         }
     }
     // reductions: min kappa (non-negative doubles order like their bits), AND found,
@@ -515,53 +550,81 @@ cudaError_t launch_to_soa(const double* src, double* dst, int64_t n_sim, int64_t
     return cudaGetLastError();
 }
 
-cudaError_t launch_fill(const FillArgs& a, bool fma, bool rng, cudaStream_t s) {
+#define RG_DISPATCH_LPC(LPC_VAR, MACRO)   \
+    do {                                   \
+        if ((LPC_VAR) == 4) MACRO(4);      \
+        else if ((LPC_VAR) == 2) MACRO(2); \
+        else MACRO(1);                     \
+    } while (0)
+
+cudaError_t launch_fill(const FillArgs& a, bool fma, bool rng, int lpc, cudaStream_t s) {
     if (a.n_rows == 0 || a.n_sim == 0) return cudaSuccess;
-    dim3 grid(blocks_for(a.n_sim, a.tpb), (unsigned)a.n_rows);
-    if (fma) {
-        if (rng) k_fill<true, true><<<grid, a.tpb, 0, s>>>(a);
-        else     k_fill<true, false><<<grid, a.tpb, 0, s>>>(a);
-    } else {
-        if (rng) k_fill<false, true><<<grid, a.tpb, 0, s>>>(a);
-        else     k_fill<false, false><<<grid, a.tpb, 0, s>>>(a);
-    }
+    dim3 grid(blocks_for(a.n_sim * lpc, a.tpb), (unsigned)a.n_rows);
+#define RG_FILL(L)                                                         \
+    do {                                                                   \
+        if (fma) {                                                         \
+            if (rng) k_fill<true, true, L><<<grid, a.tpb, 0, s>>>(a);      \
+            else     k_fill<true, false, L><<<grid, a.tpb, 0, s>>>(a);     \
+        } else {                                                           \
+            if (rng) k_fill<false, true, L><<<grid, a.tpb, 0, s>>>(a);     \
+            else     k_fill<false, false, L><<<grid, a.tpb, 0, s>>>(a);    \
+        }                                                                  \
+    } while (0)
+    RG_DISPATCH_LPC(lpc, RG_FILL);
+#undef RG_FILL
     return cudaGetLastError();
 }
 
-cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, cudaStream_t s) {
-    dim3 grid(blocks_for(a.n_sim, a.tpb), (unsigned)a.m_grid);
-#define RG_GRID(F, R, P) k_grid<F, R, P><<<grid, a.tpb, 0, s>>>(a)
-    if (fma) {
-        if (rng) { if (poll) RG_GRID(true, true, true); else RG_GRID(true, true, false); }
-        else     { if (poll) RG_GRID(true, false, true); else RG_GRID(true, false, false); }
-    } else {
-        if (rng) { if (poll) RG_GRID(false, true, true); else RG_GRID(false, true, false); }
-        else     { if (poll) RG_GRID(false, false, true); else RG_GRID(false, false, false); }
-    }
+cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, int lpc,
+                        cudaStream_t s) {
+    dim3 grid(blocks_for(a.n_sim * lpc, a.tpb), (unsigned)a.m_grid);
+#define RG_GRID(F, R, P, L) k_grid<F, R, P, L><<<grid, a.tpb, 0, s>>>(a)
+#define RG_GRID_L(L)                                                             \
+    do {                                                                         \
+        if (fma) {                                                               \
+            if (rng) { if (poll) RG_GRID(true, true, true, L); else RG_GRID(true, true, false, L); }   \
+            else     { if (poll) RG_GRID(true, false, true, L); else RG_GRID(true, false, false, L); } \
+        } else {                                                                 \
+            if (rng) { if (poll) RG_GRID(false, true, true, L); else RG_GRID(false, true, false, L); } \
+            else     { if (poll) RG_GRID(false, false, true, L); else RG_GRID(false, false, false, L); } \
+        }                                                                        \
+    } while (0)
+    RG_DISPATCH_LPC(lpc, RG_GRID_L);
+#undef RG_GRID_L
 #undef RG_GRID
     return cudaGetLastError();
 }
 
-cudaError_t launch_grid_batch(const BatchArgs& a, bool fma, bool poll, cudaStream_t s) {
-    dim3 grid(blocks_for(a.n_sim, a.tpb), (unsigned)a.m_grid, (unsigned)a.n_ep);
-    if (fma) {
-        if (poll) k_grid_batch<true, true><<<grid, a.tpb, 0, s>>>(a);
-        else      k_grid_batch<true, false><<<grid, a.tpb, 0, s>>>(a);
-    } else {
-        if (poll) k_grid_batch<false, true><<<grid, a.tpb, 0, s>>>(a);
-        else      k_grid_batch<false, false><<<grid, a.tpb, 0, s>>>(a);
-    }
+cudaError_t launch_grid_batch(const BatchArgs& a, bool fma, bool poll, int lpc, cudaStream_t s) {
+    dim3 grid(blocks_for(a.n_sim * lpc, a.tpb), (unsigned)a.m_grid, (unsigned)a.n_ep);
+#define RG_BATCH(L)                                                              \
+    do {                                                                         \
+        if (fma) {                                                               \
+            if (poll) k_grid_batch<true, true, L><<<grid, a.tpb, 0, s>>>(a);     \
+            else      k_grid_batch<true, false, L><<<grid, a.tpb, 0, s>>>(a);    \
+        } else {                                                                 \
+            if (poll) k_grid_batch<false, true, L><<<grid, a.tpb, 0, s>>>(a);    \
+            else      k_grid_batch<false, false, L><<<grid, a.tpb, 0, s>>>(a);   \
+        }                                                                        \
+    } while (0)
+    RG_DISPATCH_LPC(lpc, RG_BATCH);
+#undef RG_BATCH
     return cudaGetLastError();
 }
 
-cudaError_t launch_bisect(const BisectArgs& a, bool fma, int src, cudaStream_t s) {
-    const unsigned g = blocks_for(a.n_sim, a.tpb);
-#define RG_BIS(F, S) k_bisect<F, S><<<g, a.tpb, 0, s>>>(a)
-    if (fma) {
-        if (src == 0) RG_BIS(true, 0); else if (src == 1) RG_BIS(true, 1); else RG_BIS(true, 2);
-    } else {
-        if (src == 0) RG_BIS(false, 0); else if (src == 1) RG_BIS(false, 1); else RG_BIS(false, 2);
-    }
+cudaError_t launch_bisect(const BisectArgs& a, bool fma, int src, int lpc, cudaStream_t s) {
+    const unsigned g = blocks_for(a.n_sim * lpc, a.tpb);
+#define RG_BIS(F, S, L) k_bisect<F, S, L><<<g, a.tpb, 0, s>>>(a)
+#define RG_BIS_L(L)                                                              \
+    do {                                                                         \
+        if (fma) {                                                               \
+            if (src == 0) RG_BIS(true, 0, L); else if (src == 1) RG_BIS(true, 1, L); else RG_BIS(true, 2, L);    \
+        } else {                                                                 \
+            if (src == 0) RG_BIS(false, 0, L); else if (src == 1) RG_BIS(false, 1, L); else RG_BIS(false, 2, L); \
+        }                                                                        \
+    } while (0)
+    RG_DISPATCH_LPC(lpc, RG_BIS_L);
+#undef RG_BIS_L
 #undef RG_BIS
     return cudaGetLastError();
 }

@@ -130,10 +130,11 @@ struct BisectArgs {
 cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s);
 cudaError_t launch_to_soa(const double* src, double* dst, int64_t n_sim, int64_t horizon,
                           int32_t j_star, int64_t ld, cudaStream_t s);
-cudaError_t launch_fill(const FillArgs& a, bool fma, bool rng, cudaStream_t s);
-cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, cudaStream_t s);
-cudaError_t launch_grid_batch(const BatchArgs& a, bool fma, bool poll, cudaStream_t s);
-cudaError_t launch_bisect(const BisectArgs& a, bool fma, int src, cudaStream_t s);
+cudaError_t launch_fill(const FillArgs& a, bool fma, bool rng, int lpc, cudaStream_t s);
+cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, int lpc,
+                        cudaStream_t s);
+cudaError_t launch_grid_batch(const BatchArgs& a, bool fma, bool poll, int lpc, cudaStream_t s);
+cudaError_t launch_bisect(const BisectArgs& a, bool fma, int src, int lpc, cudaStream_t s);
 cudaError_t launch_tanh(const double* x, double* y, int64_t n, bool fma, bool lockstep,
                         cudaStream_t s);
 cudaError_t launch_gen_soa(const ScenarioStream& st, int64_t k0, int64_t n_sim, int32_t j_star,

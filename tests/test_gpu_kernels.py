@@ -48,15 +48,17 @@ def test_lockstep_tanh_bit_exact(ctx, orc):
     assert mism.size == 0, f"{mism.size} mismatches, first x={x[mism[:5]]}"
 
 
+@pytest.mark.parametrize("lpc", [1, 2, 4])
 @pytest.mark.parametrize("mode", ["fused", "staged"])
 @pytest.mark.parametrize("idx", range(N_FILL))
-def test_grid_step_both_rng_paths(ctx, golden, idx, mode):
+def test_grid_step_both_rng_paths(ctx, golden, idx, mode, lpc):
     c = fill_case(golden, idx)
     m = rg.DisturbanceModel(c["ranges"])
     scen = _capi.make_scenarios(c["seed"], 0, c["n_sim"], m.lo, m.span)
     prob = _problem(c["lower"], c["upper"], c["anchor"], c["eps"], c["j_star"])
     res, viol, pbits = ctx.grid_step(prob, c["x0"], c["v_prev"], c["r"], c["m_grid"],
-                                     c["prefix"], None, c["n_sim"], scen, True, rng_mode=mode)
+                                     c["prefix"], None, c["n_sim"], scen, True, rng_mode=mode,
+                                     lpc=lpc)
     P = np.unpackbits(pbits.view(np.uint8), axis=1, bitorder="little")[:, :c["n_sim"]]
     ss = c["ss_ok"]
     # simulated rows carry their own bits; the reference's P has the same rows
@@ -70,15 +72,22 @@ def test_grid_step_both_rng_paths(ctx, golden, idx, mode):
     assert kappa == c["result"][0]
 
 
+@pytest.mark.parametrize("lpc", [1, 2, 4])
 @pytest.mark.parametrize("mode", ["fused", "staged"])
 @pytest.mark.parametrize("idx", range(N_BIS))
-def test_bisect_both_rng_paths(ctx, golden, idx, mode):
+def test_bisect_both_rng_paths(ctx, golden, idx, mode, lpc):
     c = bis_case(golden, idx)
     m = rg.DisturbanceModel(c["ranges"])
     scen = _capi.make_scenarios(c["seed"], 0, c["n_sim"], m.lo, m.span)
     prob = _problem(c["lower"], c["upper"], c["anchor"], c["eps"], c["j_star"])
-    res, per, _ = ctx.bisect(prob, c["x0"], c["v_prev"], c["r"], c["n_kappa"], None,
-                             c["n_sim"], scen, per_scenario=True, rng_mode=mode)
+    res, per, paths = ctx.bisect(prob, c["x0"], c["v_prev"], c["r"], c["n_kappa"], None,
+                                 c["n_sim"], scen, per_scenario=True, paths=True,
+                                 rng_mode=mode, lpc=lpc)
+    pk, po = paths
+    ref_k = c["paths"][..., 0]
+    used = ~np.isnan(ref_k)
+    assert np.array_equal(pk[used], ref_k[used]) and np.array_equal(np.isnan(pk), ~used)
+    assert np.array_equal(po[used], c["paths"][..., 1][used].astype(np.uint8))
     assert np.array_equal(np.stack(per, axis=1).astype(np.float64), c["per"]), c["name"]
     assert (res.kappa, float(res.found), res.cells, res.early) == \
         (c["result"][0], c["result"][2], c["result"][3], c["result"][4])
@@ -129,3 +138,37 @@ def test_staged_and_fused_agree_at_scale(ctx):
     b = ctx.grid_step(prob, x0, -0.4, -2.5, M, False, None, n, sc, True, rng_mode="staged")
     assert a[0].row == b[0].row and a[0].early_terms == b[0].early_terms
     assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+
+
+@pytest.mark.parametrize("lpc", [1, 2, 4])
+@pytest.mark.parametrize("idx", range(N_FILL))
+def test_fill_cells_every_lane_split(ctx, golden, idx, lpc):
+    c = fill_case(golden, idx)
+    grid = rg.grid_kappas(c["m_grid"])
+    v_rows = np.array([rg.update_setpoint(c["v_prev"], c["r"], float(k)) for k in grid])
+    S = np.full((c["m_grid"], c["n_sim"]), 7, np.uint8)
+    steps = np.full((c["m_grid"], c["n_sim"]), -1, np.int32)
+    m = rg.DisturbanceModel(c["ranges"])
+    scen = _capi.make_scenarios(c["seed"], 0, c["n_sim"], m.lo, m.span)
+    ctx.fill(_problem(c["lower"], c["upper"], c["anchor"], c["eps"], c["j_star"]), c["x0"],
+             v_rows, np.arange(c["m_grid"], dtype=np.int32), None, c["n_sim"], scen, S, steps,
+             lpc=lpc)
+    assert np.array_equal(S, c["S_all"]) and np.array_equal(steps, c["steps_all"]), c["name"]
+
+
+@pytest.mark.parametrize("lpc", [1, 2, 4])
+def test_batch_every_lane_split(ctx, lpc):
+    rng = np.random.default_rng(3)
+    E, n, M = 12, 70, 16
+    vp = rng.uniform(-1, 1, E)
+    r = rng.uniform(-2.5, 2.5, E)
+    X = np.stack([[np.tanh(v), v, np.tanh(v) / 2] for v in vp]) + rng.uniform(-0.05, 0.05, (E, 3))
+    seeds = [int(x) for x in rng.integers(0, 2**62, E)]
+    m = rg.DisturbanceModel.scaled(0.02, 3)
+    prob = _problem(-0.9, 0.9, 0.0, 0.05, 96)
+    ref = ctx.grid_step_batch(prob, X, vp, r, seeds, 0, n, m.lo, m.span, M, lpc=1,
+                              abandon=False, want_viol=True)
+    got = ctx.grid_step_batch(prob, X, vp, r, seeds, 0, n, m.lo, m.span, M, lpc=lpc,
+                              abandon=False, want_viol=True)
+    for a, b in zip(ref, got):
+        assert np.array_equal(a, b)
