@@ -208,8 +208,8 @@ class Context:
         if dist is not None:
             dist = np.ascontiguousarray(dist, dtype=np.float64)
             horizon = dist.shape[1]
-        viol = np.zeros(m_grid, dtype=np.uint32)
-        pbits = np.zeros((m_grid, (n_sim + 31) // 32), dtype=np.uint32) if want_pbits else None
+        viol = np.empty(m_grid, dtype=np.uint32)
+        pbits = np.empty((m_grid, (n_sim + 31) // 32), dtype=np.uint32) if want_pbits else None
         res = GridResult()
         flags = (RG_ABANDON if abandon else 0) | _RNG_FLAGS[rng_mode] | _LPC_FLAGS[lpc]
         check(self.lib.rg_grid_step(self.handle, ctypes.byref(prob), _p(x0), float(v_prev),

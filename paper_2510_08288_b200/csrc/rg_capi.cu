@@ -127,7 +127,8 @@ struct rg_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // grid-step accumulators and outputs
     int grid_cap = 0;
-    DevBuf g_viol, g_early, g_ovf, g_aband, g_src, g_ticket, g_violout, g_out;
+    int last_m = 0;
+    DevBuf g_viol, g_early, g_ovf, g_aband, g_src, g_ticket, g_out;
     // bisection accumulators and outputs
     DevBuf b_acc, b_out;
     // batched grid step: inputs, accumulators (zeroed on growth, reset by the kernel), outputs
@@ -223,6 +224,13 @@ bool want_stage(int64_t n_sim, int32_t j_star, int32_t flags) {
     return n_sim * (int64_t)j_star <= kStageMaxScenarioSteps;
 }
 
+// The grid step's results live in one device block -- [GridOut | viol_out[m] |
+// pbits[m][pwords] when requested] -- so a synchronous call reads everything
+// back with a single copy.
+constexpr size_t kOutHead = 128;  // >= sizeof(GridOut), keeps viol_out aligned
+static_assert(sizeof(rg::GridOut) <= kOutHead, "result block header too small");
+size_t viol_bytes(int64_t m) { return ((size_t)m * sizeof(unsigned) + 15) / 16 * 16; }
+
 int32_t grow_grid(rg_ctx* ctx, int m) {
     if (m <= ctx->grid_cap) return RG_OK;
     const int cap = std::max(m, 64);
@@ -231,9 +239,8 @@ int32_t grow_grid(rg_ctx* ctx, int m) {
     RG_CUDA(ctx->g_ovf.ensure(cap * sizeof(unsigned long long)));
     RG_CUDA(ctx->g_aband.ensure(cap * sizeof(unsigned long long)));
     RG_CUDA(ctx->g_src.ensure(cap * sizeof(int)));
-    RG_CUDA(ctx->g_violout.ensure(cap * sizeof(unsigned)));
     RG_CUDA(ctx->g_ticket.ensure(sizeof(unsigned)));
-    RG_CUDA(ctx->g_out.ensure(sizeof(rg::GridOut)));
+    RG_CUDA(ctx->g_out.ensure(kOutHead + viol_bytes(cap)));
     RG_CUDA(cudaMemsetAsync(ctx->g_viol.p, 0, ctx->g_viol.bytes, ctx->stream));
     RG_CUDA(cudaMemsetAsync(ctx->g_early.p, 0, ctx->g_early.bytes, ctx->stream));
     RG_CUDA(cudaMemsetAsync(ctx->g_ovf.p, 0, ctx->g_ovf.bytes, ctx->stream));
@@ -355,7 +362,7 @@ int32_t rg_destroy(rg_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     DevBuf* bufs[] = {&ctx->g_viol, &ctx->g_early, &ctx->g_ovf, &ctx->g_aband, &ctx->g_src,
-                      &ctx->g_ticket, &ctx->g_violout, &ctx->g_out, &ctx->b_acc, &ctx->b_out,
+                      &ctx->g_ticket, &ctx->g_out, &ctx->b_acc, &ctx->b_out,
                       &ctx->dist_raw, &ctx->soa, &ctx->S, &ctx->steps, &ctx->pbits, &ctx->rows,
                       &ctx->vrows, &ctx->tmp_a, &ctx->tmp_b, &ctx->kap_k, &ctx->fnd_k,
                       &ctx->cel_k, &ctx->erl_k, &ctx->path_k, &ctx->path_o, &ctx->e_in,
@@ -523,22 +530,15 @@ int32_t rg_fill(rg_ctx* ctx, const rg_problem* prob, const double* x0, const dou
 }
 
 static int32_t read_grid(rg_ctx* ctx, uint32_t* row_viol, int32_t m_grid, rg_grid_result* out,
-                         bool viol_is_device, bool timed) {
-    RG_CUDA(ctx->h_stage.ensure(sizeof(rg::GridOut) + (size_t)m_grid * sizeof(unsigned)));
-    rg::GridOut* ho = ctx->h_stage.as<rg::GridOut>();
-    unsigned* hv = reinterpret_cast<unsigned*>(ho + 1);
-    RG_CUDA(cudaMemcpyAsync(ho, ctx->g_out.p, sizeof(rg::GridOut), cudaMemcpyDeviceToHost,
-                            ctx->stream));
-    if (row_viol) {
-        if (viol_is_device)
-            RG_CUDA(cudaMemcpyAsync(row_viol, ctx->g_violout.p, m_grid * sizeof(unsigned),
-                                    cudaMemcpyDeviceToDevice, ctx->stream));
-        else
-            RG_CUDA(cudaMemcpyAsync(hv, ctx->g_violout.p, m_grid * sizeof(unsigned),
-                                    cudaMemcpyDeviceToHost, ctx->stream));
-    }
+                         uint32_t* pbits_host, size_t pbits_bytes, bool timed) {
+    const size_t bytes = kOutHead + viol_bytes(m_grid) + pbits_bytes;
+    RG_CUDA(ctx->h_stage.ensure(bytes));
+    char* h = ctx->h_stage.as<char>();
+    RG_CUDA(cudaMemcpyAsync(h, ctx->g_out.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
     RG_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (row_viol && !viol_is_device) memcpy(row_viol, hv, m_grid * sizeof(unsigned));
+    const rg::GridOut* ho = reinterpret_cast<const rg::GridOut*>(h);
+    if (row_viol) memcpy(row_viol, h + kOutHead, m_grid * sizeof(unsigned));
+    if (pbits_host) memcpy(pbits_host, h + kOutHead + viol_bytes(m_grid), pbits_bytes);
     if (out) {
         out->row = ho->row;
         out->n_active = ho->n_active;
@@ -600,45 +600,48 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
     a.abandoned = ctx->g_aband.as<unsigned long long>();
     a.row_src = ctx->g_src.as<int>();
     a.ticket = ctx->g_ticket.as<unsigned>();
-    a.viol_out = ctx->g_violout.as<unsigned>();
-    a.out = ctx->g_out.as<rg::GridOut>();
     a.pwords = (n_sim + 31) / 32;
+    const size_t pbytes = pbits ? (size_t)m_grid * a.pwords * sizeof(unsigned) : 0;
+    const bool pbits_in_block = pbits && !(flags & RG_DEVICE_PTRS);
+    RG_CUDA(ctx->g_out.ensure(kOutHead + viol_bytes(m_grid) + (pbits_in_block ? pbytes : 0)));
+    char* blk = ctx->g_out.as<char>();
+    a.out = reinterpret_cast<rg::GridOut*>(blk);
+    a.viol_out = reinterpret_cast<unsigned*>(blk + kOutHead);
     const bool abandon = (flags & RG_ABANDON) && !pbits;
-    if (pbits) {
-        if (flags & RG_DEVICE_PTRS) {
-            a.pbits = pbits;
-        } else {
-            RG_CUDA(ctx->pbits.ensure((size_t)m_grid * a.pwords * sizeof(unsigned)));
-            a.pbits = ctx->pbits.as<unsigned>();
-        }
-    }
+    if (pbits)
+        a.pbits = pbits_in_block ? reinterpret_cast<unsigned*>(blk + kOutHead + viol_bytes(m_grid))
+                                 : pbits;
     const int lpc = lpc_for(ctx, (int64_t)m_grid * n_sim, flags);
     a.tpb = tpb_for(ctx, n_sim * lpc, m_grid);
     if (pbits && lpc > 1)  // lanes OR their bits in
-        RG_CUDA(cudaMemsetAsync(a.pbits, 0, (size_t)m_grid * a.pwords * sizeof(unsigned),
-                                ctx->stream));
+        RG_CUDA(cudaMemsetAsync(a.pbits, 0, pbytes, ctx->stream));
     const bool timed = !(flags & RG_NO_TIMING);
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
     RG_CUDA(rg::launch_grid(a, ctx->variant == rg::kTanhFma, use_rng, abandon, lpc,
                             ctx->stream));
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
-    if (pbits && !(flags & RG_DEVICE_PTRS))
-        RG_CUDA(cudaMemcpyAsync(pbits, a.pbits, (size_t)m_grid * a.pwords * sizeof(unsigned),
-                                cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->last_m = m_grid;
     if (flags & RG_ASYNC) {
         if (row_viol && (flags & RG_DEVICE_PTRS))
-            RG_CUDA(cudaMemcpyAsync(row_viol, ctx->g_violout.p, m_grid * sizeof(unsigned),
+            RG_CUDA(cudaMemcpyAsync(row_viol, a.viol_out, m_grid * sizeof(unsigned),
                                     cudaMemcpyDeviceToDevice, ctx->stream));
         return RG_OK;
     }
-    return read_grid(ctx, row_viol, m_grid, out, (flags & RG_DEVICE_PTRS) != 0, timed);
+    if (row_viol && (flags & RG_DEVICE_PTRS)) {
+        RG_CUDA(cudaMemcpyAsync(row_viol, a.viol_out, m_grid * sizeof(unsigned),
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+        row_viol = nullptr;
+    }
+    return read_grid(ctx, row_viol, m_grid, out, pbits_in_block ? pbits : nullptr,
+                     pbits_in_block ? pbytes : 0, timed);
 }
 
 int32_t rg_grid_fetch(rg_ctx* ctx, uint32_t* row_viol, int32_t m_grid, rg_grid_result* out) {
     int32_t rc = enter(ctx);
     if (rc) return rc;
-    if (m_grid < 1 || m_grid > ctx->grid_cap) return fail(RG_E_ARGS, "bad m_grid %d", m_grid);
-    return read_grid(ctx, row_viol, m_grid, out, false, false);
+    if (m_grid < 1 || m_grid > ctx->grid_cap || m_grid != ctx->last_m)
+        return fail(RG_E_ARGS, "bad m_grid %d (last step used %d)", m_grid, ctx->last_m);
+    return read_grid(ctx, row_viol, m_grid, out, nullptr, 0, false);
 }
 
 int32_t rg_bisect(rg_ctx* ctx, const rg_problem* prob, const double* x0, double v_prev,

@@ -100,7 +100,7 @@ class ScenarioSet:
     entry (k, j, i) is the counter-RNG value at scenario index k0 + k.
     """
 
-    __slots__ = ("_data", "seed", "model", "_n_sim", "_horizon", "k0", "device")
+    __slots__ = ("_data", "seed", "model", "_n_sim", "_horizon", "k0", "device", "_stream")
 
     def __init__(self, data=None, seed=None, model=None):
         d = np.asarray(data, dtype=np.float64)
@@ -114,6 +114,7 @@ class ScenarioSet:
         self._n_sim, self._horizon = d.shape[0], d.shape[1]
         self.k0 = 0
         self.device = 0
+        self._stream = None
 
     @classmethod
     def generated(cls, model: DisturbanceModel, n_sim: int, horizon: int, seed: int,
@@ -126,6 +127,7 @@ class ScenarioSet:
         obj._horizon = int(horizon)
         obj.k0 = int(k0)
         obj.device = int(device)
+        obj._stream = None
         return obj
 
     @property

@@ -217,9 +217,11 @@ def _source(scenarios, j_star: int):
         if scenarios.horizon < j_star + 1:
             raise ConfigError(f"scenario horizon {scenarios.horizon} too short: need >= "
                               f"j_star+1 = {j_star + 1}")
-        return None, scenarios.n_sim, _capi.make_scenarios(
-            scenarios.seed, scenarios.k0, scenarios.n_sim, scenarios.model.lo,
-            scenarios.model.span)
+        if scenarios._stream is None:  # the rg_scenarios block is immutable: build it once
+            scenarios._stream = _capi.make_scenarios(scenarios.seed, scenarios.k0,
+                                                     scenarios.n_sim, scenarios.model.lo,
+                                                     scenarios.model.span)
+        return None, scenarios.n_sim, scenarios._stream
     data = scenarios.data if hasattr(scenarios, "data") else np.asarray(scenarios)
     data = np.asarray(data)
     if data.ndim != 3 or data.shape[2] != 3:
@@ -232,42 +234,31 @@ def _source(scenarios, j_star: int):
     return np.ascontiguousarray(data, dtype=np.float64), data.shape[0], None
 
 
-def _host_rows(v_prev: float, r: float, grid: np.ndarray, interval):
+def _host_rows(v_prev: float, r: float, grid, interval):
     """v per row, the steady-state gate and the dedup map (governor.py:286, 302-317).
 
-    Vectorised: numpy evaluates v_prev + kappa*(r - v_prev) with the same three
-    roundings as update_setpoint (the endpoints are set exactly as it does),
-    the gate is the verified setpoint interval of ssgate.py (identical to
-    tight.contains(np.tanh(v)) for every double), and rows with equal v map
-    to the first such row like the reference's dict.  For an ascending grid v
-    is monotone, so equal values are adjacent; the general dict walk is kept
-    for the (rounding-induced) non-monotone corner.
+    The reference's own loop in Python floats (same three roundings as
+    update_setpoint, endpoints exact), with the gate evaluated as the verified
+    setpoint interval of ssgate.py -- identical to tight.contains(np.tanh(v))
+    for every double -- and duplicates mapped to the first equal row through a
+    dict, exactly as governor.py:306-317.  Returns Python lists.
     """
-    v_rows = v_prev + grid * (r - v_prev)
-    v_rows[grid == 0.0] = v_prev
-    v_rows[grid == 1.0] = r
-    ss_ok = (v_rows >= interval[0]) & (v_rows <= interval[1])
-    m = grid.size
-    dv = np.diff(v_rows)
-    if (dv >= 0).all() or (dv <= 0).all():
-        same = np.zeros(m, dtype=bool)
-        same[1:] = (dv == 0) & ss_ok[1:] & ss_ok[:-1]
-        pos = np.arange(m)
-        first = np.maximum.accumulate(np.where(same, 0, pos))
-        dup_src = np.where(same, first, -1)
-        reps = np.flatnonzero(ss_ok & ~same)
-        return v_rows, ss_ok, dup_src, reps.astype(np.int32)
-    first_of: dict = {}
-    dup_src = np.full(m, -1, dtype=np.int64)
+    lo, hi = interval
+    d = r - v_prev
+    v_rows = [v_prev if k == 0.0 else (r if k == 1.0 else v_prev + k * d) for k in grid]
+    ss_ok = [lo <= v <= hi for v in v_rows]
+    first: dict = {}
+    dup_src = [-1] * len(v_rows)
     reps = []
-    for i in np.flatnonzero(ss_ok):
-        v = float(v_rows[i])
-        if v in first_of:
-            dup_src[i] = first_of[v]
-        else:
-            first_of[v] = i
-            reps.append(i)
-    return v_rows, ss_ok, dup_src, np.array(reps, dtype=np.int32)
+    for i, v in enumerate(v_rows):
+        if ss_ok[i]:
+            j = first.get(v)
+            if j is None:
+                first[v] = i
+                reps.append(i)
+            else:
+                dup_src[i] = j
+    return v_rows, ss_ok, dup_src, reps
 
 
 @functools.lru_cache(maxsize=256)
@@ -279,7 +270,7 @@ def _prepared(step_size, lower, upper, anchor, eps, mode, j_star, m_grid):
     prob = _capi.Problem(float(step_size), float(lower), float(upper), interval[0],
                          interval[1], int(j_star), 0)
     grid = grid_kappas(m_grid) if m_grid else None
-    return prob, interval, grid
+    return prob, interval, grid, (grid.tolist() if m_grid else None)
 
 
 def _backend_check(backend: str) -> None:
@@ -316,9 +307,13 @@ def fill_feasibility(backend, plant, x0, v_prev, r_t, grid, scenarios, cset, eps
     tight = _tightened(cset, eps, tighten_mode)
 
     t0 = time.perf_counter()
-    prob, interval, _ = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor, eps,
-                                  tighten_mode, j_star, 0)
-    v_rows, ss_ok, dup_src, rows = _host_rows(float(v_prev), float(r_t), grid, interval)
+    prob, interval, _, _ = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor, eps,
+                                     tighten_mode, j_star, 0)
+    v_rows, ss_ok, dup_src, rows = _host_rows(float(v_prev), float(r_t), grid.tolist(), interval)
+    v_rows = np.array(v_rows)
+    ss_ok = np.array(ss_ok, dtype=bool)
+    dup_src = np.array(dup_src, dtype=np.int64)
+    rows = np.array(rows, dtype=np.int32)
     m = grid.size
     S = np.zeros((m, n_sim), dtype=np.uint8)
     steps = np.zeros((m, n_sim), dtype=np.int32)
@@ -354,30 +349,34 @@ def robust_rg_parallel(plant, x_t, state, r_t, cset, scenarios, config, backend=
     _require_device_plant(plant)
     if config.tighten_mode == "scale":
         validate_epsilon(config.epsilon)
-    prob, interval, grid = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor,
-                                     config.epsilon, config.tighten_mode, config.j_star,
-                                     config.m_grid)
+    prob, interval, grid, grid_list = _prepared(plant.step_size, cset.lower, cset.upper,
+                                                cset.anchor, config.epsilon,
+                                                config.tighten_mode, config.j_star,
+                                                config.m_grid)
     dist, n_sim, stream = _source(scenarios, config.j_star)
     device = getattr(config, "device", 0)
     keep = getattr(config, "keep_matrix", True)
 
     t0 = time.perf_counter()
-    v_rows, ss_ok, dup_src, rows = _host_rows(float(state.v_prev), float(r_t), grid, interval)
+    _, ss_ok, dup_src, _ = _host_rows(float(state.v_prev), float(r_t), grid_list, interval)
     ctx = _capi.context(device)
     res, viol, pbits = ctx.grid_step(prob, x_t, state.v_prev, r_t, config.m_grid,
                                      config.prefix_mode, dist, n_sim, stream, want_pbits=keep,
                                      abandon=not keep)
-    # the device gate (verified interval) and dedup must agree with numpy's
-    if res.ss_pruned_rows != int(np.count_nonzero(~ss_ok)) or \
-            res.dedup_rows != int(np.count_nonzero(dup_src >= 0)):
-        raise RefgovError("device steady-state gate disagrees with numpy tanh")
+    # the device gate (verified interval) and dedup must agree with the host's
+    n_pruned = ss_ok.count(False)
+    n_dup = len(dup_src) - dup_src.count(-1)
+    if res.ss_pruned_rows != n_pruned or res.dedup_rows != n_dup:
+        raise RefgovError("device steady-state gate disagrees with the host gate")
     P = None
     if keep:
-        bits = np.unpackbits(pbits.view(np.uint8), axis=1, bitorder="little")[:, :n_sim]
-        P = bits.astype(bool)
-        P[~ss_ok] = False
-        for i in np.flatnonzero(dup_src >= 0):
-            P[i] = P[dup_src[i]]
+        # pruned and duplicate rows come back as zero bits; duplicates copy their source
+        P = np.unpackbits(pbits.view(np.uint8), axis=1, bitorder="little")[:, :n_sim]
+        P = P.view(np.bool_)
+        if n_dup:
+            for i, src in enumerate(dup_src):
+                if src >= 0:
+                    P[i] = P[src]
     row = None if res.row < 0 else res.row + 1
     stats = dict(
         backend="cuda", workers=1, device=ctx.device, sims_run=int(res.sims_run),
@@ -415,8 +414,8 @@ def robust_rg_parallel_batch(plant, X, v_prev, r, cset, model, n_sim, seeds, con
         raise ConfigError("state entries must be finite")
     if model.state_dim != 3 or model.kind != "uniform":
         raise ConfigError("the batched step needs a 3-state uniform disturbance model")
-    prob, _, _ = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor, config.epsilon,
-                           config.tighten_mode, config.j_star, 0)
+    prob, _, _, _ = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor,
+                              config.epsilon, config.tighten_mode, config.j_star, 0)
     ctx = _capi.context(getattr(config, "device", 0))
     row, kappa, v, early = ctx.grid_step_batch(prob, X, v_prev, r, seeds, k0, n_sim, model.lo,
                                                model.span, config.m_grid, config.prefix_mode)
@@ -428,8 +427,8 @@ def robust_rg_parallel_batch(plant, X, v_prev, r, cset, model, n_sim, seeds, con
 # ---------------------------------------------------------------------------
 
 def _bisect_call(plant, x_t, state, r_t, cset, config, dist, n_sim, stream):
-    prob, _, _ = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor, config.epsilon,
-                           config.tighten_mode, config.j_star, 0)
+    prob, _, _, _ = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor,
+                              config.epsilon, config.tighten_mode, config.j_star, 0)
     ctx = _capi.context(getattr(config, "device", 0))
     res, _, _ = ctx.bisect(prob, x_t, state.v_prev, r_t, config.n_kappa, dist, n_sim, stream)
     return res

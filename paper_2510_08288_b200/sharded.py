@@ -78,12 +78,15 @@ def robust_rg_parallel_sharded(plant, x_t, state, r_t, cset, scenarios, config, 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     x_t = _validate_state(plant, x_t)
     _require_device_plant(plant)
-    prob, interval, grid = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor,
-                                     config.epsilon, config.tighten_mode, config.j_star,
-                                     config.m_grid)
+    prob, interval, grid, grid_list = _prepared(plant.step_size, cset.lower, cset.upper,
+                                                cset.anchor, config.epsilon,
+                                                config.tighten_mode, config.j_star,
+                                                config.m_grid)
     shard = scenarios.shard(rank, world)
     t0 = time.perf_counter()
-    v_rows, ss_ok, dup_src, rows = _host_rows(float(state.v_prev), float(r_t), grid, interval)
+    _, ss_ok, dup_src, rows = _host_rows(float(state.v_prev), float(r_t), grid_list, interval)
+    ss_ok = np.array(ss_ok, dtype=bool)
+    dup_src = np.array(dup_src, dtype=np.int64)
     if local_step is None:
         ctx = _capi.context(getattr(config, "device", 0))
         dist_t, n_sim, stream = _source(shard, config.j_star)
@@ -96,7 +99,7 @@ def robust_rg_parallel_sharded(plant, x_t, state, r_t, cset, scenarios, config, 
     counts = global_row_counts(viol, group, dev)
     row = extract_row(counts, dup_src, config.prefix_mode)
     diag = {"method": "parallel-grid-sharded", "ranks": world, "backend": "cuda",
-            "sims_run": int(rows.size) * scenarios.n_sim,
+            "sims_run": len(rows) * scenarios.n_sim,
             "ss_pruned_rows": int(np.count_nonzero(~ss_ok)),
             "dedup_rows": int(np.count_nonzero(dup_src >= 0)),
             "wall_us": int((time.perf_counter() - t0) * 1e6)}
@@ -143,8 +146,8 @@ def robust_rg_sequential_sharded(plant, x_t, state, r_t, cset, scenarios, config
     t0 = time.perf_counter()
     dev = None
     if local_step is None:
-        prob, _, _ = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor,
-                               config.epsilon, config.tighten_mode, config.j_star, 0)
+        prob, _, _, _ = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor,
+                                  config.epsilon, config.tighten_mode, config.j_star, 0)
         ctx = _capi.context(getattr(config, "device", 0))
         dist_t, n_sim, stream = _source(shard, config.j_star)
         res, _, _ = ctx.bisect(prob, x_t, state.v_prev, r_t, config.n_kappa, dist_t, n_sim,

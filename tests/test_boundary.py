@@ -129,13 +129,14 @@ def test_host_rows_match_reference_gate_and_dedup():
 
     plant = rg.make_plant("surrogate-fc")
     tight = rg.tighten(rg.ConstraintSet(-0.9, 0.9), 0.05)
-    _, iv, g = _prepared(0.01, -0.9, 0.9, 0.0, 0.05, "scale", 256, 32)
+    _, iv, g, _ = _prepared(0.01, -0.9, 0.9, 0.0, 0.05, "scale", 256, 32)
     rng = np.random.default_rng(1)
     for trial in range(1500):
         vp = float(rng.choice([rng.uniform(-2, 2), 0.3, -0.0, 1.2744531163104806]))
         r = float(rng.choice([rng.uniform(-3, 3), vp, 2.5, np.nextafter(vp, 9)]))
         grid = g if trial % 2 else np.sort(rng.uniform(0, 1, 17))
-        v, ok, dup, reps = _host_rows(vp, r, grid, iv)
+        v, ok, dup, reps = _host_rows(vp, r, grid.tolist(), iv)
+        v = np.array(v)
         v_ref = [rg.update_setpoint(vp, r, float(k)) for k in grid]
         ok_ref = [tight.contains(plant.steady_state_output(x)) for x in v_ref]
         first, dup_ref, reps_ref = {}, [-1] * len(grid), []
