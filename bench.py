@@ -42,6 +42,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "robust RG step latency (ms) at N scenarios; scenario-steps/sec vs FP64 roofline"
 UNIT = "cell-steps/s"
 FLOPS_PER_CELL_STEP = 210  # 58 explicit ops + 4 tanh x 38
+FP64_INSTR_PER_CELL_STEP = 267  # ncu, round 1: DFMA+DADD+DMUL+DSETP per cell-step (k_grid)
 J_STAR, M_GRID, N_PER_GPU, R_REF = 256, 32, 1000, 0.5
 BASE_SEED = 7
 
@@ -289,8 +290,13 @@ def run_own(args, rank, world, local_rank):
     roof = None
     if kernel_ms:
         achieved = FLOPS_PER_CELL_STEP * cells_rank / (kernel_ms * 1e-3)
+        # the instruction-mix view: ncu counts ~267 FP64-pipe instructions per
+        # cell-step (the 210-flop convention counts each division as 1 flop)
+        fp64_instr_rate = cells_rank / (kernel_ms * 1e-3) * FP64_INSTR_PER_CELL_STEP
         roof = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
                 "unit": "TFLOP/s", "frac": achieved / peak, "traffic": _ncu_traffic(),
+                "fp64_pipe_frac": fp64_instr_rate / (peak / 2.0),
+                "fp64_instr_per_cell_step": FP64_INSTR_PER_CELL_STEP,
                 "peak_source": "measured in this run: rg_fp64_peak (independent DFMA chains, "
                                "2 flop per DFMA); MEASURED_PEAKS.json has no FP64 figure",
                 "flops_per_cell_step": FLOPS_PER_CELL_STEP, "cell_steps_per_launch": cells_rank,
