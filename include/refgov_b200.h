@@ -87,14 +87,29 @@ typedef struct {
 } rg_problem;
 
 /* Counter-RNG scenario set (disturbance.py:179-203): scenario k of the set is
- * k0 + k of the stream `seed`, entry (k, j, i) = lo[i] + span[i] * u. */
+ * k0 + k of the stream `seed`, entry (k, j, i) = lo[i] + span[i] * u.  The
+ * surrogate plant uses components 0..2, a linear plant 0..n-1 (n <= 4). */
 typedef struct {
     uint64_t seed;
     int64_t k0;
     int64_t n_sim;
-    double lo[3];
-    double span[3];
+    double lo[4];
+    double span[4];
 } rg_scenarios;
+
+/* A LinearOraclePlant (dynamics.py:162-206): x+ = A x + B v, y = C x + D v,
+ * n <= 4 states, A row-major; the steady-state gate is
+ * ss_lower <= dc_gain * v <= ss_upper (governor.py:302 with the tightened set). */
+typedef struct {
+    int32_t n;
+    int32_t _pad;
+    double A[16];
+    double B[4];
+    double C[4];
+    double D;
+    double dc_gain;
+    double ss_lower, ss_upper;
+} rg_linear_plant;
 
 /* Result of rg_grid_step (robust_rg_parallel, governor.py:520-579). */
 typedef struct {
@@ -195,6 +210,23 @@ RG_API int32_t rg_grid_step_batch(rg_ctx *ctx, const rg_problem *prob, int32_t n
                                   int32_t prefix_mode, int32_t *row_out, double *kappa_out,
                                   double *v_out, int64_t *early_out, uint32_t *row_viol,
                                   int32_t flags);
+
+/* Linear-plant counterparts of rg_fill and rg_bisect (kernels.py:90-118 behind
+ * governor.py:245-348, 380-517).  `prob` supplies j_star and the output bounds
+ * (its setpoint-interval fields are unused); dist is [n_sim][horizon][n]; x0 has n
+ * entries.  The reference's GPU backend refuses linear plants
+ * (backend_gpu.py:66-71); this library runs them. */
+RG_API int32_t rg_fill_linear(rg_ctx *ctx, const rg_linear_plant *plant, const rg_problem *prob,
+                              const double *x0, const double *v_rows, int32_t m_rows,
+                              const int32_t *rows, int32_t n_rows, const double *dist,
+                              int64_t n_sim, int64_t horizon, const rg_scenarios *rng,
+                              uint8_t *S, int32_t *steps, int32_t flags);
+RG_API int32_t rg_bisect_linear(rg_ctx *ctx, const rg_linear_plant *plant,
+                                const rg_problem *prob, const double *x0, double v_prev,
+                                double r, int32_t n_kappa, const double *dist, int64_t n_sim,
+                                int64_t horizon, const rg_scenarios *rng, double *kappa_k,
+                                int32_t *found_k, int32_t *cells_k, int32_t *early_k,
+                                rg_bisect_result *out, int32_t flags);
 
 /* FP64 roofline probe: independent DFMA chains; returns achieved FLOP/s. */
 RG_API int32_t rg_fp64_peak(rg_ctx *ctx, double *flops_per_s);

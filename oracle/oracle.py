@@ -77,6 +77,8 @@ def lib():
     L.orc_bisect_all.restype = None
     L.orc_bisect_all.argtypes = [_d, _p, _d, _d, _d, _d, _p, _i64, _i64, _i32, _i32, _d, _d,
                                  _p, _p, _p, _p]
+    L.orc_cell_lin.restype = ctypes.c_int
+    L.orc_cell_lin.argtypes = [_i32, _p, _p, _p, _d, _p, _d, _p, _i32, _d, _d, _p]
     L.orc_libm_tanh.restype = _d
     L.orc_libm_tanh.argtypes = [_d]
     L.orc_libm_tanh_many.restype = None
@@ -422,6 +424,136 @@ def profile_schedule(points, steps):
             idx += 1
         out[t] = r
     return out
+
+
+# --------------------------------------------------------------------------
+# Linear plant (kernels.py:90-118; dynamics.py:162-206; governor.py paths)
+# --------------------------------------------------------------------------
+
+def cell_lin(A, B, C, D, x0, v, dist, n_steps, lo, hi):
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    B = np.ascontiguousarray(B, dtype=np.float64)
+    C = np.ascontiguousarray(C, dtype=np.float64)
+    x0 = np.ascontiguousarray(x0, dtype=np.float64)
+    dist = np.ascontiguousarray(dist, dtype=np.float64)
+    sr = np.zeros(1, dtype=np.int32)
+    st = lib().orc_cell_lin(int(x0.size), _ptr(A), _ptr(B), _ptr(C), float(D), _ptr(x0),
+                            float(v), _ptr(dist), int(n_steps), float(lo), float(hi), _ptr(sr))
+    return int(st), int(sr[0])
+
+
+def fill_feasibility_lin(A, B, C, D, dc_gain, x0, v_prev, r, grid, dist, lo, hi, tlo, thi,
+                         j_star):
+    """governor.py:245-348 for a LinearOraclePlant (gate: tight.contains(dc_gain * v))."""
+    grid = np.asarray(grid, dtype=np.float64)
+    m, n_sim = grid.size, dist.shape[0]
+    v_rows = [update_setpoint(v_prev, r, float(k)) for k in grid]
+    ok = np.array([tlo <= dc_gain * v <= thi for v in v_rows])
+    first, reps, dup = {}, [], np.full(m, -1)
+    for i in range(m):
+        if ok[i]:
+            if v_rows[i] in first:
+                dup[i] = first[v_rows[i]]
+            else:
+                first[v_rows[i]] = i
+                reps.append(i)
+    S = np.zeros((m, n_sim), dtype=np.uint8)
+    steps = np.zeros((m, n_sim), dtype=np.int32)
+    for i in reps:
+        for k in range(n_sim):
+            S[i, k], steps[i, k] = cell_lin(A, B, C, D, x0, v_rows[i], dist[k], j_star, lo, hi)
+    for i in range(m):
+        if dup[i] >= 0:
+            S[i], steps[i] = S[dup[i]], steps[dup[i]]
+    P = (S == CELL_OK) & ok[:, None]
+    return P, S, steps
+
+
+def bisect_kappa_lin(A, B, C, D, dc_gain, x0, v_prev, r, lo, hi, tlo, thi, dist_k, j_star,
+                     n_kappa):
+    """_bisect_kappa (governor.py:380-430) for a LinearOraclePlant."""
+    def feasible_at(kappa):
+        v = update_setpoint(v_prev, r, kappa)
+        if not tlo <= dc_gain * v <= thi:
+            return False, 0
+        st, sr = cell_lin(A, B, C, D, x0, v, dist_k, j_star, lo, hi)
+        return st == CELL_OK, sr
+
+    cells, early = 1, 0
+    ok, sr = feasible_at(1.0)
+    if sr < j_star and not ok:
+        early += 1
+    if ok:
+        return 1.0, True, cells, early
+    klo, khi, kopt, found = 0.0, 1.0, 0.0, False
+    for _ in range(n_kappa):
+        kappa = 0.5 * (klo + khi)
+        ok, sr = feasible_at(kappa)
+        cells += 1
+        if sr < j_star and not ok:
+            early += 1
+        if ok:
+            kopt, found, klo = kappa, True, kappa
+        else:
+            khi = kappa
+    return kopt, found, cells, early
+
+
+def linear_maximal_kappa(A, B, C, D, x0, v_prev, r, lower, upper, tlo, thi, j_star,
+                         resolution=1_000_001):
+    """oracle.py:115-198 of the reference: the exact maximal kappa of a stable
+    linear plant on the nominal prediction, snapped to a 10^6-point grid.
+
+    y_j = c_j + g_j v with c_j = C A^j x0 and g_j = C sum_{l<j} A^l B + D; each
+    bound at each step admits a closed-form kappa interval.
+    """
+    A = np.atleast_2d(np.asarray(A, dtype=np.float64))
+    B = np.asarray(B, dtype=np.float64)
+    C = np.asarray(C, dtype=np.float64)
+    n = A.shape[0]
+    gain = float(C @ np.linalg.solve(np.eye(n) - A, B) + D)
+    c = np.empty(j_star + 1)
+    g = np.empty(j_star + 1)
+    alpha = np.asarray(x0, dtype=np.float64).copy()
+    beta = np.zeros(n)
+    for j in range(j_star + 1):
+        c[j] = float(C @ alpha)
+        g[j] = float(C @ beta) + D
+        alpha = A @ alpha
+        beta = A @ beta + B
+    delta = r - v_prev
+    lo_k, hi_k = 0.0, 1.0
+
+    def clamp(p, q, lo, hi):
+        nonlocal lo_k, hi_k
+        if q == 0.0:
+            return lo <= p <= hi
+        a, b = (lo - p) / q, (hi - p) / q
+        if a > b:
+            a, b = b, a
+        lo_k, hi_k = max(lo_k, a), min(hi_k, b)
+        return True
+
+    for j in range(j_star + 1):
+        if not clamp(c[j] + g[j] * v_prev, g[j] * delta, lower, upper):
+            return None
+    if not clamp(gain * v_prev, gain * delta, tlo, thi) or lo_k > hi_k:
+        return None
+
+    def ok_at(kappa):
+        v = update_setpoint(v_prev, r, kappa)
+        y = c + g * v
+        return bool(np.all(y >= lower) and np.all(y <= upper) and tlo <= gain * v <= thi)
+
+    i = min(resolution - 1, int(np.floor(hi_k * (resolution - 1) + 1e-12)))
+    for _ in range(4):
+        if i < 0:
+            return None
+        kappa = i / (resolution - 1)
+        if ok_at(kappa):
+            return float(kappa)
+        i -= 1
+    return None
 
 
 def libm_tanh(x: np.ndarray) -> np.ndarray:

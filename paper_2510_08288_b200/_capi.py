@@ -38,7 +38,28 @@ class Problem(ctypes.Structure):
 
 
 class Scenarios(ctypes.Structure):
-    _fields_ = [("seed", _u64), ("k0", _i64), ("n_sim", _i64), ("lo", _d * 3), ("span", _d * 3)]
+    _fields_ = [("seed", _u64), ("k0", _i64), ("n_sim", _i64), ("lo", _d * 4), ("span", _d * 4)]
+
+
+class LinearPlant(ctypes.Structure):
+    _fields_ = [("n", _i32), ("_pad", _i32), ("A", _d * 16), ("B", _d * 4), ("C", _d * 4),
+                ("D", _d), ("dc_gain", _d), ("ss_lower", _d), ("ss_upper", _d)]
+
+
+def make_linear(plant, ss_lower: float, ss_upper: float) -> "LinearPlant":
+    """rg_linear_plant for a LinearOraclePlant (n <= 4 states)."""
+    n = int(plant.state_dim)
+    if not 1 <= n <= 4:
+        raise BackendUnavailableError(f"the device linear kernels support 1..4 states, got {n}")
+    A = np.zeros(16)
+    A[: n * n] = np.asarray(plant.A, dtype=np.float64).reshape(-1)
+    B = np.zeros(4)
+    B[:n] = plant.B
+    C = np.zeros(4)
+    C[:n] = plant.C
+    d16, d4 = _d * 16, _d * 4
+    return LinearPlant(n, 0, d16(*A), d4(*B), d4(*C), float(plant.D), float(plant.dc_gain),
+                       float(ss_lower), float(ss_upper))
 
 
 class GridResult(ctypes.Structure):
@@ -55,9 +76,10 @@ class BisectResult(ctypes.Structure):
 
 def make_scenarios(seed: int, k0: int, n_sim: int, lo, span) -> "Scenarios":
     """rg_scenarios for the counter-RNG stream ``seed`` (masked to 64 bits)."""
-    d3 = _d * 3
-    return Scenarios(int(seed) & (2**64 - 1), int(k0), int(n_sim), d3(*map(float, lo)),
-                     d3(*map(float, span)))
+    d4 = _d * 4
+    lo = list(map(float, lo)) + [0.0] * (4 - len(lo))
+    span = list(map(float, span)) + [0.0] * (4 - len(span))
+    return Scenarios(int(seed) & (2**64 - 1), int(k0), int(n_sim), d4(*lo[:4]), d4(*span[:4]))
 
 
 # name -> (restype, argtypes); the exact export list of include/refgov_b200.h
@@ -83,6 +105,12 @@ SIGNATURES = {
                          ctypes.POINTER(BisectResult), _i32]),
     "rg_grid_step_batch": (_i32, [_vp, ctypes.POINTER(Problem), _i32, _vp, _vp, _vp, _vp, _i64,
                                   _i64, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i32]),
+    "rg_fill_linear": (_i32, [_vp, ctypes.POINTER(LinearPlant), ctypes.POINTER(Problem), _vp,
+                              _vp, _i32, _vp, _i32, _vp, _i64, _i64, ctypes.POINTER(Scenarios),
+                              _vp, _vp, _i32]),
+    "rg_bisect_linear": (_i32, [_vp, ctypes.POINTER(LinearPlant), ctypes.POINTER(Problem), _vp,
+                                _d, _d, _i32, _vp, _i64, _i64, ctypes.POINTER(Scenarios), _vp,
+                                _vp, _vp, _vp, ctypes.POINTER(BisectResult), _i32]),
     "rg_fp64_peak": (_i32, [_vp, ctypes.POINTER(_d)]),
 }
 
@@ -266,6 +294,43 @@ class Context:
                                           _p(row), _p(kap), _p(v), _p(early), _p(viol),
                                           (RG_ABANDON if abandon else 0) | _LPC_FLAGS[lpc]))
         return (row, kap, v, early, viol) if want_viol else (row, kap, v, early)
+
+    def fill_linear(self, lin: LinearPlant, prob: Problem, x0, v_rows, rows, dist, n_sim,
+                    scen: Scenarios | None, S: np.ndarray, steps: np.ndarray) -> None:
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        v_rows = np.ascontiguousarray(v_rows, dtype=np.float64)
+        rows = np.ascontiguousarray(rows, dtype=np.int32)
+        horizon = 0
+        if dist is not None:
+            dist = np.ascontiguousarray(dist, dtype=np.float64)
+            horizon = dist.shape[1]
+        check(self.lib.rg_fill_linear(self.handle, ctypes.byref(lin), ctypes.byref(prob), _p(x0),
+                                      _p(v_rows), v_rows.size, _p(rows), rows.size, _p(dist),
+                                      int(n_sim), int(horizon),
+                                      ctypes.byref(scen) if scen is not None else None, _p(S),
+                                      _p(steps), 0))
+
+    def bisect_linear(self, lin: LinearPlant, prob: Problem, x0, v_prev, r, n_kappa, dist,
+                      n_sim, scen: Scenarios | None, per_scenario: bool = False):
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        horizon = 0
+        if dist is not None:
+            dist = np.ascontiguousarray(dist, dtype=np.float64)
+            horizon = dist.shape[1]
+        kap = fnd = cel = erl = None
+        if per_scenario:
+            kap = np.empty(n_sim, dtype=np.float64)
+            fnd = np.empty(n_sim, dtype=np.int32)
+            cel = np.empty(n_sim, dtype=np.int32)
+            erl = np.empty(n_sim, dtype=np.int32)
+        res = BisectResult()
+        check(self.lib.rg_bisect_linear(self.handle, ctypes.byref(lin), ctypes.byref(prob),
+                                        _p(x0), float(v_prev), float(r), int(n_kappa), _p(dist),
+                                        int(n_sim), int(horizon),
+                                        ctypes.byref(scen) if scen is not None else None,
+                                        _p(kap), _p(fnd), _p(cel), _p(erl), ctypes.byref(res),
+                                        0))
+        return res, ((kap, fnd, cel, erl) if per_scenario else None)
 
     def fp64_peak(self) -> float:
         f = _d()

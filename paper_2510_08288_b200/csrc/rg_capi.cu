@@ -174,7 +174,7 @@ rg::ScenarioStream make_stream(const rg_scenarios* s) {
         st.lo[i] = s->lo[i];
         st.span[i] = s->span[i];
     }
-    return st;
+    return st;  // the surrogate's three components
 }
 
 cudaMemcpyKind kind_h2d(int32_t flags) {
@@ -853,6 +853,193 @@ int32_t rg_grid_step_batch(rg_ctx* ctx, const rg_problem* prob, int32_t n_episod
     if (early_out) memcpy(early_out, hk + 2 * E, E * sizeof(int64_t));
     memcpy(row_out, hk + 3 * E, E * sizeof(int32_t));
     if (row_viol) memcpy(row_viol, hviol, (size_t)E * M * sizeof(unsigned));
+    return RG_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// [n_sim][horizon][n] (host or device) -> SoA d[(j*n+i)*ld + k], rows j < j_star.
+__global__ void k_to_soa_w(const double* __restrict__ src, double* __restrict__ dst,
+                           int64_t n_sim, int64_t horizon, int n, int32_t j_star, int64_t ld) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int32_t j = blockIdx.y;
+    if (k >= n_sim) return;
+    for (int i = 0; i < n; ++i)
+        dst[((int64_t)j * n + i) * ld + k] = src[(k * horizon + j) * n + i];
+}
+
+int32_t make_linear(const rg_linear_plant* pl, const rg_problem* prob, const double* x0,
+                    rg::LinArgs* a) {
+    if (!pl || !x0) return fail(RG_E_ARGS, "null argument");
+    if (pl->n < 1 || pl->n > 4) return fail(RG_E_ARGS, "linear plant state dim must be 1..4, got %d", pl->n);
+    int32_t rc = make_problem(prob, &a->p);
+    if (rc) return rc;
+    a->L.n = pl->n;
+    for (int i = 0; i < 16; ++i) a->L.A[i] = pl->A[i];
+    for (int i = 0; i < 4; ++i) {
+        a->L.B[i] = pl->B[i];
+        a->L.C[i] = pl->C[i];
+        a->x0[i] = i < pl->n ? x0[i] : 0.0;
+    }
+    a->L.D = pl->D;
+    a->L.gain = pl->dc_gain;
+    a->L.tlo = pl->ss_lower;
+    a->L.thi = pl->ss_upper;
+    for (int i = 0; i < pl->n; ++i)
+        if (!isfinite(x0[i])) return fail(RG_E_ARGS, "state entries must be finite");
+    return RG_OK;
+}
+
+int32_t linear_source(rg_ctx* ctx, const rg_linear_plant* pl, const double* dist, int64_t n_sim,
+                      int64_t horizon, const rg_scenarios* rng, int32_t flags, rg::LinArgs* a) {
+    const int n = pl->n;
+    const int32_t J = a->p.j_star;
+    if (dist) {
+        if (horizon < (int64_t)J + 1)
+            return fail(RG_E_ARGS, "scenario horizon %lld too short: need >= j_star+1 = %d",
+                        (long long)horizon, J + 1);
+        const size_t raw = (size_t)n_sim * horizon * n * sizeof(double);
+        const double* d = dist;
+        if (!(flags & RG_DEVICE_PTRS)) {
+            RG_CUDA(ctx->dist_raw.ensure(raw));
+            RG_CUDA(cudaMemcpyAsync(ctx->dist_raw.p, dist, raw, cudaMemcpyHostToDevice,
+                                    ctx->stream));
+            d = ctx->dist_raw.as<double>();
+        }
+        a->ld = (n_sim + 31) / 32 * 32;
+        RG_CUDA(ctx->soa.ensure((size_t)J * n * a->ld * sizeof(double)));
+        dim3 grid((unsigned)((n_sim + 127) / 128), (unsigned)J);
+        k_to_soa_w<<<grid, 128, 0, ctx->stream>>>(d, ctx->soa.as<double>(), n_sim, horizon, n, J,
+                                                  a->ld);
+        RG_CUDA(cudaGetLastError());
+        a->soa = ctx->soa.as<double>();
+    } else {
+        if (!rng) return fail(RG_E_ARGS, "need a scenario tensor or an RNG stream");
+        a->hs = rg::splitmix64(rng->seed);
+        a->k0 = rng->k0;
+        for (int i = 0; i < 4; ++i) {
+            a->lo[i] = rng->lo[i];
+            a->span[i] = rng->span[i];
+        }
+        a->soa = nullptr;
+    }
+    return RG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t rg_fill_linear(rg_ctx* ctx, const rg_linear_plant* plant, const rg_problem* prob,
+                       const double* x0, const double* v_rows, int32_t m_rows,
+                       const int32_t* rows, int32_t n_rows, const double* dist, int64_t n_sim,
+                       int64_t horizon, const rg_scenarios* rng, uint8_t* S, int32_t* steps,
+                       int32_t flags) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    rg::LinArgs a{};
+    if ((rc = make_linear(plant, prob, x0, &a))) return rc;
+    if (!v_rows || (n_rows > 0 && !rows) || !S || !steps) return fail(RG_E_ARGS, "null buffer");
+    if (m_rows < 1 || n_rows < 0 || n_rows > m_rows || n_sim < 1)
+        return fail(RG_E_ARGS, "bad sizes");
+    for (int32_t q = 0; q < n_rows; ++q)
+        if (rows[q] < 0 || rows[q] >= m_rows) return fail(RG_E_ARGS, "row index out of range");
+    if (n_rows == 0) return RG_OK;
+    if ((rc = linear_source(ctx, plant, dist, n_sim, horizon, rng, flags, &a))) return rc;
+    RG_CUDA(ctx->vrows.ensure(m_rows * sizeof(double)));
+    RG_CUDA(ctx->rows.ensure(n_rows * sizeof(int32_t)));
+    RG_CUDA(cudaMemcpyAsync(ctx->vrows.p, v_rows, m_rows * sizeof(double),
+                            cudaMemcpyHostToDevice, ctx->stream));
+    RG_CUDA(cudaMemcpyAsync(ctx->rows.p, rows, n_rows * sizeof(int32_t), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    a.v_rows = ctx->vrows.as<double>();
+    a.rows = ctx->rows.as<int32_t>();
+    a.n_rows = n_rows;
+    a.n_sim = n_sim;
+    const size_t cells = (size_t)m_rows * n_sim;
+    RG_CUDA(ctx->S.ensure(cells));
+    RG_CUDA(ctx->steps.ensure(cells * sizeof(int32_t)));
+    a.S = ctx->S.as<uint8_t>();
+    a.steps = ctx->steps.as<int32_t>();
+    a.tpb = tpb_for(ctx, n_sim, n_rows);
+    RG_CUDA(rg::launch_fill_lin(a, ctx->stream));
+    for (int32_t q = 0; q < n_rows; ++q) {
+        const int64_t off = (int64_t)rows[q] * n_sim;
+        RG_CUDA(cudaMemcpyAsync(S + off, a.S + off, n_sim, cudaMemcpyDeviceToHost, ctx->stream));
+        RG_CUDA(cudaMemcpyAsync(steps + off, a.steps + off, n_sim * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RG_OK;
+}
+
+int32_t rg_bisect_linear(rg_ctx* ctx, const rg_linear_plant* plant, const rg_problem* prob,
+                         const double* x0, double v_prev, double r, int32_t n_kappa,
+                         const double* dist, int64_t n_sim, int64_t horizon,
+                         const rg_scenarios* rng, double* kappa_k, int32_t* found_k,
+                         int32_t* cells_k, int32_t* early_k, rg_bisect_result* out,
+                         int32_t flags) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    rg::LinArgs a{};
+    if ((rc = make_linear(plant, prob, x0, &a))) return rc;
+    if (n_kappa < 1) return fail(RG_E_ARGS, "n_kappa must be >= 1, got %d", n_kappa);
+    if (n_sim < 1) return fail(RG_E_ARGS, "n_sim must be >= 1");
+    if (!isfinite(v_prev) || !isfinite(r)) return fail(RG_E_ARGS, "v_prev and r must be finite");
+    if ((kappa_k || found_k || cells_k || early_k) && !(kappa_k && found_k && cells_k && early_k))
+        return fail(RG_E_ARGS, "per-scenario outputs come as a set of four");
+    if (dist || rng) {
+        if ((rc = linear_source(ctx, plant, dist, n_sim, horizon, rng, flags, &a))) return rc;
+    } else {  // nominal: the zero scenario, staged
+        a.ld = 32;
+        RG_CUDA(ctx->soa.ensure((size_t)a.p.j_star * plant->n * a.ld * sizeof(double)));
+        RG_CUDA(cudaMemsetAsync(ctx->soa.p, 0, (size_t)a.p.j_star * plant->n * a.ld * sizeof(double),
+                                ctx->stream));
+        a.soa = ctx->soa.as<double>();
+        n_sim = 1;
+    }
+    a.v_prev = v_prev;
+    a.r = r;
+    a.n_kappa = n_kappa;
+    a.n_sim = n_sim;
+    if (kappa_k) {
+        RG_CUDA(ctx->kap_k.ensure(n_sim * sizeof(double)));
+        RG_CUDA(ctx->fnd_k.ensure(n_sim * sizeof(int32_t)));
+        RG_CUDA(ctx->cel_k.ensure(n_sim * sizeof(int32_t)));
+        RG_CUDA(ctx->erl_k.ensure(n_sim * sizeof(int32_t)));
+        a.kappa_k = ctx->kap_k.as<double>();
+        a.found_k = ctx->fnd_k.as<int32_t>();
+        a.cells_k = ctx->cel_k.as<int32_t>();
+        a.early_k = ctx->erl_k.as<int32_t>();
+    }
+    a.acc = ctx->b_acc.as<rg::BisectAcc>();
+    a.out = ctx->b_out.as<rg::BisectOut>();
+    a.tpb = tpb_for(ctx, n_sim, 1);
+    RG_CUDA(rg::launch_bisect_lin(a, ctx->stream));
+    if (kappa_k) {
+        RG_CUDA(cudaMemcpyAsync(kappa_k, a.kappa_k, n_sim * sizeof(double),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+        RG_CUDA(cudaMemcpyAsync(found_k, a.found_k, n_sim * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+        RG_CUDA(cudaMemcpyAsync(cells_k, a.cells_k, n_sim * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+        RG_CUDA(cudaMemcpyAsync(early_k, a.early_k, n_sim * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    RG_CUDA(ctx->h_stage.ensure(sizeof(rg::BisectOut)));
+    rg::BisectOut* ho = ctx->h_stage.as<rg::BisectOut>();
+    RG_CUDA(cudaMemcpyAsync(ho, ctx->b_out.p, sizeof(rg::BisectOut), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (out) {
+        out->kappa = ho->kappa;
+        out->found = ho->found;
+        out->cells = ho->cells;
+        out->early = ho->early;
+        out->kernel_ms = 0.f;
+    }
     return RG_OK;
 }
 

@@ -313,6 +313,92 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
     return status;
 }
 
+// ---- linear plant: kernels.py:90-118 (_cell_lin) ----------------------------
+//
+// x+ = A x + B v + d, y = C x + D v with n <= 4 states; numba evaluates
+// `s += A[i, l] * x[l]` as a separate multiply and add, in this order.
+
+struct LinPlant {
+    int32_t n;
+    double A[16];  // row-major n x n
+    double B[4], C[4], D;
+    double gain, tlo, thi;  // steady-state gate: tlo <= gain * v <= thi
+};
+
+template <int N>
+struct LinSoaSource {  // d[(j*N + i) * ld + k]
+    const double* d;
+    int64_t ld;
+    __device__ __forceinline__ double at(int32_t j, int i) const {
+        return __ldg(d + ((int64_t)j * N + i) * ld);
+    }
+};
+
+template <int N>
+struct LinRngSource {
+    uint64_t K;
+    double lo[4], span[4];
+    __device__ __forceinline__ void step(int32_t j, double (&d)[N]) const {
+        const uint64_t J = splitmix64(K ^ (uint64_t)j);
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+            d[i] = add(lo[i], mul(span[i], unit_double(splitmix64(J ^ (uint64_t)i))));
+    }
+};
+
+template <int N>
+__device__ __forceinline__ double lin_output(const LinPlant& L, const double (&x)[N], double v) {
+    double y = mul(L.D, v);
+#pragma unroll
+    for (int l = 0; l < N; ++l) y = add(y, mul(L.C[l], x[l]));
+    return y;
+}
+
+template <int N, bool RNG, class Src>
+__device__ int rollout_lin(const LinPlant& L, const CellConst& p, const double* x0, double v,
+                           const Src& src, int32_t& steps) {
+    double x[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = x0[i];
+    if (!in_bounds(lin_output<N>(L, x, v), p.ylo, p.yhi)) {
+        steps = 0;
+        return kViolated;
+    }
+    for (int32_t j = 0; j < p.j_star; ++j) {
+        double d[N];
+        if constexpr (RNG) {
+            src.step(j, d);
+        } else {
+#pragma unroll
+            for (int i = 0; i < N; ++i) d[i] = src.at(j, i);
+        }
+        double xn[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            double s = mul(L.B[i], v);
+#pragma unroll
+            for (int l = 0; l < N; ++l) s = add(s, mul(L.A[i * N + l], x[l]));
+            xn[i] = add(s, d[i]);
+        }
+        bool ok = true;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            x[i] = xn[i];
+            ok = ok && fabs(x[i]) <= kStateLimit;
+        }
+        if (!ok) {
+            steps = j + 1;
+            return kOverflow;
+        }
+        if (!in_bounds(lin_output<N>(L, x, v), p.ylo, p.yhi)) {
+            steps = j + 1;
+            return kViolated;
+        }
+    }
+    steps = p.j_star;
+    return kOk;
+}
+
 // governor.py:151-159: exact at both endpoints, three roundings otherwise.
 RG_HD double update_setpoint(double v_prev, double r, double kappa) {
     if (kappa == 0.0) return v_prev;

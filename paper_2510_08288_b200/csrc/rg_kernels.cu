@@ -491,6 +491,132 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_bisect(BisectArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// linear plant: parity fill and exact Alg. 2
+// ---------------------------------------------------------------------------
+
+__global__ void k_gen_soa_w(uint64_t hs, double4 lo4, double4 span4, int width, int64_t k0,
+                            int64_t n_sim, int32_t j_star, int64_t ld, double* __restrict__ dst) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int32_t j = blockIdx.y;
+    if (k >= n_sim || j >= j_star) return;
+    const double lo[4] = {lo4.x, lo4.y, lo4.z, lo4.w};
+    const double span[4] = {span4.x, span4.y, span4.z, span4.w};
+    const uint64_t K = splitmix64(hs ^ (uint64_t)(k0 + k));
+    const uint64_t J = splitmix64(K ^ (uint64_t)j);
+    for (int i = 0; i < width; ++i)
+        dst[((int64_t)j * width + i) * ld + k] =
+            add(lo[i], mul(span[i], unit_double(splitmix64(J ^ (uint64_t)i))));
+}
+
+template <int N>
+__device__ __forceinline__ int lin_cell(const LinArgs& a, const CellConst& c, int64_t k, double v,
+                                        int32_t& steps) {
+    if (a.soa) {
+        LinSoaSource<N> src{a.soa + k, a.ld};
+        return rollout_lin<N, false>(a.L, c, a.x0, v, src, steps);
+    }
+    LinRngSource<N> src;
+    src.K = splitmix64(a.hs ^ (uint64_t)(a.k0 + k));
+    for (int i = 0; i < 4; ++i) {
+        src.lo[i] = a.lo[i];
+        src.span[i] = a.span[i];
+    }
+    return rollout_lin<N, true>(a.L, c, a.x0, v, src, steps);
+}
+
+template <int N>
+__global__ void __launch_bounds__(128) k_fill_lin(LinArgs a) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= a.n_sim) return;
+    const int32_t row = a.rows[blockIdx.y];
+    int32_t steps = 0;
+    const int st = lin_cell<N>(a, make_cell(a.p), k, a.v_rows[row], steps);
+    a.S[(int64_t)row * a.n_sim + k] = (uint8_t)st;
+    a.steps[(int64_t)row * a.n_sim + k] = steps;
+}
+
+template <int N>
+__global__ void __launch_bounds__(128) k_bisect_lin(LinArgs a) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = k < a.n_sim;
+    double kopt = 1.0;
+    int found = 1, cells = 0, early = 0;
+    if (live) {
+        const CellConst c = make_cell(a.p);
+        double klo = 0.0, khi = 1.0;
+        kopt = 0.0;
+        found = 0;
+        for (int it = -1; it < a.n_kappa; ++it) {
+            const double kappa = it < 0 ? 1.0 : mul(0.5, add(klo, khi));
+            const double v = update_setpoint(a.v_prev, a.r, kappa);
+            bool ok = false;
+            int32_t sr = 0;
+            const double yss = mul(a.L.gain, v);  // LinearOraclePlant.steady_state_output
+            if (a.L.tlo <= yss && yss <= a.L.thi) ok = lin_cell<N>(a, c, k, v, sr) == kOk;
+            cells += 1;
+            if (sr < a.p.j_star && !ok) early += 1;
+            if (it < 0) {
+                if (ok) {
+                    kopt = 1.0;
+                    found = 1;
+                    break;
+                }
+                continue;
+            }
+            if (ok) {
+                kopt = kappa;
+                found = 1;
+                klo = kappa;
+            } else {
+                khi = kappa;
+            }
+        }
+        if (a.kappa_k) {
+            a.kappa_k[k] = kopt;
+            a.found_k[k] = found;
+            a.cells_k[k] = cells;
+            a.early_k[k] = early;
+        }
+    }
+    unsigned long long kb = (unsigned long long)__double_as_longlong(kopt);
+    int all_found = found;
+    long long sc = cells, se = early;
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long ob = __shfl_down_sync(0xffffffffu, kb, off);
+        kb = ob < kb ? ob : kb;
+        all_found &= __shfl_down_sync(0xffffffffu, all_found, off);
+        sc += __shfl_down_sync(0xffffffffu, sc, off);
+        se += __shfl_down_sync(0xffffffffu, se, off);
+    }
+    if (lane_id() == 0) {
+        atomicMin(&a.acc->kappa_bits, kb);
+        if (!all_found) atomicAnd(&a.acc->found, 0);
+        atomicAdd(&a.acc->cells, (unsigned long long)sc);
+        atomicAdd(&a.acc->early, (unsigned long long)se);
+    }
+    __shared__ bool s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&a.acc->ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    __threadfence();
+    volatile BisectAcc* acc = a.acc;
+    a.out->kappa = __longlong_as_double((long long)acc->kappa_bits);
+    a.out->found = acc->found;
+    a.out->cells = (long long)acc->cells;
+    a.out->early = (long long)acc->early;
+    a.out->seq += 1;
+    acc->kappa_bits = 0x3ff0000000000000ull;
+    acc->found = 1;
+    acc->cells = 0ull;
+    acc->early = 0ull;
+    acc->ticket = 0u;
+}
+
+// ---------------------------------------------------------------------------
 // tanh self-test
 // ---------------------------------------------------------------------------
 
@@ -640,6 +766,41 @@ cudaError_t launch_tanh(const double* x, double* y, int64_t n, bool fma, bool lo
         if (fma) k_tanh<true><<<blocks_for(n, 256), 256, 0, s>>>(x, y, n);
         else     k_tanh<false><<<blocks_for(n, 256), 256, 0, s>>>(x, y, n);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_lin(const LinArgs& a, cudaStream_t s) {
+    if (a.n_rows == 0 || a.n_sim == 0) return cudaSuccess;
+    dim3 grid(blocks_for(a.n_sim, a.tpb), (unsigned)a.n_rows);
+    switch (a.L.n) {
+        case 1: k_fill_lin<1><<<grid, a.tpb, 0, s>>>(a); break;
+        case 2: k_fill_lin<2><<<grid, a.tpb, 0, s>>>(a); break;
+        case 3: k_fill_lin<3><<<grid, a.tpb, 0, s>>>(a); break;
+        default: k_fill_lin<4><<<grid, a.tpb, 0, s>>>(a); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bisect_lin(const LinArgs& a, cudaStream_t s) {
+    const unsigned g = blocks_for(a.n_sim, a.tpb);
+    switch (a.L.n) {
+        case 1: k_bisect_lin<1><<<g, a.tpb, 0, s>>>(a); break;
+        case 2: k_bisect_lin<2><<<g, a.tpb, 0, s>>>(a); break;
+        case 3: k_bisect_lin<3><<<g, a.tpb, 0, s>>>(a); break;
+        default: k_bisect_lin<4><<<g, a.tpb, 0, s>>>(a); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gen_soa_w(uint64_t hs, const double* lo, const double* span, int width,
+                             int64_t k0, int64_t n_sim, int32_t j_star, int64_t ld, double* dst,
+                             cudaStream_t s) {
+    double4 l4 = make_double4(lo[0], width > 1 ? lo[1] : 0, width > 2 ? lo[2] : 0,
+                              width > 3 ? lo[3] : 0);
+    double4 s4 = make_double4(span[0], width > 1 ? span[1] : 0, width > 2 ? span[2] : 0,
+                              width > 3 ? span[3] : 0);
+    dim3 grid(blocks_for(n_sim, 128), (unsigned)j_star);
+    k_gen_soa_w<<<grid, 128, 0, s>>>(hs, l4, s4, width, k0, n_sim, j_star, ld, dst);
     return cudaGetLastError();
 }
 

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "rg_cell.cuh"
 #include "rg_rng.cuh"
 
 namespace rg {
@@ -93,6 +94,32 @@ struct BatchArgs {
     int tpb;
 };
 
+// Linear-plant fill and bisection (kernels.py:90-118 behind governor.py).
+struct LinArgs {
+    LinPlant L;
+    ProblemDev p;           // j_star, y bounds (the setpoint interval fields are unused)
+    double x0[4];
+    int64_t n_sim, k0;
+    uint64_t hs;            // RNG source: splitmix64(seed), lo/span in L-independent arrays
+    double lo[4], span[4];
+    const double* soa;      // staged source d[(j*n+i)*ld + k], or null for the RNG
+    int64_t ld;
+    // fill
+    const double* v_rows;
+    const int32_t* rows;
+    int32_t n_rows;
+    uint8_t* S;
+    int32_t* steps;
+    // bisection
+    double v_prev, r;
+    int32_t n_kappa;
+    double* kappa_k;
+    int32_t *found_k, *cells_k, *early_k;
+    struct BisectAcc* acc;
+    struct BisectOut* out;
+    int tpb;
+};
+
 struct BisectAcc {
     unsigned long long kappa_bits;  // min over scenarios (as bits; kappa >= 0)
     int found;                      // AND
@@ -135,6 +162,11 @@ cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, int lp
                         cudaStream_t s);
 cudaError_t launch_grid_batch(const BatchArgs& a, bool fma, bool poll, int lpc, cudaStream_t s);
 cudaError_t launch_bisect(const BisectArgs& a, bool fma, int src, int lpc, cudaStream_t s);
+cudaError_t launch_fill_lin(const LinArgs& a, cudaStream_t s);
+cudaError_t launch_bisect_lin(const LinArgs& a, cudaStream_t s);
+cudaError_t launch_gen_soa_w(uint64_t hs, const double* lo, const double* span, int width,
+                             int64_t k0, int64_t n_sim, int32_t j_star, int64_t ld, double* dst,
+                             cudaStream_t s);
 cudaError_t launch_tanh(const double* x, double* y, int64_t n, bool fma, bool lockstep,
                         cudaStream_t s);
 cudaError_t launch_gen_soa(const ScenarioStream& st, int64_t k0, int64_t n_sim, int32_t j_star,

@@ -183,19 +183,30 @@ def _tightened(cset, eps: float, mode: str) -> ConstraintSet:
     raise ConfigError(f"tighten_mode must be scale or margin, got {mode!r}")
 
 
-def _require_device_plant(plant) -> None:
-    if getattr(plant, "kernel_kind", None) != "surrogate-fc":
+_DEVICE_KINDS = ("surrogate-fc", "linear")
+
+
+def _require_device_plant(plant) -> str:
+    kind = getattr(plant, "kernel_kind", None)
+    if kind not in _DEVICE_KINDS:
         raise BackendUnavailableError(
-            "the device kernels are specialised to the surrogate fuel-cell plant; "
-            f"got plant kernel kind {getattr(plant, 'kernel_kind', None)!r}")
+            "the device kernels cover the surrogate fuel-cell plant and linear plants; "
+            f"got plant kernel kind {kind!r}")
+    return kind
+
+
+def _require_surrogate(plant) -> None:
+    if _require_device_plant(plant) != "surrogate-fc":
+        raise BackendUnavailableError("this entry point is specialised to the surrogate plant")
 
 
 def _validate_state(plant, x) -> np.ndarray:
     if hasattr(plant, "validate_state"):
         return plant.validate_state(x)
+    n = int(getattr(plant, "state_dim", 3))
     x = np.asarray(x, dtype=np.float64)
-    if x.shape != (3,) or not np.all(np.isfinite(x)):
-        raise ConfigError("state must be a finite vector of shape (3,)")
+    if x.shape != (n,) or not np.all(np.isfinite(x)):
+        raise ConfigError(f"state must be a finite vector of shape ({n},)")
     return x
 
 
@@ -205,14 +216,14 @@ def _problem(plant, cset, tight, j_star: int) -> _capi.Problem:
                          v_hi, int(j_star), 0)
 
 
-def _source(scenarios, j_star: int):
+def _source(scenarios, j_star: int, n_states: int = 3):
     """(dense tensor | None, n_sim, RNG stream | None) for the kernels.
 
     Mirrors _scenario_tensor (governor.py:169-179) for the shape checks.
     """
     if isinstance(scenarios, ScenarioSet) and scenarios.is_generated:
-        if scenarios.state_dim != 3:
-            raise ConfigError(f"scenarios must be (n_sim, horizon, 3), got state dim "
+        if scenarios.state_dim != n_states:
+            raise ConfigError(f"scenarios must be (n_sim, horizon, {n_states}), got state dim "
                               f"{scenarios.state_dim}")
         if scenarios.horizon < j_star + 1:
             raise ConfigError(f"scenario horizon {scenarios.horizon} too short: need >= "
@@ -224,8 +235,8 @@ def _source(scenarios, j_star: int):
         return None, scenarios.n_sim, scenarios._stream
     data = scenarios.data if hasattr(scenarios, "data") else np.asarray(scenarios)
     data = np.asarray(data)
-    if data.ndim != 3 or data.shape[2] != 3:
-        raise ConfigError(f"scenarios must be (n_sim, horizon, 3), got {data.shape}")
+    if data.ndim != 3 or data.shape[2] != n_states:
+        raise ConfigError(f"scenarios must be (n_sim, horizon, {n_states}), got {data.shape}")
     if data.shape[1] < j_star + 1:
         raise ConfigError(f"scenario horizon {data.shape[1]} too short: need >= "
                           f"j_star+1 = {j_star + 1}")
@@ -234,7 +245,7 @@ def _source(scenarios, j_star: int):
     return np.ascontiguousarray(data, dtype=np.float64), data.shape[0], None
 
 
-def _host_rows(v_prev: float, r: float, grid, interval):
+def _host_rows(v_prev: float, r: float, grid, interval, gate=None):
     """v per row, the steady-state gate and the dedup map (governor.py:286, 302-317).
 
     The reference's own loop in Python floats (same three roundings as
@@ -243,10 +254,13 @@ def _host_rows(v_prev: float, r: float, grid, interval):
     for every double -- and duplicates mapped to the first equal row through a
     dict, exactly as governor.py:306-317.  Returns Python lists.
     """
-    lo, hi = interval
     d = r - v_prev
     v_rows = [v_prev if k == 0.0 else (r if k == 1.0 else v_prev + k * d) for k in grid]
-    ss_ok = [lo <= v <= hi for v in v_rows]
+    if gate is None:
+        lo, hi = interval
+        ss_ok = [lo <= v <= hi for v in v_rows]
+    else:
+        ss_ok = [gate(v) for v in v_rows]
     first: dict = {}
     dup_src = [-1] * len(v_rows)
     reps = []
@@ -302,14 +316,18 @@ def fill_feasibility(backend, plant, x0, v_prev, r_t, grid, scenarios, cset, eps
         validate_epsilon(eps)
     if j_star < 1:
         raise ConfigError(f"j_star must be >= 1, got {j_star}")
-    _require_device_plant(plant)
-    dist, n_sim, stream = _source(scenarios, j_star)
+    kind = _require_device_plant(plant)
+    dist, n_sim, stream = _source(scenarios, j_star, int(plant.state_dim))
     tight = _tightened(cset, eps, tighten_mode)
 
     t0 = time.perf_counter()
-    prob, interval, _, _ = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor, eps,
-                                     tighten_mode, j_star, 0)
-    v_rows, ss_ok, dup_src, rows = _host_rows(float(v_prev), float(r_t), grid.tolist(), interval)
+    prob, interval, _, _ = _prepared(plant.step_size if kind == "surrogate-fc" else 1.0,
+                                     cset.lower, cset.upper, cset.anchor, eps, tighten_mode,
+                                     j_star, 0)
+    gate = None if kind == "surrogate-fc" else (
+        lambda v: tight.contains(plant.steady_state_output(v)))  # dc_gain * v (dynamics.py:199)
+    v_rows, ss_ok, dup_src, rows = _host_rows(float(v_prev), float(r_t), grid.tolist(), interval,
+                                              gate)
     v_rows = np.array(v_rows)
     ss_ok = np.array(ss_ok, dtype=bool)
     dup_src = np.array(dup_src, dtype=np.int64)
@@ -318,7 +336,11 @@ def fill_feasibility(backend, plant, x0, v_prev, r_t, grid, scenarios, cset, eps
     S = np.zeros((m, n_sim), dtype=np.uint8)
     steps = np.zeros((m, n_sim), dtype=np.int32)
     ctx = _capi.context(device)
-    ctx.fill(prob, x0, v_rows, rows, dist, n_sim, stream, S, steps)
+    if kind == "surrogate-fc":
+        ctx.fill(prob, x0, v_rows, rows, dist, n_sim, stream, S, steps)
+    else:
+        lin = _capi.make_linear(plant, tight.lower, tight.upper)
+        ctx.fill_linear(lin, prob, x0, v_rows, rows, dist, n_sim, stream, S, steps)
     for i in np.flatnonzero(dup_src >= 0):
         S[i] = S[dup_src[i]]
         steps[i] = steps[dup_src[i]]
@@ -341,12 +363,37 @@ def fill_feasibility(backend, plant, x0, v_prev, r_t, grid, scenarios, cset, eps
 # Alg. 3: robust grid step
 # ---------------------------------------------------------------------------
 
+def _robust_rg_parallel_via_fill(plant, x_t, state, r_t, cset, scenarios, config, backend):
+    """governor.py:520-579 literally: fill the matrix, extract on the host (linear plants)."""
+    grid = grid_kappas(config.m_grid)
+    stats: dict = {}
+    t0 = time.perf_counter()
+    P = fill_feasibility(backend, plant, x_t, state.v_prev, r_t, grid, scenarios, cset,
+                         config.epsilon, config.j_star, stats=stats,
+                         tighten_mode=config.tighten_mode, device=getattr(config, "device", 0))
+    row, _ = extract_kappa_opt(P, prefix_mode=config.prefix_mode)
+    stats["wall_us"] = int((time.perf_counter() - t0) * 1e6)
+    stats["method"] = "parallel-grid"
+    if row is None:
+        if config.infeasible_policy == "error":
+            raise InfeasibleError("no candidate feasible, including kappa=0 (hold current "
+                                  "setpoint)")
+        return KappaResult(kappa_opt=0.0, v_applied=state.v_prev, feasible=False,
+                           diagnostics=stats, matrix=P)
+    kappa = float(grid[row - 1])
+    v = update_setpoint(state.v_prev, r_t, kappa)
+    state.v_prev = v
+    return KappaResult(kappa_opt=kappa, v_applied=v, feasible=True, diagnostics=stats, matrix=P)
+
+
 def robust_rg_parallel(plant, x_t, state, r_t, cset, scenarios, config, backend=None):
     """Scenario-robust governor step by grid search (governor.py:520-579)."""
     x_t = _validate_state(plant, x_t)
     backend = backend or config.backend
     _backend_check(backend)
-    _require_device_plant(plant)
+    if _require_device_plant(plant) == "linear":
+        return _robust_rg_parallel_via_fill(plant, x_t, state, r_t, cset, scenarios, config,
+                                            backend)
     if config.tighten_mode == "scale":
         validate_epsilon(config.epsilon)
     prob, interval, grid, grid_list = _prepared(plant.step_size, cset.lower, cset.upper,
@@ -406,7 +453,7 @@ def robust_rg_parallel_batch(plant, X, v_prev, r, cset, model, n_sim, seeds, con
     each equal to the single-episode call's result.  Rows already known to be
     infeasible stop early (verdicts are unaffected).
     """
-    _require_device_plant(plant)
+    _require_surrogate(plant)
     if config.tighten_mode == "scale":
         validate_epsilon(config.epsilon)
     X = np.ascontiguousarray(X, dtype=np.float64).reshape(-1, 3)
@@ -427,9 +474,17 @@ def robust_rg_parallel_batch(plant, X, v_prev, r, cset, model, n_sim, seeds, con
 # ---------------------------------------------------------------------------
 
 def _bisect_call(plant, x_t, state, r_t, cset, config, dist, n_sim, stream):
-    prob, _, _, _ = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor,
-                              config.epsilon, config.tighten_mode, config.j_star, 0)
+    kind = _require_device_plant(plant)
+    prob, _, _, _ = _prepared(plant.step_size if kind == "surrogate-fc" else 1.0, cset.lower,
+                              cset.upper, cset.anchor, config.epsilon, config.tighten_mode,
+                              config.j_star, 0)
     ctx = _capi.context(getattr(config, "device", 0))
+    if kind == "linear":
+        tight = _tightened(cset, config.epsilon, config.tighten_mode)
+        lin = _capi.make_linear(plant, tight.lower, tight.upper)
+        res, _ = ctx.bisect_linear(lin, prob, x_t, state.v_prev, r_t, config.n_kappa, dist,
+                                   n_sim, stream)
+        return res
     res, _, _ = ctx.bisect(prob, x_t, state.v_prev, r_t, config.n_kappa, dist, n_sim, stream)
     return res
 
@@ -456,7 +511,7 @@ def robust_rg_sequential(plant, x_t, state, r_t, cset, scenarios, config):
         raise ConfigError(f"scenario count {scenarios.n_sim} does not match config.n_sim "
                           f"{config.n_sim}")
     _require_device_plant(plant)
-    dist, n_sim, stream = _source(scenarios, config.j_star)
+    dist, n_sim, stream = _source(scenarios, config.j_star, int(plant.state_dim))
     t0 = time.perf_counter()
     res = _bisect_call(plant, x_t, state, r_t, cset, config, dist, n_sim, stream)
     kappa = float(res.kappa)
@@ -475,7 +530,7 @@ def bisect_paths(plant, x_t, v_prev, r_t, cset, scenarios, config):
     path slots are NaN / 255.
     """
     x_t = _validate_state(plant, x_t)
-    _require_device_plant(plant)
+    _require_surrogate(plant)
     dist, n_sim, stream = _source(scenarios, config.j_star)
     tight = _tightened(cset, config.epsilon, config.tighten_mode)
     ctx = _capi.context(getattr(config, "device", 0))
@@ -492,21 +547,27 @@ def bisect_paths(plant, x_t, v_prev, r_t, cset, scenarios, config):
 def probe_candidate(plant, x0, v, scenario, cset, eps, j_star, tighten_mode="scale",
                     device: int = 0) -> CellProbe:
     x0 = _validate_state(plant, x0)
+    n = int(plant.state_dim)
     scenario = np.asarray(scenario, dtype=np.float64)
-    if scenario.ndim != 2 or scenario.shape[1] != 3:
-        raise ConfigError(f"scenario must be 2-D with 3 columns, got {scenario.shape}")
+    if scenario.ndim != 2 or scenario.shape[1] != n:
+        raise ConfigError(f"scenario must be 2-D with {n} columns, got {scenario.shape}")
     if scenario.shape[0] < j_star + 1:
         raise ConfigError(f"scenario length {scenario.shape[0]} too short: need >= "
                           f"{j_star + 1}")
-    _require_device_plant(plant)
+    kind = _require_device_plant(plant)
     tight = _tightened(cset, eps, tighten_mode)
     if not tight.contains(plant.steady_state_output(v)):
         return CellProbe(False, False, CELL_VIOLATED, 0, None)
     S = np.zeros((1, 1), dtype=np.uint8)
     steps = np.zeros((1, 1), dtype=np.int32)
     ctx = _capi.context(device)
-    ctx.fill(_problem(plant, cset, tight, j_star), x0, np.array([float(v)]),
-             np.array([0], np.int32), scenario[None], 1, None, S, steps)
+    prob, _, _, _ = _prepared(plant.step_size if kind == "surrogate-fc" else 1.0, cset.lower,
+                              cset.upper, cset.anchor, eps, tighten_mode, j_star, 0)
+    args = (x0, np.array([float(v)]), np.array([0], np.int32), scenario[None], 1, None, S, steps)
+    if kind == "linear":
+        ctx.fill_linear(_capi.make_linear(plant, tight.lower, tight.upper), prob, *args)
+    else:
+        ctx.fill(prob, *args)
     st, sr = int(S[0, 0]), int(steps[0, 0])
     ok = st == CELL_OK
     return CellProbe(ok, True, st, sr, None if ok else sr)

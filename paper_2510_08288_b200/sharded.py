@@ -23,8 +23,9 @@ import numpy as np
 
 from . import _capi
 from .errors import InfeasibleError
-from .governor import (KappaResult, _prepared, _source, _validate_state, _require_device_plant,
-                       _host_rows, update_setpoint)
+from .governor import (KappaResult, _prepared, _source, _validate_state, _host_rows,
+                       update_setpoint)
+from .governor import _require_surrogate as _require_device_plant
 
 __all__ = ["PRUNED", "global_row_counts", "extract_row", "robust_rg_parallel_sharded",
            "robust_rg_sequential_sharded", "combine_bisection"]

@@ -70,6 +70,22 @@ def bis_case(golden, idx):
     )
 
 
+def lin_case(golden, idx):
+    pre = f"lin_{idx}_"
+    s = golden[pre + "scalars"]
+    A = golden[pre + "A"]
+    n = A.shape[0]
+    bcd = golden[pre + "BCD"]
+    return dict(name=str(golden["lin_names"][idx]), A=A, B=bcd[:n], C=bcd[n:2 * n],
+                D=float(bcd[2 * n]), gain=float(bcd[2 * n + 1]), x0=golden[pre + "x0"],
+                v_prev=float(s[0]), r=float(s[1]), eps=float(s[2]), lower=float(s[3]),
+                upper=float(s[4]), anchor=float(s[5]), j_star=int(s[6]), m_grid=int(s[7]),
+                n_sim=int(s[8]), mag=float(s[9]), seed=int(golden[pre + "seed"][0]),
+                S_all=golden[pre + "S_all"], steps_all=golden[pre + "steps_all"],
+                P=golden[pre + "P"], stats=golden[pre + "stats"],
+                results=golden[pre + "results"])
+
+
 def n_fill_cases(golden):
     return len(golden["fill_names"])
 

@@ -230,6 +230,82 @@ nb = bisection_rg(plant, np.zeros(3), GovernorState(0.0), 2.5, box, GovernorConf
 put("nominal_anchor", np.array([nb.kappa_opt, nb.v_applied, float(nb.feasible),
                                 nb.diagnostics["sims_run"], nb.diagnostics["early_terms"]]))
 
+# ---------------------------------------------------------------- linear plant
+# kernels.py:90-118 (_cell_lin) behind the same governors; shapes from the
+# reference's oracle suite (oracle.py:201-232: n in 1..3, stable A, |dc gain| >= 0.2)
+from refgov import LinearOraclePlant, linear_maximal_kappa
+lin_cases = []
+
+
+def add_linear(name, A, B, C, D, x0, v_prev, r, m_grid, n_sim, j_star, eps, mag, seed, cset):
+    lp = LinearOraclePlant(A, B, C, D)
+    n = lp.state_dim
+    model = DisturbanceModel.scaled(mag, n)
+    scen = sample_scenarios(model, n_sim, j_star + 1, seed=seed)
+    x0 = np.asarray(x0, dtype=np.float64)
+    grid = G.grid_kappas(m_grid)
+    v_rows = np.array([update_setpoint(v_prev, r, float(k)) for k in grid])
+    S = np.zeros((m_grid, n_sim), dtype=np.uint8)
+    steps = np.zeros((m_grid, n_sim), dtype=np.int32)
+    K.run_cells(lp, x0, v_rows, np.arange(m_grid), scen.data, j_star, cset.lower, cset.upper,
+                S, steps, mode="serial")
+    stats = {}
+    P = G.fill_feasibility("serial", lp, x0, v_prev, r, grid, scen, cset, eps, j_star,
+                           stats=stats)
+    cfg = GovernorConfig(j_star=j_star, epsilon=eps, m_grid=m_grid, n_sim=n_sim)
+    par = robust_rg_parallel(lp, x0, GovernorState(v_prev), r, cset, scen, cfg)
+    seq = robust_rg_sequential(lp, x0, GovernorState(v_prev), r, cset, scen, cfg)
+    nom = bisection_rg(lp, x0, GovernorState(v_prev), r, cset, cfg)
+    pre = f"lin_{len(lin_cases)}_"
+    lin_cases.append(name)
+    put(pre + "A", lp.A)
+    put(pre + "BCD", np.concatenate([lp.B, lp.C, [lp.D, lp.dc_gain]]))
+    put(pre + "x0", x0)
+    put(pre + "scalars", np.array([v_prev, r, eps, cset.lower, cset.upper, cset.anchor,
+                                   float(j_star), float(m_grid), float(n_sim), mag]))
+    put(pre + "seed", np.array([seed], dtype=np.uint64))
+    put(pre + "S_all", S)
+    put(pre + "steps_all", steps)
+    put(pre + "P", P)
+    put(pre + "stats", np.array([stats["sims_run"], stats["early_terms"], stats["overflows"],
+                                 stats["ss_pruned_rows"], stats["dedup_rows"]]))
+    put(pre + "results", np.array([
+        par.kappa_opt, par.v_applied, float(par.feasible),
+        seq.kappa_opt, seq.v_applied, float(seq.feasible), seq.diagnostics["sims_run"],
+        seq.diagnostics["early_terms"],
+        nom.kappa_opt, nom.v_applied, float(nom.feasible), nom.diagnostics["sims_run"],
+        nom.diagnostics["early_terms"]]))
+
+
+lbox = ConstraintSet(-0.9, 0.9)
+# the reference's own known answer: kappa* = 0.81 (tests/test_oracle.py:27-34)
+add_linear("scalar_kappa081", [[0.5]], [0.5], [1.0], 0.0, [0.0], 0.0, 1.0, 32, 8, 256, 0.1,
+           1e-4, 1, lbox)
+add_linear("two_state", [[0.85, 0.1], [0.0, 0.7]], [0.0, 0.3], [1.0, 0.0], 0.0, [0.0, 0.0],
+           0.1, 1.0, 16, 24, 64, 0.1, 0.005, 4, lbox)
+lrng = np.random.default_rng(424242)
+for trial in range(6):
+    while True:
+        n = int(lrng.integers(1, 4))
+        A = lrng.uniform(-1.0, 1.0, size=(n, n))
+        rho = float(np.max(np.abs(np.linalg.eigvals(A))))
+        if rho > 1e-12:
+            A *= lrng.uniform(0.3, 0.95) / rho
+        B = lrng.uniform(-1.0, 1.0, size=n)
+        C = lrng.uniform(-1.0, 1.0, size=n)
+        if abs(LinearOraclePlant(A, B, C).dc_gain) >= 0.2:
+            break
+    add_linear(f"random_{trial}_n{n}", A, B, C, float(lrng.uniform(-0.2, 0.2)),
+               lrng.uniform(-0.3, 0.3, size=n), float(lrng.uniform(-0.5, 0.5)),
+               float(lrng.uniform(-3, 3)), 32, 32, 128, 0.1, 0.01, 100 + trial,
+               ConstraintSet(-1.0, 1.0))
+add_linear("overflow_big_dist", [[0.9, 0.0, 0.0], [0.1, 0.5, 0.0], [0.0, 0.2, 0.3]],
+           [1.0, 0.0, 0.0], [0.0, 0.0, 1.0], 0.0, [0.0, 0.0, 0.0], 0.0, 0.5, 8, 16, 16, 0.1,
+           2e6, 9, ConstraintSet(-np.inf, 0.9))
+put("lin_names", np.array(lin_cases))
+put("lin_kappa_star_081", np.array([linear_maximal_kappa([[0.5]], [0.5], [1.0], np.zeros(1),
+                                                          0.0, 1.0, lbox, 0.1, 256)]))
+
 # ---------------------------------------------------------------- closed loops
 setup = load_config({})
 tight = tighten(setup.cset, setup.epsilon)

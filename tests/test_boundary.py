@@ -35,7 +35,8 @@ def test_library_exports_every_declared_symbol():
 def test_struct_layouts_match_header():
     # sizes of the C structs, computed from their field lists in the header
     assert ctypes.sizeof(_capi.Problem) == 5 * 8 + 2 * 4
-    assert ctypes.sizeof(_capi.Scenarios) == 8 * 3 + 6 * 8
+    assert ctypes.sizeof(_capi.Scenarios) == 8 * 3 + 8 * 8
+    assert ctypes.sizeof(_capi.LinearPlant) == 8 + 8 * (16 + 4 + 4 + 4)
     assert ctypes.sizeof(_capi.GridResult) == 4 * 4 + 4 * 8 + 4 + 4
     assert ctypes.sizeof(_capi.BisectResult) == 8 + 4 + 4 + 8 + 8 + 4 + 4
 

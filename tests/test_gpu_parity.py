@@ -240,9 +240,11 @@ def test_errors_map_to_reference_types():
     with pytest.raises(rg.ConfigError):   # non-finite state
         rg.robust_rg_parallel(PLANT, np.array([np.nan, 0, 0]), rg.GovernorState(), 1.0, box,
                               rg.zero_scenarios(3, 65), cfg)
-    lin = rg.LinearOraclePlant([[0.5]], [0.5], [1.0])
+    class OtherPlant(rg.Plant):   # neither the surrogate nor a linear plant
+        kernel_kind = None
+        state_dim = 1
     with pytest.raises(rg.BackendUnavailableError):  # backend_gpu.py:66-71
-        rg.fill_feasibility("cuda", lin, np.zeros(1), 0.0, 1.0, rg.grid_kappas(4),
+        rg.fill_feasibility("cuda", OtherPlant(), np.zeros(1), 0.0, 1.0, rg.grid_kappas(4),
                             rg.ScenarioSet(np.zeros((1, 33, 1))), box, 0.05, 32)
     with pytest.raises(rg.ConfigError):
         rg.fill_feasibility("serial", PLANT, np.zeros(3), 0.0, 1.0, rg.grid_kappas(4),

@@ -12,7 +12,7 @@ import hashlib
 import numpy as np
 import pytest
 
-from conftest import GOLDEN, bis_case, fill_case
+from conftest import GOLDEN, bis_case, fill_case, lin_case
 
 with np.load(GOLDEN) as _z:
     N_FILL = len(_z["fill_names"])
@@ -145,3 +145,36 @@ def test_closed_loop_desk_grid_trace(orc, golden):
     assert not aborted
     got = np.array([[r[2], r[3], r[4], float(r[5])] for r in rows])
     assert np.array_equal(got, golden["desk_grid_trace"])
+
+
+with np.load(GOLDEN) as _z:
+    N_LIN = len(_z["lin_names"])
+
+
+@pytest.mark.parametrize("idx", range(N_LIN))
+def test_linear_cells_and_governors_match_reference(orc, golden, idx):
+    c = lin_case(golden, idx)
+    n = c["A"].shape[0]
+    dist = orc.sample(c["seed"], c["n_sim"], c["j_star"] + 1, [(-c["mag"], c["mag"])] * n)
+    grid = orc.grid_kappas(c["m_grid"])
+    for i, kappa in enumerate(grid):
+        v = orc.update_setpoint(c["v_prev"], c["r"], float(kappa))
+        for k in range(c["n_sim"]):
+            assert orc.cell_lin(c["A"], c["B"], c["C"], c["D"], c["x0"], v, dist[k],
+                                c["j_star"], c["lower"], c["upper"]) == \
+                (int(c["S_all"][i, k]), int(c["steps_all"][i, k])), (c["name"], i, k)
+    tlo, thi = orc.tighten(c["lower"], c["upper"], c["anchor"], c["eps"])
+    P, _, _ = orc.fill_feasibility_lin(c["A"], c["B"], c["C"], c["D"], c["gain"], c["x0"],
+                                       c["v_prev"], c["r"], grid, dist, c["lower"], c["upper"],
+                                       tlo, thi, c["j_star"])
+    assert np.array_equal(P, c["P"]), c["name"]
+    kap = [orc.bisect_kappa_lin(c["A"], c["B"], c["C"], c["D"], c["gain"], c["x0"],
+                                c["v_prev"], c["r"], c["lower"], c["upper"], tlo, thi, dist[k],
+                                c["j_star"], 8) for k in range(c["n_sim"])]
+    assert min(min(k[0] for k in kap), 1.0) == c["results"][3]
+    assert sum(k[2] for k in kap) == c["results"][6] and sum(k[3] for k in kap) == \
+        c["results"][7]
+
+
+def test_linear_known_answer(golden):
+    assert abs(float(golden["lin_kappa_star_081"][0]) - 0.81) < 1e-5
