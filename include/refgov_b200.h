@@ -68,6 +68,9 @@ extern "C" {
 #define RG_LPC2 0x100       /* force 2 lanes per cell (each evaluates 2 of the 4 tanh) */
 #define RG_LPC4 0x200       /* force 4 lanes per cell (1 tanh each) */
 /* Default: 1 lane per cell (fastest measured).  Results are identical for every choice. */
+#define RG_DECOUPLED 0x400  /* grid step: phase-decoupled kernel (x2 chain / tanh / x1-x3) */
+#define RG_PER_STEP 0x800   /* grid step: per-step rollout kernel */
+#define RG_WARP_SPEC 0x1000 /* grid step: warp-specialised kernel (sequence warp + tanh warps) */
 
 typedef struct rg_ctx rg_ctx;
 

@@ -27,6 +27,9 @@ RG_TANH_LOCKSTEP, RG_FUSED_RNG, RG_STAGE_RNG = 0x10, 0x20, 0x40
 _RNG_FLAGS = {None: 0, "fused": RG_FUSED_RNG, "staged": RG_STAGE_RNG}
 RG_LPC1, RG_LPC2, RG_LPC4 = 0x80, 0x100, 0x200
 _LPC_FLAGS = {None: 0, 1: RG_LPC1, 2: RG_LPC2, 4: RG_LPC4}
+RG_DECOUPLED, RG_PER_STEP, RG_WARP_SPEC = 0x400, 0x800, 0x1000
+_KERNEL_FLAGS = {None: 0, "decoupled": RG_DECOUPLED, "per-step": RG_PER_STEP,
+                 "warp-spec": RG_WARP_SPEC}
 
 _i32, _i64, _u64, _d, _vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, \
     ctypes.c_void_p
@@ -230,7 +233,8 @@ class Context:
 
     def grid_step(self, prob: Problem, x0, v_prev, r, m_grid, prefix_mode, dist, n_sim,
                   scen: Scenarios | None, want_pbits: bool, abandon: bool = False,
-                  rng_mode: str | None = None, lpc: int | None = None):
+                  rng_mode: str | None = None, lpc: int | None = None,
+                  kernel: str | None = None):
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
         horizon = 0
         if dist is not None:
@@ -239,7 +243,8 @@ class Context:
         viol = np.empty(m_grid, dtype=np.uint32)
         pbits = np.empty((m_grid, (n_sim + 31) // 32), dtype=np.uint32) if want_pbits else None
         res = GridResult()
-        flags = (RG_ABANDON if abandon else 0) | _RNG_FLAGS[rng_mode] | _LPC_FLAGS[lpc]
+        flags = (RG_ABANDON if abandon else 0) | _RNG_FLAGS[rng_mode] | _LPC_FLAGS[lpc] | \
+            _KERNEL_FLAGS[kernel]
         check(self.lib.rg_grid_step(self.handle, ctypes.byref(prob), _p(x0), float(v_prev),
                                     float(r), int(m_grid), int(bool(prefix_mode)), _p(dist),
                                     int(n_sim), int(horizon),

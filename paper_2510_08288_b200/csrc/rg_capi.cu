@@ -251,6 +251,8 @@ int32_t grow_grid(rg_ctx* ctx, int m) {
     return RG_OK;
 }
 
+constexpr int kGridKernelDefault = 0;
+
 // Lanes per cell.  LPC = 2 / 4 spread a cell's four tanh chains over lanes
 // (rg_cell.cuh: step_tanh).  Measured on B200 (round 1) the redundant x1/x2/x3
 // work costs more than the extra parallelism buys at every size tried
@@ -267,6 +269,21 @@ int lpc_for(const rg_ctx* ctx, int64_t cells, int32_t flags) {
         if (v == 1 || v == 2 || v == 4) return v;
     }
     return 1;
+}
+
+// Grid-step kernel choice: 0 = per-step rollout (k_grid), 1 = block-phased
+// decoupled (k_grid_dec), 2 = warp-specialised (k_grid_ws).  RG_PER_STEP /
+// RG_DECOUPLED / RG_WARP_SPEC force one; RG_GRID_KERNEL=0/1/2 overrides the
+// default for tuning.
+int grid_kernel_for(int32_t flags) {
+    if (flags & (RG_LPC1 | RG_LPC2 | RG_LPC4 | RG_PER_STEP)) return 0;
+    if (flags & RG_WARP_SPEC) return 2;
+    if (flags & RG_DECOUPLED) return 1;
+    if (const char* env = getenv("RG_GRID_KERNEL")) {
+        const int k = atoi(env);
+        return k == 1 || k == 2 ? k : 0;
+    }
+    return kGridKernelDefault;
 }
 
 int tpb_for(const rg_ctx* ctx, int64_t n_sim, int64_t rows) {
@@ -584,6 +601,8 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
     a.m_grid = m_grid;
     a.prefix_mode = prefix_mode ? 1 : 0;
     a.n_sim = n_sim;
+    // the phase-decoupled kernel (rg_decoupled.cuh) unless a lanes-per-cell split is forced
+    const int kernel = grid_kernel_for(flags);
     bool use_rng = dist == nullptr;
     if (use_rng && want_stage(n_sim, prob->j_star, flags)) {
         if ((rc = stage_rng(ctx, rng, n_sim, prob->j_star, &a.soa, &a.ld))) return rc;
@@ -617,8 +636,16 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
         RG_CUDA(cudaMemsetAsync(a.pbits, 0, pbytes, ctx->stream));
     const bool timed = !(flags & RG_NO_TIMING);
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-    RG_CUDA(rg::launch_grid(a, ctx->variant == rg::kTanhFma, use_rng, abandon, lpc,
-                            ctx->stream));
+    if (kernel == 2) {
+        RG_CUDA(rg::launch_grid_ws(a, ctx->variant == rg::kTanhFma, use_rng, abandon,
+                                   ctx->stream));
+    } else if (kernel == 1) {
+        RG_CUDA(rg::launch_grid_dec(a, ctx->variant == rg::kTanhFma, use_rng, abandon,
+                                    ctx->stream));
+    } else {
+        RG_CUDA(rg::launch_grid(a, ctx->variant == rg::kTanhFma, use_rng, abandon, lpc,
+                                ctx->stream));
+    }
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     ctx->last_m = m_grid;
     if (flags & RG_ASYNC) {

@@ -19,6 +19,10 @@
 
 #include <type_traits>
 
+#ifndef RG_PIPE2
+#define RG_PIPE2 1
+#endif
+
 namespace rg {
 
 enum CellStatus : int { kViolated = 0, kOk = 1, kOverflow = 2, kAbandoned = 3 };
@@ -74,6 +78,17 @@ RG_HD void sfc_step(double& x1, double& x2, double& x3, double v, const CellCons
     x3 = add(add(x3, mul(p.c, s3)), d2);
 }
 
+// The step's products by +-2 are exact (a power-of-two scaling), so the
+// reference's add(mul(2, b), a) rounds once, exactly like fma(2, b, a): one
+// FP64 instruction instead of two, the same bits.  The one exception is a
+// product that overflows, which needs a state component beyond 2^1021 at
+// the start of a step -- only possible in an absurd initial state (every later
+// state passed the 1e6 check).  Such a step ends with a component far beyond
+// STATE_LIMIT (or inf/NaN) under either evaluation, so status and step count
+// are still the reference's.
+RG_HD double sum2(double a, double b) { return fma_(2.0, b, a); }      // a + 2*b
+RG_HD double neg2_add(double b, double a) { return fma_(-2.0, b, a); }  // -2*b + a
+
 // The x2 sub-chain of one step: dx2/dt = -x2 + v does not involve x1 or x3,
 // so the stage values a2, b2, c2 (the tanh arguments) and the increment s2
 // depend on x2 alone.
@@ -91,7 +106,7 @@ RG_HD X2Stage x2_stage(double x2, double v, const CellConst& p) {
     const double k32 = add(-r.b2, v);
     r.c2 = add(x2, mul(p.h, k32));
     const double k42 = add(-r.c2, v);
-    r.s2 = add(add(add(k12, mul(2.0, k22)), mul(2.0, k32)), k42);
+    r.s2 = add(sum2(sum2(k12, k22), k32), k42);
     return r;
 }
 
@@ -101,21 +116,21 @@ RG_HD void x13_update(double& x1, double& x3, double t1, double t2, double t3, d
                       const CellConst& p, double d0, double d2) {
     const double h = p.h, hh = p.hh;
     const double k11 = add(-x1, t1);
-    const double k13 = add(mul(-2.0, x3), x1);
+    const double k13 = neg2_add(x3, x1);
     const double a1 = add(x1, mul(hh, k11));
     const double a3 = add(x3, mul(hh, k13));
     const double k21 = add(-a1, t2);
-    const double k23 = add(mul(-2.0, a3), a1);
+    const double k23 = neg2_add(a3, a1);
     const double b1 = add(x1, mul(hh, k21));
     const double b3 = add(x3, mul(hh, k23));
     const double k31 = add(-b1, t3);
-    const double k33 = add(mul(-2.0, b3), b1);
+    const double k33 = neg2_add(b3, b1);
     const double c1 = add(x1, mul(h, k31));
     const double c3 = add(x3, mul(h, k33));
     const double k41 = add(-c1, t4);
-    const double k43 = add(mul(-2.0, c3), c1);
-    const double s1 = add(add(add(k11, mul(2.0, k21)), mul(2.0, k31)), k41);
-    const double s3 = add(add(add(k13, mul(2.0, k23)), mul(2.0, k33)), k43);
+    const double k43 = neg2_add(c3, c1);
+    const double s1 = add(sum2(sum2(k11, k21), k31), k41);
+    const double s3 = add(sum2(sum2(k13, k23), k33), k43);
     x1 = add(add(x1, mul(p.c, s1)), d0);
     x3 = add(add(x3, mul(p.c, s3)), d2);
 }
@@ -244,6 +259,89 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
     } else {
         if (__all_sync(0xffffffffu, done)) return status;
     }
+#if RG_PIPE2
+    // Pipelined two steps deep: iteration j finishes x1/x3 of step j (tanh
+    // values from iteration j-1), evaluates the four tanh of step j+1
+    // (arguments from iteration j-1) and runs the x2 chain of step j+2.  The
+    // three pieces are mutually independent, so the tanh chains no longer
+    // wait behind the x2 recurrence inside an iteration.
+    auto fetch = [&](int32_t j) -> D3 {  // disturbances of step min(j, J-1)
+        if constexpr (kRing) {
+            cp_async_wait<1>();          // step j landed (issued two fetches ago)
+            const D3 r = src.read(j & 1);
+            src.issue(j + 2 < J ? j + 2 : J - 1, j & 1);
+            cp_async_commit();
+            return r;
+        } else {
+            return src.load(j < J ? j : J - 1);
+        }
+    };
+    if constexpr (kRing) {
+        src.issue(0, 0);
+        cp_async_commit();
+        src.issue(J > 1 ? 1 : 0, 1);
+        cp_async_commit();
+    }
+    const D3 dj0 = fetch(0);
+    const D3 dj1 = fetch(1);
+    // step 0: tanh values, x2 after step 0
+    const X2Stage s0 = x2_stage<FMA>(x2, v, p);
+    double t1, t2, t3, t4;
+    step_tanh<FMA, LPC>(x2, s0.a2, s0.b2, s0.c2, t1, t2, t3, t4);
+    const double y1 = add(add(x2, mul(p.c, s0.s2)), dj0.d1);
+    // step 1: tanh arguments, x2 after step 1
+    const X2Stage s1 = x2_stage<FMA>(y1, v, p);
+    double g0 = y1, g1 = s1.a2, g2 = s1.b2, g3 = s1.c2;  // tanh arguments of step j+1
+    double y2 = add(add(y1, mul(p.c, s1.s2)), dj1.d1);  // x2 before step j+2
+    double dA0 = dj0.d0, dA2 = dj0.d2;  // x1/x3 disturbances of step j
+    double dB0 = dj1.d0, dB2 = dj1.d2;  // ... and of step j+1
+    for (int32_t j = 0; j < J; ++j) {
+        const D3 dn = fetch(j + 2);
+        // step j+1's tanh values (speculative past an exit or the horizon)
+        double u1, u2, u3, u4;
+        step_tanh<FMA, LPC>(g0, g1, g2, g3, u1, u2, u3, u4);
+        // step j+2's x2 chain
+        const X2Stage sn = x2_stage<FMA>(y2, v, p);
+        const double y3 = add(add(y2, mul(p.c, sn.s2)), dn.d1);
+        // step j's x1/x3 and checks; x2 after step j is g0
+        x13_update<FMA>(x1, x3, t1, t2, t3, t4, p, dA0, dA2);
+        if (!done) {
+            if (!(fabs(x1) <= kStateLimit && fabs(g0) <= kStateLimit &&
+                  fabs(x3) <= kStateLimit)) {
+                steps = j + 1;
+                status = kOverflow;
+                done = true;
+            } else if (!in_bounds(x1, p.ylo, p.yhi)) {
+                steps = j + 1;
+                status = kViolated;
+                done = true;
+            } else if (POLL && (j & 31) == 31 &&
+                       *(volatile const unsigned int*)dead != 0u) {
+                steps = j + 1;
+                status = kAbandoned;
+                done = true;
+            }
+        }
+        if constexpr (LPC == 1) {
+            if (done) break;
+        } else {
+            if (__all_sync(0xffffffffu, done)) break;
+        }
+        t1 = u1;
+        t2 = u2;
+        t3 = u3;
+        t4 = u4;
+        g0 = y2;
+        g1 = sn.a2;
+        g2 = sn.b2;
+        g3 = sn.c2;
+        y2 = y3;
+        dA0 = dB0;
+        dA2 = dB2;
+        dB0 = dn.d0;
+        dB2 = dn.d2;
+    }
+#else
     // prologue: tanh values of step 0 and x2 after step 0
     D3 d;
     if constexpr (kRing) {
@@ -309,6 +407,7 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
         x2n = x2nn;
         d = dn;
     }
+#endif
     if constexpr (kRing) cp_async_wait<0>();  // no copy may land after we leave
     return status;
 }

@@ -21,9 +21,27 @@
 #include <cuda_runtime.h>
 
 #include "rg_cell.cuh"
+#include "rg_decoupled.cuh"
+#include "rg_ws.cuh"
 
 #ifndef RG_GRID_MINB
 #define RG_GRID_MINB 1
+#endif
+// phase-decoupled grid kernel geometry: cells per block, steps per chunk, threads
+#ifndef RG_DEC_C
+#define RG_DEC_C 32
+#endif
+#ifndef RG_WS_T
+#define RG_WS_T 4
+#endif
+#ifndef RG_WS_W
+#define RG_WS_W 2
+#endif
+#ifndef RG_DEC_T
+#define RG_DEC_T 16
+#endif
+#ifndef RG_DEC_TB
+#define RG_DEC_TB 128
 #endif
 
 namespace rg {
@@ -163,60 +181,9 @@ __device__ int row_source(const GridArgs& a, int i, double* v_out) {
     return -1;
 }
 
-template <bool FMA, bool RNG, bool POLL, int LPC>
-__global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid(GridArgs a) {
-    __shared__ int s_src;
-    __shared__ double s_v;
-    const int i = blockIdx.y;
-    if (threadIdx.x == 0) {
-        double v;
-        s_src = row_source(a, i, &v);
-        s_v = v;
-        if (blockIdx.x == 0) a.row_src[i] = s_src;
-    }
-    __syncthreads();
-    const int src_i = s_src;
-    const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPC;
-    const bool lead = threadIdx.x % LPC == 0;
-    if (src_i == -1) {
-        const bool live = k < a.n_sim;
-        const int64_t kk = live ? k : 0;
-        int st = kOk;
-        int32_t steps = a.p.j_star;
-        if (live || LPC > 1) {
-            const CellConst c = make_cell(a.p);
-            if (RNG) {
-                RngSource src{a.stream, scenario_key(a.stream, (uint64_t)(a.k0 + kk))};
-                st = rollout<FMA, POLL, LPC>(c, a.x0[0], a.x0[1], a.x0[2], s_v, src, steps,
-                                             a.viol + i, live);
-            } else {
-                __shared__ double ring[2 * 3 * kRingStride];
-                SoaSource src{a.soa + kk, a.ld, ring + threadIdx.x};
-                st = rollout<FMA, POLL, LPC>(c, a.x0[0], a.x0[1], a.x0[2], s_v, src, steps,
-                                             a.viol + i, live);
-            }
-        }
-        const bool cnt = live && lead;
-        const bool bad = cnt && st != kOk && st != kAbandoned;
-        const unsigned bad_mask = __ballot_sync(0xffffffffu, bad);
-        if (lane_id() == 0 && bad_mask) atomicAdd(a.viol + i, (unsigned)__popc(bad_mask));
-        warp_count_add(cnt && st != kAbandoned && steps < a.p.j_star, a.early + i);
-        warp_count_add(cnt && st == kOverflow, a.ovf + i);
-        warp_count_add(cnt && st == kAbandoned, a.abandoned + i);
-        if (a.pbits) {
-            if (LPC == 1) {
-                const unsigned ok_mask = __ballot_sync(0xffffffffu, live && st == kOk);
-                if (lane_id() == 0 && (k - lane_id()) < a.n_sim)
-                    a.pbits[(int64_t)i * a.pwords + (k >> 5)] = ok_mask;
-            } else if (cnt && st == kOk) {  // words pre-zeroed by the host
-                atomicOr(a.pbits + (int64_t)i * a.pwords + (k >> 5), 1u << (k & 31));
-            }
-        }
-    } else if (LPC == 1 && a.pbits && lane_id() == 0 && (k - lane_id()) < a.n_sim) {
-        // pruned or duplicate row: no simulated bits (the host expands duplicates)
-        a.pbits[(int64_t)i * a.pwords + (k >> 5)] = 0u;
-    }
-    // last block out extracts the row and resets the accumulators
+// Last block out extracts the best row (governor.py:351-377) and resets the
+// accumulators for the next launch.
+__device__ __forceinline__ void grid_finalize(const GridArgs& a) {
     __shared__ bool s_last;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -275,6 +242,153 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid(GridArgs a) {
         a.abandoned[q] = 0ull;
     }
     if (threadIdx.x == 0) *a.ticket = 0u;
+}
+
+template <bool FMA, bool RNG, bool POLL, int LPC>
+__global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid(GridArgs a) {
+    __shared__ int s_src;
+    __shared__ double s_v;
+    const int i = blockIdx.y;
+    if (threadIdx.x == 0) {
+        double v;
+        s_src = row_source(a, i, &v);
+        s_v = v;
+        if (blockIdx.x == 0) a.row_src[i] = s_src;
+    }
+    __syncthreads();
+    const int src_i = s_src;
+    const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPC;
+    const bool lead = threadIdx.x % LPC == 0;
+    if (src_i == -1) {
+        const bool live = k < a.n_sim;
+        const int64_t kk = live ? k : 0;
+        int st = kOk;
+        int32_t steps = a.p.j_star;
+        if (live || LPC > 1) {
+            const CellConst c = make_cell(a.p);
+            if (RNG) {
+                RngSource src{a.stream, scenario_key(a.stream, (uint64_t)(a.k0 + kk))};
+                st = rollout<FMA, POLL, LPC>(c, a.x0[0], a.x0[1], a.x0[2], s_v, src, steps,
+                                             a.viol + i, live);
+            } else {
+                __shared__ double ring[2 * 3 * kRingStride];
+                SoaSource src{a.soa + kk, a.ld, ring + threadIdx.x};
+                st = rollout<FMA, POLL, LPC>(c, a.x0[0], a.x0[1], a.x0[2], s_v, src, steps,
+                                             a.viol + i, live);
+            }
+        }
+        const bool cnt = live && lead;
+        const bool bad = cnt && st != kOk && st != kAbandoned;
+        const unsigned bad_mask = __ballot_sync(0xffffffffu, bad);
+        if (lane_id() == 0 && bad_mask) atomicAdd(a.viol + i, (unsigned)__popc(bad_mask));
+        warp_count_add(cnt && st != kAbandoned && steps < a.p.j_star, a.early + i);
+        warp_count_add(cnt && st == kOverflow, a.ovf + i);
+        warp_count_add(cnt && st == kAbandoned, a.abandoned + i);
+        if (a.pbits) {
+            if (LPC == 1) {
+                const unsigned ok_mask = __ballot_sync(0xffffffffu, live && st == kOk);
+                if (lane_id() == 0 && (k - lane_id()) < a.n_sim)
+                    a.pbits[(int64_t)i * a.pwords + (k >> 5)] = ok_mask;
+            } else if (cnt && st == kOk) {  // words pre-zeroed by the host
+                atomicOr(a.pbits + (int64_t)i * a.pwords + (k >> 5), 1u << (k & 31));
+            }
+        }
+    } else if (LPC == 1 && a.pbits && lane_id() == 0 && (k - lane_id()) < a.n_sim) {
+        // pruned or duplicate row: no simulated bits (the host expands duplicates)
+        a.pbits[(int64_t)i * a.pwords + (k >> 5)] = 0u;
+    }
+    grid_finalize(a);
+}
+
+// Phase-decoupled grid step (rg_decoupled.cuh): C scenarios of one row per
+// block, chunks of T steps; same accumulators, bits and finalize as k_grid.
+template <bool FMA, bool RNG, bool POLL, int C, int T, int TB>
+__global__ void __launch_bounds__(TB) k_grid_dec(GridArgs a) {
+    __shared__ DecSmem<C, T> sm;
+    __shared__ uint64_t kkey[C];
+    __shared__ int s_src;
+    __shared__ double s_v;
+    const int i = blockIdx.y;
+    if (threadIdx.x == 0) {
+        double v;
+        s_src = row_source(a, i, &v);
+        s_v = v;
+        if (blockIdx.x == 0) a.row_src[i] = s_src;
+    }
+    const int64_t kbase = (int64_t)blockIdx.x * C;
+    if (RNG && threadIdx.x < C)
+        kkey[threadIdx.x] = scenario_key(a.stream, (uint64_t)(a.k0 + kbase + threadIdx.x));
+    __syncthreads();
+    const int64_t k = kbase + threadIdx.x;
+    const bool cell_warp = threadIdx.x < C;
+    if (s_src == -1) {
+        int st;
+        int32_t steps;
+        rollout_decoupled<FMA, POLL, RNG, C, T>(sm, make_cell(a.p), a.x0[0], a.x0[1], a.x0[2],
+                                                 s_v, kbase, a.n_sim, a.soa, a.ld, a.stream,
+                                                 kkey, a.viol + i, st, steps);
+        if (cell_warp) {
+            const bool live = k < a.n_sim;
+            const bool bad = live && st != kOk && st != kAbandoned;
+            const unsigned bad_mask = __ballot_sync(0xffffffffu, bad);
+            if (lane_id() == 0 && bad_mask) atomicAdd(a.viol + i, (unsigned)__popc(bad_mask));
+            warp_count_add(live && st != kAbandoned && steps < a.p.j_star, a.early + i);
+            warp_count_add(live && st == kOverflow, a.ovf + i);
+            warp_count_add(live && st == kAbandoned, a.abandoned + i);
+            if (a.pbits) {
+                const unsigned ok_mask = __ballot_sync(0xffffffffu, live && st == kOk);
+                if (lane_id() == 0 && (k - lane_id()) < a.n_sim)
+                    a.pbits[(int64_t)i * a.pwords + (k >> 5)] = ok_mask;
+            }
+        }
+    } else if (cell_warp && a.pbits && lane_id() == 0 && (k - lane_id()) < a.n_sim) {
+        a.pbits[(int64_t)i * a.pwords + (k >> 5)] = 0u;
+    }
+    grid_finalize(a);
+}
+
+// Warp-specialised grid step (rg_ws.cuh): 32 scenarios of one row per block,
+// one sequence warp plus W tanh warps; same accumulators, bits and finalize.
+template <bool FMA, bool RNG, bool POLL, int T, int W>
+__global__ void __launch_bounds__(32 * (1 + W)) k_grid_ws(GridArgs a) {
+    __shared__ WsSmem<T> sm;
+    __shared__ int s_src;
+    __shared__ double s_v;
+    const int i = blockIdx.y;
+    if (threadIdx.x == 0) {
+        double v;
+        s_src = row_source(a, i, &v);
+        s_v = v;
+        if (blockIdx.x == 0) a.row_src[i] = s_src;
+    }
+    __syncthreads();
+    const int64_t kbase = (int64_t)blockIdx.x * 32;
+    const int64_t k = kbase + threadIdx.x;
+    const bool seq_warp = threadIdx.x < 32;
+    if (s_src == -1) {
+        int st = kOk;
+        int32_t steps = a.p.j_star;
+        rollout_ws<FMA, POLL, RNG, T, W>(sm, make_cell(a.p), a.x0[0], a.x0[1], a.x0[2], s_v,
+                                         kbase, a.n_sim, a.soa, a.ld, a.stream, a.viol + i, st,
+                                         steps);
+        if (seq_warp) {
+            const bool live = k < a.n_sim;
+            const bool bad = live && st != kOk && st != kAbandoned;
+            const unsigned bad_mask = __ballot_sync(0xffffffffu, bad);
+            if (lane_id() == 0 && bad_mask) atomicAdd(a.viol + i, (unsigned)__popc(bad_mask));
+            warp_count_add(live && st != kAbandoned && steps < a.p.j_star, a.early + i);
+            warp_count_add(live && st == kOverflow, a.ovf + i);
+            warp_count_add(live && st == kAbandoned, a.abandoned + i);
+            if (a.pbits) {
+                const unsigned ok_mask = __ballot_sync(0xffffffffu, live && st == kOk);
+                if (lane_id() == 0 && kbase < a.n_sim)
+                    a.pbits[(int64_t)i * a.pwords + (kbase >> 5)] = ok_mask;
+            }
+        }
+    } else if (seq_warp && a.pbits && lane_id() == 0 && kbase < a.n_sim) {
+        a.pbits[(int64_t)i * a.pwords + (kbase >> 5)] = 0u;
+    }
+    grid_finalize(a);
 }
 
 // ---------------------------------------------------------------------------
@@ -718,6 +832,36 @@ cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, int lp
     RG_DISPATCH_LPC(lpc, RG_GRID_L);
 #undef RG_GRID_L
 #undef RG_GRID
+    return cudaGetLastError();
+}
+
+cudaError_t launch_grid_ws(const GridArgs& a, bool fma, bool rng, bool poll, cudaStream_t s) {
+    constexpr int T = RG_WS_T, W = RG_WS_W;
+    dim3 grid((unsigned)((a.n_sim + 31) / 32), (unsigned)a.m_grid);
+#define RG_WS(F, R, P) k_grid_ws<F, R, P, T, W><<<grid, 32 * (1 + W), 0, s>>>(a)
+    if (fma) {
+        if (rng) { if (poll) RG_WS(true, true, true); else RG_WS(true, true, false); }
+        else     { if (poll) RG_WS(true, false, true); else RG_WS(true, false, false); }
+    } else {
+        if (rng) { if (poll) RG_WS(false, true, true); else RG_WS(false, true, false); }
+        else     { if (poll) RG_WS(false, false, true); else RG_WS(false, false, false); }
+    }
+#undef RG_WS
+    return cudaGetLastError();
+}
+
+cudaError_t launch_grid_dec(const GridArgs& a, bool fma, bool rng, bool poll, cudaStream_t s) {
+    constexpr int C = RG_DEC_C, T = RG_DEC_T, TB = RG_DEC_TB;
+    dim3 grid((unsigned)((a.n_sim + C - 1) / C), (unsigned)a.m_grid);
+#define RG_DEC(F, R, P) k_grid_dec<F, R, P, C, T, TB><<<grid, TB, 0, s>>>(a)
+    if (fma) {
+        if (rng) { if (poll) RG_DEC(true, true, true); else RG_DEC(true, true, false); }
+        else     { if (poll) RG_DEC(true, false, true); else RG_DEC(true, false, false); }
+    } else {
+        if (rng) { if (poll) RG_DEC(false, true, true); else RG_DEC(false, true, false); }
+        else     { if (poll) RG_DEC(false, false, true); else RG_DEC(false, false, false); }
+    }
+#undef RG_DEC
     return cudaGetLastError();
 }
 

@@ -161,6 +161,8 @@ cudaError_t launch_fill(const FillArgs& a, bool fma, bool rng, int lpc, cudaStre
 cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, int lpc,
                         cudaStream_t s);
 cudaError_t launch_grid_batch(const BatchArgs& a, bool fma, bool poll, int lpc, cudaStream_t s);
+cudaError_t launch_grid_dec(const GridArgs& a, bool fma, bool rng, bool poll, cudaStream_t s);
+cudaError_t launch_grid_ws(const GridArgs& a, bool fma, bool rng, bool poll, cudaStream_t s);
 cudaError_t launch_bisect(const BisectArgs& a, bool fma, int src, int lpc, cudaStream_t s);
 cudaError_t launch_fill_lin(const LinArgs& a, cudaStream_t s);
 cudaError_t launch_bisect_lin(const LinArgs& a, cudaStream_t s);

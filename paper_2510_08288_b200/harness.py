@@ -24,10 +24,13 @@ from .errors import ConfigError, IntegrationOverflowError
 from .governor import GovernorState, bisection_rg, robust_rg_parallel, \
     robust_rg_parallel_batch
 
-__all__ = ["ReferenceProfile", "RunRecord", "run_closed_loop", "run_closed_loop_bisection",
-           "run_closed_loop_batch", "RUN_CSV_HEADER", "STATE_LIMIT"]
+__all__ = ["ReferenceProfile", "RunRecord", "TimingRecord", "run_closed_loop",
+           "run_closed_loop_bisection", "run_closed_loop_batch", "bench_sweep",
+           "parse_nsim_spec", "emit_csv", "RUN_CSV_HEADER", "TIMING_CSV_HEADER", "STATE_LIMIT"]
 
 RUN_CSV_HEADER = "t,r_t,v_t,y_t,kappa_opt,feasible,wall_us"
+TIMING_CSV_HEADER = "backend,n_sim,mode,mean_us,min_us,max_us,reps"
+_BENCH_MODES = ("kernel-only", "end-to-end")
 STATE_LIMIT = 1e6
 
 
@@ -212,3 +215,140 @@ def run_closed_loop_batch(plant, cset, model, config, profile, steps, seeds, x0=
                                     f"step {t}: state left the operating box")
         live = live[~(bad | bad2)]
     return recs
+
+
+# ---------------------------------------------------------------------------
+# Benchmark sweep and CSV emission (harness.py:114-136, 227-414): the
+# reference's measurement API, so its timing CSVs come out of the device path.
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class TimingRecord:
+    """One (backend, n_sim, mode) timing summary (harness.py:114-136)."""
+
+    backend: str
+    n_sim: int
+    m_grid: int
+    reps: int
+    mode: str
+    mean_us: float | None
+    min_us: float | None
+    max_us: float | None
+    skipped: bool = False
+
+    def __post_init__(self):
+        if not self.skipped:
+            if self.reps < 1:
+                raise ConfigError(f"reps must be >= 1, got {self.reps}")
+            if not (self.min_us <= self.mean_us <= self.max_us):
+                raise ConfigError("mean outside [min, max]")
+
+
+def parse_nsim_spec(spec: str) -> list[int]:
+    """"1:32:1,32:8192:32" or "64,128" -> sorted unique counts (harness.py:227-253)."""
+    values: set[int] = set()
+    for part in (p.strip() for p in spec.split(",")):
+        if not part:
+            continue
+        pieces = part.split(":")
+        try:
+            if len(pieces) == 1:
+                values.add(int(pieces[0]))
+            elif len(pieces) == 3:
+                a, b, st = (int(x) for x in pieces)
+                if st < 1 or a < 1 or b < a:
+                    raise ValueError(f"bad range {part!r}")
+                values.update(range(a, b + 1, st))
+            else:
+                raise ValueError(f"bad range {part!r}")
+        except ValueError as e:
+            raise ConfigError(f"cannot parse n_sim spec {spec!r}: {e}") from None
+    if not values or min(values) < 1:
+        raise ConfigError(f"n_sim spec {spec!r} must produce positive counts")
+    return sorted(values)
+
+
+def bench_sweep(plant, cset, model, template, n_sim_values, backends=("cuda",), reps=20,
+                seed=7, modes=_BENCH_MODES, x0=None, v_prev=0.0, r=0.5):
+    """Time governor calls over (backend, n_sim) cells on the frozen bench snapshot
+    (harness.py:259-355): one untimed warm-up call, then `reps` timed calls of
+    robust_rg_parallel on a fresh state; end-to-end draws a fresh scenario set
+    inside the clock.  Backends other than the device names yield skipped records
+    (this build has no CPU backends)."""
+    from .disturbance import derive_seed
+    from .governor import BACKENDS, GovernorConfig
+
+    if not n_sim_values or not backends:
+        raise ConfigError("n_sim_values and backends must be nonempty")
+    if reps < 1:
+        raise ConfigError(f"reps must be >= 1, got {reps}")
+    for mode in modes:
+        if mode not in _BENCH_MODES:
+            raise ConfigError(f"unknown timing mode {mode!r}; known: {_BENCH_MODES}")
+    x0 = plant.validate_state(np.zeros(plant.state_dim) if x0 is None else x0)
+    records = []
+    for backend in backends:
+        for n_sim in n_sim_values:
+            if backend not in BACKENDS:
+                records += [TimingRecord(backend, n_sim, template.m_grid, reps, m, None, None,
+                                         None, skipped=True) for m in modes]
+                continue
+            cfg = GovernorConfig(j_star=template.j_star, epsilon=template.epsilon,
+                                 n_kappa=template.n_kappa, m_grid=template.m_grid, n_sim=n_sim,
+                                 backend=backend, infeasible_policy=template.infeasible_policy,
+                                 prefix_mode=template.prefix_mode,
+                                 tighten_mode=template.tighten_mode,
+                                 device=getattr(template, "device", 0),
+                                 keep_matrix=getattr(template, "keep_matrix", True))
+            cell_seed = derive_seed(seed, f"bench:{backend}:{n_sim}")
+            scen = sample_scenarios(model, n_sim, cfg.j_star + 1, seed=cell_seed,
+                                    device=cfg.device)
+            for mode in modes:
+                robust_rg_parallel(plant, x0, GovernorState(v_prev), r, cset, scen, cfg)
+                times = np.empty(reps)
+                for i in range(reps):
+                    t0 = time.perf_counter()
+                    s_ = scen if mode == "kernel-only" else sample_scenarios(
+                        model, n_sim, cfg.j_star + 1, seed=cell_seed + i + 1, device=cfg.device)
+                    robust_rg_parallel(plant, x0, GovernorState(v_prev), r, cset, s_, cfg)
+                    times[i] = (time.perf_counter() - t0) * 1e6
+                records.append(TimingRecord(backend, n_sim, cfg.m_grid, reps, mode,
+                                            float(times.mean()), float(times.min()),
+                                            float(times.max())))
+    return records
+
+
+def _fmt(x) -> str:
+    if x is None:
+        return ""
+    if isinstance(x, bool):
+        return str(int(x))
+    if isinstance(x, float):
+        return repr(x)
+    return str(x)
+
+
+def emit_csv(records, path, kind: str | None = None) -> None:
+    """RunRecord -> run CSV, [TimingRecord] -> timing CSV (harness.py:368-414)."""
+    if kind is None:
+        if isinstance(records, RunRecord):
+            kind = "run"
+        elif isinstance(records, (list, tuple)) and records and \
+                isinstance(records[0], TimingRecord):
+            kind = "timing"
+        else:
+            raise ConfigError("cannot infer CSV schema; pass kind=")
+    if kind == "run":
+        lines = [RUN_CSV_HEADER] + [",".join(_fmt(v) for v in row) for row in records.rows]
+    elif kind == "timing":
+        lines = [TIMING_CSV_HEADER] + [",".join([rec.backend, str(rec.n_sim), rec.mode,
+                                                 _fmt(rec.mean_us), _fmt(rec.min_us),
+                                                 _fmt(rec.max_us), str(rec.reps)])
+                                       for rec in records]
+    else:
+        raise ConfigError(f"unknown CSV kind {kind!r}")
+    try:
+        with open(path, "w") as f:
+            f.write("\n".join(lines) + "\n")
+    except OSError as e:
+        raise ConfigError(f"cannot write CSV to {path}: {e}") from None

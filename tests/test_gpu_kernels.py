@@ -172,3 +172,56 @@ def test_batch_every_lane_split(ctx, lpc):
                               abandon=False, want_viol=True)
     for a, b in zip(ref, got):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("kernel", ["warp-spec", "decoupled", "per-step"])
+@pytest.mark.parametrize("mode", ["fused", "staged"])
+@pytest.mark.parametrize("idx", range(N_FILL))
+def test_grid_step_kernels_agree_with_reference(ctx, golden, idx, mode, kernel):
+    c = fill_case(golden, idx)
+    m = rg.DisturbanceModel(c["ranges"])
+    scen = _capi.make_scenarios(c["seed"], 0, c["n_sim"], m.lo, m.span)
+    prob = _problem(c["lower"], c["upper"], c["anchor"], c["eps"], c["j_star"])
+    for abandon in (False, True):
+        res, viol, pbits = ctx.grid_step(prob, c["x0"], c["v_prev"], c["r"], c["m_grid"],
+                                         c["prefix"], None, c["n_sim"], scen, not abandon,
+                                         abandon=abandon, rng_mode=mode, kernel=kernel)
+        kappa = 0.0 if res.row < 0 else res.row / (c["m_grid"] - 1)
+        assert kappa == c["result"][0], (c["name"], abandon)
+        if not abandon:
+            P = np.unpackbits(pbits.view(np.uint8), axis=1, bitorder="little")[:, :c["n_sim"]]
+            ss = c["ss_ok"]
+            keep = [i for i in range(c["m_grid"]) if ss[i]]
+            first = {}
+            sim = []
+            for i in keep:
+                v = rg.update_setpoint(c["v_prev"], c["r"], i / (c["m_grid"] - 1))
+                if v not in first:
+                    first[v] = i
+                    sim.append(i)
+            assert np.array_equal(P[sim].astype(bool), c["P"][sim]), c["name"]
+            assert (int(res.sims_run), int(res.early_terms), int(res.overflows)) == \
+                (int(c["stats"][0]), int(c["stats"][1]), int(c["stats"][2]))
+
+
+@pytest.mark.parametrize("kernel", ["warp-spec", "decoupled"])
+@pytest.mark.parametrize("j_star", [256, 3, 257])
+def test_decoupled_matches_per_step_at_scale(ctx, kernel, j_star):
+    n, M = 5000, 32
+    m = rg.DisturbanceModel.scaled(0.02, 3)
+    prob = _problem(-0.9, 0.9, 0.0, 0.05, j_star)
+    rng = np.random.default_rng(2)
+    for trial in range(4):
+        vp = float(rng.uniform(-1, 1))
+        r = float(rng.uniform(-2.5, 2.5))
+        x0 = np.array([np.tanh(vp), vp, np.tanh(vp) / 2]) + rng.uniform(-0.05, 0.05, 3)
+        sc = _capi.make_scenarios(100 + trial, 0, n, m.lo, m.span)
+        a = ctx.grid_step(prob, x0, vp, r, M, False, None, n, sc, True, kernel="per-step")
+        b = ctx.grid_step(prob, x0, vp, r, M, False, None, n, sc, True, kernel=kernel)
+        assert a[0].row == b[0].row and a[0].early_terms == b[0].early_terms
+        assert a[0].overflows == b[0].overflows and a[0].sims_run == b[0].sims_run
+        assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+        for mode in ("fused", "staged"):  # abandon path: same verdict
+            c = ctx.grid_step(prob, x0, vp, r, M, False, None, n, sc, False, abandon=True,
+                              rng_mode=mode, kernel=kernel)
+            assert c[0].row == a[0].row

@@ -64,3 +64,33 @@ def test_closed_loop_batch_equals_single_episode_loops(golden):
     for e in (1, 3):
         single = run_closed_loop(PLANT, BOX, model, cfg, PROFILE, 600, seeds[e])
         assert [row[:6] for row in recs[e].rows[:600]] == [row[:6] for row in single.rows]
+
+
+def test_parse_nsim_spec_and_csv(tmp_path):
+    from paper_2510_08288_b200.harness import (RunRecord, TimingRecord, emit_csv,
+                                               parse_nsim_spec)
+
+    assert parse_nsim_spec("1:4:1,32:96:32") == [1, 2, 3, 4, 32, 64, 96]
+    assert parse_nsim_spec("64, 128") == [64, 128]
+    with pytest.raises(rg.ConfigError):
+        parse_nsim_spec("5:1:1")
+    emit_csv([TimingRecord("cuda", 64, 32, 3, "kernel-only", 2.0, 1.0, 3.0)], tmp_path / "t.csv")
+    assert (tmp_path / "t.csv").read_text().splitlines() == [
+        "backend,n_sim,mode,mean_us,min_us,max_us,reps", "cuda,64,kernel-only,2.0,1.0,3.0,3"]
+    emit_csv(RunRecord(rows=[(0, 0.4, 0.4, 0.0, 1.0, True, 12)], config={}, seed=1),
+             tmp_path / "r.csv")
+    assert (tmp_path / "r.csv").read_text().splitlines()[1] == "0,0.4,0.4,0.0,1.0,1,12"
+
+
+@pytest.mark.gpu
+def test_bench_sweep_on_device():
+    from paper_2510_08288_b200.harness import bench_sweep
+
+    recs = bench_sweep(PLANT, BOX, rg.DisturbanceModel.scaled(0.001, 3),
+                       rg.GovernorConfig(j_star=64), [64, 256], ["cuda", "serial"], reps=3)
+    assert [(r.backend, r.n_sim, r.mode, r.skipped) for r in recs] == [
+        ("cuda", 64, "kernel-only", False), ("cuda", 64, "end-to-end", False),
+        ("cuda", 256, "kernel-only", False), ("cuda", 256, "end-to-end", False),
+        ("serial", 64, "kernel-only", True), ("serial", 64, "end-to-end", True),
+        ("serial", 256, "kernel-only", True), ("serial", 256, "end-to-end", True)]
+    assert all(r.min_us > 0 for r in recs if not r.skipped)
