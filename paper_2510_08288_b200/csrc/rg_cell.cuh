@@ -22,6 +22,9 @@
 #ifndef RG_PIPE2
 #define RG_PIPE2 1
 #endif
+#ifndef RG_SMALL_TANH
+#define RG_SMALL_TANH 1
+#endif
 
 namespace rg {
 
@@ -200,7 +203,11 @@ template <bool FMA, int LPC>
 __device__ __forceinline__ void step_tanh(double x2, double a2, double b2, double c2,
                                           double& u1, double& u2, double& u3, double& u4) {
     if constexpr (LPC == 1) {
+#if RG_SMALL_TANH
+        tanh4_auto<FMA>(x2, a2, b2, c2, u1, u2, u3, u4);
+#else
         tanh4<FMA>(x2, a2, b2, c2, u1, u2, u3, u4);
+#endif
     } else if constexpr (LPC == 2) {
         const bool q = (threadIdx.x & 1u) != 0;
         const double in[2] = {q ? a2 : x2, q ? c2 : b2};

@@ -747,7 +747,7 @@ __global__ void k_tanh4(const double* __restrict__ x, double* __restrict__ y, in
     if (i >= n) return;
     double a[4], z[4];
     for (int q = 0; q < 4; ++q) a[q] = i + q < n ? x[i + q] : 0.0;
-    tanh4<FMA>(a[0], a[1], a[2], a[3], z[0], z[1], z[2], z[3]);
+    tanh4_auto<FMA>(a[0], a[1], a[2], a[3], z[0], z[1], z[2], z[3]);
     for (int q = 0; q < 4; ++q)
         if (i + q < n) y[i + q] = z[q];
 }

@@ -48,6 +48,34 @@ def test_lockstep_tanh_bit_exact(ctx, orc):
     assert mism.size == 0, f"{mism.size} mismatches, first x={x[mism[:5]]}"
 
 
+def test_small_range_tanh_bit_exact(ctx, orc):
+    """The warp-voted small-argument form (|x| < 0.51986, tanh_lockstep_small):
+    whole warps of in-range arguments, the k = 0 / k = -1 boundary word, the
+    range's last hi word and the 2^-55 floor, each with random low words."""
+    rng = np.random.default_rng(23)
+
+    def words(hi, n):
+        lo = rng.integers(0, 2**32, n, dtype=np.uint64)
+        return ((np.uint64(hi) << np.uint64(32)) | lo).view(np.float64)
+
+    parts = [rng.uniform(-0.5198, 0.5198, 2_000_000),
+             rng.uniform(-0.2, 0.2, 500_000),
+             np.ldexp(rng.uniform(0.5, 1.0, 200_000), rng.integers(-54, -1, 200_000))]
+    for hi in (0x3FC62E41, 0x3FC62E42, 0x3FC62E43, 0x3FE0A2B1, 0x3C800000, 0x3C800001):
+        w = words(hi, 128 * 512)
+        parts += [w, -w]
+    x = np.concatenate(parts)
+    ref = orc.libm_tanh(x)
+    y = ctx.tanh(x, lockstep=True)
+    mism = np.flatnonzero(_bits(y) != _bits(ref))
+    assert mism.size == 0, f"{mism.size} mismatches, first x={x[mism[:5]]}"
+    # and mixed warps: small arguments next to one out-of-range argument per warp
+    x2 = rng.uniform(-0.5, 0.5, 128 * 4096)
+    x2[::128] = rng.uniform(0.6, 5.0, 4096)
+    y2 = ctx.tanh(x2, lockstep=True)
+    assert np.array_equal(_bits(y2), _bits(orc.libm_tanh(x2)))
+
+
 @pytest.mark.parametrize("lpc", [1, 2, 4])
 @pytest.mark.parametrize("mode", ["fused", "staged"])
 @pytest.mark.parametrize("idx", range(N_FILL))
