@@ -58,7 +58,7 @@ extern "C" {
 #define RG_DEVICE_PTRS 0x1  /* array arguments are device pointers (x0[3] is always host) */
 #define RG_ASYNC 0x2        /* enqueue only; no host readback, no sync */
 #define RG_ABANDON 0x4      /* grid step: stop rows already known infeasible */
-#define RG_NO_TIMING 0x8    /* skip the CUDA-event kernel timing */
+#define RG_NO_TIMING 0x8    /* no CUDA-event timing: kernel_ms is the device clock's span (globaltimer) */
 #define RG_TANH_LOCKSTEP 0x10 /* rg_tanh: use the rollout's lockstep form */
 #define RG_FUSED_RNG 0x20   /* RNG source: hash inside the rollout loop */
 #define RG_STAGE_RNG 0x40   /* RNG source: generate the SoA tensor first */

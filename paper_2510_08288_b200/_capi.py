@@ -77,12 +77,29 @@ class BisectResult(ctypes.Structure):
                 ("early", _i64), ("kernel_ms", ctypes.c_float), ("_pad2", _i32)]
 
 
+_RANGE4: dict = {}
+
+
+def _range4(lo, span):
+    """The padded double[4] lo/span pair, cached by value (bytes of the float64 arrays)."""
+    lo = np.ascontiguousarray(lo, dtype=np.float64)
+    span = np.ascontiguousarray(span, dtype=np.float64)
+    key = (lo.tobytes(), span.tobytes())
+    r = _RANGE4.get(key)
+    if r is None:
+        d4 = _d * 4
+        a = lo.tolist() + [0.0] * (4 - lo.size)
+        b = span.tolist() + [0.0] * (4 - span.size)
+        if len(_RANGE4) > 256:
+            _RANGE4.clear()
+        r = _RANGE4[key] = (d4(*a[:4]), d4(*b[:4]))
+    return r
+
+
 def make_scenarios(seed: int, k0: int, n_sim: int, lo, span) -> "Scenarios":
     """rg_scenarios for the counter-RNG stream ``seed`` (masked to 64 bits)."""
-    d4 = _d * 4
-    lo = list(map(float, lo)) + [0.0] * (4 - len(lo))
-    span = list(map(float, span)) + [0.0] * (4 - len(span))
-    return Scenarios(int(seed) & (2**64 - 1), int(k0), int(n_sim), d4(*lo[:4]), d4(*span[:4]))
+    lo4, span4 = _range4(lo, span)
+    return Scenarios(int(seed) & (2**64 - 1), int(k0), int(n_sim), lo4, span4)
 
 
 # name -> (restype, argtypes); the exact export list of include/refgov_b200.h
@@ -234,7 +251,7 @@ class Context:
     def grid_step(self, prob: Problem, x0, v_prev, r, m_grid, prefix_mode, dist, n_sim,
                   scen: Scenarios | None, want_pbits: bool, abandon: bool = False,
                   rng_mode: str | None = None, lpc: int | None = None,
-                  kernel: str | None = None):
+                  kernel: str | None = None, timing: bool = True):
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
         horizon = 0
         if dist is not None:
@@ -244,7 +261,7 @@ class Context:
         pbits = np.empty((m_grid, (n_sim + 31) // 32), dtype=np.uint32) if want_pbits else None
         res = GridResult()
         flags = (RG_ABANDON if abandon else 0) | _RNG_FLAGS[rng_mode] | _LPC_FLAGS[lpc] | \
-            _KERNEL_FLAGS[kernel]
+            _KERNEL_FLAGS[kernel] | (0 if timing else RG_NO_TIMING)
         check(self.lib.rg_grid_step(self.handle, ctypes.byref(prob), _p(x0), float(v_prev),
                                     float(r), int(m_grid), int(bool(prefix_mode)), _p(dist),
                                     int(n_sim), int(horizon),

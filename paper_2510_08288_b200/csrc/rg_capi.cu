@@ -128,7 +128,7 @@ struct rg_ctx {
     // grid-step accumulators and outputs
     int grid_cap = 0;
     int last_m = 0;
-    DevBuf g_viol, g_early, g_ovf, g_aband, g_src, g_ticket, g_out;
+    DevBuf g_viol, g_early, g_ovf, g_aband, g_src, g_ticket, g_t0, g_out;
     // bisection accumulators and outputs
     DevBuf b_acc, b_out;
     // batched grid step: inputs, accumulators (zeroed on growth, reset by the kernel), outputs
@@ -240,12 +240,14 @@ int32_t grow_grid(rg_ctx* ctx, int m) {
     RG_CUDA(ctx->g_aband.ensure(cap * sizeof(unsigned long long)));
     RG_CUDA(ctx->g_src.ensure(cap * sizeof(int)));
     RG_CUDA(ctx->g_ticket.ensure(sizeof(unsigned)));
+    RG_CUDA(ctx->g_t0.ensure(sizeof(unsigned long long)));
     RG_CUDA(ctx->g_out.ensure(kOutHead + viol_bytes(cap)));
     RG_CUDA(cudaMemsetAsync(ctx->g_viol.p, 0, ctx->g_viol.bytes, ctx->stream));
     RG_CUDA(cudaMemsetAsync(ctx->g_early.p, 0, ctx->g_early.bytes, ctx->stream));
     RG_CUDA(cudaMemsetAsync(ctx->g_ovf.p, 0, ctx->g_ovf.bytes, ctx->stream));
     RG_CUDA(cudaMemsetAsync(ctx->g_aband.p, 0, ctx->g_aband.bytes, ctx->stream));
     RG_CUDA(cudaMemsetAsync(ctx->g_ticket.p, 0, ctx->g_ticket.bytes, ctx->stream));
+    RG_CUDA(cudaMemsetAsync(ctx->g_t0.p, 0xff, ctx->g_t0.bytes, ctx->stream));
     RG_CUDA(cudaMemsetAsync(ctx->g_out.p, 0, ctx->g_out.bytes, ctx->stream));
     ctx->grid_cap = cap;
     return RG_OK;
@@ -379,7 +381,7 @@ int32_t rg_destroy(rg_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     DevBuf* bufs[] = {&ctx->g_viol, &ctx->g_early, &ctx->g_ovf, &ctx->g_aband, &ctx->g_src,
-                      &ctx->g_ticket, &ctx->g_out, &ctx->b_acc, &ctx->b_out,
+                      &ctx->g_ticket, &ctx->g_t0, &ctx->g_out, &ctx->b_acc, &ctx->b_out,
                       &ctx->dist_raw, &ctx->soa, &ctx->S, &ctx->steps, &ctx->pbits, &ctx->rows,
                       &ctx->vrows, &ctx->tmp_a, &ctx->tmp_b, &ctx->kap_k, &ctx->fnd_k,
                       &ctx->cel_k, &ctx->erl_k, &ctx->path_k, &ctx->path_o, &ctx->e_in,
@@ -565,7 +567,7 @@ static int32_t read_grid(rg_ctx* ctx, uint32_t* row_viol, int32_t m_grid, rg_gri
         out->early_terms = ho->early_terms;
         out->overflows = ho->overflows;
         out->abandoned = ho->abandoned;
-        out->kernel_ms = 0.f;
+        out->kernel_ms = (float)((double)ho->kernel_ns * 1e-6);  // device globaltimer span
         if (timed) {
             float ms = 0.f;
             if (cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) == cudaSuccess) out->kernel_ms = ms;
@@ -619,6 +621,7 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
     a.abandoned = ctx->g_aband.as<unsigned long long>();
     a.row_src = ctx->g_src.as<int>();
     a.ticket = ctx->g_ticket.as<unsigned>();
+    a.t0 = ctx->g_t0.as<unsigned long long>();
     a.pwords = (n_sim + 31) / 32;
     const size_t pbytes = pbits ? (size_t)m_grid * a.pwords * sizeof(unsigned) : 0;
     const bool pbits_in_block = pbits && !(flags & RG_DEVICE_PTRS);

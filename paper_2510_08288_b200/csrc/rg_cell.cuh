@@ -25,6 +25,9 @@
 #ifndef RG_SMALL_TANH
 #define RG_SMALL_TANH 1
 #endif
+#ifndef RG_TANH_WITH
+#define RG_TANH_WITH 1
+#endif
 
 namespace rg {
 
@@ -304,14 +307,26 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
     double dB0 = dj1.d0, dB2 = dj1.d2;  // ... and of step j+1
     for (int32_t j = 0; j < J; ++j) {
         const D3 dn = fetch(j + 2);
-        // step j+1's tanh values (speculative past an exit or the horizon)
+        // step j+2's x2 chain and step j's x1/x3: independent of the tanh
+        // values of step j+1 evaluated alongside (speculative past an exit)
+        X2Stage sn;
+        double y3;
+        auto side = [&]() {
+            sn = x2_stage<FMA>(y2, v, p);
+            y3 = add(add(y2, mul(p.c, sn.s2)), dn.d1);
+            x13_update<FMA>(x1, x3, t1, t2, t3, t4, p, dA0, dA2);
+        };
         double u1, u2, u3, u4;
-        step_tanh<FMA, LPC>(g0, g1, g2, g3, u1, u2, u3, u4);
-        // step j+2's x2 chain
-        const X2Stage sn = x2_stage<FMA>(y2, v, p);
-        const double y3 = add(add(y2, mul(p.c, sn.s2)), dn.d1);
-        // step j's x1/x3 and checks; x2 after step j is g0
-        x13_update<FMA>(x1, x3, t1, t2, t3, t4, p, dA0, dA2);
+#if RG_SMALL_TANH && RG_TANH_WITH
+        if constexpr (LPC == 1) {
+            tanh4_with<FMA>(g0, g1, g2, g3, u1, u2, u3, u4, side);
+        } else
+#endif
+        {
+            step_tanh<FMA, LPC>(g0, g1, g2, g3, u1, u2, u3, u4);
+            side();
+        }
+        // step j's checks; x2 after step j is g0
         if (!done) {
             if (!(fabs(x1) <= kStateLimit && fabs(g0) <= kStateLimit &&
                   fabs(x3) <= kStateLimit)) {

@@ -181,6 +181,40 @@ __device__ int row_source(const GridArgs& a, int i, double* v_out) {
     return -1;
 }
 
+// row_source with the first warp: lane q evaluates candidate q's setpoint, a
+// ballot finds the first equal gated row (same result, no serial loop of
+// divisions in front of every block's rollout).  All 32 lanes must call it.
+__device__ int row_source_warp(const GridArgs& a, int i, double* v_out) {
+    const int lane = threadIdx.x & 31;
+    const double den = (double)(a.m_grid - 1);
+    const double v = update_setpoint(a.v_prev, a.r, dvd((double)i, den));
+    *v_out = v;
+    if (!ss_gate(v, a.p)) return -2;
+    for (int q0 = 0; q0 < i; q0 += 32) {
+        const int q = q0 + lane;
+        bool hit = false;
+        if (q < i) {
+            const double vq = update_setpoint(a.v_prev, a.r, dvd((double)q, den));
+            hit = ss_gate(vq, a.p) && vq == v;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (m) return q0 + __ffs(m) - 1;
+    }
+    return -1;
+}
+
+// Device-side span of a grid step for the diagnostics (kernel_us) without
+// host event records: each block's first thread lowers t0 to its start time,
+// the finalizing block reads it against its own end time and re-arms t0.
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void grid_clock_start(const GridArgs& a) {
+    if (a.t0) atomicMin(a.t0, global_ns());
+}
+
 // Last block out extracts the best row (governor.py:351-377) and resets the
 // accumulators for the next launch.
 __device__ __forceinline__ void grid_finalize(const GridArgs& a) {
@@ -233,6 +267,10 @@ __device__ __forceinline__ void grid_finalize(const GridArgs& a) {
         a.out->abandoned = (long long)aband;
         a.out->sims_run = (long long)n_active * a.n_sim;
         a.out->seq += 1;
+        if (a.t0) {
+            a.out->kernel_ns = global_ns() - *(volatile unsigned long long*)a.t0;
+            *a.t0 = ~0ull;
+        }
     }
     __syncthreads();
     for (int q = threadIdx.x; q < a.m_grid; q += blockDim.x) {
@@ -249,11 +287,15 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid(GridArgs a) {
     __shared__ int s_src;
     __shared__ double s_v;
     const int i = blockIdx.y;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
         double v;
-        s_src = row_source(a, i, &v);
-        s_v = v;
-        if (blockIdx.x == 0) a.row_src[i] = s_src;
+        const int src = row_source_warp(a, i, &v);
+        if (threadIdx.x == 0) {
+            grid_clock_start(a);
+            s_src = src;
+            s_v = v;
+            if (blockIdx.x == 0) a.row_src[i] = src;
+        }
     }
     __syncthreads();
     const int src_i = s_src;
@@ -309,11 +351,15 @@ __global__ void __launch_bounds__(TB) k_grid_dec(GridArgs a) {
     __shared__ int s_src;
     __shared__ double s_v;
     const int i = blockIdx.y;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
         double v;
-        s_src = row_source(a, i, &v);
-        s_v = v;
-        if (blockIdx.x == 0) a.row_src[i] = s_src;
+        const int src = row_source_warp(a, i, &v);
+        if (threadIdx.x == 0) {
+            grid_clock_start(a);
+            s_src = src;
+            s_v = v;
+            if (blockIdx.x == 0) a.row_src[i] = src;
+        }
     }
     const int64_t kbase = (int64_t)blockIdx.x * C;
     if (RNG && threadIdx.x < C)
@@ -355,11 +401,15 @@ __global__ void __launch_bounds__(32 * (1 + W)) k_grid_ws(GridArgs a) {
     __shared__ int s_src;
     __shared__ double s_v;
     const int i = blockIdx.y;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
         double v;
-        s_src = row_source(a, i, &v);
-        s_v = v;
-        if (blockIdx.x == 0) a.row_src[i] = s_src;
+        const int src = row_source_warp(a, i, &v);
+        if (threadIdx.x == 0) {
+            grid_clock_start(a);
+            s_src = src;
+            s_v = v;
+            if (blockIdx.x == 0) a.row_src[i] = src;
+        }
     }
     __syncthreads();
     const int64_t kbase = (int64_t)blockIdx.x * 32;

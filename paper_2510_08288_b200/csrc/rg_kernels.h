@@ -46,6 +46,7 @@ struct GridOut {
     int32_t n_active, ss_pruned_rows, dedup_rows;
     long long sims_run, early_terms, overflows, abandoned;
     unsigned long long seq;
+    unsigned long long kernel_ns;  // device span of the step (globaltimer)
 };
 
 struct GridArgs {
@@ -64,6 +65,7 @@ struct GridArgs {
     unsigned long long* abandoned;  // [m]
     int* row_src;                   // [m]
     unsigned* ticket;
+    unsigned long long* t0;  // earliest block start (globaltimer), re-armed to ~0 by finalize
     unsigned* viol_out;             // [m] per-row violation count (0xffffffff = pruned)
     GridOut* out;
     unsigned* pbits;                // optional [m][pwords] feasibility bitmask

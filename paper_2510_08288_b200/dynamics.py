@@ -14,6 +14,8 @@ are kept as numpy so they stay bit-identical with the reference.
 
 from __future__ import annotations
 
+import math
+
 import numpy as np
 
 from .errors import ConfigError, IntegrationOverflowError
@@ -43,7 +45,7 @@ class Plant:
         x = np.asarray(x, dtype=np.float64)
         if x.shape != (self.state_dim,):
             raise ConfigError(f"state must have shape ({self.state_dim},), got {x.shape}")
-        if not np.all(np.isfinite(x)):
+        if not all(map(math.isfinite, x.tolist())):
             raise ConfigError("state entries must be finite")
         return x
 

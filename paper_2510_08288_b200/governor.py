@@ -405,16 +405,19 @@ def robust_rg_parallel(plant, x_t, state, r_t, cset, scenarios, config, backend=
     keep = getattr(config, "keep_matrix", True)
 
     t0 = time.perf_counter()
-    _, ss_ok, dup_src, _ = _host_rows(float(state.v_prev), float(r_t), grid_list, interval)
     ctx = _capi.context(device)
     res, viol, pbits = ctx.grid_step(prob, x_t, state.v_prev, r_t, config.m_grid,
                                      config.prefix_mode, dist, n_sim, stream, want_pbits=keep,
-                                     abandon=not keep)
-    # the device gate (verified interval) and dedup must agree with the host's
-    n_pruned = ss_ok.count(False)
-    n_dup = len(dup_src) - dup_src.count(-1)
-    if res.ss_pruned_rows != n_pruned or res.dedup_rows != n_dup:
-        raise RefgovError("device steady-state gate disagrees with the host gate")
+                                     abandon=not keep, timing=False)
+    n_dup = 0
+    if res.ss_pruned_rows or res.dedup_rows:
+        # rows the device gated or deduplicated: the host's loop (governor.py:302-317)
+        # names them, and must agree with the device's counts
+        _, ss_ok, dup_src, _ = _host_rows(float(state.v_prev), float(r_t), grid_list, interval)
+        n_pruned = ss_ok.count(False)
+        n_dup = len(dup_src) - dup_src.count(-1)
+        if res.ss_pruned_rows != n_pruned or res.dedup_rows != n_dup:
+            raise RefgovError("device steady-state gate disagrees with the host gate")
     P = None
     if keep:
         # pruned and duplicate rows come back as zero bits; duplicates copy their source
