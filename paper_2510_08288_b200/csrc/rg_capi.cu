@@ -289,6 +289,10 @@ int grid_kernel_for(int32_t flags) {
 }
 
 int tpb_for(const rg_ctx* ctx, int64_t n_sim, int64_t rows) {
+    if (const char* env = getenv("RG_FORCE_TPB")) {  // tuning override: 32, 64 or 128
+        const int t = atoi(env);
+        if (t == 32 || t == 64 || t == 128) return t;
+    }
     // Small problems: small blocks spread the warps over more SMs.
     const int64_t warps = (n_sim + 31) / 32 * std::max<int64_t>(rows, 1);
     if (warps < (int64_t)ctx->sm_count * 8) return 32;

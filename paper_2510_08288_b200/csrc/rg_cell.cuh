@@ -250,10 +250,18 @@ __device__ __forceinline__ void step_tanh(double x2, double a2, double b2, doubl
 // is done (lanes of finished or out-of-range cells keep computing throwaway
 // values), so the shuffles in step_tanh always see full warps.  `live` marks
 // lanes whose cell exists.
-template <bool FMA, bool POLL, int LPC, class Src>
+//
+// WARP (LPC = 1 only): the caller guarantees that all 32 lanes call, and the
+// lanes then run as one: out-of-range and finished lanes keep computing
+// throwaway values until every lane is done, the exit and the tanh range vote
+// are full-warp votes, and the per-step checks are predicated into the
+// iteration's single basic block (no divergent branches inside the loop).
+template <bool FMA, bool POLL, int LPC, class Src, bool WARP = false>
 __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2, double x3,
                                        double v, const Src& src, int32_t& steps,
                                        const unsigned int* dead, bool live = true) {
+    static_assert(!WARP || LPC == 1, "WARP is the one-lane-per-cell form");
+    constexpr bool kUniform = WARP || LPC > 1;  // all lanes run the loop together
     const int32_t J = p.j_star;
     constexpr bool kRing = std::is_same<Src, SoaSource>::value;
     int status = kOk;
@@ -264,7 +272,7 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
         status = kViolated;
         done = true;
     }
-    if constexpr (LPC == 1) {
+    if constexpr (!kUniform) {
         if (done) return status;
     } else {
         if (__all_sync(0xffffffffu, done)) return status;
@@ -311,29 +319,41 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
         // values of step j+1 evaluated alongside (speculative past an exit)
         X2Stage sn;
         double y3;
+        bool bad_ovf, bad_bnd;
         auto side = [&]() {
             sn = x2_stage<FMA>(y2, v, p);
             y3 = add(add(y2, mul(p.c, sn.s2)), dn.d1);
             x13_update<FMA>(x1, x3, t1, t2, t3, t4, p, dA0, dA2);
+            // step j's checks (x2 after step j is g0), as predicates
+            bad_ovf = !(fabs(x1) <= kStateLimit && fabs(g0) <= kStateLimit &&
+                        fabs(x3) <= kStateLimit);
+            bad_bnd = !in_bounds(x1, p.ylo, p.yhi);
         };
         double u1, u2, u3, u4;
 #if RG_SMALL_TANH && RG_TANH_WITH
         if constexpr (LPC == 1) {
-            tanh4_with<FMA>(g0, g1, g2, g3, u1, u2, u3, u4, side);
+            tanh4_with<FMA, WARP>(g0, g1, g2, g3, u1, u2, u3, u4, side);
         } else
 #endif
         {
             step_tanh<FMA, LPC>(g0, g1, g2, g3, u1, u2, u3, u4);
             side();
         }
-        // step j's checks; x2 after step j is g0
-        if (!done) {
-            if (!(fabs(x1) <= kStateLimit && fabs(g0) <= kStateLimit &&
-                  fabs(x3) <= kStateLimit)) {
+        if constexpr (WARP) {
+            // the reference's order: overflow, then the output bound, then the poll
+            bool aband = false;
+            if (POLL && (j & 31) == 31) aband = *(volatile const unsigned int*)dead != 0u;
+            const bool now = !done && (bad_ovf || bad_bnd || aband);
+            const int code = bad_ovf ? kOverflow : (bad_bnd ? kViolated : kAbandoned);
+            status = now ? code : status;
+            steps = now ? j + 1 : steps;
+            done = done || now;
+        } else if (!done) {
+            if (bad_ovf) {
                 steps = j + 1;
                 status = kOverflow;
                 done = true;
-            } else if (!in_bounds(x1, p.ylo, p.yhi)) {
+            } else if (bad_bnd) {
                 steps = j + 1;
                 status = kViolated;
                 done = true;
@@ -344,7 +364,7 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
                 done = true;
             }
         }
-        if constexpr (LPC == 1) {
+        if constexpr (!kUniform) {
             if (done) break;
         } else {
             if (__all_sync(0xffffffffu, done)) break;

@@ -34,6 +34,9 @@
 #ifndef RG_WS_T
 #define RG_WS_T 4
 #endif
+#ifndef RG_GRID_WARP
+#define RG_GRID_WARP 1  // k_grid, one lane per cell: warp-uniform rollout (rollout<..., WARP>)
+#endif
 #ifndef RG_WS_W
 #define RG_WS_W 2
 #endif
@@ -306,17 +309,18 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid(GridArgs a) {
         const int64_t kk = live ? k : 0;
         int st = kOk;
         int32_t steps = a.p.j_star;
-        if (live || LPC > 1) {
+        constexpr bool W = LPC == 1 && RG_GRID_WARP;  // whole warps run the rollout
+        if (live || LPC > 1 || W) {
             const CellConst c = make_cell(a.p);
             if (RNG) {
                 RngSource src{a.stream, scenario_key(a.stream, (uint64_t)(a.k0 + kk))};
-                st = rollout<FMA, POLL, LPC>(c, a.x0[0], a.x0[1], a.x0[2], s_v, src, steps,
-                                             a.viol + i, live);
+                st = rollout<FMA, POLL, LPC, RngSource, W>(c, a.x0[0], a.x0[1], a.x0[2], s_v,
+                                                           src, steps, a.viol + i, live);
             } else {
                 __shared__ double ring[2 * 3 * kRingStride];
                 SoaSource src{a.soa + kk, a.ld, ring + threadIdx.x};
-                st = rollout<FMA, POLL, LPC>(c, a.x0[0], a.x0[1], a.x0[2], s_v, src, steps,
-                                             a.viol + i, live);
+                st = rollout<FMA, POLL, LPC, SoaSource, W>(c, a.x0[0], a.x0[1], a.x0[2], s_v,
+                                                           src, steps, a.viol + i, live);
             }
         }
         const bool cnt = live && lead;
