@@ -18,6 +18,8 @@
 // the early exits mostly agree across the warp.
 #include "rg_kernels.h"
 
+#include <mutex>
+
 #include <cuda_runtime.h>
 
 #include "rg_cell.cuh"
@@ -218,8 +220,16 @@ __device__ __forceinline__ void grid_clock_start(const GridArgs& a) {
     if (a.t0) atomicMin(a.t0, global_ns());
 }
 
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
 // Last block out extracts the best row (governor.py:351-377) and resets the
-// accumulators for the next launch.
+// accumulators for the next launch.  The first warp reads 32 rows at a time
+// (one per lane) and reduces with ballots and shuffles, so the step's tail is
+// a few L2 round trips rather than one chain of loads per row.
 __device__ __forceinline__ void grid_finalize(const GridArgs& a) {
     __shared__ bool s_last;
     __syncthreads();
@@ -231,48 +241,63 @@ __device__ __forceinline__ void grid_finalize(const GridArgs& a) {
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
         int best = -1;
+        bool open = true;  // prefix mode: every row so far was feasible
         int n_active = 0, pruned = 0, dup = 0;
         unsigned long long early = 0, ovf = 0, aband = 0;
-        for (int q = 0; q < a.m_grid; ++q) {
-            const int s = ((volatile int*)a.row_src)[q];
-            bool full;
-            if (s == -2) {
-                full = false;
-                ++pruned;
-            } else if (s == -1) {
-                ++n_active;
-                full = ((volatile unsigned*)a.viol)[q] == 0u &&
-                       ((volatile unsigned long long*)a.abandoned)[q] == 0ull;
-                early += ((volatile unsigned long long*)a.early)[q];
-                ovf += ((volatile unsigned long long*)a.ovf)[q];
-                aband += ((volatile unsigned long long*)a.abandoned)[q];
-            } else {
-                ++dup;
-                full = ((volatile unsigned*)a.viol)[s] == 0u &&
-                       ((volatile unsigned long long*)a.abandoned)[s] == 0ull;
+        for (int q0 = 0; q0 < a.m_grid; q0 += 32) {
+            const int q = q0 + lane;
+            const bool in = q < a.m_grid;
+            int sq = -2;
+            unsigned vq = 0u;
+            unsigned long long ab = 0ull, ea = 0ull, ov = 0ull;
+            if (in) {
+                sq = ((volatile int*)a.row_src)[q];
+                vq = ((volatile unsigned*)a.viol)[q];
+                ab = ((volatile unsigned long long*)a.abandoned)[q];
+                ea = ((volatile unsigned long long*)a.early)[q];
+                ov = ((volatile unsigned long long*)a.ovf)[q];
             }
-            a.viol_out[q] = s == -2 ? 0xffffffffu
-                                    : ((volatile unsigned*)a.viol)[s < 0 ? q : s];
+            if (in && sq >= 0) {  // a duplicate row takes its source row's verdict
+                vq = ((volatile unsigned*)a.viol)[sq];
+                ab = ((volatile unsigned long long*)a.abandoned)[sq];
+            }
+            const bool act = in && sq == -1;
+            const bool full = in && sq != -2 && vq == 0u && ab == 0ull;
+            n_active += __popc(__ballot_sync(0xffffffffu, act));
+            pruned += __popc(__ballot_sync(0xffffffffu, in && sq == -2));
+            dup += __popc(__ballot_sync(0xffffffffu, in && sq >= 0));
+            early += warp_sum_u64(act ? ea : 0ull);
+            ovf += warp_sum_u64(act ? ov : 0ull);
+            aband += warp_sum_u64(act ? ab : 0ull);
+            if (in) a.viol_out[q] = sq == -2 ? 0xffffffffu : vq;
+            const unsigned fm = __ballot_sync(0xffffffffu, full);
             if (a.prefix_mode) {
-                if (best == q - 1 && full) best = q;
-            } else if (full) {
-                best = q;
+                if (open) {  // the run of feasible rows from row 0 (governor.py:370-375)
+                    const int run = ~fm == 0u ? 32 : __ffs(~fm) - 1;
+                    if (run > 0) best = q0 + run - 1;
+                    open = run == 32;
+                }
+            } else if (fm) {
+                best = q0 + 31 - __clz(fm);
             }
         }
-        a.out->row = best;
-        a.out->n_active = n_active;
-        a.out->ss_pruned_rows = pruned;
-        a.out->dedup_rows = dup;
-        a.out->early_terms = (long long)early;
-        a.out->overflows = (long long)ovf;
-        a.out->abandoned = (long long)aband;
-        a.out->sims_run = (long long)n_active * a.n_sim;
-        a.out->seq += 1;
-        if (a.t0) {
-            a.out->kernel_ns = global_ns() - *(volatile unsigned long long*)a.t0;
-            *a.t0 = ~0ull;
+        if (lane == 0) {
+            a.out->row = best;
+            a.out->n_active = n_active;
+            a.out->ss_pruned_rows = pruned;
+            a.out->dedup_rows = dup;
+            a.out->early_terms = (long long)early;
+            a.out->overflows = (long long)ovf;
+            a.out->abandoned = (long long)aband;
+            a.out->sims_run = (long long)n_active * a.n_sim;
+            a.out->seq += 1;
+            if (a.t0) {
+                a.out->kernel_ns = global_ns() - *(volatile unsigned long long*)a.t0;
+                *a.t0 = ~0ull;
+            }
         }
     }
     __syncthreads();
@@ -869,10 +894,54 @@ cudaError_t launch_fill(const FillArgs& a, bool fma, bool rng, int lpc, cudaStre
     return cudaGetLastError();
 }
 
+// Dynamic shared memory that caps a kernel at `cap` resident blocks per SM:
+// each block's footprint becomes smem_per_sm / cap, so cap + 1 blocks do not
+// fit.  The block scheduler then cannot stack extra warps onto some SM
+// sub-partitions while others idle (a latency-bound rollout runs as slow as
+// its most loaded sub-partition).  Per-kernel attributes are cached.
+template <class Kern>
+size_t occ_cap_smem(Kern kern, int cap, int smem_per_sm, int reserved) {
+    if (cap <= 0) return 0;
+    struct Slot { const void* fn; size_t stat; size_t set; };
+    static Slot cache[64];
+    static int n_cache = 0;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    Slot* sl = nullptr;
+    for (int q = 0; q < n_cache; ++q)
+        if (cache[q].fn == (const void*)kern) sl = &cache[q];
+    if (!sl) {
+        cudaFuncAttributes fa;
+        if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess || n_cache == 64) {
+            cudaGetLastError();
+            return 0;
+        }
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cache[n_cache] = Slot{(const void*)kern, fa.sharedSizeBytes, 48 * 1024};
+        sl = &cache[n_cache++];
+    }
+    const size_t per = (size_t)smem_per_sm / (size_t)cap;
+    const size_t need = sl->stat + (size_t)reserved;
+    const size_t dyn = per > need ? per - need : 0;
+    if (dyn > sl->set) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) !=
+            cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+        sl->set = dyn;
+    }
+    return dyn;
+}
+
 cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, int lpc,
                         cudaStream_t s) {
     dim3 grid(blocks_for(a.n_sim * lpc, a.tpb), (unsigned)a.m_grid);
-#define RG_GRID(F, R, P, L) k_grid<F, R, P, L><<<grid, a.tpb, 0, s>>>(a)
+#define RG_GRID(F, R, P, L)                                                            \
+    k_grid<F, R, P, L><<<grid, a.tpb,                                                  \
+                         occ_cap_smem(k_grid<F, R, P, L>, a.occ_cap, a.smem_per_sm,    \
+                                      a.smem_reserved),                                \
+                         s>>>(a)
 #define RG_GRID_L(L)                                                             \
     do {                                                                         \
         if (fma) {                                                               \

@@ -71,6 +71,9 @@ struct GridArgs {
     unsigned* pbits;                // optional [m][pwords] feasibility bitmask
     int64_t pwords;
     int tpb;
+    // occupancy cap (host side of the launch): at most occ_cap blocks per SM,
+    // enforced with dynamic shared memory; 0 = no cap
+    int occ_cap, smem_per_sm, smem_reserved;
 };
 
 // Batch of independent governor instances (episodes): one launch covers
