@@ -185,6 +185,18 @@ struct SoaSource {
         const double* r = ring + slot * 3 * kRingStride;
         return D3{r[0], r[kRingStride], r[2 * kRingStride]};
     }
+    // issue() from a precomputed step pointer p = d + j*3*ld (the rollout
+    // walks the steps in order, so it advances p instead of multiplying)
+    __device__ __forceinline__ void issue_at(const double* p, int slot) const {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(ring + slot * 3 * kRingStride);
+        const double* p1 = p + ld;
+        const double* p2 = p1 + ld;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(p));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa + 8 * kRingStride),
+                     "l"(p1));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa + 16 * kRingStride),
+                     "l"(p2));
+    }
 };
 
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
@@ -283,11 +295,21 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
     // (arguments from iteration j-1) and runs the x2 chain of step j+2.  The
     // three pieces are mutually independent, so the tanh chains no longer
     // wait behind the x2 recurrence inside an iteration.
+    // staged source: the next step to issue, as a pointer (steps 2, 3, ..., J-1, J-1, ...)
+    const double* nxt = nullptr;
+    const double* last = nullptr;
+    int64_t stride = 0;
+    if constexpr (kRing) {
+        stride = 3 * src.ld;
+        nxt = src.d + (J > 2 ? 2 : J - 1) * stride;
+        last = src.d + (int64_t)(J - 1) * stride;
+    }
     auto fetch = [&](int32_t j) -> D3 {  // disturbances of step min(j, J-1)
         if constexpr (kRing) {
             cp_async_wait<1>();          // step j landed (issued two fetches ago)
             const D3 r = src.read(j & 1);
-            src.issue(j + 2 < J ? j + 2 : J - 1, j & 1);
+            src.issue_at(nxt, j & 1);    // step min(j + 2, J - 1)
+            nxt = nxt == last ? nxt : nxt + stride;
             cp_async_commit();
             return r;
         } else {
