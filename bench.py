@@ -42,7 +42,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "robust RG step latency (ms) at N scenarios; scenario-steps/sec vs FP64 roofline"
 UNIT = "cell-steps/s"
 FLOPS_PER_CELL_STEP = 210  # 58 explicit ops + 4 tanh x 38
-FP64_INSTR_PER_CELL_STEP = 267  # ncu, round 1: DFMA+DADD+DMUL+DSETP per cell-step (k_grid)
+FP64_INSTR_PER_CELL_STEP = 226  # fallback only; bench reads profiles/k_grid_ncu.json (ncu count)
 J_STAR, M_GRID, N_PER_GPU, R_REF = 256, 32, 1000, 0.5
 BASE_SEED = 7
 
@@ -290,13 +290,15 @@ def run_own(args, rank, world, local_rank):
     roof = None
     if kernel_ms:
         achieved = FLOPS_PER_CELL_STEP * cells_rank / (kernel_ms * 1e-3)
-        # the instruction-mix view: ncu counts ~267 FP64-pipe instructions per
-        # cell-step (the 210-flop convention counts each division as 1 flop)
-        fp64_instr_rate = cells_rank / (kernel_ms * 1e-3) * FP64_INSTR_PER_CELL_STEP
+        # the instruction-mix view: FP64-pipe instructions per cell-step as
+        # counted by ncu on this kernel (profiles/k_grid_ncu.json); the 210-flop
+        # convention counts each division as 1 flop
+        fp64_per_cell = _ncu_summary().get("fp64_instr_per_cell_step", FP64_INSTR_PER_CELL_STEP)
+        fp64_instr_rate = cells_rank / (kernel_ms * 1e-3) * fp64_per_cell
         roof = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
                 "unit": "TFLOP/s", "frac": achieved / peak, "traffic": _ncu_traffic(),
                 "fp64_pipe_frac": fp64_instr_rate / (peak / 2.0),
-                "fp64_instr_per_cell_step": FP64_INSTR_PER_CELL_STEP,
+                "fp64_instr_per_cell_step": fp64_per_cell,
                 "peak_source": "measured in this run: rg_fp64_peak (independent DFMA chains, "
                                "2 flop per DFMA); MEASURED_PEAKS.json has no FP64 figure",
                 "flops_per_cell_step": FLOPS_PER_CELL_STEP, "cell_steps_per_launch": cells_rank,
@@ -409,7 +411,9 @@ def run_own(args, rank, world, local_rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": "C2 bench snapshot: robust grid step (Alg. 3), fused RNG",
+            "config": {"workload": "C2 bench snapshot: robust grid step (Alg. 3), " + (
+                           "staged RNG (k_gen_soa + k_grid)" if launches_per_step == 2
+                           else "fused RNG (k_grid)"),
                        "n_sim": n_sim * world, "n_sim_per_gpu": n_sim, "j_star": j_star,
                        "m_grid": M_GRID, "plant": "surrogate-fc", "disturbance": "U(+-0.001)",
                        "r": R_REF, "cell_steps_per_step": cells_rank * world,
@@ -432,13 +436,18 @@ def ctypes_vp():
     return ctypes.c_void_p
 
 
+def _ncu_summary():
+    """The committed ncu --set full summary of k_grid at C2 (scripts/ncu_summary.py)."""
+    p = ROOT / "profiles" / "k_grid_ncu.json"
+    try:
+        return json.loads(p.read_text())
+    except (OSError, ValueError):
+        return {}
+
+
 def _ncu_traffic():
     """dram bytes per k_grid launch from the committed ncu --set full summary."""
-    p = ROOT / "profiles" / "k_grid_traffic.json"
-    try:
-        return json.loads(p.read_text())["dram_bytes_per_launch"]
-    except (OSError, ValueError, KeyError):
-        return None
+    return _ncu_summary().get("dram_bytes_per_launch")
 
 
 def main():
