@@ -174,7 +174,9 @@ def check(code: int) -> None:
 
 
 def _p(a: np.ndarray | None):
-    return None if a is None else a.ctypes.data_as(_vp)
+    # the integer address: ctypes passes it for c_void_p arguments, and it is
+    # several times cheaper to produce than a.ctypes.data_as(c_void_p)
+    return None if a is None else a.ctypes.data
 
 
 def device_count() -> int:
@@ -251,13 +253,13 @@ class Context:
     def grid_step(self, prob: Problem, x0, v_prev, r, m_grid, prefix_mode, dist, n_sim,
                   scen: Scenarios | None, want_pbits: bool, abandon: bool = False,
                   rng_mode: str | None = None, lpc: int | None = None,
-                  kernel: str | None = None, timing: bool = True):
+                  kernel: str | None = None, timing: bool = True, want_viol: bool = True):
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
         horizon = 0
         if dist is not None:
             dist = np.ascontiguousarray(dist, dtype=np.float64)
             horizon = dist.shape[1]
-        viol = np.empty(m_grid, dtype=np.uint32)
+        viol = np.empty(m_grid, dtype=np.uint32) if want_viol else None
         pbits = np.empty((m_grid, (n_sim + 31) // 32), dtype=np.uint32) if want_pbits else None
         res = GridResult()
         flags = (RG_ABANDON if abandon else 0) | _RNG_FLAGS[rng_mode] | _LPC_FLAGS[lpc] | \

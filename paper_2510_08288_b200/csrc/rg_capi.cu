@@ -13,6 +13,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <string>
 
 #include "../../include/refgov_b200.h"
@@ -139,6 +140,8 @@ struct rg_ctx {
     DevBuf dist_raw, soa, S, steps, pbits, rows, vrows, tmp_a, tmp_b, kap_k, fnd_k, cel_k,
         erl_k, path_k, path_o;
     HostBuf h_stage;
+    HostBuf h_out;                  // zero-copy grid result block (pinned, UVA-mapped)
+    unsigned long long seq_ctr = 0; // grid-step publication tokens
 };
 
 namespace {
@@ -410,6 +413,7 @@ int32_t rg_destroy(rg_ctx* ctx) {
                       &ctx->e_violout};
     for (DevBuf* b : bufs) b->release();
     ctx->h_stage.release();
+    ctx->h_out.release();
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -569,6 +573,32 @@ int32_t rg_fill(rg_ctx* ctx, const rg_problem* prob, const double* x0, const dou
     return RG_OK;
 }
 
+// Spin until the grid step publishes `token` in the pinned result block.  The
+// stream is polled now and then so a failed launch surfaces as an error
+// instead of a hang.
+static cudaError_t wait_token(rg_ctx* ctx, volatile rg::GridOut* ho, unsigned long long token) {
+    for (unsigned long n = 1;; ++n) {
+        if (ho->seq == token) break;
+        if ((n & 1023u) == 0) {
+            const cudaError_t q = cudaStreamQuery(ctx->stream);
+            if (q == cudaSuccess) {  // stream drained: the token must be there now
+                if (ho->seq == token) break;
+                return cudaErrorUnknown;
+            }
+            if (q != cudaErrorNotReady) return q;
+        }
+#if defined(__x86_64__)
+        __builtin_ia32_pause();
+#endif
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    return cudaSuccess;
+}
+
+static int32_t unpack_grid(rg_ctx* ctx, const char* h, uint32_t* row_viol, int32_t m_grid,
+                           rg_grid_result* out, uint32_t* pbits_host, size_t pbits_bytes,
+                           bool timed);
+
 static int32_t read_grid(rg_ctx* ctx, uint32_t* row_viol, int32_t m_grid, rg_grid_result* out,
                          uint32_t* pbits_host, size_t pbits_bytes, bool timed) {
     const size_t bytes = kOutHead + viol_bytes(m_grid) + pbits_bytes;
@@ -576,6 +606,12 @@ static int32_t read_grid(rg_ctx* ctx, uint32_t* row_viol, int32_t m_grid, rg_gri
     char* h = ctx->h_stage.as<char>();
     RG_CUDA(cudaMemcpyAsync(h, ctx->g_out.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
     RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return unpack_grid(ctx, h, row_viol, m_grid, out, pbits_host, pbits_bytes, timed);
+}
+
+static int32_t unpack_grid(rg_ctx* ctx, const char* h, uint32_t* row_viol, int32_t m_grid,
+                           rg_grid_result* out, uint32_t* pbits_host, size_t pbits_bytes,
+                           bool timed) {
     const rg::GridOut* ho = reinterpret_cast<const rg::GridOut*>(h);
     if (row_viol) memcpy(row_viol, h + kOutHead, m_grid * sizeof(unsigned));
     if (pbits_host) memcpy(pbits_host, h + kOutHead + viol_bytes(m_grid), pbits_bytes);
@@ -591,6 +627,7 @@ static int32_t read_grid(rg_ctx* ctx, uint32_t* row_viol, int32_t m_grid, rg_gri
         out->kernel_ms = (float)((double)ho->kernel_ns * 1e-6);  // device globaltimer span
         if (timed) {
             float ms = 0.f;
+            cudaEventSynchronize(ctx->ev1);
             if (cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) == cudaSuccess) out->kernel_ms = ms;
             cudaGetLastError();
         }
@@ -646,8 +683,16 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
     a.pwords = (n_sim + 31) / 32;
     const size_t pbytes = pbits ? (size_t)m_grid * a.pwords * sizeof(unsigned) : 0;
     const bool pbits_in_block = pbits && !(flags & RG_DEVICE_PTRS);
-    RG_CUDA(ctx->g_out.ensure(kOutHead + viol_bytes(m_grid) + (pbits_in_block ? pbytes : 0)));
-    char* blk = ctx->g_out.as<char>();
+    // synchronous host-pointer calls: results land in pinned host memory and the
+    // call returns when the kernel publishes its token (no copy, no stream sync)
+    const bool zero_copy = !(flags & (RG_ASYNC | RG_DEVICE_PTRS));
+    const size_t blk_bytes = kOutHead + viol_bytes(m_grid) + (pbits_in_block ? pbytes : 0);
+    RG_CUDA(ctx->g_out.ensure(blk_bytes));
+    if (zero_copy) RG_CUDA(ctx->h_out.ensure(blk_bytes));
+    char* blk = zero_copy ? ctx->h_out.as<char>() : ctx->g_out.as<char>();
+    a.host_out = zero_copy ? 1 : 0;
+    a.seq_token = ++ctx->seq_ctr;
+    if (zero_copy) reinterpret_cast<volatile rg::GridOut*>(blk)->seq = 0ull;
     a.out = reinterpret_cast<rg::GridOut*>(blk);
     a.viol_out = reinterpret_cast<unsigned*>(blk + kOutHead);
     const bool abandon = (flags & RG_ABANDON) && !pbits;
@@ -659,8 +704,10 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
     a.occ_cap = occ_cap_for(ctx, (n_sim * lpc + a.tpb - 1) / a.tpb * m_grid, a.tpb);
     a.smem_per_sm = ctx->smem_per_sm;
     a.smem_reserved = ctx->smem_reserved;
-    if (pbits && lpc > 1)  // lanes OR their bits in
-        RG_CUDA(cudaMemsetAsync(a.pbits, 0, pbytes, ctx->stream));
+    if (pbits && lpc > 1) {  // lanes OR their bits in
+        if (zero_copy) memset(a.pbits, 0, pbytes);
+        else RG_CUDA(cudaMemsetAsync(a.pbits, 0, pbytes, ctx->stream));
+    }
     const bool timed = !(flags & RG_NO_TIMING);
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
     if (kernel == 2) {
@@ -680,6 +727,11 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
             RG_CUDA(cudaMemcpyAsync(row_viol, a.viol_out, m_grid * sizeof(unsigned),
                                     cudaMemcpyDeviceToDevice, ctx->stream));
         return RG_OK;
+    }
+    if (zero_copy) {
+        RG_CUDA(wait_token(ctx, reinterpret_cast<volatile rg::GridOut*>(blk), a.seq_token));
+        return unpack_grid(ctx, blk, row_viol, m_grid, out, pbits_in_block ? pbits : nullptr,
+                           pbits_in_block ? pbytes : 0, timed);
     }
     if (row_viol && (flags & RG_DEVICE_PTRS)) {
         RG_CUDA(cudaMemcpyAsync(row_viol, a.viol_out, m_grid * sizeof(unsigned),

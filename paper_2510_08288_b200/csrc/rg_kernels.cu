@@ -234,7 +234,8 @@ __device__ __forceinline__ void grid_finalize(const GridArgs& a) {
     __shared__ bool s_last;
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
+        if (a.host_out) __threadfence_system();  // this block's P bits reach the host first
+        else __threadfence();
         const unsigned total = gridDim.x * gridDim.y;
         s_last = atomicAdd(a.ticket, 1u) == total - 1;
     }
@@ -293,11 +294,13 @@ __device__ __forceinline__ void grid_finalize(const GridArgs& a) {
             a.out->overflows = (long long)ovf;
             a.out->abandoned = (long long)aband;
             a.out->sims_run = (long long)n_active * a.n_sim;
-            a.out->seq += 1;
             if (a.t0) {
                 a.out->kernel_ns = global_ns() - *(volatile unsigned long long*)a.t0;
                 *a.t0 = ~0ull;
             }
+            // publish: every result word above (and every block's P bits) before seq
+            __threadfence_system();
+            *(volatile unsigned long long*)&a.out->seq = a.seq_token;
         }
     }
     __syncthreads();

@@ -74,6 +74,10 @@ struct GridArgs {
     // occupancy cap (host side of the launch): at most occ_cap blocks per SM,
     // enforced with dynamic shared memory; 0 = no cap
     int occ_cap, smem_per_sm, smem_reserved;
+    // out/viol_out/pbits live in pinned host memory (zero-copy): system-scope
+    // fences before the ticket, and out->seq = seq_token published last
+    int host_out;
+    unsigned long long seq_token;
 };
 
 // Batch of independent governor instances (episodes): one launch covers

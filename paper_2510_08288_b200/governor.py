@@ -408,7 +408,7 @@ def robust_rg_parallel(plant, x_t, state, r_t, cset, scenarios, config, backend=
     ctx = _capi.context(device)
     res, viol, pbits = ctx.grid_step(prob, x_t, state.v_prev, r_t, config.m_grid,
                                      config.prefix_mode, dist, n_sim, stream, want_pbits=keep,
-                                     abandon=not keep, timing=False)
+                                     abandon=not keep, timing=False, want_viol=False)
     n_dup = 0
     if res.ss_pruned_rows or res.dedup_rows:
         # rows the device gated or deduplicated: the host's loop (governor.py:302-317)
