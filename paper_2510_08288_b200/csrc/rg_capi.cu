@@ -667,6 +667,7 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
     if (use_rng && want_stage(n_sim, prob->j_star, flags)) {
         if ((rc = stage_rng(ctx, rng, n_sim, prob->j_star, &a.soa, &a.ld))) return rc;
         use_rng = false;
+        a.pdl = getenv("RG_NO_PDL") ? 0 : 1;  // k_gen_soa is the kernel right before
     } else if (use_rng) {
         a.stream = make_stream(rng);
         a.k0 = rng->k0;

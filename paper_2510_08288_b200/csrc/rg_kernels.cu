@@ -101,6 +101,10 @@ __global__ void k_sample(SampleArgs a) {
 // one thread per (scenario, step); lanes run over scenarios, so stores coalesce.
 __global__ void k_gen_soa(ScenarioStream st, int64_t k0, int64_t n_sim, int32_t j_star,
                           int64_t ld, double* __restrict__ dst) {
+    // a grid step launched behind this kernel with programmatic stream
+    // serialization may start its prologue now; it waits (griddepcontrol.wait)
+    // for this grid's completion before it reads the block
+    asm volatile("griddepcontrol.launch_dependents;");
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int32_t j = blockIdx.y;
     if (k >= n_sim || j >= j_star) return;
@@ -329,6 +333,9 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid(GridArgs a) {
         }
     }
     __syncthreads();
+    // staged scenarios: the generator launched just before may still be running
+    // (programmatic dependent launch); no-op otherwise
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int src_i = s_src;
     const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPC;
     const bool lead = threadIdx.x % LPC == 0;
@@ -937,14 +944,33 @@ size_t occ_cap_smem(Kern kern, int cap, int smem_per_sm, int reserved) {
     return dyn;
 }
 
+// Launch with programmatic stream serialization (PDL) when `pdl`: the grid may
+// start while the previous kernel on the stream (k_gen_soa) is still running.
+template <class Kern, class Args>
+cudaError_t launch_ex(Kern kern, dim3 grid, int block, size_t smem, cudaStream_t s, bool pdl,
+                      const Args& a) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = pdl ? attr : nullptr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
 cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, int lpc,
                         cudaStream_t s) {
     dim3 grid(blocks_for(a.n_sim * lpc, a.tpb), (unsigned)a.m_grid);
-#define RG_GRID(F, R, P, L)                                                            \
-    k_grid<F, R, P, L><<<grid, a.tpb,                                                  \
-                         occ_cap_smem(k_grid<F, R, P, L>, a.occ_cap, a.smem_per_sm,    \
-                                      a.smem_reserved),                                \
-                         s>>>(a)
+    cudaError_t e = cudaSuccess;
+#define RG_GRID(F, R, P, L)                                                              \
+    e = launch_ex(k_grid<F, R, P, L>, grid, a.tpb,                                       \
+                  occ_cap_smem(k_grid<F, R, P, L>, a.occ_cap, a.smem_per_sm,             \
+                               a.smem_reserved),                                         \
+                  s, a.pdl != 0, a)
 #define RG_GRID_L(L)                                                             \
     do {                                                                         \
         if (fma) {                                                               \
@@ -958,6 +984,7 @@ cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, int lp
     RG_DISPATCH_LPC(lpc, RG_GRID_L);
 #undef RG_GRID_L
 #undef RG_GRID
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

@@ -78,6 +78,7 @@ struct GridArgs {
     // fences before the ticket, and out->seq = seq_token published last
     int host_out;
     unsigned long long seq_token;
+    int pdl;  // launched behind k_gen_soa with programmatic stream serialization
 };
 
 // Batch of independent governor instances (episodes): one launch covers
