@@ -28,6 +28,11 @@
 #ifndef RG_TANH_WITH
 #define RG_TANH_WITH 1
 #endif
+#ifndef RG_UNROLL
+#define RG_UNROLL 2
+#endif
+#define RG_PRAGMA(x) _Pragma(#x)
+#define RG_UNROLL_PRAGMA(n) RG_PRAGMA(unroll n)
 
 namespace rg {
 
@@ -335,6 +340,7 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
     double y2 = add(add(y1, mul(p.c, s1.s2)), dj1.d1);  // x2 before step j+2
     double dA0 = dj0.d0, dA2 = dj0.d2;  // x1/x3 disturbances of step j
     double dB0 = dj1.d0, dB2 = dj1.d2;  // ... and of step j+1
+    RG_UNROLL_PRAGMA(RG_UNROLL)
     for (int32_t j = 0; j < J; ++j) {
         const D3 dn = fetch(j + 2);
         // step j+2's x2 chain and step j's x1/x3: independent of the tanh
