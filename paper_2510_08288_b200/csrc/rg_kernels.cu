@@ -151,7 +151,8 @@ template <bool FMA, bool RNG, int LPC>
 __global__ void __launch_bounds__(128, RG_GRID_MINB) k_fill(FillArgs a) {
     const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPC;
     const bool live = k < a.n_sim;
-    if (LPC == 1 && !live) return;
+    constexpr bool W = LPC == 1 && RG_GRID_WARP;  // whole warps run the rollout
+    if (LPC == 1 && !W && !live) return;
     const int32_t row = a.rows[blockIdx.y];
     const double v = a.v_rows[row];
     const CellConst c = make_cell(a.p);
@@ -160,11 +161,13 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_fill(FillArgs a) {
     int st;
     if (RNG) {
         RngSource src{a.stream, scenario_key(a.stream, (uint64_t)(a.k0 + kk))};
-        st = rollout<FMA, false, LPC>(c, a.x0[0], a.x0[1], a.x0[2], v, src, steps, nullptr, live);
+        st = rollout<FMA, false, LPC, RngSource, W>(c, a.x0[0], a.x0[1], a.x0[2], v, src, steps,
+                                                    nullptr, live);
     } else {
         __shared__ double ring[2 * 3 * kRingStride];
         SoaSource src{a.soa + kk, a.ld, ring + threadIdx.x};
-        st = rollout<FMA, false, LPC>(c, a.x0[0], a.x0[1], a.x0[2], v, src, steps, nullptr, live);
+        st = rollout<FMA, false, LPC, SoaSource, W>(c, a.x0[0], a.x0[1], a.x0[2], v, src, steps,
+                                                    nullptr, live);
     }
     if (live && threadIdx.x % LPC == 0) {
         a.S[(int64_t)row * a.n_sim + k] = (uint8_t)st;
@@ -512,7 +515,8 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid_batch(BatchArgs a) {
         const bool live = k < a.n_sim;
         int st = kOk;
         int32_t steps = a.p.j_star;
-        if (live || LPC > 1) {
+        constexpr bool W = LPC == 1 && RG_GRID_WARP;  // whole warps run the rollout
+        if (live || LPC > 1 || W) {
             ScenarioStream ss;
             ss.hs = a.hs[e];
             for (int c = 0; c < 3; ++c) {
@@ -521,8 +525,8 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid_batch(BatchArgs a) {
             }
             RngSource src{ss, scenario_key(ss, (uint64_t)(a.k0 + (live ? k : 0)))};
             const double* x0 = a.x0 + 3 * (int64_t)e;
-            st = rollout<FMA, POLL, LPC>(make_cell(a.p), x0[0], x0[1], x0[2], s_v, src, steps,
-                                         viol + i, live);
+            st = rollout<FMA, POLL, LPC, RngSource, W>(make_cell(a.p), x0[0], x0[1], x0[2], s_v,
+                                                       src, steps, viol + i, live);
         }
         const bool cnt = live && lead;
         const unsigned bad = __ballot_sync(0xffffffffu, cnt && st != kOk && st != kAbandoned);
@@ -577,7 +581,11 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_bisect(BisectArgs a) {
     const bool lead = threadIdx.x % LPC == 0;
     double kopt = 1.0;
     int found = 1, cells = 0, early = 0;
-    if (live || LPC > 1) {
+    // U: every lane of the warp walks the candidates (LPC > 1 shuffles, or the
+    // warp-uniform one-lane-per-cell rollout); finished lanes keep it company
+    constexpr bool W = LPC == 1 && RG_GRID_WARP;
+    constexpr bool U = LPC > 1 || W;
+    if (live || U) {
         const int64_t kk = live ? k : 0;
         const CellConst c = make_cell(a.p);
         RngSource rsrc{};
@@ -593,7 +601,7 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_bisect(BisectArgs a) {
         // live = false and only keep the warp company.
         bool fin = !live;
         for (int it = -1; it < a.n_kappa; ++it) {
-            if (LPC == 1) {
+            if (!U) {
                 if (fin) break;
             } else if (__all_sync(0xffffffffu, fin)) {
                 break;
@@ -603,17 +611,18 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_bisect(BisectArgs a) {
             const bool run = !fin && ss_gate(v, a.p);
             bool ok = false;
             int32_t sr = 0;
-            if (run || LPC > 1) {
+            if (run || U) {
                 int st;
                 if (SRC == 1)
-                    st = rollout<FMA, false, LPC>(c, a.x0[0], a.x0[1], a.x0[2], v, rsrc, sr,
-                                                  nullptr, run);
+                    st = rollout<FMA, false, LPC, RngSource, W>(c, a.x0[0], a.x0[1], a.x0[2], v,
+                                                                rsrc, sr, nullptr, run);
                 else if (SRC == 2)
-                    st = rollout<FMA, false, LPC>(c, a.x0[0], a.x0[1], a.x0[2], v, ssrc, sr,
-                                                  nullptr, run);
+                    st = rollout<FMA, false, LPC, SoaSource, W>(c, a.x0[0], a.x0[1], a.x0[2], v,
+                                                                ssrc, sr, nullptr, run);
                 else
-                    st = rollout<FMA, false, LPC>(c, a.x0[0], a.x0[1], a.x0[2], v,
-                                                  ZeroSource{}, sr, nullptr, run);
+                    st = rollout<FMA, false, LPC, ZeroSource, W>(c, a.x0[0], a.x0[1], a.x0[2],
+                                                                 v, ZeroSource{}, sr, nullptr,
+                                                                 run);
                 ok = run && st == kOk;
                 if (!run) sr = 0;
             }
