@@ -19,15 +19,6 @@
 
 #include <type_traits>
 
-#ifndef RG_PIPE2
-#define RG_PIPE2 1
-#endif
-#ifndef RG_SMALL_TANH
-#define RG_SMALL_TANH 1
-#endif
-#ifndef RG_TANH_WITH
-#define RG_TANH_WITH 1
-#endif
 #ifndef RG_UNROLL
 #define RG_UNROLL 2
 #endif
@@ -223,11 +214,7 @@ template <bool FMA, int LPC>
 __device__ __forceinline__ void step_tanh(double x2, double a2, double b2, double c2,
                                           double& u1, double& u2, double& u3, double& u4) {
     if constexpr (LPC == 1) {
-#if RG_SMALL_TANH
         tanh4_auto<FMA>(x2, a2, b2, c2, u1, u2, u3, u4);
-#else
-        tanh4<FMA>(x2, a2, b2, c2, u1, u2, u3, u4);
-#endif
     } else if constexpr (LPC == 2) {
         const bool q = (threadIdx.x & 1u) != 0;
         const double in[2] = {q ? a2 : x2, q ? c2 : b2};
@@ -255,13 +242,10 @@ __device__ __forceinline__ void step_tanh(double x2, double a2, double b2, doubl
 // One cell.  POLL: every 32 steps check a row-level "already infeasible"
 // flag and abandon (used only when the caller wants verdicts, not P).
 //
-// Software-pipelined by one step: iteration j finishes x1/x3 of step j with
-// the tanh values computed in iteration j-1, while it already runs the x2
-// chain and the four tanh of step j+1 (they need x2_{j+1} only).  The two
-// halves are independent, so their instruction streams interleave; every
-// value is still produced by the reference's operations on the reference's
-// operands, so the bits are those of sfc_step.  A step j+1 that is never
-// reached (early exit) only wastes its speculative tanh work.
+// Software-pipelined two steps deep (see the loop): every value is still
+// produced by the reference's operations on the reference's operands, so the
+// bits are those of sfc_step.  Steps past an early exit or past the horizon are
+// computed speculatively and never observed.
 //
 // LPC > 1: all 32 lanes of the warp run the loop until every cell of the warp
 // is done (lanes of finished or out-of-range cells keep computing throwaway
@@ -294,7 +278,6 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
     } else {
         if (__all_sync(0xffffffffu, done)) return status;
     }
-#if RG_PIPE2
     // Pipelined two steps deep: iteration j finishes x1/x3 of step j (tanh
     // values from iteration j-1), evaluates the four tanh of step j+1
     // (arguments from iteration j-1) and runs the x2 chain of step j+2.  The
@@ -358,12 +341,9 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
             bad_bnd = !in_bounds(x1, p.ylo, p.yhi);
         };
         double u1, u2, u3, u4;
-#if RG_SMALL_TANH && RG_TANH_WITH
         if constexpr (LPC == 1) {
             tanh4_with<FMA, WARP>(g0, g1, g2, g3, u1, u2, u3, u4, side);
-        } else
-#endif
-        {
+        } else {
             step_tanh<FMA, LPC>(g0, g1, g2, g3, u1, u2, u3, u4);
             side();
         }
@@ -411,73 +391,6 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
         dB0 = dn.d0;
         dB2 = dn.d2;
     }
-#else
-    // prologue: tanh values of step 0 and x2 after step 0
-    D3 d;
-    if constexpr (kRing) {
-        src.issue(0, 0);
-        cp_async_commit();
-        src.issue(J > 1 ? 1 : 0, 1);
-        cp_async_commit();
-        cp_async_wait<1>();
-        d = src.read(0);
-    } else {
-        d = src.load(0);
-    }
-    X2Stage st = x2_stage<FMA>(x2, v, p);
-    double t1, t2, t3, t4;
-    step_tanh<FMA, LPC>(x2, st.a2, st.b2, st.c2, t1, t2, t3, t4);
-    double x2n = add(add(x2, mul(p.c, st.s2)), d.d1);
-    for (int32_t j = 0; j < J; ++j) {
-        // step j's slot was drained into `d` last iteration: refill it with step j+2
-        if constexpr (kRing) {
-            if (j + 2 < J) src.issue(j + 2, j & 1);
-            cp_async_commit();
-        }
-        // step j+1's x2 chain and tanh values (speculative past an exit)
-        const X2Stage sn = x2_stage<FMA>(x2n, v, p);
-        double u1, u2, u3, u4;
-        step_tanh<FMA, LPC>(x2n, sn.a2, sn.b2, sn.c2, u1, u2, u3, u4);
-        D3 dn;
-        if constexpr (kRing) {
-            cp_async_wait<1>();  // step j+1 landed (issued one iteration ago)
-            dn = src.read((j + 1) & 1);
-        } else {
-            dn = src.load(j + 1 < J ? j + 1 : j);
-        }
-        const double x2nn = add(add(x2n, mul(p.c, sn.s2)), dn.d1);
-        // step j's x1/x3
-        x13_update<FMA>(x1, x3, t1, t2, t3, t4, p, d.d0, d.d2);
-        if (!done) {
-            if (!(fabs(x1) <= kStateLimit && fabs(x2n) <= kStateLimit &&
-                  fabs(x3) <= kStateLimit)) {
-                steps = j + 1;
-                status = kOverflow;
-                done = true;
-            } else if (!in_bounds(x1, p.ylo, p.yhi)) {
-                steps = j + 1;
-                status = kViolated;
-                done = true;
-            } else if (POLL && (j & 31) == 31 &&
-                       *(volatile const unsigned int*)dead != 0u) {
-                steps = j + 1;
-                status = kAbandoned;
-                done = true;
-            }
-        }
-        if constexpr (LPC == 1) {
-            if (done) break;
-        } else {
-            if (__all_sync(0xffffffffu, done)) break;
-        }
-        t1 = u1;
-        t2 = u2;
-        t3 = u3;
-        t4 = u4;
-        x2n = x2nn;
-        d = dn;
-    }
-#endif
     if constexpr (kRing) cp_async_wait<0>();  // no copy may land after we leave
     return status;
 }
