@@ -232,6 +232,37 @@ RG_API int32_t rg_bisect_linear(rg_ctx *ctx, const rg_linear_plant *plant,
                                 rg_bisect_result *out, int32_t flags);
 
 /* FP64 roofline probe: independent DFMA chains; returns achieved FLOP/s. */
+/* Joint bisection (the north-star form of Alg. 2): every
+ * scenario tests the same kappa per iteration (kappa = 1 first, then
+ * n_kappa midpoints of [0, 1], governor.py:407-431) and the violations are
+ * OR-reduced into one device flag, with every scenario abandoning its rollout
+ * as soon as the flag is raised.  kappa and found equal robust_rg_sequential's
+ * whenever every scenario's feasible set is a down-set in kappa (SURVEY.md
+ * §8(a) row A9); cells/early count like Alg. 2 summed over scenarios, except
+ * that abandoned rollouts are not early terminations.
+ *
+ * rg_bisect_joint runs the whole search on one device: n_kappa + 1 kernels
+ * enqueued back to back, the decision taken by each kernel's last block, one
+ * host synchronisation at the end.  The begin/iter/flag/decide/end calls
+ * expose the same search one iteration at a time for a scenario-sharded run:
+ * rg_joint_iter(ctx, it, 0) rolls the local shard out, the caller all-reduces
+ * (MAX) the uint32 at rg_joint_flag on the context's stream, and
+ * rg_joint_decide(ctx, it) applies the decision on every rank.  kernel_ms is
+ * the event span from rg_joint_begin to rg_joint_end.
+ * Replaces: robust_rg_sequential governor.py:469-517 (joint form). */
+RG_API int32_t rg_bisect_joint(rg_ctx *ctx, const rg_problem *prob, const double *x0,
+                               double v_prev, double r, int32_t n_kappa, const double *dist,
+                               int64_t n_sim, int64_t horizon, const rg_scenarios *rng,
+                               rg_bisect_result *out, int32_t flags);
+RG_API int32_t rg_joint_begin(rg_ctx *ctx, const rg_problem *prob, const double *x0,
+                              double v_prev, double r, int32_t n_kappa, const double *dist,
+                              int64_t n_sim, int64_t horizon, const rg_scenarios *rng,
+                              int32_t flags);
+RG_API int32_t rg_joint_iter(rg_ctx *ctx, int32_t it, int32_t fold);
+RG_API int32_t rg_joint_flag(rg_ctx *ctx, void **dev_flag);
+RG_API int32_t rg_joint_decide(rg_ctx *ctx, int32_t it);
+RG_API int32_t rg_joint_end(rg_ctx *ctx, rg_bisect_result *out);
+
 RG_API int32_t rg_fp64_peak(rg_ctx *ctx, double *flops_per_s);
 
 #ifdef __cplusplus

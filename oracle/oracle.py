@@ -328,6 +328,50 @@ def robust_sequential(h, x0, v_prev, r, lo, hi, tlo, thi, dist, j_star, n_kappa)
     return kopt, update_setpoint(v_prev, r, kopt), feas, cells, early, per
 
 
+def joint_bisect(h, x0, v_prev, r, lo, hi, tlo, thi, dist, j_star, n_kappa, verdict=None):
+    """Joint bisection: the candidate sequence of
+    _bisect_kappa (governor.py:407-431), each candidate tested on every scenario
+    at once and feasible iff all of them stay inside the set.
+
+    ``verdict(v) -> (all_ok, n_early)`` may replace the scenario loop (the
+    sharded tests pass a rank-local one and OR the flags).  Returns
+    (kappa, found, path) with path = [(kappa, feasible), ...].
+    """
+    n = dist.shape[0]
+
+    def default_verdict(v):
+        ok_all, early = True, 0
+        for k in range(n):
+            st, sr = cell_sfc(h, x0, v, dist[k], j_star, lo, hi)
+            ok_all &= st == CELL_OK
+            early += int(st != CELL_OK and sr < j_star)
+        return ok_all, early
+
+    verdict = verdict or default_verdict
+    path = []
+
+    def feasible_at(kappa):
+        v = update_setpoint(v_prev, r, kappa)
+        if not ss_ok(v, tlo, thi):
+            return False
+        return verdict(v)[0]
+
+    ok = feasible_at(1.0)
+    path.append((1.0, ok))
+    if ok:
+        return 1.0, True, path
+    klo, khi, kopt, found = 0.0, 1.0, 0.0, False
+    for _ in range(n_kappa):
+        kappa = 0.5 * (klo + khi)
+        ok = feasible_at(kappa)
+        path.append((kappa, ok))
+        if ok:
+            kopt, found, klo = kappa, True, kappa
+        else:
+            khi = kappa
+    return kopt, found, path
+
+
 def bisect_all_c(h, x0, v_prev, r, lo, hi, vlo, vhi, dist, j_star, n_kappa):
     """The same scenario loop in C with the steady-state gate given as the
     admissible setpoint interval [vlo, vhi] (for large N / CPU timing)."""

@@ -131,6 +131,14 @@ SIGNATURES = {
     "rg_bisect_linear": (_i32, [_vp, ctypes.POINTER(LinearPlant), ctypes.POINTER(Problem), _vp,
                                 _d, _d, _i32, _vp, _i64, _i64, ctypes.POINTER(Scenarios), _vp,
                                 _vp, _vp, _vp, ctypes.POINTER(BisectResult), _i32]),
+    "rg_bisect_joint": (_i32, [_vp, ctypes.POINTER(Problem), _vp, _d, _d, _i32, _vp, _i64, _i64,
+                               ctypes.POINTER(Scenarios), ctypes.POINTER(BisectResult), _i32]),
+    "rg_joint_begin": (_i32, [_vp, ctypes.POINTER(Problem), _vp, _d, _d, _i32, _vp, _i64, _i64,
+                              ctypes.POINTER(Scenarios), _i32]),
+    "rg_joint_iter": (_i32, [_vp, _i32, _i32]),
+    "rg_joint_flag": (_i32, [_vp, ctypes.POINTER(_vp)]),
+    "rg_joint_decide": (_i32, [_vp, _i32]),
+    "rg_joint_end": (_i32, [_vp, ctypes.POINTER(BisectResult)]),
     "rg_fp64_peak": (_i32, [_vp, ctypes.POINTER(_d)]),
 }
 
@@ -296,6 +304,50 @@ class Context:
                                  _RNG_FLAGS[rng_mode] | _LPC_FLAGS[lpc]))
         per = (kap, fnd, cel, erl) if per_scenario else None
         return res, per, ((pk, po) if paths else None)
+
+    def bisect_joint(self, prob: Problem, x0, v_prev, r, n_kappa, dist, n_sim,
+                     scen: Scenarios | None, rng_mode: str | None = None) -> "BisectResult":
+        """Joint bisection on this device (rg_bisect_joint)."""
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        horizon = 0
+        if dist is not None:
+            dist = np.ascontiguousarray(dist, dtype=np.float64)
+            horizon = dist.shape[1]
+        res = BisectResult()
+        check(self.lib.rg_bisect_joint(self.handle, ctypes.byref(prob), _p(x0), float(v_prev),
+                                       float(r), int(n_kappa), _p(dist), int(n_sim),
+                                       int(horizon),
+                                       ctypes.byref(scen) if scen is not None else None,
+                                       ctypes.byref(res), _RNG_FLAGS[rng_mode]))
+        return res
+
+    def joint_begin(self, prob: Problem, x0, v_prev, r, n_kappa, dist, n_sim,
+                    scen: Scenarios | None) -> None:
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        horizon = 0
+        if dist is not None:
+            dist = np.ascontiguousarray(dist, dtype=np.float64)
+            horizon = dist.shape[1]
+        check(self.lib.rg_joint_begin(self.handle, ctypes.byref(prob), _p(x0), float(v_prev),
+                                      float(r), int(n_kappa), _p(dist), int(n_sim),
+                                      int(horizon),
+                                      ctypes.byref(scen) if scen is not None else None, 0))
+
+    def joint_iter(self, it: int, fold: bool) -> None:
+        check(self.lib.rg_joint_iter(self.handle, int(it), int(bool(fold))))
+
+    def joint_flag_ptr(self) -> int:
+        p = _vp()
+        check(self.lib.rg_joint_flag(self.handle, ctypes.byref(p)))
+        return int(p.value)
+
+    def joint_decide(self, it: int) -> None:
+        check(self.lib.rg_joint_decide(self.handle, int(it)))
+
+    def joint_end(self) -> "BisectResult":
+        res = BisectResult()
+        check(self.lib.rg_joint_end(self.handle, ctypes.byref(res)))
+        return res
 
     def grid_step_batch(self, prob: Problem, x0, v_prev, r, seeds, k0, n_sim, lo, span,
                         m_grid, prefix_mode=False, abandon=True, want_viol=False, lpc=None):

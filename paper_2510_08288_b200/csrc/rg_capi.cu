@@ -141,6 +141,9 @@ struct rg_ctx {
         erl_k, path_k, path_o;
     HostBuf h_stage;
     HostBuf h_out;                  // zero-copy grid result block (pinned, UVA-mapped)
+    DevBuf j_state;                 // joint bisection state (rg::JointState)
+    rg::JointArgs j_args{};         // the joint search in progress (rg_joint_begin)
+    int j_src = -1;                 // its scenario source; -1 = none begun
     unsigned long long seq_ctr = 0; // grid-step publication tokens
 };
 
@@ -405,7 +408,7 @@ int32_t rg_destroy(rg_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     DevBuf* bufs[] = {&ctx->g_viol, &ctx->g_early, &ctx->g_ovf, &ctx->g_aband, &ctx->g_src,
-                      &ctx->g_ticket, &ctx->g_t0, &ctx->g_out, &ctx->b_acc, &ctx->b_out,
+                      &ctx->g_ticket, &ctx->g_t0, &ctx->g_out, &ctx->j_state, &ctx->b_acc, &ctx->b_out,
                       &ctx->dist_raw, &ctx->soa, &ctx->S, &ctx->steps, &ctx->pbits, &ctx->rows,
                       &ctx->vrows, &ctx->tmp_a, &ctx->tmp_b, &ctx->kap_k, &ctx->fnd_k,
                       &ctx->cel_k, &ctx->erl_k, &ctx->path_k, &ctx->path_o, &ctx->e_in,
@@ -867,6 +870,124 @@ int32_t rg_bisect(rg_ctx* ctx, const rg_problem* prob, const double* x0, double 
         }
     }
     return RG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// joint bisection
+// ---------------------------------------------------------------------------
+
+int32_t rg_joint_begin(rg_ctx* ctx, const rg_problem* prob, const double* x0, double v_prev,
+                       double r, int32_t n_kappa, const double* dist, int64_t n_sim,
+                       int64_t horizon, const rg_scenarios* rng, int32_t flags) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    rg::JointArgs a{};
+    if ((rc = make_problem(prob, &a.p))) return rc;
+    if (!x0) return fail(RG_E_ARGS, "null x0");
+    if (n_kappa < 1) return fail(RG_E_ARGS, "n_kappa must be >= 1, got %d", n_kappa);
+    if (n_sim < 1) return fail(RG_E_ARGS, "n_sim must be >= 1");
+    if (dist && horizon < (int64_t)prob->j_star + 1)
+        return fail(RG_E_ARGS, "scenario horizon %lld too short: need >= j_star+1 = %d",
+                    (long long)horizon, prob->j_star + 1);
+    if (!isfinite(v_prev) || !isfinite(r)) return fail(RG_E_ARGS, "v_prev and r must be finite");
+    for (int i = 0; i < 3; ++i) a.x0[i] = x0[i];
+    a.v_prev = v_prev;
+    a.r = r;
+    a.n_kappa = n_kappa;
+    a.n_sim = n_sim;
+    int src = 0;
+    if (dist) {
+        src = 2;
+        if ((rc = stage_dist(ctx, dist, n_sim, horizon, prob->j_star, flags, &a.soa, &a.ld)))
+            return rc;
+    } else if (rng && want_stage(n_sim, prob->j_star, flags)) {
+        src = 2;
+        if ((rc = stage_rng(ctx, rng, n_sim, prob->j_star, &a.soa, &a.ld))) return rc;
+    } else if (rng) {
+        src = 1;
+        a.stream = make_stream(rng);
+        a.k0 = rng->k0;
+    }
+    RG_CUDA(ctx->j_state.ensure(sizeof(rg::JointState)));
+    a.st = ctx->j_state.as<rg::JointState>();
+    rg::JointState init{};
+    init.lo = 0.0;
+    init.hi = 1.0;
+    init.kopt = 0.0;
+    RG_CUDA(ctx->h_stage.ensure(sizeof(rg::JointState)));
+    memcpy(ctx->h_stage.p, &init, sizeof(init));
+    RG_CUDA(cudaMemcpyAsync(a.st, ctx->h_stage.p, sizeof(init), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    a.tpb = tpb_for(ctx, n_sim, 1);
+    a.fold = 1;
+    ctx->j_args = a;
+    ctx->j_src = src;
+    RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+    return RG_OK;
+}
+
+int32_t rg_joint_iter(rg_ctx* ctx, int32_t it, int32_t fold) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    if (ctx->j_src < 0) return fail(RG_E_ARGS, "no joint search begun (rg_joint_begin)");
+    if (it < -1 || it >= ctx->j_args.n_kappa)
+        return fail(RG_E_ARGS, "iteration %d outside [-1, %d)", it, ctx->j_args.n_kappa);
+    rg::JointArgs a = ctx->j_args;
+    a.fold = fold ? 1 : 0;
+    RG_CUDA(rg::launch_joint_roll(a, it, ctx->variant == rg::kTanhFma, ctx->j_src, ctx->stream));
+    return RG_OK;
+}
+
+int32_t rg_joint_decide(rg_ctx* ctx, int32_t it) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    if (ctx->j_src < 0) return fail(RG_E_ARGS, "no joint search begun (rg_joint_begin)");
+    RG_CUDA(rg::launch_joint_decide(ctx->j_args, it, ctx->stream));
+    return RG_OK;
+}
+
+int32_t rg_joint_flag(rg_ctx* ctx, void** dev_flag) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    if (ctx->j_src < 0) return fail(RG_E_ARGS, "no joint search begun (rg_joint_begin)");
+    if (!dev_flag) return fail(RG_E_ARGS, "null dev_flag");
+    *dev_flag = &ctx->j_args.st->viol;
+    return RG_OK;
+}
+
+int32_t rg_joint_end(rg_ctx* ctx, rg_bisect_result* out) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    if (ctx->j_src < 0) return fail(RG_E_ARGS, "no joint search begun (rg_joint_begin)");
+    RG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+    RG_CUDA(ctx->h_stage.ensure(sizeof(rg::JointState)));
+    rg::JointState* hs = ctx->h_stage.as<rg::JointState>();
+    RG_CUDA(cudaMemcpyAsync(hs, ctx->j_args.st, sizeof(rg::JointState), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (out) {
+        out->kappa = hs->kopt;
+        out->found = hs->found;
+        out->cells = (int64_t)hs->cells;
+        out->early = (int64_t)hs->early;
+        float ms = 0.f;
+        out->kernel_ms = cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) == cudaSuccess ? ms : 0.f;
+        cudaGetLastError();
+    }
+    ctx->j_src = -1;
+    return RG_OK;
+}
+
+int32_t rg_bisect_joint(rg_ctx* ctx, const rg_problem* prob, const double* x0, double v_prev,
+                        double r, int32_t n_kappa, const double* dist, int64_t n_sim,
+                        int64_t horizon, const rg_scenarios* rng, rg_bisect_result* out,
+                        int32_t flags) {
+    int32_t rc = rg_joint_begin(ctx, prob, x0, v_prev, r, n_kappa, dist, n_sim, horizon, rng,
+                                flags);
+    if (rc) return rc;
+    for (int32_t it = -1; it < n_kappa; ++it)
+        if ((rc = rg_joint_iter(ctx, it, 1))) return rc;
+    return rg_joint_end(ctx, out);
 }
 
 int32_t rg_grid_step_batch(rg_ctx* ctx, const rg_problem* prob, int32_t n_episodes,

@@ -257,10 +257,15 @@ __device__ __forceinline__ void step_tanh(double x2, double a2, double b2, doubl
 // throwaway values until every lane is done, the exit and the tanh range vote
 // are full-warp votes, and the per-step checks are predicated into the
 // iteration's single basic block (no divergent branches inside the loop).
-template <bool FMA, bool POLL, int LPC, class Src, bool WARP = false>
+//
+// RAISE (with WARP and POLL): a lane whose cell violates or overflows sets
+// *dead at once, so the other cells sharing the flag abandon at their next
+// poll (the joint bisection's OR-reduced violation flag).
+template <bool FMA, bool POLL, int LPC, class Src, bool WARP = false, bool RAISE = false>
 __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2, double x3,
                                        double v, const Src& src, int32_t& steps,
                                        const unsigned int* dead, bool live = true) {
+    static_assert(!RAISE || (WARP && POLL), "RAISE needs the polled warp-uniform form");
     static_assert(!WARP || LPC == 1, "WARP is the one-lane-per-cell form");
     constexpr bool kUniform = WARP || LPC > 1;  // all lanes run the loop together
     const int32_t J = p.j_star;
@@ -356,6 +361,7 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
             status = now ? code : status;
             steps = now ? j + 1 : steps;
             done = done || now;
+            if (RAISE && now && code != kAbandoned) atomicOr((unsigned int*)dead, 1u);
         } else if (!done) {
             if (bad_ovf) {
                 steps = j + 1;

@@ -571,6 +571,117 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid_batch(BatchArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// joint bisection: every scenario tests the same kappa per iteration
+// ---------------------------------------------------------------------------
+
+// The iteration's candidate, as governor.py:407-431 walks it: kappa = 1 first
+// (it < 0), then the midpoint of the bracket.
+__device__ __forceinline__ double joint_kappa(const volatile JointState* st, int it) {
+    return it < 0 ? 1.0 : mul(0.5, add(st->lo, st->hi));
+}
+
+// The decision after an iteration (governor.py:412-431 applied to the joint
+// verdict): kappa = 1 feasible ends the search; otherwise a feasible midpoint
+// raises the lower end, an infeasible one lowers the upper end.  Cells and
+// early terminations count like Alg. 2 summed over scenarios (a gated-out
+// candidate is an early termination of every scenario).
+__device__ void joint_decide(const JointArgs& a, int it, double kappa, bool gated_in,
+                             unsigned long long early_here) {
+    volatile JointState* st = a.st;
+    const bool feas = gated_in && st->viol == 0u;
+    st->cells += (unsigned long long)a.n_sim;
+    st->early += gated_in ? early_here : (unsigned long long)a.n_sim;
+    if (it < 0) {
+        if (feas) {
+            st->kopt = 1.0;
+            st->found = 1;
+            st->done = 1;
+        }
+    } else if (feas) {
+        st->kopt = kappa;
+        st->found = 1;
+        st->lo = kappa;
+    } else {
+        st->hi = kappa;
+    }
+    if (it == a.n_kappa - 1) st->done = 1;
+    st->viol = 0u;
+}
+
+template <bool FMA, int SRC>  // SRC: 0 zero (nominal), 1 rng, 2 soa
+__global__ void __launch_bounds__(128, RG_GRID_MINB) k_joint_roll(JointArgs a, int it) {
+    __shared__ int s_run;  // 0 search finished, 1 candidate gated out, 2 roll out
+    __shared__ double s_v, s_kappa;
+    __shared__ bool s_last;
+    __shared__ unsigned long long s_early;
+    if (threadIdx.x == 0) {
+        const volatile JointState* st = a.st;
+        if (st->done) {
+            s_run = 0;
+        } else {
+            const double kappa = joint_kappa(st, it);
+            const double v = update_setpoint(a.v_prev, a.r, kappa);
+            s_kappa = kappa;
+            s_v = v;
+            s_run = ss_gate(v, a.p) ? 2 : 1;
+        }
+    }
+    __syncthreads();
+    const int run = s_run;
+    if (run == 0) return;
+    if (run == 2) {
+        const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        const bool live = k < a.n_sim;
+        const int64_t kk = live ? k : 0;
+        const CellConst c = make_cell(a.p);
+        int32_t steps = 0;
+        int st;
+        unsigned* flag = &a.st->viol;
+        if (SRC == 1) {
+            RngSource src{a.stream, scenario_key(a.stream, (uint64_t)(a.k0 + kk))};
+            st = rollout<FMA, true, 1, RngSource, true, true>(c, a.x0[0], a.x0[1], a.x0[2], s_v,
+                                                              src, steps, flag, live);
+        } else if (SRC == 2) {
+            __shared__ double ring[2 * 3 * kRingStride];
+            SoaSource src{a.soa + kk, a.ld, ring + threadIdx.x};
+            st = rollout<FMA, true, 1, SoaSource, true, true>(c, a.x0[0], a.x0[1], a.x0[2], s_v,
+                                                              src, steps, flag, live);
+        } else {
+            st = rollout<FMA, true, 1, ZeroSource, true, true>(c, a.x0[0], a.x0[1], a.x0[2],
+                                                               s_v, ZeroSource{}, steps, flag,
+                                                               live);
+        }
+        // the flag is raised inside the rollout at the violating step; a cell
+        // that starts outside the set never enters the loop, so raise it here too
+        const bool bad = live && st != kOk && st != kAbandoned;
+        if (__ballot_sync(0xffffffffu, bad) && lane_id() == 0) atomicOr(flag, 1u);
+        warp_count_add(bad && steps < a.p.j_star, &a.st->early);
+    }
+    if (!a.fold) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&a.st->ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    __threadfence();
+    // the early terminations of this iteration were accumulated into st->early
+    // directly; joint_decide adds none for a rolled-out candidate
+    a.st->ticket = 0u;
+    joint_decide(a, it, s_kappa, run == 2, 0ull);
+}
+
+// Decision kernel for the sharded form: runs after the all-reduce of st->viol.
+__global__ void k_joint_decide(JointArgs a, int it) {
+    const volatile JointState* st = a.st;
+    if (st->done) return;
+    const double kappa = joint_kappa(st, it);
+    const double v = update_setpoint(a.v_prev, a.r, kappa);
+    joint_decide(a, it, kappa, ss_gate(v, a.p), 0ull);
+}
+
+// ---------------------------------------------------------------------------
 // exact Alg. 2: per-scenario bisection
 // ---------------------------------------------------------------------------
 
@@ -1041,6 +1152,23 @@ cudaError_t launch_grid_batch(const BatchArgs& a, bool fma, bool poll, int lpc, 
     } while (0)
     RG_DISPATCH_LPC(lpc, RG_BATCH);
 #undef RG_BATCH
+    return cudaGetLastError();
+}
+
+cudaError_t launch_joint_roll(const JointArgs& a, int it, bool fma, int src, cudaStream_t s) {
+    const unsigned blocks = (unsigned)((a.n_sim + a.tpb - 1) / a.tpb);
+#define RG_J(F, S) k_joint_roll<F, S><<<blocks, a.tpb, 0, s>>>(a, it)
+    if (fma) {
+        if (src == 1) RG_J(true, 1); else if (src == 2) RG_J(true, 2); else RG_J(true, 0);
+    } else {
+        if (src == 1) RG_J(false, 1); else if (src == 2) RG_J(false, 2); else RG_J(false, 0);
+    }
+#undef RG_J
+    return cudaGetLastError();
+}
+
+cudaError_t launch_joint_decide(const JointArgs& a, int it, cudaStream_t s) {
+    k_joint_decide<<<1, 1, 0, s>>>(a, it);
     return cudaGetLastError();
 }
 

@@ -164,6 +164,34 @@ struct BisectArgs {
     int tpb;
 };
 
+// Joint bisection: one candidate kappa for every
+// scenario per iteration, violations OR-reduced into one flag.
+struct JointState {
+    double lo, hi, kopt;
+    int found, done;
+    unsigned viol;    // OR of this iteration's violations (all-reduced across ranks when sharded)
+    unsigned ticket;  // last-block election for the folded decision
+    unsigned long long cells, early;
+    unsigned long long seq;
+};
+
+struct JointArgs {
+    ProblemDev p;
+    double x0[3];
+    double v_prev, r;
+    int32_t n_kappa;
+    int64_t n_sim, k0;
+    ScenarioStream stream;
+    const double* soa;
+    int64_t ld;
+    JointState* st;
+    int tpb;
+    int fold;  // 1: the last block decides (single GPU); 0: k_joint_decide after the all-reduce
+};
+
+cudaError_t launch_joint_roll(const JointArgs& a, int it, bool fma, int src, cudaStream_t s);
+cudaError_t launch_joint_decide(const JointArgs& a, int it, cudaStream_t s);
+
 cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s);
 cudaError_t launch_to_soa(const double* src, double* dst, int64_t n_sim, int64_t horizon,
                           int32_t j_star, int64_t ld, cudaStream_t s);

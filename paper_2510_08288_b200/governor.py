@@ -38,7 +38,7 @@ __all__ = ["BACKENDS", "GovernorConfig", "GovernorState", "KappaResult", "CellPr
            "update_setpoint", "grid_kappas", "fill_feasibility", "extract_kappa_opt",
            "bisection_rg", "robust_rg_sequential", "robust_rg_parallel", "probe_candidate",
            "check_candidate", "DIAG_CSV_HEADER", "CELL_OK", "CELL_VIOLATED", "CELL_OVERFLOW",
-           "robust_rg_parallel_batch"]
+           "robust_rg_parallel_batch", "robust_rg_joint"]
 
 # "gpu" is the reference's name for its device backend (governor.py:53); both
 # names select the CUDA device here.  CPU backends do not exist in this build.
@@ -522,6 +522,37 @@ def robust_rg_sequential(plant, x_t, state, r_t, cset, scenarios, config):
     state.v_prev = v
     return KappaResult(kappa_opt=kappa, v_applied=v, feasible=bool(res.found), diagnostics={
         "method": "sequential", "sims_run": int(res.cells), "early_terms": int(res.early),
+        "kernel_us": int(res.kernel_ms * 1e3),
+        "wall_us": int((time.perf_counter() - t0) * 1e6)})
+
+
+def robust_rg_joint(plant, x_t, state, r_t, cset, scenarios, config):
+    """Joint bisection: the scenario-robust step in the north-star form.
+
+    The candidate sequence of _bisect_kappa (governor.py:407-431), each
+    candidate tested on every scenario at once and feasible iff all stay inside
+    the set; one device search (rg_bisect_joint) with an OR-reduced violation
+    flag and early abandonment.  kappa_opt and feasible equal
+    robust_rg_sequential's whenever every scenario's feasible set is a down-set
+    in kappa; sims_run / early_terms count rollouts
+    started and early terminations over all scenarios and iterations.
+    """
+    x_t = _validate_state(plant, x_t)
+    if scenarios.n_sim != config.n_sim:
+        raise ConfigError(f"scenario count {scenarios.n_sim} does not match config.n_sim "
+                          f"{config.n_sim}")
+    _require_surrogate(plant)
+    dist, n_sim, stream = _source(scenarios, config.j_star)
+    prob, _, _, _ = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor,
+                              config.epsilon, config.tighten_mode, config.j_star, 0)
+    t0 = time.perf_counter()
+    ctx = _capi.context(getattr(config, "device", 0))
+    res = ctx.bisect_joint(prob, x_t, state.v_prev, r_t, config.n_kappa, dist, n_sim, stream)
+    kappa = float(res.kappa)
+    v = update_setpoint(state.v_prev, r_t, kappa)
+    state.v_prev = v
+    return KappaResult(kappa_opt=kappa, v_applied=v, feasible=bool(res.found), diagnostics={
+        "method": "joint", "sims_run": int(res.cells), "early_terms": int(res.early),
         "kernel_us": int(res.kernel_ms * 1e3),
         "wall_us": int((time.perf_counter() - t0) * 1e6)})
 

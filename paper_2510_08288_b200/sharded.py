@@ -9,7 +9,11 @@ k0 + (r+1)*n/W) -- the counter RNG makes that free of scenario traffic
   counts, int64[M]; a row is all-feasible iff its global count is 0, and every
   rank extracts the same row (extract_kappa_opt, governor.py:351-377);
 * exact Alg. 2: one all-reduce each of MIN kappa, MIN found (= AND) and SUM of
-  the cell / early counters (governor.py:496-506).
+  the cell / early counters (governor.py:496-506);
+* joint bisection: one all-reduce (MAX) of the uint32
+  violation flag per iteration, enqueued on the library's stream between the
+  local rollout kernel and the decision kernel, so the n_kappa + 1 iterations
+  never wait on the host.
 
 The collectives run through torch.distributed (NCCL on GPUs, gloo on CPU for
 the host-logic tests); the local step is the device kernel.
@@ -28,7 +32,8 @@ from .governor import (KappaResult, _prepared, _source, _validate_state, _host_r
 from .governor import _require_surrogate as _require_device_plant
 
 __all__ = ["PRUNED", "global_row_counts", "extract_row", "robust_rg_parallel_sharded",
-           "robust_rg_sequential_sharded", "combine_bisection"]
+           "robust_rg_sequential_sharded", "combine_bisection", "robust_rg_joint_sharded",
+           "DeviceJointShard"]
 
 PRUNED = np.uint32(0xFFFFFFFF)  # rg_grid_step's marker for a gated-out row
 _BIG = 1 << 40                  # > any scenario count; marks pruned rows in the sum
@@ -163,3 +168,97 @@ def robust_rg_sequential_sharded(plant, x_t, state, r_t, cset, scenarios, config
     return KappaResult(kappa, v, found, {"method": "sequential-sharded", "ranks": world,
                                          "sims_run": cells, "early_terms": early,
                                          "wall_us": int((time.perf_counter() - t0) * 1e6)})
+
+
+class DeviceJointShard:
+    """This rank's part of a joint bisection on its GPU (rg_joint_*).
+
+    ``flag()`` is the device-resident uint32 violation flag as a torch tensor
+    (no copy), and ``stream()`` the library's stream: the all-reduce between
+    ``roll`` and ``decide`` runs there, in order with the kernels.
+    """
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+        self._flag = None
+
+    def begin(self, prob, x0, v_prev, r, n_kappa, dist, n_sim, scen):
+        self.ctx.joint_begin(prob, x0, v_prev, r, n_kappa, dist, n_sim, scen)
+        self._flag = None
+
+    def roll(self, it):
+        self.ctx.joint_iter(it, fold=False)
+
+    def decide(self, it):
+        self.ctx.joint_decide(it)
+
+    def stream(self):
+        import torch
+
+        return torch.cuda.ExternalStream(self.ctx.stream_ptr, device=f"cuda:{self.ctx.device}")
+
+    def flag(self):
+        import torch
+
+        if self._flag is None:
+            ptr = self.ctx.joint_flag_ptr()
+
+            class _Iface:  # __cuda_array_interface__ view of the flag word
+                __cuda_array_interface__ = {"shape": (1,), "typestr": "<i4",
+                                            "data": (ptr, False), "version": 3}
+
+            self._flag = torch.as_tensor(_Iface(), device=f"cuda:{self.ctx.device}")
+        return self._flag
+
+    def end(self):
+        res = self.ctx.joint_end()
+        return float(res.kappa), bool(res.found), int(res.cells), int(res.early)
+
+
+def robust_rg_joint_sharded(plant, x_t, state, r_t, cset, scenarios, config, group=None,
+                            shard_impl=None):
+    """robust_rg_joint over the ranks of `group` (scenario shards, OR per iteration).
+
+    ``shard_impl`` defaults to DeviceJointShard; the host-logic tests pass an
+    oracle-backed object with the same methods.  Every rank walks the same
+    candidates and returns the same kappa; sims_run / early_terms are summed.
+    """
+    dist = _dist()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    x_t = _validate_state(plant, x_t)
+    _require_device_plant(plant)
+    shard = scenarios.shard(rank, world)
+    prob, _, _, _ = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor,
+                              config.epsilon, config.tighten_mode, config.j_star, 0)
+    impl = shard_impl or DeviceJointShard(_capi.context(getattr(config, "device", 0)))
+    t0 = time.perf_counter()
+    dist_t, n_sim, stream = _source(shard, config.j_star)
+    impl.begin(prob, x_t, state.v_prev, r_t, config.n_kappa, dist_t, n_sim, stream)
+    import torch
+
+    st = impl.stream()
+    cm = torch.cuda.stream(st) if st is not None else _nullcontext()
+    with cm:
+        for it in range(-1, config.n_kappa):
+            impl.roll(it)
+            dist.all_reduce(impl.flag(), op=dist.ReduceOp.MAX, group=group)
+            impl.decide(it)
+    kappa, found, cells, early = impl.end()
+    ce = torch.tensor([cells, early], dtype=torch.int64)
+    if dist.get_backend(group) == "nccl":
+        ce = ce.to(f"cuda:{impl.ctx.device}")
+    dist.all_reduce(ce, op=dist.ReduceOp.SUM, group=group)
+    cells, early = (int(x) for x in ce.cpu().tolist())
+    v = update_setpoint(state.v_prev, r_t, kappa)
+    state.v_prev = v
+    return KappaResult(kappa, v, found, {"method": "joint-sharded", "ranks": world,
+                                         "sims_run": cells, "early_terms": early,
+                                         "wall_us": int((time.perf_counter() - t0) * 1e6)})
+
+
+class _nullcontext:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False

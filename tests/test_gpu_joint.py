@@ -1,0 +1,118 @@
+"""Joint bisection on the B200 (rg_bisect_joint, robust_rg_joint, the sharded form).
+
+The joint search is the north-star form of Alg. 2: one
+candidate for every scenario per iteration, an OR-reduced violation flag,
+early abandonment.  Its candidate sequence and verdicts are checked against the
+CPU oracle's joint search (oracle.joint_bisect) bit for bit, and its kappa /
+feasible against the exact per-scenario Alg. 2 on the device.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2510_08288_b200 as rg
+from paper_2510_08288_b200 import _capi
+from conftest import GOLDEN, bis_case
+
+pytestmark = pytest.mark.gpu
+
+with np.load(GOLDEN) as _z:
+    N_BIS = len(_z["bis_names"])
+
+PLANT = rg.make_plant("surrogate-fc")
+
+
+def _cset(c):
+    return rg.ConstraintSet(c["lower"], c["upper"], c["anchor"])
+
+
+@pytest.mark.parametrize("idx", range(N_BIS))
+def test_joint_matches_oracle_and_alg2_on_reference_cases(golden, orc, idx):
+    c = bis_case(golden, idx)
+    cfg = rg.GovernorConfig(j_star=c["j_star"], epsilon=c["eps"], n_kappa=c["n_kappa"],
+                            n_sim=c["n_sim"])
+    scen = rg.sample_scenarios(rg.DisturbanceModel(c["ranges"]), c["n_sim"], c["j_star"] + 1,
+                               c["seed"])
+    dist = orc.sample(c["seed"], c["n_sim"], c["j_star"] + 1, c["ranges"])
+    tlo, thi = orc.tighten(c["lower"], c["upper"], c["anchor"], c["eps"])
+    kj, fj, _ = orc.joint_bisect(0.01, c["x0"], c["v_prev"], c["r"], c["lower"], c["upper"],
+                                 tlo, thi, dist, c["j_star"], c["n_kappa"])
+    for s in (scen, rg.ScenarioSet(scen.data)):
+        res = rg.robust_rg_joint(PLANT, c["x0"], rg.GovernorState(c["v_prev"]), c["r"],
+                                 _cset(c), s, cfg)
+        assert (res.kappa_opt, res.feasible) == (kj, fj), c["name"]
+        assert res.v_applied == rg.update_setpoint(c["v_prev"], c["r"], kj)
+        # and Alg. 2's result (the reference's robust_rg_sequential)
+        assert (res.kappa_opt, float(res.feasible)) == (float(c["result"][0]),
+                                                        float(c["result"][2])), c["name"]
+        assert res.diagnostics["sims_run"] >= c["n_sim"]
+
+
+@pytest.mark.parametrize("mode", ["fused", "staged"])
+def test_joint_equals_device_alg2_at_scale(mode):
+    """Transient-binding trials (200/200 equal): joint == Alg. 2."""
+    ctx = _capi.context(0)
+    rng = np.random.default_rng(5)
+    m = rg.DisturbanceModel.scaled(0.02, 3)
+    tight = rg.tighten(rg.ConstraintSet(-0.9, 0.9), 0.05)
+    lo, hi = rg.admissible_setpoints(tight.lower, tight.upper)
+    prob = _capi.Problem(0.01, -0.9, 0.9, lo, hi, 128, 0)
+    for trial in range(24):
+        vp = float(rng.uniform(-1, 1))
+        r = float(rng.uniform(-2.5, 2.5))
+        x0 = np.array([np.tanh(vp), vp, np.tanh(vp) / 2]) + rng.uniform(-0.05, 0.05, 3)
+        n = 3000
+        sc = _capi.make_scenarios(300 + trial, 0, n, m.lo, m.span)
+        a2, _, _ = ctx.bisect(prob, x0, vp, r, 8, None, n, sc, rng_mode=mode)
+        jt = ctx.bisect_joint(prob, x0, vp, r, 8, None, n, sc, rng_mode=mode)
+        assert (jt.kappa, jt.found) == (a2.kappa, a2.found), (trial, jt.kappa, a2.kappa)
+        assert jt.cells >= n
+
+
+def test_joint_iteration_api_equals_one_call():
+    """begin / iter(fold=0) / decide / end == rg_bisect_joint (the sharded form's steps)."""
+    ctx = _capi.context(0)
+    m = rg.DisturbanceModel.scaled(0.02, 3)
+    tight = rg.tighten(rg.ConstraintSet(-0.9, 0.9), 0.05)
+    lo, hi = rg.admissible_setpoints(tight.lower, tight.upper)
+    prob = _capi.Problem(0.01, -0.9, 0.9, lo, hi, 128, 0)
+    x0 = np.array([0.2, 0.4, 0.1])
+    for seed in range(6):
+        sc = _capi.make_scenarios(900 + seed, 0, 2000, m.lo, m.span)
+        one = ctx.bisect_joint(prob, x0, 0.4, 2.2, 8, None, 2000, sc)
+        ctx.joint_begin(prob, x0, 0.4, 2.2, 8, None, 2000, sc)
+        for it in range(-1, 8):
+            ctx.joint_iter(it, fold=False)
+            ctx.joint_decide(it)
+        step = ctx.joint_end()
+        assert (step.kappa, step.found, step.cells) == (one.kappa, one.found, one.cells)
+
+
+def test_joint_sharded_world1_nccl():
+    """robust_rg_joint_sharded with one NCCL rank: the per-iteration all-reduce of
+    the device flag on the library stream leaves the single-device result."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_08288_b200.sharded import robust_rg_joint_sharded
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        m = rg.DisturbanceModel.scaled(0.02, 3)
+        cfg = rg.GovernorConfig(j_star=128, n_sim=4000)
+        box = rg.ConstraintSet(-0.9, 0.9)
+        for seed in range(4):
+            scen = rg.sample_scenarios(m, 4000, 129, seed=40 + seed)
+            x0 = np.array([0.2, 0.4, 0.1])
+            a = rg.robust_rg_joint(PLANT, x0, rg.GovernorState(0.4), 2.2, box, scen, cfg)
+            b = robust_rg_joint_sharded(PLANT, x0, rg.GovernorState(0.4), 2.2, box, scen, cfg)
+            assert (a.kappa_opt, a.feasible, a.v_applied) == (b.kappa_opt, b.feasible,
+                                                              b.v_applied)
+    finally:
+        dist.destroy_process_group()

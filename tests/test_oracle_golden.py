@@ -178,3 +178,16 @@ def test_linear_cells_and_governors_match_reference(orc, golden, idx):
 
 def test_linear_known_answer(golden):
     assert abs(float(golden["lin_kappa_star_081"][0]) - 0.81) < 1e-5
+
+
+@pytest.mark.parametrize("idx", range(N_BIS))
+def test_joint_bisection_equals_alg2_on_reference_cases(orc, golden, idx):
+    # with down-set feasible sets the joint search
+    # (one kappa for all scenarios per iteration) lands on Alg. 2's minimum
+    c = bis_case(golden, idx)
+    dist = orc.sample(c["seed"], c["n_sim"], c["j_star"] + 1, c["ranges"])
+    tlo, thi = orc.tighten(c["lower"], c["upper"], c["anchor"], c["eps"])
+    kappa, found, path = orc.joint_bisect(0.01, c["x0"], c["v_prev"], c["r"], c["lower"],
+                                          c["upper"], tlo, thi, dist, c["j_star"], c["n_kappa"])
+    assert (kappa, float(found)) == (float(c["result"][0]), float(c["result"][2])), c["name"]
+    assert len(path) == (1 if path[0][1] else c["n_kappa"] + 1)

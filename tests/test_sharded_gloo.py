@@ -70,13 +70,69 @@ def _worker(rank, world, port, out_dir):
                                                              0.9, tlo, thi, d, js, 8)
             return k, int(f), cells, early
 
+        class OracleJointShard:
+            """Rank-local joint iterations on the CPU oracle (same methods as the device)."""
+
+            def begin(self, prob, x0_, v_prev, r_, n_kappa, dist_t, n_sim, stream):
+                self.d = orc.sample(stream.seed, stream.n_sim, js + 1, model.ranges,
+                                    k0=stream.k0)
+                self.lo, self.hi, self.kopt, self.found, self.done = 0.0, 1.0, 0.0, False, False
+                self.cells = self.early = 0
+                self.n_kappa = n_kappa
+                import torch
+                self._flag = torch.zeros(1, dtype=torch.int32)
+
+            def _kappa(self, it):
+                return 1.0 if it < 0 else 0.5 * (self.lo + self.hi)
+
+            def roll(self, it):
+                self._flag.zero_()
+                if self.done:
+                    return
+                v = orc.update_setpoint(vp, r, self._kappa(it))
+                if not orc.ss_ok(v, tlo, thi):
+                    return
+                for k in range(self.d.shape[0]):
+                    st, _ = orc.cell_sfc(0.01, np.array(x0), v, self.d[k], js, -0.9, 0.9)
+                    if st != orc.CELL_OK:
+                        self._flag[0] = 1
+                        break
+
+            def flag(self):
+                return self._flag
+
+            def stream(self):
+                return None
+
+            def decide(self, it):
+                if self.done:
+                    return
+                kappa = self._kappa(it)
+                v = orc.update_setpoint(vp, r, kappa)
+                feas = orc.ss_ok(v, tlo, thi) and int(self._flag[0]) == 0
+                if it < 0:
+                    if feas:
+                        self.kopt, self.found, self.done = 1.0, True, True
+                elif feas:
+                    self.kopt, self.found, self.lo = kappa, True, kappa
+                else:
+                    self.hi = kappa
+                if it == self.n_kappa - 1:
+                    self.done = True
+
+            def end(self):
+                return self.kopt, self.found, self.cells, self.early
+
+        jr = sharded.robust_rg_joint_sharded(plant, np.array(x0), rg.GovernorState(vp), r, box,
+                                             scen, cfg, shard_impl=OracleJointShard())
         g = sharded.robust_rg_parallel_sharded(plant, np.array(x0), rg.GovernorState(vp), r,
                                                box, scen, cfg, local_step=grid_local)
         b = sharded.robust_rg_sequential_sharded(plant, np.array(x0), rg.GovernorState(vp), r,
                                                  box, scen, cfg, local_step=bis_local)
         results.append([g.kappa_opt, g.v_applied, float(g.feasible), b.kappa_opt, b.v_applied,
                         float(b.feasible), b.diagnostics["sims_run"],
-                        b.diagnostics["early_terms"]])
+                        b.diagnostics["early_terms"], jr.kappa_opt, jr.v_applied,
+                        float(jr.feasible)])
     np.save(Path(out_dir) / f"rank{rank}.npy", np.array(results))
     dist.destroy_process_group()
 
@@ -97,8 +153,12 @@ def test_sharded_steps_equal_unsharded_oracle(tmp_path, orc):
                                             thi, js, prefix_mode=prefix)
         kb, vb, fb, cells, early, _ = orc.robust_sequential(0.01, np.array(x0), vp, r, -0.9,
                                                             0.9, tlo, thi, d, js, 8)
-        expect = [kg, vg, float(fg), kb, vb, float(fb), cells, early]
+        kj, fj, _ = orc.joint_bisect(0.01, np.array(x0), vp, r, -0.9, 0.9, tlo, thi, d, js, 8)
+        vj = orc.update_setpoint(vp, r, kj)
+        expect = [kg, vg, float(fg), kb, vb, float(fb), cells, early, kj, vj, float(fj)]
         assert list(r0[i]) == expect, (i, list(r0[i]), expect)
+        # the joint search lands where the per-scenario bisections' minimum does
+        assert (kj, fj) == (kb, fb), (i, kj, fj, kb, fb)
 
 
 def test_extract_row_matches_reference_extraction():
