@@ -398,6 +398,24 @@ def run_own(args, rank, world, local_rank):
                       "ms_per_step": t_c3 * 1e3 / 400, "violations": rec.violations(box),
                       "timing": "wall clock, host true-plant step included (reference: "
                                 "~650 ms/step on 8 CPU cores, SURVEY.md §6)"})
+        # the bisection searches on a transient step (r=2.5 from rest, kappa* = 0.5078):
+        # exact Alg. 2 (per-scenario bisections, min) and the joint search (one kappa
+        # for all scenarios per iteration, OR-reduced flag); both land on the same kappa
+        for n_b in (10_000, 1 << 20):
+            sc = _capi.make_scenarios(BASE_SEED + 9000, 0, n_b, model.lo, model.span)
+            for name, call in (
+                    ("alg2", lambda: ctx.bisect(prob, x0, 0.0, 2.5, 8, None, n_b, sc)[0]),
+                    ("joint", lambda: ctx.bisect_joint(prob, x0, 0.0, 2.5, 8, None, n_b, sc))):
+                call()
+                reps = 10
+                t0 = time.perf_counter()
+                for _ in range(reps):
+                    res_b = call()
+                t_b = (time.perf_counter() - t0) / reps
+                sweep.append({"workload": f"bisection ({name}), r=2.5 transient, n_sim={n_b}",
+                              "ms_per_step": t_b * 1e3, "kappa": float(res_b.kappa),
+                              "rollouts": int(res_b.cells),
+                              "timing": "wall clock around the synchronous C-ABI call"})
 
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
