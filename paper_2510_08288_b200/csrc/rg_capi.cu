@@ -694,24 +694,28 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
     RG_CUDA(ctx->g_out.ensure(blk_bytes));
     if (zero_copy) RG_CUDA(ctx->h_out.ensure(blk_bytes));
     char* blk = zero_copy ? ctx->h_out.as<char>() : ctx->g_out.as<char>();
+    char* dblk = ctx->g_out.as<char>();  // device copy: the blocks' P bits land here
     a.host_out = zero_copy ? 1 : 0;
     a.seq_token = ++ctx->seq_ctr;
     if (zero_copy) reinterpret_cast<volatile rg::GridOut*>(blk)->seq = 0ull;
     a.out = reinterpret_cast<rg::GridOut*>(blk);
     a.viol_out = reinterpret_cast<unsigned*>(blk + kOutHead);
     const bool abandon = (flags & RG_ABANDON) && !pbits;
-    if (pbits)
-        a.pbits = pbits_in_block ? reinterpret_cast<unsigned*>(blk + kOutHead + viol_bytes(m_grid))
+    if (pbits) {
+        // blocks write P to device memory; in zero-copy mode the finalizing block
+        // copies it into the pinned result block
+        a.pbits = pbits_in_block ? reinterpret_cast<unsigned*>(dblk + kOutHead + viol_bytes(m_grid))
                                  : pbits;
+        if (zero_copy && pbits_in_block)
+            a.pbits_host = reinterpret_cast<unsigned*>(blk + kOutHead + viol_bytes(m_grid));
+    }
     const int lpc = lpc_for(ctx, (int64_t)m_grid * n_sim, flags);
     a.tpb = tpb_for(ctx, n_sim * lpc, m_grid);
     a.occ_cap = occ_cap_for(ctx, (n_sim * lpc + a.tpb - 1) / a.tpb * m_grid, a.tpb);
     a.smem_per_sm = ctx->smem_per_sm;
     a.smem_reserved = ctx->smem_reserved;
-    if (pbits && lpc > 1) {  // lanes OR their bits in
-        if (zero_copy) memset(a.pbits, 0, pbytes);
-        else RG_CUDA(cudaMemsetAsync(a.pbits, 0, pbytes, ctx->stream));
-    }
+    if (pbits && lpc > 1)  // lanes OR their bits in
+        RG_CUDA(cudaMemsetAsync(a.pbits, 0, pbytes, ctx->stream));
     const bool timed = !(flags & RG_NO_TIMING);
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
     if (kernel == 2) {

@@ -241,14 +241,32 @@ __device__ __forceinline__ void grid_finalize(const GridArgs& a) {
     __shared__ bool s_last;
     __syncthreads();
     if (threadIdx.x == 0) {
-        if (a.host_out) __threadfence_system();  // this block's P bits reach the host first
-        else __threadfence();
+        __threadfence();
         const unsigned total = gridDim.x * gridDim.y;
         s_last = atomicAdd(a.ticket, 1u) == total - 1;
     }
     __syncthreads();
     if (!s_last) return;
     __threadfence();
+    if (a.pbits_host) {  // zero-copy result: the P bits go to pinned host memory in one pass
+        // eight independent L2 loads in flight per thread, then the eight host stores
+        const int64_t nw = (int64_t)a.m_grid * a.pwords;
+        const int64_t step = blockDim.x;
+        for (int64_t q0 = threadIdx.x; q0 < nw; q0 += 8 * step) {
+            unsigned w[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t q = q0 + u * step;
+                w[u] = q < nw ? __ldcg(a.pbits + q) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t q = q0 + u * step;
+                if (q < nw) a.pbits_host[q] = w[u];
+            }
+        }
+        __syncthreads();
+    }
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
         int best = -1;

@@ -69,6 +69,7 @@ struct GridArgs {
     unsigned* viol_out;             // [m] per-row violation count (0xffffffff = pruned)
     GridOut* out;
     unsigned* pbits;                // optional [m][pwords] feasibility bitmask
+    unsigned* pbits_host;           // zero-copy: finalize copies pbits here (pinned)
     int64_t pwords;
     int tpb;
     // occupancy cap (host side of the launch): at most occ_cap blocks per SM,
