@@ -76,6 +76,32 @@ def test_small_range_tanh_bit_exact(ctx, orc):
     assert np.array_equal(_bits(y2), _bits(orc.libm_tanh(x2)))
 
 
+def test_big_range_tanh_bit_exact(ctx, orc):
+    """The warp-voted 1 <= |x| < 6.5 form (tanh_lockstep_big): whole warps in range,
+    the range's first and last hi words, every reduction index k = 3..19."""
+    rng = np.random.default_rng(29)
+
+    def words(hi, n):
+        lo = rng.integers(0, 2**32, n, dtype=np.uint64)
+        return ((np.uint64(hi) << np.uint64(32)) | lo).view(np.float64)
+
+    parts = [rng.uniform(1.0, 6.5, 2_000_000), rng.uniform(-6.5, -1.0, 500_000)]
+    for hi in (0x3FF00000, 0x3FF00001, 0x40199999, 0x40199FFF):
+        w = words(hi, 128 * 512)
+        parts += [w, -w]
+    # arguments around every k boundary: y = 2|x| = (k - 0.5) ln2
+    for k in range(3, 20):
+        b = (k - 0.5) * np.log(2.0) / 2.0
+        parts.append(b * (1.0 + rng.uniform(-1e-12, 1e-12, 128 * 64)))
+    x = np.concatenate(parts)
+    x = x[np.abs(x) < 6.5]
+    x = x[: x.size // 128 * 128]
+    ref = orc.libm_tanh(x)
+    y = ctx.tanh(x, lockstep=True)
+    mism = np.flatnonzero(_bits(y) != _bits(ref))
+    assert mism.size == 0, f"{mism.size} mismatches, first x={x[mism[:5]]}"
+
+
 @pytest.mark.parametrize("lpc", [1, 2, 4])
 @pytest.mark.parametrize("mode", ["fused", "staged"])
 @pytest.mark.parametrize("idx", range(N_FILL))
