@@ -278,7 +278,7 @@ def run_own(args, rank, world, local_rank):
         assert out.row == M_GRID - 1 and out.early_terms == 0, (out.row, out.early_terms)
 
     # k_gen_soa + k_grid when the scenario block is staged in L2, k_grid alone when fused
-    launches_per_step = 2 if n_sim * j_star <= (4 << 20) else 1
+    launches_per_step = 2 if n_sim * j_star * 24 <= (16 << 30) else 1
     cells_total = cells_rank * world * args.steps
     value = cells_total / (total_ms * 1e-3)
     ms_per_step = total_ms / args.steps
@@ -344,7 +344,7 @@ def run_own(args, rank, world, local_rank):
             rate = cells / (t.mean() * 1e-3)
             sweep.append({"n_sim": n_big, "ms_per_step": float(t.mean()), "value": rate,
                           "unit": UNIT, "roofline_frac": FLOPS_PER_CELL_STEP * rate / peak,
-                          "rng": "staged" if n_big * j_star <= (4 << 20) else "fused"})
+                          "rng": "staged" if n_big * j_star * 24 <= (16 << 30) else "fused"})
 
     if world > 1:
         from paper_2510_08288_b200.sharded import robust_rg_parallel_sharded

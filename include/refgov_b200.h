@@ -62,8 +62,10 @@ extern "C" {
 #define RG_TANH_LOCKSTEP 0x10 /* rg_tanh: use the rollout's lockstep form */
 #define RG_FUSED_RNG 0x20   /* RNG source: hash inside the rollout loop */
 #define RG_STAGE_RNG 0x40   /* RNG source: generate the SoA tensor first */
-/* With neither RG_FUSED_RNG nor RG_STAGE_RNG an RNG source is staged when
- * n_sim * j_star <= 4M scenario-steps (it then stays in L2) and fused above. */
+/* With neither RG_FUSED_RNG nor RG_STAGE_RNG an RNG source is staged when the
+ * SoA block (n_sim * j_star * 24 bytes) is at most 16 GB for the fill and the
+ * grid step (all candidate rows share it), at most 96 MB for the bisections
+ * (whose rollouts often stop after a few steps), and fused above. */
 #define RG_LPC1 0x80        /* force 1 lane per (row, scenario) cell */
 #define RG_LPC2 0x100       /* force 2 lanes per cell (each evaluates 2 of the 4 tanh) */
 #define RG_LPC4 0x200       /* force 4 lanes per cell (1 tanh each) */

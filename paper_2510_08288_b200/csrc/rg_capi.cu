@@ -213,7 +213,12 @@ int32_t stage_dist(rg_ctx* ctx, const double* dist, int64_t n_sim, int64_t horiz
 // Small scenario sets: generate the RNG stream once into SoA scratch (L2
 // resident) so the per-cell loop loads three doubles per step instead of
 // re-hashing them for every candidate row.  Large sets keep the fused RNG.
-constexpr int64_t kStageMaxScenarioSteps = 4ll << 20;  // 96 MB of SoA
+// Staging the scenario block (k_gen_soa, then SoA reads) beats generating the
+// disturbances inside every rollout at every measured size -- the block is
+// shared by all M candidate rows, and its reads are a small fraction of HBM
+// bandwidth even when it does not fit in L2 (1M scenarios: 6.4 GB, 116 vs 142
+// ms per step).  Above 16 GB of SoA the rollout generates them (fused).
+constexpr int64_t kStageMaxScenarioSteps = (16ll << 30) / 24;
 
 int32_t stage_rng(rg_ctx* ctx, const rg_scenarios* rng, int64_t n_sim, int32_t j_star,
                   const double** soa, int64_t* ld) {
@@ -225,10 +230,15 @@ int32_t stage_rng(rg_ctx* ctx, const rg_scenarios* rng, int64_t n_sim, int32_t j
     return RG_OK;
 }
 
-bool want_stage(int64_t n_sim, int32_t j_star, int32_t flags) {
+// The bisections run each scenario only until it fails, often a few steps:
+// generating the whole block up front pays off only while it is L2-sized.
+constexpr int64_t kStageMaxScenarioStepsBisect = 4ll << 20;  // 96 MB of SoA
+
+bool want_stage(int64_t n_sim, int32_t j_star, int32_t flags,
+                int64_t max_steps = kStageMaxScenarioSteps) {
     if (flags & RG_FUSED_RNG) return false;
     if (flags & RG_STAGE_RNG) return true;
-    return n_sim * (int64_t)j_star <= kStageMaxScenarioSteps;
+    return n_sim * (int64_t)j_star <= max_steps;
 }
 
 // The grid step's results live in one device block -- [GridOut | viol_out[m] |
@@ -314,11 +324,11 @@ int tpb_for(const rg_ctx* ctx, int64_t n_sim, int64_t rows) {
         const int t = atoi(env);
         if (t == 32 || t == 64 || t == 128) return t;
     }
-    // Small problems: small blocks spread the warps over more SMs.
+    // Small problems: single-warp blocks spread the warps over more SMs; above
+    // one wave, 64-thread blocks (measured equal or better than 128 at 10k-1M).
     const int64_t warps = (n_sim + 31) / 32 * std::max<int64_t>(rows, 1);
-    if (warps < (int64_t)ctx->sm_count * 8) return 32;
-    if (warps < (int64_t)ctx->sm_count * 16) return 64;
-    return 128;
+    if (warps <= (int64_t)ctx->sm_count * 8) return 32;
+    return 64;
 }
 
 }  // namespace
@@ -788,7 +798,7 @@ int32_t rg_bisect(rg_ctx* ctx, const rg_problem* prob, const double* x0, double 
         src = 2;
         if ((rc = stage_dist(ctx, dist, n_sim, horizon, prob->j_star, flags, &a.soa, &a.ld)))
             return rc;
-    } else if (rng && want_stage(n_sim, prob->j_star, flags)) {
+    } else if (rng && want_stage(n_sim, prob->j_star, flags, kStageMaxScenarioStepsBisect)) {
         src = 2;
         if ((rc = stage_rng(ctx, rng, n_sim, prob->j_star, &a.soa, &a.ld))) return rc;
     } else if (rng) {
@@ -904,7 +914,7 @@ int32_t rg_joint_begin(rg_ctx* ctx, const rg_problem* prob, const double* x0, do
         src = 2;
         if ((rc = stage_dist(ctx, dist, n_sim, horizon, prob->j_star, flags, &a.soa, &a.ld)))
             return rc;
-    } else if (rng && want_stage(n_sim, prob->j_star, flags)) {
+    } else if (rng && want_stage(n_sim, prob->j_star, flags, kStageMaxScenarioStepsBisect)) {
         src = 2;
         if ((rc = stage_rng(ctx, rng, n_sim, prob->j_star, &a.soa, &a.ld))) return rc;
     } else if (rng) {
