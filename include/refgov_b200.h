@@ -181,7 +181,12 @@ RG_API int32_t rg_fill(rg_ctx *ctx, const rg_problem *prob, const double *x0, co
  *   row_viol[m]       per-row violating-scenario counts (UINT32_MAX = pruned)
  *   pbits[m][ceil(n_sim/32)]  P as a bitmask, bit k%32 of word k/32
  * With RG_ASYNC nothing is read back; the result lands in device memory and
- * rg_grid_fetch copies it out later. */
+ * rg_grid_fetch copies it out later.  A synchronous call with host outputs has
+ * the kernel write its result straight into pinned host memory and returns once
+ * the kernel has published it (no copy, no stream synchronisation); work that
+ * only resets device counters may still be in flight on the context's stream,
+ * ordered before any later call.  rg_grid_fetch after such a call returns the
+ * same result again. */
 RG_API int32_t rg_grid_step(rg_ctx *ctx, const rg_problem *prob, const double *x0, double v_prev,
                      double r, int32_t m_grid, int32_t prefix_mode, const double *dist,
                      int64_t n_sim, int64_t horizon, const rg_scenarios *rng,

@@ -145,6 +145,7 @@ struct rg_ctx {
     rg::JointArgs j_args{};         // the joint search in progress (rg_joint_begin)
     int j_src = -1;                 // its scenario source; -1 = none begun
     unsigned long long seq_ctr = 0; // grid-step publication tokens
+    bool last_zero_copy = false;    // the last grid step published into h_out
 };
 
 namespace {
@@ -746,6 +747,7 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
                                     cudaMemcpyDeviceToDevice, ctx->stream));
         return RG_OK;
     }
+    ctx->last_zero_copy = zero_copy;
     if (zero_copy) {
         RG_CUDA(wait_token(ctx, reinterpret_cast<volatile rg::GridOut*>(blk), a.seq_token));
         return unpack_grid(ctx, blk, row_viol, m_grid, out, pbits_in_block ? pbits : nullptr,
@@ -765,6 +767,8 @@ int32_t rg_grid_fetch(rg_ctx* ctx, uint32_t* row_viol, int32_t m_grid, rg_grid_r
     if (rc) return rc;
     if (m_grid < 1 || m_grid > ctx->grid_cap || m_grid != ctx->last_m)
         return fail(RG_E_ARGS, "bad m_grid %d (last step used %d)", m_grid, ctx->last_m);
+    if (ctx->last_zero_copy)  // the last step published into the pinned block
+        return unpack_grid(ctx, ctx->h_out.as<char>(), row_viol, m_grid, out, nullptr, 0, false);
     return read_grid(ctx, row_viol, m_grid, out, nullptr, 0, false);
 }
 

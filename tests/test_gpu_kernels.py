@@ -279,3 +279,28 @@ def test_decoupled_matches_per_step_at_scale(ctx, kernel, j_star):
             c = ctx.grid_step(prob, x0, vp, r, M, False, None, n, sc, False, abandon=True,
                               rng_mode=mode, kernel=kernel)
             assert c[0].row == a[0].row
+
+
+def test_grid_fetch_after_sync_and_async_steps(ctx):
+    """rg_grid_fetch returns the last step's result: after a synchronous
+    (zero-copy) step and after an RG_ASYNC step, identical to the direct result."""
+    import ctypes
+
+    m = rg.DisturbanceModel.scaled(0.02, 3)
+    prob = _problem(-0.9, 0.9, 0.0, 0.05, 128)
+    x0 = np.array([0.1, 0.3, 0.05])
+    sc = _capi.make_scenarios(77, 0, 3000, m.lo, m.span)
+    res, viol, _ = ctx.grid_step(prob, x0, 0.3, 2.4, 32, False, None, 3000, sc, False)
+    lib = ctx.lib
+    for flags in (0, _capi.RG_ASYNC):
+        if flags:
+            out = _capi.GridResult()
+            _capi.check(lib.rg_grid_step(ctx.handle, ctypes.byref(prob), x0.ctypes.data, 0.3,
+                                         2.4, 32, 0, None, 3000, 0, ctypes.byref(sc), None,
+                                         None, ctypes.byref(out), flags))
+        got = _capi.GridResult()
+        v2 = np.empty(32, np.uint32)
+        _capi.check(lib.rg_grid_fetch(ctx.handle, v2.ctypes.data, 32, ctypes.byref(got)))
+        assert (got.row, got.sims_run, got.early_terms, got.overflows) == \
+            (res.row, res.sims_run, res.early_terms, res.overflows)
+        assert np.array_equal(v2, viol)
