@@ -124,7 +124,6 @@ struct rg_ctx {
     int device = 0;
     int variant = rg::kTanhFma;
     int sm_count = 0;
-    int smem_per_sm = 0, smem_reserved = 0;  // shared memory per SM / reserved per block
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // grid-step accumulators and outputs
@@ -306,20 +305,6 @@ int grid_kernel_for(int32_t flags) {
     return kGridKernelDefault;
 }
 
-// Blocks-per-SM cap for a one-wave launch: the fewest warps per SM that still
-// hold every block at once, rounded up to whole warps per sub-partition.  Above
-// 12 warps per SM (the register limit is 13) no cap.  RG_OCC_CAP=0 disables it,
-// RG_OCC_CAP=n forces n blocks per SM (tuning).
-int occ_cap_for(const rg_ctx* ctx, int64_t blocks, int tpb) {
-    if (const char* env = getenv("RG_OCC_CAP")) return std::max(0, atoi(env));
-    const int wpb = tpb / 32;
-    const int64_t warps = blocks * wpb;
-    int64_t per_sm = (warps + ctx->sm_count - 1) / ctx->sm_count;
-    per_sm = (per_sm + 3) / 4 * 4;
-    if (per_sm > 12 || ctx->smem_per_sm <= 0) return 0;
-    return (int)std::max<int64_t>(1, per_sm / wpb);
-}
-
 int tpb_for(const rg_ctx* ctx, int64_t n_sim, int64_t rows) {
     if (const char* env = getenv("RG_FORCE_TPB")) {  // tuning override: 32, 64 or 128
         const int t = atoi(env);
@@ -382,8 +367,6 @@ int32_t rg_create(int32_t device, int32_t tanh_variant, rg_ctx** out) {
     ctx->device = device;
     ctx->variant = variant;
     ctx->sm_count = prop.multiProcessorCount;
-    ctx->smem_per_sm = (int)prop.sharedMemPerMultiprocessor;
-    ctx->smem_reserved = (int)prop.reservedSharedMemPerBlock;
     int32_t rc = enter(ctx);
     if (rc) { delete ctx; return rc; }
     if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -722,9 +705,6 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
     }
     const int lpc = lpc_for(ctx, (int64_t)m_grid * n_sim, flags);
     a.tpb = tpb_for(ctx, n_sim * lpc, m_grid);
-    a.occ_cap = occ_cap_for(ctx, (n_sim * lpc + a.tpb - 1) / a.tpb * m_grid, a.tpb);
-    a.smem_per_sm = ctx->smem_per_sm;
-    a.smem_reserved = ctx->smem_reserved;
     if (pbits && lpc > 1)  // lanes OR their bits in
         RG_CUDA(cudaMemsetAsync(a.pbits, 0, pbytes, ctx->stream));
     const bool timed = !(flags & RG_NO_TIMING);

@@ -18,8 +18,6 @@
 // the early exits mostly agree across the warp.
 #include "rg_kernels.h"
 
-#include <mutex>
-
 #include <cuda_runtime.h>
 
 #include "rg_cell.cuh"
@@ -1042,46 +1040,6 @@ cudaError_t launch_fill(const FillArgs& a, bool fma, bool rng, int lpc, cudaStre
     return cudaGetLastError();
 }
 
-// Dynamic shared memory that caps a kernel at `cap` resident blocks per SM:
-// each block's footprint becomes smem_per_sm / cap, so cap + 1 blocks do not
-// fit.  The block scheduler then cannot stack extra warps onto some SM
-// sub-partitions while others idle (a latency-bound rollout runs as slow as
-// its most loaded sub-partition).  Per-kernel attributes are cached.
-template <class Kern>
-size_t occ_cap_smem(Kern kern, int cap, int smem_per_sm, int reserved) {
-    if (cap <= 0) return 0;
-    struct Slot { const void* fn; size_t stat; size_t set; };
-    static Slot cache[64];
-    static int n_cache = 0;
-    static std::mutex mu;
-    std::lock_guard<std::mutex> lock(mu);
-    Slot* sl = nullptr;
-    for (int q = 0; q < n_cache; ++q)
-        if (cache[q].fn == (const void*)kern) sl = &cache[q];
-    if (!sl) {
-        cudaFuncAttributes fa;
-        if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess || n_cache == 64) {
-            cudaGetLastError();
-            return 0;
-        }
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cache[n_cache] = Slot{(const void*)kern, fa.sharedSizeBytes, 48 * 1024};
-        sl = &cache[n_cache++];
-    }
-    const size_t per = (size_t)smem_per_sm / (size_t)cap;
-    const size_t need = sl->stat + (size_t)reserved;
-    const size_t dyn = per > need ? per - need : 0;
-    if (dyn > sl->set) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) !=
-            cudaSuccess) {
-            cudaGetLastError();
-            return 0;
-        }
-        sl->set = dyn;
-    }
-    return dyn;
-}
-
 // Launch with programmatic stream serialization (PDL) when `pdl`: the grid may
 // start while the previous kernel on the stream (k_gen_soa) is still running.
 template <class Kern, class Args>
@@ -1105,10 +1063,7 @@ cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, int lp
     dim3 grid(blocks_for(a.n_sim * lpc, a.tpb), (unsigned)a.m_grid);
     cudaError_t e = cudaSuccess;
 #define RG_GRID(F, R, P, L)                                                              \
-    e = launch_ex(k_grid<F, R, P, L>, grid, a.tpb,                                       \
-                  occ_cap_smem(k_grid<F, R, P, L>, a.occ_cap, a.smem_per_sm,             \
-                               a.smem_reserved),                                         \
-                  s, a.pdl != 0, a)
+    e = launch_ex(k_grid<F, R, P, L>, grid, a.tpb, 0, s, a.pdl != 0, a)
 #define RG_GRID_L(L)                                                             \
     do {                                                                         \
         if (fma) {                                                               \

@@ -72,9 +72,6 @@ struct GridArgs {
     unsigned* pbits_host;           // zero-copy: finalize copies pbits here (pinned)
     int64_t pwords;
     int tpb;
-    // occupancy cap (host side of the launch): at most occ_cap blocks per SM,
-    // enforced with dynamic shared memory; 0 = no cap
-    int occ_cap, smem_per_sm, smem_reserved;
     // out/viol_out/pbits live in pinned host memory (zero-copy): system-scope
     // fences before the ticket, and out->seq = seq_token published last
     int host_out;
