@@ -124,6 +124,7 @@ struct rg_ctx {
     int device = 0;
     int variant = rg::kTanhFma;
     int sm_count = 0;
+    int smem_per_sm = 0;  // bytes of shared memory per SM
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // grid-step accumulators and outputs
@@ -317,6 +318,29 @@ int tpb_for(const rg_ctx* ctx, int64_t n_sim, int64_t rows) {
     return 64;
 }
 
+// Single-wave placement of the grid step.  The step's time is set by the SM
+// sub-partition (SMSP) holding the most warps: each SMSP has its own FP64 unit and
+// issue slot, and one to three resident rollout warps share them.  With single-warp
+// blocks the block scheduler decides how a wave's warps land on SMSPs, and at
+// C2 (1024 warps over 592 SMSPs) about 40% of the steps put three warps on some
+// SMSP: 226 us instead of 165 us (scripts/timing_dist.py).  When one wave holds
+// the step, this picks blocks of 4L warps (L per SMSP, the smallest L that fits)
+// and requests more than half an SM's shared memory, so the scheduler can place
+// only one block per SM: no SMSP ever holds more than L warps.
+void grid_placement(const rg_ctx* ctx, int64_t n_sim, int32_t rows, int* tpb, int* smem_dyn) {
+    *smem_dyn = 0;
+    if (getenv("RG_FORCE_TPB") || getenv("RG_NO_PLACEMENT")) return;
+    for (int L = 1; L <= 2; ++L) {
+        const int t = 128 * L;
+        const int64_t blocks = (n_sim + t - 1) / t * (int64_t)rows;
+        if (blocks <= ctx->sm_count) {
+            *tpb = t;
+            *smem_dyn = ctx->smem_per_sm / 2 + 1024;
+            return;
+        }
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -367,6 +391,7 @@ int32_t rg_create(int32_t device, int32_t tanh_variant, rg_ctx** out) {
     ctx->device = device;
     ctx->variant = variant;
     ctx->sm_count = prop.multiProcessorCount;
+    ctx->smem_per_sm = (int)prop.sharedMemPerMultiprocessor;
     int32_t rc = enter(ctx);
     if (rc) { delete ctx; return rc; }
     if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -705,6 +730,7 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
     }
     const int lpc = lpc_for(ctx, (int64_t)m_grid * n_sim, flags);
     a.tpb = tpb_for(ctx, n_sim * lpc, m_grid);
+    if (kernel == 0 && lpc == 1) grid_placement(ctx, n_sim, m_grid, &a.tpb, &a.smem_dyn);
     if (pbits && lpc > 1)  // lanes OR their bits in
         RG_CUDA(cudaMemsetAsync(a.pbits, 0, pbytes, ctx->stream));
     const bool timed = !(flags & RG_NO_TIMING);

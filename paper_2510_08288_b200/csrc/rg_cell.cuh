@@ -143,7 +143,7 @@ struct D3 {
     double d0, d1, d2;
 };
 
-constexpr int kRingStride = 128;  // max threads per block of the rollout kernels
+constexpr int kRingStride = 256;  // max threads per block of the rollout kernels
 
 // Fused counter RNG: the scenario tensor never exists in memory.
 struct RngSource {

@@ -337,7 +337,7 @@ __device__ __forceinline__ void grid_finalize(const GridArgs& a) {
 }
 
 template <bool FMA, bool RNG, bool POLL, int LPC>
-__global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid(GridArgs a) {
+__global__ void __launch_bounds__(256, RG_GRID_MINB) k_grid(GridArgs a) {
     __shared__ int s_src;
     __shared__ double s_v;
     const int i = blockIdx.y;
@@ -1058,12 +1058,29 @@ cudaError_t launch_ex(Kern kern, dim3 grid, int block, size_t smem, cudaStream_t
     return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
+constexpr int kMaxDevices = 64;
+
 cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, int lpc,
                         cudaStream_t s) {
     dim3 grid(blocks_for(a.n_sim * lpc, a.tpb), (unsigned)a.m_grid);
     cudaError_t e = cudaSuccess;
 #define RG_GRID(F, R, P, L)                                                              \
-    e = launch_ex(k_grid<F, R, P, L>, grid, a.tpb, 0, s, a.pdl != 0, a)
+    do {                                                                                 \
+        if (a.smem_dyn > 0) {                                                            \
+            /* raise the opt-in limit once per instantiation and device */                \
+            static int set_bytes[kMaxDevices] = {};                                      \
+            int dev = 0;                                                                 \
+            if ((e = cudaGetDevice(&dev)) != cudaSuccess) break;                         \
+            if (dev >= kMaxDevices || set_bytes[dev] < a.smem_dyn) {                     \
+                e = cudaFuncSetAttribute(k_grid<F, R, P, L>,                             \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                         a.smem_dyn);                                    \
+                if (e != cudaSuccess) break;                                             \
+                if (dev < kMaxDevices) set_bytes[dev] = a.smem_dyn;                      \
+            }                                                                            \
+        }                                                                                \
+        e = launch_ex(k_grid<F, R, P, L>, grid, a.tpb, (size_t)a.smem_dyn, s, a.pdl != 0, a); \
+    } while (0)
 #define RG_GRID_L(L)                                                             \
     do {                                                                         \
         if (fma) {                                                               \

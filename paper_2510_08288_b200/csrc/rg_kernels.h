@@ -77,6 +77,9 @@ struct GridArgs {
     int host_out;
     unsigned long long seq_token;
     int pdl;  // launched behind k_gen_soa with programmatic stream serialization
+    // dynamic shared memory of the launch: more than half an SM's pins one block per
+    // SM (the single-wave placement, see rg_capi.cu: grid_placement); 0 otherwise
+    int smem_dyn;
 };
 
 // Batch of independent governor instances (episodes): one launch covers
