@@ -318,7 +318,7 @@ int tpb_for(const rg_ctx* ctx, int64_t n_sim, int64_t rows) {
     return 64;
 }
 
-// Single-wave placement of the grid step.  The step's time is set by the SM
+// Single-wave placement of the grid step (and of the bisection kernels).  The step's time is set by the SM
 // sub-partition (SMSP) holding the most warps: each SMSP has its own FP64 unit and
 // issue slot, and one to three resident rollout warps share them.  With single-warp
 // blocks the block scheduler decides how a wave's warps land on SMSPs, and at
@@ -853,6 +853,7 @@ int32_t rg_bisect(rg_ctx* ctx, const rg_problem* prob, const double* x0, double 
     a.out = ctx->b_out.as<rg::BisectOut>();
     const int lpc = lpc_for(ctx, n_sim, flags);
     a.tpb = tpb_for(ctx, n_sim * lpc, 1);
+    if (lpc == 1) grid_placement(ctx, n_sim, 1, &a.tpb, &a.smem_dyn);
     const bool timed = !(flags & RG_NO_TIMING);
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
     RG_CUDA(rg::launch_bisect(a, ctx->variant == rg::kTanhFma, src, lpc, ctx->stream));
@@ -943,6 +944,7 @@ int32_t rg_joint_begin(rg_ctx* ctx, const rg_problem* prob, const double* x0, do
     RG_CUDA(cudaMemcpyAsync(a.st, ctx->h_stage.p, sizeof(init), cudaMemcpyHostToDevice,
                             ctx->stream));
     a.tpb = tpb_for(ctx, n_sim, 1);
+    grid_placement(ctx, n_sim, 1, &a.tpb, &a.smem_dyn);
     a.fold = 1;
     ctx->j_args = a;
     ctx->j_src = src;

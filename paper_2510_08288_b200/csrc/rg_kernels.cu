@@ -20,6 +20,8 @@
 
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include "rg_cell.cuh"
 #include "rg_decoupled.cuh"
 #include "rg_ws.cuh"
@@ -625,7 +627,7 @@ __device__ void joint_decide(const JointArgs& a, int it, double kappa, bool gate
 }
 
 template <bool FMA, int SRC>  // SRC: 0 zero (nominal), 1 rng, 2 soa
-__global__ void __launch_bounds__(128, RG_GRID_MINB) k_joint_roll(JointArgs a, int it) {
+__global__ void __launch_bounds__(256, RG_GRID_MINB) k_joint_roll(JointArgs a, int it) {
     __shared__ int s_run;  // 0 search finished, 1 candidate gated out, 2 roll out
     __shared__ double s_v, s_kappa;
     __shared__ bool s_last;
@@ -702,7 +704,7 @@ __global__ void k_joint_decide(JointArgs a, int it) {
 // ---------------------------------------------------------------------------
 
 template <bool FMA, int SRC, int LPC>  // SRC: 0 zero (nominal), 1 rng, 2 soa
-__global__ void __launch_bounds__(128, RG_GRID_MINB) k_bisect(BisectArgs a) {
+__global__ void __launch_bounds__(256, RG_GRID_MINB) k_bisect(BisectArgs a) {
     const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPC;
     const bool live = k < a.n_sim;
     const bool lead = threadIdx.x % LPC == 0;
@@ -1058,7 +1060,27 @@ cudaError_t launch_ex(Kern kern, dim3 grid, int block, size_t smem, cudaStream_t
     return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-constexpr int kMaxDevices = 64;
+// Opt a kernel in to `bytes` of dynamic shared memory (the single-wave placement's
+// occupancy pin), once per kernel and device.
+cudaError_t allow_dyn_smem(const void* fn, int bytes) {
+    if (bytes <= 0) return cudaSuccess;
+    struct Entry {
+        const void* fn;
+        int dev, bytes;
+    };
+    static Entry tab[256];
+    static int n = 0;
+    static std::mutex mu;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    for (int i = 0; i < n; ++i)
+        if (tab[i].fn == fn && tab[i].dev == dev && tab[i].bytes >= bytes) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess && n < 256) tab[n++] = Entry{fn, dev, bytes};
+    return e;
+}
 
 cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, int lpc,
                         cudaStream_t s) {
@@ -1066,19 +1088,8 @@ cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, int lp
     cudaError_t e = cudaSuccess;
 #define RG_GRID(F, R, P, L)                                                              \
     do {                                                                                 \
-        if (a.smem_dyn > 0) {                                                            \
-            /* raise the opt-in limit once per instantiation and device */                \
-            static int set_bytes[kMaxDevices] = {};                                      \
-            int dev = 0;                                                                 \
-            if ((e = cudaGetDevice(&dev)) != cudaSuccess) break;                         \
-            if (dev >= kMaxDevices || set_bytes[dev] < a.smem_dyn) {                     \
-                e = cudaFuncSetAttribute(k_grid<F, R, P, L>,                             \
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                                         a.smem_dyn);                                    \
-                if (e != cudaSuccess) break;                                             \
-                if (dev < kMaxDevices) set_bytes[dev] = a.smem_dyn;                      \
-            }                                                                            \
-        }                                                                                \
+        if ((e = allow_dyn_smem((const void*)k_grid<F, R, P, L>, a.smem_dyn)) != cudaSuccess) \
+            break;                                                                       \
         e = launch_ex(k_grid<F, R, P, L>, grid, a.tpb, (size_t)a.smem_dyn, s, a.pdl != 0, a); \
     } while (0)
 #define RG_GRID_L(L)                                                             \
@@ -1147,7 +1158,13 @@ cudaError_t launch_grid_batch(const BatchArgs& a, bool fma, bool poll, int lpc, 
 
 cudaError_t launch_joint_roll(const JointArgs& a, int it, bool fma, int src, cudaStream_t s) {
     const unsigned blocks = (unsigned)((a.n_sim + a.tpb - 1) / a.tpb);
-#define RG_J(F, S) k_joint_roll<F, S><<<blocks, a.tpb, 0, s>>>(a, it)
+    cudaError_t e = cudaSuccess;
+#define RG_J(F, S)                                                                      \
+    do {                                                                                \
+        if ((e = allow_dyn_smem((const void*)k_joint_roll<F, S>, a.smem_dyn)) != cudaSuccess) \
+            return e;                                                                   \
+        k_joint_roll<F, S><<<blocks, a.tpb, (size_t)a.smem_dyn, s>>>(a, it);            \
+    } while (0)
     if (fma) {
         if (src == 1) RG_J(true, 1); else if (src == 2) RG_J(true, 2); else RG_J(true, 0);
     } else {
@@ -1164,7 +1181,13 @@ cudaError_t launch_joint_decide(const JointArgs& a, int it, cudaStream_t s) {
 
 cudaError_t launch_bisect(const BisectArgs& a, bool fma, int src, int lpc, cudaStream_t s) {
     const unsigned g = blocks_for(a.n_sim * lpc, a.tpb);
-#define RG_BIS(F, S, L) k_bisect<F, S, L><<<g, a.tpb, 0, s>>>(a)
+    cudaError_t e = cudaSuccess;
+#define RG_BIS(F, S, L)                                                                 \
+    do {                                                                                \
+        if ((e = allow_dyn_smem((const void*)k_bisect<F, S, L>, a.smem_dyn)) != cudaSuccess) \
+            return e;                                                                   \
+        k_bisect<F, S, L><<<g, a.tpb, (size_t)a.smem_dyn, s>>>(a);                      \
+    } while (0)
 #define RG_BIS_L(L)                                                              \
     do {                                                                         \
         if (fma) {                                                               \

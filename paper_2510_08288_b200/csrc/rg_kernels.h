@@ -163,6 +163,7 @@ struct BisectArgs {
     BisectAcc* acc;
     BisectOut* out;
     int tpb;
+    int smem_dyn;  // dynamic shared memory (single-wave placement pin), bytes
 };
 
 // Joint bisection: one candidate kappa for every
@@ -187,6 +188,7 @@ struct JointArgs {
     int64_t ld;
     JointState* st;
     int tpb;
+    int smem_dyn;  // dynamic shared memory (single-wave placement pin), bytes
     int fold;  // 1: the last block decides (single GPU); 0: k_joint_decide after the all-reduce
 };
 
