@@ -308,6 +308,7 @@ def run_own(args, rank, world, local_rank):
         roof = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
                 "unit": "TFLOP/s", "frac": achieved / peak, "traffic": _ncu_traffic(),
                 "fp64_pipe_frac": fp64_instr_rate / (peak / 2.0),
+                "issue_model": issue_model(n_sim, j_star, kernel_ms, clocks),
                 "fp64_instr_per_cell_step": fp64_per_cell,
                 "peak_source": "measured in this run: rg_fp64_peak (independent DFMA chains, "
                                "2 flop per DFMA); MEASURED_PEAKS.json has no FP64 figure",
@@ -354,6 +355,8 @@ def run_own(args, rank, world, local_rank):
             rate = cells / (t.mean() * 1e-3)
             sweep.append({"n_sim": n_big, "ms_per_step": float(t.mean()), "value": rate,
                           "unit": UNIT, "roofline_frac": FLOPS_PER_CELL_STEP * rate / peak,
+                          "issue_frac": issue_model(n_big, j_star, float(t.mean()),
+                                                    clocks)["frac"],
                           "rng": "staged" if n_big * j_star * 24 <= (16 << 30) else "fused"})
 
     if world > 1:
@@ -471,6 +474,27 @@ def _ncu_summary():
         return json.loads(p.read_text())
     except (OSError, ValueError):
         return {}
+
+
+def issue_model(n_sim, j_star, ms, clocks, sm_count=148):
+    """The rollout's instruction-issue bound.  Each SM sub-partition (SMSP) issues
+    one warp-instruction per cycle, and an FP64 warp-instruction holds the issue
+    slot for two (16 FP64 lanes per SMSP): a warp-step costs 2*FP64 + other cycles
+    (ncu counts, profiles/k_grid_ncu.json).  Bound = all warp-steps spread evenly
+    over the 4*148 SMSPs at the measured SM clock; frac = bound / measured."""
+    ncu = _ncu_summary()
+    fp64 = ncu.get("fp64_instr_per_cell_step")
+    total = ncu.get("instr_per_cell_step")
+    if not fp64 or not total or not ms:
+        return {"frac": None}
+    cyc = 2.0 * fp64 + (total - fp64)
+    mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    warp_steps = (n_sim + 31) // 32 * M_GRID * j_star
+    bound_ms = warp_steps / (4 * sm_count) * cyc / (mhz * 1e3)
+    return {"cycles_per_warp_step": cyc, "bound_ms": bound_ms, "frac": bound_ms / ms,
+            "note": "2 issue cycles per FP64 warp-instruction + 1 per other, all warp-steps "
+                    "balanced over 592 SMSPs (at 1000 scenarios the 1000 warps cannot "
+                    "balance below 2 per loaded SMSP: that bound is 1.16x this one)"}
 
 
 def _ncu_traffic():

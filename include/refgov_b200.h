@@ -65,7 +65,9 @@ extern "C" {
 /* With neither RG_FUSED_RNG nor RG_STAGE_RNG an RNG source is staged when the
  * SoA block (n_sim * j_star * 24 bytes) is at most 16 GB for the fill and the
  * grid step (all candidate rows share it), at most 96 MB for the bisections
- * (whose rollouts often stop after a few steps), and fused above. */
+ * (whose rollouts often stop after a few steps), and fused above.  The batched
+ * grid step stages each episode's block, in chunks of episodes of at most 16 GB,
+ * unless RG_FUSED_RNG (or a lanes-per-cell split) is given. */
 #define RG_LPC1 0x80        /* force 1 lane per (row, scenario) cell */
 #define RG_LPC2 0x100       /* force 2 lanes per cell (each evaluates 2 of the 4 tanh) */
 #define RG_LPC4 0x200       /* force 4 lanes per cell (1 tanh each) */

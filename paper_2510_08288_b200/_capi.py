@@ -350,8 +350,10 @@ class Context:
         return res
 
     def grid_step_batch(self, prob: Problem, x0, v_prev, r, seeds, k0, n_sim, lo, span,
-                        m_grid, prefix_mode=False, abandon=True, want_viol=False, lpc=None):
-        """Batched robust grid step; returns (row, kappa, v, early[, viol])."""
+                        m_grid, prefix_mode=False, abandon=True, want_viol=False, lpc=None,
+                        fused=False):
+        """Batched robust grid step; returns (row, kappa, v, early[, viol]).  The
+        scenario blocks are staged per episode unless `fused` (or lpc > 1)."""
         x0 = np.ascontiguousarray(x0, dtype=np.float64).reshape(-1, 3)
         E = x0.shape[0]
         v_prev = np.ascontiguousarray(v_prev, dtype=np.float64).reshape(E)
@@ -368,7 +370,8 @@ class Context:
                                           _p(r), _p(seeds), int(k0), int(n_sim), _p(lo),
                                           _p(span), int(m_grid), int(bool(prefix_mode)),
                                           _p(row), _p(kap), _p(v), _p(early), _p(viol),
-                                          (RG_ABANDON if abandon else 0) | _LPC_FLAGS[lpc]))
+                                          (RG_ABANDON if abandon else 0) | _LPC_FLAGS[lpc]
+                                          | (RG_FUSED_RNG if fused else 0)))
         return (row, kap, v, early, viol) if want_viol else (row, kap, v, early)
 
     def fill_linear(self, lin: LinearPlant, prob: Problem, x0, v_rows, rows, dist, n_sim,

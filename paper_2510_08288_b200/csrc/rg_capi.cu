@@ -1091,8 +1091,33 @@ int32_t rg_grid_step_batch(rg_ctx* ctx, const rg_problem* prob, int32_t n_episod
     a.viol_out = row_viol ? ctx->e_violout.as<unsigned>() : nullptr;
     const int lpc = lpc_for(ctx, n_sim * E * M, flags);
     a.tpb = tpb_for(ctx, n_sim * E * lpc, m_grid);
-    RG_CUDA(rg::launch_grid_batch(a, ctx->variant == rg::kTanhFma, (flags & RG_ABANDON) != 0,
-                                  lpc, ctx->stream));
+    const bool fma = ctx->variant == rg::kTanhFma, poll = (flags & RG_ABANDON) != 0;
+    // Staged: each episode's scenario block is generated into SoA once and shared by
+    // its M rows (~20% faster than regenerating it in every cell, as for the single
+    // step); episodes go in chunks of at most 16 GB of SoA.  Fused otherwise.
+    const int64_t ld = (n_sim + 31) / 32 * 32;
+    const int64_t ep_stride = (int64_t)prob->j_star * 3 * ld;
+    const int64_t per_chunk = kStageMaxScenarioSteps / std::max<int64_t>(1, n_sim * prob->j_star);
+    if (lpc == 1 && !(flags & RG_FUSED_RNG) && per_chunk >= 1) {
+        int64_t ec = std::min<int64_t>(E, per_chunk);
+        if (const char* env = getenv("RG_BATCH_CHUNK"))  // tests: force several chunks
+            ec = std::max<int64_t>(1, std::min<int64_t>(ec, atoll(env)));
+        RG_CUDA(ctx->soa.ensure((size_t)ec * ep_stride * sizeof(double)));
+        a.soa = ctx->soa.as<double>();
+        a.ld = ld;
+        a.ep_stride = ep_stride;
+        for (int64_t e0 = 0; e0 < E; e0 += ec) {
+            const int32_t n = (int32_t)std::min<int64_t>(ec, E - e0);
+            RG_CUDA(rg::launch_gen_soa_batch(a.hs + e0, lo, span, k0, n_sim, prob->j_star, ld, n,
+                                             ep_stride, ctx->soa.as<double>(), ctx->stream));
+            a.e0 = (int32_t)e0;
+            a.n_ep = n;
+            RG_CUDA(rg::launch_grid_batch(a, fma, poll, 1, ctx->stream));
+        }
+        a.n_ep = n_episodes;
+    } else {
+        RG_CUDA(rg::launch_grid_batch(a, fma, poll, lpc, ctx->stream));
+    }
     char* hout = reinterpret_cast<char*>(hin + 6 * E);
     const size_t out_bytes = (size_t)E * (3 * sizeof(double) + sizeof(int));
     RG_CUDA(cudaMemcpyAsync(hout, dout, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));

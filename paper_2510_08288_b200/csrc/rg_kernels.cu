@@ -117,6 +117,31 @@ __global__ void k_gen_soa(ScenarioStream st, int64_t k0, int64_t n_sim, int32_t 
     o[2 * ld] = d2;
 }
 
+// k_gen_soa for a batch of episodes (blockIdx.z), each with its own stream key hs[z]
+// and a block of its own at dst + z * ep_stride.
+__global__ void k_gen_soa_batch(const uint64_t* __restrict__ hs, double3 lo, double3 span,
+                                int64_t k0, int64_t n_sim, int32_t j_star, int64_t ld,
+                                int64_t ep_stride, double* __restrict__ dst) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int32_t j = blockIdx.y;
+    if (k >= n_sim || j >= j_star) return;
+    ScenarioStream st;
+    st.hs = hs[blockIdx.z];
+    st.lo[0] = lo.x;
+    st.lo[1] = lo.y;
+    st.lo[2] = lo.z;
+    st.span[0] = span.x;
+    st.span[1] = span.y;
+    st.span[2] = span.z;
+    const uint64_t K = scenario_key(st, (uint64_t)(k0 + k));
+    double d0, d1, d2;
+    disturbance_at(st, K, (uint64_t)j, d0, d1, d2);
+    double* o = dst + (int64_t)blockIdx.z * ep_stride + (int64_t)j * 3 * ld + k;
+    o[0] = d0;
+    o[ld] = d1;
+    o[2 * ld] = d2;
+}
+
 // tile transpose of [n_sim][horizon][3] (rows j < j_star) into d[(j*3+i)*ld + k]
 __global__ void k_to_soa(const double* __restrict__ src, double* __restrict__ dst,
                          int64_t n_sim, int64_t horizon, int32_t j_star, int64_t ld) {
@@ -505,12 +530,12 @@ __global__ void __launch_bounds__(32 * (1 + W)) k_grid_ws(GridArgs a) {
 // batched grid step: E independent governor instances in one launch
 // ---------------------------------------------------------------------------
 
-template <bool FMA, bool POLL, int LPC>
+template <bool FMA, bool POLL, int LPC, bool SOA = false>
 __global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid_batch(BatchArgs a) {
     __shared__ int s_src;
     __shared__ double s_v;
     __shared__ bool s_last;
-    const int e = blockIdx.z;
+    const int e = a.e0 + (int)blockIdx.z;
     const int i = blockIdx.y;
     const int M = a.m_grid;
     const double vp = a.v_prev[e], rr = a.r[e];
@@ -535,16 +560,24 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid_batch(BatchArgs a) {
         int32_t steps = a.p.j_star;
         constexpr bool W = LPC == 1 && RG_GRID_WARP;  // whole warps run the rollout
         if (live || LPC > 1 || W) {
-            ScenarioStream ss;
-            ss.hs = a.hs[e];
-            for (int c = 0; c < 3; ++c) {
-                ss.lo[c] = a.lo[c];
-                ss.span[c] = a.span[c];
-            }
-            RngSource src{ss, scenario_key(ss, (uint64_t)(a.k0 + (live ? k : 0)))};
             const double* x0 = a.x0 + 3 * (int64_t)e;
-            st = rollout<FMA, POLL, LPC, RngSource, W>(make_cell(a.p), x0[0], x0[1], x0[2], s_v,
-                                                       src, steps, viol + i, live);
+            if constexpr (SOA) {  // staged block of this episode (k_gen_soa_batch)
+                __shared__ double ring[2 * 3 * kRingStride];
+                SoaSource src{a.soa + (int64_t)blockIdx.z * a.ep_stride + (live ? k : 0), a.ld,
+                              ring + threadIdx.x};
+                st = rollout<FMA, POLL, LPC, SoaSource, W>(make_cell(a.p), x0[0], x0[1], x0[2],
+                                                           s_v, src, steps, viol + i, live);
+            } else {
+                ScenarioStream ss;
+                ss.hs = a.hs[e];
+                for (int c = 0; c < 3; ++c) {
+                    ss.lo[c] = a.lo[c];
+                    ss.span[c] = a.span[c];
+                }
+                RngSource src{ss, scenario_key(ss, (uint64_t)(a.k0 + (live ? k : 0)))};
+                st = rollout<FMA, POLL, LPC, RngSource, W>(make_cell(a.p), x0[0], x0[1], x0[2],
+                                                           s_v, src, steps, viol + i, live);
+            }
         }
         const bool cnt = live && lead;
         const unsigned bad = __ballot_sync(0xffffffffu, cnt && st != kOk && st != kAbandoned);
@@ -1151,8 +1184,28 @@ cudaError_t launch_grid_batch(const BatchArgs& a, bool fma, bool poll, int lpc, 
             else      k_grid_batch<false, false, L><<<grid, a.tpb, 0, s>>>(a);   \
         }                                                                        \
     } while (0)
+    if (a.soa) {  // staged episodes: one lane per cell only
+        if (fma) {
+            if (poll) k_grid_batch<true, true, 1, true><<<grid, a.tpb, 0, s>>>(a);
+            else      k_grid_batch<true, false, 1, true><<<grid, a.tpb, 0, s>>>(a);
+        } else {
+            if (poll) k_grid_batch<false, true, 1, true><<<grid, a.tpb, 0, s>>>(a);
+            else      k_grid_batch<false, false, 1, true><<<grid, a.tpb, 0, s>>>(a);
+        }
+        return cudaGetLastError();
+    }
     RG_DISPATCH_LPC(lpc, RG_BATCH);
 #undef RG_BATCH
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gen_soa_batch(const uint64_t* hs, const double* lo, const double* span,
+                                 int64_t k0, int64_t n_sim, int32_t j_star, int64_t ld,
+                                 int32_t n_ep, int64_t ep_stride, double* dst, cudaStream_t s) {
+    dim3 grid(blocks_for(n_sim, 128), (unsigned)j_star, (unsigned)n_ep);
+    k_gen_soa_batch<<<grid, 128, 0, s>>>(hs, make_double3(lo[0], lo[1], lo[2]),
+                                          make_double3(span[0], span[1], span[2]), k0, n_sim,
+                                          j_star, ld, ep_stride, dst);
     return cudaGetLastError();
 }
 

@@ -103,6 +103,11 @@ struct BatchArgs {
     long long* early_out;   // [E]
     unsigned* viol_out;     // [E][M] or null
     int tpb;
+    // staged source (k_gen_soa_batch): episodes [e0, e0 + gridDim.z) of this launch,
+    // episode e's block at soa + (e - e0) * ep_stride, d[(j*3+i)*ld + k]; null: fused RNG
+    const double* soa;
+    int64_t ld, ep_stride;
+    int32_t e0;
 };
 
 // Linear-plant fill and bisection (kernels.py:90-118 behind governor.py).
@@ -199,6 +204,9 @@ cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s);
 cudaError_t launch_to_soa(const double* src, double* dst, int64_t n_sim, int64_t horizon,
                           int32_t j_star, int64_t ld, cudaStream_t s);
 cudaError_t launch_fill(const FillArgs& a, bool fma, bool rng, int lpc, cudaStream_t s);
+cudaError_t launch_gen_soa_batch(const uint64_t* hs, const double* lo, const double* span,
+                                 int64_t k0, int64_t n_sim, int32_t j_star, int64_t ld,
+                                 int32_t n_ep, int64_t ep_stride, double* dst, cudaStream_t s);
 cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, int lpc,
                         cudaStream_t s);
 cudaError_t launch_grid_batch(const BatchArgs& a, bool fma, bool poll, int lpc, cudaStream_t s);

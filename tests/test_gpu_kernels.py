@@ -228,6 +228,30 @@ def test_batch_every_lane_split(ctx, lpc):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("abandon", [False, True])
+@pytest.mark.parametrize("chunk", [None, 5, 1])
+def test_batch_staged_chunks_equal_fused(ctx, monkeypatch, chunk, abandon):
+    """Staged episode blocks (k_gen_soa_batch), in one or several chunks of
+    episodes, against the fused in-rollout RNG: same rows, kappas, setpoints,
+    early counts and per-row violation counts."""
+    if chunk is not None:
+        monkeypatch.setenv("RG_BATCH_CHUNK", str(chunk))
+    rng = np.random.default_rng(11)
+    E, n, M = 13, 150, 8
+    vp = rng.uniform(-1, 1, E)
+    r = rng.uniform(-2.5, 2.5, E)
+    X = np.stack([[np.tanh(v), v, np.tanh(v) / 2] for v in vp]) + rng.uniform(-0.05, 0.05, (E, 3))
+    seeds = [int(x) for x in rng.integers(0, 2**63, E)]
+    m = rg.DisturbanceModel.scaled(0.02, 3)
+    prob = _problem(-0.9, 0.9, 0.0, 0.05, 64)
+    ref = ctx.grid_step_batch(prob, X, vp, r, seeds, 7, n, m.lo, m.span, M, abandon=abandon,
+                              want_viol=not abandon, fused=True)
+    got = ctx.grid_step_batch(prob, X, vp, r, seeds, 7, n, m.lo, m.span, M, abandon=abandon,
+                              want_viol=not abandon)
+    for a, b in zip(ref, got):
+        assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("kernel", ["warp-spec", "decoupled", "per-step"])
 @pytest.mark.parametrize("mode", ["fused", "staged"])
 @pytest.mark.parametrize("idx", range(N_FILL))
