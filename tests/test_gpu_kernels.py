@@ -328,3 +328,34 @@ def test_grid_fetch_after_sync_and_async_steps(ctx):
         assert (got.row, got.sims_run, got.early_terms, got.overflows) == \
             (res.row, res.sims_run, res.early_terms, res.overflows)
         assert np.array_equal(v2, viol)
+
+
+@pytest.mark.parametrize("env", [{"RG_NO_PLACEMENT": "1"}, {"RG_FORCE_TPB": "32"},
+                                 {"RG_FORCE_TPB": "128"}])
+@pytest.mark.parametrize("shape", [(1000, 32), (300, 32), (4000, 32), (97, 5)])
+def test_single_wave_placement_changes_no_bit(ctx, monkeypatch, env, shape):
+    """The single-wave placement (blocks of 4L warps pinned one per SM) against the
+    other block shapes, on transient-binding inputs: same P bits, per-row counts,
+    result row and counters; and the same for the bisections."""
+    n, M = shape
+    rng = np.random.default_rng(n + M)
+    vp = 0.4
+    x0 = np.array([np.tanh(vp), vp, np.tanh(vp) / 2]) + rng.uniform(-0.05, 0.05, 3)
+    m = rg.DisturbanceModel.scaled(0.02, 3)
+    scen = _capi.make_scenarios(4242 + n, 0, n, m.lo, m.span)
+    prob = _problem(-0.9, 0.9, 0.0, 0.05, 256)
+
+    def run():
+        res, viol, pbits = ctx.grid_step(prob, x0, vp, 2.4, M, False, None, n, scen, True)
+        b, _, _ = ctx.bisect(prob, x0, vp, 2.4, 8, None, n, scen)
+        j = ctx.bisect_joint(prob, x0, vp, 2.4, 8, None, n, scen)
+        return (res.row, res.sims_run, res.early_terms, res.overflows, viol.copy(),
+                pbits.copy(), b.kappa, b.found, b.cells, b.early, j.kappa, j.found, j.cells)
+
+    ref = run()
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    got = run()
+    assert ref[1] > 0 and 0 < int(np.count_nonzero(ref[4])) , "inputs must bind some rows"
+    for a, b in zip(ref, got):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
