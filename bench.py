@@ -370,6 +370,35 @@ def run_own(args, rank, world, local_rank):
                "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e * 1e3,
                "api": "paper_2510_08288_b200.robust_rg_parallel (keep_matrix=True)"}
 
+    # latency split of one synchronous step (the C ABI call a user makes, no P):
+    # host call -> result in host memory, the device span of k_grid (first block
+    # start to publication, globaltimer), and the final reduction inside it
+    latency = None
+    if world == 1:
+        sync_res = _capi.GridResult()
+        walls, spans, reds = [], [], []
+        for s in range(220):
+            scen = _capi.make_scenarios(BASE_SEED + 20000 + s, k0, n_sim, model.lo, model.span)
+            t0 = time.perf_counter()
+            _capi.check(lib.rg_grid_step(ctx.handle, prob, x0_ptr, 0.0, R_REF, M_GRID, 0, None,
+                                         n_sim, 0, scen, None, None, sync_res,
+                                         _capi.RG_NO_TIMING))
+            dt = time.perf_counter() - t0
+            if s >= 20:
+                walls.append(dt * 1e6)
+                spans.append(sync_res.kernel_ms * 1e3)
+                reds.append(sync_res.reduce_us)
+        latency = {"api_call_us": float(np.median(walls)),
+                   "k_grid_span_us": float(np.median(spans)),
+                   "launch_overhead_us": float(np.median(walls) - np.median(spans)),
+                   "reduction_us": float(np.median(reds)),
+                   "note": "median of 200 synchronous rg_grid_step calls at the workload "
+                           "(no P): api_call = host wall time of the call; k_grid_span = "
+                           "first block start to result publication (device globaltimer); "
+                           "launch_overhead = the difference (host enqueue, launch latency, "
+                           "k_gen_soa, result visibility); reduction = the last block's row "
+                           "extraction and publication inside the span"}
+
     # larger scenario counts (BASELINE C3 size and the C4 shard size), same step
     sweep = []
     if world == 1 and not args.no_sweep:
@@ -488,7 +517,8 @@ def run_own(args, rank, world, local_rank):
                        "parallelism": f"scenario shards x{world}" + (", NCCL all-reduce of "
                                                                      "row counts" if world > 1
                                                                      else "")},
-            "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "sweep": sweep,
+            "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "latency": latency,
+            "sweep": sweep,
             "gpu_launches": args.steps * launches_per_step, "clocks": clocks,
             "host_enqueue_ms_per_step": wall * 1e3 / args.steps,  # incl. the chunks' device sleep
             "kernel_ms_p50": float(np.median(per)), "kernel_ms_min": float(per.min()),

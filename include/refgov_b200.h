@@ -129,7 +129,9 @@ typedef struct {
     int64_t overflows;      /* cells ending in CELL_OVERFLOW (governor.py:343) */
     int64_t abandoned;      /* cells stopped by RG_ABANDON (0 without it) */
     float kernel_ms;        /* CUDA-event time of the step kernel */
-    int32_t _pad;
+    float reduce_us;        /* device time of the final reduction: the last block's row
+                               extraction and result publication (globaltimer; 0 when the
+                               kernel does not record it) */
 } rg_grid_result;
 
 /* Result of rg_bisect (robust_rg_sequential / bisection_rg). */

@@ -69,7 +69,7 @@ class GridResult(ctypes.Structure):
     _fields_ = [("row", _i32), ("n_active", _i32), ("ss_pruned_rows", _i32),
                 ("dedup_rows", _i32), ("sims_run", _i64), ("early_terms", _i64),
                 ("overflows", _i64), ("abandoned", _i64), ("kernel_ms", ctypes.c_float),
-                ("_pad", _i32)]
+                ("reduce_us", ctypes.c_float)]
 
 
 class BisectResult(ctypes.Structure):

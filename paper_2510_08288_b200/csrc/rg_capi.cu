@@ -647,6 +647,7 @@ static int32_t unpack_grid(rg_ctx* ctx, const char* h, uint32_t* row_viol, int32
         out->overflows = ho->overflows;
         out->abandoned = ho->abandoned;
         out->kernel_ms = (float)((double)ho->kernel_ns * 1e-6);  // device globaltimer span
+        out->reduce_us = (float)((double)ho->reduce_ns * 1e-3);
         if (timed) {
             float ms = 0.f;
             cudaEventSynchronize(ctx->ev1);

@@ -264,11 +264,13 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 // a few L2 round trips rather than one chain of loads per row.
 __device__ __forceinline__ void grid_finalize(const GridArgs& a) {
     __shared__ bool s_last;
+    __shared__ unsigned long long s_tfin;  // globaltimer when this block won the ticket
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         const unsigned total = gridDim.x * gridDim.y;
         s_last = atomicAdd(a.ticket, 1u) == total - 1;
+        s_tfin = global_ns();
     }
     __syncthreads();
     if (!s_last) return;
@@ -345,7 +347,9 @@ __device__ __forceinline__ void grid_finalize(const GridArgs& a) {
             a.out->abandoned = (long long)aband;
             a.out->sims_run = (long long)n_active * a.n_sim;
             if (a.t0) {
-                a.out->kernel_ns = global_ns() - *(volatile unsigned long long*)a.t0;
+                const unsigned long long now = global_ns();
+                a.out->kernel_ns = now - *(volatile unsigned long long*)a.t0;
+                a.out->reduce_ns = now - s_tfin;
                 *a.t0 = ~0ull;
             }
             // publish: every result word above (and every block's P bits) before seq

@@ -47,6 +47,7 @@ struct GridOut {
     long long sims_run, early_terms, overflows, abandoned;
     unsigned long long seq;
     unsigned long long kernel_ns;  // device span of the step (globaltimer)
+    unsigned long long reduce_ns;  // the last block's row extraction and publication
 };
 
 struct GridArgs {
