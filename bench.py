@@ -18,8 +18,8 @@ scenario seed every step.  All 32 rows are feasible, so one step is exactly
          every host core, same workload.
 
 Multi-GPU (torchrun): rank r takes scenarios [r*n, (r+1)*n) of one global
-stream (weak scaling); per-row violation counts are summed with one NCCL
-all-reduce per step and every rank extracts the same row.
+stream (weak scaling); the per-row violation counts go through one NCCL
+all-reduce (MAX) per step and every rank extracts the same row on the device.
 """
 
 from __future__ import annotations
@@ -259,7 +259,8 @@ def run_own(args, rank, world, local_rank):
     x0_ptr = x0.ctypes.data_as(ctypes_vp())  # kernel parameter: host memory
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32,
                         device=f"cuda:{local_rank}")
-    big = torch.tensor(1 << 40, dtype=torch.int64, device=f"cuda:{local_rank}")
+    row_idx = torch.arange(M_GRID, dtype=torch.int32, device=f"cuda:{local_rank}")
+    minus1 = torch.full_like(row_idx, -1)
 
     def step(s):
         scen = _capi.make_scenarios(BASE_SEED + s, k0, n_sim, model.lo, model.span)
@@ -268,14 +269,10 @@ def run_own(args, rank, world, local_rank):
                                      ctypes_vp()(viol.data_ptr()) if world > 1 else None,
                                      None, res, flags))
         if world > 1:
-            import torch.distributed as dist
-            c = viol.to(torch.int64)
-            c = torch.where(c == -1, big, c)
-            dist.all_reduce(c)
-            full = c == 0
-            idx = torch.arange(M_GRID, device=c.device)
-            best = torch.where(full, idx, torch.full_like(idx, -1)).max()
-            return best
+            # per-row violating-scenario counts, int32 (a gated-out row is -1 on every
+            # rank): the global MAX is 0 exactly for the rows feasible on every shard
+            torch.distributed.all_reduce(viol, op=torch.distributed.ReduceOp.MAX)
+            return torch.where(viol == 0, row_idx, minus1).max()  # literal Eq. 4
         return None
 
     with torch.cuda.stream(stream):
@@ -515,7 +512,7 @@ def run_own(args, rank, world, local_rank):
                        "r": R_REF, "cell_steps_per_step": cells_rank * world,
                        "l2": "flushed between timed steps (256 MB write, outside the events)",
                        "parallelism": f"scenario shards x{world}" + (", NCCL all-reduce of "
-                                                                     "row counts" if world > 1
+                                                                     "row counts (MAX)" if world > 1
                                                                      else "")},
             "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "latency": latency,
             "sweep": sweep,
