@@ -261,7 +261,8 @@ __device__ __forceinline__ void step_tanh(double x2, double a2, double b2, doubl
 // RAISE (with WARP and POLL): a lane whose cell violates or overflows sets
 // *dead at once, so the other cells sharing the flag abandon at their next
 // poll (the joint bisection's OR-reduced violation flag).
-template <bool FMA, bool POLL, int LPC, class Src, bool WARP = false, bool RAISE = false>
+template <bool FMA, bool POLL, int LPC, class Src, bool WARP = false, bool RAISE = false,
+          bool MOD = false>
 __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2, double x3,
                                        double v, const Src& src, int32_t& steps,
                                        const unsigned int* dead, bool live = true) {
@@ -347,7 +348,7 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
         };
         double u1, u2, u3, u4;
         if constexpr (LPC == 1) {
-            tanh4_with<FMA, WARP>(g0, g1, g2, g3, u1, u2, u3, u4, side);
+            tanh4_with<FMA, WARP, decltype(side)&, MOD>(g0, g1, g2, g3, u1, u2, u3, u4, side);
         } else {
             step_tanh<FMA, LPC>(g0, g1, g2, g3, u1, u2, u3, u4);
             side();

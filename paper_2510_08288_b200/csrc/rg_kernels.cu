@@ -367,7 +367,9 @@ __device__ __forceinline__ void grid_finalize(const GridArgs& a) {
     if (threadIdx.x == 0) *a.ticket = 0u;
 }
 
-template <bool FMA, bool RNG, bool POLL, int LPC>
+// MOD: the tanh forms' operand-modifier variant (rg_math.cuh), for the
+// issue-bound multi-wave steps; the single-wave (latency-bound) step keeps MOD off.
+template <bool FMA, bool RNG, bool POLL, int LPC, bool MOD = false>
 __global__ void __launch_bounds__(256, RG_GRID_MINB) k_grid(GridArgs a) {
     __shared__ int s_src;
     __shared__ double s_v;
@@ -399,12 +401,12 @@ __global__ void __launch_bounds__(256, RG_GRID_MINB) k_grid(GridArgs a) {
             const CellConst c = make_cell(a.p);
             if (RNG) {
                 RngSource src{a.stream, scenario_key(a.stream, (uint64_t)(a.k0 + kk))};
-                st = rollout<FMA, POLL, LPC, RngSource, W>(c, a.x0[0], a.x0[1], a.x0[2], s_v,
+                st = rollout<FMA, POLL, LPC, RngSource, W, false, MOD>(c, a.x0[0], a.x0[1], a.x0[2], s_v,
                                                            src, steps, a.viol + i, live);
             } else {
                 __shared__ double ring[2 * 3 * kRingStride];
                 SoaSource src{a.soa + kk, a.ld, ring + threadIdx.x};
-                st = rollout<FMA, POLL, LPC, SoaSource, W>(c, a.x0[0], a.x0[1], a.x0[2], s_v,
+                st = rollout<FMA, POLL, LPC, SoaSource, W, false, MOD>(c, a.x0[0], a.x0[1], a.x0[2], s_v,
                                                            src, steps, a.viol + i, live);
             }
         }
@@ -534,8 +536,10 @@ __global__ void __launch_bounds__(32 * (1 + W)) k_grid_ws(GridArgs a) {
 // batched grid step: E independent governor instances in one launch
 // ---------------------------------------------------------------------------
 
+// Launch bounds: at most 168 registers (3 blocks of 128 threads per SM), so the
+// 64-thread blocks keep 12 warps per SM (3 per SMSP) in this always multi-wave kernel.
 template <bool FMA, bool POLL, int LPC, bool SOA = false>
-__global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid_batch(BatchArgs a) {
+__global__ void __launch_bounds__(128, 3) k_grid_batch(BatchArgs a) {
     __shared__ int s_src;
     __shared__ double s_v;
     __shared__ bool s_last;
@@ -569,7 +573,7 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid_batch(BatchArgs a) {
                 __shared__ double ring[2 * 3 * kRingStride];
                 SoaSource src{a.soa + (int64_t)blockIdx.z * a.ep_stride + (live ? k : 0), a.ld,
                               ring + threadIdx.x};
-                st = rollout<FMA, POLL, LPC, SoaSource, W>(make_cell(a.p), x0[0], x0[1], x0[2],
+                st = rollout<FMA, POLL, LPC, SoaSource, W, false, true>(make_cell(a.p), x0[0], x0[1], x0[2],
                                                            s_v, src, steps, viol + i, live);
             } else {
                 ScenarioStream ss;
@@ -579,7 +583,7 @@ __global__ void __launch_bounds__(128, RG_GRID_MINB) k_grid_batch(BatchArgs a) {
                     ss.span[c] = a.span[c];
                 }
                 RngSource src{ss, scenario_key(ss, (uint64_t)(a.k0 + (live ? k : 0)))};
-                st = rollout<FMA, POLL, LPC, RngSource, W>(make_cell(a.p), x0[0], x0[1], x0[2],
+                st = rollout<FMA, POLL, LPC, RngSource, W, false, true>(make_cell(a.p), x0[0], x0[1], x0[2],
                                                            s_v, src, steps, viol + i, live);
             }
         }
@@ -1123,11 +1127,17 @@ cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, int lp
                         cudaStream_t s) {
     dim3 grid(blocks_for(a.n_sim * lpc, a.tpb), (unsigned)a.m_grid);
     cudaError_t e = cudaSuccess;
+#define RG_GRID_M(F, R, P, L, M)                                                         \
+    do {                                                                                 \
+        if ((e = allow_dyn_smem((const void*)k_grid<F, R, P, L, M>, a.smem_dyn)) != cudaSuccess) \
+            break;                                                                       \
+        e = launch_ex(k_grid<F, R, P, L, M>, grid, a.tpb, (size_t)a.smem_dyn, s, a.pdl != 0, a); \
+    } while (0)
+    // the operand-modifier tanh forms above one wave (issue-bound), one lane per cell
 #define RG_GRID(F, R, P, L)                                                              \
     do {                                                                                 \
-        if ((e = allow_dyn_smem((const void*)k_grid<F, R, P, L>, a.smem_dyn)) != cudaSuccess) \
-            break;                                                                       \
-        e = launch_ex(k_grid<F, R, P, L>, grid, a.tpb, (size_t)a.smem_dyn, s, a.pdl != 0, a); \
+        if (L == 1 && a.smem_dyn == 0) RG_GRID_M(F, R, P, 1, true);                      \
+        else RG_GRID_M(F, R, P, L, false);                                               \
     } while (0)
 #define RG_GRID_L(L)                                                             \
     do {                                                                         \
@@ -1142,6 +1152,7 @@ cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, int lp
     RG_DISPATCH_LPC(lpc, RG_GRID_L);
 #undef RG_GRID_L
 #undef RG_GRID
+#undef RG_GRID_M
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
