@@ -530,9 +530,10 @@ def ctypes_vp():
     return ctypes.c_void_p
 
 
-def _ncu_summary():
-    """The committed ncu --set full summary of k_grid at C2 (scripts/ncu_summary.py)."""
-    p = ROOT / "profiles" / "k_grid_ncu.json"
+def _ncu_summary(name="k_grid_ncu.json"):
+    """A committed ncu --set full summary of k_grid (scripts/ncu_summary.py): at C2
+    by default, k_grid_ncu_10k.json for the multi-wave form."""
+    p = ROOT / "profiles" / name
     try:
         return json.loads(p.read_text())
     except (OSError, ValueError):
@@ -545,7 +546,10 @@ def issue_model(n_sim, j_star, ms, clocks, sm_count=148):
     slot for two (16 FP64 lanes per SMSP): a warp-step costs 2*FP64 + other cycles
     (ncu counts, profiles/k_grid_ncu.json).  Bound = all warp-steps spread evenly
     over the 4*148 SMSPs at the measured SM clock; frac = bound / measured."""
-    ncu = _ncu_summary()
+    # the single-wave step runs the integer tanh forms (profiles/k_grid_ncu.json, C2),
+    # above one wave the operand-modifier forms (profiles/k_grid_ncu_10k.json)
+    single_wave = (n_sim + 255) // 256 * M_GRID <= sm_count
+    ncu = _ncu_summary() if single_wave else _ncu_summary("k_grid_ncu_10k.json")
     fp64 = ncu.get("fp64_instr_per_cell_step")
     total = ncu.get("instr_per_cell_step")
     if not fp64 or not total or not ms:
@@ -555,6 +559,7 @@ def issue_model(n_sim, j_star, ms, clocks, sm_count=148):
     warp_steps = (n_sim + 31) // 32 * M_GRID * j_star
     bound_ms = warp_steps / (4 * sm_count) * cyc / (mhz * 1e3)
     return {"cycles_per_warp_step": cyc, "bound_ms": bound_ms, "frac": bound_ms / ms,
+            "instr_source": ncu.get("workload"),
             "note": "2 issue cycles per FP64 warp-instruction + 1 per other, all warp-steps "
                     "balanced over 592 SMSPs (at 1000 scenarios the 1000 warps cannot "
                     "balance below 2 per loaded SMSP: that bound is 1.16x this one)"}

@@ -28,11 +28,21 @@ hdr, vals = raw[0], raw[2]
 m = dict(zip(hdr, vals))
 
 
+units = dict(zip(hdr, raw[1]))
+_TIME = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,
+         "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6}
+
+
 def num(key):
     try:
         return float(m[key].replace(",", ""))
     except (KeyError, ValueError):
         return None
+
+
+def usecs(key):
+    v = num(key)
+    return None if v is None else v * _TIME.get(units.get(key, "usecond"), 1.0)
 
 
 src = page("--page", "source", "--print-source", "sass")
@@ -62,7 +72,7 @@ summary = {
     "kernel": src[0][1] if len(src[0]) > 1 else "",
     "workload": workload,
     "source": rep.split("/")[-1] + " (ncu --set full --clock-control none --import-source on)",
-    "duration_us": num("gpu__time_duration.sum"),
+    "duration_us": usecs("gpu__time_duration.sum"),
     "dram_bytes_per_launch": None,
     "warp_instructions": total,
     "fp64_warp_instructions": fp64,
