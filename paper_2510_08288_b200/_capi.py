@@ -279,6 +279,20 @@ class Context:
                                     _p(pbits), ctypes.byref(res), flags))
         return res, viol, pbits
 
+    def grid_step_to_device(self, prob: Problem, x0, v_prev, r, m_grid, prefix_mode, n_sim,
+                            scen: Scenarios, viol_dev: int, abandon: bool = True) -> None:
+        """Enqueue a grid step on the library's stream; the per-row violation
+        counts (uint32, 0xffffffff = gated out) land at the device address
+        `viol_dev`.  No host synchronisation (RG_ASYNC | RG_DEVICE_PTRS)."""
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        res = GridResult()
+        check(self.lib.rg_grid_step(self.handle, ctypes.byref(prob), _p(x0), float(v_prev),
+                                    float(r), int(m_grid), int(bool(prefix_mode)), None,
+                                    int(n_sim), 0, ctypes.byref(scen), ctypes.c_void_p(viol_dev),
+                                    None, ctypes.byref(res),
+                                    RG_ASYNC | RG_DEVICE_PTRS | RG_NO_TIMING
+                                    | (RG_ABANDON if abandon else 0)))
+
     def bisect(self, prob: Problem, x0, v_prev, r, n_kappa, dist, n_sim,
                scen: Scenarios | None, per_scenario: bool = False, paths: bool = False,
                rng_mode: str | None = None, lpc: int | None = None):

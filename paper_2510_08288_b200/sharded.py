@@ -73,6 +73,39 @@ def extract_row(counts: np.ndarray, dup_src: np.ndarray, prefix_mode: bool) -> i
     return None if idx < 0 else idx
 
 
+_DEV_COUNTS: dict = {}
+
+
+def _device_row(ctx, dist, group, prob, x_t, v_prev, r_t, config, n_sim, stream):
+    """The grid step with its exchange on the device: the kernel writes this shard's
+    per-row counts (int32 view; a gated-out row is -1 on every rank) into a device
+    buffer, one NCCL all-reduce (MAX) runs on the library's stream after it, and only
+    the M reduced counts come back to the host.  The global MAX is 0 exactly for the
+    rows feasible on every shard; duplicate rows already carry their source's count
+    (the kernel's finalize), so the extraction needs no dedup map."""
+    import torch
+
+    key = (ctx.device, config.m_grid)
+    viol = _DEV_COUNTS.get(key)
+    if viol is None:
+        viol = _DEV_COUNTS[key] = torch.empty(config.m_grid, dtype=torch.int32,
+                                              device=f"cuda:{ctx.device}")
+    ctx.grid_step_to_device(prob, x_t, v_prev, r_t, config.m_grid, config.prefix_mode, n_sim,
+                            stream, viol.data_ptr())
+    with torch.cuda.stream(torch.cuda.ExternalStream(ctx.stream_ptr,
+                                                     device=f"cuda:{ctx.device}")):
+        dist.all_reduce(viol, op=dist.ReduceOp.MAX, group=group)
+        counts = viol.cpu().numpy()
+    full = counts == 0
+    if config.prefix_mode:
+        bad = np.flatnonzero(~full)
+        idx = (int(bad[0]) if bad.size else full.size) - 1
+    else:
+        ok = np.flatnonzero(full)
+        idx = int(ok[-1]) if ok.size else -1
+    return None if idx < 0 else idx
+
+
 def robust_rg_parallel_sharded(plant, x_t, state, r_t, cset, scenarios, config, group=None,
                                local_step=None):
     """robust_rg_parallel over the ranks of `group`; every rank returns the same result.
@@ -96,14 +129,18 @@ def robust_rg_parallel_sharded(plant, x_t, state, r_t, cset, scenarios, config, 
     if local_step is None:
         ctx = _capi.context(getattr(config, "device", 0))
         dist_t, n_sim, stream = _source(shard, config.j_star)
-        res, viol, _ = ctx.grid_step(prob, x_t, state.v_prev, r_t, config.m_grid,
-                                     config.prefix_mode, dist_t, n_sim, stream, False,
-                                     abandon=True)
-        dev = f"cuda:{ctx.device}" if dist.get_backend(group) == "nccl" else None
+        if dist_t is None and dist.get_backend(group) == "nccl":
+            row = _device_row(ctx, dist, group, prob, x_t, state.v_prev, r_t, config, n_sim,
+                              stream)
+        else:
+            res, viol, _ = ctx.grid_step(prob, x_t, state.v_prev, r_t, config.m_grid,
+                                         config.prefix_mode, dist_t, n_sim, stream, False,
+                                         abandon=True)
+            dev = f"cuda:{ctx.device}" if dist.get_backend(group) == "nccl" else None
+            row = extract_row(global_row_counts(viol, group, dev), dup_src, config.prefix_mode)
     else:
-        viol, dev = np.asarray(local_step(shard), dtype=np.uint32), None
-    counts = global_row_counts(viol, group, dev)
-    row = extract_row(counts, dup_src, config.prefix_mode)
+        viol = np.asarray(local_step(shard), dtype=np.uint32)
+        row = extract_row(global_row_counts(viol, group, None), dup_src, config.prefix_mode)
     diag = {"method": "parallel-grid-sharded", "ranks": world, "backend": "cuda",
             "sims_run": len(rows) * scenarios.n_sim,
             "ss_pruned_rows": int(np.count_nonzero(~ss_ok)),

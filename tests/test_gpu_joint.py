@@ -116,3 +116,41 @@ def test_joint_sharded_world1_nccl():
                                                               b.v_applied)
     finally:
         dist.destroy_process_group()
+
+
+def test_grid_and_alg2_sharded_world1_nccl():
+    """robust_rg_parallel_sharded (device counts, NCCL MAX on the library stream)
+    and robust_rg_sequential_sharded with one NCCL rank equal the single-device
+    steps: transient inputs, literal and prefix extraction, a grid with gated-out
+    and duplicate rows."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_08288_b200.sharded import (robust_rg_parallel_sharded,
+                                               robust_rg_sequential_sharded)
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29534")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        m = rg.DisturbanceModel.scaled(0.02, 3)
+        box = rg.ConstraintSet(-0.9, 0.9)
+        cases = [(0.4, 2.2, False, 32), (0.4, 2.2, True, 32), (1.2, -2.5, False, 32),
+                 (0.9, 0.9, False, 16), (0.0, 2.5, True, 9)]
+        for i, (vp, r, prefix, M) in enumerate(cases):
+            cfg = rg.GovernorConfig(j_star=128, n_sim=3000, m_grid=M, prefix_mode=prefix)
+            scen = rg.sample_scenarios(m, 3000, 129, seed=70 + i)
+            x0 = np.array([np.tanh(vp), vp, np.tanh(vp) / 2]) + 0.02
+            a = rg.robust_rg_parallel(PLANT, x0, rg.GovernorState(vp), r, box, scen, cfg)
+            b = robust_rg_parallel_sharded(PLANT, x0, rg.GovernorState(vp), r, box, scen, cfg)
+            assert (a.kappa_opt, a.feasible, a.v_applied) == (b.kappa_opt, b.feasible,
+                                                              b.v_applied), (i, a, b)
+            c = rg.robust_rg_sequential(PLANT, x0, rg.GovernorState(vp), r, box, scen, cfg)
+            d = robust_rg_sequential_sharded(PLANT, x0, rg.GovernorState(vp), r, box, scen,
+                                             cfg)
+            assert (c.kappa_opt, c.feasible, c.v_applied) == (d.kappa_opt, d.feasible,
+                                                              d.v_applied), (i, c, d)
+    finally:
+        dist.destroy_process_group()
