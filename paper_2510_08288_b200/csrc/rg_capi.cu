@@ -732,6 +732,7 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
     const int lpc = lpc_for(ctx, (int64_t)m_grid * n_sim, flags);
     a.tpb = tpb_for(ctx, n_sim * lpc, m_grid);
     if (kernel == 0 && lpc == 1) grid_placement(ctx, n_sim, m_grid, &a.tpb, &a.smem_dyn);
+    a.no_s2 = getenv("RG_NO_STEP2") ? 1 : 0;
     if (pbits && lpc > 1)  // lanes OR their bits in
         RG_CUDA(cudaMemsetAsync(a.pbits, 0, pbytes, ctx->stream));
     const bool timed = !(flags & RG_NO_TIMING);

@@ -402,6 +402,268 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
     return status;
 }
 
+// ---- two RK4 steps per loop iteration (the single-wave grid step) ------------
+//
+// At one or two resident warps per SM sub-partition (the C2 step) the rollout is
+// latency-bound: rollout()'s iteration holds four tanh chains of ~30 dependent
+// FP64 operations each.  rollout2 runs two steps per iteration, pipelined one
+// step deeper: iteration j (j even) finishes x1/x3 of steps j and j+1 (tanh
+// values from iteration j-2), evaluates the eight tanh of steps j+2 and j+3 side
+// by side (arguments from iteration j-2) and runs the x2 chain of steps j+4 and
+// j+5.  Twice the independent work per basic block at the same chain length.
+// Every operation, operand and rounding is still sfc_step's.
+//
+// Sources: start() gives steps 0..3, next(j) steps j+4 and j+5 (clamped to J-1),
+// into registers.  The staged source is a per-lane ring of two slot pairs in
+// shared memory ([pair][slot][comp][lane], conflict-free): in iteration j one pair
+// is read (steps j+4, j+5) and the other, read in iteration j-2, receives the
+// cp.async copies of steps j+6, j+7; then the pairs swap roles.
+
+constexpr int kRing4Stride = 256;  // threads per block of the two-step rollout, at most
+
+struct Soa4Source {
+    const double* d;  // already offset by k
+    int64_t ld;
+    double* ring;     // &ring[0][0][0][threadIdx.x] of a [2][2][3][kRing4Stride] array
+    const double* nxt = nullptr;   // next step to issue (clamped walk)
+    const double* last = nullptr;  // step J-1
+    int64_t stride = 0;
+    uint32_t base = 0;  // shared-memory address of this lane's pair 0, slot 0, component 0
+    uint32_t rd = 0;    // byte offset of the pair read in this iteration (0 or kPair)
+    static constexpr uint32_t kComp = 8 * kRing4Stride, kSlot = 3 * kComp, kPair = 2 * kSlot;
+    __device__ __forceinline__ void init(int32_t J) {
+        stride = 3 * ld;
+        nxt = d;
+        last = d + (int64_t)(J - 1) * stride;
+        base = (uint32_t)__cvta_generic_to_shared(ring);
+        rd = 0;
+    }
+    __device__ __forceinline__ void issue_one(uint32_t sa) {
+        const double* p1 = nxt + ld;
+        const double* p2 = p1 + ld;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(nxt));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa + kComp), "l"(p1));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa + 2 * kComp), "l"(p2));
+        nxt = nxt == last ? nxt : nxt + stride;
+    }
+    // the next two steps (in order) into the slot pair at byte offset `pair`
+    __device__ __forceinline__ void issue_pair(uint32_t pair) {
+        const uint32_t sa = base + pair;
+        issue_one(sa);
+        issue_one(sa + kSlot);
+        asm volatile("cp.async.commit_group;");
+    }
+    __device__ __forceinline__ void wait() { asm volatile("cp.async.wait_group 0;"); }
+    __device__ __forceinline__ static double lds(uint32_t a) {
+        double v;
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+        return v;
+    }
+    __device__ __forceinline__ void read_slot(uint32_t a, double (&o)[3]) const {
+        o[0] = lds(a);
+        o[1] = lds(a + kComp);
+        o[2] = lds(a + 2 * kComp);
+    }
+    // prologue: steps 0, 1 read; steps 2, 3 in flight into pair 1 (read by next(-2))
+    __device__ __forceinline__ void start(double (&dd)[2][3]) {
+        issue_pair(0);
+        issue_pair(kPair);
+        asm volatile("cp.async.wait_group 1;");
+        read_slot(base, dd[0]);
+        read_slot(base + kSlot, dd[1]);
+        rd = kPair;
+    }
+    // iteration j: steps j+4, j+5 (landed in pair rd) read, steps j+6, j+7 issued into
+    // the other pair (read, into registers, in iteration j-2); the pairs swap roles
+    __device__ __forceinline__ void next(int32_t, double (&e4)[3], double (&e5)[3]) {
+        wait();
+        const uint32_t a = base + rd;
+        read_slot(a, e4);
+        read_slot(a + kSlot, e5);
+        rd = kPair - rd;
+        issue_pair(rd);
+    }
+    __device__ __forceinline__ void finish() { wait(); }
+};
+
+struct Rng4Source {  // fused counter RNG (micro-benchmarks)
+    ScenarioStream st;
+    uint64_t K;
+    int32_t J = 0;
+    __device__ __forceinline__ void init(int32_t j_star) { J = j_star; }
+    __device__ __forceinline__ void at(int32_t s, double (&o)[3]) const {
+        disturbance_at(st, K, (uint64_t)(s < J ? s : J - 1), o[0], o[1], o[2]);
+    }
+    __device__ __forceinline__ void start(double (&d)[2][3]) {
+        at(0, d[0]);
+        at(1, d[1]);
+    }
+    __device__ __forceinline__ void next(int32_t j, double (&e4)[3], double (&e5)[3]) {
+        at(j + 4, e4);
+        at(j + 5, e5);
+    }
+    __device__ __forceinline__ void finish() {}
+};
+
+struct Zero4Source {  // nominal prediction / micro-benchmarks
+    __device__ __forceinline__ void init(int32_t) {}
+    __device__ __forceinline__ void start(double (&d)[2][3]) {
+        for (int s = 0; s < 2; ++s) d[s][0] = d[s][1] = d[s][2] = 0.0;
+    }
+    __device__ __forceinline__ void next(int32_t, double (&e4)[3], double (&e5)[3]) {
+        e4[0] = e4[1] = e4[2] = e5[0] = e5[1] = e5[2] = 0.0;
+    }
+    __device__ __forceinline__ void finish() {}
+};
+
+template <bool FMA, bool POLL, class Src>
+struct Rollout2 {
+    const CellConst& p;
+    const double v;
+    Src& src;
+    const unsigned int* dead;
+    int32_t J;
+    double x1, x3;
+    double y;         // x2 before step j+4
+    double x2n1;      // x2 after step j (the first tanh argument of step j+1)
+    double T[8];      // tanh values of steps j, j+1
+    double G[8];      // tanh arguments of steps j+2, j+3
+    double D[4];      // d0, d2 of steps j, j+1
+    double Dn[4];     // d0, d2 of steps j+2, j+3
+    int status = kOk;
+    int32_t steps = 0;
+    bool done = false;
+
+    __device__ __forceinline__ Rollout2(const CellConst& p_, double v_, Src& src_,
+                                        const unsigned int* dead_)
+        : p(p_), v(v_), src(src_), dead(dead_), J(p_.j_star) {}
+
+    // iteration j (even): true once every lane of the warp is done
+    __device__ __forceinline__ bool iter(int32_t j) {
+        double e4[3], e5[3];
+        src.next(j, e4, e5);
+        double Gn[8];
+        double yn, x1j, x3j;
+        auto side = [&]() {
+            const X2Stage s4 = x2_stage<FMA>(y, v, p);
+            const double y5 = add(add(y, mul(p.c, s4.s2)), e4[1]);
+            const X2Stage s5 = x2_stage<FMA>(y5, v, p);
+            yn = add(add(y5, mul(p.c, s5.s2)), e5[1]);
+            Gn[0] = y;
+            Gn[1] = s4.a2;
+            Gn[2] = s4.b2;
+            Gn[3] = s4.c2;
+            Gn[4] = y5;
+            Gn[5] = s5.a2;
+            Gn[6] = s5.b2;
+            Gn[7] = s5.c2;
+            double u1 = x1, u3 = x3;
+            x13_update<FMA>(u1, u3, T[0], T[1], T[2], T[3], p, D[0], D[1]);
+            x1j = u1;
+            x3j = u3;
+            x13_update<FMA>(u1, u3, T[4], T[5], T[6], T[7], p, D[2], D[3]);
+            // the pipeline-fill iteration (j = -2) has no steps j, j+1: its x1/x3
+            // update runs on unset tanh values and is dropped
+            x1 = j >= 0 ? u1 : x1;
+            x3 = j >= 0 ? u3 : x3;
+        };
+        double U[8];
+        tanhN_with<FMA, true, 8>(G, U, side);
+        {  // step j: overflow, then the output bound (x2 after step j is x2n1)
+            const bool ovf = !(fabs(x1j) <= kStateLimit && fabs(x2n1) <= kStateLimit &&
+                               fabs(x3j) <= kStateLimit);
+            const bool bnd = !in_bounds(x1j, p.ylo, p.yhi);
+            const bool now = !done && j >= 0 && (ovf || bnd);
+            status = now ? (ovf ? kOverflow : kViolated) : status;
+            steps = now ? j + 1 : steps;
+            done = done || now;
+        }
+        {  // step j+1 inside the horizon: overflow, bound, then the poll (x2 after it: G[0])
+            const bool ovf = !(fabs(x1) <= kStateLimit && fabs(G[0]) <= kStateLimit &&
+                               fabs(x3) <= kStateLimit);
+            const bool bnd = !in_bounds(x1, p.ylo, p.yhi);
+            bool aband = false;
+            if (POLL && ((j + 1) & 31) == 31) aband = *(volatile const unsigned int*)dead != 0u;
+            const bool now = !done && j >= 0 && j + 1 < J && (ovf || bnd || aband);
+            status = now ? (ovf ? kOverflow : (bnd ? kViolated : kAbandoned)) : status;
+            steps = now ? j + 2 : steps;
+            done = done || now;
+        }
+        if (__all_sync(0xffffffffu, done)) return true;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) T[q] = U[q];
+        x2n1 = G[4];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) G[q] = Gn[q];
+        y = yn;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) D[q] = Dn[q];
+        Dn[0] = e4[0];
+        Dn[1] = e4[2];
+        Dn[2] = e5[0];
+        Dn[3] = e5[2];
+        return false;
+    }
+
+    __device__ __forceinline__ int run(double x1_0, double x2_0, double x3_0, bool live,
+                                       int32_t& steps_out) {
+        x1 = x1_0;
+        x3 = x3_0;
+        steps = J;
+        done = !live;
+        if (live && !in_bounds(x1, p.ylo, p.yhi)) {
+            steps = 0;
+            status = kViolated;
+            done = true;
+        }
+        if (__all_sync(0xffffffffu, done)) {
+            steps_out = steps;
+            return status;
+        }
+        // prologue: the x2 chain of steps 0 and 1 (the tanh arguments G); the loop
+        // starts with a pipeline-fill iteration j = -2 that evaluates their tanh and
+        // the x2 chain of steps 2, 3 (so the tanh block has one copy in the code)
+        src.init(J);
+        double d[2][3];
+        src.start(d);
+        double yy = x2_0;
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const X2Stage st = x2_stage<FMA>(yy, v, p);
+            G[4 * s] = yy;
+            G[4 * s + 1] = st.a2;
+            G[4 * s + 2] = st.b2;
+            G[4 * s + 3] = st.c2;
+            yy = add(add(yy, mul(p.c, st.s2)), d[s][1]);
+        }
+        y = yy;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) T[q] = 0.0;
+        x2n1 = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) D[q] = 0.0;
+        Dn[0] = d[0][0];
+        Dn[1] = d[0][2];
+        Dn[2] = d[1][0];
+        Dn[3] = d[1][2];
+        for (int32_t j = -2; j < J; j += 2)
+            if (iter(j)) break;
+        src.finish();  // no copy may land after we leave
+        steps_out = steps;
+        return status;
+    }
+};
+
+// One cell, warp-uniform (all 32 lanes call, like rollout<..., WARP>), two steps per
+// iteration; same status / steps semantics as rollout.
+template <bool FMA, bool POLL, class Src>
+__device__ __forceinline__ int rollout2(const CellConst& p, double x1, double x2, double x3,
+                                        double v, Src& src, int32_t& steps,
+                                        const unsigned int* dead, bool live) {
+    Rollout2<FMA, POLL, Src> r(p, v, src, dead);
+    return r.run(x1, x2, x3, live, steps);
+}
+
 // ---- linear plant: kernels.py:90-118 (_cell_lin) ----------------------------
 //
 // x+ = A x + B v + d, y = C x + D v with n <= 4 states; numba evaluates

@@ -369,7 +369,9 @@ __device__ __forceinline__ void grid_finalize(const GridArgs& a) {
 
 // MOD: the tanh forms' operand-modifier variant (rg_math.cuh), for the
 // issue-bound multi-wave steps; the single-wave (latency-bound) step keeps MOD off.
-template <bool FMA, bool RNG, bool POLL, int LPC, bool MOD = false>
+// S2: the two-steps-per-iteration rollout (rollout2) for the latency-bound
+// single-wave step over a staged block (blocks of at most 256 threads).
+template <bool FMA, bool RNG, bool POLL, int LPC, bool MOD = false, bool S2 = false>
 __global__ void __launch_bounds__(256, RG_GRID_MINB) k_grid(GridArgs a) {
     __shared__ int s_src;
     __shared__ double s_v;
@@ -397,7 +399,16 @@ __global__ void __launch_bounds__(256, RG_GRID_MINB) k_grid(GridArgs a) {
         int st = kOk;
         int32_t steps = a.p.j_star;
         constexpr bool W = LPC == 1 && RG_GRID_WARP;  // whole warps run the rollout
-        if (live || LPC > 1 || W) {
+        if constexpr (S2) {
+            static_assert(!RNG && LPC == 1, "the two-step rollout reads a staged block");
+            __shared__ double ring4[4 * 3 * kRing4Stride];
+            Soa4Source src;
+            src.d = a.soa + kk;
+            src.ld = a.ld;
+            src.ring = ring4 + threadIdx.x;
+            st = rollout2<FMA, POLL>(make_cell(a.p), a.x0[0], a.x0[1], a.x0[2], s_v, src, steps,
+                                     a.viol + i, live);
+        } else if (live || LPC > 1 || W) {
             const CellConst c = make_cell(a.p);
             if (RNG) {
                 RngSource src{a.stream, scenario_key(a.stream, (uint64_t)(a.k0 + kk))};
@@ -1101,13 +1112,16 @@ cudaError_t launch_ex(Kern kern, dim3 grid, int block, size_t smem, cudaStream_t
     return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-// Opt a kernel in to `bytes` of dynamic shared memory (the single-wave placement's
-// occupancy pin), once per kernel and device.
-cudaError_t allow_dyn_smem(const void* fn, int bytes) {
-    if (bytes <= 0) return cudaSuccess;
+// The single-wave placement's occupancy pin: `total` bytes of shared memory per
+// block (more than half an SM's), of which the kernel's static shared memory is a
+// part.  Sets *dyn to the dynamic remainder and opts the kernel in to it, once per
+// kernel and device.  total <= 0: no pin (*dyn = 0).
+cudaError_t pin_smem(const void* fn, int total, int* dyn) {
+    *dyn = 0;
+    if (total <= 0) return cudaSuccess;
     struct Entry {
         const void* fn;
-        int dev, bytes;
+        int dev, total, dyn;
     };
     static Entry tab[256];
     static int n = 0;
@@ -1117,27 +1131,43 @@ cudaError_t allow_dyn_smem(const void* fn, int bytes) {
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lock(mu);
     for (int i = 0; i < n; ++i)
-        if (tab[i].fn == fn && tab[i].dev == dev && tab[i].bytes >= bytes) return cudaSuccess;
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    if (e == cudaSuccess && n < 256) tab[n++] = Entry{fn, dev, bytes};
-    return e;
+        if (tab[i].fn == fn && tab[i].dev == dev && tab[i].total == total) {
+            *dyn = tab[i].dyn;
+            return cudaSuccess;
+        }
+    cudaFuncAttributes attr;
+    if ((e = cudaFuncGetAttributes(&attr, fn)) != cudaSuccess) return e;
+    const int d = total > (int)attr.sharedSizeBytes ? total - (int)attr.sharedSizeBytes : 0;
+    if (d > 0 &&
+        (e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, d)) !=
+            cudaSuccess)
+        return e;
+    if (n < 256) tab[n++] = Entry{fn, dev, total, d};
+    *dyn = d;
+    return cudaSuccess;
 }
 
 cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, int lpc,
                         cudaStream_t s) {
     dim3 grid(blocks_for(a.n_sim * lpc, a.tpb), (unsigned)a.m_grid);
     cudaError_t e = cudaSuccess;
-#define RG_GRID_M(F, R, P, L, M)                                                         \
+#define RG_GRID_M(F, R, P, L, M, S)                                                      \
     do {                                                                                 \
-        if ((e = allow_dyn_smem((const void*)k_grid<F, R, P, L, M>, a.smem_dyn)) != cudaSuccess) \
+        int dyn = 0;                                                                     \
+        if ((e = pin_smem((const void*)k_grid<F, R, P, L, M, S>, a.smem_dyn, &dyn)) !=    \
+            cudaSuccess)                                                                 \
             break;                                                                       \
-        e = launch_ex(k_grid<F, R, P, L, M>, grid, a.tpb, (size_t)a.smem_dyn, s, a.pdl != 0, a); \
+        e = launch_ex(k_grid<F, R, P, L, M, S>, grid, a.tpb, (size_t)dyn, s, a.pdl != 0, \
+                      a);                                                                \
     } while (0)
-    // the operand-modifier tanh forms above one wave (issue-bound), one lane per cell
+    // one lane per cell: above one wave (issue-bound) the operand-modifier tanh forms,
+    // in one wave over a staged block (latency-bound) the two-step rollout
 #define RG_GRID(F, R, P, L)                                                              \
     do {                                                                                 \
-        if (L == 1 && a.smem_dyn == 0) RG_GRID_M(F, R, P, 1, true);                      \
-        else RG_GRID_M(F, R, P, L, false);                                               \
+        if (L == 1 && a.smem_dyn == 0) RG_GRID_M(F, R, P, 1, true, false);               \
+        else if (L == 1 && !R && a.tpb <= kRing4Stride && !a.no_s2)                      \
+            RG_GRID_M(F, false, P, 1, false, true);                                      \
+        else RG_GRID_M(F, R, P, L, false, false);                                        \
     } while (0)
 #define RG_GRID_L(L)                                                             \
     do {                                                                         \
@@ -1229,9 +1259,10 @@ cudaError_t launch_joint_roll(const JointArgs& a, int it, bool fma, int src, cud
     cudaError_t e = cudaSuccess;
 #define RG_J(F, S)                                                                      \
     do {                                                                                \
-        if ((e = allow_dyn_smem((const void*)k_joint_roll<F, S>, a.smem_dyn)) != cudaSuccess) \
+        int dyn = 0;                                                                    \
+        if ((e = pin_smem((const void*)k_joint_roll<F, S>, a.smem_dyn, &dyn)) != cudaSuccess) \
             return e;                                                                   \
-        k_joint_roll<F, S><<<blocks, a.tpb, (size_t)a.smem_dyn, s>>>(a, it);            \
+        k_joint_roll<F, S><<<blocks, a.tpb, (size_t)dyn, s>>>(a, it);                   \
     } while (0)
     if (fma) {
         if (src == 1) RG_J(true, 1); else if (src == 2) RG_J(true, 2); else RG_J(true, 0);
@@ -1252,9 +1283,10 @@ cudaError_t launch_bisect(const BisectArgs& a, bool fma, int src, int lpc, cudaS
     cudaError_t e = cudaSuccess;
 #define RG_BIS(F, S, L)                                                                 \
     do {                                                                                \
-        if ((e = allow_dyn_smem((const void*)k_bisect<F, S, L>, a.smem_dyn)) != cudaSuccess) \
+        int dyn = 0;                                                                    \
+        if ((e = pin_smem((const void*)k_bisect<F, S, L>, a.smem_dyn, &dyn)) != cudaSuccess) \
             return e;                                                                   \
-        k_bisect<F, S, L><<<g, a.tpb, (size_t)a.smem_dyn, s>>>(a);                      \
+        k_bisect<F, S, L><<<g, a.tpb, (size_t)dyn, s>>>(a);                             \
     } while (0)
 #define RG_BIS_L(L)                                                              \
     do {                                                                         \

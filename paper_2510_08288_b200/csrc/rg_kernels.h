@@ -78,9 +78,11 @@ struct GridArgs {
     int host_out;
     unsigned long long seq_token;
     int pdl;  // launched behind k_gen_soa with programmatic stream serialization
-    // dynamic shared memory of the launch: more than half an SM's pins one block per
-    // SM (the single-wave placement, see rg_capi.cu: grid_placement); 0 otherwise
+    // shared memory per block (static + dynamic) of the launch: more than half an
+    // SM's pins one block per SM (the single-wave placement, see rg_capi.cu:
+    // grid_placement); 0: no pin
     int smem_dyn;
+    int no_s2;  // single-wave step without the two-step rollout (A/B and tests)
 };
 
 // Batch of independent governor instances (episodes): one launch covers
@@ -169,7 +171,7 @@ struct BisectArgs {
     BisectAcc* acc;
     BisectOut* out;
     int tpb;
-    int smem_dyn;  // dynamic shared memory (single-wave placement pin), bytes
+    int smem_dyn;  // shared memory per block, static + dynamic (single-wave placement pin)
 };
 
 // Joint bisection: one candidate kappa for every
@@ -194,7 +196,7 @@ struct JointArgs {
     int64_t ld;
     JointState* st;
     int tpb;
-    int smem_dyn;  // dynamic shared memory (single-wave placement pin), bytes
+    int smem_dyn;  // shared memory per block, static + dynamic (single-wave placement pin)
     int fold;  // 1: the last block decides (single GPU); 0: k_joint_decide after the all-reduce
 };
 

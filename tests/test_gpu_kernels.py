@@ -331,12 +331,13 @@ def test_grid_fetch_after_sync_and_async_steps(ctx):
 
 
 @pytest.mark.parametrize("env", [{"RG_NO_PLACEMENT": "1"}, {"RG_FORCE_TPB": "32"},
-                                 {"RG_FORCE_TPB": "128"}])
+                                 {"RG_FORCE_TPB": "128"}, {"RG_NO_STEP2": "1"}])
 @pytest.mark.parametrize("shape", [(1000, 32), (300, 32), (4000, 32), (97, 5)])
 def test_single_wave_placement_changes_no_bit(ctx, monkeypatch, env, shape):
-    """The single-wave placement (blocks of 4L warps pinned one per SM) against the
-    other block shapes, on transient-binding inputs: same P bits, per-row counts,
-    result row and counters; and the same for the bisections."""
+    """The single-wave placement (blocks of 4L warps pinned one per SM, with the
+    two-step rollout over the staged block) against the other block shapes and the
+    one-step rollout (the multi-wave forms), on transient-binding inputs: same P
+    bits, per-row counts, result row and counters; and the same for the bisections."""
     n, M = shape
     rng = np.random.default_rng(n + M)
     vp = 0.4
