@@ -360,3 +360,37 @@ def test_single_wave_placement_changes_no_bit(ctx, monkeypatch, env, shape):
     assert ref[1] > 0 and 0 < int(np.count_nonzero(ref[4])) , "inputs must bind some rows"
     for a, b in zip(ref, got):
         assert np.array_equal(np.asarray(a), np.asarray(b))
+
+
+@pytest.mark.parametrize("j_star", [1, 2, 3, 31, 32, 33, 64, 257])
+@pytest.mark.parametrize("shape", [(1000, 32), (300, 8)])
+def test_two_step_rollout_edges(ctx, monkeypatch, shape, j_star):
+    """The single-wave two-step rollout (rollout2) at odd and short horizons, with
+    and without abandonment (the polled form), against the one-step rollout."""
+    n, M = shape
+    m = rg.DisturbanceModel.scaled(0.02, 3)
+    prob = _problem(-0.9, 0.9, 0.0, 0.05, j_star)
+    rng = np.random.default_rng(j_star * 7 + n)
+    cases = []
+    for trial in range(3):
+        vp = float(rng.uniform(-1, 1))
+        r = float(rng.uniform(-2.5, 2.5))
+        x0 = np.array([np.tanh(vp), vp, np.tanh(vp) / 2]) + rng.uniform(-0.05, 0.05, 3)
+        cases.append((vp, r, x0, _capi.make_scenarios(500 + trial, 0, n, m.lo, m.span)))
+
+    def run():
+        out = []
+        for vp, r, x0, sc in cases:
+            a = ctx.grid_step(prob, x0, vp, r, M, False, None, n, sc, True)
+            b = ctx.grid_step(prob, x0, vp, r, M, False, None, n, sc, False, abandon=True)
+            out.append((a[0].row, a[0].early_terms, a[0].overflows, a[0].sims_run, a[1].copy(),
+                        a[2].copy(), b[0].row, b[1] == 0))
+        return out
+
+    got = run()
+    monkeypatch.setenv("RG_NO_STEP2", "1")
+    ref = run()
+    for g, f in zip(got, ref):
+        for x, y in zip(g, f):
+            assert np.array_equal(np.asarray(x), np.asarray(y))
+        assert g[6] == g[0]  # abandonment changes no verdict
