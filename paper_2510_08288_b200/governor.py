@@ -22,6 +22,7 @@ every call raises BackendUnavailableError.
 from __future__ import annotations
 
 import functools
+import math
 import time
 from dataclasses import dataclass, field
 
@@ -104,7 +105,7 @@ class GovernorState:
     v_prev: float = 0.0
 
     def __post_init__(self):
-        if not np.isfinite(self.v_prev):
+        if not math.isfinite(self.v_prev):
             raise ConfigError(f"v_prev must be finite, got {self.v_prev}")
 
 
@@ -428,13 +429,11 @@ def robust_rg_parallel(plant, x_t, state, r_t, cset, scenarios, config, backend=
                 if src >= 0:
                     P[i] = P[src]
     row = None if res.row < 0 else res.row + 1
-    stats = dict(
-        backend="cuda", workers=1, device=ctx.device, sims_run=int(res.sims_run),
-        early_terms=int(res.early_terms), overflows=int(res.overflows),
-        ss_pruned_rows=int(res.ss_pruned_rows), dedup_rows=int(res.dedup_rows),
-        abandoned=int(res.abandoned), kernel_us=int(res.kernel_ms * 1e3),
-        wall_us=int((time.perf_counter() - t0) * 1e6), method="parallel-grid",
-    )
+    stats = {"backend": "cuda", "workers": 1, "device": ctx.device, "sims_run": res.sims_run,
+             "early_terms": res.early_terms, "overflows": res.overflows,
+             "ss_pruned_rows": res.ss_pruned_rows, "dedup_rows": res.dedup_rows,
+             "abandoned": res.abandoned, "kernel_us": int(res.kernel_ms * 1e3),
+             "wall_us": int((time.perf_counter() - t0) * 1e6), "method": "parallel-grid"}
     if row is None:
         if config.infeasible_policy == "error":
             raise InfeasibleError("no candidate feasible, including kappa=0 (hold current "
