@@ -92,14 +92,25 @@ def _range4(lo, span):
         b = span.tolist() + [0.0] * (4 - span.size)
         if len(_RANGE4) > 256:
             _RANGE4.clear()
+            _SCEN_TEMPLATE.clear()
         r = _RANGE4[key] = (d4(*a[:4]), d4(*b[:4]))
     return r
+
+
+_SCEN_TEMPLATE: dict = {}
 
 
 def make_scenarios(seed: int, k0: int, n_sim: int, lo, span) -> "Scenarios":
     """rg_scenarios for the counter-RNG stream ``seed`` (masked to 64 bits)."""
     lo4, span4 = _range4(lo, span)
-    return Scenarios(int(seed) & (2**64 - 1), int(k0), int(n_sim), lo4, span4)
+    t = _SCEN_TEMPLATE.get((id(lo4), id(span4)))
+    if t is None:  # one template per cached range pair; copying it is cheaper than a build
+        t = _SCEN_TEMPLATE[(id(lo4), id(span4))] = (Scenarios(0, 0, 0, lo4, span4), lo4, span4)
+    s = Scenarios.from_buffer_copy(t[0])
+    s.seed = int(seed) & (2**64 - 1)
+    s.k0 = int(k0)
+    s.n_sim = int(n_sim)
+    return s
 
 
 # name -> (restype, argtypes); the exact export list of include/refgov_b200.h

@@ -73,6 +73,13 @@ class DisturbanceModel:
         if self.kind not in ("uniform", "gaussian"):
             raise ConfigError(f"unknown disturbance kind {self.kind!r}")
         object.__setattr__(self, "ranges", rr)
+        # the model is immutable: lo and span are built once (read-only arrays)
+        lo = np.array([a for a, _ in rr], dtype=np.float64)
+        span = np.array([b - a for a, b in rr], dtype=np.float64)  # disturbance.py:193
+        lo.flags.writeable = False
+        span.flags.writeable = False
+        object.__setattr__(self, "_lo", lo)
+        object.__setattr__(self, "_span", span)
 
     @property
     def state_dim(self) -> int:
@@ -80,12 +87,12 @@ class DisturbanceModel:
 
     @property
     def lo(self) -> np.ndarray:
-        return np.array([a for a, _ in self.ranges], dtype=np.float64)
+        return self._lo
 
     @property
     def span(self) -> np.ndarray:
         # hi - lo rounded as the reference computes it (disturbance.py:193)
-        return np.array([b - a for a, b in self.ranges], dtype=np.float64)
+        return self._span
 
     @classmethod
     def scaled(cls, magnitude: float, state_dim: int) -> "DisturbanceModel":
