@@ -150,6 +150,21 @@ def cpu_baseline(n_sim: int, j_star: int, seconds: float, reps_max: int = 20):
     t0 = time.perf_counter()
     orc.grid_step(0.01, x0, 0.0, R_REF, M_GRID, d_ser, -0.9, 0.9, tlo, thi, j_star, workers=1)
     t_ser = time.perf_counter() - t0
+    # the same grid step on 8 workers (the survey's host), and the reference's other entry
+    # point on the same scenarios: robust_rg_sequential (Alg. 2, one core; at r = 0.5
+    # every scenario's kappa = 1 probe is feasible, one rollout per scenario)
+    t8 = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        orc.grid_step(0.01, x0, 0.0, R_REF, M_GRID, dist, -0.9, 0.9, tlo, thi, j_star,
+                      workers=min(8, cores))
+        t8.append(time.perf_counter() - t0)
+    import paper_2510_08288_b200 as rg
+    vlo, vhi = rg.admissible_setpoints(tlo, thi)
+    t0 = time.perf_counter()
+    kap = orc.bisect_all_c(0.01, x0, 0.0, R_REF, -0.9, 0.9, vlo, vhi, dist, j_star, 8)[0]
+    t_alg2 = time.perf_counter() - t0
+    assert np.all(kap == 1.0)
     best = min(times)
     return {
         "value": cells / best, "unit": UNIT, "cores": cores, "kind": "port",
@@ -158,6 +173,11 @@ def cpu_baseline(n_sim: int, j_star: int, seconds: float, reps_max: int = 20):
         "ms_per_step": best * 1e3, "ms_per_step_mean": statistics.mean(times) * 1e3,
         "serial_1core": {"value": ser_cells / t_ser, "unit": UNIT,
                          "sample": f"1 step at n_sim={min(n_sim, 250)}"},
+        "multicore_8_workers": {"value": cells / min(t8), "unit": UNIT,
+                                "ms_per_step": min(t8) * 1e3, "sample": "best of 3 full steps"},
+        "sequential_alg2_1core": {"ms_per_step": t_alg2 * 1e3, "n_sim": n_sim,
+                                  "sample": "robust_rg_sequential on the step's scenarios, "
+                                            "1 core (C scenario loop)"},
     }
 
 
@@ -476,6 +496,17 @@ def run_own(args, rank, world, local_rank):
         # the bisection searches on a transient step (r=2.5 from rest, kappa* = 0.5078):
         # exact Alg. 2 (per-scenario bisections, min) and the joint search (one kappa
         # for all scenarios per iteration, OR-reduced flag); both land on the same kappa
+        # Alg. 2 on the C2 step itself (r = 0.5: one feasible rollout per scenario), the
+        # device side of cpu_baseline.sequential_alg2_1core
+        sc = _capi.make_scenarios(BASE_SEED, k0, n_sim, model.lo, model.span)
+        ctx.bisect(prob, x0, 0.0, R_REF, 8, None, n_sim, sc)
+        t0 = time.perf_counter()
+        for _ in range(20):
+            res_b = ctx.bisect(prob, x0, 0.0, R_REF, 8, None, n_sim, sc)[0]
+        sweep.append({"workload": f"bisection (alg2), C2 snapshot r=0.5, n_sim={n_sim}",
+                      "ms_per_step": (time.perf_counter() - t0) / 20 * 1e3,
+                      "kappa": float(res_b.kappa), "rollouts": int(res_b.cells),
+                      "timing": "wall clock around the synchronous C-ABI call"})
         for n_b in (10_000, 1 << 20):
             sc = _capi.make_scenarios(BASE_SEED + 9000, 0, n_b, model.lo, model.span)
             for name, call in (
@@ -496,7 +527,8 @@ def run_own(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         c = cpu_baseline(n_sim, j_star, args.cpu_seconds)
         cb = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
-        cb["serial_1core"] = c["serial_1core"]
+        for k in ("serial_1core", "multicore_8_workers", "sequential_alg2_1core"):
+            cb[k] = c[k]
 
     if rank == 0:
         line = {
