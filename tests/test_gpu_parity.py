@@ -229,6 +229,23 @@ def test_closed_loop_c3_truncated(golden):
     assert np.array_equal(got, golden["c3_trace40"])
 
 
+def test_closed_loop_c3_10k_prefix():
+    """C3 at its named size: 10,000 scenarios per step, the first 440 steps of the
+    desk trace (rise to r = 0.4, then the r = 2.5 step at t = 400), equal to the
+    real reference's trace (tests/golden/make_c3_golden.py)."""
+    from paper_2510_08288_b200.harness import ReferenceProfile, run_closed_loop
+
+    with np.load(GOLDEN.with_name("c3_10k_trace.npz")) as z:
+        want, steps, n_sim, seed = z["trace"], int(z["steps"]), int(z["n_sim"]), int(z["seed"])
+    prof = ReferenceProfile(((0, 0.4), (400, 2.5), (1000, -2.5), (1600, 0.2)))
+    rec = run_closed_loop(PLANT, rg.ConstraintSet(-0.9, 0.9),
+                          rg.DisturbanceModel.scaled(0.001, 3),
+                          rg.GovernorConfig(n_sim=n_sim), prof, steps, seed)
+    assert not rec.aborted
+    got = np.array([[row[2], row[3], row[4], float(row[5])] for row in rec.rows])
+    assert np.array_equal(got, want)
+
+
 # ----------------------------------------------------------------- edges & errors
 
 def test_errors_map_to_reference_types():

@@ -147,6 +147,20 @@ def test_closed_loop_desk_grid_trace(orc, golden):
     assert np.array_equal(got, golden["desk_grid_trace"])
 
 
+def test_closed_loop_c3_10k_prefix(orc, golden):
+    """The oracle reproduces the first steps of the reference's 10k-scenario C3 trace
+    (tests/golden/make_c3_golden.py); the device runs all of it (test_gpu_parity)."""
+    with np.load(GOLDEN.with_name("c3_10k_trace.npz")) as z:
+        want, n_sim, seed = z["trace"], int(z["n_sim"]), int(z["seed"])
+    steps = 6
+    sched = golden["desk_profile"][:steps]
+    rows, aborted = orc.closed_loop(0.01, -0.9, 0.9, 0.0, 0.05, [(-0.001, 0.001)] * 3, sched,
+                                    steps, seed, "grid", n_sim=n_sim, workers=orc.cpu_count())
+    assert not aborted
+    got = np.array([[r[2], r[3], r[4], float(r[5])] for r in rows])
+    assert np.array_equal(got, want[:steps])
+
+
 with np.load(GOLDEN) as _z:
     N_LIN = len(_z["lin_names"])
 
