@@ -422,8 +422,9 @@ def robust_rg_parallel(plant, x_t, state, r_t, cset, scenarios, config, backend=
     P = None
     if keep:
         # pruned and duplicate rows come back as zero bits; duplicates copy their source
-        P = np.unpackbits(pbits.view(np.uint8), axis=1, bitorder="little")[:, :n_sim]
-        P = P.view(np.bool_)
+        # one flat unpack (row-major, little-endian words) is cheaper than axis=1
+        P = np.unpackbits(pbits.view(np.uint8).ravel(), bitorder="little")
+        P = P.reshape(pbits.shape[0], -1)[:, :n_sim].view(np.bool_)
         if n_dup:
             for i, src in enumerate(dup_src):
                 if src >= 0:
