@@ -246,6 +246,27 @@ def test_closed_loop_c3_10k_prefix():
     assert np.array_equal(got, want)
 
 
+def test_closed_loop_c5_batch_10k():
+    """C5's batched path at 10k scenarios per episode: episode seeds base + e, one
+    rg_grid_step_batch launch per step.  Episode 0 (seed 2024) equals the real
+    reference's C3 trace; the others equal their single-episode loops."""
+    from paper_2510_08288_b200.harness import (ReferenceProfile, run_closed_loop,
+                                               run_closed_loop_batch)
+
+    with np.load(GOLDEN.with_name("c3_10k_trace.npz")) as z:
+        want, steps, n_sim, seed = z["trace"], int(z["steps"]), int(z["n_sim"]), int(z["seed"])
+    prof = ReferenceProfile(((0, 0.4), (400, 2.5), (1000, -2.5), (1600, 0.2)))
+    box, model = rg.ConstraintSet(-0.9, 0.9), rg.DisturbanceModel.scaled(0.001, 3)
+    cfg = rg.GovernorConfig(n_sim=n_sim)
+    seeds = [seed + e for e in range(4)]
+    recs = run_closed_loop_batch(PLANT, box, model, cfg, prof, steps, seeds)
+    got = np.array([[row[2], row[3], row[4], float(row[5])] for row in recs[0].rows])
+    assert np.array_equal(got, want)
+    for e in (1, 3):
+        single = run_closed_loop(PLANT, box, model, cfg, prof, steps, seeds[e])
+        assert [row[:6] for row in recs[e].rows] == [row[:6] for row in single.rows]
+
+
 # ----------------------------------------------------------------- edges & errors
 
 def test_errors_map_to_reference_types():
