@@ -319,3 +319,24 @@ def test_repeated_steps_reset_device_accumulators():
                                         scen, cfg)
             outs.append((r, res.kappa_opt, res.diagnostics["early_terms"]))
     assert outs[0:2] == outs[2:4] == outs[4:6]
+
+
+def test_c4_million_scenario_step_matches_reference():
+    """C4 at its full per-step size: the robust grid step over 2^20 scenarios, j* = 256,
+    through the public API.  The 32 x 2^20 matrix P (packed-bit sha256 and per-row
+    counts) and (kappa, v, feasible) equal the real reference's
+    (tests/golden/make_c4_golden.py, multicore fill on the build container)."""
+    with np.load(GOLDEN.with_name("c4_1m_step.npz")) as z:
+        g = {k: z[k] for k in z.files}
+    n, j_star, m = int(g["n_sim"]), int(g["j_star"]), int(g["m_grid"])
+    v_prev, r = float(g["v_prev"]), float(g["r"])
+    scen = rg.sample_scenarios(rg.DisturbanceModel.scaled(float(g["range"]), 3), n, j_star + 1,
+                               seed=int(g["seed"]))
+    state = rg.GovernorState(v_prev)
+    res = rg.robust_rg_parallel(PLANT, g["x0"], state, r, rg.ConstraintSet(-0.9, 0.9, 0.0), scen,
+                                rg.GovernorConfig(j_star=j_star, m_grid=m, n_sim=n))
+    P = res.matrix
+    assert P.shape == (m, n)
+    assert np.array_equal(P.sum(axis=1), g["row_counts"])
+    assert hashlib.sha256(np.packbits(P, axis=1).tobytes()).digest() == g["p_sha"].tobytes()
+    assert (res.kappa_opt, res.v_applied, float(res.feasible)) == tuple(g["result"])
