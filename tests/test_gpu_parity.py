@@ -340,3 +340,25 @@ def test_c4_million_scenario_step_matches_reference():
     assert np.array_equal(P.sum(axis=1), g["row_counts"])
     assert hashlib.sha256(np.packbits(P, axis=1).tobytes()).digest() == g["p_sha"].tobytes()
     assert (res.kappa_opt, res.v_applied, float(res.feasible)) == tuple(g["result"])
+
+
+def test_c4_million_scenario_alg2_matches_reference():
+    """Alg. 2 (robust_rg_sequential) over the same 2^20 scenarios: kappa, v, feasible
+    and the rollout/early-termination counters equal the real reference's
+    (tests/golden/make_c4_seq_golden.py); the joint search lands on the same kappa."""
+    with np.load(GOLDEN.with_name("c4_1m_step.npz")) as z:
+        g = {k: z[k] for k in z.files}
+    with np.load(GOLDEN.with_name("c4_1m_seq.npz")) as z:
+        want = tuple(float(v) for v in z["result"])
+    n, j_star = int(g["n_sim"]), int(g["j_star"])
+    v_prev, r = float(g["v_prev"]), float(g["r"])
+    scen = rg.sample_scenarios(rg.DisturbanceModel.scaled(float(g["range"]), 3), n, j_star + 1,
+                               seed=int(g["seed"]))
+    box = rg.ConstraintSet(-0.9, 0.9, 0.0)
+    cfg = rg.GovernorConfig(j_star=j_star, n_sim=n, n_kappa=8)
+    res = rg.robust_rg_sequential(PLANT, g["x0"], rg.GovernorState(v_prev), r, box, scen, cfg)
+    d = res.diagnostics
+    assert (res.kappa_opt, res.v_applied, float(res.feasible), d["sims_run"],
+            d["early_terms"]) == want
+    jt = rg.robust_rg_joint(PLANT, g["x0"], rg.GovernorState(v_prev), r, box, scen, cfg)
+    assert (jt.kappa_opt, jt.feasible) == (res.kappa_opt, res.feasible)
