@@ -67,14 +67,7 @@ extern "C" {
  * grid step (all candidate rows share it), at most 96 MB for the bisections
  * (whose rollouts often stop after a few steps), and fused above.  The batched
  * grid step stages each episode's block, in chunks of episodes of at most 16 GB,
- * unless RG_FUSED_RNG (or a lanes-per-cell split) is given. */
-#define RG_LPC1 0x80        /* force 1 lane per (row, scenario) cell */
-#define RG_LPC2 0x100       /* force 2 lanes per cell (each evaluates 2 of the 4 tanh) */
-#define RG_LPC4 0x200       /* force 4 lanes per cell (1 tanh each) */
-/* Default: 1 lane per cell (fastest measured).  Results are identical for every choice. */
-#define RG_DECOUPLED 0x400  /* grid step: phase-decoupled kernel (x2 chain / tanh / x1-x3) */
-#define RG_PER_STEP 0x800   /* grid step: per-step rollout kernel */
-#define RG_WARP_SPEC 0x1000 /* grid step: warp-specialised kernel (sequence warp + tanh warps) */
+ * unless RG_FUSED_RNG is given. */
 
 typedef struct rg_ctx rg_ctx;
 
@@ -153,6 +146,12 @@ RG_API int32_t rg_device_count(int32_t *n);
 RG_API int32_t rg_create(int32_t device, int32_t tanh_variant, rg_ctx **out);
 RG_API int32_t rg_destroy(rg_ctx *ctx);
 RG_API int32_t rg_get_tanh_variant(rg_ctx *ctx, int32_t *variant);
+/* Per-context tuning knobs (none changes a result bit): "force_tpb" (0/32/64/128),
+ * "no_placement", "no_pdl", "no_step2" (0/1), "batch_chunk" (episodes per staged
+ * chunk, 0 = automatic).  Defaults come from the RG_FORCE_TPB, RG_NO_PLACEMENT,
+ * RG_NO_PDL, RG_NO_STEP2 and RG_BATCH_CHUNK environment variables, read once at
+ * rg_create.  Unknown names give RG_E_ARGS. */
+RG_API int32_t rg_set_option(rg_ctx *ctx, const char *name, int64_t value);
 /* The cudaStream_t the context launches on, as an opaque pointer. */
 RG_API int32_t rg_get_stream(rg_ctx *ctx, void **stream);
 RG_API int32_t rg_synchronize(rg_ctx *ctx);

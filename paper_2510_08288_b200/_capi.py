@@ -25,11 +25,6 @@ RG_TANH_AUTO, RG_TANH_FMA, RG_TANH_GENERIC = 0, 1, 2
 RG_DEVICE_PTRS, RG_ASYNC, RG_ABANDON, RG_NO_TIMING = 0x1, 0x2, 0x4, 0x8
 RG_TANH_LOCKSTEP, RG_FUSED_RNG, RG_STAGE_RNG = 0x10, 0x20, 0x40
 _RNG_FLAGS = {None: 0, "fused": RG_FUSED_RNG, "staged": RG_STAGE_RNG}
-RG_LPC1, RG_LPC2, RG_LPC4 = 0x80, 0x100, 0x200
-_LPC_FLAGS = {None: 0, 1: RG_LPC1, 2: RG_LPC2, 4: RG_LPC4}
-RG_DECOUPLED, RG_PER_STEP, RG_WARP_SPEC = 0x400, 0x800, 0x1000
-_KERNEL_FLAGS = {None: 0, "decoupled": RG_DECOUPLED, "per-step": RG_PER_STEP,
-                 "warp-spec": RG_WARP_SPEC}
 
 _i32, _i64, _u64, _d, _vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, \
     ctypes.c_void_p
@@ -121,6 +116,7 @@ SIGNATURES = {
     "rg_create": (_i32, [_i32, _i32, ctypes.POINTER(_vp)]),
     "rg_destroy": (_i32, [_vp]),
     "rg_get_tanh_variant": (_i32, [_vp, ctypes.POINTER(_i32)]),
+    "rg_set_option": (_i32, [_vp, ctypes.c_char_p, _i64]),
     "rg_get_stream": (_i32, [_vp, ctypes.POINTER(_vp)]),
     "rg_synchronize": (_i32, [_vp]),
     "rg_tanh": (_i32, [_vp, _vp, _vp, _i64, _i32]),
@@ -205,10 +201,32 @@ def device_count() -> int:
     return int(n.value) if rc == RG_OK else 0
 
 
+def _locked(fn):
+    """Hold the context's lock for the whole call: an rg_ctx serves one call at a
+    time (its scratch buffers, pinned result block and publication token are
+    shared), and ctypes releases the GIL while the C function runs."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(self, *args, **kwargs):
+        with self.lock:
+            return fn(self, *args, **kwargs)
+
+    return wrapper
+
+
 class Context:
-    """One CUDA context per device: stream, scratch buffers, result staging."""
+    """One CUDA context per device: stream, scratch buffers, result staging.
+
+    Thread-safe: every entry point holds ``lock`` (re-entrant), so concurrent
+    governor calls on one device -- the reference service runs /govern/step in a
+    thread pool -- are serialised instead of racing on the shared scratch.  A
+    caller issuing a sequence of calls that must not interleave (the sharded
+    joint search) holds ``lock`` around the sequence.
+    """
 
     def __init__(self, device: int = 0, tanh_variant: int = RG_TANH_AUTO):
+        self.lock = threading.RLock()
         self.lib = load_library()
         h = _vp()
         check(self.lib.rg_create(int(device), int(tanh_variant), ctypes.byref(h)))
@@ -235,10 +253,17 @@ class Context:
         check(self.lib.rg_get_stream(self.handle, ctypes.byref(s)))
         return int(s.value or 0)
 
+    @_locked
     def synchronize(self):
         check(self.lib.rg_synchronize(self.handle))
 
+    @_locked
+    def set_option(self, name: str, value: int) -> None:
+        """rg_set_option: a tuning knob of this context (no result bit depends on it)."""
+        check(self.lib.rg_set_option(self.handle, name.encode(), int(value)))
+
     # -- entry points ---------------------------------------------------
+    @_locked
     def tanh(self, x: np.ndarray, lockstep: bool = False) -> np.ndarray:
         x = np.ascontiguousarray(x, dtype=np.float64)
         y = np.empty_like(x)
@@ -246,6 +271,7 @@ class Context:
                                RG_TANH_LOCKSTEP if lockstep else 0))
         return y
 
+    @_locked
     def sample(self, seed: int, k0: int, n_sim: int, horizon: int, lo, span) -> np.ndarray:
         lo = np.ascontiguousarray(lo, dtype=np.float64)
         span = np.ascontiguousarray(span, dtype=np.float64)
@@ -254,9 +280,9 @@ class Context:
                                            lo.size, _p(lo), _p(span), _p(out), 0))
         return out
 
+    @_locked
     def fill(self, prob: Problem, x0, v_rows, rows, dist, n_sim, scen: Scenarios | None,
-             S: np.ndarray, steps: np.ndarray, rng_mode: str | None = None,
-             lpc: int | None = None) -> None:
+             S: np.ndarray, steps: np.ndarray, rng_mode: str | None = None) -> None:
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
         v_rows = np.ascontiguousarray(v_rows, dtype=np.float64)
         rows = np.ascontiguousarray(rows, dtype=np.int32)
@@ -267,12 +293,12 @@ class Context:
         check(self.lib.rg_fill(self.handle, ctypes.byref(prob), _p(x0), _p(v_rows), v_rows.size,
                                _p(rows), rows.size, _p(dist), int(n_sim), int(horizon),
                                ctypes.byref(scen) if scen is not None else None, _p(S),
-                               _p(steps), _RNG_FLAGS[rng_mode] | _LPC_FLAGS[lpc]))
+                               _p(steps), _RNG_FLAGS[rng_mode]))
 
+    @_locked
     def grid_step(self, prob: Problem, x0, v_prev, r, m_grid, prefix_mode, dist, n_sim,
                   scen: Scenarios | None, want_pbits: bool, abandon: bool = False,
-                  rng_mode: str | None = None, lpc: int | None = None,
-                  kernel: str | None = None, timing: bool = True, want_viol: bool = True):
+                  rng_mode: str | None = None, timing: bool = True, want_viol: bool = True):
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
         horizon = 0
         if dist is not None:
@@ -281,8 +307,8 @@ class Context:
         viol = np.empty(m_grid, dtype=np.uint32) if want_viol else None
         pbits = np.empty((m_grid, (n_sim + 31) // 32), dtype=np.uint32) if want_pbits else None
         res = GridResult()
-        flags = (RG_ABANDON if abandon else 0) | _RNG_FLAGS[rng_mode] | _LPC_FLAGS[lpc] | \
-            _KERNEL_FLAGS[kernel] | (0 if timing else RG_NO_TIMING)
+        flags = (RG_ABANDON if abandon else 0) | _RNG_FLAGS[rng_mode] | \
+            (0 if timing else RG_NO_TIMING)
         check(self.lib.rg_grid_step(self.handle, ctypes.byref(prob), _p(x0), float(v_prev),
                                     float(r), int(m_grid), int(bool(prefix_mode)), _p(dist),
                                     int(n_sim), int(horizon),
@@ -290,6 +316,7 @@ class Context:
                                     _p(pbits), ctypes.byref(res), flags))
         return res, viol, pbits
 
+    @_locked
     def grid_step_to_device(self, prob: Problem, x0, v_prev, r, m_grid, prefix_mode, n_sim,
                             scen: Scenarios, viol_dev: int, abandon: bool = True) -> None:
         """Enqueue a grid step on the library's stream; the per-row violation
@@ -304,9 +331,10 @@ class Context:
                                     RG_ASYNC | RG_DEVICE_PTRS | RG_NO_TIMING
                                     | (RG_ABANDON if abandon else 0)))
 
+    @_locked
     def bisect(self, prob: Problem, x0, v_prev, r, n_kappa, dist, n_sim,
                scen: Scenarios | None, per_scenario: bool = False, paths: bool = False,
-               rng_mode: str | None = None, lpc: int | None = None):
+               rng_mode: str | None = None):
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
         horizon = 0
         if dist is not None:
@@ -326,10 +354,11 @@ class Context:
                                  int(n_kappa), _p(dist), int(n_sim), int(horizon),
                                  ctypes.byref(scen) if scen is not None else None, _p(kap),
                                  _p(fnd), _p(cel), _p(erl), _p(pk), _p(po), ctypes.byref(res),
-                                 _RNG_FLAGS[rng_mode] | _LPC_FLAGS[lpc]))
+                                 _RNG_FLAGS[rng_mode]))
         per = (kap, fnd, cel, erl) if per_scenario else None
         return res, per, ((pk, po) if paths else None)
 
+    @_locked
     def bisect_joint(self, prob: Problem, x0, v_prev, r, n_kappa, dist, n_sim,
                      scen: Scenarios | None, rng_mode: str | None = None) -> "BisectResult":
         """Joint bisection on this device (rg_bisect_joint)."""
@@ -346,6 +375,7 @@ class Context:
                                        ctypes.byref(res), _RNG_FLAGS[rng_mode]))
         return res
 
+    @_locked
     def joint_begin(self, prob: Problem, x0, v_prev, r, n_kappa, dist, n_sim,
                     scen: Scenarios | None) -> None:
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
@@ -358,27 +388,31 @@ class Context:
                                       int(horizon),
                                       ctypes.byref(scen) if scen is not None else None, 0))
 
+    @_locked
     def joint_iter(self, it: int, fold: bool) -> None:
         check(self.lib.rg_joint_iter(self.handle, int(it), int(bool(fold))))
 
+    @_locked
     def joint_flag_ptr(self) -> int:
         p = _vp()
         check(self.lib.rg_joint_flag(self.handle, ctypes.byref(p)))
         return int(p.value)
 
+    @_locked
     def joint_decide(self, it: int) -> None:
         check(self.lib.rg_joint_decide(self.handle, int(it)))
 
+    @_locked
     def joint_end(self) -> "BisectResult":
         res = BisectResult()
         check(self.lib.rg_joint_end(self.handle, ctypes.byref(res)))
         return res
 
+    @_locked
     def grid_step_batch(self, prob: Problem, x0, v_prev, r, seeds, k0, n_sim, lo, span,
-                        m_grid, prefix_mode=False, abandon=True, want_viol=False, lpc=None,
-                        fused=False):
+                        m_grid, prefix_mode=False, abandon=True, want_viol=False, fused=False):
         """Batched robust grid step; returns (row, kappa, v, early[, viol]).  The
-        scenario blocks are staged per episode unless `fused` (or lpc > 1)."""
+        scenario blocks are staged per episode unless `fused`."""
         x0 = np.ascontiguousarray(x0, dtype=np.float64).reshape(-1, 3)
         E = x0.shape[0]
         v_prev = np.ascontiguousarray(v_prev, dtype=np.float64).reshape(E)
@@ -395,10 +429,11 @@ class Context:
                                           _p(r), _p(seeds), int(k0), int(n_sim), _p(lo),
                                           _p(span), int(m_grid), int(bool(prefix_mode)),
                                           _p(row), _p(kap), _p(v), _p(early), _p(viol),
-                                          (RG_ABANDON if abandon else 0) | _LPC_FLAGS[lpc]
+                                          (RG_ABANDON if abandon else 0)
                                           | (RG_FUSED_RNG if fused else 0)))
         return (row, kap, v, early, viol) if want_viol else (row, kap, v, early)
 
+    @_locked
     def fill_linear(self, lin: LinearPlant, prob: Problem, x0, v_rows, rows, dist, n_sim,
                     scen: Scenarios | None, S: np.ndarray, steps: np.ndarray) -> None:
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
@@ -414,6 +449,7 @@ class Context:
                                       ctypes.byref(scen) if scen is not None else None, _p(S),
                                       _p(steps), 0))
 
+    @_locked
     def bisect_linear(self, lin: LinearPlant, prob: Problem, x0, v_prev, r, n_kappa, dist,
                       n_sim, scen: Scenarios | None, per_scenario: bool = False):
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
@@ -436,6 +472,7 @@ class Context:
                                         0))
         return res, ((kap, fnd, cel, erl) if per_scenario else None)
 
+    @_locked
     def fp64_peak(self) -> float:
         f = _d()
         check(self.lib.rg_fp64_peak(self.handle, ctypes.byref(f)))

@@ -16,7 +16,7 @@ LIB = HERE / "_lib" / "librefgov_b200.so"
 
 
 def build(force: bool = False) -> Path:
-    cmd = ["make", "-s", "-C", str(CSRC)]
+    cmd = ["make", "-s", "-j8", "-C", str(CSRC)]
     if force:
         cmd.append("-B")
     subprocess.run(cmd, check=True)

@@ -120,8 +120,21 @@ int probe_host_tanh() {
 
 }  // namespace
 
+// Tuning knobs for experiments and tests.  Read from the environment once, at
+// rg_create (RG_FORCE_TPB, RG_NO_PLACEMENT, RG_NO_PDL, RG_NO_STEP2,
+// RG_BATCH_CHUNK), and settable per context with rg_set_option.  None changes a
+// result bit; the defaults are the measured-best configuration.
+struct Tuning {
+    int force_tpb = 0;        // 32 / 64 / 128: fixed block size, no single-wave placement
+    int no_placement = 0;     // single-wave placement off
+    int no_pdl = 0;           // grid step not launched with programmatic dependent launch
+    int no_step2 = 0;         // single-wave step with the one-step rollout
+    int64_t batch_chunk = 0;  // batched step: at most this many staged episodes per chunk
+};
+
 struct rg_ctx {
     int device = 0;
+    Tuning tune;
     int variant = rg::kTanhFma;
     int sm_count = 0;
     int smem_per_sm = 0;  // bytes of shared memory per SM
@@ -271,46 +284,25 @@ int32_t grow_grid(rg_ctx* ctx, int m) {
     return RG_OK;
 }
 
-constexpr int kGridKernelDefault = 0;
+// One lane per (row, scenario) cell everywhere.  Round 1 measured two alternatives
+// on the B200 and removed them: 2 or 4 lanes per cell sharing its four tanh (more
+// total FP64 work: 0.322 / 0.417 ms at C2 against 0.255 then), and phase-decoupled
+// or warp-specialised grid kernels (barrier and handoff overhead: 0.451 / 0.292 ms
+// at C2).  DESIGN.md §4 keeps the table.
 
-// Lanes per cell.  LPC = 2 / 4 spread a cell's four tanh chains over lanes
-// (rg_cell.cuh: step_tanh).  Measured on B200 (round 1) the redundant x1/x2/x3
-// work costs more than the extra parallelism buys at every size tried
-// (1k-10k scenarios: 0.255 / 0.322 / 0.417 ms at 1k for LPC 1 / 2 / 4), so the
-// default is one lane per cell; RG_LPC2 / RG_LPC4 remain for experiments and
-// are covered by the parity tests.
-int lpc_for(const rg_ctx* ctx, int64_t cells, int32_t flags) {
-    (void)ctx;
-    (void)cells;
-    if (flags & RG_LPC2) return 2;
-    if (flags & RG_LPC4) return 4;
-    if (const char* env = getenv("RG_FORCE_LPC")) {  // tuning experiments only
-        const int v = atoi(env);
-        if (v == 1 || v == 2 || v == 4) return v;
-    }
-    return 1;
-}
-
-// Grid-step kernel choice: 0 = per-step rollout (k_grid), 1 = block-phased
-// decoupled (k_grid_dec), 2 = warp-specialised (k_grid_ws).  RG_PER_STEP /
-// RG_DECOUPLED / RG_WARP_SPEC force one; RG_GRID_KERNEL=0/1/2 overrides the
-// default for tuning.
-int grid_kernel_for(int32_t flags) {
-    if (flags & (RG_LPC1 | RG_LPC2 | RG_LPC4 | RG_PER_STEP)) return 0;
-    if (flags & RG_WARP_SPEC) return 2;
-    if (flags & RG_DECOUPLED) return 1;
-    if (const char* env = getenv("RG_GRID_KERNEL")) {
-        const int k = atoi(env);
-        return k == 1 || k == 2 ? k : 0;
-    }
-    return kGridKernelDefault;
+Tuning env_tuning() {
+    Tuning t;
+    if (const char* e = getenv("RG_FORCE_TPB")) t.force_tpb = atoi(e);
+    if (getenv("RG_NO_PLACEMENT")) t.no_placement = 1;
+    if (getenv("RG_NO_PDL")) t.no_pdl = 1;
+    if (getenv("RG_NO_STEP2")) t.no_step2 = 1;
+    if (const char* e = getenv("RG_BATCH_CHUNK")) t.batch_chunk = atoll(e);
+    if (!(t.force_tpb == 32 || t.force_tpb == 64 || t.force_tpb == 128)) t.force_tpb = 0;
+    return t;
 }
 
 int tpb_for(const rg_ctx* ctx, int64_t n_sim, int64_t rows) {
-    if (const char* env = getenv("RG_FORCE_TPB")) {  // tuning override: 32, 64 or 128
-        const int t = atoi(env);
-        if (t == 32 || t == 64 || t == 128) return t;
-    }
+    if (ctx->tune.force_tpb) return ctx->tune.force_tpb;
     // Small problems: single-warp blocks spread the warps over more SMs; above
     // one wave, 64-thread blocks (measured equal or better than 128 at 10k-1M).
     const int64_t warps = (n_sim + 31) / 32 * std::max<int64_t>(rows, 1);
@@ -329,7 +321,7 @@ int tpb_for(const rg_ctx* ctx, int64_t n_sim, int64_t rows) {
 // only one block per SM: no SMSP ever holds more than L warps.
 void grid_placement(const rg_ctx* ctx, int64_t n_sim, int32_t rows, int* tpb, int* smem_dyn) {
     *smem_dyn = 0;
-    if (getenv("RG_FORCE_TPB") || getenv("RG_NO_PLACEMENT")) return;
+    if (ctx->tune.force_tpb || ctx->tune.no_placement) return;
     for (int L = 1; L <= 2; ++L) {
         const int t = 128 * L;
         const int64_t blocks = (n_sim + t - 1) / t * (int64_t)rows;
@@ -392,6 +384,7 @@ int32_t rg_create(int32_t device, int32_t tanh_variant, rg_ctx** out) {
     ctx->variant = variant;
     ctx->sm_count = prop.multiProcessorCount;
     ctx->smem_per_sm = (int)prop.sharedMemPerMultiprocessor;
+    ctx->tune = env_tuning();
     int32_t rc = enter(ctx);
     if (rc) { delete ctx; return rc; }
     if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -440,6 +433,28 @@ int32_t rg_destroy(rg_ctx* ctx) {
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
+    return RG_OK;
+}
+
+int32_t rg_set_option(rg_ctx* ctx, const char* name, int64_t value) {
+    if (!ctx || !name) return fail(RG_E_ARGS, "null argument");
+    Tuning& t = ctx->tune;
+    if (!strcmp(name, "force_tpb")) {
+        if (value != 0 && value != 32 && value != 64 && value != 128)
+            return fail(RG_E_ARGS, "force_tpb must be 0, 32, 64 or 128, got %lld", (long long)value);
+        t.force_tpb = (int)value;
+    } else if (!strcmp(name, "no_placement")) {
+        t.no_placement = value != 0;
+    } else if (!strcmp(name, "no_pdl")) {
+        t.no_pdl = value != 0;
+    } else if (!strcmp(name, "no_step2")) {
+        t.no_step2 = value != 0;
+    } else if (!strcmp(name, "batch_chunk")) {
+        if (value < 0) return fail(RG_E_ARGS, "batch_chunk must be >= 0");
+        t.batch_chunk = value;
+    } else {
+        return fail(RG_E_ARGS, "unknown option '%s'", name);
+    }
     return RG_OK;
 }
 
@@ -577,9 +592,7 @@ int32_t rg_fill(rg_ctx* ctx, const rg_problem* prob, const double* x0, const dou
         a.steps = ctx->steps.as<int32_t>();
     }
     RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-    const int lpc = lpc_for(ctx, (int64_t)n_rows * n_sim, flags);
-    a.tpb = tpb_for(ctx, n_sim * lpc, n_rows);
-    RG_CUDA(rg::launch_fill(a, ctx->variant == rg::kTanhFma, use_rng, lpc, ctx->stream));
+    RG_CUDA(rg::launch_fill(a, ctx->variant == rg::kTanhFma, use_rng, ctx->stream));
     RG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     if (!(flags & RG_DEVICE_PTRS)) {
         // copy back only the active rows: the caller's other rows stay untouched
@@ -684,13 +697,11 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
     a.m_grid = m_grid;
     a.prefix_mode = prefix_mode ? 1 : 0;
     a.n_sim = n_sim;
-    // the phase-decoupled kernel (rg_decoupled.cuh) unless a lanes-per-cell split is forced
-    const int kernel = grid_kernel_for(flags);
     bool use_rng = dist == nullptr;
     if (use_rng && want_stage(n_sim, prob->j_star, flags)) {
         if ((rc = stage_rng(ctx, rng, n_sim, prob->j_star, &a.soa, &a.ld))) return rc;
         use_rng = false;
-        a.pdl = getenv("RG_NO_PDL") ? 0 : 1;  // k_gen_soa is the kernel right before
+        a.pdl = ctx->tune.no_pdl ? 0 : 1;  // k_gen_soa is the kernel right before
     } else if (use_rng) {
         a.stream = make_stream(rng);
         a.k0 = rng->k0;
@@ -729,33 +740,22 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
         if (zero_copy && pbits_in_block)
             a.pbits_host = reinterpret_cast<unsigned*>(blk + kOutHead + viol_bytes(m_grid));
     }
-    const int lpc = lpc_for(ctx, (int64_t)m_grid * n_sim, flags);
-    a.tpb = tpb_for(ctx, n_sim * lpc, m_grid);
-    if (kernel == 0 && lpc == 1) grid_placement(ctx, n_sim, m_grid, &a.tpb, &a.smem_dyn);
-    a.no_s2 = getenv("RG_NO_STEP2") ? 1 : 0;
-    if (pbits && lpc > 1)  // lanes OR their bits in
-        RG_CUDA(cudaMemsetAsync(a.pbits, 0, pbytes, ctx->stream));
+    a.tpb = tpb_for(ctx, n_sim, m_grid);
+    grid_placement(ctx, n_sim, m_grid, &a.tpb, &a.smem_dyn);
+    a.no_s2 = ctx->tune.no_step2;
     const bool timed = !(flags & RG_NO_TIMING);
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-    if (kernel == 2) {
-        RG_CUDA(rg::launch_grid_ws(a, ctx->variant == rg::kTanhFma, use_rng, abandon,
-                                   ctx->stream));
-    } else if (kernel == 1) {
-        RG_CUDA(rg::launch_grid_dec(a, ctx->variant == rg::kTanhFma, use_rng, abandon,
-                                    ctx->stream));
-    } else {
-        RG_CUDA(rg::launch_grid(a, ctx->variant == rg::kTanhFma, use_rng, abandon, lpc,
-                                ctx->stream));
-    }
+    RG_CUDA(rg::launch_grid(a, ctx->variant == rg::kTanhFma, use_rng, abandon, ctx->stream));
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     ctx->last_m = m_grid;
+    // rg_grid_fetch reads the pinned block only after a synchronous zero-copy step
+    ctx->last_zero_copy = zero_copy;
     if (flags & RG_ASYNC) {
         if (row_viol && (flags & RG_DEVICE_PTRS))
             RG_CUDA(cudaMemcpyAsync(row_viol, a.viol_out, m_grid * sizeof(unsigned),
                                     cudaMemcpyDeviceToDevice, ctx->stream));
         return RG_OK;
     }
-    ctx->last_zero_copy = zero_copy;
     if (zero_copy) {
         RG_CUDA(wait_token(ctx, reinterpret_cast<volatile rg::GridOut*>(blk), a.seq_token));
         return unpack_grid(ctx, blk, row_viol, m_grid, out, pbits_in_block ? pbits : nullptr,
@@ -853,12 +853,11 @@ int32_t rg_bisect(rg_ctx* ctx, const rg_problem* prob, const double* x0, double 
     }
     a.acc = ctx->b_acc.as<rg::BisectAcc>();
     a.out = ctx->b_out.as<rg::BisectOut>();
-    const int lpc = lpc_for(ctx, n_sim, flags);
-    a.tpb = tpb_for(ctx, n_sim * lpc, 1);
-    if (lpc == 1) grid_placement(ctx, n_sim, 1, &a.tpb, &a.smem_dyn);
+    a.tpb = tpb_for(ctx, n_sim, 1);
+    grid_placement(ctx, n_sim, 1, &a.tpb, &a.smem_dyn);
     const bool timed = !(flags & RG_NO_TIMING);
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-    RG_CUDA(rg::launch_bisect(a, ctx->variant == rg::kTanhFma, src, lpc, ctx->stream));
+    RG_CUDA(rg::launch_bisect(a, ctx->variant == rg::kTanhFma, src, ctx->stream));
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     if (!dev) {
         if (kappa_k) {
@@ -1091,8 +1090,7 @@ int32_t rg_grid_step_batch(rg_ctx* ctx, const rg_problem* prob, int32_t n_episod
     a.early_out = reinterpret_cast<long long*>(a.v_out + E);
     a.row_out = reinterpret_cast<int*>(a.early_out + E);
     a.viol_out = row_viol ? ctx->e_violout.as<unsigned>() : nullptr;
-    const int lpc = lpc_for(ctx, n_sim * E * M, flags);
-    a.tpb = tpb_for(ctx, n_sim * E * lpc, m_grid);
+    a.tpb = tpb_for(ctx, n_sim * E, m_grid);
     const bool fma = ctx->variant == rg::kTanhFma, poll = (flags & RG_ABANDON) != 0;
     // Staged: each episode's scenario block is generated into SoA once and shared by
     // its M rows (~20% faster than regenerating it in every cell, as for the single
@@ -1100,10 +1098,10 @@ int32_t rg_grid_step_batch(rg_ctx* ctx, const rg_problem* prob, int32_t n_episod
     const int64_t ld = (n_sim + 31) / 32 * 32;
     const int64_t ep_stride = (int64_t)prob->j_star * 3 * ld;
     const int64_t per_chunk = kStageMaxScenarioSteps / std::max<int64_t>(1, n_sim * prob->j_star);
-    if (lpc == 1 && !(flags & RG_FUSED_RNG) && per_chunk >= 1) {
+    if (!(flags & RG_FUSED_RNG) && per_chunk >= 1) {
         int64_t ec = std::min<int64_t>(E, per_chunk);
-        if (const char* env = getenv("RG_BATCH_CHUNK"))  // tests: force several chunks
-            ec = std::max<int64_t>(1, std::min<int64_t>(ec, atoll(env)));
+        if (ctx->tune.batch_chunk > 0)  // tests: force several chunks
+            ec = std::max<int64_t>(1, std::min<int64_t>(ec, ctx->tune.batch_chunk));
         RG_CUDA(ctx->soa.ensure((size_t)ec * ep_stride * sizeof(double)));
         a.soa = ctx->soa.as<double>();
         a.ld = ld;
@@ -1114,11 +1112,11 @@ int32_t rg_grid_step_batch(rg_ctx* ctx, const rg_problem* prob, int32_t n_episod
                                              ep_stride, ctx->soa.as<double>(), ctx->stream));
             a.e0 = (int32_t)e0;
             a.n_ep = n;
-            RG_CUDA(rg::launch_grid_batch(a, fma, poll, 1, ctx->stream));
+            RG_CUDA(rg::launch_grid_batch(a, fma, poll, ctx->stream));
         }
         a.n_ep = n_episodes;
     } else {
-        RG_CUDA(rg::launch_grid_batch(a, fma, poll, lpc, ctx->stream));
+        RG_CUDA(rg::launch_grid_batch(a, fma, poll, ctx->stream));
     }
     char* hout = reinterpret_cast<char*>(hin + 6 * E);
     const size_t out_bytes = (size_t)E * (3 * sizeof(double) + sizeof(int));

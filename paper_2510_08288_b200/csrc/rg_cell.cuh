@@ -204,41 +204,6 @@ struct ZeroSource {
     RG_HD D3 load(int32_t) const { return D3{0.0, 0.0, 0.0}; }
 };
 
-// The four tanh values of one step.  LPC lanes cooperate on a cell: with
-// LPC = 2 each lane of a pair evaluates two of the four (in lockstep) and the
-// pair swaps results with one shuffle per value; with LPC = 4 each lane
-// evaluates one.  ptxas serialises independent tanh chains inside a thread,
-// so spreading them over lanes turns ILP the compiler will not schedule into
-// TLP the warp schedulers do.  Every lane ends with all four values.
-template <bool FMA, int LPC>
-__device__ __forceinline__ void step_tanh(double x2, double a2, double b2, double c2,
-                                          double& u1, double& u2, double& u3, double& u4) {
-    if constexpr (LPC == 1) {
-        tanh4_auto<FMA>(x2, a2, b2, c2, u1, u2, u3, u4);
-    } else if constexpr (LPC == 2) {
-        const bool q = (threadIdx.x & 1u) != 0;
-        const double in[2] = {q ? a2 : x2, q ? c2 : b2};
-        double out[2];
-        tanh_lockstep<FMA, 2>(in, out);
-        const double o0 = __shfl_xor_sync(0xffffffffu, out[0], 1);
-        const double o1 = __shfl_xor_sync(0xffffffffu, out[1], 1);
-        u1 = q ? o0 : out[0];
-        u2 = q ? out[0] : o0;
-        u3 = q ? o1 : out[1];
-        u4 = q ? out[1] : o1;
-    } else {
-        const unsigned q = threadIdx.x & 3u;
-        const double in[1] = {q == 0 ? x2 : (q == 1 ? a2 : (q == 2 ? b2 : c2))};
-        double out[1];
-        tanh_lockstep<FMA, 1>(in, out);
-        const int base = (int)(threadIdx.x & 31u) & ~3;
-        u1 = __shfl_sync(0xffffffffu, out[0], base + 0);
-        u2 = __shfl_sync(0xffffffffu, out[0], base + 1);
-        u3 = __shfl_sync(0xffffffffu, out[0], base + 2);
-        u4 = __shfl_sync(0xffffffffu, out[0], base + 3);
-    }
-}
-
 // One cell.  POLL: every 32 steps check a row-level "already infeasible"
 // flag and abandon (used only when the caller wants verdicts, not P).
 //
@@ -247,12 +212,7 @@ __device__ __forceinline__ void step_tanh(double x2, double a2, double b2, doubl
 // bits are those of sfc_step.  Steps past an early exit or past the horizon are
 // computed speculatively and never observed.
 //
-// LPC > 1: all 32 lanes of the warp run the loop until every cell of the warp
-// is done (lanes of finished or out-of-range cells keep computing throwaway
-// values), so the shuffles in step_tanh always see full warps.  `live` marks
-// lanes whose cell exists.
-//
-// WARP (LPC = 1 only): the caller guarantees that all 32 lanes call, and the
+// WARP: the caller guarantees that all 32 lanes call, and the
 // lanes then run as one: out-of-range and finished lanes keep computing
 // throwaway values until every lane is done, the exit and the tanh range vote
 // are full-warp votes, and the per-step checks are predicated into the
@@ -261,14 +221,13 @@ __device__ __forceinline__ void step_tanh(double x2, double a2, double b2, doubl
 // RAISE (with WARP and POLL): a lane whose cell violates or overflows sets
 // *dead at once, so the other cells sharing the flag abandon at their next
 // poll (the joint bisection's OR-reduced violation flag).
-template <bool FMA, bool POLL, int LPC, class Src, bool WARP = false, bool RAISE = false,
+template <bool FMA, bool POLL, class Src, bool WARP = false, bool RAISE = false,
           bool MOD = false>
 __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2, double x3,
                                        double v, const Src& src, int32_t& steps,
                                        const unsigned int* dead, bool live = true) {
     static_assert(!RAISE || (WARP && POLL), "RAISE needs the polled warp-uniform form");
-    static_assert(!WARP || LPC == 1, "WARP is the one-lane-per-cell form");
-    constexpr bool kUniform = WARP || LPC > 1;  // all lanes run the loop together
+    constexpr bool kUniform = WARP;  // all lanes run the loop together
     const int32_t J = p.j_star;
     constexpr bool kRing = std::is_same<Src, SoaSource>::value;
     int status = kOk;
@@ -321,7 +280,7 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
     // step 0: tanh values, x2 after step 0
     const X2Stage s0 = x2_stage<FMA>(x2, v, p);
     double t1, t2, t3, t4;
-    step_tanh<FMA, LPC>(x2, s0.a2, s0.b2, s0.c2, t1, t2, t3, t4);
+    tanh4_auto<FMA>(x2, s0.a2, s0.b2, s0.c2, t1, t2, t3, t4);
     const double y1 = add(add(x2, mul(p.c, s0.s2)), dj0.d1);
     // step 1: tanh arguments, x2 after step 1
     const X2Stage s1 = x2_stage<FMA>(y1, v, p);
@@ -347,12 +306,7 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
             bad_bnd = !in_bounds(x1, p.ylo, p.yhi);
         };
         double u1, u2, u3, u4;
-        if constexpr (LPC == 1) {
-            tanh4_with<FMA, WARP, decltype(side)&, MOD>(g0, g1, g2, g3, u1, u2, u3, u4, side);
-        } else {
-            step_tanh<FMA, LPC>(g0, g1, g2, g3, u1, u2, u3, u4);
-            side();
-        }
+        tanh4_with<FMA, WARP, decltype(side)&, MOD>(g0, g1, g2, g3, u1, u2, u3, u4, side);
         if constexpr (WARP) {
             // the reference's order: overflow, then the output bound, then the poll
             bool aband = false;

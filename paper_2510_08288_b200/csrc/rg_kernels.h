@@ -206,16 +206,13 @@ cudaError_t launch_joint_decide(const JointArgs& a, int it, cudaStream_t s);
 cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s);
 cudaError_t launch_to_soa(const double* src, double* dst, int64_t n_sim, int64_t horizon,
                           int32_t j_star, int64_t ld, cudaStream_t s);
-cudaError_t launch_fill(const FillArgs& a, bool fma, bool rng, int lpc, cudaStream_t s);
+cudaError_t launch_fill(const FillArgs& a, bool fma, bool rng, cudaStream_t s);
 cudaError_t launch_gen_soa_batch(const uint64_t* hs, const double* lo, const double* span,
                                  int64_t k0, int64_t n_sim, int32_t j_star, int64_t ld,
                                  int32_t n_ep, int64_t ep_stride, double* dst, cudaStream_t s);
-cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, int lpc,
-                        cudaStream_t s);
-cudaError_t launch_grid_batch(const BatchArgs& a, bool fma, bool poll, int lpc, cudaStream_t s);
-cudaError_t launch_grid_dec(const GridArgs& a, bool fma, bool rng, bool poll, cudaStream_t s);
-cudaError_t launch_grid_ws(const GridArgs& a, bool fma, bool rng, bool poll, cudaStream_t s);
-cudaError_t launch_bisect(const BisectArgs& a, bool fma, int src, int lpc, cudaStream_t s);
+cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, cudaStream_t s);
+cudaError_t launch_grid_batch(const BatchArgs& a, bool fma, bool poll, cudaStream_t s);
+cudaError_t launch_bisect(const BisectArgs& a, bool fma, int src, cudaStream_t s);
 cudaError_t launch_fill_lin(const LinArgs& a, cudaStream_t s);
 cudaError_t launch_bisect_lin(const LinArgs& a, cudaStream_t s);
 cudaError_t launch_gen_soa_w(uint64_t hs, const double* lo, const double* span, int width,

@@ -451,10 +451,12 @@ def robust_rg_parallel_batch(plant, X, v_prev, r, cset, model, n_sim, seeds, con
     """E independent robust grid steps in one device launch (BASELINE C3/C5).
 
     Episode e is robust_rg_parallel(plant, X[e], GovernorState(v_prev[e]), r[e],
-    cset, sample_scenarios(model, n_sim, j_star+1, seeds[e]), config) with the
-    "hold" policy: returns (kappa[E], v_applied[E], feasible[E], early[E]),
-    each equal to the single-episode call's result.  Rows already known to be
-    infeasible stop early (verdicts are unaffected).
+    cset, sample_scenarios(model, n_sim, j_star+1, seeds[e]), config): returns
+    (kappa[E], v_applied[E], feasible[E], early[E]), each equal to the
+    single-episode call's result.  Under the "error" policy an episode with no
+    feasible candidate raises InfeasibleError, as the single call does
+    (governor.py:562-573).  Rows already known to be infeasible stop early
+    (verdicts are unaffected).
     """
     _require_surrogate(plant)
     if config.tighten_mode == "scale":
@@ -469,6 +471,10 @@ def robust_rg_parallel_batch(plant, X, v_prev, r, cset, model, n_sim, seeds, con
     ctx = _capi.context(getattr(config, "device", 0))
     row, kappa, v, early = ctx.grid_step_batch(prob, X, v_prev, r, seeds, k0, n_sim, model.lo,
                                                model.span, config.m_grid, config.prefix_mode)
+    if config.infeasible_policy == "error" and np.any(row < 0):
+        bad = np.flatnonzero(row < 0)
+        raise InfeasibleError(f"no candidate feasible, including kappa=0 (hold current "
+                              f"setpoint), in episode(s) {bad[:8].tolist()}")
     return kappa, v, row >= 0, early
 
 

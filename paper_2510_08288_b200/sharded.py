@@ -26,7 +26,7 @@ import time
 import numpy as np
 
 from . import _capi
-from .errors import InfeasibleError
+from .errors import ConfigError, InfeasibleError
 from .governor import (KappaResult, _prepared, _source, _validate_state, _host_rows,
                        update_setpoint)
 from .governor import _require_surrogate as _require_device_plant
@@ -43,6 +43,15 @@ def _dist():
     import torch.distributed as dist
 
     return dist
+
+
+def _check_shardable(scenarios, world: int) -> None:
+    """Every rank needs at least one scenario.  The check reads only the global
+    set, which every rank holds, so all ranks raise together before any device
+    work or collective (no rank is left waiting in an all-reduce)."""
+    if scenarios.n_sim < world:
+        raise ConfigError(f"{scenarios.n_sim} scenarios cannot be sharded over {world} ranks "
+                          "(each rank needs at least one)")
 
 
 def global_row_counts(local_viol: np.ndarray, group=None, device=None) -> np.ndarray:
@@ -117,6 +126,7 @@ def robust_rg_parallel_sharded(plant, x_t, state, r_t, cset, scenarios, config, 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     x_t = _validate_state(plant, x_t)
     _require_device_plant(plant)
+    _check_shardable(scenarios, world)
     prob, interval, grid, grid_list = _prepared(plant.step_size, cset.lower, cset.upper,
                                                 cset.anchor, config.epsilon,
                                                 config.tighten_mode, config.j_star,
@@ -185,6 +195,7 @@ def robust_rg_sequential_sharded(plant, x_t, state, r_t, cset, scenarios, config
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     x_t = _validate_state(plant, x_t)
     _require_device_plant(plant)
+    _check_shardable(scenarios, world)
     shard = scenarios.shard(rank, world)
     t0 = time.perf_counter()
     dev = None
@@ -264,6 +275,7 @@ def robust_rg_joint_sharded(plant, x_t, state, r_t, cset, scenarios, config, gro
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     x_t = _validate_state(plant, x_t)
     _require_device_plant(plant)
+    _check_shardable(scenarios, world)
     shard = scenarios.shard(rank, world)
     prob, _, _, _ = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor,
                               config.epsilon, config.tighten_mode, config.j_star, 0)

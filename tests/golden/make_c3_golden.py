@@ -2,8 +2,9 @@
 
 BASELINE.json configs[2] (10k scenarios, the desk-scale setpoint trace) run by the
 unmodified reference (`refgov.run_closed_loop`, `harness.py:138-224`, multicore
-fill) for the first STEPS steps, which cover the rise from rest to r = 0.4 and the
-r = 2.5 step at t = 400.  Writes tests/golden/c3_10k_trace.npz with the rows
+fill) for all 2000 steps of the desk-scale profile (STEPS env var to truncate): the rise
+from rest to r = 0.4, the r = 2.5 step at t = 400, r = -2.5 at t = 1000 and r = 0.2
+at t = 1600.  Writes tests/golden/c3_10k_trace.npz with the rows
 (v_t, y_t, kappa_t, feasible_t) per step.
 
 Run in the build container (needs /root/reference):
@@ -11,12 +12,13 @@ Run in the build container (needs /root/reference):
         python tests/golden/make_c3_golden.py
 """
 
+import os
 from pathlib import Path
 
 import numpy as np
 from refgov import load_config, run_closed_loop
 
-STEPS = 440
+STEPS = int(os.environ.get("STEPS", "2000"))
 
 setup = load_config({"governor": {"n_sim": 10000, "backend": "multicore"}})
 rec = run_closed_loop(setup.plant, setup.cset, setup.model, setup.governor, setup.profile,

@@ -22,6 +22,19 @@ def ctx():
     return _capi.context(0)
 
 
+_DEFAULTS = {"force_tpb": 0, "no_placement": 0, "no_pdl": 0, "no_step2": 0, "batch_chunk": 0}
+
+
+@pytest.fixture
+def tuned(ctx):
+    """Set rg_set_option knobs on the shared context; restored to the defaults after."""
+    def set_(**opts):
+        for k, v in opts.items():
+            ctx.set_option(k, v)
+    yield set_
+    set_(**_DEFAULTS)
+
+
 def _bits(a):
     return np.ascontiguousarray(a, dtype=np.float64).view(np.uint64)
 
@@ -102,17 +115,15 @@ def test_big_range_tanh_bit_exact(ctx, orc):
     assert mism.size == 0, f"{mism.size} mismatches, first x={x[mism[:5]]}"
 
 
-@pytest.mark.parametrize("lpc", [1, 2, 4])
 @pytest.mark.parametrize("mode", ["fused", "staged"])
 @pytest.mark.parametrize("idx", range(N_FILL))
-def test_grid_step_both_rng_paths(ctx, golden, idx, mode, lpc):
+def test_grid_step_both_rng_paths(ctx, golden, idx, mode):
     c = fill_case(golden, idx)
     m = rg.DisturbanceModel(c["ranges"])
     scen = _capi.make_scenarios(c["seed"], 0, c["n_sim"], m.lo, m.span)
     prob = _problem(c["lower"], c["upper"], c["anchor"], c["eps"], c["j_star"])
     res, viol, pbits = ctx.grid_step(prob, c["x0"], c["v_prev"], c["r"], c["m_grid"],
-                                     c["prefix"], None, c["n_sim"], scen, True, rng_mode=mode,
-                                     lpc=lpc)
+                                     c["prefix"], None, c["n_sim"], scen, True, rng_mode=mode)
     P = np.unpackbits(pbits.view(np.uint8), axis=1, bitorder="little")[:, :c["n_sim"]]
     ss = c["ss_ok"]
     # simulated rows carry their own bits; the reference's P has the same rows
@@ -126,17 +137,16 @@ def test_grid_step_both_rng_paths(ctx, golden, idx, mode, lpc):
     assert kappa == c["result"][0]
 
 
-@pytest.mark.parametrize("lpc", [1, 2, 4])
 @pytest.mark.parametrize("mode", ["fused", "staged"])
 @pytest.mark.parametrize("idx", range(N_BIS))
-def test_bisect_both_rng_paths(ctx, golden, idx, mode, lpc):
+def test_bisect_both_rng_paths(ctx, golden, idx, mode):
     c = bis_case(golden, idx)
     m = rg.DisturbanceModel(c["ranges"])
     scen = _capi.make_scenarios(c["seed"], 0, c["n_sim"], m.lo, m.span)
     prob = _problem(c["lower"], c["upper"], c["anchor"], c["eps"], c["j_star"])
     res, per, paths = ctx.bisect(prob, c["x0"], c["v_prev"], c["r"], c["n_kappa"], None,
                                  c["n_sim"], scen, per_scenario=True, paths=True,
-                                 rng_mode=mode, lpc=lpc)
+                                 rng_mode=mode)
     pk, po = paths
     ref_k = c["paths"][..., 0]
     used = ~np.isnan(ref_k)
@@ -194,9 +204,8 @@ def test_staged_and_fused_agree_at_scale(ctx):
     assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
 
 
-@pytest.mark.parametrize("lpc", [1, 2, 4])
 @pytest.mark.parametrize("idx", range(N_FILL))
-def test_fill_cells_every_lane_split(ctx, golden, idx, lpc):
+def test_fill_cells_all_rows(ctx, golden, idx):
     c = fill_case(golden, idx)
     grid = rg.grid_kappas(c["m_grid"])
     v_rows = np.array([rg.update_setpoint(c["v_prev"], c["r"], float(k)) for k in grid])
@@ -205,37 +214,18 @@ def test_fill_cells_every_lane_split(ctx, golden, idx, lpc):
     m = rg.DisturbanceModel(c["ranges"])
     scen = _capi.make_scenarios(c["seed"], 0, c["n_sim"], m.lo, m.span)
     ctx.fill(_problem(c["lower"], c["upper"], c["anchor"], c["eps"], c["j_star"]), c["x0"],
-             v_rows, np.arange(c["m_grid"], dtype=np.int32), None, c["n_sim"], scen, S, steps,
-             lpc=lpc)
+             v_rows, np.arange(c["m_grid"], dtype=np.int32), None, c["n_sim"], scen, S, steps)
     assert np.array_equal(S, c["S_all"]) and np.array_equal(steps, c["steps_all"]), c["name"]
-
-
-@pytest.mark.parametrize("lpc", [1, 2, 4])
-def test_batch_every_lane_split(ctx, lpc):
-    rng = np.random.default_rng(3)
-    E, n, M = 12, 70, 16
-    vp = rng.uniform(-1, 1, E)
-    r = rng.uniform(-2.5, 2.5, E)
-    X = np.stack([[np.tanh(v), v, np.tanh(v) / 2] for v in vp]) + rng.uniform(-0.05, 0.05, (E, 3))
-    seeds = [int(x) for x in rng.integers(0, 2**62, E)]
-    m = rg.DisturbanceModel.scaled(0.02, 3)
-    prob = _problem(-0.9, 0.9, 0.0, 0.05, 96)
-    ref = ctx.grid_step_batch(prob, X, vp, r, seeds, 0, n, m.lo, m.span, M, lpc=1,
-                              abandon=False, want_viol=True)
-    got = ctx.grid_step_batch(prob, X, vp, r, seeds, 0, n, m.lo, m.span, M, lpc=lpc,
-                              abandon=False, want_viol=True)
-    for a, b in zip(ref, got):
-        assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("abandon", [False, True])
 @pytest.mark.parametrize("chunk", [None, 5, 1])
-def test_batch_staged_chunks_equal_fused(ctx, monkeypatch, chunk, abandon):
+def test_batch_staged_chunks_equal_fused(ctx, tuned, chunk, abandon):
     """Staged episode blocks (k_gen_soa_batch), in one or several chunks of
     episodes, against the fused in-rollout RNG: same rows, kappas, setpoints,
     early counts and per-row violation counts."""
     if chunk is not None:
-        monkeypatch.setenv("RG_BATCH_CHUNK", str(chunk))
+        tuned(batch_chunk=chunk)
     rng = np.random.default_rng(11)
     E, n, M = 13, 150, 8
     vp = rng.uniform(-1, 1, E)
@@ -252,88 +242,47 @@ def test_batch_staged_chunks_equal_fused(ctx, monkeypatch, chunk, abandon):
         assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("kernel", ["warp-spec", "decoupled", "per-step"])
-@pytest.mark.parametrize("mode", ["fused", "staged"])
-@pytest.mark.parametrize("idx", range(N_FILL))
-def test_grid_step_kernels_agree_with_reference(ctx, golden, idx, mode, kernel):
-    c = fill_case(golden, idx)
-    m = rg.DisturbanceModel(c["ranges"])
-    scen = _capi.make_scenarios(c["seed"], 0, c["n_sim"], m.lo, m.span)
-    prob = _problem(c["lower"], c["upper"], c["anchor"], c["eps"], c["j_star"])
-    for abandon in (False, True):
-        res, viol, pbits = ctx.grid_step(prob, c["x0"], c["v_prev"], c["r"], c["m_grid"],
-                                         c["prefix"], None, c["n_sim"], scen, not abandon,
-                                         abandon=abandon, rng_mode=mode, kernel=kernel)
-        kappa = 0.0 if res.row < 0 else res.row / (c["m_grid"] - 1)
-        assert kappa == c["result"][0], (c["name"], abandon)
-        if not abandon:
-            P = np.unpackbits(pbits.view(np.uint8), axis=1, bitorder="little")[:, :c["n_sim"]]
-            ss = c["ss_ok"]
-            keep = [i for i in range(c["m_grid"]) if ss[i]]
-            first = {}
-            sim = []
-            for i in keep:
-                v = rg.update_setpoint(c["v_prev"], c["r"], i / (c["m_grid"] - 1))
-                if v not in first:
-                    first[v] = i
-                    sim.append(i)
-            assert np.array_equal(P[sim].astype(bool), c["P"][sim]), c["name"]
-            assert (int(res.sims_run), int(res.early_terms), int(res.overflows)) == \
-                (int(c["stats"][0]), int(c["stats"][1]), int(c["stats"][2]))
-
-
-@pytest.mark.parametrize("kernel", ["warp-spec", "decoupled"])
-@pytest.mark.parametrize("j_star", [256, 3, 257])
-def test_decoupled_matches_per_step_at_scale(ctx, kernel, j_star):
-    n, M = 5000, 32
-    m = rg.DisturbanceModel.scaled(0.02, 3)
-    prob = _problem(-0.9, 0.9, 0.0, 0.05, j_star)
-    rng = np.random.default_rng(2)
-    for trial in range(4):
-        vp = float(rng.uniform(-1, 1))
-        r = float(rng.uniform(-2.5, 2.5))
-        x0 = np.array([np.tanh(vp), vp, np.tanh(vp) / 2]) + rng.uniform(-0.05, 0.05, 3)
-        sc = _capi.make_scenarios(100 + trial, 0, n, m.lo, m.span)
-        a = ctx.grid_step(prob, x0, vp, r, M, False, None, n, sc, True, kernel="per-step")
-        b = ctx.grid_step(prob, x0, vp, r, M, False, None, n, sc, True, kernel=kernel)
-        assert a[0].row == b[0].row and a[0].early_terms == b[0].early_terms
-        assert a[0].overflows == b[0].overflows and a[0].sims_run == b[0].sims_run
-        assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
-        for mode in ("fused", "staged"):  # abandon path: same verdict
-            c = ctx.grid_step(prob, x0, vp, r, M, False, None, n, sc, False, abandon=True,
-                              rng_mode=mode, kernel=kernel)
-            assert c[0].row == a[0].row
-
-
 def test_grid_fetch_after_sync_and_async_steps(ctx):
-    """rg_grid_fetch returns the last step's result: after a synchronous
-    (zero-copy) step and after an RG_ASYNC step, identical to the direct result."""
+    """rg_grid_fetch returns the LAST step's result: after a synchronous (zero-copy)
+    step it re-reads that step; after an RG_ASYNC step on different inputs it returns
+    the async step's result, not the pinned block of the synchronous one before it."""
     import ctypes
 
     m = rg.DisturbanceModel.scaled(0.02, 3)
     prob = _problem(-0.9, 0.9, 0.0, 0.05, 128)
     x0 = np.array([0.1, 0.3, 0.05])
-    sc = _capi.make_scenarios(77, 0, 3000, m.lo, m.span)
-    res, viol, _ = ctx.grid_step(prob, x0, 0.3, 2.4, 32, False, None, 3000, sc, False)
+    sc_a = _capi.make_scenarios(77, 0, 3000, m.lo, m.span)
+    sc_b = _capi.make_scenarios(78, 0, 3000, m.lo, m.span)
     lib = ctx.lib
-    for flags in (0, _capi.RG_ASYNC):
-        if flags:
-            out = _capi.GridResult()
-            _capi.check(lib.rg_grid_step(ctx.handle, ctypes.byref(prob), x0.ctypes.data, 0.3,
-                                         2.4, 32, 0, None, 3000, 0, ctypes.byref(sc), None,
-                                         None, ctypes.byref(out), flags))
+    # reference results of both inputs, each from its own synchronous step
+    res_b, viol_b, _ = ctx.grid_step(prob, x0, 0.3, 1.9, 32, False, None, 3000, sc_b, False)
+    res_a, viol_a, _ = ctx.grid_step(prob, x0, 0.3, 2.4, 32, False, None, 3000, sc_a, False)
+    assert not np.array_equal(viol_a, viol_b), "the two inputs must give different counts"
+
+    def fetch():
         got = _capi.GridResult()
         v2 = np.empty(32, np.uint32)
         _capi.check(lib.rg_grid_fetch(ctx.handle, v2.ctypes.data, 32, ctypes.byref(got)))
-        assert (got.row, got.sims_run, got.early_terms, got.overflows) == \
-            (res.row, res.sims_run, res.early_terms, res.overflows)
-        assert np.array_equal(v2, viol)
+        return got, v2
+
+    got, v2 = fetch()  # after the synchronous step on inputs a
+    assert (got.row, got.sims_run, got.early_terms, got.overflows) == \
+        (res_a.row, res_a.sims_run, res_a.early_terms, res_a.overflows)
+    assert np.array_equal(v2, viol_a)
+    out = _capi.GridResult()
+    _capi.check(lib.rg_grid_step(ctx.handle, ctypes.byref(prob), x0.ctypes.data, 0.3, 1.9, 32, 0,
+                                 None, 3000, 0, ctypes.byref(sc_b), None, None,
+                                 ctypes.byref(out), _capi.RG_ASYNC))
+    got, v2 = fetch()  # after the asynchronous step on inputs b
+    assert (got.row, got.sims_run, got.early_terms, got.overflows) == \
+        (res_b.row, res_b.sims_run, res_b.early_terms, res_b.overflows)
+    assert np.array_equal(v2, viol_b)
 
 
-@pytest.mark.parametrize("env", [{"RG_NO_PLACEMENT": "1"}, {"RG_FORCE_TPB": "32"},
-                                 {"RG_FORCE_TPB": "128"}, {"RG_NO_STEP2": "1"}])
+@pytest.mark.parametrize("opts", [{"no_placement": 1}, {"force_tpb": 32}, {"force_tpb": 128},
+                                  {"no_step2": 1}, {"no_pdl": 1}])
 @pytest.mark.parametrize("shape", [(1000, 32), (300, 32), (4000, 32), (97, 5)])
-def test_single_wave_placement_changes_no_bit(ctx, monkeypatch, env, shape):
+def test_single_wave_placement_changes_no_bit(ctx, tuned, opts, shape):
     """The single-wave placement (blocks of 4L warps pinned one per SM, with the
     two-step rollout over the staged block) against the other block shapes and the
     one-step rollout (the multi-wave forms), on transient-binding inputs: same P
@@ -354,8 +303,7 @@ def test_single_wave_placement_changes_no_bit(ctx, monkeypatch, env, shape):
                 pbits.copy(), b.kappa, b.found, b.cells, b.early, j.kappa, j.found, j.cells)
 
     ref = run()
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
+    tuned(**opts)
     got = run()
     assert ref[1] > 0 and 0 < int(np.count_nonzero(ref[4])) , "inputs must bind some rows"
     for a, b in zip(ref, got):
@@ -364,7 +312,7 @@ def test_single_wave_placement_changes_no_bit(ctx, monkeypatch, env, shape):
 
 @pytest.mark.parametrize("j_star", [1, 2, 3, 31, 32, 33, 64, 257])
 @pytest.mark.parametrize("shape", [(1000, 32), (300, 8)])
-def test_two_step_rollout_edges(ctx, monkeypatch, shape, j_star):
+def test_two_step_rollout_edges(ctx, tuned, shape, j_star):
     """The single-wave two-step rollout (rollout2) at odd and short horizons, with
     and without abandonment (the polled form), against the one-step rollout."""
     n, M = shape
@@ -388,9 +336,42 @@ def test_two_step_rollout_edges(ctx, monkeypatch, shape, j_star):
         return out
 
     got = run()
-    monkeypatch.setenv("RG_NO_STEP2", "1")
+    tuned(no_step2=1)
     ref = run()
     for g, f in zip(got, ref):
         for x, y in zip(g, f):
             assert np.array_equal(np.asarray(x), np.asarray(y))
         assert g[6] == g[0]  # abandonment changes no verdict
+
+
+def test_concurrent_calls_on_one_context_are_serialised():
+    """The reference service runs /govern/step in a thread pool: concurrent governor
+    calls on one device (one shared context) must each get their own result --
+    the same as the calls made one after another."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    plant = rg.make_plant("surrogate-fc")
+    box = rg.ConstraintSet(-0.9, 0.9, anchor=0.0)
+    model = rg.DisturbanceModel.scaled(0.02, 3)
+    cfg = rg.GovernorConfig(j_star=128, n_sim=2000, m_grid=32, n_kappa=8)
+    rng = np.random.default_rng(5)
+    jobs = []
+    for q in range(16):
+        vp = float(rng.uniform(-1, 1))
+        x0 = np.array([np.tanh(vp), vp, np.tanh(vp) / 2]) + rng.uniform(-0.05, 0.05, 3)
+        jobs.append((x0, vp, float(rng.uniform(-2.5, 2.5)), 900 + q))
+
+    def call(job):
+        x0, vp, r, seed = job
+        scen = rg.sample_scenarios(model, cfg.n_sim, cfg.j_star + 1, seed=seed)
+        a = rg.robust_rg_parallel(plant, x0, rg.GovernorState(vp), r, box, scen, cfg)
+        b = rg.robust_rg_sequential(plant, x0, rg.GovernorState(vp), r, box, scen, cfg)
+        return a.kappa_opt, a.v_applied, a.feasible, a.matrix.copy(), b.kappa_opt, \
+            b.diagnostics["sims_run"]
+
+    serial = [call(j) for j in jobs]
+    for _ in range(3):
+        with ThreadPoolExecutor(max_workers=8) as ex:
+            conc = list(ex.map(call, jobs))
+        for s_, c_ in zip(serial, conc):
+            assert s_[:3] == c_[:3] and np.array_equal(s_[3], c_[3]) and s_[4:] == c_[4:]
