@@ -5,18 +5,24 @@ contiguous counter ranges, rank r simulating scenarios [k0 + r*n/W,
 k0 + (r+1)*n/W) -- the counter RNG makes that free of scenario traffic
 (disturbance.py:85-92).  The only exchange is per step:
 
-* grid step (Alg. 3): one all-reduce (SUM) of the per-row violating-scenario
-  counts, int64[M]; a row is all-feasible iff its global count is 0, and every
-  rank extracts the same row (extract_kappa_opt, governor.py:351-377);
-* exact Alg. 2: one all-reduce each of MIN kappa, MIN found (= AND) and SUM of
-  the cell / early counters (governor.py:496-506);
+* grid step (Alg. 3): the kernel writes this shard's per-row violating-scenario
+  counts (int32, -1 for a gated-out row) into device memory and one all-reduce
+  (MAX) runs on the library's stream right after it; a row is all-feasible iff
+  its global count is 0, and every rank extracts the same row
+  (extract_kappa_opt, governor.py:351-377).  128 bytes per step;
+* exact Alg. 2: ONE all-reduce per step: every rank writes (kappa as its
+  dyadic-number bits, found, cells, early) into its own slot of a zeroed
+  int64[4 * world] vector and the SUM all-reduce gathers them; each rank then
+  takes MIN kappa, AND found and the sums (governor.py:496-506);
 * joint bisection: one all-reduce (MAX) of the uint32
   violation flag per iteration, enqueued on the library's stream between the
   local rollout kernel and the decision kernel, so the n_kappa + 1 iterations
   never wait on the host.
 
-The collectives run through torch.distributed (NCCL on GPUs, gloo on CPU for
-the host-logic tests); the local step is the device kernel.
+The collectives run through torch.distributed on device tensors: NCCL on the
+GPUs, or gloo (which all-reduces CUDA tensors through the host) for the
+world-size-2 tests that run both ranks on one GPU.  The local step is the
+device kernel.
 """
 
 from __future__ import annotations
@@ -112,7 +118,7 @@ def _device_row(ctx, dist, group, prob, x_t, v_prev, r_t, config, n_sim, stream)
     else:
         ok = np.flatnonzero(full)
         idx = int(ok[-1]) if ok.size else -1
-    return None if idx < 0 else idx
+    return (None if idx < 0 else idx), counts
 
 
 def robust_rg_parallel_sharded(plant, x_t, state, r_t, cset, scenarios, config, group=None,
@@ -120,7 +126,9 @@ def robust_rg_parallel_sharded(plant, x_t, state, r_t, cset, scenarios, config, 
     """robust_rg_parallel over the ranks of `group`; every rank returns the same result.
 
     ``local_step(shard) -> uint32[M]`` computes this rank's per-row counts; the
-    default is the device kernel (rg_grid_step).  matrix is None (P is sharded).
+    default is the device kernel (rg_grid_step) with the exchange on the device
+    (_device_row).  A dense host scenario tensor is stepped synchronously and its
+    counts all-reduced from the host.  matrix is None (P is sharded).
     """
     dist = _dist()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
@@ -136,12 +144,14 @@ def robust_rg_parallel_sharded(plant, x_t, state, r_t, cset, scenarios, config, 
     _, ss_ok, dup_src, rows = _host_rows(float(state.v_prev), float(r_t), grid_list, interval)
     ss_ok = np.array(ss_ok, dtype=bool)
     dup_src = np.array(dup_src, dtype=np.int64)
+    counts = None
     if local_step is None:
         ctx = _capi.context(getattr(config, "device", 0))
         dist_t, n_sim, stream = _source(shard, config.j_star)
-        if dist_t is None and dist.get_backend(group) == "nccl":
-            row = _device_row(ctx, dist, group, prob, x_t, state.v_prev, r_t, config, n_sim,
-                              stream)
+        if dist_t is None:
+            with ctx.lock:
+                row, counts = _device_row(ctx, dist, group, prob, x_t, state.v_prev, r_t,
+                                          config, n_sim, stream)
         else:
             res, viol, _ = ctx.grid_step(prob, x_t, state.v_prev, r_t, config.m_grid,
                                          config.prefix_mode, dist_t, n_sim, stream, False,
@@ -152,6 +162,11 @@ def robust_rg_parallel_sharded(plant, x_t, state, r_t, cset, scenarios, config, 
         viol = np.asarray(local_step(shard), dtype=np.uint32)
         row = extract_row(global_row_counts(viol, group, None), dup_src, config.prefix_mode)
     diag = {"method": "parallel-grid-sharded", "ranks": world, "backend": "cuda",
+            "device_exchange": counts is not None,
+            # global per-row verdict words: 0 = feasible on every shard, -1 = gated out,
+            # > 0 = some shard violated (rows already known infeasible stop early, so a
+            # positive word is not a full count)
+            "row_words": None if counts is None else counts.tolist(),
             "sims_run": len(rows) * scenarios.n_sim,
             "ss_pruned_rows": int(np.count_nonzero(~ss_ok)),
             "dedup_rows": int(np.count_nonzero(dup_src >= 0)),
@@ -169,20 +184,25 @@ def robust_rg_parallel_sharded(plant, x_t, state, r_t, cset, scenarios, config, 
 
 def combine_bisection(kappa: float, found: int, cells: int, early: int, group=None,
                       device=None):
-    """MIN kappa, AND found, SUM cells/early over ranks (governor.py:496-506)."""
+    """MIN kappa, AND found, SUM cells/early over ranks (governor.py:496-506), in ONE
+    all-reduce: rank r writes (bits(kappa), found, cells, early) into slots 4r..4r+3 of a
+    zeroed int64[4 * world] vector, the SUM all-reduce gathers every rank's four numbers,
+    and each rank reduces them itself.  kappa >= 0, so its IEEE bits order like its
+    value; the slots are exact (each is a sum of one number and zeros)."""
     import torch
 
     dist = _dist()
-    k = torch.tensor([kappa], dtype=torch.float64)
-    f = torch.tensor([int(found)], dtype=torch.int64)
-    ce = torch.tensor([int(cells), int(early)], dtype=torch.int64)
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    v = torch.zeros(4 * world, dtype=torch.int64)
+    v[4 * rank: 4 * rank + 4] = torch.tensor(
+        [int(np.float64(kappa).view(np.int64)), int(bool(found)), int(cells), int(early)],
+        dtype=torch.int64)
     if device is not None:
-        k, f, ce = k.to(device), f.to(device), ce.to(device)
-    dist.all_reduce(k, op=dist.ReduceOp.MIN, group=group)
-    dist.all_reduce(f, op=dist.ReduceOp.MIN, group=group)
-    dist.all_reduce(ce, op=dist.ReduceOp.SUM, group=group)
-    ce = ce.cpu().numpy()
-    return float(k.item()), bool(f.item()), int(ce[0]), int(ce[1])
+        v = v.to(device)
+    dist.all_reduce(v, op=dist.ReduceOp.SUM, group=group)
+    a = v.cpu().numpy().reshape(world, 4)
+    kappa = float(a[:, 0].min().astype(np.int64).view(np.float64))
+    return kappa, bool(a[:, 1].min()), int(a[:, 2].sum()), int(a[:, 3].sum())
 
 
 def robust_rg_sequential_sharded(plant, x_t, state, r_t, cset, scenarios, config, group=None,
@@ -207,7 +227,7 @@ def robust_rg_sequential_sharded(plant, x_t, state, r_t, cset, scenarios, config
         res, _, _ = ctx.bisect(prob, x_t, state.v_prev, r_t, config.n_kappa, dist_t, n_sim,
                                stream)
         local = (res.kappa, res.found, res.cells, res.early)
-        dev = f"cuda:{ctx.device}" if dist.get_backend(group) == "nccl" else None
+        dev = f"cuda:{ctx.device}"
     else:
         local = local_step(shard)
     kappa, found, cells, early = combine_bisection(*local, group=group, device=dev)
@@ -281,6 +301,25 @@ def robust_rg_joint_sharded(plant, x_t, state, r_t, cset, scenarios, config, gro
                               config.epsilon, config.tighten_mode, config.j_star, 0)
     impl = shard_impl or DeviceJointShard(_capi.context(getattr(config, "device", 0)))
     t0 = time.perf_counter()
+    lock = impl.ctx.lock if hasattr(impl, "ctx") else _nullcontext()
+    with lock:  # begin .. end is one search on the context: no other call may interleave
+        kappa, found, cells, early = _joint_iterations(impl, dist, group, prob, x_t, state, r_t,
+                                                       config, shard)
+    import torch
+
+    ce = torch.tensor([cells, early], dtype=torch.int64)
+    if hasattr(impl, "ctx"):
+        ce = ce.to(f"cuda:{impl.ctx.device}")
+    dist.all_reduce(ce, op=dist.ReduceOp.SUM, group=group)
+    cells, early = (int(x) for x in ce.cpu().tolist())
+    v = update_setpoint(state.v_prev, r_t, kappa)
+    state.v_prev = v
+    return KappaResult(kappa, v, found, {"method": "joint-sharded", "ranks": world,
+                                         "sims_run": cells, "early_terms": early,
+                                         "wall_us": int((time.perf_counter() - t0) * 1e6)})
+
+
+def _joint_iterations(impl, dist, group, prob, x_t, state, r_t, config, shard):
     dist_t, n_sim, stream = _source(shard, config.j_star)
     impl.begin(prob, x_t, state.v_prev, r_t, config.n_kappa, dist_t, n_sim, stream)
     import torch
@@ -292,17 +331,7 @@ def robust_rg_joint_sharded(plant, x_t, state, r_t, cset, scenarios, config, gro
             impl.roll(it)
             dist.all_reduce(impl.flag(), op=dist.ReduceOp.MAX, group=group)
             impl.decide(it)
-    kappa, found, cells, early = impl.end()
-    ce = torch.tensor([cells, early], dtype=torch.int64)
-    if dist.get_backend(group) == "nccl":
-        ce = ce.to(f"cuda:{impl.ctx.device}")
-    dist.all_reduce(ce, op=dist.ReduceOp.SUM, group=group)
-    cells, early = (int(x) for x in ce.cpu().tolist())
-    v = update_setpoint(state.v_prev, r_t, kappa)
-    state.v_prev = v
-    return KappaResult(kappa, v, found, {"method": "joint-sharded", "ranks": world,
-                                         "sims_run": cells, "early_terms": early,
-                                         "wall_us": int((time.perf_counter() - t0) * 1e6)})
+    return impl.end()
 
 
 class _nullcontext:

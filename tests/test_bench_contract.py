@@ -23,10 +23,53 @@ def test_reference_arm_line():
                 "cpu_baseline", "e2e"):
         assert key in d, key
     assert d["impl"] == "reference" and d["steps"] == 2 and d["higher_is_better"] is True
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    # the unmodified reference (oracle/_ref, numba) when staged, else the oracle's C port
+    assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
     assert d["cpu_baseline"]["value"] == d["value"] == d["e2e"]["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["config"]["workload"].startswith("C2 bench snapshot")
+    assert d["config"]["n_sim"] == 200
+
+
+def test_config_is_shared_by_both_arms():
+    """Both arms print the same config dict (the driver's same_config check)."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    for wl in ("c2", "c4", "c5"):
+        spec = dict(bench.WORKLOADS[wl])
+        a = bench.config_of(wl, spec, 4, 256)
+        b = bench.config_of(wl, dict(spec), 4, 256)
+        assert a == b and a["workload"] == spec["name"]
+    assert bench.config_of("c4", dict(bench.WORKLOADS["c4"]), 8, 256)["n_sim"] == 1 << 20
+
+
+def test_gpus_flag_must_match_world_size():
+    env = dict(**__import__("os").environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "4", "--impl",
+                          "reference", "--steps", "1"], capture_output=True, text=True, env=env,
+                         timeout=120)
+    assert out.returncode == 2 and "WORLD_SIZE=2" in out.stderr
+
+
+def test_active_cells_matches_host_rows():
+    """C5's work count (the reference's sims_run / n_sim per episode) against the
+    product's own host gate + dedup loop (governor._host_rows)."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    from paper_2510_08288_b200.governor import _host_rows, grid_kappas
+
+    rng = __import__("numpy").random.default_rng(0)
+    import numpy as np
+    E = 300
+    vp = np.concatenate([rng.uniform(-1.5, 1.5, E - 50), np.full(50, 0.4)])
+    r = np.concatenate([rng.uniform(-2.5, 2.5, E - 100), np.full(50, 0.4), np.full(50, 2.5)])
+    interval = (-1.27, 1.27)
+    got = bench.active_cells(vp, r, 32, interval)
+    grid = grid_kappas(32).tolist()
+    for e in range(E):
+        _, _, _, reps = _host_rows(float(vp[e]), float(r[e]), grid, interval)
+        assert got[e] == len(reps), e
 
 
 def test_issue_model_arithmetic():
