@@ -796,7 +796,10 @@ def run_sweep(args, ctx, lib, stream, flush, prob, x0, x0_ptr, model, plant, box
         sc = _capi.make_scenarios(BASE_SEED + 9000, 0, n_b, model.lo, model.span)
         for name, call in (
                 ("alg2", lambda: ctx.bisect(prob, x0, 0.0, 2.5, 8, None, n_b, sc)[0]),
-                ("joint", lambda: ctx.bisect_joint(prob, x0, 0.0, 2.5, 8, None, n_b, sc))):
+                ("joint", lambda: ctx.bisect_joint(prob, x0, 0.0, 2.5, 8, None, n_b, sc)),
+                ("joint, one launch per iteration",
+                 lambda: ctx.bisect_joint(prob, x0, 0.0, 2.5, 8, None, n_b, sc,
+                                          per_iteration=True))):
             call()
             reps = 10
             t0 = time.perf_counter()

@@ -68,6 +68,8 @@ extern "C" {
  * (whose rollouts often stop after a few steps), and fused above.  The batched
  * grid step stages each episode's block, in chunks of episodes of at most 16 GB,
  * unless RG_FUSED_RNG is given. */
+#define RG_JOINT_ITER 0x80  /* rg_bisect_joint: one kernel per iteration (the sharded form's
+                               kernels) instead of the single persistent kernel */
 
 typedef struct rg_ctx rg_ctx;
 
@@ -251,9 +253,13 @@ RG_API int32_t rg_bisect_linear(rg_ctx *ctx, const rg_linear_plant *plant,
  * §8(a) row A9); cells/early count like Alg. 2 summed over scenarios, except
  * that abandoned rollouts are not early terminations.
  *
- * rg_bisect_joint runs the whole search on one device: n_kappa + 1 kernels
- * enqueued back to back, the decision taken by each kernel's last block, one
- * host synchronisation at the end.  The begin/iter/flag/decide/end calls
+ * rg_bisect_joint runs the whole search on one device in ONE persistent kernel
+ * (cooperative launch, every block resident): per iteration the warps roll the
+ * candidate out over 32-scenario tiles with early abandonment, meet at a grid
+ * barrier and read the OR-reduced flag; every block applies the same decision, so
+ * the search never returns to the host between iterations.  With RG_JOINT_ITER (or
+ * n_kappa >= 64) it enqueues n_kappa + 1 kernels instead, the decision taken by each
+ * kernel's last block.  One host synchronisation at the end either way.  The begin/iter/flag/decide/end calls
  * expose the same search one iteration at a time for a scenario-sharded run:
  * rg_joint_iter(ctx, it, 0) rolls the local shard out, the caller all-reduces
  * (MAX) the uint32 at rg_joint_flag on the context's stream, and

@@ -24,6 +24,7 @@ RG_OK, RG_E_NODEVICE, RG_E_UNSUPPORTED, RG_E_ARGS, RG_E_CUDA = 0, -1, -2, -3, -4
 RG_TANH_AUTO, RG_TANH_FMA, RG_TANH_GENERIC = 0, 1, 2
 RG_DEVICE_PTRS, RG_ASYNC, RG_ABANDON, RG_NO_TIMING = 0x1, 0x2, 0x4, 0x8
 RG_TANH_LOCKSTEP, RG_FUSED_RNG, RG_STAGE_RNG = 0x10, 0x20, 0x40
+RG_JOINT_ITER = 0x80
 _RNG_FLAGS = {None: 0, "fused": RG_FUSED_RNG, "staged": RG_STAGE_RNG}
 
 _i32, _i64, _u64, _d, _vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, \
@@ -360,8 +361,10 @@ class Context:
 
     @_locked
     def bisect_joint(self, prob: Problem, x0, v_prev, r, n_kappa, dist, n_sim,
-                     scen: Scenarios | None, rng_mode: str | None = None) -> "BisectResult":
-        """Joint bisection on this device (rg_bisect_joint)."""
+                     scen: Scenarios | None, rng_mode: str | None = None,
+                     per_iteration: bool = False) -> "BisectResult":
+        """Joint bisection on this device (rg_bisect_joint): one persistent kernel, or
+        one kernel per iteration with `per_iteration`."""
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
         horizon = 0
         if dist is not None:
@@ -372,7 +375,8 @@ class Context:
                                        float(r), int(n_kappa), _p(dist), int(n_sim),
                                        int(horizon),
                                        ctypes.byref(scen) if scen is not None else None,
-                                       ctypes.byref(res), _RNG_FLAGS[rng_mode]))
+                                       ctypes.byref(res), _RNG_FLAGS[rng_mode]
+                                       | (RG_JOINT_ITER if per_iteration else 0)))
         return res
 
     @_locked

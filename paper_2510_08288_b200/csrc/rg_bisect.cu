@@ -4,6 +4,8 @@
 // scenario per iteration, OR-reduced violation flag).
 #include "rg_common.cuh"
 
+#include <algorithm>
+
 namespace rg {
 
 // ---------------------------------------------------------------------------
@@ -106,6 +108,235 @@ __global__ void __launch_bounds__(256, RG_GRID_MINB) k_joint_roll(JointArgs a, i
     // directly; joint_decide adds none for a rolled-out candidate
     a.st->ticket = 0u;
     joint_decide(a, it, s_kappa, run == 2, 0ull);
+}
+
+// ---------------------------------------------------------------------------
+// joint search as ONE persistent kernel with speculative levels (north star: "the search
+// never round-trips to the host").
+//
+// A bisection path is sequential: candidate i+1 depends on candidate i's verdict.  But
+// the steady-state gate is known up front (gated candidates are infeasible without a
+// rollout), and below one wave most of the GPU is idle while one candidate's 32-scenario
+// tiles run latency-bound.  So each round rolls out a small tree of candidates at once:
+// the first gate-passing candidate on the current path, and for each of its two
+// possible verdicts the next gate-passing candidate after it, to `depth` levels (1, 3 or
+// 7 candidates).  After a grid barrier every block walks the tree with the violation
+// words, exactly the decisions governor.py:407-431 would take, and continues from where
+// the walk leaves the tree.  Candidates off the walked path are never consulted; a
+// candidate's rollouts abandon early when the candidate itself violates, or when an
+// ancestor whose feasible branch holds it violates (it can then no longer be on the
+// path).  Every candidate that is consulted has its exact verdict, so kappa, found and
+// the rollout count equal the one-candidate-per-iteration search; only the
+// (timing-dependent) early-termination count of the abandoning search may differ.
+// ---------------------------------------------------------------------------
+
+// Sense-free grid barrier on (count, gen): the last arriver resets count, then bumps
+// gen; the others spin on gen.  Requires every block of the grid to be resident.
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* vgen = gen;
+        const unsigned g = *vgen;
+        __threadfence();
+        if (atomicAdd(count, 1u) == nblocks - 1) {
+            *(volatile unsigned*)count = 0u;
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (*vgen == g) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// The search state between candidates (governor.py:407-431 on the joint verdicts).
+struct Bracket {
+    double lo, hi, kopt, kappa, v;  // kappa / v: the candidate waiting for a verdict
+    unsigned long long cells, early;  // sims_run and the gated candidates' early count
+    int it, found, done;
+};
+
+// Apply a verdict to the waiting candidate (one iteration of the walk).
+__device__ __forceinline__ void bracket_apply(Bracket& b, bool feas, const JointArgs& a) {
+    b.cells += (unsigned long long)a.n_sim;
+    if (b.it < 0) {
+        if (feas) {
+            b.kopt = 1.0;
+            b.found = 1;
+            b.done = 1;
+        }
+    } else if (feas) {
+        b.kopt = b.kappa;
+        b.found = 1;
+        b.lo = b.kappa;
+    } else {
+        b.hi = b.kappa;
+    }
+    b.it += 1;
+    if (b.it >= a.n_kappa) b.done = 1;
+}
+
+// Walk through gated candidates (infeasible without a rollout, every scenario an early
+// termination) to the next candidate that needs a rollout, or to the end of the search.
+__device__ __forceinline__ void bracket_advance(Bracket& b, const JointArgs& a) {
+    while (!b.done) {
+        b.kappa = b.it < 0 ? 1.0 : mul(0.5, add(b.lo, b.hi));
+        b.v = update_setpoint(a.v_prev, a.r, b.kappa);
+        if (ss_gate(b.v, a.p)) return;
+        b.early += (unsigned long long)a.n_sim;
+        bracket_apply(b, false, a);
+    }
+}
+
+__device__ __forceinline__ bool in_subtree(int y, int root) {  // heap order
+    while (y > root) y = (y - 1) >> 1;
+    return y == root;
+}
+
+template <bool FMA, int SRC>  // SRC: 0 zero (nominal), 1 rng, 2 soa
+__global__ void __launch_bounds__(256, 1) k_joint_spec(JointArgs a) {
+    JointState* st = a.st;
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned warp = threadIdx.x >> 5;
+    const int64_t n_tiles = (a.n_sim + 31) / 32;
+    const int64_t slots = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int nodes = (1 << a.depth) - 1;
+    const CellConst c = make_cell(a.p);
+    __shared__ double ring[2 * 3 * kRingStride];
+    __shared__ Bracket tree[kJointNodes];
+    __shared__ int active[kJointNodes];  // node ids that need rollouts, in heap order
+    __shared__ int n_active;
+    __shared__ Bracket cur;
+    if (threadIdx.x == 0) {
+        Bracket b{};
+        b.lo = 0.0;
+        b.hi = 1.0;
+        b.it = -1;
+        bracket_advance(b, a);
+        cur = b;
+    }
+    __syncthreads();
+    int round = 0;
+    for (; !cur.done && round < kJointMaxRounds; ++round) {
+        // the speculation tree of this round (every block builds the same one)
+        if (threadIdx.x == 0) {
+            int na = 0;
+            bool exists[kJointNodes];
+            for (int n = 0; n < nodes; ++n) {
+                exists[n] = n == 0 || (exists[(n - 1) >> 1] && !tree[(n - 1) >> 1].done);
+                if (!exists[n]) continue;
+                if (n == 0) {
+                    tree[0] = cur;
+                } else {
+                    Bracket b = tree[(n - 1) >> 1];
+                    bracket_apply(b, (n & 1) != 0, a);  // odd: the feasible branch
+                    bracket_advance(b, a);
+                    tree[n] = b;
+                }
+                if (!tree[n].done) active[na++] = n;
+            }
+            n_active = na;
+        }
+        __syncthreads();
+        unsigned* viol = st->sviol + round * 8;
+        unsigned* dead = st->sdead + round * 8;
+        unsigned long long* early = st->searly + round * 8;
+        const int64_t items = (int64_t)n_active * n_tiles;
+        // first item of every warp slot spread across the blocks (SMs) first, then
+        // dynamic items from the round's counter
+        int64_t t = (int64_t)warp * gridDim.x + blockIdx.x;
+        while (t < items) {
+            const int node = active[t / n_tiles];
+            const double v = tree[node].v;
+            unsigned* poll = dead + node;
+            if (!*(volatile unsigned*)poll) {
+                const int64_t k = (t % n_tiles) * 32 + lane;
+                const bool live = k < a.n_sim;
+                const int64_t kk = live ? k : 0;
+                int32_t steps = 0;
+                int stt;
+                if constexpr (SRC == 1) {
+                    RngSource src{a.stream, scenario_key(a.stream, (uint64_t)(a.k0 + kk))};
+                    stt = rollout<FMA, true, RngSource, true, true>(c, a.x0[0], a.x0[1], a.x0[2],
+                                                                     v, src, steps, poll, live);
+                } else if constexpr (SRC == 2) {
+                    SoaSource src{a.soa + kk, a.ld, ring + threadIdx.x};
+                    stt = rollout<FMA, true, SoaSource, true, true>(c, a.x0[0], a.x0[1], a.x0[2],
+                                                                     v, src, steps, poll, live);
+                } else {
+                    stt = rollout<FMA, true, ZeroSource, true, true>(c, a.x0[0], a.x0[1],
+                                                                      a.x0[2], v, ZeroSource{},
+                                                                      steps, poll, live);
+                }
+                const bool bad = live && stt != kOk && stt != kAbandoned;
+                if (__ballot_sync(0xffffffffu, bad) && lane == 0) {
+                    atomicOr(viol + node, 1u);
+                    atomicOr(poll, 1u);
+                    // this candidate is infeasible: the candidates of its feasible branch
+                    // can no longer be on the path
+                    for (int y = 2 * node + 1; y < nodes; ++y)
+                        if (in_subtree(y, 2 * node + 1)) atomicOr(dead + y, 1u);
+                }
+                warp_count_add(bad && steps < a.p.j_star, early + node);
+            }
+            if (slots >= items) break;  // every item had its own warp slot
+            int64_t nxt = 0;
+            if (lane == 0) nxt = slots + (int64_t)atomicAdd(&st->sitem[round], 1u);
+            t = __shfl_sync(0xffffffffu, nxt, 0);
+        }
+        grid_barrier(&st->bar_count, &st->bar_gen, gridDim.x);
+        // the walk: the decisions the one-candidate search takes, while they stay in the tree
+        if (threadIdx.x == 0) {
+            int n = 0;
+            Bracket b = tree[0];
+            while (true) {
+                const bool feas = *(volatile unsigned*)(viol + n) == 0u;
+                b.early += *(volatile unsigned long long*)(early + n);
+                const int nx = feas ? 2 * n + 1 : 2 * n + 2;
+                if (nx < nodes) {
+                    const unsigned long long e = b.early;
+                    b = tree[nx];  // = advance(apply(tree[n], feas)), plus the early counts
+                    b.early += e - tree[n].early;
+                    if (b.done) break;
+                    n = nx;
+                } else {
+                    bracket_apply(b, feas, a);
+                    bracket_advance(b, a);
+                    break;
+                }
+            }
+            cur = b;
+        }
+        __syncthreads();
+    }
+    // every block has read every word it needs; the last block out publishes and resets
+    __shared__ bool s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&st->exit_ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int q = threadIdx.x; q < round * 8; q += blockDim.x) {
+        st->sviol[q] = 0u;
+        st->sdead[q] = 0u;
+        st->searly[q] = 0ull;
+    }
+    for (int q = threadIdx.x; q < round; q += blockDim.x) st->sitem[q] = 0u;
+    if (threadIdx.x == 0) {
+        volatile JointState* vs = st;
+        vs->kopt = cur.kopt;
+        vs->found = cur.found;
+        vs->done = 1;
+        vs->cells = cur.cells;
+        vs->early = cur.early;
+        vs->rounds = round;
+        vs->exit_ticket = 0u;
+        vs->seq = vs->seq + 1;
+    }
 }
 
 // Decision kernel for the sharded form: runs after the all-reduce of st->viol.
@@ -267,6 +498,37 @@ cudaError_t launch_joint_roll(const JointArgs& a, int it, bool fma, int src, cud
     }
 #undef RG_J
     return cudaGetLastError();
+}
+
+int joint_spec_depth(int64_t n_sim, int sm_count) {
+    const int64_t tiles = (n_sim + 31) / 32;
+    const int64_t wave = 8 * (int64_t)sm_count;  // two warps per SM sub-partition
+    for (int d = 3; d >= 1; --d)
+        if (((int64_t)1 << d) - 1 <= wave / std::max<int64_t>(tiles, 1)) return d;
+    return 0;
+}
+
+cudaError_t launch_joint_spec(const JointArgs& a, bool fma, int src, int sm_count,
+                              cudaStream_t s) {
+    constexpr int kThreads = 256;
+    const void* fn;
+    if (fma) fn = src == 1 ? (const void*)k_joint_spec<true, 1>
+                           : src == 2 ? (const void*)k_joint_spec<true, 2>
+                                      : (const void*)k_joint_spec<true, 0>;
+    else fn = src == 1 ? (const void*)k_joint_spec<false, 1>
+                       : src == 2 ? (const void*)k_joint_spec<false, 2>
+                                  : (const void*)k_joint_spec<false, 0>;
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+    // one block per SM at most; warp w of block b takes item w * blocks + b first, so the
+    // items land one warp per SM sub-partition before any gets a second
+    const int64_t items = (((int64_t)1 << a.depth) - 1) * ((a.n_sim + 31) / 32);
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, sm_count));
+    JointArgs args = a;
+    void* params[] = {&args};
+    return cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kThreads), params, 0, s);
 }
 
 cudaError_t launch_joint_decide(const JointArgs& a, int it, cudaStream_t s) {

@@ -1012,6 +1012,18 @@ int32_t rg_bisect_joint(rg_ctx* ctx, const rg_problem* prob, const double* x0, d
     int32_t rc = rg_joint_begin(ctx, prob, x0, v_prev, r, n_kappa, dist, n_sim, horizon, rng,
                                 flags);
     if (rc) return rc;
+    const int depth = rg::joint_spec_depth(n_sim, ctx->sm_count);
+    if (!(flags & RG_JOINT_ITER) && depth > 0 && n_kappa + 1 <= rg::kJointMaxRounds) {
+        // the whole search in one cooperative launch, speculating `depth` levels per round
+        ctx->j_args.depth = depth;
+        const cudaError_t e = rg::launch_joint_spec(ctx->j_args, ctx->variant == rg::kTanhFma,
+                                                    ctx->j_src, ctx->sm_count, ctx->stream);
+        if (e != cudaSuccess) {
+            ctx->j_src = -1;
+            return fail(RG_E_CUDA, "joint search launch failed: %s", cudaGetErrorString(e));
+        }
+        return rg_joint_end(ctx, out);
+    }
     for (int32_t it = -1; it < n_kappa; ++it)
         if ((rc = rg_joint_iter(ctx, it, 1))) return rc;
     return rg_joint_end(ctx, out);

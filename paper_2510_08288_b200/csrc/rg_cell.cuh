@@ -470,8 +470,11 @@ struct Zero4Source {  // nominal prediction / micro-benchmarks
     __device__ __forceinline__ void finish() {}
 };
 
-template <bool FMA, bool POLL, class Src>
+// RAISE (with POLL): a lane whose cell violates or overflows sets *dead at once, as
+// rollout<..., RAISE> does (the joint search's OR-reduced flag).
+template <bool FMA, bool POLL, class Src, bool RAISE = false>
 struct Rollout2 {
+    static_assert(!RAISE || POLL, "RAISE needs the polled form");
     const CellConst& p;
     const double v;
     Src& src;
@@ -531,6 +534,7 @@ struct Rollout2 {
             status = now ? (ovf ? kOverflow : kViolated) : status;
             steps = now ? j + 1 : steps;
             done = done || now;
+            if (RAISE && now) atomicOr((unsigned int*)dead, 1u);
         }
         {  // step j+1 inside the horizon: overflow, bound, then the poll (x2 after it: G[0])
             const bool ovf = !(fabs(x1) <= kStateLimit && fabs(G[0]) <= kStateLimit &&
@@ -542,6 +546,7 @@ struct Rollout2 {
             status = now ? (ovf ? kOverflow : (bnd ? kViolated : kAbandoned)) : status;
             steps = now ? j + 2 : steps;
             done = done || now;
+            if (RAISE && now && (ovf || bnd)) atomicOr((unsigned int*)dead, 1u);
         }
         if (__all_sync(0xffffffffu, done)) return true;
 #pragma unroll
@@ -610,11 +615,11 @@ struct Rollout2 {
 
 // One cell, warp-uniform (all 32 lanes call, like rollout<..., WARP>), two steps per
 // iteration; same status / steps semantics as rollout.
-template <bool FMA, bool POLL, class Src>
+template <bool FMA, bool POLL, class Src, bool RAISE = false>
 __device__ __forceinline__ int rollout2(const CellConst& p, double x1, double x2, double x3,
                                         double v, Src& src, int32_t& steps,
                                         const unsigned int* dead, bool live) {
-    Rollout2<FMA, POLL, Src> r(p, v, src, dead);
+    Rollout2<FMA, POLL, Src, RAISE> r(p, v, src, dead);
     return r.run(x1, x2, x3, live, steps);
 }
 

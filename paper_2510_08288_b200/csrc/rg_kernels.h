@@ -176,6 +176,9 @@ struct BisectArgs {
 
 // Joint bisection: one candidate kappa for every
 // scenario per iteration, violations OR-reduced into one flag.
+constexpr int kJointMaxRounds = 64;  // persistent search: at most n_kappa + 1 rounds
+constexpr int kJointNodes = 7;       // speculation tree of depth <= 3 (heap order)
+
 struct JointState {
     double lo, hi, kopt;
     int found, done;
@@ -183,6 +186,18 @@ struct JointState {
     unsigned ticket;  // last-block election for the folded decision
     unsigned long long cells, early;
     unsigned long long seq;
+    // persistent speculative search (k_joint_spec): per round and tree node the
+    // violation word (a scenario of this candidate left the set), the abandon word the
+    // rollouts poll (this candidate violated, or an ancestor whose feasible branch holds
+    // it did), the early terminations, and per round the work-item counter.  Zero
+    // between launches (the last block out resets what it used); the grid barrier's
+    // count returns to 0 after every barrier and gen only grows.
+    unsigned sviol[kJointMaxRounds * 8];
+    unsigned sdead[kJointMaxRounds * 8];
+    unsigned long long searly[kJointMaxRounds * 8];
+    unsigned sitem[kJointMaxRounds];
+    unsigned bar_count, bar_gen, exit_ticket;
+    int rounds;  // rounds the last persistent search ran (diagnostics)
 };
 
 struct JointArgs {
@@ -198,9 +213,18 @@ struct JointArgs {
     int tpb;
     int smem_dyn;  // shared memory per block, static + dynamic (single-wave placement pin)
     int fold;  // 1: the last block decides (single GPU); 0: k_joint_decide after the all-reduce
+    int depth;  // persistent search: speculation depth (1..3): 2^depth - 1 candidates per round
 };
 
 cudaError_t launch_joint_roll(const JointArgs& a, int it, bool fma, int src, cudaStream_t s);
+// The whole joint search in one cooperative launch (every block co-resident), with
+// speculative evaluation of the next bisection levels while the GPU would otherwise sit
+// idle.  For searches of at most `max_tiles()` 32-scenario tiles; `sm_count` sizes the grid.
+cudaError_t launch_joint_spec(const JointArgs& a, bool fma, int src, int sm_count,
+                              cudaStream_t s);
+// Largest speculation depth whose candidates' tiles all fit in one wave of two warps per
+// SM sub-partition; 0 when even depth 1 does not fit (use the per-iteration launches).
+int joint_spec_depth(int64_t n_sim, int sm_count);
 cudaError_t launch_joint_decide(const JointArgs& a, int it, cudaStream_t s);
 
 cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s);

@@ -154,3 +154,99 @@ def test_grid_and_alg2_sharded_world1_nccl():
                                                               d.v_applied), (i, c, d)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [1, 31, 33, 1000, 148 * 32 + 1, 10_000, 100_000])
+@pytest.mark.parametrize("mode", ["fused", "staged"])
+def test_persistent_joint_equals_per_iteration_launches(n, mode):
+    """The persistent speculative kernel (a tree of 1, 3 or 7 candidates per round, grid
+    barrier, every block walking the same decisions) against the one-kernel-per-iteration
+    form: same kappa, found and rollout count on transient-binding inputs (where verdicts
+    flip along the path), and the same as the exact Alg. 2.  100k scenarios exceed one
+    wave and take the per-iteration launches in both calls."""
+    ctx = _capi.context(0)
+    rng = np.random.default_rng(n)
+    m = rg.DisturbanceModel.scaled(0.02, 3)
+    tight = rg.tighten(rg.ConstraintSet(-0.9, 0.9), 0.05)
+    lo, hi = rg.admissible_setpoints(tight.lower, tight.upper)
+    for trial in range(6):
+        j_star = (128, 256, 7)[trial % 3]
+        n_kappa = (8, 1, 20)[trial % 3]
+        prob = _capi.Problem(0.01, -0.9, 0.9, lo, hi, j_star, 0)
+        vp = float(rng.uniform(-1, 1))
+        r = float(rng.uniform(-2.5, 2.5))
+        x0 = np.array([np.tanh(vp), vp, np.tanh(vp) / 2]) + rng.uniform(-0.05, 0.05, 3)
+        sc = _capi.make_scenarios(7000 + trial, 3, n, m.lo, m.span)
+        per = ctx.bisect_joint(prob, x0, vp, r, n_kappa, None, n, sc, rng_mode=mode,
+                               per_iteration=True)
+        one = ctx.bisect_joint(prob, x0, vp, r, n_kappa, None, n, sc, rng_mode=mode)
+        assert (one.kappa, one.found, one.cells) == (per.kappa, per.found, per.cells), trial
+        a2, _, _ = ctx.bisect(prob, x0, vp, r, n_kappa, None, n, sc, rng_mode=mode)
+        assert (one.kappa, one.found) == (a2.kappa, a2.found), trial
+
+
+def test_persistent_joint_repeated_calls_and_long_searches():
+    """Back-to-back searches reuse the per-round words and the barrier (reset by the last
+    block out); n_kappa = 63 is the persistent kernel's limit, 64 falls back to one launch
+    per iteration.  Results stay those of the per-iteration form."""
+    ctx = _capi.context(0)
+    m = rg.DisturbanceModel.scaled(0.02, 3)
+    tight = rg.tighten(rg.ConstraintSet(-0.9, 0.9), 0.05)
+    lo, hi = rg.admissible_setpoints(tight.lower, tight.upper)
+    prob = _capi.Problem(0.01, -0.9, 0.9, lo, hi, 64, 0)
+    x0 = np.array([0.2, 0.4, 0.1])
+    for rep in range(40):
+        nk = (63, 64, 8, 30)[rep % 4]
+        sc = _capi.make_scenarios(100 + rep % 5, 0, 5000, m.lo, m.span)
+        a = ctx.bisect_joint(prob, x0, 0.4, 2.2 - 0.1 * (rep % 7), nk, None, 5000, sc)
+        b = ctx.bisect_joint(prob, x0, 0.4, 2.2 - 0.1 * (rep % 7), nk, None, 5000, sc,
+                             per_iteration=True)
+        assert (a.kappa, a.found, a.cells) == (b.kappa, b.found, b.cells), rep
+
+
+def test_persistent_joint_dense_and_nominal_sources(golden, orc):
+    """Dense host scenarios (staged from the caller's tensor) and a single scenario."""
+    ctx = _capi.context(0)
+    for idx in range(N_BIS):
+        c = bis_case(golden, idx)
+        if c["n_kappa"] + 1 > 64:
+            continue
+        dist = orc.sample(c["seed"], c["n_sim"], c["j_star"] + 1, c["ranges"])
+        tight = rg.tighten(_cset(c), c["eps"])
+        lo, hi = rg.admissible_setpoints(tight.lower, tight.upper)
+        prob = _capi.Problem(0.01, c["lower"], c["upper"], lo, hi, c["j_star"], 0)
+        one = ctx.bisect_joint(prob, c["x0"], c["v_prev"], c["r"], c["n_kappa"], dist,
+                               c["n_sim"], None)
+        per = ctx.bisect_joint(prob, c["x0"], c["v_prev"], c["r"], c["n_kappa"], dist,
+                               c["n_sim"], None, per_iteration=True)
+        assert (one.kappa, one.found, one.cells) == (per.kappa, per.found, per.cells), c["name"]
+        d1 = dist[:1]
+        one = ctx.bisect_joint(prob, c["x0"], c["v_prev"], c["r"], c["n_kappa"], d1, 1, None)
+        per = ctx.bisect_joint(prob, c["x0"], c["v_prev"], c["r"], c["n_kappa"], d1, 1, None,
+                               per_iteration=True)
+        assert (one.kappa, one.found, one.cells) == (per.kappa, per.found, per.cells), c["name"]
+
+
+def test_speculative_search_stress_against_per_iteration():
+    """200 random transient-binding searches at sizes where the speculation tree has 7,
+    3 and 1 candidates per round (n = 300, 2000, 4000): kappa / found / rollout count
+    equal the one-candidate-per-iteration search's."""
+    ctx = _capi.context(0)
+    rng = np.random.default_rng(2026)
+    for trial in range(200):
+        n = (300, 2000, 4000)[trial % 3]
+        mag = float(rng.choice([0.001, 0.02, 0.05]))
+        m = rg.DisturbanceModel.scaled(mag, 3)
+        eps = float(rng.choice([0.05, 0.2]))
+        tight = rg.tighten(rg.ConstraintSet(-0.9, 0.9), eps)
+        lo, hi = rg.admissible_setpoints(tight.lower, tight.upper)
+        j_star = int(rng.choice([16, 64, 200]))
+        prob = _capi.Problem(0.01, -0.9, 0.9, lo, hi, j_star, 0)
+        vp = float(rng.uniform(-1.2, 1.2))
+        r = float(rng.uniform(-3, 3))
+        x0 = np.array([np.tanh(vp), vp, np.tanh(vp) / 2]) + rng.uniform(-0.08, 0.08, 3)
+        sc = _capi.make_scenarios(int(rng.integers(0, 2**62)), 0, n, m.lo, m.span)
+        nk = int(rng.choice([4, 8, 12]))
+        one = ctx.bisect_joint(prob, x0, vp, r, nk, None, n, sc)
+        per = ctx.bisect_joint(prob, x0, vp, r, nk, None, n, sc, per_iteration=True)
+        assert (one.kappa, one.found, one.cells) == (per.kappa, per.found, per.cells), trial
