@@ -229,10 +229,11 @@ def test_closed_loop_c3_truncated(golden):
     assert np.array_equal(got, golden["c3_trace40"])
 
 
-def test_closed_loop_c3_10k_prefix():
-    """C3 at its named size: 10,000 scenarios per step, the first 440 steps of the
-    desk trace (rise to r = 0.4, then the r = 2.5 step at t = 400), equal to the
-    real reference's trace (tests/golden/make_c3_golden.py)."""
+def test_closed_loop_c3_10k_full_trace():
+    """C3 at its named size: 10,000 scenarios per step, the whole 2000-step desk trace
+    (rise to r = 0.4, r = 2.5 at t = 400, r = -2.5 at t = 1000, r = 0.2 at t = 1600;
+    1200 steps with kappa < 1), equal bit for bit to the real reference's trace
+    (tests/golden/make_c3_golden.py, multicore fill in the build container)."""
     from paper_2510_08288_b200.harness import ReferenceProfile, run_closed_loop
 
     with np.load(GOLDEN.with_name("c3_10k_trace.npz")) as z:
@@ -248,8 +249,8 @@ def test_closed_loop_c3_10k_prefix():
 
 def test_closed_loop_c5_batch_10k():
     """C5's batched path at 10k scenarios per episode: episode seeds base + e, one
-    rg_grid_step_batch launch per step.  Episode 0 (seed 2024) equals the real
-    reference's C3 trace; the others equal their single-episode loops."""
+    rg_grid_step_batch launch per step, the whole 2000-step trace.  Episode 0 (seed 2024)
+    equals the real reference's C3 trace; the others equal their single-episode loops."""
     from paper_2510_08288_b200.harness import (ReferenceProfile, run_closed_loop,
                                                run_closed_loop_batch)
 

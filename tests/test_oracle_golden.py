@@ -147,7 +147,7 @@ def test_closed_loop_desk_grid_trace(orc, golden):
     assert np.array_equal(got, golden["desk_grid_trace"])
 
 
-def test_closed_loop_c3_10k_prefix(orc, golden):
+def test_closed_loop_c3_10k_first_steps(orc, golden):
     """The oracle reproduces the first steps of the reference's 10k-scenario C3 trace
     (tests/golden/make_c3_golden.py); the device runs all of it (test_gpu_parity)."""
     with np.load(GOLDEN.with_name("c3_10k_trace.npz")) as z:
