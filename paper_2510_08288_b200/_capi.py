@@ -414,9 +414,11 @@ class Context:
 
     @_locked
     def grid_step_batch(self, prob: Problem, x0, v_prev, r, seeds, k0, n_sim, lo, span,
-                        m_grid, prefix_mode=False, abandon=True, want_viol=False, fused=False):
-        """Batched robust grid step; returns (row, kappa, v, early[, viol]).  The
-        scenario blocks are staged per episode unless `fused`."""
+                        m_grid, prefix_mode=False, abandon=True, want_viol=False, fused=False,
+                        staged=False):
+        """Batched robust grid step; returns (row, kappa, v, early[, viol]).  The library
+        stages each episode's scenario block when more than two rows per episode are live
+        and fuses the RNG into the rollouts otherwise; `fused` / `staged` force one."""
         x0 = np.ascontiguousarray(x0, dtype=np.float64).reshape(-1, 3)
         E = x0.shape[0]
         v_prev = np.ascontiguousarray(v_prev, dtype=np.float64).reshape(E)
@@ -434,7 +436,8 @@ class Context:
                                           _p(span), int(m_grid), int(bool(prefix_mode)),
                                           _p(row), _p(kap), _p(v), _p(early), _p(viol),
                                           (RG_ABANDON if abandon else 0)
-                                          | (RG_FUSED_RNG if fused else 0)))
+                                          | (RG_FUSED_RNG if fused else 0)
+                                          | (RG_STAGE_RNG if staged else 0)))
         return (row, kap, v, early, viol) if want_viol else (row, kap, v, early)
 
     @_locked

@@ -30,80 +30,66 @@ __global__ void k_gen_soa_batch(const uint64_t* __restrict__ hs, double3 lo, dou
 }
 
 // ---------------------------------------------------------------------------
-// batched grid step: E independent governor instances in one launch
+// batched grid step over the compacted (episode, row) pairs
 // ---------------------------------------------------------------------------
 
 // Launch bounds: at most 168 registers (3 blocks of 128 threads per SM), so the
 // 64-thread blocks keep 12 warps per SM (3 per SMSP) in this always multi-wave kernel.
-template <bool FMA, bool POLL, bool SOA = false>
-__global__ void __launch_bounds__(128, 3) k_grid_batch(BatchArgs a) {
-    __shared__ int s_src;
-    __shared__ double s_v;
+template <bool FMA, bool POLL, bool SOA>
+__global__ void __launch_bounds__(128, 3) k_grid_pairs(BatchArgs a) {
     __shared__ bool s_last;
-    const int e = a.e0 + (int)blockIdx.z;
-    const int i = blockIdx.y;
+    const int64_t pair = a.p0 + blockIdx.x / (unsigned)a.bpr;
+    const int64_t kb = blockIdx.x % (unsigned)a.bpr;
+    const int e = a.pair_e[pair];
+    const int i = a.pair_i[pair];
+    const double v = a.pair_v[pair];
     const int M = a.m_grid;
-    const double vp = a.v_prev[e], rr = a.r[e];
-    if (threadIdx.x == 0) {
-        const double v = update_setpoint(vp, rr, dvd((double)i, (double)(M - 1)));
-        int src = ss_gate(v, a.p) ? -1 : -2;
-        for (int q = 0; src == -1 && q < i; ++q) {
-            const double vq = update_setpoint(vp, rr, dvd((double)q, (double)(M - 1)));
-            if (ss_gate(vq, a.p) && vq == v) src = q;
-        }
-        s_src = src;
-        s_v = v;
-        if (blockIdx.x == 0) a.row_src[(int64_t)e * M + i] = src;
-    }
-    __syncthreads();
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t k = kb * blockDim.x + threadIdx.x;
     unsigned* viol = a.viol + (int64_t)e * M;
-    if (s_src == -1) {
-        const bool live = k < a.n_sim;
-        int st = kOk;
-        int32_t steps = a.p.j_star;
-        {  // whole warps run the rollout
-            const double* x0 = a.x0 + 3 * (int64_t)e;
-            if constexpr (SOA) {  // staged block of this episode (k_gen_soa_batch)
-                __shared__ double ring[2 * 3 * kRingStride];
-                SoaSource src{a.soa + (int64_t)blockIdx.z * a.ep_stride + (live ? k : 0), a.ld,
-                              ring + threadIdx.x};
-                st = rollout<FMA, POLL, SoaSource, true, false, true>(
-                    make_cell(a.p), x0[0], x0[1], x0[2], s_v, src, steps, viol + i, live);
-            } else {
-                ScenarioStream ss;
-                ss.hs = a.hs[e];
-                for (int c = 0; c < 3; ++c) {
-                    ss.lo[c] = a.lo[c];
-                    ss.span[c] = a.span[c];
-                }
-                RngSource src{ss, scenario_key(ss, (uint64_t)(a.k0 + (live ? k : 0)))};
-                st = rollout<FMA, POLL, RngSource, true, false, true>(
-                    make_cell(a.p), x0[0], x0[1], x0[2], s_v, src, steps, viol + i, live);
+    const bool live = k < a.n_sim;
+    int st = kOk;
+    int32_t steps = a.p.j_star;
+    {  // whole warps run the rollout
+        const double* x0 = a.x0 + 3 * (int64_t)e;
+        if constexpr (SOA) {  // staged block of this episode (k_gen_soa_batch)
+            __shared__ double ring[2 * 3 * kRingStride];
+            SoaSource src{a.soa + (int64_t)(e - a.e0) * a.ep_stride + (live ? k : 0), a.ld,
+                          ring + threadIdx.x};
+            st = rollout<FMA, POLL, SoaSource, true, false, true>(
+                make_cell(a.p), x0[0], x0[1], x0[2], v, src, steps, viol + i, live);
+        } else {
+            ScenarioStream ss;
+            ss.hs = a.hs[e];
+            for (int c = 0; c < 3; ++c) {
+                ss.lo[c] = a.lo[c];
+                ss.span[c] = a.span[c];
             }
+            RngSource src{ss, scenario_key(ss, (uint64_t)(a.k0 + (live ? k : 0)))};
+            st = rollout<FMA, POLL, RngSource, true, false, true>(
+                make_cell(a.p), x0[0], x0[1], x0[2], v, src, steps, viol + i, live);
         }
-        const bool cnt = live;
-        const unsigned bad = __ballot_sync(0xffffffffu, cnt && st != kOk && st != kAbandoned);
-        if (lane_id() == 0 && bad) atomicAdd(viol + i, (unsigned)__popc(bad));
-        warp_count_add(cnt && st != kAbandoned && steps < a.p.j_star, a.early + e);
     }
+    const unsigned bad = __ballot_sync(0xffffffffu, live && st != kOk && st != kAbandoned);
+    if (lane_id() == 0 && bad) atomicAdd(viol + i, (unsigned)__popc(bad));
+    warp_count_add(live && st != kAbandoned && steps < a.p.j_star, a.early + e);
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
-        s_last = atomicAdd(a.ticket + e, 1u) == gridDim.x * gridDim.y - 1;
+        s_last = atomicAdd(a.ticket + e, 1u) == a.expect[e] - 1;
     }
     __syncthreads();
     if (!s_last) return;
     __threadfence();
+    // last block of episode e: extract its best row (governor.py:351-377), apply it
     if (threadIdx.x == 0) {
         const int* rs = a.row_src + (int64_t)e * M;
+        const double vp = a.v_prev[e], rr = a.r[e];
         int best = -1;
         for (int q = 0; q < M; ++q) {
-            const int s = ((volatile const int*)rs)[q];
-            const bool full = s != -2 && ((volatile unsigned*)viol)[s < 0 ? q : s] == 0u;
-            if (a.viol_out)
-                a.viol_out[(int64_t)e * M + q] =
-                    s == -2 ? 0xffffffffu : ((volatile unsigned*)viol)[s < 0 ? q : s];
+            const int s = rs[q];
+            const unsigned vq = s == -2 ? 0xffffffffu : ((volatile unsigned*)viol)[s < 0 ? q : s];
+            const bool full = s != -2 && vq == 0u;
+            if (a.viol_out) a.viol_out[(int64_t)e * M + q] = vq;
             if (a.prefix_mode) {
                 if (best == q - 1 && full) best = q;
             } else if (full) {
@@ -128,23 +114,21 @@ __global__ void __launch_bounds__(128, 3) k_grid_batch(BatchArgs a) {
 // launchers
 // ---------------------------------------------------------------------------
 
-cudaError_t launch_grid_batch(const BatchArgs& a, bool fma, bool poll, cudaStream_t s) {
-    dim3 grid(blocks_for(a.n_sim, a.tpb), (unsigned)a.m_grid, (unsigned)a.n_ep);
-    if (a.soa) {  // staged episode blocks
-        if (fma) {
-            if (poll) k_grid_batch<true, true, true><<<grid, a.tpb, 0, s>>>(a);
-            else      k_grid_batch<true, false, true><<<grid, a.tpb, 0, s>>>(a);
-        } else {
-            if (poll) k_grid_batch<false, true, true><<<grid, a.tpb, 0, s>>>(a);
-            else      k_grid_batch<false, false, true><<<grid, a.tpb, 0, s>>>(a);
-        }
-    } else if (fma) {
-        if (poll) k_grid_batch<true, true, false><<<grid, a.tpb, 0, s>>>(a);
-        else      k_grid_batch<true, false, false><<<grid, a.tpb, 0, s>>>(a);
+cudaError_t launch_grid_batch(const BatchArgs& a, int64_t n_pairs, bool fma, bool poll,
+                              cudaStream_t s) {
+    if (n_pairs <= 0) return cudaSuccess;
+    const int64_t blocks = n_pairs * a.bpr;
+    if (blocks > 0x7fffffffll) return cudaErrorInvalidConfiguration;
+    const dim3 grid((unsigned)blocks);
+#define RG_PAIRS(F, P, S) k_grid_pairs<F, P, S><<<grid, a.tpb, 0, s>>>(a)
+    if (a.soa) {
+        if (fma) { if (poll) RG_PAIRS(true, true, true); else RG_PAIRS(true, false, true); }
+        else     { if (poll) RG_PAIRS(false, true, true); else RG_PAIRS(false, false, true); }
     } else {
-        if (poll) k_grid_batch<false, true, false><<<grid, a.tpb, 0, s>>>(a);
-        else      k_grid_batch<false, false, false><<<grid, a.tpb, 0, s>>>(a);
+        if (fma) { if (poll) RG_PAIRS(true, true, false); else RG_PAIRS(true, false, false); }
+        else     { if (poll) RG_PAIRS(false, true, false); else RG_PAIRS(false, false, false); }
     }
+#undef RG_PAIRS
     return cudaGetLastError();
 }
 

@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <atomic>
 #include <string>
+#include <vector>
 
 #include "../../include/refgov_b200.h"
 #include "rg_kernels.h"
@@ -148,7 +149,11 @@ struct rg_ctx {
     DevBuf b_acc, b_out;
     // batched grid step: inputs, accumulators (zeroed on growth, reset by the kernel), outputs
     int batch_cap = 0;
-    DevBuf e_in, e_viol, e_early, e_src, e_ticket, e_out, e_violout;
+    int64_t batch_cap_m = 0;
+    DevBuf e_in, e_viol, e_early, e_ticket, e_out, e_violout;
+    std::vector<int> b_src;        // host: [E][M] row status of the batched step
+    std::vector<double> b_v;       // host: one episode's candidate setpoints
+    std::vector<int64_t> b_first;  // host: first pair of every episode (E + 1)
     // scratch
     DevBuf dist_raw, soa, S, steps, pbits, rows, vrows, tmp_a, tmp_b, kap_k, fnd_k, cel_k,
         erl_k, path_k, path_o;
@@ -424,7 +429,7 @@ int32_t rg_destroy(rg_ctx* ctx) {
                       &ctx->dist_raw, &ctx->soa, &ctx->S, &ctx->steps, &ctx->pbits, &ctx->rows,
                       &ctx->vrows, &ctx->tmp_a, &ctx->tmp_b, &ctx->kap_k, &ctx->fnd_k,
                       &ctx->cel_k, &ctx->erl_k, &ctx->path_k, &ctx->path_o, &ctx->e_in,
-                      &ctx->e_viol, &ctx->e_early, &ctx->e_src, &ctx->e_ticket, &ctx->e_out,
+                      &ctx->e_viol, &ctx->e_early, &ctx->e_ticket, &ctx->e_out,
                       &ctx->e_violout};
     for (DevBuf* b : bufs) b->release();
     ctx->h_stage.release();
@@ -1029,6 +1034,49 @@ int32_t rg_bisect_joint(rg_ctx* ctx, const rg_problem* prob, const double* x0, d
     return rg_joint_end(ctx, out);
 }
 
+// One episode's candidate rows on the host, exactly as the device (and governor.py:286-317)
+// evaluates them: v_i = update_setpoint(v_prev, r, i/(M-1)), the steady-state gate as the
+// verified setpoint interval, duplicates mapped to the first gated row with the same v.
+// Returns the number of simulated rows; src[i] = -2 gated out, -1 simulated, q duplicate.
+// The setpoints are monotone in i except where rounding at kappa = 1 (exact r) breaks it,
+// so a new value is compared with the previous distinct one and, only once the sequence
+// stops being strictly monotone, with every earlier one.
+static int32_t episode_rows(const rg::ProblemDev& p, double v_prev, double r, int32_t M,
+                            int* src, double* v) {
+    int32_t n = 0, last = -1;
+    int dir = 0;          // +1 / -1 once two distinct gated values were seen
+    bool monotone = true;
+    for (int32_t i = 0; i < M; ++i) {
+        const double vi = rg::update_setpoint(v_prev, r, rg::dvd((double)i, (double)(M - 1)));
+        v[i] = vi;
+        if (!(p.vlo <= vi && vi <= p.vhi)) {  // NaN -> gated out, like ConstraintSet.contains
+            src[i] = -2;
+            continue;
+        }
+        int dup = -1;
+        if (last >= 0) {
+            if (v[last] == vi) {
+                dup = src[last] >= 0 ? src[last] : last;
+            } else {
+                const int d = vi > v[last] ? 1 : -1;
+                if (dir == 0) dir = d;
+                if (d != dir) monotone = false;
+                if (!monotone) {
+                    for (int32_t q = 0; q < i; ++q)
+                        if (src[q] == -1 && v[q] == vi) {
+                            dup = q;
+                            break;
+                        }
+                }
+            }
+        }
+        src[i] = dup;
+        if (dup < 0) ++n;
+        last = i;
+    }
+    return n;
+}
+
 int32_t rg_grid_step_batch(rg_ctx* ctx, const rg_problem* prob, int32_t n_episodes,
                            const double* x0, const double* v_prev, const double* r,
                            const uint64_t* seeds, int64_t k0, int64_t n_sim, const double* lo,
@@ -1039,8 +1087,8 @@ int32_t rg_grid_step_batch(rg_ctx* ctx, const rg_problem* prob, int32_t n_episod
     if (rc) return rc;
     rg::BatchArgs a{};
     if ((rc = make_problem(prob, &a.p))) return rc;
-    if (n_episodes < 1 || n_episodes > 65535)
-        return fail(RG_E_ARGS, "n_episodes must be in [1, 65535], got %d", n_episodes);
+    if (n_episodes < 1 || n_episodes > (1 << 24))
+        return fail(RG_E_ARGS, "n_episodes must be in [1, 2^24], got %d", n_episodes);
     if (m_grid < 2 || m_grid > 65535) return fail(RG_E_ARGS, "m_grid must be in [2, 65535]");
     if (n_sim < 1 || k0 < 0) return fail(RG_E_ARGS, "bad scenario range");
     if (!x0 || !v_prev || !r || !seeds || !lo || !span || !row_out || !kappa_out || !v_out)
@@ -1052,12 +1100,55 @@ int32_t rg_grid_step_batch(rg_ctx* ctx, const rg_problem* prob, int32_t n_episod
             return fail(RG_E_ARGS, "episode %lld: state, v_prev and r must be finite",
                         (long long)e);
     }
-    if (E > ctx->batch_cap || M * E > (int64_t)(ctx->e_viol.bytes / sizeof(unsigned))) {
-        const int64_t cap = std::max<int64_t>(E, 64);
-        const int64_t capm = std::max<int64_t>(E * M, 64 * 32);
-        RG_CUDA(ctx->e_in.ensure(cap * 6 * sizeof(double)));
+    const int tpb = ctx->tune.force_tpb ? ctx->tune.force_tpb : 64;  // always multi-wave
+    const int bpr = (int)((n_sim + tpb - 1) / tpb);
+    // host: every episode's rows, and the compacted pairs (episode-major)
+    ctx->b_src.resize((size_t)E * M);
+    ctx->b_v.resize((size_t)M);
+    ctx->b_first.resize((size_t)E + 1);
+    int64_t P = 0;
+    for (int64_t e = 0; e < E; ++e) {
+        ctx->b_first[e] = P;
+        P += episode_rows(a.p, v_prev[e], r[e], m_grid, ctx->b_src.data() + e * M,
+                          ctx->b_v.data());
+    }
+    ctx->b_first[E] = P;
+    // one pinned staging block, one host-to-device copy:
+    // [x0 3E | v_prev E | r E | hs E | pair_v P] doubles, [row_src E*M | pair_e P | pair_i P |
+    // expect E] 32-bit words
+    const size_t nd = (size_t)E * 6 + (size_t)P;
+    const size_t nw = (size_t)E * M + 2 * (size_t)P + (size_t)E;
+    const size_t in_bytes = nd * sizeof(double) + nw * sizeof(int32_t);
+    const size_t out_bytes = (size_t)E * (3 * sizeof(double) + sizeof(int));
+    const size_t viol_bytes_all = row_viol ? (size_t)E * M * sizeof(unsigned) : 0;
+    RG_CUDA(ctx->h_stage.ensure(in_bytes + out_bytes + viol_bytes_all + 64));
+    double* hd = ctx->h_stage.as<double>();
+    memcpy(hd, x0, (size_t)E * 3 * sizeof(double));
+    memcpy(hd + 3 * E, v_prev, (size_t)E * sizeof(double));
+    memcpy(hd + 4 * E, r, (size_t)E * sizeof(double));
+    uint64_t* hhs = reinterpret_cast<uint64_t*>(hd + 5 * E);
+    for (int64_t e = 0; e < E; ++e) hhs[e] = rg::splitmix64(seeds[e]);
+    double* hpv = hd + 6 * E;
+    int32_t* hw = reinterpret_cast<int32_t*>(hd + nd);
+    memcpy(hw, ctx->b_src.data(), (size_t)E * M * sizeof(int32_t));
+    int32_t* hpe = hw + E * M;
+    int32_t* hpi = hpe + P;
+    uint32_t* hexp = reinterpret_cast<uint32_t*>(hpi + P);
+    for (int64_t e = 0; e < E; ++e) {
+        const int* src = ctx->b_src.data() + e * M;
+        int64_t q = ctx->b_first[e];
+        for (int32_t i = 0; i < M; ++i) {
+            if (src[i] != -1) continue;
+            hpe[q] = (int32_t)e;
+            hpi[q] = i;
+            hpv[q] = rg::update_setpoint(v_prev[e], r[e], rg::dvd((double)i, (double)(M - 1)));
+            ++q;
+        }
+        hexp[e] = (uint32_t)((ctx->b_first[e + 1] - ctx->b_first[e]) * bpr);
+    }
+    if (E > ctx->batch_cap || E * M > ctx->batch_cap_m) {
+        const int64_t cap = std::max<int64_t>(E, 64), capm = std::max<int64_t>(E * M, 64 * 32);
         RG_CUDA(ctx->e_viol.ensure(capm * sizeof(unsigned)));
-        RG_CUDA(ctx->e_src.ensure(capm * sizeof(int)));
         RG_CUDA(ctx->e_violout.ensure(capm * sizeof(unsigned)));
         RG_CUDA(ctx->e_early.ensure(cap * sizeof(unsigned long long)));
         RG_CUDA(ctx->e_ticket.ensure(cap * sizeof(unsigned)));
@@ -1066,23 +1157,21 @@ int32_t rg_grid_step_batch(rg_ctx* ctx, const rg_problem* prob, int32_t n_episod
         RG_CUDA(cudaMemsetAsync(ctx->e_early.p, 0, ctx->e_early.bytes, ctx->stream));
         RG_CUDA(cudaMemsetAsync(ctx->e_ticket.p, 0, ctx->e_ticket.bytes, ctx->stream));
         ctx->batch_cap = (int)cap;
+        ctx->batch_cap_m = capm;
     }
-    // stage inputs: [x0 (3E) | v_prev (E) | r (E) | hs (E)] through pinned memory
-    const size_t in_bytes = (size_t)E * 6 * sizeof(double);
-    RG_CUDA(ctx->h_stage.ensure(in_bytes + (size_t)E * (sizeof(int) + 3 * sizeof(double)) +
-                                (size_t)E * M * sizeof(unsigned)));
-    double* hin = ctx->h_stage.as<double>();
-    memcpy(hin, x0, (size_t)E * 3 * sizeof(double));
-    memcpy(hin + 3 * E, v_prev, (size_t)E * sizeof(double));
-    memcpy(hin + 4 * E, r, (size_t)E * sizeof(double));
-    uint64_t* hhs = reinterpret_cast<uint64_t*>(hin + 5 * E);
-    for (int64_t e = 0; e < E; ++e) hhs[e] = rg::splitmix64(seeds[e]);
-    RG_CUDA(cudaMemcpyAsync(ctx->e_in.p, hin, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
-    double* din = ctx->e_in.as<double>();
+    RG_CUDA(ctx->e_in.ensure(in_bytes));
+    RG_CUDA(cudaMemcpyAsync(ctx->e_in.p, hd, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    const double* din = ctx->e_in.as<double>();
+    const int32_t* dw = reinterpret_cast<const int32_t*>(din + nd);
     a.x0 = din;
     a.v_prev = din + 3 * E;
     a.r = din + 4 * E;
     a.hs = reinterpret_cast<const uint64_t*>(din + 5 * E);
+    a.pair_v = din + 6 * E;
+    a.row_src = dw;
+    a.pair_e = dw + E * M;
+    a.pair_i = a.pair_e + P;
+    a.expect = reinterpret_cast<const unsigned*>(a.pair_i + P);
     a.n_ep = n_episodes;
     a.m_grid = m_grid;
     a.prefix_mode = prefix_mode ? 1 : 0;
@@ -1094,7 +1183,6 @@ int32_t rg_grid_step_batch(rg_ctx* ctx, const rg_problem* prob, int32_t n_episod
     }
     a.viol = ctx->e_viol.as<unsigned>();
     a.early = ctx->e_early.as<unsigned long long>();
-    a.row_src = ctx->e_src.as<int>();
     a.ticket = ctx->e_ticket.as<unsigned>();
     char* dout = ctx->e_out.as<char>();
     a.kappa_out = reinterpret_cast<double*>(dout);
@@ -1102,15 +1190,20 @@ int32_t rg_grid_step_batch(rg_ctx* ctx, const rg_problem* prob, int32_t n_episod
     a.early_out = reinterpret_cast<long long*>(a.v_out + E);
     a.row_out = reinterpret_cast<int*>(a.early_out + E);
     a.viol_out = row_viol ? ctx->e_violout.as<unsigned>() : nullptr;
-    a.tpb = tpb_for(ctx, n_sim * E, m_grid);
+    a.tpb = tpb;
+    a.bpr = bpr;
     const bool fma = ctx->variant == rg::kTanhFma, poll = (flags & RG_ABANDON) != 0;
-    // Staged: each episode's scenario block is generated into SoA once and shared by
-    // its M rows (~20% faster than regenerating it in every cell, as for the single
-    // step); episodes go in chunks of at most 16 GB of SoA.  Fused otherwise.
+    // Scenario source.  Staged, each episode's block is generated once into SoA and
+    // shared by its live rows; fused, every cell hashes its own disturbances.  Staging
+    // pays 48 bytes of HBM traffic per scenario-step on top of the same hashing, so it
+    // wins only when several rows share a block: fused up to 2 live rows per episode
+    // (a closed loop has ~1.05), staged above (the bench snapshot: 32).
     const int64_t ld = (n_sim + 31) / 32 * 32;
     const int64_t ep_stride = (int64_t)prob->j_star * 3 * ld;
     const int64_t per_chunk = kStageMaxScenarioSteps / std::max<int64_t>(1, n_sim * prob->j_star);
-    if (!(flags & RG_FUSED_RNG) && per_chunk >= 1) {
+    const bool staged = !(flags & RG_FUSED_RNG) && per_chunk >= 1 &&
+                        ((flags & RG_STAGE_RNG) || P > 2 * E);
+    if (staged) {
         int64_t ec = std::min<int64_t>(E, per_chunk);
         if (ctx->tune.batch_chunk > 0)  // tests: force several chunks
             ec = std::max<int64_t>(1, std::min<int64_t>(ec, ctx->tune.batch_chunk));
@@ -1119,19 +1212,22 @@ int32_t rg_grid_step_batch(rg_ctx* ctx, const rg_problem* prob, int32_t n_episod
         a.ld = ld;
         a.ep_stride = ep_stride;
         for (int64_t e0 = 0; e0 < E; e0 += ec) {
-            const int32_t n = (int32_t)std::min<int64_t>(ec, E - e0);
-            RG_CUDA(rg::launch_gen_soa_batch(a.hs + e0, lo, span, k0, n_sim, prob->j_star, ld, n,
-                                             ep_stride, ctx->soa.as<double>(), ctx->stream));
+            const int64_t e1 = std::min<int64_t>(E, e0 + ec);
+            const int64_t p0 = ctx->b_first[e0], np = ctx->b_first[e1] - p0;
+            if (np == 0) continue;
+            RG_CUDA(rg::launch_gen_soa_batch(a.hs + e0, lo, span, k0, n_sim, prob->j_star, ld,
+                                             (int32_t)(e1 - e0), ep_stride, ctx->soa.as<double>(),
+                                             ctx->stream));
             a.e0 = (int32_t)e0;
-            a.n_ep = n;
-            RG_CUDA(rg::launch_grid_batch(a, fma, poll, ctx->stream));
+            a.p0 = p0;
+            RG_CUDA(rg::launch_grid_batch(a, np, fma, poll, ctx->stream));
         }
-        a.n_ep = n_episodes;
     } else {
-        RG_CUDA(rg::launch_grid_batch(a, fma, poll, ctx->stream));
+        a.soa = nullptr;
+        a.p0 = 0;
+        RG_CUDA(rg::launch_grid_batch(a, P, fma, poll, ctx->stream));
     }
-    char* hout = reinterpret_cast<char*>(hin + 6 * E);
-    const size_t out_bytes = (size_t)E * (3 * sizeof(double) + sizeof(int));
+    char* hout = reinterpret_cast<char*>(ctx->h_stage.as<char>() + in_bytes);
     RG_CUDA(cudaMemcpyAsync(hout, dout, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
     unsigned* hviol = reinterpret_cast<unsigned*>(hout + out_bytes);
     if (row_viol)
@@ -1139,11 +1235,24 @@ int32_t rg_grid_step_batch(rg_ctx* ctx, const rg_problem* prob, int32_t n_episod
                                 cudaMemcpyDeviceToHost, ctx->stream));
     RG_CUDA(cudaStreamSynchronize(ctx->stream));
     const double* hk = reinterpret_cast<const double*>(hout);
-    memcpy(kappa_out, hk, E * sizeof(double));
-    memcpy(v_out, hk + E, E * sizeof(double));
-    if (early_out) memcpy(early_out, hk + 2 * E, E * sizeof(int64_t));
-    memcpy(row_out, hk + 3 * E, E * sizeof(int32_t));
-    if (row_viol) memcpy(row_viol, hviol, (size_t)E * M * sizeof(unsigned));
+    const long long* he = reinterpret_cast<const long long*>(hk + 2 * E);
+    const int* hr = reinterpret_cast<const int*>(hk + 3 * E);
+    for (int64_t e = 0; e < E; ++e) {
+        if (ctx->b_first[e + 1] > ctx->b_first[e]) {
+            kappa_out[e] = hk[e];
+            v_out[e] = hk[E + e];
+            if (early_out) early_out[e] = he[e];
+            row_out[e] = hr[e];
+            if (row_viol) memcpy(row_viol + e * M, hviol + e * M, (size_t)M * sizeof(unsigned));
+        } else {  // every row gated out: nothing ran, hold (governor.py:562-573)
+            kappa_out[e] = 0.0;
+            v_out[e] = v_prev[e];
+            if (early_out) early_out[e] = 0;
+            row_out[e] = -1;
+            if (row_viol)
+                for (int64_t q = 0; q < M; ++q) row_viol[e * M + q] = 0xffffffffu;
+        }
+    }
     return RG_OK;
 }
 

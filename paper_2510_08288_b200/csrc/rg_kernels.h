@@ -85,8 +85,12 @@ struct GridArgs {
     int no_s2;  // single-wave step without the two-step rollout (A/B and tests)
 };
 
-// Batch of independent governor instances (episodes): one launch covers
-// E episodes x M rows x n_sim scenarios; per-episode arrays are indexed by e.
+// Batch of independent governor instances (episodes).  The host evaluates every
+// episode's candidate rows (setpoint, steady-state gate, dedup -- the reference's
+// governor.py:286-317, same arithmetic as the device) and hands the kernel a compacted
+// list of the (episode, row) pairs that need rollouts: in a closed loop about one row
+// per episode is live, so a launch over E x M x blocks would be
+// ~97% empty blocks.  One launch covers pairs [p0, p0 + gridDim.x / bpr).
 struct BatchArgs {
     ProblemDev p;
     int32_t n_ep, m_grid, prefix_mode;
@@ -96,9 +100,15 @@ struct BatchArgs {
     const double* v_prev;   // [E]
     const double* r;        // [E]
     const uint64_t* hs;     // [E] splitmix64(seed_e)
+    const int* row_src;     // [E][M]: -2 gated out, -1 simulated, >= 0 duplicate of that row
+    const int* pair_e;      // [P] episode of each simulated pair
+    const int* pair_i;      // [P] row of each simulated pair
+    const double* pair_v;   // [P] its setpoint
+    const unsigned* expect; // [E] blocks that report to episode e (its pairs x bpr)
+    int64_t p0;             // first pair of this launch
+    int bpr;                // blocks per pair (ceil(n_sim / tpb))
     unsigned* viol;         // [E][M] accumulators (reset by the last block of e)
     unsigned long long* early;  // [E]
-    int* row_src;           // [E][M]
     unsigned* ticket;       // [E]
     int* row_out;           // [E]
     double* kappa_out;      // [E]
@@ -106,8 +116,8 @@ struct BatchArgs {
     long long* early_out;   // [E]
     unsigned* viol_out;     // [E][M] or null
     int tpb;
-    // staged source (k_gen_soa_batch): episodes [e0, e0 + gridDim.z) of this launch,
-    // episode e's block at soa + (e - e0) * ep_stride, d[(j*3+i)*ld + k]; null: fused RNG
+    // staged source (k_gen_soa_batch): episode e's block at soa + (e - e0) * ep_stride,
+    // d[(j*3+i)*ld + k]; null: fused RNG
     const double* soa;
     int64_t ld, ep_stride;
     int32_t e0;
@@ -235,7 +245,9 @@ cudaError_t launch_gen_soa_batch(const uint64_t* hs, const double* lo, const dou
                                  int64_t k0, int64_t n_sim, int32_t j_star, int64_t ld,
                                  int32_t n_ep, int64_t ep_stride, double* dst, cudaStream_t s);
 cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, cudaStream_t s);
-cudaError_t launch_grid_batch(const BatchArgs& a, bool fma, bool poll, cudaStream_t s);
+// Pairs [a.p0, a.p0 + n_pairs) of the compacted list, a.bpr blocks of a.tpb threads each.
+cudaError_t launch_grid_batch(const BatchArgs& a, int64_t n_pairs, bool fma, bool poll,
+                              cudaStream_t s);
 cudaError_t launch_bisect(const BisectArgs& a, bool fma, int src, cudaStream_t s);
 cudaError_t launch_fill_lin(const LinArgs& a, cudaStream_t s);
 cudaError_t launch_bisect_lin(const LinArgs& a, cudaStream_t s);

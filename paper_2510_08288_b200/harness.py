@@ -165,21 +165,32 @@ def _rk4_batch(h: float, X: np.ndarray, V: np.ndarray) -> np.ndarray:
     return X + (h / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
 
 
-def run_closed_loop_batch(plant, cset, model, config, profile, steps, seeds, x0=None, v0=0.0):
+def run_closed_loop_batch(plant, cset, model, config, profile, steps, seeds, x0=None, v0=0.0,
+                          devices=None):
     """E independent governed closed loops (BASELINE C5), one device launch per step.
 
     Episode e is run_closed_loop(plant, cset, model, config, profile, steps,
     seeds[e]) -- same scenario and plant streams, same arithmetic -- with all
     live episodes' governor steps batched into rg_grid_step_batch and the true
     plants advanced together with numpy.  `profile` is one profile for all
-    episodes or an (E, steps) array of requests.  Returns one RunRecord per
-    episode (rows: t, r_t, v_t, y_t, kappa, feasible, wall_us=0).
+    episodes or an (E, steps) array of requests.  `devices` (default: config.device)
+    spreads the episodes over several GPUs as replicas: contiguous episode ranges, one
+    batched launch per device per step, the devices' calls issued concurrently from
+    host threads (each device has its own context and stream; the C calls release the
+    GIL).  Returns one RunRecord per episode (rows: t, r_t, v_t, y_t, kappa, feasible,
+    wall_us=0).
     """
+    import dataclasses
+    from concurrent.futures import ThreadPoolExecutor
+
     seeds = [int(s_) for s_ in seeds]
     E = len(seeds)
     if steps < 1 or E < 1:
         raise ConfigError("steps and the number of episodes must be >= 1")
-    device = getattr(config, "device", 0)
+    devices = [getattr(config, "device", 0)] if devices is None else [int(d) for d in devices]
+    if not devices:
+        raise ConfigError("devices must be nonempty")
+    device = devices[0]
     X = np.tile(np.zeros(3) if x0 is None else np.asarray(x0, dtype=np.float64), (E, 1))
     Vp = np.full(E, float(v0))
     if isinstance(profile, ReferenceProfile):
@@ -190,30 +201,55 @@ def run_closed_loop_batch(plant, cset, model, config, profile, steps, seeds, x0=
     D = np.stack([_true_disturbance(model, steps, s_, device) for s_ in seeds])
     recs = [RunRecord(rows=[], config={"j_star": config.j_star, "n_sim": config.n_sim,
                                        "m_grid": config.m_grid, "steps": steps,
-                                       "backend": "cuda", "batched": E}, seed=s_)
+                                       "backend": "cuda", "batched": E,
+                                       "devices": list(devices)}, seed=s_)
             for s_ in seeds]
+    # episode e runs on devices[owner[e]]: contiguous ranges, as even as possible
+    owner = (np.arange(E) * len(devices)) // E
+    cfgs = [dataclasses.replace(config, device=d) for d in devices]
+    pool = ThreadPoolExecutor(len(devices)) if len(devices) > 1 else None
     live = np.arange(E)
-    for t in range(steps):
-        if live.size == 0:
-            break
-        kap, v, feas, _ = robust_rg_parallel_batch(
-            plant, X[live], Vp[live], R[live, t], cset, model, config.n_sim,
-            [(int(scen_seeds[e]) + t) for e in live], config)
-        for j, e in enumerate(live):
-            recs[e].rows.append((t, float(R[e, t]), float(v[j]), float(X[e, 0]),
-                                 float(kap[j]), bool(feas[j]), 0))
-        Vp[live] = v
-        Xn = _rk4_batch(plant.step_size, X[live], v)
-        bad = np.any(~np.isfinite(Xn) | (np.abs(Xn) > STATE_LIMIT), axis=1)
-        Xn = Xn + D[live, t]
-        bad2 = np.any(~np.isfinite(Xn) | (np.abs(Xn) > STATE_LIMIT), axis=1)
-        X[live] = Xn
-        for j in np.flatnonzero(bad | bad2):
-            e = live[j]
-            recs[e].aborted = True
-            recs[e].abort_reason = (f"step {t}: integration overflow" if bad[j] else
-                                    f"step {t}: state left the operating box")
-        live = live[~(bad | bad2)]
+
+    def governor(q, idx, t):
+        return robust_rg_parallel_batch(plant, X[idx], Vp[idx], R[idx, t], cset, model,
+                                        config.n_sim, [(int(scen_seeds[e]) + t) for e in idx],
+                                        cfgs[q])
+
+    try:
+        for t in range(steps):
+            if live.size == 0:
+                break
+            parts = [live[owner[live] == q] for q in range(len(devices))]
+            jobs = [(q, idx) for q, idx in enumerate(parts) if idx.size]
+            if pool is None:
+                outs = [governor(q, idx, t) for q, idx in jobs]
+            else:
+                outs = list(pool.map(lambda j: governor(j[0], j[1], t), jobs))
+            kap = np.empty(live.size)
+            v = np.empty(live.size)
+            feas = np.empty(live.size, dtype=bool)
+            pos = {e: j for j, e in enumerate(live)}
+            for (q, idx), (k_, v_, f_, _) in zip(jobs, outs):
+                at = np.array([pos[e] for e in idx])
+                kap[at], v[at], feas[at] = k_, v_, f_
+            for j, e in enumerate(live):
+                recs[e].rows.append((t, float(R[e, t]), float(v[j]), float(X[e, 0]),
+                                     float(kap[j]), bool(feas[j]), 0))
+            Vp[live] = v
+            Xn = _rk4_batch(plant.step_size, X[live], v)
+            bad = np.any(~np.isfinite(Xn) | (np.abs(Xn) > STATE_LIMIT), axis=1)
+            Xn = Xn + D[live, t]
+            bad2 = np.any(~np.isfinite(Xn) | (np.abs(Xn) > STATE_LIMIT), axis=1)
+            X[live] = Xn
+            for j in np.flatnonzero(bad | bad2):
+                e = live[j]
+                recs[e].aborted = True
+                recs[e].abort_reason = (f"step {t}: integration overflow" if bad[j] else
+                                        f"step {t}: state left the operating box")
+            live = live[~(bad | bad2)]
+    finally:
+        if pool is not None:
+            pool.shutdown()
     return recs
 
 

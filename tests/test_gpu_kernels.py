@@ -237,7 +237,7 @@ def test_batch_staged_chunks_equal_fused(ctx, tuned, chunk, abandon):
     ref = ctx.grid_step_batch(prob, X, vp, r, seeds, 7, n, m.lo, m.span, M, abandon=abandon,
                               want_viol=not abandon, fused=True)
     got = ctx.grid_step_batch(prob, X, vp, r, seeds, 7, n, m.lo, m.span, M, abandon=abandon,
-                              want_viol=not abandon)
+                              want_viol=not abandon, staged=True)
     for a, b in zip(ref, got):
         assert np.array_equal(a, b)
 
@@ -375,3 +375,40 @@ def test_concurrent_calls_on_one_context_are_serialised():
             conc = list(ex.map(call, jobs))
         for s_, c_ in zip(serial, conc):
             assert s_[:3] == c_[:3] and np.array_equal(s_[3], c_[3]) and s_[4:] == c_[4:]
+
+
+@pytest.mark.parametrize("rng_mode", ["auto", "fused", "staged"])
+@pytest.mark.parametrize("prefix", [False, True])
+def test_batch_pairs_equal_single_steps(ctx, tuned, rng_mode, prefix):
+    """The compacted batched step (host gate + dedup, one launch over the live (episode,
+    row) pairs) against one rg_grid_step per episode on the same stream: every episode's
+    row, kappa, v, early count and per-row counts -- with episodes whose rows are all
+    duplicates (v_prev == r), all gated out (nothing runs), partly violating, and staged
+    chunks of a few episodes."""
+    rng = np.random.default_rng(77)
+    E, n, M = 41, 333, 32
+    vp = rng.uniform(-1.2, 1.2, E)
+    r = rng.uniform(-3.0, 3.0, E)
+    r[:5] = vp[:5]                      # all rows the same setpoint
+    vp[5:8], r[5:8] = 2.9, 2.95         # every row gated out
+    X = np.stack([[np.tanh(v), v, np.tanh(v) / 2] for v in vp]) + rng.uniform(-0.06, 0.06,
+                                                                               (E, 3))
+    seeds = [int(x) for x in rng.integers(0, 2**63, E)]
+    m = rg.DisturbanceModel.scaled(0.02, 3)
+    prob = _problem(-0.9, 0.9, 0.0, 0.05, 96)
+    if rng_mode == "staged":
+        tuned(batch_chunk=4)
+    kw = {"fused": rng_mode == "fused", "staged": rng_mode == "staged"}
+    row, kap, v, early, viol = ctx.grid_step_batch(prob, X, vp, r, seeds, 5, n, m.lo, m.span, M,
+                                                   prefix_mode=prefix, abandon=False,
+                                                   want_viol=True, **kw)
+    for e in range(E):
+        sc = _capi.make_scenarios(seeds[e], 5, n, m.lo, m.span)
+        res, vi, _ = ctx.grid_step(prob, X[e], vp[e], r[e], M, prefix, None, n, sc, False)
+        assert row[e] == res.row and early[e] == res.early_terms, e
+        assert np.array_equal(viol[e], vi), e
+        k = 0.0 if res.row < 0 else res.row / (M - 1)
+        assert kap[e] == k and v[e] == (vp[e] if res.row < 0 else rg.update_setpoint(vp[e], r[e], k))
+    ab = ctx.grid_step_batch(prob, X, vp, r, seeds, 5, n, m.lo, m.span, M, prefix_mode=prefix,
+                             abandon=True, **kw)
+    assert np.array_equal(ab[0], row) and np.array_equal(ab[1], kap) and np.array_equal(ab[2], v)

@@ -363,3 +363,41 @@ def test_c4_million_scenario_alg2_matches_reference():
             d["early_terms"]) == want
     jt = rg.robust_rg_joint(PLANT, g["x0"], rg.GovernorState(v_prev), r, box, scen, cfg)
     assert (jt.kappa_opt, jt.feasible) == (res.kappa_opt, res.feasible)
+
+
+# ----------------------------------------------------------------- C2 transient variant
+
+def _c2_transient():
+    with np.load(GOLDEN.with_name("c2_transient.npz")) as z:
+        return {k: z[k] for k in z.files}
+
+
+@pytest.mark.parametrize("source", ["generated", "dense"])
+@pytest.mark.parametrize("trial", range(16))
+def test_c2_transient_grid_alg2_joint_match_reference(trial, source):
+    """C2's transient-binding variant at its named size (1000 scenarios, j* = 256, M = 32,
+    scaled(0.02), state off equilibrium; tests/golden/make_c2_transient_golden.py): the
+    device grid step's P, decision and stats, Alg. 2's five numbers and the joint search's
+    kappa / feasible equal the real reference's -- through the public API, with the
+    scenarios generated on the device or passed as a dense host tensor."""
+    g = _c2_transient()
+    n, js, m, nk = int(g["n_sim"]), int(g["j_star"]), int(g["m_grid"]), int(g["n_kappa"])
+    x0, vp, r = g["x0"][trial], float(g["v_prev"][trial]), float(g["r"][trial])
+    scen = rg.sample_scenarios(rg.DisturbanceModel.scaled(float(g["range"]), 3), n, js + 1,
+                               seed=int(g["seed"][trial]))
+    if source == "dense":
+        scen = rg.ScenarioSet(scen.data)
+    box = rg.ConstraintSet(-0.9, 0.9, 0.0)
+    cfg = rg.GovernorConfig(j_star=js, m_grid=m, n_sim=n, n_kappa=nk)
+    res = rg.robust_rg_parallel(PLANT, x0, rg.GovernorState(vp), r, box, scen, cfg)
+    assert np.array_equal(np.packbits(res.matrix, axis=1), g["p_packed"][trial])
+    assert [res.kappa_opt, res.v_applied, float(res.feasible)] == g["grid"][trial].tolist()
+    d = res.diagnostics
+    assert [d["sims_run"], d["early_terms"], d["overflows"], d["ss_pruned_rows"],
+            d["dedup_rows"]] == g["stats"][trial].tolist()
+    seq = rg.robust_rg_sequential(PLANT, x0, rg.GovernorState(vp), r, box, scen, cfg)
+    assert [seq.kappa_opt, seq.v_applied, float(seq.feasible), seq.diagnostics["sims_run"],
+            seq.diagnostics["early_terms"]] == g["seq"][trial].tolist()
+    jt = rg.robust_rg_joint(PLANT, x0, rg.GovernorState(vp), r, box, scen, cfg)
+    assert (jt.kappa_opt, float(jt.feasible)) == (seq.kappa_opt, float(seq.feasible))
+    assert jt.v_applied == seq.v_applied

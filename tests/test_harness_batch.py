@@ -94,3 +94,22 @@ def test_bench_sweep_on_device():
         ("serial", 64, "kernel-only", True), ("serial", 64, "end-to-end", True),
         ("serial", 256, "kernel-only", True), ("serial", 256, "end-to-end", True)]
     assert all(r.min_us > 0 for r in recs if not r.skipped)
+
+
+@pytest.mark.gpu
+def test_closed_loop_batch_over_devices_equals_one_device():
+    """C5's N-device form: episodes split over devices (contiguous ranges, concurrent
+    calls from host threads).  On the one-GPU box the 'devices' are the same GPU listed
+    three times -- the split, the concurrent calls on one context and the merge are the
+    code that runs on 8 GPUs.  Every episode equals the one-device batch and, for two
+    episodes, the single-episode loop."""
+    model = rg.DisturbanceModel.scaled(0.001, 3)
+    cfg = rg.GovernorConfig(n_sim=300)
+    seeds = [2024 + e for e in range(10)]
+    one = run_closed_loop_batch(PLANT, BOX, model, cfg, PROFILE, 700, seeds)
+    many = run_closed_loop_batch(PLANT, BOX, model, cfg, PROFILE, 700, seeds, devices=[0, 0, 0])
+    for a, b in zip(one, many):
+        assert [row[:6] for row in a.rows] == [row[:6] for row in b.rows]
+    for e in (0, 9):
+        single = run_closed_loop(PLANT, BOX, model, cfg, PROFILE, 700, seeds[e])
+        assert [row[:6] for row in many[e].rows] == [row[:6] for row in single.rows]

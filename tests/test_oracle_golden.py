@@ -205,3 +205,31 @@ def test_joint_bisection_equals_alg2_on_reference_cases(orc, golden, idx):
                                           c["upper"], tlo, thi, dist, c["j_star"], c["n_kappa"])
     assert (kappa, float(found)) == (float(c["result"][0]), float(c["result"][2])), c["name"]
     assert len(path) == (1 if path[0][1] else c["n_kappa"] + 1)
+
+
+def _c2_transient():
+    with np.load(GOLDEN.with_name("c2_transient.npz")) as z:
+        return {k: z[k] for k in z.files}
+
+
+@pytest.mark.parametrize("trial", range(16))
+def test_c2_transient_grid_and_alg2_match_reference(orc, trial):
+    """The oracle's grid step and Alg. 2 on the C2 transient-binding variant (1000
+    scenarios, tests/golden/make_c2_transient_golden.py) equal the real reference's."""
+    g = _c2_transient()
+    n, js, m, nk = int(g["n_sim"]), int(g["j_star"]), int(g["m_grid"]), int(g["n_kappa"])
+    rr = float(g["range"])
+    x0, vp, r = g["x0"][trial], float(g["v_prev"][trial]), float(g["r"][trial])
+    d = orc.sample(int(g["seed"][trial]), n, js + 1, [(-rr, rr)] * 3)
+    tlo, thi = orc.tighten(-0.9, 0.9, 0.0, 0.05)
+    k, v, f, _, P, st = orc.grid_step(0.01, x0, vp, r, m, d, -0.9, 0.9, tlo, thi, js,
+                                      workers=orc.cpu_count())
+    assert np.array_equal(np.packbits(P, axis=1), g["p_packed"][trial])
+    assert [k, v, float(f)] == g["grid"][trial].tolist()
+    assert [st["sims_run"], st["early_terms"], st["overflows"], st["ss_pruned_rows"],
+            st["dedup_rows"]] == g["stats"][trial].tolist()
+    ks, vs, fs, cells, early, _ = orc.robust_sequential(0.01, x0, vp, r, -0.9, 0.9, tlo, thi, d,
+                                                        js, nk)
+    assert [ks, vs, float(fs), cells, early] == g["seq"][trial].tolist()
+    kj, fj, _ = orc.joint_bisect(0.01, x0, vp, r, -0.9, 0.9, tlo, thi, d, js, nk)
+    assert (kj, float(fj)) == (ks, float(fs))
