@@ -57,42 +57,50 @@ def _bound(b, default):
     return default if b is None else float(b)
 
 
+def fill_rows(h, x0, v_rows, dist, j_star, lo, hi, slo, shi, device=0):
+    """The runner's fill (backend_gpu.py:50-140 contract): every gated row rolled out
+    against every scenario on the device, P = OK & steady-state gate.  Returns
+    (P, early_terms, kernel_us)."""
+    from . import _capi
+    from .ssgate import admissible_setpoints
+
+    x0 = np.asarray(x0, dtype=np.float64)
+    v_rows = np.ascontiguousarray(v_rows, dtype=np.float64)
+    if dist.shape[2] != 3 or x0.shape != (3,):
+        raise ValueError("the surrogate plant has 3 states")
+    m, n_sim = v_rows.size, dist.shape[0]
+    vlo, vhi = admissible_setpoints(slo, shi)
+    gate = (v_rows >= vlo) & (v_rows <= vhi)
+    rows = np.flatnonzero(gate).astype(np.int32)
+    ctx = _capi.context(int(device))
+    prob = _capi.Problem(float(h), lo, hi, vlo, vhi, int(j_star), 0)
+    S = np.zeros((m, n_sim), dtype=np.uint8)
+    steps = np.zeros((m, n_sim), dtype=np.int32)
+    t1 = time.perf_counter()
+    ctx.fill(prob, x0, v_rows, rows, dist, n_sim, None, S, steps)
+    kernel_us = int((time.perf_counter() - t1) * 1e6)
+    P = (S == 1) & gate[:, None]
+    early = int(np.count_nonzero(steps[rows] < j_star)) if rows.size else 0
+    return P, early, kernel_us
+
+
 def serve(request_path: str) -> int:
     t0 = time.perf_counter()
     req = json.loads(Path(request_path).read_text())
     resp_path = Path(req["response"])
     try:
-        from . import _capi
-        from .ssgate import admissible_setpoints
-
         plant = req["plant"]
         if plant.get("kind") != "surrogate-fc":
             raise ValueError(f"unsupported plant kind {plant.get('kind')!r}")
         h = float(plant.get("step_size", 0.01))
-        x0 = np.asarray(req["x0"], dtype=np.float64)
-        v_rows = np.asarray(req["v_rows"], dtype=np.float64)
-        j_star = int(req["j_star"])
         lo = _bound(req["bounds"]["lower"], -math.inf)
         hi = _bound(req["bounds"]["upper"], math.inf)
         slo = _bound(req["ss_bounds"]["lower"], -math.inf)
         shi = _bound(req["ss_bounds"]["upper"], math.inf)
         dist = read_rgsc(req["scenarios"])
-        if dist.shape[2] != 3 or x0.shape != (3,):
-            raise ValueError("the surrogate plant has 3 states")
-        m, n_sim = v_rows.size, dist.shape[0]
-        vlo, vhi = admissible_setpoints(slo, shi)
-        gate = (v_rows >= vlo) & (v_rows <= vhi)
-        rows = np.flatnonzero(gate).astype(np.int32)
-        ctx = _capi.context(int(req.get("device", 0)))
-        prob = _capi.Problem(h, lo, hi, vlo, vhi, j_star, 0)
-        S = np.zeros((m, n_sim), dtype=np.uint8)
-        steps = np.zeros((m, n_sim), dtype=np.int32)
-        t1 = time.perf_counter()
-        ctx.fill(prob, x0, v_rows, rows, dist, n_sim, None, S, steps)
-        kernel_us = int((time.perf_counter() - t1) * 1e6)
-        P = (S == 1) & gate[:, None]
+        P, early, kernel_us = fill_rows(h, req["x0"], req["v_rows"], dist, int(req["j_star"]), lo,
+                                        hi, slo, shi, int(req.get("device", 0)))
         Path(req["p_out"]).write_bytes(P.astype(np.uint8).tobytes())
-        early = int(np.count_nonzero(steps[rows] < j_star)) if rows.size else 0
         resp = {"ok": True, "kernel_us": kernel_us,
                 "total_us": int((time.perf_counter() - t0) * 1e6), "early_terms": early}
         resp_path.write_text(json.dumps(resp))
