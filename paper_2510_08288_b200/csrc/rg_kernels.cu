@@ -56,9 +56,12 @@ __global__ void k_gen_soa(ScenarioStream st, int64_t k0, int64_t n_sim, int32_t 
     o[2 * ld] = d2;
 }
 
-// tile transpose of [n_sim][horizon][3] (rows j < j_star) into d[(j*3+i)*ld + k]
+// tile transpose of [n_sim][horizon][3] (rows j < j_star) into d[(j*3+i)*ld + k], columns
+// k < ncols (scenarios past n_sim are zero padding); a chunk of scenarios passes src and
+// dst already offset to its first scenario
 __global__ void k_to_soa(const double* __restrict__ src, double* __restrict__ dst,
-                         int64_t n_sim, int64_t horizon, int32_t j_star, int64_t ld) {
+                         int64_t n_sim, int64_t horizon, int32_t j_star, int64_t ld,
+                         int64_t ncols) {
     __shared__ double tile[32][32 * 3 + 1];
     const int64_t k0 = (int64_t)blockIdx.x * 32;
     const int32_t j0 = blockIdx.y * 32;
@@ -78,7 +81,7 @@ __global__ void k_to_soa(const double* __restrict__ src, double* __restrict__ ds
         const int32_t j = j0 + r / 3;
         const int i = r % 3;
         const int64_t k = k0 + threadIdx.x;
-        if (j < j_star && k < ld) dst[((int64_t)j * 3 + i) * ld + k] = tile[threadIdx.x][r];
+        if (j < j_star && k < ncols) dst[((int64_t)j * 3 + i) * ld + k] = tile[threadIdx.x][r];
     }
 }
 
@@ -290,9 +293,10 @@ cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_to_soa(const double* src, double* dst, int64_t n_sim, int64_t horizon,
-                          int32_t j_star, int64_t ld, cudaStream_t s) {
-    dim3 grid((unsigned)((ld + 31) / 32), (unsigned)((j_star + 31) / 32));
-    k_to_soa<<<grid, dim3(32, 8), 0, s>>>(src, dst, n_sim, horizon, j_star, ld);
+                          int32_t j_star, int64_t ld, cudaStream_t s, int64_t ncols) {
+    if (ncols < 0) ncols = ld;
+    dim3 grid((unsigned)((ncols + 31) / 32), (unsigned)((j_star + 31) / 32));
+    k_to_soa<<<grid, dim3(32, 8), 0, s>>>(src, dst, n_sim, horizon, j_star, ld, ncols);
     return cudaGetLastError();
 }
 

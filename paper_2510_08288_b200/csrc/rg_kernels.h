@@ -239,7 +239,7 @@ cudaError_t launch_joint_decide(const JointArgs& a, int it, cudaStream_t s);
 
 cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s);
 cudaError_t launch_to_soa(const double* src, double* dst, int64_t n_sim, int64_t horizon,
-                          int32_t j_star, int64_t ld, cudaStream_t s);
+                          int32_t j_star, int64_t ld, cudaStream_t s, int64_t ncols = -1);
 cudaError_t launch_fill(const FillArgs& a, bool fma, bool rng, cudaStream_t s);
 cudaError_t launch_gen_soa_batch(const uint64_t* hs, const double* lo, const double* span,
                                  int64_t k0, int64_t n_sim, int32_t j_star, int64_t ld,

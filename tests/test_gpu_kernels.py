@@ -412,3 +412,24 @@ def test_batch_pairs_equal_single_steps(ctx, tuned, rng_mode, prefix):
     ab = ctx.grid_step_batch(prob, X, vp, r, seeds, 5, n, m.lo, m.span, M, prefix_mode=prefix,
                              abandon=True, **kw)
     assert np.array_equal(ab[0], row) and np.array_equal(ab[1], kap) and np.array_equal(ab[2], v)
+
+
+@pytest.mark.parametrize("n", [1, 31, 97, 1000, 4099])
+def test_dense_host_tensor_staging_equals_generated(ctx, n):
+    """A caller's dense host tensor goes through pinned staging in chunks of scenarios
+    (parallel host copies, async DMA, per-chunk transposes): every size, including chunk
+    tails and padding, gives the generated stream's bits, twice in a row (staging reuse)."""
+    m = rg.DisturbanceModel.scaled(0.02, 3)
+    prob = _problem(-0.9, 0.9, 0.0, 0.05, 200)
+    x0 = np.array([0.12, 0.3, 0.07])
+    sc = _capi.make_scenarios(4040 + n, 0, n, m.lo, m.span)
+    dense = rg.sample_scenarios(m, n, 201, seed=4040 + n).data
+    ref = ctx.grid_step(prob, x0, 0.3, 2.2, 32, False, None, n, sc, True)
+    for _ in range(2):
+        got = ctx.grid_step(prob, x0, 0.3, 2.2, 32, False, dense, n, None, True)
+        assert got[0].row == ref[0].row and got[0].early_terms == ref[0].early_terms
+        assert np.array_equal(got[1], ref[1]) and np.array_equal(got[2], ref[2])
+    b_ref = ctx.bisect(prob, x0, 0.3, 2.2, 8, None, n, sc)[0]
+    b_got = ctx.bisect(prob, x0, 0.3, 2.2, 8, dense, n, None)[0]
+    assert (b_got.kappa, b_got.found, b_got.cells, b_got.early) == \
+        (b_ref.kappa, b_ref.found, b_ref.cells, b_ref.early)
