@@ -130,26 +130,6 @@ __global__ void __launch_bounds__(256, RG_GRID_MINB) k_joint_roll(JointArgs a, i
 // (timing-dependent) early-termination count of the abandoning search may differ.
 // ---------------------------------------------------------------------------
 
-// Sense-free grid barrier on (count, gen): the last arriver resets count, then bumps
-// gen; the others spin on gen.  Requires every block of the grid to be resident.
-__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, unsigned nblocks) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        volatile unsigned* vgen = gen;
-        const unsigned g = *vgen;
-        __threadfence();
-        if (atomicAdd(count, 1u) == nblocks - 1) {
-            *(volatile unsigned*)count = 0u;
-            __threadfence();
-            atomicAdd(gen, 1u);
-        } else {
-            while (*vgen == g) __nanosleep(32);
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
-
 // The search state between candidates (governor.py:407-431 on the joint verdicts).
 struct Bracket {
     double lo, hi, kopt, kappa, v;  // kappa / v: the candidate waiting for a verdict

@@ -130,6 +130,7 @@ struct Tuning {
     int no_placement = 0;     // single-wave placement off
     int no_pdl = 0;           // grid step not launched with programmatic dependent launch
     int no_step2 = 0;         // single-wave step with the one-step rollout
+    int no_fused_gen = 0;     // single-wave staged step: generator as its own kernel
     int64_t batch_chunk = 0;  // batched step: at most this many staged episodes per chunk
 };
 
@@ -144,7 +145,7 @@ struct rg_ctx {
     // grid-step accumulators and outputs
     int grid_cap = 0;
     int last_m = 0;
-    DevBuf g_viol, g_early, g_ovf, g_aband, g_src, g_ticket, g_t0, g_out;
+    DevBuf g_viol, g_early, g_ovf, g_aband, g_src, g_ticket, g_t0, g_out, g_bar;
     // bisection accumulators and outputs
     DevBuf b_acc, b_out;
     // batched grid step: inputs, accumulators (zeroed on growth, reset by the kernel), outputs
@@ -280,6 +281,7 @@ int32_t grow_grid(rg_ctx* ctx, int m) {
     RG_CUDA(ctx->g_src.ensure(cap * sizeof(int)));
     RG_CUDA(ctx->g_ticket.ensure(sizeof(unsigned)));
     RG_CUDA(ctx->g_t0.ensure(sizeof(unsigned long long)));
+    RG_CUDA(ctx->g_bar.ensure(2 * sizeof(unsigned)));
     RG_CUDA(ctx->g_out.ensure(kOutHead + viol_bytes(cap)));
     RG_CUDA(cudaMemsetAsync(ctx->g_viol.p, 0, ctx->g_viol.bytes, ctx->stream));
     RG_CUDA(cudaMemsetAsync(ctx->g_early.p, 0, ctx->g_early.bytes, ctx->stream));
@@ -287,6 +289,7 @@ int32_t grow_grid(rg_ctx* ctx, int m) {
     RG_CUDA(cudaMemsetAsync(ctx->g_aband.p, 0, ctx->g_aband.bytes, ctx->stream));
     RG_CUDA(cudaMemsetAsync(ctx->g_ticket.p, 0, ctx->g_ticket.bytes, ctx->stream));
     RG_CUDA(cudaMemsetAsync(ctx->g_t0.p, 0xff, ctx->g_t0.bytes, ctx->stream));
+    RG_CUDA(cudaMemsetAsync(ctx->g_bar.p, 0, ctx->g_bar.bytes, ctx->stream));
     RG_CUDA(cudaMemsetAsync(ctx->g_out.p, 0, ctx->g_out.bytes, ctx->stream));
     ctx->grid_cap = cap;
     return RG_OK;
@@ -304,6 +307,7 @@ Tuning env_tuning() {
     if (getenv("RG_NO_PLACEMENT")) t.no_placement = 1;
     if (getenv("RG_NO_PDL")) t.no_pdl = 1;
     if (getenv("RG_NO_STEP2")) t.no_step2 = 1;
+    if (getenv("RG_NO_FUSED_GEN")) t.no_fused_gen = 1;
     if (const char* e = getenv("RG_BATCH_CHUNK")) t.batch_chunk = atoll(e);
     if (!(t.force_tpb == 32 || t.force_tpb == 64 || t.force_tpb == 128)) t.force_tpb = 0;
     return t;
@@ -428,7 +432,7 @@ int32_t rg_destroy(rg_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     DevBuf* bufs[] = {&ctx->g_viol, &ctx->g_early, &ctx->g_ovf, &ctx->g_aband, &ctx->g_src,
-                      &ctx->g_ticket, &ctx->g_t0, &ctx->g_out, &ctx->j_state, &ctx->b_acc, &ctx->b_out,
+                      &ctx->g_ticket, &ctx->g_t0, &ctx->g_out, &ctx->g_bar, &ctx->j_state, &ctx->b_acc, &ctx->b_out,
                       &ctx->dist_raw, &ctx->soa, &ctx->S, &ctx->steps, &ctx->pbits, &ctx->rows,
                       &ctx->vrows, &ctx->tmp_a, &ctx->tmp_b, &ctx->kap_k, &ctx->fnd_k,
                       &ctx->cel_k, &ctx->erl_k, &ctx->path_k, &ctx->path_o, &ctx->e_in,
@@ -457,6 +461,8 @@ int32_t rg_set_option(rg_ctx* ctx, const char* name, int64_t value) {
         t.no_pdl = value != 0;
     } else if (!strcmp(name, "no_step2")) {
         t.no_step2 = value != 0;
+    } else if (!strcmp(name, "no_fused_gen")) {
+        t.no_fused_gen = value != 0;
     } else if (!strcmp(name, "batch_chunk")) {
         if (value < 0) return fail(RG_E_ARGS, "batch_chunk must be >= 0");
         t.batch_chunk = value;
@@ -706,7 +712,24 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
     a.prefix_mode = prefix_mode ? 1 : 0;
     a.n_sim = n_sim;
     bool use_rng = dist == nullptr;
-    if (use_rng && want_stage(n_sim, prob->j_star, flags)) {
+    a.tpb = tpb_for(ctx, n_sim, m_grid);
+    grid_placement(ctx, n_sim, m_grid, &a.tpb, &a.smem_dyn);
+    a.no_s2 = ctx->tune.no_step2;
+    // the single-wave staged step runs the two-step rollout (rg_kernels.cu: launch_grid) and
+    // generates its own scenario block: every block is resident, so a grid barrier can
+    // stand in for the separate generator kernel and its launch
+    const bool single_wave_s2 = a.smem_dyn > 0 && a.tpb <= rg::kRing4Stride && !a.no_s2;
+    if (use_rng && want_stage(n_sim, prob->j_star, flags) && single_wave_s2 &&
+        !ctx->tune.no_fused_gen) {
+        a.ld = (n_sim + 31) / 32 * 32;
+        RG_CUDA(ctx->soa.ensure((size_t)prob->j_star * 3 * a.ld * sizeof(double)));
+        a.soa = a.soa_w = ctx->soa.as<double>();
+        a.stream = make_stream(rng);
+        a.k0 = rng->k0;
+        a.gen = 1;
+        a.bar = ctx->g_bar.as<unsigned>();
+        use_rng = false;
+    } else if (use_rng && want_stage(n_sim, prob->j_star, flags)) {
         if ((rc = stage_rng(ctx, rng, n_sim, prob->j_star, &a.soa, &a.ld))) return rc;
         use_rng = false;
         a.pdl = ctx->tune.no_pdl ? 0 : 1;  // k_gen_soa is the kernel right before
@@ -748,9 +771,6 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
         if (zero_copy && pbits_in_block)
             a.pbits_host = reinterpret_cast<unsigned*>(blk + kOutHead + viol_bytes(m_grid));
     }
-    a.tpb = tpb_for(ctx, n_sim, m_grid);
-    grid_placement(ctx, n_sim, m_grid, &a.tpb, &a.smem_dyn);
-    a.no_s2 = ctx->tune.no_step2;
     const bool timed = !(flags & RG_NO_TIMING);
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
     RG_CUDA(rg::launch_grid(a, ctx->variant == rg::kTanhFma, use_rng, abandon, ctx->stream));

@@ -187,9 +187,30 @@ __global__ void __launch_bounds__(256, RG_GRID_MINB) k_grid(GridArgs a) {
         }
     }
     __syncthreads();
-    // staged scenarios: the generator launched just before may still be running
-    // (programmatic dependent launch); no-op otherwise
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (S2 && a.gen) {
+        // the generator fused in: this block's share of the scenario block (consecutive
+        // threads take consecutive scenarios: coalesced stores), then every block waits
+        // for every share
+        const int64_t total = a.n_sim * a.p.j_star;
+        const int64_t nth = (int64_t)gridDim.x * gridDim.y * blockDim.x;
+        int64_t idx = ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+        for (; idx < total; idx += nth) {
+            const int64_t j = idx / a.n_sim;
+            const int64_t kq = idx - j * a.n_sim;
+            const uint64_t K = scenario_key(a.stream, (uint64_t)(a.k0 + kq));
+            double d0, d1, d2;
+            disturbance_at(a.stream, K, (uint64_t)j, d0, d1, d2);
+            double* o = a.soa_w + j * 3 * a.ld + kq;
+            o[0] = d0;
+            o[a.ld] = d1;
+            o[2 * a.ld] = d2;
+        }
+        grid_barrier(a.bar, a.bar + 1, gridDim.x * gridDim.y);
+    } else {
+        // staged scenarios: the generator launched just before may still be running
+        // (programmatic dependent launch); no-op otherwise
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
     const int src_i = s_src;
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (src_i == -1) {
@@ -246,6 +267,9 @@ __global__ void __launch_bounds__(256, RG_GRID_MINB) k_grid(GridArgs a) {
 
 cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, cudaStream_t s) {
     dim3 grid(blocks_for(a.n_sim, a.tpb), (unsigned)a.m_grid);
+    // the fused generator exists only in the single-wave two-step form
+    if (a.gen && !(a.smem_dyn != 0 && !rng && a.tpb <= kRing4Stride && !a.no_s2))
+        return cudaErrorInvalidValue;
     cudaError_t e = cudaSuccess;
 #define RG_GRID_M(F, R, P, M, S)                                                        \
     do {                                                                                \
@@ -253,7 +277,8 @@ cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, cudaSt
         if ((e = pin_smem((const void*)k_grid<F, R, P, M, S>, a.smem_dyn, &dyn)) !=     \
             cudaSuccess)                                                                \
             break;                                                                      \
-        e = launch_ex(k_grid<F, R, P, M, S>, grid, a.tpb, (size_t)dyn, s, a.pdl != 0, a); \
+        e = launch_ex(k_grid<F, R, P, M, S>, grid, a.tpb, (size_t)dyn, s, a.pdl != 0, a, \
+                      S && a.gen != 0);                                                  \
     } while (0)
     // above one wave (issue-bound) the operand-modifier tanh forms, in one wave over a
     // staged block (latency-bound) the two-step rollout

@@ -83,6 +83,12 @@ struct GridArgs {
     // grid_placement); 0: no pin
     int smem_dyn;
     int no_s2;  // single-wave step without the two-step rollout (A/B and tests)
+    // single-wave staged step with the generator fused in (gen = 1): every block writes its
+    // share of the SoA block to soa_w, then a grid barrier (bar[0] count, bar[1] generation;
+    // cooperative launch, every block resident) before any rollout reads it
+    int gen;
+    double* soa_w;
+    unsigned* bar;
 };
 
 // Batch of independent governor instances (episodes).  The host evaluates every
