@@ -130,7 +130,7 @@ struct Tuning {
     int no_placement = 0;     // single-wave placement off
     int no_pdl = 0;           // grid step not launched with programmatic dependent launch
     int no_step2 = 0;         // single-wave step with the one-step rollout
-    int no_fused_gen = 0;     // single-wave staged step: generator as its own kernel
+    int fused_gen = 0;        // single-wave staged step generates its block itself (grid barrier)
     int64_t batch_chunk = 0;  // batched step: at most this many staged episodes per chunk
 };
 
@@ -307,7 +307,7 @@ Tuning env_tuning() {
     if (getenv("RG_NO_PLACEMENT")) t.no_placement = 1;
     if (getenv("RG_NO_PDL")) t.no_pdl = 1;
     if (getenv("RG_NO_STEP2")) t.no_step2 = 1;
-    if (getenv("RG_NO_FUSED_GEN")) t.no_fused_gen = 1;
+    if (getenv("RG_FUSED_GEN")) t.fused_gen = 1;
     if (const char* e = getenv("RG_BATCH_CHUNK")) t.batch_chunk = atoll(e);
     if (!(t.force_tpb == 32 || t.force_tpb == 64 || t.force_tpb == 128)) t.force_tpb = 0;
     return t;
@@ -461,8 +461,8 @@ int32_t rg_set_option(rg_ctx* ctx, const char* name, int64_t value) {
         t.no_pdl = value != 0;
     } else if (!strcmp(name, "no_step2")) {
         t.no_step2 = value != 0;
-    } else if (!strcmp(name, "no_fused_gen")) {
-        t.no_fused_gen = value != 0;
+    } else if (!strcmp(name, "fused_gen")) {
+        t.fused_gen = value != 0;
     } else if (!strcmp(name, "batch_chunk")) {
         if (value < 0) return fail(RG_E_ARGS, "batch_chunk must be >= 0");
         t.batch_chunk = value;
@@ -715,12 +715,14 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
     a.tpb = tpb_for(ctx, n_sim, m_grid);
     grid_placement(ctx, n_sim, m_grid, &a.tpb, &a.smem_dyn);
     a.no_s2 = ctx->tune.no_step2;
-    // the single-wave staged step runs the two-step rollout (rg_kernels.cu: launch_grid) and
-    // generates its own scenario block: every block is resident, so a grid barrier can
-    // stand in for the separate generator kernel and its launch
+    // Option: the single-wave staged step (the two-step rollout, rg_grid.cu: launch_grid)
+    // generates its own scenario block -- every block is resident, so a grid barrier can
+    // stand in for the separate generator kernel.  Measured slower at C2 (0.1618 vs 0.1583
+    // ms: k_gen_soa behind programmatic dependent launch overlaps the step's prologue,
+    // scripts/ab_fused_gen.py), so it is off by default.
     const bool single_wave_s2 = a.smem_dyn > 0 && a.tpb <= rg::kRing4Stride && !a.no_s2;
     if (use_rng && want_stage(n_sim, prob->j_star, flags) && single_wave_s2 &&
-        !ctx->tune.no_fused_gen) {
+        ctx->tune.fused_gen) {
         a.ld = (n_sim + 31) / 32 * 32;
         RG_CUDA(ctx->soa.ensure((size_t)prob->j_star * 3 * a.ld * sizeof(double)));
         a.soa = a.soa_w = ctx->soa.as<double>();

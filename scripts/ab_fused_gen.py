@@ -1,3 +1,5 @@
+"""A/B of the fused generator in the single-wave C2 step (rg_set_option "fused_gen"): event
+times of 400 L2-flushed steps, three alternations."""
 import sys, time, json
 sys.path.insert(0, '.')
 import numpy as np, torch
@@ -13,7 +15,7 @@ x0 = np.zeros(3); x0p = x0.ctypes.data
 res = _capi.GridResult()
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 def run(opt, steps=400):
-    ctx.set_option("no_fused_gen", opt)
+    ctx.set_option("fused_gen", 1 - opt)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     with torch.cuda.stream(stream):
         for s in range(steps + 20):

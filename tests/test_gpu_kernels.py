@@ -22,7 +22,7 @@ def ctx():
     return _capi.context(0)
 
 
-_DEFAULTS = {"force_tpb": 0, "no_placement": 0, "no_pdl": 0, "no_step2": 0, "no_fused_gen": 0,
+_DEFAULTS = {"force_tpb": 0, "no_placement": 0, "no_pdl": 0, "no_step2": 0, "fused_gen": 0,
              "batch_chunk": 0}
 
 
@@ -281,7 +281,7 @@ def test_grid_fetch_after_sync_and_async_steps(ctx):
 
 
 @pytest.mark.parametrize("opts", [{"no_placement": 1}, {"force_tpb": 32}, {"force_tpb": 128},
-                                  {"no_step2": 1}, {"no_pdl": 1}, {"no_fused_gen": 1}])
+                                  {"no_step2": 1}, {"no_pdl": 1}, {"fused_gen": 1}])
 @pytest.mark.parametrize("shape", [(1000, 32), (300, 32), (4000, 32), (97, 5)])
 def test_single_wave_placement_changes_no_bit(ctx, tuned, opts, shape):
     """The single-wave placement (blocks of 4L warps pinned one per SM, with the
