@@ -14,6 +14,9 @@ scenario-steps/sec vs FP64 roofline", unit cell-steps/s):
       [r*n/N, (r+1)*n/N) of one stream (no scenario traffic); the per-row violation
       counts go through one all-reduce (MAX, int32) per step and every rank extracts
       the same row on its device.
+  c3  (configs[2])  the desk-scale closed loop at 10k scenarios per step, the whole
+      2000-step setpoint trace (seed 2024), governor on the device, true plant on the host;
+      at N>1 every rank runs its own episode (seed 2024 + rank, replicas).
   c5  (configs[4])  4096 independent desk-scale closed-loop episodes x 10k scenarios
       (episode seeds 2024 + e), episodes spread over the N GPUs as replicas; K timed
       closed-loop steps after W warm-up steps of the trace.
@@ -66,6 +69,8 @@ WORKLOADS = {
            "n_per_gpu": 1000, "scaling": "weak", "steps": 3000, "warmup": 20},
     "c4": {"name": "C4: robust grid step (Alg. 3) over 2^20 scenarios sharded across the GPUs",
            "n_total": 1 << 20, "scaling": "strong", "steps": 20, "warmup": 3},
+    "c3": {"name": "C3: desk-scale closed loop, 10k scenarios per step, the whole 2000-step trace",
+           "n_sim": 10_000, "scaling": "weak", "steps": 2000, "warmup": 200},
     "c5": {"name": "C5: 4096 desk-scale closed-loop episodes x 10k scenarios, episodes as "
                    "replicas across the GPUs", "episodes": 4096, "n_sim": 10_000,
            "scaling": "strong", "steps": 5, "warmup": 3},
@@ -78,7 +83,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=None)
     ap.add_argument("--impl", default="own", choices=["own", "reference"])
-    ap.add_argument("--workload", default="auto", choices=["auto", "c2", "c4", "c5"])
+    ap.add_argument("--workload", default="auto", choices=["auto", "c2", "c3", "c4", "c5"])
     ap.add_argument("--n-sim", type=int, default=None,
                     help="c2: scenarios per GPU; c4: total scenarios; c5: scenarios per episode")
     ap.add_argument("--episodes", type=int, default=None, help="c5: total episodes")
@@ -104,11 +109,13 @@ def resolve(args, world):
     args.steps = spec["steps"] if args.steps is None else args.steps
     args.warmup = spec["warmup"] if args.warmup is None else args.warmup
     if args.e2e_steps is None:
-        args.e2e_steps = {"c2": 300, "c4": 5, "c5": 0}[wl]
+        args.e2e_steps = {"c2": 300, "c3": 0, "c4": 5, "c5": 0}[wl]
     if wl == "c2":
         spec["n_per_gpu"] = args.n_sim or spec["n_per_gpu"]
     elif wl == "c4":
         spec["n_total"] = args.n_sim or spec["n_total"]
+    elif wl == "c3":
+        spec["n_sim"] = args.n_sim or spec["n_sim"]
     else:
         spec["n_sim"] = args.n_sim or spec["n_sim"]
         spec["episodes"] = args.episodes or spec["episodes"]
@@ -124,6 +131,11 @@ def config_of(wl, spec, world, j_star):
     if wl == "c4":
         return {"workload": spec["name"], "n_sim": spec["n_total"], "disturbance": "U(+-0.001)",
                 "r": R_REF, **base}
+    if wl == "c3":
+        return {"workload": spec["name"], "n_sim": spec["n_sim"],
+                "disturbance": "U(+-0.001) (desk-scale preset)", "profile": "desk-scale "
+                "[[0,0.4],[400,2.5],[1000,-2.5],[1600,0.2]]", "seed": "2024 (+ rank at N>1)",
+                **base}
     return {"workload": spec["name"], "episodes": spec["episodes"], "n_sim": spec["n_sim"],
             "disturbance": "U(+-0.001) (desk-scale preset)", "profile": "desk-scale "
             "[[0,0.4],[400,2.5],[1000,-2.5],[1600,0.2]]", "seeds": "2024 + e", **base}
@@ -288,8 +300,8 @@ def grid_sample_size(wl, spec, world):
 def cpu_baseline(cpu: RefCPU, wl, spec, world, j_star, seconds):
     """Bounded CPU baseline on rank 0 (about `seconds` of timed work): the grid step on
     every core (best rep), one serial rep, and the sequential entry point."""
-    if wl == "c5":
-        return c5_cpu_baseline(cpu, spec, j_star, seconds)
+    if wl in ("c3", "c5"):
+        return closed_loop_cpu_baseline(cpu, spec, j_star, seconds)
     n = grid_sample_size(wl, spec, world)
     cells = M_GRID * n * j_star
     pool = [cpu.scenarios(n, j_star, BASE_SEED + q) for q in range(4)]
@@ -321,13 +333,14 @@ def cpu_baseline(cpu: RefCPU, wl, spec, world, j_star, seconds):
     }
 
 
-def c5_cpu_baseline(cpu: RefCPU, spec, j_star, seconds):
-    """C5 on the host: the reference's run_closed_loop for one episode (seed 2024) at
-    spec n_sim scenarios, as many closed-loop steps as fit in `seconds` (min 2)."""
+def closed_loop_cpu_baseline(cpu: RefCPU, spec, j_star, seconds):
+    """C3 / C5 on the host: the reference's run_closed_loop for one episode (seed 2024) at
+    spec n_sim scenarios from t = 0, as many closed-loop steps as fit in `seconds` (min 2),
+    after one untimed step (numba JIT, thread pool)."""
     n = spec["n_sim"]
     if cpu.ref is None:
         return {"value": None, "unit": UNIT, "cores": cpu.cores(), "kind": "port",
-                "sample": "the C port has no closed-loop driver; c5 needs the reference"}
+                "sample": "the C port has no closed-loop driver; c3 / c5 need the reference"}
     rf = cpu.ref
     setup = rf.load_config({"governor": {"n_sim": n, "backend": "multicore"}})
     t0 = time.perf_counter()
@@ -343,7 +356,7 @@ def c5_cpu_baseline(cpu: RefCPU, spec, j_star, seconds):
         getattr(rec, "diag_rows", None) else None
     cells = (sims * j_star) if sims else None
     return {"value": (cells / dt) if cells else None, "unit": UNIT, "cores": cpu.cores(),
-            "kind": cpu.kind, "ms_per_closed_loop_step": dt * 1e3 / steps,
+            "kind": cpu.kind, "steps": steps, "ms_per_closed_loop_step": dt * 1e3 / steps,
             "episode_steps_per_s": steps / dt,
             "sample": f"1 episode (seed {setup.seed}) x {steps} closed-loop steps at n_sim={n} "
                       "through refgov.run_closed_loop (host sampling included, as the reference "
@@ -362,11 +375,11 @@ def run_reference(args, rank, world, wl, spec):
     cpu = RefCPU()
     j_star = args.j_star
     config = config_of(wl, spec, world, j_star)
-    if wl == "c5":
-        cb = c5_cpu_baseline(cpu, spec, j_star, min(REF_BUDGET_S, 40.0))
+    if wl in ("c3", "c5"):
+        cb = closed_loop_cpu_baseline(cpu, spec, j_star, min(REF_BUDGET_S, 40.0))
         value = cb["value"]
         line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-                "n_gpus": world, "steps": None, "warmup": 1, "higher_is_better": True,
+                "n_gpus": world, "steps": cb.get("steps"), "warmup": 1, "higher_is_better": True,
                 "scaling": spec["scaling"], "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": config, "cpu_baseline": cb,
                 "ms_per_step": cb.get("ms_per_closed_loop_step"),
@@ -442,6 +455,8 @@ def run_own(args, rank, world, local_rank, wl, spec):
         backend, cpu_group = init_dist(world, local_rank)
     if wl == "c5":
         line = run_c5(args, rank, world, local_rank, spec, backend, cpu_group)
+    elif wl == "c3":
+        line = run_c3(args, rank, world, local_rank, spec, backend, cpu_group)
     else:
         line = run_grid(args, rank, world, local_rank, wl, spec, backend, cpu_group)
     if rank == 0:
@@ -832,6 +847,70 @@ def active_cells(V_prev, R, m_grid, interval):
     return distinct.sum(axis=1)
 
 
+def run_c3(args, rank, world, local_rank, spec, backend, cpu_group):
+    """C3: the reference's desk-scale closed loop (harness.py:138-224) at n_sim scenarios per
+    step through the public API (run_closed_loop: robust_rg_parallel on the device, the true
+    plant on the host).  W untimed closed-loop steps of another episode (seed + 1000), then
+    the timed episode from t = 0 for K steps; host wall clock of the whole loop (it is the
+    latency a controller sees: sampling descriptor, device step, result, plant update), the
+    max over ranks.  Cell-steps = the reference's sims_run x j* summed over the timed steps."""
+    import torch
+
+    import paper_2510_08288_b200 as rg
+    from paper_2510_08288_b200.harness import ReferenceProfile, run_closed_loop
+
+    dev = f"cuda:{local_rank}"
+    n, j_star = spec["n_sim"], args.j_star
+    plant = rg.make_plant("surrogate-fc")
+    box = rg.ConstraintSet(-0.9, 0.9, anchor=0.0)
+    model = rg.DisturbanceModel.scaled(0.001, 3)
+    cfg = rg.GovernorConfig(j_star=j_star, m_grid=M_GRID, n_sim=n, device=local_rank)
+    prof = ReferenceProfile(((0, 0.4), (400, 2.5), (1000, -2.5), (1600, 0.2)))
+    seed = 2024 + rank
+    if args.warmup > 0:
+        run_closed_loop(plant, box, model, cfg, prof, args.warmup, seed + 1000)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    t0 = time.perf_counter()
+    rec = run_closed_loop(plant, box, model, cfg, prof, args.steps, seed)
+    wall = time.perf_counter() - t0
+    clocks = sampler.stop()
+    assert not rec.aborted
+    sims = sum(int(d.split(",")[4]) for d in rec.diag_rows)
+    total = _max_over_ranks(wall, world, dev)
+    if world > 1:
+        t = torch.tensor([sims], dtype=torch.int64, device=dev)
+        torch.distributed.all_reduce(t)
+        sims = int(t.item())
+    value = sims * j_star / total
+    cb = None
+    if world > 1:
+        torch.distributed.barrier()
+    if rank == 0 and not args.no_cpu_baseline:
+        cb = closed_loop_cpu_baseline(RefCPU(), spec, j_star, args.cpu_seconds)
+    if world > 1:
+        torch.distributed.barrier(group=cpu_group)
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": spec["scaling"], "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": config_of("c3", spec, world, j_star),
+        "parallelism": f"one closed-loop episode per GPU x{world} (replicas)",
+        "run": {"violations": rec.violations(box), "sims_run_total": sims,
+                "active_rows_mean": sims / (n * args.steps * world),
+                "timing": "host wall clock of the whole timed closed loop (device governor step, "
+                          "host true-plant step, result readback), max over ranks"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 5 * 8 + 112,
+                "d2h_bytes_per_step": M_GRID * ((n + 31) // 32) * 4 + 64,
+                "note": "the timed loop is the public API end to end (run_closed_loop -> "
+                        "robust_rg_parallel with P returned)"},
+        "roofline": None, "cpu_baseline": cb, "clocks": clocks, "gpu_launches": 2 * args.steps,
+    }
+
+
 def run_c5(args, rank, world, local_rank, spec, backend, cpu_group):
     """C5: the desk-scale closed loop for E episodes (seeds 2024 + e) at n_sim scenarios,
     episodes split over the ranks (replicas, no collective on the data path).  W closed-loop
@@ -900,7 +979,7 @@ def run_c5(args, rank, world, local_rank, spec, backend, cpu_group):
     if world > 1:
         torch.distributed.barrier()
     if rank == 0 and not args.no_cpu_baseline:
-        cb = c5_cpu_baseline(RefCPU(), spec, j_star, args.cpu_seconds)
+        cb = closed_loop_cpu_baseline(RefCPU(), spec, j_star, args.cpu_seconds)
     if world > 1:
         torch.distributed.barrier(group=cpu_group)
     return {
