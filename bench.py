@@ -54,6 +54,11 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+# The multi-rank code path (torch.distributed, the per-step all-reduce) runs when
+# WORLD_SIZE > 1, or at world size 1 with RG_BENCH_FORCE_DIST=1 (NCCL with one rank: the
+# N>1 path exercised end to end on a one-GPU box).  Set in main().
+MULTI = False
+
 METRIC = "robust RG step latency (ms) at N scenarios; scenario-steps/sec vs FP64 roofline"
 UNIT = "cell-steps/s"
 FLOPS_PER_CELL_STEP = 210  # 58 explicit ops + 4 tanh x 38
@@ -436,6 +441,12 @@ def init_dist(world, local_rank):
     import torch.distributed as dist
 
     backend = os.environ.get("RG_BENCH_DIST_BACKEND", "nccl")
+    if "WORLD_SIZE" not in os.environ:  # RG_BENCH_FORCE_DIST at world size 1, no torchrun
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0",
+                          WORLD_SIZE="1", LOCAL_RANK="0")
     if backend == "nccl":
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     else:
@@ -451,7 +462,7 @@ def run_own(args, rank, world, local_rank, wl, spec):
         local_rank = int(os.environ["RG_BENCH_DEVICE"])
     torch.cuda.set_device(local_rank)
     backend, cpu_group = (None, None)
-    if world > 1:
+    if MULTI:
         backend, cpu_group = init_dist(world, local_rank)
     if wl == "c5":
         line = run_c5(args, rank, world, local_rank, spec, backend, cpu_group)
@@ -461,12 +472,12 @@ def run_own(args, rank, world, local_rank, wl, spec):
         line = run_grid(args, rank, world, local_rank, wl, spec, backend, cpu_group)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if MULTI:
         torch.distributed.destroy_process_group()
 
 
 def _max_over_ranks(x: float, world, device) -> float:
-    if world == 1:
+    if not MULTI:
         return float(x)
     import torch
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
@@ -504,19 +515,19 @@ def run_grid(args, rank, world, local_rank, wl, spec, backend, cpu_group):
     res = _capi.GridResult()
     viol = torch.zeros(M_GRID, dtype=torch.int32, device=dev)
     flags = _capi.RG_ASYNC | _capi.RG_NO_TIMING
-    if world > 1:
+    if MULTI:
         flags |= _capi.RG_DEVICE_PTRS
     x0_ptr = x0.ctypes.data_as(_vp())  # kernel parameter: host memory
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     row_idx = torch.arange(M_GRID, dtype=torch.int32, device=dev)
     minus1 = torch.full_like(row_idx, -1)
-    dist = torch.distributed if world > 1 else None
+    dist = torch.distributed if MULTI else None
 
     def launch(s):
         scen = _capi.make_scenarios(BASE_SEED + s, k0, n_rank, model.lo, model.span)
         _capi.check(lib.rg_grid_step(ctx.handle, prob, x0_ptr, 0.0, R_REF, M_GRID, 0, None,
                                      n_rank, 0, scen,
-                                     _vp()(viol.data_ptr()) if world > 1 else None,
+                                     _vp()(viol.data_ptr()) if MULTI else None,
                                      None, res, flags))
 
     def exchange():
@@ -528,10 +539,10 @@ def run_grid(args, rank, world, local_rank, wl, spec, backend, cpu_group):
     with torch.cuda.stream(stream):
         for s in range(args.warmup):
             launch(s)
-            if world > 1:
+            if MULTI:
                 exchange()
         torch.cuda.synchronize()
-        if world > 1:
+        if MULTI:
             dist.barrier()
         sampler = ClockSampler(local_rank)
         sampler.start()
@@ -540,14 +551,14 @@ def run_grid(args, rank, world, local_rank, wl, spec, backend, cpu_group):
               for _ in range(args.steps)]
         best_rows = []
         torch.cuda.synchronize()
-        if world > 1:
+        if MULTI:
             dist.barrier()
         # The timed steps are enqueued in chunks behind a device-side sleep, so the device
         # never idles waiting for the host to submit the next step inside an event pair.
         wall = 0.0
         for c0 in range(0, args.steps, CHUNK):
             c1 = min(args.steps, c0 + CHUNK)
-            if world == 1:
+            if not MULTI:
                 torch.cuda._sleep(int(SLEEP_CYCLES_PER_STEP * (c1 - c0)))
             w0 = time.perf_counter()
             for s in range(c0, c1):
@@ -555,12 +566,12 @@ def run_grid(args, rank, world, local_rank, wl, spec, backend, cpu_group):
                 ev[s][0].record(stream)
                 launch(args.warmup + s)
                 ev[s][1].record(stream)
-                if world > 1:
+                if MULTI:
                     best_rows.append(exchange())
                 ev[s][2].record(stream)
             torch.cuda.synchronize()
             wall += time.perf_counter() - w0
-        if world > 1:
+        if MULTI:
             dist.barrier()
         clocks = sampler.stop()
     per = np.array([a.elapsed_time(c) for a, _, c in ev])  # ms, whole step
@@ -569,7 +580,7 @@ def run_grid(args, rank, world, local_rank, wl, spec, backend, cpu_group):
     total_ms = _max_over_ranks(float(per.sum()), world, dev)
     kernel_ms = _max_over_ranks(float(kern.mean()), world, dev)
     # the step's decision must be the reference's: all 32 rows feasible -> kappa = 1
-    if world == 1:
+    if not MULTI:
         out = _capi.GridResult()
         _capi.check(lib.rg_grid_fetch(ctx.handle, None, M_GRID, out))
         assert out.row == M_GRID - 1 and out.early_terms == 0, (out.row, out.early_terms)
@@ -605,7 +616,7 @@ def run_grid(args, rank, world, local_rank, wl, spec, backend, cpu_group):
                        j_star, dev)
 
     latency = None
-    if world == 1:
+    if not MULTI:
         latency = latency_split(ctx, lib, prob, x0_ptr, model, k0, n_rank)
     else:
         latency = {"allreduce_us_p50": float(np.median(xch) * 1e3),
@@ -617,21 +628,21 @@ def run_grid(args, rank, world, local_rank, wl, spec, backend, cpu_group):
                            "the slowest rank"}
 
     sweep = []
-    if world == 1 and not args.no_sweep:
+    if not MULTI and not args.no_sweep:
         sweep = run_sweep(args, ctx, lib, stream, flush, prob, x0, x0_ptr, model, plant, box,
                           rg, _capi, res, flags, j_star, n_rank, peak, clocks, torch)
 
     cb = None
-    if world > 1:
+    if MULTI:
         torch.distributed.barrier()
     if rank == 0 and not args.no_cpu_baseline:
         cb = cpu_baseline(RefCPU(), wl, spec, world, j_star, args.cpu_seconds)
-    if world > 1:
+    if MULTI:
         torch.distributed.barrier(group=cpu_group)  # gloo: the other ranks block, not spin
 
     par = f"scenario shards x{world}" + (
         f", {backend} all-reduce (MAX) of the int32[{M_GRID}] row counts per step, row "
-        "extracted on every device" if world > 1 else "")
+        "extracted on every device" if MULTI else "")
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -657,7 +668,7 @@ def e2e_grid(args, rank, world, local_rank, rg, plant, box, model, n_total, n_ra
     """The same step through the public API with host inputs, the result on the host."""
     import torch
 
-    if world == 1:
+    if not MULTI:
         cfg = rg.GovernorConfig(j_star=j_star, m_grid=M_GRID, n_sim=n_rank, device=local_rank)
         for s in range(5):
             rg.robust_rg_parallel(plant, np.zeros(3), rg.GovernorState(0.0), R_REF, box,
@@ -870,7 +881,7 @@ def run_c3(args, rank, world, local_rank, spec, backend, cpu_group):
     if args.warmup > 0:
         run_closed_loop(plant, box, model, cfg, prof, args.warmup, seed + 1000)
     torch.cuda.synchronize()
-    if world > 1:
+    if MULTI:
         torch.distributed.barrier()
     sampler = ClockSampler(local_rank)
     sampler.start()
@@ -881,17 +892,17 @@ def run_c3(args, rank, world, local_rank, spec, backend, cpu_group):
     assert not rec.aborted
     sims = sum(int(d.split(",")[4]) for d in rec.diag_rows)
     total = _max_over_ranks(wall, world, dev)
-    if world > 1:
+    if MULTI:
         t = torch.tensor([sims], dtype=torch.int64, device=dev)
         torch.distributed.all_reduce(t)
         sims = int(t.item())
     value = sims * j_star / total
     cb = None
-    if world > 1:
+    if MULTI:
         torch.distributed.barrier()
     if rank == 0 and not args.no_cpu_baseline:
         cb = closed_loop_cpu_baseline(RefCPU(), spec, j_star, args.cpu_seconds)
-    if world > 1:
+    if MULTI:
         torch.distributed.barrier(group=cpu_group)
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -954,7 +965,7 @@ def run_c5(args, rank, world, local_rank, spec, backend, cpu_group):
         v, X, _ = step(t)
         Vp = v
     torch.cuda.synchronize()
-    if world > 1:
+    if MULTI:
         torch.distributed.barrier()
     sampler = ClockSampler(local_rank)
     sampler.start()
@@ -968,7 +979,7 @@ def run_c5(args, rank, world, local_rank, spec, backend, cpu_group):
     clocks = sampler.stop()
     total = _max_over_ranks(sum(times), world, dev)
     acts_all = acts
-    if world > 1:
+    if MULTI:
         t = torch.tensor([acts], dtype=torch.int64, device=dev)
         torch.distributed.all_reduce(t)
         acts_all = int(t.item())
@@ -976,11 +987,11 @@ def run_c5(args, rank, world, local_rank, spec, backend, cpu_group):
     value = cells / total
     ms = total * 1e3 / args.steps
     cb = None
-    if world > 1:
+    if MULTI:
         torch.distributed.barrier()
     if rank == 0 and not args.no_cpu_baseline:
         cb = closed_loop_cpu_baseline(RefCPU(), spec, j_star, args.cpu_seconds)
-    if world > 1:
+    if MULTI:
         torch.distributed.barrier(group=cpu_group)
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -1055,6 +1066,8 @@ def main():
     if "WORLD_SIZE" in os.environ and args.gpus != world:
         print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
         sys.exit(2)
+    global MULTI
+    MULTI = world > 1 or os.environ.get("RG_BENCH_FORCE_DIST") == "1"
     wl, spec = resolve(args, world)
     if args.impl == "reference":
         run_reference(args, rank, world, wl, spec)
