@@ -387,8 +387,14 @@ def _robust_rg_parallel_via_fill(plant, x_t, state, r_t, cset, scenarios, config
     return KappaResult(kappa_opt=kappa, v_applied=v, feasible=True, diagnostics=stats, matrix=P)
 
 
-def robust_rg_parallel(plant, x_t, state, r_t, cset, scenarios, config, backend=None):
-    """Scenario-robust governor step by grid search (governor.py:520-579)."""
+def robust_rg_parallel(plant, x_t, state, r_t, cset, scenarios, config, backend=None,
+                       _matrix=None):
+    """Scenario-robust governor step by grid search (governor.py:520-579).
+
+    ``_matrix`` (internal): override config.keep_matrix for the matrix only -- False skips P
+    but keeps every rollout to its end, so the diagnostics stay the reference's (the closed
+    loop, which never reads P, uses it).
+    """
     x_t = _validate_state(plant, x_t)
     backend = backend or config.backend
     _backend_check(backend)
@@ -407,9 +413,11 @@ def robust_rg_parallel(plant, x_t, state, r_t, cset, scenarios, config, backend=
 
     t0 = time.perf_counter()
     ctx = _capi.context(device)
+    want_p = keep if _matrix is None else bool(_matrix)
     res, viol, pbits = ctx.grid_step(prob, x_t, state.v_prev, r_t, config.m_grid,
-                                     config.prefix_mode, dist, n_sim, stream, want_pbits=keep,
+                                     config.prefix_mode, dist, n_sim, stream, want_pbits=want_p,
                                      abandon=not keep, timing=False, want_viol=False)
+    keep = want_p
     n_dup = 0
     if res.ss_pruned_rows or res.dedup_rows:
         # rows the device gated or deduplicated: the host's loop (governor.py:302-317)

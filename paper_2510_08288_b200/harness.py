@@ -107,7 +107,8 @@ def run_closed_loop(plant, cset, model, config, profile, steps, seed, governor_o
             scen = sample_scenarios(model, config.n_sim, config.j_star + 1, seed=scen_seed + t,
                                     device=device)
             t0 = time.perf_counter()
-            res = robust_rg_parallel(plant, x, state, r_t, cset, scen, config)
+            # the loop never reads P: skip it, keep the reference's diagnostics
+            res = robust_rg_parallel(plant, x, state, r_t, cset, scen, config, _matrix=False)
             wall_us = int((time.perf_counter() - t0) * 1e6)
             v_t, kappa, feas = res.v_applied, res.kappa_opt, res.feasible
             rec.diag_rows.append(res.diagnostics_csv_row(t))
