@@ -174,8 +174,7 @@ __device__ __forceinline__ bool in_subtree(int y, int root) {  // heap order
     return y == root;
 }
 
-// MOD: the operand-modifier tanh forms (rg_math.cuh) in the rollouts.
-template <bool FMA, int SRC, bool MOD>  // SRC: 0 zero (nominal), 1 rng, 2 soa
+template <bool FMA, int SRC>  // SRC: 0 zero (nominal), 1 rng, 2 soa
 __global__ void __launch_bounds__(256, 1) k_joint_spec(JointArgs a) {
     JointState* st = a.st;
     const unsigned lane = threadIdx.x & 31u;
@@ -239,14 +238,14 @@ __global__ void __launch_bounds__(256, 1) k_joint_spec(JointArgs a) {
                 int stt;
                 if constexpr (SRC == 1) {
                     RngSource src{a.stream, scenario_key(a.stream, (uint64_t)(a.k0 + kk))};
-                    stt = rollout<FMA, true, RngSource, true, true, MOD>(c, a.x0[0], a.x0[1], a.x0[2],
+                    stt = rollout<FMA, true, RngSource, true, true>(c, a.x0[0], a.x0[1], a.x0[2],
                                                                      v, src, steps, poll, live);
                 } else if constexpr (SRC == 2) {
                     SoaSource src{a.soa + kk, a.ld, ring + threadIdx.x};
-                    stt = rollout<FMA, true, SoaSource, true, true, MOD>(c, a.x0[0], a.x0[1], a.x0[2],
+                    stt = rollout<FMA, true, SoaSource, true, true>(c, a.x0[0], a.x0[1], a.x0[2],
                                                                      v, src, steps, poll, live);
                 } else {
-                    stt = rollout<FMA, true, ZeroSource, true, true, MOD>(c, a.x0[0], a.x0[1],
+                    stt = rollout<FMA, true, ZeroSource, true, true>(c, a.x0[0], a.x0[1],
                                                                       a.x0[2], v, ZeroSource{},
                                                                       steps, poll, live);
                 }
@@ -493,11 +492,12 @@ cudaError_t launch_joint_spec(const JointArgs& a, bool fma, int src, int sm_coun
                               cudaStream_t s) {
     constexpr int kThreads = 256;
     const void* fn;
-#define RG_JS(F, M) (src == 1 ? (const void*)k_joint_spec<F, 1, M> \
-                   : src == 2 ? (const void*)k_joint_spec<F, 2, M> : (const void*)k_joint_spec<F, 0, M>)
-    if (fma) fn = a.mod ? RG_JS(true, true) : RG_JS(true, false);
-    else fn = a.mod ? RG_JS(false, true) : RG_JS(false, false);
-#undef RG_JS
+    if (fma) fn = src == 1 ? (const void*)k_joint_spec<true, 1>
+                           : src == 2 ? (const void*)k_joint_spec<true, 2>
+                                      : (const void*)k_joint_spec<true, 0>;
+    else fn = src == 1 ? (const void*)k_joint_spec<false, 1>
+                       : src == 2 ? (const void*)k_joint_spec<false, 2>
+                                  : (const void*)k_joint_spec<false, 0>;
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0);
     if (e != cudaSuccess) return e;

@@ -131,7 +131,6 @@ struct Tuning {
     int no_pdl = 0;           // grid step not launched with programmatic dependent launch
     int no_step2 = 0;         // single-wave step with the one-step rollout
     int fused_gen = 0;        // single-wave staged step generates its block itself (grid barrier)
-    int joint_mod = 0;        // persistent joint search: operand-modifier tanh forms
     int64_t batch_chunk = 0;  // batched step: at most this many staged episodes per chunk
 };
 
@@ -309,7 +308,6 @@ Tuning env_tuning() {
     if (getenv("RG_NO_PDL")) t.no_pdl = 1;
     if (getenv("RG_NO_STEP2")) t.no_step2 = 1;
     if (getenv("RG_FUSED_GEN")) t.fused_gen = 1;
-    if (const char* e = getenv("RG_JOINT_MOD")) t.joint_mod = atoi(e) != 0;
     if (const char* e = getenv("RG_BATCH_CHUNK")) t.batch_chunk = atoll(e);
     if (!(t.force_tpb == 32 || t.force_tpb == 64 || t.force_tpb == 128)) t.force_tpb = 0;
     return t;
@@ -465,8 +463,6 @@ int32_t rg_set_option(rg_ctx* ctx, const char* name, int64_t value) {
         t.no_step2 = value != 0;
     } else if (!strcmp(name, "fused_gen")) {
         t.fused_gen = value != 0;
-    } else if (!strcmp(name, "joint_mod")) {
-        t.joint_mod = value != 0;
     } else if (!strcmp(name, "batch_chunk")) {
         if (value < 0) return fail(RG_E_ARGS, "batch_chunk must be >= 0");
         t.batch_chunk = value;
@@ -1050,7 +1046,6 @@ int32_t rg_bisect_joint(rg_ctx* ctx, const rg_problem* prob, const double* x0, d
     if (!(flags & RG_JOINT_ITER) && depth > 0 && n_kappa + 1 <= rg::kJointMaxRounds) {
         // the whole search in one cooperative launch, speculating `depth` levels per round
         ctx->j_args.depth = depth;
-        ctx->j_args.mod = ctx->tune.joint_mod;
         const cudaError_t e = rg::launch_joint_spec(ctx->j_args, ctx->variant == rg::kTanhFma,
                                                     ctx->j_src, ctx->sm_count, ctx->stream);
         if (e != cudaSuccess) {

@@ -230,7 +230,6 @@ struct JointArgs {
     int smem_dyn;  // shared memory per block, static + dynamic (single-wave placement pin)
     int fold;  // 1: the last block decides (single GPU); 0: k_joint_decide after the all-reduce
     int depth;  // persistent search: speculation depth (1..3): 2^depth - 1 candidates per round
-    int mod;    // persistent search: the operand-modifier tanh forms
 };
 
 cudaError_t launch_joint_roll(const JointArgs& a, int it, bool fma, int src, cudaStream_t s);
