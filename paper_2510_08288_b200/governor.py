@@ -430,9 +430,9 @@ def robust_rg_parallel(plant, x_t, state, r_t, cset, scenarios, config, backend=
     P = None
     if keep:
         # pruned and duplicate rows come back as zero bits; duplicates copy their source
-        # one flat unpack (row-major, little-endian words) is cheaper than axis=1
-        P = np.unpackbits(pbits.view(np.uint8).ravel(), bitorder="little")
-        P = P.reshape(pbits.shape[0], -1)[:, :n_sim].view(np.bool_)
+        # (little-endian words: bit k % 32 of word k / 32 is byte-bit k % 8 of byte k / 8)
+        P = np.unpackbits(pbits.view(np.uint8), axis=1, count=n_sim,
+                          bitorder="little").view(np.bool_)
         if n_dup:
             for i, src in enumerate(dup_src):
                 if src >= 0:
