@@ -897,6 +897,9 @@ def run_c3(args, rank, world, local_rank, spec, backend, cpu_group):
         torch.distributed.all_reduce(t)
         sims = int(t.item())
     value = sims * j_star / total
+    roof = wall_roofline(value / world, local_rank,
+                         "host wall clock of the closed loop per GPU (device step, result "
+                         "readback, host true-plant step): a lower bound on the kernels' rate")
     cb = None
     if MULTI:
         torch.distributed.barrier()
@@ -918,7 +921,7 @@ def run_c3(args, rank, world, local_rank, spec, backend, cpu_group):
                 "d2h_bytes_per_step": M_GRID * ((n + 31) // 32) * 4 + 64,
                 "note": "the timed loop is the public API end to end (run_closed_loop -> "
                         "robust_rg_parallel with P returned)"},
-        "roofline": None, "cpu_baseline": cb, "clocks": clocks, "gpu_launches": 2 * args.steps,
+        "roofline": roof, "cpu_baseline": cb, "clocks": clocks, "gpu_launches": 2 * args.steps,
     }
 
 
@@ -986,6 +989,10 @@ def run_c5(args, rank, world, local_rank, spec, backend, cpu_group):
     cells = acts_all * n * j_star  # the reference's sims_run x j* over all episodes and steps
     value = cells / total
     ms = total * 1e3 / args.steps
+    roof = wall_roofline(value / world, local_rank,
+                         "host wall clock per GPU of the batched governor call (host compaction, "
+                         "copies, k_grid_pairs) plus the host true-plant step",
+                         _ncu_summary("r02_k_grid_pairs_512_ncu.json"))
     cb = None
     if MULTI:
         torch.distributed.barrier()
@@ -1009,12 +1016,28 @@ def run_c5(args, rank, world, local_rank, spec, backend, cpu_group):
                 "d2h_bytes_per_step": E_total * 28,
                 "note": "the timed loop already runs through the public API "
                         "(robust_rg_parallel_batch) with host inputs and host results"},
-        "roofline": None, "cpu_baseline": cb, "clocks": clocks,
-        "gpu_launches": None,
+        "roofline": roof, "cpu_baseline": cb, "clocks": clocks,
+        "gpu_launches": args.steps,
     }
 
 
 # ---------------------------------------------------------------- ncu summaries
+
+def wall_roofline(rate_per_gpu, device, timing, ncu=None):
+    """The FP64 roofline fraction of a wall-clock rate (closed loops: the host is in the loop)."""
+    from paper_2510_08288_b200 import _capi
+
+    peak = _capi.context(device).fp64_peak()
+    achieved = FLOPS_PER_CELL_STEP * rate_per_gpu
+    out = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
+           "frac": achieved / peak, "traffic": (ncu or {}).get("dram_bytes_per_launch"),
+           "flops_per_cell_step": FLOPS_PER_CELL_STEP, "timing": timing,
+           "peak_source": "measured in this run: rg_fp64_peak (independent DFMA chains)"}
+    if ncu:
+        out["ncu"] = {k: ncu.get(k) for k in ("workload", "fp64_instr_per_cell_step",
+                                               "instr_per_cell_step", "fp64_pipe_pct_of_peak")}
+    return out
+
 
 def _ncu_summary(name="k_grid_ncu.json"):
     """A committed ncu --set full summary of k_grid (scripts/ncu_summary.py): at C2

@@ -36,7 +36,7 @@ def test_config_is_shared_by_both_arms():
     sys.path.insert(0, str(ROOT))
     import bench
 
-    for wl in ("c2", "c4", "c5"):
+    for wl in ("c2", "c3", "c4", "c5"):
         spec = dict(bench.WORKLOADS[wl])
         a = bench.config_of(wl, spec, 4, 256)
         b = bench.config_of(wl, dict(spec), 4, 256)

@@ -113,3 +113,21 @@ def test_closed_loop_batch_over_devices_equals_one_device():
     for e in (0, 9):
         single = run_closed_loop(PLANT, BOX, model, cfg, PROFILE, 700, seeds[e])
         assert [row[:6] for row in many[e].rows] == [row[:6] for row in single.rows]
+
+
+@pytest.mark.gpu
+def test_batch_step_infeasible_policy_error():
+    """robust_rg_parallel_batch honours infeasible_policy="error" like the single call
+    (governor.py:562-573): an episode with no feasible candidate raises InfeasibleError."""
+    model = rg.DisturbanceModel.scaled(0.02, 3)
+    X = np.array([[0.0, 0.0, 0.0], [2.0, 0.0, 0.0]])   # episode 1 starts outside the set
+    for policy, raises in (("hold", False), ("error", True)):
+        cfg = rg.GovernorConfig(j_star=64, m_grid=8, n_sim=50, infeasible_policy=policy)
+        if raises:
+            with pytest.raises(rg.InfeasibleError):
+                rg.robust_rg_parallel_batch(PLANT, X, np.zeros(2), np.full(2, 0.5), BOX, model,
+                                            50, [1, 2], cfg)
+        else:
+            kap, v, feas, _ = rg.robust_rg_parallel_batch(PLANT, X, np.zeros(2), np.full(2, 0.5),
+                                                          BOX, model, 50, [1, 2], cfg)
+            assert feas.tolist() == [True, False] and v[1] == 0.0

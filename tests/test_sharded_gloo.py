@@ -175,3 +175,41 @@ def test_extract_row_matches_reference_extraction():
             row, _ = extract_kappa_opt(P, prefix_mode=prefix)
             got = extract_row(counts.astype(np.int64), dup, prefix)
             assert (None if row is None else row - 1) == got
+
+
+def _worker_empty(rank, world, port, out_dir):
+    sys.path.insert(0, str(ROOT))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+
+    import paper_2510_08288_b200 as rg
+    from paper_2510_08288_b200 import sharded
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    plant = rg.make_plant("surrogate-fc")
+    box = rg.ConstraintSet(-0.9, 0.9)
+    scen = rg.sample_scenarios(rg.DisturbanceModel.scaled(0.01, 3), 1, 33, seed=1)
+    cfg = rg.GovernorConfig(j_star=32, m_grid=8, n_sim=1)
+    raised = []
+    for fn in (sharded.robust_rg_parallel_sharded, sharded.robust_rg_sequential_sharded,
+               sharded.robust_rg_joint_sharded):
+        try:
+            fn(plant, np.zeros(3), rg.GovernorState(0.0), 0.5, box, scen, cfg,
+               **({"local_step": lambda sh: None} if fn is not sharded.robust_rg_joint_sharded
+                  else {"shard_impl": object()}))
+        except rg.ConfigError:
+            raised.append(1)
+    dist.barrier()  # every rank got here: nobody was left waiting in a collective
+    np.save(Path(out_dir) / f"empty{rank}.npy", np.array(raised))
+    dist.destroy_process_group()
+
+
+def test_empty_shards_rejected_on_every_rank(tmp_path):
+    """n_sim < world: every rank raises ConfigError before any collective."""
+    import torch.multiprocessing as mp
+
+    mp.start_processes(_worker_empty, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True,
+                       start_method="spawn")
+    for r in (0, 1):
+        assert np.load(tmp_path / f"empty{r}.npy").tolist() == [1, 1, 1]
