@@ -609,13 +609,17 @@ int32_t rg_fill(rg_ctx* ctx, const rg_problem* prob, const double* x0, const dou
     RG_CUDA(rg::launch_fill(a, ctx->variant == rg::kTanhFma, use_rng, ctx->stream));
     RG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     if (!(flags & RG_DEVICE_PTRS)) {
-        // copy back only the active rows: the caller's other rows stay untouched
-        for (int32_t q = 0; q < n_rows; ++q) {
-            const int64_t off = (int64_t)rows[q] * n_sim;
-            RG_CUDA(cudaMemcpyAsync(S + off, a.S + off, n_sim, cudaMemcpyDeviceToHost,
-                                    ctx->stream));
-            RG_CUDA(cudaMemcpyAsync(steps + off, a.steps + off, n_sim * sizeof(int32_t),
+        // copy back only the active rows (the caller's other rows stay untouched), one copy
+        // per run of consecutive rows: the reference's active rows are ascending and mostly
+        // contiguous, so a 32-row fill is one or two copies instead of 64
+        for (int32_t q = 0; q < n_rows;) {
+            int32_t e = q + 1;
+            while (e < n_rows && rows[e] == rows[e - 1] + 1) ++e;
+            const int64_t off = (int64_t)rows[q] * n_sim, cnt = (int64_t)(e - q) * n_sim;
+            RG_CUDA(cudaMemcpyAsync(S + off, a.S + off, cnt, cudaMemcpyDeviceToHost, ctx->stream));
+            RG_CUDA(cudaMemcpyAsync(steps + off, a.steps + off, cnt * sizeof(int32_t),
                                     cudaMemcpyDeviceToHost, ctx->stream));
+            q = e;
         }
     }
     if (!(flags & RG_ASYNC)) RG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1390,11 +1394,14 @@ int32_t rg_fill_linear(rg_ctx* ctx, const rg_linear_plant* plant, const rg_probl
     a.steps = ctx->steps.as<int32_t>();
     a.tpb = tpb_for(ctx, n_sim, n_rows);
     RG_CUDA(rg::launch_fill_lin(a, ctx->stream));
-    for (int32_t q = 0; q < n_rows; ++q) {
-        const int64_t off = (int64_t)rows[q] * n_sim;
-        RG_CUDA(cudaMemcpyAsync(S + off, a.S + off, n_sim, cudaMemcpyDeviceToHost, ctx->stream));
-        RG_CUDA(cudaMemcpyAsync(steps + off, a.steps + off, n_sim * sizeof(int32_t),
+    for (int32_t q = 0; q < n_rows;) {  // one copy per run of consecutive active rows
+        int32_t e = q + 1;
+        while (e < n_rows && rows[e] == rows[e - 1] + 1) ++e;
+        const int64_t off = (int64_t)rows[q] * n_sim, cnt = (int64_t)(e - q) * n_sim;
+        RG_CUDA(cudaMemcpyAsync(S + off, a.S + off, cnt, cudaMemcpyDeviceToHost, ctx->stream));
+        RG_CUDA(cudaMemcpyAsync(steps + off, a.steps + off, cnt * sizeof(int32_t),
                                 cudaMemcpyDeviceToHost, ctx->stream));
+        q = e;
     }
     RG_CUDA(cudaStreamSynchronize(ctx->stream));
     return RG_OK;
