@@ -631,6 +631,28 @@ def run_grid(args, rank, world, local_rank, wl, spec, backend, cpu_group):
     if not MULTI and not args.no_sweep:
         sweep = run_sweep(args, ctx, lib, stream, flush, prob, x0, x0_ptr, model, plant, box,
                           rg, _capi, res, flags, j_star, n_rank, peak, clocks, torch)
+    one_gpu = None
+    if MULTI and wl == "c4" and rank == 0:
+        # the whole c4 step on rank 0's GPU alone (no shard, no exchange), same run: the
+        # one-GPU point of this workload, beside the N-GPU value
+        ts = []
+        with torch.cuda.stream(stream):
+            for s_i in range(4):
+                flush.zero_()
+                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_.record(stream)
+                sc = _capi.make_scenarios(BASE_SEED + 77 + s_i, 0, n_total, model.lo, model.span)
+                _capi.check(lib.rg_grid_step(ctx.handle, prob, x0_ptr, 0.0, R_REF, M_GRID, 0, None,
+                                             n_total, 0, sc, None, None, res,
+                                             _capi.RG_ASYNC | _capi.RG_NO_TIMING))
+                b_.record(stream)
+                torch.cuda.synchronize()
+                if s_i:
+                    ts.append(a_.elapsed_time(b_))
+        one_gpu = {"n_sim": n_total, "ms_per_step": float(np.mean(ts)),
+                   "value": cells_step / (float(np.mean(ts)) * 1e-3), "unit": UNIT,
+                   "note": "the same c4 step, all 2^20 scenarios on rank 0's GPU alone, measured "
+                           "in this run after the timed region (3 steps after 1 warm-up)"}
 
     cb = None
     if MULTI:
@@ -655,7 +677,7 @@ def run_grid(args, rank, world, local_rank, wl, spec, backend, cpu_group):
                 "n_sim_per_gpu": n_rank, "cell_steps_per_step": cells_step,
                 "dist_backend": backend},
         "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "latency": latency,
-        "sweep": sweep,
+        "sweep": sweep, "c4_one_gpu_same_run": one_gpu,
         "gpu_launches": args.steps * launches_per_step, "clocks": clocks,
         "host_enqueue_ms_per_step": wall * 1e3 / args.steps,
         "kernel_ms_p50": float(np.median(kern)), "step_ms_p50": float(np.median(per)),
