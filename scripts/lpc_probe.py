@@ -1,7 +1,10 @@
+# Ran once in round 2 against the ROUND-1 library (git 23d38c9, which still had the lanes-per-cell
+# forms), built to scripts/micro/oldlib with its package copied to scripts/micro/oldpkg (both
+# git-ignored).  Output: profiles/r02_lpc_probe_round1_library.txt.
 # Round-1 library (lanes-per-cell forms) on the latency-bound shapes: 10k scenarios with ONE
 # live row (a closed-loop step: v_prev == r) and Alg. 2 at 10k (r = 2.5 transient).
 import os, sys, time
-HERE = os.path.dirname(os.path.abspath(__file__))
+HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "micro")
 os.environ["RG_LIB_PATH"] = os.path.join(HERE, "oldlib", "librefgov_b200.so")
 sys.path.insert(0, os.path.join(HERE, "oldpkg"))
 import numpy as np
