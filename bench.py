@@ -94,6 +94,9 @@ def parse():
     ap.add_argument("--episodes", type=int, default=None, help="c5: total episodes")
     ap.add_argument("--j-star", type=int, default=J_STAR)
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--xchg", default="nccl", choices=["nccl", "p2p"],
+                    help="N>1 grid steps: the row counts' all-reduce through NCCL, or fused into "
+                         "the step kernel over NVLink (rg_xchg_*, RG_XCHG)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-sweep", action="store_true",
@@ -523,6 +526,12 @@ def run_grid(args, rank, world, local_rank, wl, spec, backend, cpu_group):
     minus1 = torch.full_like(row_idx, -1)
     dist = torch.distributed if MULTI else None
 
+    p2p = MULTI and args.xchg == "p2p"
+    if p2p:  # the exchange fused into the step kernel: no collective call per step
+        from paper_2510_08288_b200.sharded import _p2p_ready
+        _p2p_ready(ctx, dist, None)
+        flags |= _capi.RG_XCHG
+
     def launch(s):
         scen = _capi.make_scenarios(BASE_SEED + s, k0, n_rank, model.lo, model.span)
         _capi.check(lib.rg_grid_step(ctx.handle, prob, x0_ptr, 0.0, R_REF, M_GRID, 0, None,
@@ -531,6 +540,8 @@ def run_grid(args, rank, world, local_rank, wl, spec, backend, cpu_group):
                                      None, res, flags))
 
     def exchange():
+        if p2p:  # done inside the kernel; the global row is in the step's result block
+            return None
         # per-row violating-scenario counts, int32 (a gated-out row is -1 on every rank):
         # the global MAX is 0 exactly for the rows feasible on every shard
         dist.all_reduce(viol, op=dist.ReduceOp.MAX)
@@ -580,10 +591,11 @@ def run_grid(args, rank, world, local_rank, wl, spec, backend, cpu_group):
     total_ms = _max_over_ranks(float(per.sum()), world, dev)
     kernel_ms = _max_over_ranks(float(kern.mean()), world, dev)
     # the step's decision must be the reference's: all 32 rows feasible -> kappa = 1
-    if not MULTI:
+    if not MULTI or p2p:
         out = _capi.GridResult()
         _capi.check(lib.rg_grid_fetch(ctx.handle, None, M_GRID, out))
-        assert out.row == M_GRID - 1 and out.early_terms == 0, (out.row, out.early_terms)
+        assert out.row == M_GRID - 1, out.row
+        assert p2p or out.early_terms == 0, out.early_terms
     else:
         assert all(int(b.item()) == M_GRID - 1 for b in best_rows[-3:])
 
@@ -664,7 +676,9 @@ def run_grid(args, rank, world, local_rank, wl, spec, backend, cpu_group):
 
     par = f"scenario shards x{world}" + (
         f", {backend} all-reduce (MAX) of the int32[{M_GRID}] row counts per step, row "
-        "extracted on every device" if MULTI else "")
+        "extracted on every device" if MULTI and not p2p else "") + (
+        ", the row counts exchanged inside the step kernel over NVLink (RG_XCHG), row "
+        "extracted on every device" if p2p else "")
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -714,21 +728,23 @@ def e2e_grid(args, rank, world, local_rank, rg, plant, box, model, n_total, n_ra
     for s in range(2):
         robust_rg_parallel_sharded(plant, np.zeros(3), rg.GovernorState(0.0), R_REF, box,
                                    rg.sample_scenarios(model, n_total, j_star + 1, seed=s,
-                                                       device=local_rank), cfg)
+                                                       device=local_rank), cfg,
+                                   exchange=args.xchg)
     torch.distributed.barrier()
     t0 = time.perf_counter()
     for s in range(args.e2e_steps):
         scen = rg.sample_scenarios(model, n_total, j_star + 1, seed=BASE_SEED + s,
                                    device=local_rank)
         r = robust_rg_parallel_sharded(plant, np.zeros(3), rg.GovernorState(0.0), R_REF, box,
-                                       scen, cfg)
+                                       scen, cfg, exchange=args.xchg)
     t_e2e = _max_over_ranks((time.perf_counter() - t0) / args.e2e_steps, world, dev)
     assert r.kappa_opt == 1.0
     return {"value": M_GRID * n_total * j_star / t_e2e, "unit": UNIT,
             "h2d_bytes_per_step": 112, "d2h_bytes_per_step": M_GRID * 4,
             "ms_per_step": t_e2e * 1e3,
-            "api": "paper_2510_08288_b200.sharded.robust_rg_parallel_sharded (every rank "
-                   "returns the KappaResult; wall clock, max over ranks)"}
+            "api": f"paper_2510_08288_b200.sharded.robust_rg_parallel_sharded(exchange="
+                   f"{args.xchg!r}) (every rank returns the KappaResult; wall clock, max over "
+                   "ranks)"}
 
 
 def latency_split(ctx, lib, prob, x0_ptr, model, k0, n_sim):

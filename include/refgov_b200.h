@@ -70,6 +70,8 @@ extern "C" {
  * unless RG_FUSED_RNG is given. */
 #define RG_JOINT_ITER 0x80  /* rg_bisect_joint: one kernel per iteration (the sharded form's
                                kernels) instead of the single persistent kernel */
+#define RG_XCHG 0x100      /* rg_grid_step: the scenario-sharded step's all-reduce fused into the
+                               kernel over NVLink (see rg_xchg_init) */
 
 typedef struct rg_ctx rg_ctx;
 
@@ -150,7 +152,7 @@ RG_API int32_t rg_destroy(rg_ctx *ctx);
 RG_API int32_t rg_get_tanh_variant(rg_ctx *ctx, int32_t *variant);
 /* Per-context tuning knobs (none changes a result bit): "force_tpb" (0/32/64/128),
  * "no_placement", "no_pdl", "no_step2", "fused_gen" (0/1), "batch_chunk" (episodes
- * per staged chunk, 0 = automatic).  Defaults come from the RG_FORCE_TPB,
+ * per staged chunk, 0 = automatic), "xchg_timeout_ms" (fused exchange, default 10000).  Defaults come from the RG_FORCE_TPB,
  * RG_NO_PLACEMENT, RG_NO_PDL, RG_NO_STEP2, RG_FUSED_GEN and RG_BATCH_CHUNK environment
  * variables, read once at rg_create.  Unknown names give RG_E_ARGS. */
 RG_API int32_t rg_set_option(rg_ctx *ctx, const char *name, int64_t value);
@@ -278,6 +280,22 @@ RG_API int32_t rg_joint_iter(rg_ctx *ctx, int32_t it, int32_t fold);
 RG_API int32_t rg_joint_flag(rg_ctx *ctx, void **dev_flag);
 RG_API int32_t rg_joint_decide(rg_ctx *ctx, int32_t it);
 RG_API int32_t rg_joint_end(rg_ctx *ctx, rg_bisect_result *out);
+
+/* Fused exchange of the scenario-sharded grid step (one process per GPU, same node).
+ * Every rank calls rg_xchg_init(ctx, rank, world, handle[64]) -- it allocates the rank's
+ * exchange window in device memory and returns its CUDA IPC handle -- gathers the world's
+ * handles (rank-major, 64 bytes each) by any means (torch.distributed.all_gather_object),
+ * and calls rg_xchg_connect(ctx, handles), which maps every peer's window.  From then on
+ * rg_grid_step(..., RG_XCHG) does the step's all-reduce inside the kernel: the finalizing
+ * block stores the shard's per-row words into every rank's window over NVLink, raises its
+ * epoch flag there, waits for all ranks' flags and extracts the GLOBAL best row (row,
+ * row_viol are global; the other counters stay the shard's).  Every rank must run the same
+ * sequence of exchanged steps; a peer missing for "xchg_timeout_ms" (rg_set_option,
+ * default 10 s) fails the step with RG_E_CUDA instead of hanging.  m_grid <= 64,
+ * world <= 16.  Replaces: the NCCL all-reduce of the row counts (sharded.py). */
+RG_API int32_t rg_xchg_init(rg_ctx *ctx, int32_t rank, int32_t world, void *handle_out);
+RG_API int32_t rg_xchg_connect(rg_ctx *ctx, const void *handles);
+RG_API int32_t rg_xchg_close(rg_ctx *ctx);
 
 RG_API int32_t rg_fp64_peak(rg_ctx *ctx, double *flops_per_s);
 

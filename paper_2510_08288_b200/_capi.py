@@ -25,6 +25,8 @@ RG_TANH_AUTO, RG_TANH_FMA, RG_TANH_GENERIC = 0, 1, 2
 RG_DEVICE_PTRS, RG_ASYNC, RG_ABANDON, RG_NO_TIMING = 0x1, 0x2, 0x4, 0x8
 RG_TANH_LOCKSTEP, RG_FUSED_RNG, RG_STAGE_RNG = 0x10, 0x20, 0x40
 RG_JOINT_ITER = 0x80
+RG_XCHG = 0x100
+XCHG_HANDLE_BYTES = 64  # sizeof(cudaIpcMemHandle_t)
 _RNG_FLAGS = {None: 0, "fused": RG_FUSED_RNG, "staged": RG_STAGE_RNG}
 
 _i32, _i64, _u64, _d, _vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, \
@@ -147,6 +149,9 @@ SIGNATURES = {
     "rg_joint_flag": (_i32, [_vp, ctypes.POINTER(_vp)]),
     "rg_joint_decide": (_i32, [_vp, _i32]),
     "rg_joint_end": (_i32, [_vp, ctypes.POINTER(BisectResult)]),
+    "rg_xchg_init": (_i32, [_vp, _i32, _i32, _vp]),
+    "rg_xchg_connect": (_i32, [_vp, _vp]),
+    "rg_xchg_close": (_i32, [_vp]),
     "rg_fp64_peak": (_i32, [_vp, ctypes.POINTER(_d)]),
 }
 
@@ -299,7 +304,8 @@ class Context:
     @_locked
     def grid_step(self, prob: Problem, x0, v_prev, r, m_grid, prefix_mode, dist, n_sim,
                   scen: Scenarios | None, want_pbits: bool, abandon: bool = False,
-                  rng_mode: str | None = None, timing: bool = True, want_viol: bool = True):
+                  rng_mode: str | None = None, timing: bool = True, want_viol: bool = True,
+                  xchg: bool = False):
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
         horizon = 0
         if dist is not None:
@@ -309,7 +315,7 @@ class Context:
         pbits = np.empty((m_grid, (n_sim + 31) // 32), dtype=np.uint32) if want_pbits else None
         res = GridResult()
         flags = (RG_ABANDON if abandon else 0) | _RNG_FLAGS[rng_mode] | \
-            (0 if timing else RG_NO_TIMING)
+            (0 if timing else RG_NO_TIMING) | (RG_XCHG if xchg else 0)
         check(self.lib.rg_grid_step(self.handle, ctypes.byref(prob), _p(x0), float(v_prev),
                                     float(r), int(m_grid), int(bool(prefix_mode)), _p(dist),
                                     int(n_sim), int(horizon),
@@ -478,6 +484,23 @@ class Context:
                                         _p(kap), _p(fnd), _p(cel), _p(erl), ctypes.byref(res),
                                         0))
         return res, ((kap, fnd, cel, erl) if per_scenario else None)
+
+    @_locked
+    def xchg_init(self, rank: int, world: int) -> bytes:
+        """rg_xchg_init: allocate this rank's exchange window; its CUDA IPC handle."""
+        h = ctypes.create_string_buffer(XCHG_HANDLE_BYTES)
+        check(self.lib.rg_xchg_init(self.handle, int(rank), int(world), h))
+        return h.raw
+
+    @_locked
+    def xchg_connect(self, handles: bytes) -> None:
+        """rg_xchg_connect: map every rank's window (handles rank-major, 64 bytes each)."""
+        buf = ctypes.create_string_buffer(bytes(handles), len(handles))
+        check(self.lib.rg_xchg_connect(self.handle, buf))
+
+    @_locked
+    def xchg_close(self) -> None:
+        check(self.lib.rg_xchg_close(self.handle))
 
     @_locked
     def fp64_peak(self) -> float:

@@ -131,6 +131,7 @@ struct Tuning {
     int no_pdl = 0;           // grid step not launched with programmatic dependent launch
     int no_step2 = 0;         // single-wave step with the one-step rollout
     int fused_gen = 0;        // single-wave staged step generates its block itself (grid barrier)
+    int64_t xchg_timeout_ms = 10000;  // fused exchange: give up on a missing peer after this
     int64_t batch_chunk = 0;  // batched step: at most this many staged episodes per chunk
 };
 
@@ -165,7 +166,16 @@ struct rg_ctx {
     int j_src = -1;                 // its scenario source; -1 = none begun
     unsigned long long seq_ctr = 0; // grid-step publication tokens
     bool last_zero_copy = false;    // the last grid step published into h_out
+    // fused cross-GPU exchange (rg_xchg_*): this rank's window, the device table of every
+    // rank's window, the peer mappings opened through CUDA IPC, the step epoch
+    DevBuf x_win, x_peers;
+    std::vector<void*> x_opened;
+    int x_rank = -1, x_world = 0;
+    unsigned long long x_epoch = 0;
+    bool x_ready = false;
 };
+
+static void xchg_release(rg_ctx* ctx);  // the fused exchange's windows and mappings
 
 namespace {
 
@@ -308,6 +318,7 @@ Tuning env_tuning() {
     if (getenv("RG_NO_PDL")) t.no_pdl = 1;
     if (getenv("RG_NO_STEP2")) t.no_step2 = 1;
     if (getenv("RG_FUSED_GEN")) t.fused_gen = 1;
+    if (const char* e = getenv("RG_XCHG_TIMEOUT_MS")) t.xchg_timeout_ms = atoll(e);
     if (const char* e = getenv("RG_BATCH_CHUNK")) t.batch_chunk = atoll(e);
     if (!(t.force_tpb == 32 || t.force_tpb == 64 || t.force_tpb == 128)) t.force_tpb = 0;
     return t;
@@ -431,6 +442,7 @@ int32_t rg_destroy(rg_ctx* ctx) {
     if (!ctx) return RG_OK;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    xchg_release(ctx);
     DevBuf* bufs[] = {&ctx->g_viol, &ctx->g_early, &ctx->g_ovf, &ctx->g_aband, &ctx->g_src,
                       &ctx->g_ticket, &ctx->g_t0, &ctx->g_out, &ctx->g_bar, &ctx->j_state, &ctx->b_acc, &ctx->b_out,
                       &ctx->dist_raw, &ctx->soa, &ctx->S, &ctx->steps, &ctx->pbits, &ctx->rows,
@@ -463,6 +475,9 @@ int32_t rg_set_option(rg_ctx* ctx, const char* name, int64_t value) {
         t.no_step2 = value != 0;
     } else if (!strcmp(name, "fused_gen")) {
         t.fused_gen = value != 0;
+    } else if (!strcmp(name, "xchg_timeout_ms")) {
+        if (value < 1) return fail(RG_E_ARGS, "xchg_timeout_ms must be >= 1");
+        t.xchg_timeout_ms = value;
     } else if (!strcmp(name, "batch_chunk")) {
         if (value < 0) return fail(RG_E_ARGS, "batch_chunk must be >= 0");
         t.batch_chunk = value;
@@ -666,6 +681,10 @@ static int32_t unpack_grid(rg_ctx* ctx, const char* h, uint32_t* row_viol, int32
                            rg_grid_result* out, uint32_t* pbits_host, size_t pbits_bytes,
                            bool timed) {
     const rg::GridOut* ho = reinterpret_cast<const rg::GridOut*>(h);
+    if (ho->xchg_failed)
+        return fail(RG_E_CUDA, "fused exchange: a peer's words did not arrive within %lld ms "
+                    "(every rank must run the same exchanged steps)",
+                    (long long)ctx->tune.xchg_timeout_ms);
     if (row_viol) memcpy(row_viol, h + kOutHead, m_grid * sizeof(unsigned));
     if (pbits_host) memcpy(pbits_host, h + kOutHead + viol_bytes(m_grid), pbits_bytes);
     if (out) {
@@ -753,6 +772,18 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
     a.ticket = ctx->g_ticket.as<unsigned>();
     a.t0 = ctx->g_t0.as<unsigned long long>();
     a.pwords = (n_sim + 31) / 32;
+    if (flags & RG_XCHG) {
+        if (!ctx->x_ready) return fail(RG_E_ARGS, "RG_XCHG without a connected exchange (rg_xchg_connect)");
+        if (m_grid > rg::kXMaxRows)
+            return fail(RG_E_ARGS, "RG_XCHG supports m_grid <= %d, got %d", rg::kXMaxRows, m_grid);
+        a.xchg = 1;
+        a.xrank = ctx->x_rank;
+        a.xworld = ctx->x_world;
+        a.xepoch = ++ctx->x_epoch;
+        a.xtimeout_ns = (unsigned long long)ctx->tune.xchg_timeout_ms * 1000000ull;
+        a.xlocal = ctx->x_win.as<rg::XWin>();
+        a.xpeers = ctx->x_peers.as<rg::XWin* const>();
+    }
     const size_t pbytes = pbits ? (size_t)m_grid * a.pwords * sizeof(unsigned) : 0;
     const bool pbits_in_block = pbits && !(flags & RG_DEVICE_PTRS);
     // synchronous host-pointer calls: results land in pinned host memory and the
@@ -802,6 +833,87 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
     }
     return read_grid(ctx, row_viol, m_grid, out, pbits_in_block ? pbits : nullptr,
                      pbits_in_block ? pbytes : 0, timed);
+}
+
+// ---------------------------------------------------------------------------
+// fused cross-GPU exchange of the grid step (RG_XCHG)
+// ---------------------------------------------------------------------------
+
+}  // extern "C"
+
+static void xchg_release(rg_ctx* ctx) {
+    for (void* p : ctx->x_opened)
+        if (p) cudaIpcCloseMemHandle(p);
+    ctx->x_opened.clear();
+    ctx->x_win.release();
+    ctx->x_peers.release();
+    ctx->x_ready = false;
+    ctx->x_rank = -1;
+    ctx->x_world = 0;
+    ctx->x_epoch = 0;
+}
+
+extern "C" {
+
+int32_t rg_xchg_init(rg_ctx* ctx, int32_t rank, int32_t world, void* handle_out) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    if (world < 1 || world > rg::kXMaxWorld || rank < 0 || rank >= world)
+        return fail(RG_E_ARGS, "rank %d / world %d outside [0, world), world <= %d", rank, world,
+                    rg::kXMaxWorld);
+    if (!handle_out) return fail(RG_E_ARGS, "null handle_out");
+    RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    xchg_release(ctx);
+    RG_CUDA(ctx->x_win.ensure(sizeof(rg::XWin)));
+    RG_CUDA(cudaMemset(ctx->x_win.p, 0, sizeof(rg::XWin)));
+    RG_CUDA(ctx->x_peers.ensure(rg::kXMaxWorld * sizeof(void*)));
+    cudaIpcMemHandle_t h;
+    RG_CUDA(cudaIpcGetMemHandle(&h, ctx->x_win.p));
+    memcpy(handle_out, &h, sizeof h);
+    ctx->x_rank = rank;
+    ctx->x_world = world;
+    return RG_OK;
+}
+
+int32_t rg_xchg_connect(rg_ctx* ctx, const void* handles) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    if (ctx->x_rank < 0) return fail(RG_E_ARGS, "rg_xchg_connect before rg_xchg_init");
+    if (!handles) return fail(RG_E_ARGS, "null handles");
+    cudaIpcMemHandle_t mine;
+    RG_CUDA(cudaIpcGetMemHandle(&mine, ctx->x_win.p));
+    void* table[rg::kXMaxWorld] = {};
+    for (int r = 0; r < ctx->x_world; ++r) {
+        const char* hr = static_cast<const char*>(handles) + (size_t)r * sizeof(cudaIpcMemHandle_t);
+        if (r == ctx->x_rank || !memcmp(hr, &mine, sizeof mine)) {
+            table[r] = ctx->x_win.p;  // our own window (or a test naming it twice)
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        memcpy(&h, hr, sizeof h);
+        void* p = nullptr;
+        const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            xchg_release(ctx);
+            return fail(RG_E_CUDA, "cudaIpcOpenMemHandle of rank %d's window failed: %s", r,
+                        cudaGetErrorString(e));
+        }
+        ctx->x_opened.push_back(p);
+        table[r] = p;
+    }
+    RG_CUDA(cudaMemcpy(ctx->x_peers.p, table, sizeof table, cudaMemcpyHostToDevice));
+    ctx->x_epoch = 0;
+    ctx->x_ready = true;
+    return RG_OK;
+}
+
+int32_t rg_xchg_close(rg_ctx* ctx) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    xchg_release(ctx);
+    return RG_OK;
 }
 
 int32_t rg_grid_fetch(rg_ctx* ctx, uint32_t* row_viol, int32_t m_grid, rg_grid_result* out) {

@@ -58,6 +58,117 @@ __device__ __forceinline__ void grid_clock_start(const GridArgs& a) {
 }
 
 
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// The finalizing block of a fused-exchange step (RG_XCHG, m_grid <= kXMaxRows): this shard's
+// per-row words (a gated-out row -1, else the shard's violating-scenario count; duplicates
+// carry their source's) go to every rank's window over NVLink, then this rank waits for
+// every rank's words of the same epoch in its own window and extracts the row from the MAX
+// (0 exactly for the rows feasible on every shard), as the NCCL path does after its
+// all-reduce.  The stats stay this shard's.  A peer missing for xtimeout_ns marks the step
+// failed instead of hanging the GPU.
+__device__ __noinline__ void grid_finalize_xchg(const GridArgs& a, unsigned long long t_fin) {
+    __shared__ int s_w[kXMaxRows];
+    __shared__ int s_src[kXMaxRows];
+    __shared__ bool s_fail;
+    const int M = a.m_grid;
+    const int par = (int)(a.xepoch & 1ull);
+    if (threadIdx.x < M) {
+        const int q = threadIdx.x;
+        const int sq = ((volatile int*)a.row_src)[q];
+        const unsigned vq = ((volatile unsigned*)a.viol)[sq >= 0 ? sq : q];
+        s_src[q] = sq;
+        s_w[q] = sq == -2 ? -1 : (int)min(vq, 0x7fffffffu);
+    }
+    if (threadIdx.x == 0) s_fail = false;
+    __syncthreads();
+    // this shard's words into every rank's window (peer stores over NVLink)
+    for (int t = threadIdx.x; t < a.xworld * M; t += blockDim.x) {
+        const int r = t / M, q = t - r * M;
+        a.xpeers[r]->words[par][a.xrank][q] = s_w[q];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x < a.xworld)
+        st_release_sys(&a.xpeers[threadIdx.x]->flag[par][a.xrank], a.xepoch);
+    // every rank's words of this epoch in our window
+    if (threadIdx.x < a.xworld) {
+        const unsigned long long* f = &a.xlocal->flag[par][threadIdx.x];
+        const unsigned long long t0 = global_ns();
+        while (ld_acquire_sys(f) < a.xepoch) {
+            if (global_ns() - t0 > a.xtimeout_ns) {
+                s_fail = true;
+                break;
+            }
+            __nanosleep(100);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < M) {
+        int g = -1;
+        for (int r = 0; r < a.xworld; ++r)
+            g = max(g, ((volatile int*)a.xlocal->words[par][r])[threadIdx.x]);
+        s_w[threadIdx.x] = g;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int best = -1, n_active = 0, pruned = 0, dup = 0;
+        unsigned long long early = 0, ovf = 0, aband = 0;
+        bool open = true;
+        for (int q = 0; q < M; ++q) {
+            const int sq = s_src[q];
+            const bool full = sq != -2 && s_w[q] == 0;
+            a.viol_out[q] = (unsigned)s_w[q];
+            n_active += sq == -1;
+            pruned += sq == -2;
+            dup += sq >= 0;
+            if (sq == -1) {
+                early += ((volatile unsigned long long*)a.early)[q];
+                ovf += ((volatile unsigned long long*)a.ovf)[q];
+                aband += ((volatile unsigned long long*)a.abandoned)[q];
+            }
+            if (a.prefix_mode) {
+                if (open && full) best = q;
+                open = open && full;
+            } else if (full) {
+                best = q;
+            }
+        }
+        a.out->row = best;
+        a.out->n_active = n_active;
+        a.out->ss_pruned_rows = pruned;
+        a.out->dedup_rows = dup;
+        a.out->early_terms = (long long)early;
+        a.out->overflows = (long long)ovf;
+        a.out->abandoned = (long long)aband;
+        a.out->sims_run = (long long)n_active * a.n_sim;
+        a.out->xchg_failed = s_fail ? 1 : 0;
+        if (a.t0) {
+            const unsigned long long now = global_ns();
+            a.out->kernel_ns = now - *(volatile unsigned long long*)a.t0;
+            a.out->reduce_ns = now - t_fin;
+            *a.t0 = ~0ull;
+        }
+        __threadfence_system();
+        *(volatile unsigned long long*)&a.out->seq = a.seq_token;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < M; q += blockDim.x) {
+        a.viol[q] = 0u;
+        a.early[q] = 0ull;
+        a.ovf[q] = 0ull;
+        a.abandoned[q] = 0ull;
+    }
+    if (threadIdx.x == 0) *a.ticket = 0u;
+}
+
 // Last block out extracts the best row (governor.py:351-377) and resets the
 // accumulators for the next launch.  The first warp reads 32 rows at a time
 // (one per lane) and reduces with ballots and shuffles, so the step's tail is
@@ -93,6 +204,10 @@ __device__ __forceinline__ void grid_finalize(const GridArgs& a) {
             }
         }
         __syncthreads();
+    }
+    if (a.xchg) {
+        grid_finalize_xchg(a, s_tfin);
+        return;
     }
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
@@ -146,6 +261,7 @@ __device__ __forceinline__ void grid_finalize(const GridArgs& a) {
             a.out->overflows = (long long)ovf;
             a.out->abandoned = (long long)aband;
             a.out->sims_run = (long long)n_active * a.n_sim;
+            a.out->xchg_failed = 0;
             if (a.t0) {
                 const unsigned long long now = global_ns();
                 a.out->kernel_ns = now - *(volatile unsigned long long*)a.t0;

@@ -48,6 +48,17 @@ struct GridOut {
     unsigned long long seq;
     unsigned long long kernel_ns;  // device span of the step (globaltimer)
     unsigned long long reduce_ns;  // the last block's row extraction and publication
+    int32_t xchg_failed;           // fused exchange: a peer's words never arrived (timeout)
+};
+
+// Cross-GPU exchange window of the fused grid step (RG_XCHG).  Every rank owns one in its
+// device memory; peers write into it over NVLink (CUDA IPC mappings).  Parity-double-buffered
+// by the step epoch: a rank can be at most one step ahead of a peer that still reads.
+constexpr int kXMaxWorld = 16;
+constexpr int kXMaxRows = 64;
+struct XWin {
+    unsigned long long flag[2][kXMaxWorld];    // [parity][sender] = epoch of the sender's words
+    int words[2][kXMaxWorld][kXMaxRows];       // [parity][sender][row] per-row verdict words
 };
 
 struct GridArgs {
@@ -89,6 +100,14 @@ struct GridArgs {
     int gen;
     double* soa_w;
     unsigned* bar;
+    // fused cross-GPU exchange (xchg = 1): the finalizing block writes this shard's per-row
+    // words into every rank's window (xpeers[r], rank xrank of xworld), raises its epoch
+    // flag there, waits for every rank's flag in its own window (xlocal) and extracts the
+    // row from the MAX over ranks -- the all-reduce done by the step kernel over NVLink
+    int xchg, xrank, xworld;
+    unsigned long long xepoch, xtimeout_ns;
+    XWin* xlocal;
+    XWin* const* xpeers;
 };
 
 // Batch of independent governor instances (episodes).  The host evaluates every

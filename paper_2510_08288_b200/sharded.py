@@ -121,14 +121,35 @@ def _device_row(ctx, dist, group, prob, x_t, v_prev, r_t, config, n_sim, stream)
     return (None if idx < 0 else idx), counts
 
 
+_P2P: dict = {}
+
+
+def _p2p_ready(ctx, dist, group):
+    """Map every rank's exchange window once per (device, group): rg_xchg_init, an
+    all_gather_object of the CUDA IPC handles, rg_xchg_connect."""
+    key = (ctx.device, id(group))
+    if key not in _P2P:
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        mine = ctx.xchg_init(rank, world)
+        handles = [None] * world
+        dist.all_gather_object(handles, mine, group=group)
+        ctx.xchg_connect(b"".join(handles))
+        _P2P[key] = True
+
+
 def robust_rg_parallel_sharded(plant, x_t, state, r_t, cset, scenarios, config, group=None,
-                               local_step=None):
+                               local_step=None, exchange="nccl"):
     """robust_rg_parallel over the ranks of `group`; every rank returns the same result.
 
     ``local_step(shard) -> uint32[M]`` computes this rank's per-row counts; the
     default is the device kernel (rg_grid_step) with the exchange on the device
     (_device_row).  A dense host scenario tensor is stepped synchronously and its
     counts all-reduced from the host.  matrix is None (P is sharded).
+
+    ``exchange="p2p"`` (generated scenarios, m_grid <= 64, ranks on one node) fuses the
+    exchange into the step kernel instead of an NCCL all-reduce: its finalizing block
+    writes the shard's per-row words into every rank's window over NVLink and extracts
+    the global row itself (rg_xchg_*, RG_XCHG).
     """
     dist = _dist()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
@@ -148,7 +169,15 @@ def robust_rg_parallel_sharded(plant, x_t, state, r_t, cset, scenarios, config, 
     if local_step is None:
         ctx = _capi.context(getattr(config, "device", 0))
         dist_t, n_sim, stream = _source(shard, config.j_star)
-        if dist_t is None:
+        if dist_t is None and exchange == "p2p":
+            with ctx.lock:
+                _p2p_ready(ctx, dist, group)
+                res, viol, _ = ctx.grid_step(prob, x_t, state.v_prev, r_t, config.m_grid,
+                                             config.prefix_mode, None, n_sim, stream, False,
+                                             abandon=True, timing=False, xchg=True)
+            counts = viol.view(np.int32)
+            row = None if res.row < 0 else int(res.row)
+        elif dist_t is None:
             with ctx.lock:
                 row, counts = _device_row(ctx, dist, group, prob, x_t, state.v_prev, r_t,
                                           config, n_sim, stream)
@@ -162,7 +191,7 @@ def robust_rg_parallel_sharded(plant, x_t, state, r_t, cset, scenarios, config, 
         viol = np.asarray(local_step(shard), dtype=np.uint32)
         row = extract_row(global_row_counts(viol, group, None), dup_src, config.prefix_mode)
     diag = {"method": "parallel-grid-sharded", "ranks": world, "backend": "cuda",
-            "device_exchange": counts is not None,
+            "device_exchange": counts is not None, "exchange": exchange,
             # global per-row verdict words: 0 = feasible on every shard, -1 = gated out,
             # > 0 = some shard violated (rows already known infeasible stop early, so a
             # positive word is not a full count)
