@@ -536,7 +536,7 @@ def run_grid(args, rank, world, local_rank, wl, spec, backend, cpu_group):
         scen = _capi.make_scenarios(BASE_SEED + s, k0, n_rank, model.lo, model.span)
         _capi.check(lib.rg_grid_step(ctx.handle, prob, x0_ptr, 0.0, R_REF, M_GRID, 0, None,
                                      n_rank, 0, scen,
-                                     _vp()(viol.data_ptr()) if MULTI else None,
+                                     _vp()(viol.data_ptr()) if MULTI and not p2p else None,
                                      None, res, flags))
 
     def exchange():
