@@ -296,6 +296,18 @@ RG_API int32_t rg_joint_end(rg_ctx *ctx, rg_bisect_result *out);
 RG_API int32_t rg_xchg_init(rg_ctx *ctx, int32_t rank, int32_t world, void *handle_out);
 RG_API int32_t rg_xchg_connect(rg_ctx *ctx, const void *handles);
 RG_API int32_t rg_xchg_close(rg_ctx *ctx);
+/* The joint search over this rank's scenario shard with the per-round exchange fused into
+ * the persistent kernel (needs a connected exchange): after each round's local barrier the
+ * shard's candidate verdicts go to every rank's window over NVLink and every block waits for
+ * all ranks' and ORs them, so each rank walks the same global decisions without leaving the
+ * kernel.  n_sim_max: the largest shard (the same on every rank, it fixes the speculation
+ * depth); it must fit in one wave.  kappa / found are global, cells / early this shard's.
+ * Replaces: robust_rg_joint_sharded's per-iteration NCCL all-reduce of the flag. */
+RG_API int32_t rg_bisect_joint_sharded(rg_ctx *ctx, const rg_problem *prob, const double *x0,
+                                       double v_prev, double r, int32_t n_kappa,
+                                       const double *dist, int64_t n_sim, int64_t horizon,
+                                       const rg_scenarios *rng, int64_t n_sim_max,
+                                       rg_bisect_result *out, int32_t flags);
 
 RG_API int32_t rg_fp64_peak(rg_ctx *ctx, double *flops_per_s);
 

@@ -152,6 +152,9 @@ SIGNATURES = {
     "rg_xchg_init": (_i32, [_vp, _i32, _i32, _vp]),
     "rg_xchg_connect": (_i32, [_vp, _vp]),
     "rg_xchg_close": (_i32, [_vp]),
+    "rg_bisect_joint_sharded": (_i32, [_vp, ctypes.POINTER(Problem), _vp, _d, _d, _i32, _vp, _i64,
+                                       _i64, ctypes.POINTER(Scenarios), _i64,
+                                       ctypes.POINTER(BisectResult), _i32]),
     "rg_fp64_peak": (_i32, [_vp, ctypes.POINTER(_d)]),
 }
 
@@ -497,6 +500,24 @@ class Context:
         """rg_xchg_connect: map every rank's window (handles rank-major, 64 bytes each)."""
         buf = ctypes.create_string_buffer(bytes(handles), len(handles))
         check(self.lib.rg_xchg_connect(self.handle, buf))
+
+    @_locked
+    def bisect_joint_sharded(self, prob: Problem, x0, v_prev, r, n_kappa, dist, n_sim,
+                             scen: Scenarios | None, n_sim_max: int) -> "BisectResult":
+        """rg_bisect_joint_sharded: this rank's shard of a joint search, the per-round
+        exchange fused into the persistent kernel (needs xchg_connect)."""
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        horizon = 0
+        if dist is not None:
+            dist = np.ascontiguousarray(dist, dtype=np.float64)
+            horizon = dist.shape[1]
+        res = BisectResult()
+        check(self.lib.rg_bisect_joint_sharded(self.handle, ctypes.byref(prob), _p(x0),
+                                               float(v_prev), float(r), int(n_kappa), _p(dist),
+                                               int(n_sim), int(horizon),
+                                               ctypes.byref(scen) if scen is not None else None,
+                                               int(n_sim_max), ctypes.byref(res), 0))
+        return res
 
     @_locked
     def xchg_close(self) -> None:

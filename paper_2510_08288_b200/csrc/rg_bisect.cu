@@ -266,12 +266,50 @@ __global__ void __launch_bounds__(256, 1) k_joint_spec(JointArgs a) {
             t = __shfl_sync(0xffffffffu, nxt, 0);
         }
         grid_barrier(&st->bar_count, &st->bar_gen, gridDim.x);
+        __shared__ unsigned s_gv[kJointNodes];  // the verdicts the walk reads
+        if (a.xchg) {
+            // the shards' verdicts: block 0 sends this shard's to every rank's window, every
+            // block waits for every rank's and ORs them (epoch xepoch0 + round, parity buffers)
+            const unsigned long long ep = a.xepoch0 + (unsigned long long)round;
+            const int par = (int)(ep & 1ull);
+            if (blockIdx.x == 0) {
+                for (int t = threadIdx.x; t < a.xworld * nodes; t += blockDim.x) {
+                    const int r = t / nodes, q = t - r * nodes;
+                    a.xpeers[r]->words[par][a.xrank][q] = *(volatile unsigned*)(viol + q) != 0u;
+                }
+                __threadfence_system();
+                __syncthreads();
+                if (threadIdx.x < a.xworld)
+                    st_release_sys(&a.xpeers[threadIdx.x]->flag[par][a.xrank], ep);
+            }
+            if (threadIdx.x < a.xworld) {
+                const unsigned long long* f = &a.xlocal->flag[par][threadIdx.x];
+                const unsigned long long t0 = global_ns();
+                while (ld_acquire_sys(f) < ep) {
+                    if (global_ns() - t0 > a.xtimeout_ns) {
+                        st->xfail = 1;
+                        break;
+                    }
+                    __nanosleep(100);
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x < nodes) {
+                int g = 0;
+                for (int r = 0; r < a.xworld; ++r)
+                    g |= ((volatile int*)a.xlocal->words[par][r])[threadIdx.x];
+                s_gv[threadIdx.x] = (unsigned)g;
+            }
+        } else if (threadIdx.x < nodes) {
+            s_gv[threadIdx.x] = *(volatile unsigned*)(viol + threadIdx.x);
+        }
+        __syncthreads();
         // the walk: the decisions the one-candidate search takes, while they stay in the tree
         if (threadIdx.x == 0) {
             int n = 0;
             Bracket b = tree[0];
             while (true) {
-                const bool feas = *(volatile unsigned*)(viol + n) == 0u;
+                const bool feas = s_gv[n] == 0u;
                 b.early += *(volatile unsigned long long*)(early + n);
                 const int nx = feas ? 2 * n + 1 : 2 * n + 2;
                 if (nx < nodes) {

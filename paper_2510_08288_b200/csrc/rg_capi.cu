@@ -1138,6 +1138,12 @@ int32_t rg_joint_end(rg_ctx* ctx, rg_bisect_result* out) {
     RG_CUDA(cudaMemcpyAsync(hs, ctx->j_args.st, sizeof(rg::JointState), cudaMemcpyDeviceToHost,
                             ctx->stream));
     RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    const bool xchg = ctx->j_args.xchg != 0;
+    if (xchg) ctx->x_epoch += (unsigned long long)hs->rounds;  // one epoch per exchanged round
+    ctx->j_src = -1;
+    if (xchg && hs->xfail)
+        return fail(RG_E_CUDA, "fused exchange: a peer's verdicts did not arrive within %lld ms "
+                    "(every rank must run the same searches)", (long long)ctx->tune.xchg_timeout_ms);
     if (out) {
         out->kappa = hs->kopt;
         out->found = hs->found;
@@ -1147,8 +1153,39 @@ int32_t rg_joint_end(rg_ctx* ctx, rg_bisect_result* out) {
         out->kernel_ms = cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) == cudaSuccess ? ms : 0.f;
         cudaGetLastError();
     }
-    ctx->j_src = -1;
     return RG_OK;
+}
+
+int32_t rg_bisect_joint_sharded(rg_ctx* ctx, const rg_problem* prob, const double* x0,
+                                double v_prev, double r, int32_t n_kappa, const double* dist,
+                                int64_t n_sim, int64_t horizon, const rg_scenarios* rng,
+                                int64_t n_sim_max, rg_bisect_result* out, int32_t flags) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    if (!ctx->x_ready) return fail(RG_E_ARGS, "no connected exchange (rg_xchg_connect)");
+    if (n_sim_max < n_sim || n_sim_max < 1) return fail(RG_E_ARGS, "n_sim_max must be >= n_sim");
+    const int depth = rg::joint_spec_depth(n_sim_max, ctx->sm_count);
+    if (depth == 0 || n_kappa + 1 > rg::kJointMaxRounds)
+        return fail(RG_E_ARGS, "the fused sharded search needs shards within one wave and "
+                    "n_kappa < %d (use rg_joint_iter with an all-reduce)", rg::kJointMaxRounds);
+    if ((rc = rg_joint_begin(ctx, prob, x0, v_prev, r, n_kappa, dist, n_sim, horizon, rng, flags)))
+        return rc;
+    rg::JointArgs& a = ctx->j_args;
+    a.depth = depth;  // from the largest shard: every rank builds the same trees
+    a.xchg = 1;
+    a.xrank = ctx->x_rank;
+    a.xworld = ctx->x_world;
+    a.xepoch0 = ctx->x_epoch + 1;
+    a.xtimeout_ns = (unsigned long long)ctx->tune.xchg_timeout_ms * 1000000ull;
+    a.xlocal = ctx->x_win.as<rg::XWin>();
+    a.xpeers = ctx->x_peers.as<rg::XWin* const>();
+    const cudaError_t e = rg::launch_joint_spec(a, ctx->variant == rg::kTanhFma, ctx->j_src,
+                                                ctx->sm_count, ctx->stream);
+    if (e != cudaSuccess) {
+        ctx->j_src = -1;
+        return fail(RG_E_CUDA, "joint search launch failed: %s", cudaGetErrorString(e));
+    }
+    return rg_joint_end(ctx, out);
 }
 
 int32_t rg_bisect_joint(rg_ctx* ctx, const rg_problem* prob, const double* x0, double v_prev,

@@ -58,15 +58,6 @@ __device__ __forceinline__ void grid_clock_start(const GridArgs& a) {
 }
 
 
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
 // The finalizing block of a fused-exchange step (RG_XCHG, m_grid <= kXMaxRows): this shard's
 // per-row words (a gated-out row -1, else the shard's violating-scenario count; duplicates
 // carry their source's) go to every rank's window over NVLink, then this rank waits for

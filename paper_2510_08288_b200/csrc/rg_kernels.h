@@ -233,6 +233,7 @@ struct JointState {
     unsigned sitem[kJointMaxRounds];
     unsigned bar_count, bar_gen, exit_ticket;
     int rounds;  // rounds the last persistent search ran (diagnostics)
+    int xfail;   // fused exchange: a peer's words did not arrive (timeout)
 };
 
 struct JointArgs {
@@ -249,6 +250,14 @@ struct JointArgs {
     int smem_dyn;  // shared memory per block, static + dynamic (single-wave placement pin)
     int fold;  // 1: the last block decides (single GPU); 0: k_joint_decide after the all-reduce
     int depth;  // persistent search: speculation depth (1..3): 2^depth - 1 candidates per round
+    // scenario-sharded persistent search with the per-round exchange fused in (xchg = 1): after
+    // the local grid barrier block 0 writes this shard's candidate verdicts into every rank's
+    // window over NVLink (epoch xepoch0 + round), every block waits for every rank's verdicts
+    // and the walk uses their OR -- no collective launch, the search stays one kernel per GPU
+    int xchg, xrank, xworld;
+    unsigned long long xepoch0, xtimeout_ns;
+    XWin* xlocal;
+    XWin* const* xpeers;
 };
 
 cudaError_t launch_joint_roll(const JointArgs& a, int it, bool fma, int src, cudaStream_t s);

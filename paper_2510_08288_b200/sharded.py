@@ -313,12 +313,17 @@ class DeviceJointShard:
 
 
 def robust_rg_joint_sharded(plant, x_t, state, r_t, cset, scenarios, config, group=None,
-                            shard_impl=None):
+                            shard_impl=None, exchange="nccl"):
     """robust_rg_joint over the ranks of `group` (scenario shards, OR per iteration).
 
     ``shard_impl`` defaults to DeviceJointShard; the host-logic tests pass an
     oracle-backed object with the same methods.  Every rank walks the same
     candidates and returns the same kappa; sims_run / early_terms are summed.
+
+    ``exchange="p2p"``: the whole search is one persistent kernel per GPU with the
+    per-round OR of the shards' verdicts done inside it over NVLink
+    (rg_bisect_joint_sharded), when the largest shard fits in one wave; otherwise, and
+    for dense scenario tensors, the per-iteration form with a collective.
     """
     dist = _dist()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
@@ -328,8 +333,22 @@ def robust_rg_joint_sharded(plant, x_t, state, r_t, cset, scenarios, config, gro
     shard = scenarios.shard(rank, world)
     prob, _, _, _ = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor,
                               config.epsilon, config.tighten_mode, config.j_star, 0)
-    impl = shard_impl or DeviceJointShard(_capi.context(getattr(config, "device", 0)))
     t0 = time.perf_counter()
+    if exchange == "p2p" and shard_impl is None:
+        got = _joint_p2p(dist, group, prob, x_t, state, r_t, config, scenarios, shard, world)
+        if got is not None:
+            kappa, found, cells, early, dev = got
+            import torch
+            ce = torch.tensor([cells, early], dtype=torch.int64, device=dev)
+            dist.all_reduce(ce, op=dist.ReduceOp.SUM, group=group)
+            cells, early = (int(x) for x in ce.cpu().tolist())
+            v = update_setpoint(state.v_prev, r_t, kappa)
+            state.v_prev = v
+            return KappaResult(kappa, v, found, {"method": "joint-sharded", "ranks": world,
+                                                 "exchange": "p2p", "sims_run": cells,
+                                                 "early_terms": early,
+                                                 "wall_us": int((time.perf_counter() - t0) * 1e6)})
+    impl = shard_impl or DeviceJointShard(_capi.context(getattr(config, "device", 0)))
     lock = impl.ctx.lock if hasattr(impl, "ctx") else _nullcontext()
     with lock:  # begin .. end is one search on the context: no other call may interleave
         kappa, found, cells, early = _joint_iterations(impl, dist, group, prob, x_t, state, r_t,
@@ -346,6 +365,27 @@ def robust_rg_joint_sharded(plant, x_t, state, r_t, cset, scenarios, config, gro
     return KappaResult(kappa, v, found, {"method": "joint-sharded", "ranks": world,
                                          "sims_run": cells, "early_terms": early,
                                          "wall_us": int((time.perf_counter() - t0) * 1e6)})
+
+
+def _joint_p2p(dist, group, prob, x_t, state, r_t, config, scenarios, shard, world):
+    """The fused form, or None when it does not apply (every rank decides alike: the test
+    reads only the global scenario count and kind)."""
+    from .errors import ConfigError as _ConfigError
+
+    ctx = _capi.context(getattr(config, "device", 0))
+    dist_t, n_sim, stream = _source(shard, config.j_star)
+    if dist_t is not None:
+        return None
+    n_max = -(-scenarios.n_sim // world)
+    with ctx.lock:
+        _p2p_ready(ctx, dist, group)
+        try:
+            res = ctx.bisect_joint_sharded(prob, x_t, state.v_prev, r_t, config.n_kappa, None,
+                                           n_sim, stream, n_max)
+        except _ConfigError:  # the largest shard exceeds one wave
+            return None
+    return float(res.kappa), bool(res.found), int(res.cells), int(res.early), \
+        f"cuda:{ctx.device}"
 
 
 def _joint_iterations(impl, dist, group, prob, x_t, state, r_t, config, shard):

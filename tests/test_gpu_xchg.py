@@ -91,6 +91,51 @@ def test_missing_peer_fails_loudly_not_hangs():
     assert res.row == 15
 
 
+def test_fused_joint_search_equals_local_search(xctx):
+    """rg_bisect_joint_sharded with one rank (the per-round exchange through its window)
+    against the local persistent search and the per-iteration form: kappa, found, cells."""
+    rng = np.random.default_rng(33)
+    m = rg.DisturbanceModel.scaled(0.02, 3)
+    for trial in range(30):
+        n = int(rng.choice([1, 100, 1000, 4000]))
+        prob = _problem(int(rng.choice([16, 128, 256])))
+        vp = float(rng.uniform(-1.2, 1.2))
+        r = float(rng.uniform(-3, 3))
+        x0 = np.array([np.tanh(vp), vp, np.tanh(vp) / 2]) + rng.uniform(-0.06, 0.06, 3)
+        sc = _capi.make_scenarios(800 + trial, 0, n, m.lo, m.span)
+        nk = int(rng.choice([1, 8, 12]))
+        a = xctx.bisect_joint(prob, x0, vp, r, nk, None, n, sc)
+        b = xctx.bisect_joint_sharded(prob, x0, vp, r, nk, None, n, sc, n)
+        c = xctx.bisect_joint(prob, x0, vp, r, nk, None, n, sc, per_iteration=True)
+        assert (a.kappa, a.found, a.cells) == (b.kappa, b.found, b.cells) == \
+            (c.kappa, c.found, c.cells), trial
+    # a grid step and a search interleave on one epoch sequence
+    sc = _capi.make_scenarios(1, 0, 2000, m.lo, m.span)
+    g = xctx.grid_step(_problem(64), np.zeros(3), 0.0, 0.5, 32, False, None, 2000, sc, False,
+                       xchg=True)
+    b = xctx.bisect_joint_sharded(_problem(64), np.zeros(3), 0.0, 2.5, 8, None, 2000, sc, 2000)
+    g2 = xctx.grid_step(_problem(64), np.zeros(3), 0.0, 0.5, 32, False, None, 2000, sc, False,
+                        xchg=True)
+    assert g[0].row == g2[0].row == 31 and b.found
+
+
+def test_fused_joint_search_missing_peer_fails_loudly():
+    ctx = _capi.context(0)
+    h = ctx.xchg_init(0, 2)
+    ctx.xchg_connect(h + h)
+    ctx.set_option("xchg_timeout_ms", 300)
+    m = rg.DisturbanceModel.scaled(0.02, 3)
+    sc = _capi.make_scenarios(9, 0, 500, m.lo, m.span)
+    try:
+        with pytest.raises(rg.RefgovError, match="did not arrive"):
+            ctx.bisect_joint_sharded(_problem(32), np.zeros(3), 0.0, 2.5, 8, None, 500, sc, 500)
+    finally:
+        ctx.set_option("xchg_timeout_ms", 10000)
+        ctx.xchg_close()
+    r = ctx.bisect_joint(_problem(32), np.zeros(3), 0.0, 2.5, 8, None, 500, sc)
+    assert r.found
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -127,6 +172,11 @@ def _worker(rank, world, port, out_dir):
             out.append((k.kappa_opt, k.v_applied, k.feasible,
                         [w == 0 for w in k.diagnostics["row_words"]]))
         res.append(out[0] == out[1])
+        jt = [sharded.robust_rg_joint_sharded(plant, x0, rg.GovernorState(vp), r, box, scen, cfg,
+                                              exchange=ex) for ex in ("nccl", "p2p")]
+        res.append((jt[0].kappa_opt, jt[0].feasible, jt[0].diagnostics["sims_run"]) ==
+                   (jt[1].kappa_opt, jt[1].feasible, jt[1].diagnostics["sims_run"]))
+        res.append(jt[1].diagnostics.get("exchange") == "p2p")
     np.save(Path(out_dir) / "xchg.npy", np.array(res))
     dist.destroy_process_group()
 
