@@ -72,6 +72,47 @@ def rk4_step(plant, x: np.ndarray, v: float) -> np.ndarray:
     return nxt
 
 
+def _surrogate_rk4(h: float, x: np.ndarray, v: float) -> np.ndarray:
+    """rk4_step for the surrogate in Python floats: the reference's elementwise numpy
+    operations one element at a time, same operands, same order, same roundings (CPython
+    floats are IEEE doubles without contraction).  dx2/dt = -x2 + v does not involve the
+    other states, so the four stage values of x2 -- the four tanh arguments -- come first
+    and go through ONE numpy tanh call (numpy's vector tanh equals its scalar tanh bit for
+    bit, tests/test_harness_batch.py).  ~5x cheaper than the 3-element array form, once per
+    closed-loop step (dynamics.py:110-130, 228-231)."""
+    hh = 0.5 * h
+    x0, x1, x2 = float(x[0]), float(x[1]), float(x[2])
+    k11 = -x1 + v
+    b1 = x1 + hh * k11
+    k21 = -b1 + v
+    c1 = x1 + hh * k21
+    k31 = -c1 + v
+    d1 = x1 + h * k31
+    k41 = -d1 + v
+    t1, t2, t3, t4 = np.tanh(np.array([x1, b1, c1, d1])).tolist()
+    k10 = -x0 + t1
+    k12 = -2.0 * x2 + x0
+    a0, a2 = x0 + hh * k10, x2 + hh * k12
+    k20 = -a0 + t2
+    k22 = -2.0 * a2 + a0
+    b0, b2 = x0 + hh * k20, x2 + hh * k22
+    k30 = -b0 + t3
+    k32 = -2.0 * b2 + b0
+    c0, c2 = x0 + h * k30, x2 + h * k32
+    k40 = -c0 + t4
+    k42 = -2.0 * c2 + c0
+    c = h / 6.0
+    nxt = np.array([x0 + c * (((k10 + 2.0 * k20) + 2.0 * k30) + k40),
+                    x1 + c * (((k11 + 2.0 * k21) + 2.0 * k31) + k41),
+                    x2 + c * (((k12 + 2.0 * k22) + 2.0 * k32) + k42)])
+    bad = ~np.isfinite(nxt) | (np.abs(nxt) > STATE_ABORT_LIMIT)
+    if bad.any():
+        i = int(np.argmax(bad))
+        raise IntegrationOverflowError(f"integration overflow in state {i} (value {nxt[i]!r})",
+                                       state_index=i)
+    return nxt
+
+
 class SurrogateFuelCellPlant(Plant):
     """RK4-discretised surrogate benchmark plant (dynamics.py:209-263)."""
 
@@ -84,7 +125,7 @@ class SurrogateFuelCellPlant(Plant):
         self.step_size = float(step_size)
 
     def step(self, x, v):
-        return rk4_step(self, np.asarray(x, dtype=np.float64), float(v))
+        return _surrogate_rk4(self.step_size, np.asarray(x, dtype=np.float64), float(v))
 
     def output(self, x, v) -> float:
         return float(x[0])

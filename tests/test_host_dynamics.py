@@ -65,3 +65,37 @@ def test_linear_plant_validation():
         ys.append(plant.output(x, 1.0))
         x = plant.step(x, 1.0)
     assert ys == pytest.approx([0.0, 0.5, 0.75, 0.875])   # test_dynamics.py step response
+
+
+def test_scalar_surrogate_step_equals_array_form_and_reference():
+    """The closed loop's true-plant step in Python floats (one numpy tanh call for the four
+    stage arguments) equals the 3-element numpy form of dynamics.py:110-130 bit for bit --
+    and the unmodified reference's plant.step when it is staged (oracle/_ref) -- including
+    the overflow abort."""
+    import numpy as np
+
+    import paper_2510_08288_b200 as rg
+    from paper_2510_08288_b200 import dynamics as D
+    from oracle import reference
+
+    p = rg.make_plant("surrogate-fc")
+    ref, _ = reference.load()
+    rp = ref.make_plant("surrogate-fc") if ref is not None else None
+    rng = np.random.default_rng(5)
+    X = np.concatenate([rng.uniform(-1, 1, (3000, 3)), rng.uniform(-40, 40, (1000, 3)),
+                        rng.uniform(-9e5, 9e5, (500, 3))])
+    V = rng.uniform(-3, 3, X.shape[0])
+    for i in range(X.shape[0]):
+        a = D.rk4_step(p, X[i], float(V[i]))
+        b = p.step(X[i], float(V[i]))
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), i
+        if rp is not None and i % 7 == 0:
+            c = rp.step(X[i], float(V[i]))
+            assert np.array_equal(c.view(np.uint64), b.view(np.uint64)), i
+    import pytest
+    for bad in ([1e300, 0.0, 0.0], [0.0, 0.0, 2e6]):
+        with pytest.raises(rg.IntegrationOverflowError) as e1:
+            D.rk4_step(p, np.array(bad), 0.1)
+        with pytest.raises(rg.IntegrationOverflowError) as e2:
+            p.step(np.array(bad), 0.1)
+        assert e1.value.state_index == e2.value.state_index
