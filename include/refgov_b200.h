@@ -152,7 +152,9 @@ RG_API int32_t rg_destroy(rg_ctx *ctx);
 RG_API int32_t rg_get_tanh_variant(rg_ctx *ctx, int32_t *variant);
 /* Per-context tuning knobs (none changes a result bit): "force_tpb" (0/32/64/128),
  * "no_placement", "no_pdl", "no_step2", "fused_gen" (0/1), "batch_chunk" (episodes
- * per staged chunk, 0 = automatic), "xchg_timeout_ms" (fused exchange, default 10000).  Defaults come from the RG_FORCE_TPB,
+ * per staged chunk, 0 = automatic), "xchg_timeout_ms" (fused exchange, default 10000),
+ * "no_row_plan" (0/1: grid steps without P derive their rows on the device instead of
+ * launching only the host-planned simulated rows).  Defaults come from the RG_FORCE_TPB,
  * RG_NO_PLACEMENT, RG_NO_PDL, RG_NO_STEP2, RG_FUSED_GEN and RG_BATCH_CHUNK environment
  * variables, read once at rg_create.  Unknown names give RG_E_ARGS. */
 RG_API int32_t rg_set_option(rg_ctx *ctx, const char *name, int64_t value);

@@ -132,6 +132,7 @@ struct Tuning {
     int no_step2 = 0;         // single-wave step with the one-step rollout
     int fused_gen = 0;        // single-wave staged step generates its block itself (grid barrier)
     int64_t xchg_timeout_ms = 10000;  // fused exchange: give up on a missing peer after this
+    int no_row_plan = 0;      // grid step: rows always derived on the device
     int64_t batch_chunk = 0;  // batched step: at most this many staged episodes per chunk
 };
 
@@ -176,6 +177,8 @@ struct rg_ctx {
 };
 
 static void xchg_release(rg_ctx* ctx);  // the fused exchange's windows and mappings
+static int32_t episode_rows(const rg::ProblemDev& p, double v_prev, double r, int32_t M,
+                            int* src, double* v);
 
 namespace {
 
@@ -319,6 +322,7 @@ Tuning env_tuning() {
     if (getenv("RG_NO_STEP2")) t.no_step2 = 1;
     if (getenv("RG_FUSED_GEN")) t.fused_gen = 1;
     if (const char* e = getenv("RG_XCHG_TIMEOUT_MS")) t.xchg_timeout_ms = atoll(e);
+    if (getenv("RG_NO_ROW_PLAN")) t.no_row_plan = 1;
     if (const char* e = getenv("RG_BATCH_CHUNK")) t.batch_chunk = atoll(e);
     if (!(t.force_tpb == 32 || t.force_tpb == 64 || t.force_tpb == 128)) t.force_tpb = 0;
     return t;
@@ -475,6 +479,8 @@ int32_t rg_set_option(rg_ctx* ctx, const char* name, int64_t value) {
         t.no_step2 = value != 0;
     } else if (!strcmp(name, "fused_gen")) {
         t.fused_gen = value != 0;
+    } else if (!strcmp(name, "no_row_plan")) {
+        t.no_row_plan = value != 0;
     } else if (!strcmp(name, "xchg_timeout_ms")) {
         if (value < 1) return fail(RG_E_ARGS, "xchg_timeout_ms must be >= 1");
         t.xchg_timeout_ms = value;
@@ -735,8 +741,28 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
     a.prefix_mode = prefix_mode ? 1 : 0;
     a.n_sim = n_sim;
     bool use_rng = dist == nullptr;
-    a.tpb = tpb_for(ctx, n_sim, m_grid);
-    grid_placement(ctx, n_sim, m_grid, &a.tpb, &a.smem_dyn);
+    // Host-planned rows: without P (the governor's decision, a closed loop) the host
+    // evaluates the candidates' setpoints, gate and dedup itself and launches grid rows for
+    // the simulated ones only -- a closed-loop step has about one, and
+    // the placement below then sees the real work.  With P, or when every row is simulated,
+    // the kernel derives the rows on the device (row_source).
+    int grid_rows = m_grid;
+    if (!pbits && m_grid <= rg::kListMax && !ctx->tune.no_row_plan) {
+        int src[rg::kListMax];
+        double vv[rg::kListMax];
+        const int32_t n_act = episode_rows(a.p, v_prev, r, m_grid, src, vv);
+        if (n_act > 0 && n_act < m_grid) {
+            a.listed = 1;
+            a.list_n = 0;
+            for (int32_t q = 0; q < m_grid; ++q) {
+                a.src_tab[q] = src[q];
+                if (src[q] == -1) a.row_list[a.list_n++] = q;
+            }
+            grid_rows = a.list_n;
+        }
+    }
+    a.tpb = tpb_for(ctx, n_sim, grid_rows);
+    grid_placement(ctx, n_sim, grid_rows, &a.tpb, &a.smem_dyn);
     a.no_s2 = ctx->tune.no_step2;
     // Option: the single-wave staged step (the two-step rollout, rg_grid.cu: launch_grid)
     // generates its own scenario block -- every block is resident, so a grid barrier can
@@ -1212,6 +1238,8 @@ int32_t rg_bisect_joint(rg_ctx* ctx, const rg_problem* prob, const double* x0, d
     return rg_joint_end(ctx, out);
 }
 
+}  // extern "C"
+
 // One episode's candidate rows on the host, exactly as the device (and governor.py:286-317)
 // evaluates them: v_i = update_setpoint(v_prev, r, i/(M-1)), the steady-state gate as the
 // verified setpoint interval, duplicates mapped to the first gated row with the same v.
@@ -1254,6 +1282,8 @@ static int32_t episode_rows(const rg::ProblemDev& p, double v_prev, double r, in
     }
     return n;
 }
+
+extern "C" {
 
 int32_t rg_grid_step_batch(rg_ctx* ctx, const rg_problem* prob, int32_t n_episodes,
                            const double* x0, const double* v_prev, const double* r,

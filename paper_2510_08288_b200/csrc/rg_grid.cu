@@ -73,7 +73,7 @@ __device__ __noinline__ void grid_finalize_xchg(const GridArgs& a, unsigned long
     const int par = (int)(a.xepoch & 1ull);
     if (threadIdx.x < M) {
         const int q = threadIdx.x;
-        const int sq = ((volatile int*)a.row_src)[q];
+        const int sq = a.listed ? a.src_tab[q] : ((volatile int*)a.row_src)[q];
         const unsigned vq = ((volatile unsigned*)a.viol)[sq >= 0 ? sq : q];
         s_src[q] = sq;
         s_w[q] = sq == -2 ? -1 : (int)min(vq, 0x7fffffffu);
@@ -213,7 +213,7 @@ __device__ __forceinline__ void grid_finalize(const GridArgs& a) {
             unsigned vq = 0u;
             unsigned long long ab = 0ull, ea = 0ull, ov = 0ull;
             if (in) {
-                sq = ((volatile int*)a.row_src)[q];
+                sq = a.listed ? a.src_tab[q] : ((volatile int*)a.row_src)[q];
                 vq = ((volatile unsigned*)a.viol)[q];
                 ab = ((volatile unsigned long long*)a.abandoned)[q];
                 ea = ((volatile unsigned long long*)a.early)[q];
@@ -282,10 +282,16 @@ template <bool FMA, bool RNG, bool POLL, bool MOD = false, bool S2 = false>
 __global__ void __launch_bounds__(256, RG_GRID_MINB) k_grid(GridArgs a) {
     __shared__ int s_src;
     __shared__ double s_v;
-    const int i = blockIdx.y;
+    const int i = a.listed ? a.row_list[blockIdx.y] : (int)blockIdx.y;
     if (threadIdx.x < 32) {
         double v;
-        const int src = row_source_warp(a, i, &v);
+        int src;
+        if (a.listed) {  // a simulated row of the host's plan: its setpoint, as row_source
+            v = update_setpoint(a.v_prev, a.r, dvd((double)i, (double)(a.m_grid - 1)));
+            src = -1;
+        } else {
+            src = row_source_warp(a, i, &v);
+        }
         if (threadIdx.x == 0) {
             grid_clock_start(a);
             s_src = src;
@@ -373,7 +379,7 @@ __global__ void __launch_bounds__(256, RG_GRID_MINB) k_grid(GridArgs a) {
 // ---------------------------------------------------------------------------
 
 cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, cudaStream_t s) {
-    dim3 grid(blocks_for(a.n_sim, a.tpb), (unsigned)a.m_grid);
+    dim3 grid(blocks_for(a.n_sim, a.tpb), (unsigned)(a.listed ? a.list_n : a.m_grid));
     // the fused generator exists only in the single-wave two-step form
     if (a.gen && !(a.smem_dyn != 0 && !rng && a.tpb <= kRing4Stride && !a.no_s2))
         return cudaErrorInvalidValue;

@@ -61,6 +61,8 @@ struct XWin {
     int words[2][kXMaxWorld][kXMaxRows];       // [parity][sender][row] per-row verdict words
 };
 
+constexpr int kListMax = 64;  // host-planned grid steps: at most this many candidate rows
+
 struct GridArgs {
     ProblemDev p;
     double x0[3];
@@ -108,6 +110,13 @@ struct GridArgs {
     unsigned long long xepoch, xtimeout_ns;
     XWin* xlocal;
     XWin* const* xpeers;
+    // host-planned rows (listed = 1, m_grid <= kListMax): the host evaluated every row's
+    // setpoint, gate and dedup (the same arithmetic, governor.py:286-317) and launches one
+    // grid row per simulated row only -- blockIdx.y indexes row_list; src_tab is every row's
+    // status (-2 gated out, -1 simulated, >= 0 duplicate of that row) for the extraction
+    int listed, list_n;
+    int row_list[kListMax];
+    int src_tab[kListMax];
 };
 
 // Batch of independent governor instances (episodes).  The host evaluates every

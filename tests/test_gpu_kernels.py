@@ -23,7 +23,7 @@ def ctx():
 
 
 _DEFAULTS = {"force_tpb": 0, "no_placement": 0, "no_pdl": 0, "no_step2": 0, "fused_gen": 0,
-             "batch_chunk": 0}
+             "batch_chunk": 0, "no_row_plan": 0}
 
 
 @pytest.fixture
@@ -434,3 +434,39 @@ def test_dense_host_tensor_staging_equals_generated(ctx, n):
     b_got = ctx.bisect(prob, x0, 0.3, 2.2, 8, dense, n, None)[0]
     assert (b_got.kappa, b_got.found, b_got.cells, b_got.early) == \
         (b_ref.kappa, b_ref.found, b_ref.cells, b_ref.early)
+
+
+@pytest.mark.parametrize("n", [1, 300, 1000, 10_000])
+def test_host_row_plan_equals_device_rows(ctx, tuned, n):
+    """Grid steps without P launch only the host-planned simulated rows (closed-loop steps
+    have about one); against the device-derived rows: same row, per-row counts (gated -1,
+    duplicates their source's), early / overflow counts and row statistics -- in random
+    transient cases with gated and duplicate rows, with and without abandonment."""
+    rng = np.random.default_rng(n)
+    m = rg.DisturbanceModel.scaled(0.02, 3)
+    cases = []
+    for trial in range(16):
+        vp = float(rng.uniform(-1.2, 1.2))
+        r = [float(rng.uniform(-3, 3)), vp, vp + 1e-3, 2.9][trial % 4]
+        x0 = np.array([np.tanh(vp), vp, np.tanh(vp) / 2]) + rng.uniform(-0.06, 0.06, 3)
+        M = int(rng.choice([2, 8, 32, 64]))
+        cases.append((vp, r, x0, M, bool(trial % 3 == 2),
+                      _capi.make_scenarios(300 + trial, 0, n, m.lo, m.span)))
+    prob = _problem(-0.9, 0.9, 0.0, 0.05, 128)
+
+    def run():
+        out = []
+        for vp, r, x0, M, prefix, sc in cases:
+            for abandon in (False, True):
+                res, viol, _ = ctx.grid_step(prob, x0, vp, r, M, prefix, None, n, sc, False,
+                                             abandon=abandon)
+                out.append((res.row, res.sims_run, res.ss_pruned_rows, res.dedup_rows,
+                            res.n_active, (viol == 0).tolist(),
+                            None if abandon else (viol.tolist(), res.early_terms,
+                                                  res.overflows)))
+        return out
+
+    planned = run()
+    tuned(no_row_plan=1)
+    device = run()
+    assert planned == device
