@@ -131,3 +131,18 @@ def test_batch_step_infeasible_policy_error():
             kap, v, feas, _ = rg.robust_rg_parallel_batch(PLANT, X, np.zeros(2), np.full(2, 0.5),
                                                           BOX, model, 50, [1, 2], cfg)
             assert feas.tolist() == [True, False] and v[1] == 0.0
+
+
+@pytest.mark.gpu
+def test_c5_named_size_batch_equals_single_episode_loops():
+    """C5 at its named size for three closed-loop steps: 4096 episodes x 10k scenarios in one
+    batched launch per step (131k candidate rows at t = 0, ~643k blocks of the pairs kernel,
+    the staged chunks of the t = 0 step).  Sampled episodes equal their single-episode loops."""
+    model = rg.DisturbanceModel.scaled(0.001, 3)
+    cfg = rg.GovernorConfig(n_sim=10_000)
+    seeds = [2024 + e for e in range(4096)]
+    recs = run_closed_loop_batch(PLANT, BOX, model, cfg, PROFILE, 3, seeds)
+    assert len(recs) == 4096 and all(len(r.rows) == 3 for r in recs)
+    for e in (0, 1, 1000, 2047, 4095):
+        single = run_closed_loop(PLANT, BOX, model, cfg, PROFILE, 3, seeds[e])
+        assert [row[:6] for row in recs[e].rows] == [row[:6] for row in single.rows], e
