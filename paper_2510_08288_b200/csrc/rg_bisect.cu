@@ -51,7 +51,6 @@ __global__ void __launch_bounds__(256, RG_GRID_MINB) k_joint_roll(JointArgs a, i
     __shared__ int s_run;  // 0 search finished, 1 candidate gated out, 2 roll out
     __shared__ double s_v, s_kappa;
     __shared__ bool s_last;
-    __shared__ unsigned long long s_early;
     if (threadIdx.x == 0) {
         const volatile JointState* st = a.st;
         if (st->done) {

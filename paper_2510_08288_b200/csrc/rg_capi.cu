@@ -220,9 +220,6 @@ rg::ScenarioStream make_stream(const rg_scenarios* s) {
 cudaMemcpyKind kind_h2d(int32_t flags) {
     return (flags & RG_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
 }
-cudaMemcpyKind kind_d2h(int32_t flags) {
-    return (flags & RG_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-}
 
 // Stage a [n_sim][horizon][3] tensor as SoA d[(j*3+i)*ld + k] (rows j < j_star).  From
 // host memory: one pageable cudaMemcpyAsync (the driver pipelines its own pinned staging;

@@ -65,7 +65,7 @@ __device__ __forceinline__ void grid_clock_start(const GridArgs& a) {
 // (0 exactly for the rows feasible on every shard), as the NCCL path does after its
 // all-reduce.  The stats stay this shard's.  A peer missing for xtimeout_ns marks the step
 // failed instead of hanging the GPU.
-__device__ __noinline__ void grid_finalize_xchg(const GridArgs& a, unsigned long long t_fin) {
+__device__ __forceinline__ void grid_finalize_xchg(const GridArgs& a, unsigned long long t_fin) {
     __shared__ int s_w[kXMaxRows];
     __shared__ int s_src[kXMaxRows];
     __shared__ bool s_fail;
