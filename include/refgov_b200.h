@@ -154,10 +154,16 @@ RG_API int32_t rg_get_tanh_variant(rg_ctx *ctx, int32_t *variant);
  * "no_placement", "no_pdl", "no_step2", "fused_gen" (0/1), "batch_chunk" (episodes
  * per staged chunk, 0 = automatic), "xchg_timeout_ms" (fused exchange, default 10000),
  * "no_row_plan" (0/1: grid steps without P derive their rows on the device instead of
- * launching only the host-planned simulated rows).  Defaults come from the RG_FORCE_TPB,
- * RG_NO_PLACEMENT, RG_NO_PDL, RG_NO_STEP2, RG_FUSED_GEN and RG_BATCH_CHUNK environment
- * variables, read once at rg_create.  Unknown names give RG_E_ARGS. */
+ * launching only the host-planned simulated rows), "no_ts" (0/1: never the time-split
+ * grid kernel for host-planned steps with few cells).  Defaults come from the
+ * RG_FORCE_TPB, RG_NO_PLACEMENT, RG_NO_PDL, RG_NO_STEP2, RG_FUSED_GEN, RG_NO_ROW_PLAN,
+ * RG_NO_TS and RG_BATCH_CHUNK environment variables, read once at rg_create.  Unknown
+ * names give RG_E_ARGS. */
 RG_API int32_t rg_set_option(rg_ctx *ctx, const char *name, int64_t value);
+/* Read a knob of rg_set_option, or the read-only "last_grid_kernel": which kernel the
+ * context's last grid step launched (0 = k_grid, one warp per 32 rollouts; 1 = k_grid_ts,
+ * the time-split form). */
+RG_API int32_t rg_get_option(rg_ctx *ctx, const char *name, int64_t *value);
 /* The cudaStream_t the context launches on, as an opaque pointer. */
 RG_API int32_t rg_get_stream(rg_ctx *ctx, void **stream);
 RG_API int32_t rg_synchronize(rg_ctx *ctx);

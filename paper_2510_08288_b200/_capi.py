@@ -120,6 +120,7 @@ SIGNATURES = {
     "rg_destroy": (_i32, [_vp]),
     "rg_get_tanh_variant": (_i32, [_vp, ctypes.POINTER(_i32)]),
     "rg_set_option": (_i32, [_vp, ctypes.c_char_p, _i64]),
+    "rg_get_option": (_i32, [_vp, ctypes.c_char_p, ctypes.POINTER(_i64)]),
     "rg_get_stream": (_i32, [_vp, ctypes.POINTER(_vp)]),
     "rg_synchronize": (_i32, [_vp]),
     "rg_tanh": (_i32, [_vp, _vp, _vp, _i64, _i32]),
@@ -270,6 +271,13 @@ class Context:
     def set_option(self, name: str, value: int) -> None:
         """rg_set_option: a tuning knob of this context (no result bit depends on it)."""
         check(self.lib.rg_set_option(self.handle, name.encode(), int(value)))
+
+    @_locked
+    def get_option(self, name: str) -> int:
+        """rg_get_option: a tuning knob, or "last_grid_kernel" (0 k_grid, 1 k_grid_ts)."""
+        v = _i64(0)
+        check(self.lib.rg_get_option(self.handle, name.encode(), ctypes.byref(v)))
+        return int(v.value)
 
     # -- entry points ---------------------------------------------------
     @_locked

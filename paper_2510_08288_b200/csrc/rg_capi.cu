@@ -133,6 +133,7 @@ struct Tuning {
     int fused_gen = 0;        // single-wave staged step generates its block itself (grid barrier)
     int64_t xchg_timeout_ms = 10000;  // fused exchange: give up on a missing peer after this
     int no_row_plan = 0;      // grid step: rows always derived on the device
+    int no_ts = 0;            // grid step: never the time-split form (rg_ts.cu)
     int64_t batch_chunk = 0;  // batched step: at most this many staged episodes per chunk
 };
 
@@ -147,6 +148,7 @@ struct rg_ctx {
     // grid-step accumulators and outputs
     int grid_cap = 0;
     int last_m = 0;
+    int last_grid_kernel = 0;  // 0 k_grid, 1 k_grid_ts (rg_get_option)
     DevBuf g_viol, g_early, g_ovf, g_aband, g_src, g_ticket, g_t0, g_out, g_bar;
     // bisection accumulators and outputs
     DevBuf b_acc, b_out;
@@ -236,7 +238,7 @@ int32_t stage_dist(rg_ctx* ctx, const double* dist, int64_t n_sim, int64_t horiz
         dsrc = ctx->dist_raw.as<double>();
     }
     *ld = (n_sim + 31) / 32 * 32;
-    RG_CUDA(ctx->soa.ensure((size_t)j_star * 3 * (*ld) * sizeof(double)));
+    RG_CUDA(ctx->soa.ensure((size_t)(j_star + rg::kTsPadSteps) * 3 * (*ld) * sizeof(double)));
     RG_CUDA(rg::launch_to_soa(dsrc, ctx->soa.as<double>(), n_sim, horizon, j_star, *ld,
                               ctx->stream));
     *soa = ctx->soa.as<double>();
@@ -256,7 +258,8 @@ constexpr int64_t kStageMaxScenarioSteps = (16ll << 30) / 24;
 int32_t stage_rng(rg_ctx* ctx, const rg_scenarios* rng, int64_t n_sim, int32_t j_star,
                   const double** soa, int64_t* ld) {
     *ld = (n_sim + 31) / 32 * 32;
-    RG_CUDA(ctx->soa.ensure((size_t)j_star * 3 * (*ld) * sizeof(double)));
+    // kTsPadSteps steps of padding: the time-split step's look-ahead loads (rg_ts.cu)
+    RG_CUDA(ctx->soa.ensure((size_t)(j_star + rg::kTsPadSteps) * 3 * (*ld) * sizeof(double)));
     RG_CUDA(rg::launch_gen_soa(make_stream(rng), rng->k0, n_sim, j_star, *ld,
                                ctx->soa.as<double>(), ctx->stream));
     *soa = ctx->soa.as<double>();
@@ -320,6 +323,7 @@ Tuning env_tuning() {
     if (getenv("RG_FUSED_GEN")) t.fused_gen = 1;
     if (const char* e = getenv("RG_XCHG_TIMEOUT_MS")) t.xchg_timeout_ms = atoll(e);
     if (getenv("RG_NO_ROW_PLAN")) t.no_row_plan = 1;
+    if (getenv("RG_NO_TS")) t.no_ts = 1;
     if (const char* e = getenv("RG_BATCH_CHUNK")) t.batch_chunk = atoll(e);
     if (!(t.force_tpb == 32 || t.force_tpb == 64 || t.force_tpb == 128)) t.force_tpb = 0;
     return t;
@@ -478,6 +482,8 @@ int32_t rg_set_option(rg_ctx* ctx, const char* name, int64_t value) {
         t.fused_gen = value != 0;
     } else if (!strcmp(name, "no_row_plan")) {
         t.no_row_plan = value != 0;
+    } else if (!strcmp(name, "no_ts")) {
+        t.no_ts = value != 0;
     } else if (!strcmp(name, "xchg_timeout_ms")) {
         if (value < 1) return fail(RG_E_ARGS, "xchg_timeout_ms must be >= 1");
         t.xchg_timeout_ms = value;
@@ -487,6 +493,23 @@ int32_t rg_set_option(rg_ctx* ctx, const char* name, int64_t value) {
     } else {
         return fail(RG_E_ARGS, "unknown option '%s'", name);
     }
+    return RG_OK;
+}
+
+int32_t rg_get_option(rg_ctx* ctx, const char* name, int64_t* value) {
+    if (!ctx || !name || !value) return fail(RG_E_ARGS, "null argument");
+    const Tuning& t = ctx->tune;
+    if (!strcmp(name, "force_tpb")) *value = t.force_tpb;
+    else if (!strcmp(name, "no_placement")) *value = t.no_placement;
+    else if (!strcmp(name, "no_pdl")) *value = t.no_pdl;
+    else if (!strcmp(name, "no_step2")) *value = t.no_step2;
+    else if (!strcmp(name, "fused_gen")) *value = t.fused_gen;
+    else if (!strcmp(name, "no_row_plan")) *value = t.no_row_plan;
+    else if (!strcmp(name, "no_ts")) *value = t.no_ts;
+    else if (!strcmp(name, "xchg_timeout_ms")) *value = t.xchg_timeout_ms;
+    else if (!strcmp(name, "batch_chunk")) *value = t.batch_chunk;
+    else if (!strcmp(name, "last_grid_kernel")) *value = ctx->last_grid_kernel;
+    else return fail(RG_E_ARGS, "unknown option '%s'", name);
     return RG_OK;
 }
 
@@ -831,11 +854,22 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
         if (zero_copy && pbits_in_block)
             a.pbits_host = reinterpret_cast<unsigned*>(blk + kOutHead + viol_bytes(m_grid));
     }
+    // A host-planned step whose simulated cells fit one wave of the time-split form
+    // (rg_ts.cu: the x2 chain, the tanh and the x1/x3 chain on separate warps) runs that
+    // instead of one warp per 32 rollouts: a closed-loop step (about one row) is bound by
+    // the rollout's per-step latency, not by FP64 throughput.
+    const int64_t ts_units = (int64_t)grid_rows * ((n_sim + 31) / 32);
+    const bool use_ts = a.listed && !use_rng && !a.gen && !abandon && !ctx->tune.no_ts &&
+                        ts_units <= (int64_t)rg::kTsUnits * ctx->sm_count;
     const bool timed = !(flags & RG_NO_TIMING);
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-    RG_CUDA(rg::launch_grid(a, ctx->variant == rg::kTanhFma, use_rng, abandon, ctx->stream));
+    if (use_ts)
+        RG_CUDA(rg::launch_grid_ts(a, ctx->variant == rg::kTanhFma, ctx->sm_count, ctx->stream));
+    else
+        RG_CUDA(rg::launch_grid(a, ctx->variant == rg::kTanhFma, use_rng, abandon, ctx->stream));
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     ctx->last_m = m_grid;
+    ctx->last_grid_kernel = use_ts ? 1 : 0;
     // rg_grid_fetch reads the pinned block only after a synchronous zero-copy step
     ctx->last_zero_copy = zero_copy;
     if (flags & RG_ASYNC) {

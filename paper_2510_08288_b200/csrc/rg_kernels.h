@@ -63,6 +63,16 @@ struct XWin {
 
 constexpr int kListMax = 64;  // host-planned grid steps: at most this many candidate rows
 
+// The time-split grid step (rg_ts.cu): per block kTsTanhWarps tanh warps and one x2-chain
+// and one x1/x3-chain warp for each of up to kTsUnits units (32 scenarios of a row), chunks
+// of kTsChunk steps through kTsSlots shared-memory slots.  The staged scenario block carries
+// kTsPadSteps steps of padding past j* for the producer's look-ahead loads.
+constexpr int kTsTanhWarps = 12, kTsUnits = 3, kTsChunk = 8, kTsSlots = 3;
+constexpr int kTsThreads = (kTsTanhWarps + 2 * kTsUnits) * 32;
+constexpr int kTsSmemDyn =
+    kTsSlots * kTsChunk * 6 * kTsUnits * 32 * 8 + kTsSlots * kTsUnits * 32 * 4;
+constexpr int kTsPadSteps = 32;
+
 struct GridArgs {
     ProblemDev p;
     double x0[3];
@@ -288,6 +298,9 @@ cudaError_t launch_gen_soa_batch(const uint64_t* hs, const double* lo, const dou
                                  int64_t k0, int64_t n_sim, int32_t j_star, int64_t ld,
                                  int32_t n_ep, int64_t ep_stride, double* dst, cudaStream_t s);
 cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, cudaStream_t s);
+// the time-split form (rg_ts.cu): staged scenarios, no polling; ts_blocks = its grid size
+int ts_blocks(int64_t units, int sms);
+cudaError_t launch_grid_ts(const GridArgs& a, bool fma, int sms, cudaStream_t s);
 // Pairs [a.p0, a.p0 + n_pairs) of the compacted list, a.bpr blocks of a.tpb threads each.
 cudaError_t launch_grid_batch(const BatchArgs& a, int64_t n_pairs, bool fma, bool poll,
                               cudaStream_t s);

@@ -1,0 +1,245 @@
+// rg_ts.cu -- the time-split grid step (k_grid_ts) for steps with few simulated cells.
+//
+// A closed-loop governor step simulates about one candidate row:
+// 10k scenarios are 313 warps, a fraction of one per SM sub-partition, and one warp
+// running a whole rollout (k_grid) is bound by the latency of its per-step chain
+// (~790 cycles per RK4 step on the B200, four tanh chains deep).  But only the x2
+// recurrence (dx2/dt = -x2 + v, the tanh arguments) and the x1/x3 recurrences are
+// sequential: the four tanh of every step depend on the x2 chain alone (rg_cell.cuh), so
+// they can be evaluated by other warps, ahead of the x1/x3 chain that consumes them.
+//
+// k_grid_ts splits each cell's rollout over three kinds of warps, per block of up to
+// kTsUnits units (a unit = 32 scenarios of one simulated row, one P-bit word):
+//   P (one per unit)  the x2 chain: writes each step's four tanh arguments and the
+//                     consumer's disturbances d0/d2 into a shared-memory chunk slot;
+//   T (kTsTanhWarps)  evaluate the slot's tanh (tanhN_with, the same warp-uniform forms as
+//                     the rollouts) in place, 32 lanes of one unit and step per batch;
+//   C (one per unit)  the x1/x3 chain and the per-step checks, reading the slot's tanh
+//                     values; then the unit's verdicts into the per-row counters.
+// Chunks of kTsChunk steps cycle through kTsSlots slots with named barriers per slot:
+// FULL_G (P -> T), FULL_T (T -> C), EMPTY (C -> P).  Every operation, operand and
+// rounding is the reference's (sfc_step); only which warp performs it changes, so the
+// verdicts are bit-identical to k_grid's (tests/test_gpu_kernels.py).  No cell exits
+// early: a finished cell's state runs on unobserved to the chunk's end, so status and
+// step count are the reference's and the counters k_grid's.
+//
+// Used for host-planned (listed) steps without P-bit polling whose units fit one wave
+// (rg_capi.cu: use_ts); the scenario block is the staged SoA, padded by kTsPadSteps steps
+// so the producer's look-ahead loads never leave the buffer.
+#include "rg_grid.cuh"
+
+namespace rg {
+
+namespace {
+
+__device__ __forceinline__ void nb_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void nb_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+constexpr int TW = kTsTanhWarps, RW = kTsUnits, CH = kTsChunk, S = kTsSlots;
+constexpr int kG = CH * 4 * RW * 32;  // doubles: tanh arguments / values of a slot
+constexpr int kD = CH * 2 * RW * 32;  // doubles: d0, d2 of a slot
+constexpr int kSlot = kG + kD;
+// named barriers (0 is __syncthreads): FULL_G 1..S, FULL_T S+1..2S, EMPTY 2S+1..3S
+constexpr int kBarG = 1, kBarT = 1 + S, kBarE = 1 + 2 * S;
+constexpr int nG = (TW + RW) * 32, nT = (TW + RW) * 32, nE = 2 * RW * 32;
+static_assert(3 * S < 16, "named barriers");
+static_assert(kTsThreads == (TW + 2 * RW) * 32, "block shape");
+static_assert(kTsSmemDyn == S * kSlot * 8 + S * RW * 32 * 4, "shared memory");
+static_assert(kTsPadSteps >= 2 * CH, "look-ahead padding");
+
+}  // namespace
+
+template <bool FMA>
+__global__ void __launch_bounds__(kTsThreads, 1) k_grid_ts(GridArgs a) {
+    extern __shared__ double sm[];
+    unsigned* OV = reinterpret_cast<unsigned*>(sm + S * kSlot);  // [S][RW][32]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) grid_clock_start(a);
+    const int W = (int)((a.n_sim + 31) / 32);
+    const int n_rows = a.listed ? a.list_n : a.m_grid;
+    const int64_t units = (int64_t)n_rows * W;
+    const int u0 = (int)(blockIdx.x * units / gridDim.x);
+    const int u1 = (int)((blockIdx.x + 1) * units / gridDim.x);
+    const int rw = u1 - u0;
+    const int J = a.p.j_star;
+    const int nch = (J + CH - 1) / CH;
+    // the staged scenario block may still be being written (PDL behind k_gen_soa)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (warp < TW) {
+        // T: slot by slot, batches (unit rr, step st) round-robin over the T warps
+        const int nbat = rw * CH;
+        int slot = 0;
+        for (int g = 0; g < nch; ++g) {
+            nb_sync(kBarG + slot, nG);
+            double* Gs = sm + slot * kSlot;
+            for (int b = warp; b < nbat; b += TW) {
+                const int rr = b / CH, st = b % CH;
+                double x[4], z[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) x[q] = Gs[((st * 4 + q) * RW + rr) * 32 + lane];
+                tanhN_with<FMA, true, 4>(x, z, [] {});
+#pragma unroll
+                for (int q = 0; q < 4; ++q) Gs[((st * 4 + q) * RW + rr) * 32 + lane] = z[q];
+            }
+            nb_arrive(kBarT + slot, nT);
+            slot = slot == S - 1 ? 0 : slot + 1;
+        }
+    } else {
+        const bool is_p = warp < TW + RW;
+        const int r = is_p ? warp - TW : warp - TW - RW;
+        const int ridx = r * 32 + lane;
+        if (r >= rw) {  // no unit in this block: keep the barrier counts
+            int slot = 0;
+            for (int g = 0; g < nch; ++g) {
+                if (is_p) {
+                    if (g >= S) nb_sync(kBarE + slot, nE);
+                    nb_arrive(kBarG + slot, nG);
+                } else {
+                    nb_sync(kBarT + slot, nT);
+                    nb_arrive(kBarE + slot, nE);
+                }
+                slot = slot == S - 1 ? 0 : slot + 1;
+            }
+        } else {
+            const int u = u0 + r;
+            const int q = u / W;
+            const int i = a.listed ? a.row_list[q] : q;  // the grid row
+            const int wd = u - q * W;                     // its P-bit word
+            const int64_t sc = (int64_t)wd * 32 + lane;
+            const bool live = sc < a.n_sim;
+            const CellConst p = make_cell(a.p);
+            const int64_t ld = a.ld, st3 = 3 * a.ld;
+            if (is_p) {
+                // P: the x2 chain.  Registers one chunk ahead: this chunk's d1 (the chain)
+                // and d0/d2 (staged for C); the next chunk's load while this one runs.
+                const double v =
+                    update_setpoint(a.v_prev, a.r, dvd((double)i, (double)(a.m_grid - 1)));
+                const double* d = a.soa + (live ? sc : 0);
+                double x2p = a.x0[1];
+                double d1c[CH], d0c[CH], d2c[CH];
+#pragma unroll
+                for (int s = 0; s < CH; ++s) {
+                    d1c[s] = __ldg(d + s * st3 + ld);
+                    d0c[s] = __ldg(d + s * st3);
+                    d2c[s] = __ldg(d + s * st3 + 2 * ld);
+                }
+                int slot = 0;
+                for (int g = 0; g < nch; ++g) {
+                    double d0n[CH], d2n[CH], d1n[CH];
+#pragma unroll
+                    for (int s = 0; s < CH; ++s) {  // chunk g+1 (inside the padding at the end)
+                        d0n[s] = __ldg(d + (CH + s) * st3);
+                        d2n[s] = __ldg(d + (CH + s) * st3 + 2 * ld);
+                        d1n[s] = __ldg(d + (CH + s) * st3 + ld);
+                    }
+                    if (g >= S) nb_sync(kBarE + slot, nE);  // C is done with chunk g - S
+                    double* Ss = sm + slot * kSlot;
+                    unsigned ov = 0u;
+#pragma unroll
+                    for (int s = 0; s < CH; ++s) {
+                        const X2Stage st = x2_stage<FMA>(x2p, v, p);
+                        Ss[(s * 4 + 0) * RW * 32 + ridx] = x2p;
+                        Ss[(s * 4 + 1) * RW * 32 + ridx] = st.a2;
+                        Ss[(s * 4 + 2) * RW * 32 + ridx] = st.b2;
+                        Ss[(s * 4 + 3) * RW * 32 + ridx] = st.c2;
+                        Ss[kG + (s * 2 + 0) * RW * 32 + ridx] = d0c[s];
+                        Ss[kG + (s * 2 + 1) * RW * 32 + ridx] = d2c[s];
+                        x2p = add(add(x2p, mul(p.c, st.s2)), d1c[s]);
+                        // step s's overflow test on x2 (x2 after the step)
+                        ov |= (fabs(x2p) <= kStateLimit ? 0u : 1u) << s;
+                    }
+#pragma unroll
+                    for (int s = 0; s < CH; ++s) {
+                        d0c[s] = d0n[s];
+                        d2c[s] = d2n[s];
+                        d1c[s] = d1n[s];
+                    }
+                    OV[slot * RW * 32 + ridx] = ov;
+                    nb_arrive(kBarG + slot, nG);
+                    d += CH * st3;
+                    slot = slot == S - 1 ? 0 : slot + 1;
+                }
+            } else {
+                // C: the x1/x3 chain, the reference's checks in its order (overflow, then
+                // the output bound), status and step count of the first failing step
+                double x1 = a.x0[0], x3 = a.x0[2];
+                int status = kOk, steps = J;
+                bool done = !live;
+                if (live && !in_bounds(x1, p.ylo, p.yhi)) {
+                    steps = 0;
+                    status = kViolated;
+                    done = true;
+                }
+                int slot = 0;
+                for (int g = 0; g < nch; ++g) {
+                    nb_sync(kBarT + slot, nT);
+                    const double* Cs = sm + slot * kSlot + ridx;
+                    const unsigned ovc = OV[slot * RW * 32 + ridx];
+                    double t[CH][4], dd[CH][2];
+#pragma unroll
+                    for (int s = 0; s < CH; ++s) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) t[s][k] = Cs[(s * 4 + k) * RW * 32];
+                        dd[s][0] = Cs[kG + (s * 2 + 0) * RW * 32];
+                        dd[s][1] = Cs[kG + (s * 2 + 1) * RW * 32];
+                    }
+                    // the slot is read out (bar.arrive orders the loads before it): P may
+                    // refill it while the chain below runs
+                    nb_arrive(kBarE + slot, nE);
+#pragma unroll
+                    for (int s = 0; s < CH; ++s) {
+                        const int j = g * CH + s;
+                        x13_update<FMA>(x1, x3, t[s][0], t[s][1], t[s][2], t[s][3], p,
+                                        dd[s][0], dd[s][1]);
+                        const bool ovf = !(fabs(x1) <= kStateLimit && !((ovc >> s) & 1u) &&
+                                           fabs(x3) <= kStateLimit);
+                        const bool bnd = !in_bounds(x1, p.ylo, p.yhi);
+                        const bool now = !done && j < J && (ovf || bnd);
+                        status = now ? (ovf ? kOverflow : kViolated) : status;
+                        steps = now ? j + 1 : steps;
+                        done = done || now;
+                    }
+                    slot = slot == S - 1 ? 0 : slot + 1;
+                }
+                // the unit's verdicts, as k_grid's warp epilogue
+                const bool bad = live && status != kOk;
+                const unsigned bad_mask = __ballot_sync(0xffffffffu, bad);
+                if (lane == 0 && bad_mask) atomicAdd(a.viol + i, (unsigned)__popc(bad_mask));
+                warp_count_add(live && steps < J, a.early + i);
+                warp_count_add(live && status == kOverflow, a.ovf + i);
+                if (a.pbits) {
+                    const unsigned ok_mask = __ballot_sync(0xffffffffu, live && status == kOk);
+                    if (lane == 0) a.pbits[(int64_t)i * a.pwords + wd] = ok_mask;
+                }
+            }
+        }
+    }
+    grid_finalize(a);
+}
+
+// Blocks for `units` units: one wave of at most kTsUnits units per block, at least one
+// block per SM while there are units to spread.
+int ts_blocks(int64_t units, int sms) {
+    const int64_t by_units = (units + kTsUnits - 1) / kTsUnits;
+    return (int)std::max<int64_t>(std::min<int64_t>(sms, units), by_units);
+}
+
+cudaError_t launch_grid_ts(const GridArgs& a, bool fma, int sms, cudaStream_t s) {
+    const int64_t units = (int64_t)(a.listed ? a.list_n : a.m_grid) * ((a.n_sim + 31) / 32);
+    const int nblk = ts_blocks(units, sms);
+    const void* fn = fma ? (const void*)k_grid_ts<true> : (const void*)k_grid_ts<false>;
+    int dyn = 0;
+    // pin_smem takes the block's total: the static part (the finalize's) is well below 4 KB
+    cudaError_t e = pin_smem(fn, kTsSmemDyn + 4096, &dyn);
+    if (e != cudaSuccess) return e;
+    e = fma ? launch_ex(k_grid_ts<true>, dim3(nblk), kTsThreads, (size_t)dyn, s, a.pdl != 0, a)
+            : launch_ex(k_grid_ts<false>, dim3(nblk), kTsThreads, (size_t)dyn, s, a.pdl != 0, a);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+}  // namespace rg

@@ -17,8 +17,12 @@ prob = _capi.Problem(0.01, -0.9, 0.9, lo, hi, 256, 0)
 m = rg.DisturbanceModel.scaled(0.001, 3)
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 res = _capi.GridResult()
-SETS = {"plan+s2": dict(no_row_plan=0, no_step2=0), "plan+s1": dict(no_row_plan=0, no_step2=1),
-        "device rows": dict(no_row_plan=1, no_step2=0)}
+SETS = {"plan+ts": dict(no_row_plan=0, no_step2=0, no_ts=0),
+        "plan+s2 (no ts)": dict(no_row_plan=0, no_step2=0, no_ts=1),
+        "device rows": dict(no_row_plan=1, no_step2=0, no_ts=1)}
+if len(sys.argv) > 1 and sys.argv[1] == "ts":  # the time-split A/B only, twice
+    SETS = {"plan+ts": SETS["plan+ts"], "plan+s2 (no ts)": SETS["plan+s2 (no ts)"],
+            "plan+ts again": SETS["plan+ts"], "plan+s2 again": SETS["plan+s2 (no ts)"]}
 
 
 def step_time(n, vp, r, reps=30):

@@ -23,7 +23,7 @@ def ctx():
 
 
 _DEFAULTS = {"force_tpb": 0, "no_placement": 0, "no_pdl": 0, "no_step2": 0, "fused_gen": 0,
-             "batch_chunk": 0, "no_row_plan": 0}
+             "batch_chunk": 0, "no_row_plan": 0, "no_ts": 0}
 
 
 @pytest.fixture
@@ -470,3 +470,51 @@ def test_host_row_plan_equals_device_rows(ctx, tuned, n):
     tuned(no_row_plan=1)
     device = run()
     assert planned == device
+
+
+@pytest.mark.parametrize("j_star", [1, 5, 8, 9, 17, 256])
+@pytest.mark.parametrize("n", [1, 33, 1000, 10_000, 13_000])
+def test_time_split_step_equals_k_grid(ctx, tuned, n, j_star):
+    """Host-planned steps whose cells fit one wave run the time-split kernel (rg_ts.cu: the
+    x2 chain, the tanh and the x1/x3 chain on separate warps); against k_grid (no_ts):
+    the same row, per-row violation counts, early-termination and overflow counts -- in
+    transient cases (violations at every step count, out-of-bounds starts, overflowing
+    states), from generated and from dense host scenarios, chunk-ragged horizons."""
+    rng = np.random.default_rng(7 * n + j_star)
+    m = rg.DisturbanceModel.scaled(0.02, 3)
+    prob = _problem(-0.9, 0.9, 0.0, 0.05, j_star)
+    cases = []
+    for trial in range(6):
+        vp = float(rng.uniform(-1.2, 1.2))
+        # r == vp: every candidate is vp, one simulated row (the closed loop's steady state)
+        r = [float(rng.uniform(-3, 3)), vp + 1e-3, vp][trial % 3]
+        x0 = np.array([np.tanh(vp), vp, np.tanh(vp) / 2]) + rng.uniform(-0.08, 0.08, 3)
+        if trial == 4:
+            x0[0] = 0.95  # out of bounds at the start: steps 0
+        if trial == 5:
+            x0[2] = 1.5e6  # beyond STATE_LIMIT: the first step overflows
+        cases.append((vp, r, x0, [8, 32][trial % 2], trial % 4 == 3,
+                      _capi.make_scenarios(900 + trial, 0, n, m.lo, m.span)))
+    dense = rg.sample_scenarios(m, n, j_star + 1, seed=77).data
+
+    kernels = []
+
+    def run():
+        out = []
+        for vp, r, x0, M, prefix, sc in cases:
+            for dist, scen in ((None, sc), (dense, None)):
+                res, viol, _ = ctx.grid_step(prob, x0, vp, r, M, prefix, dist, n, scen, False)
+                out.append((res.row, res.sims_run, res.n_active, viol.tolist(),
+                            res.early_terms, res.overflows))
+                kernels.append(ctx.get_option("last_grid_kernel"))
+        return out
+
+    ts = run()
+    assert 1 in kernels  # the time-split kernel ran (one wave holds <= 3 units per SM)
+    tuned(no_ts=1)
+    kernels.clear()
+    ref = run()
+    assert set(kernels) == {0}
+    assert ts == ref
+    # the cases exercise the verdict paths: some violations, some overflow
+    assert any(o[4] > 0 for o in ref) and any(o[5] > 0 for o in ref)
