@@ -1,12 +1,12 @@
 // rg_ts.cu -- the time-split grid step (k_grid_ts) for steps with few simulated cells.
 //
 // A closed-loop governor step simulates about one candidate row:
-// 10k scenarios are 313 warps, a fraction of one per SM sub-partition, and one warp
-// running a whole rollout (k_grid) is bound by the latency of its per-step chain
-// (~790 cycles per RK4 step on the B200, four tanh chains deep).  But only the x2
-// recurrence (dx2/dt = -x2 + v, the tanh arguments) and the x1/x3 recurrences are
-// sequential: the four tanh of every step depend on the x2 chain alone (rg_cell.cuh), so
-// they can be evaluated by other warps, ahead of the x1/x3 chain that consumes them.
+// 10k scenarios are 313 warps, half a warp per SM sub-partition, and one warp running a
+// whole rollout (k_grid) is bound by the latency of its per-step chain (~790 cycles per
+// RK4 step, four tanh deep).  But only the x2 recurrence (dx2/dt = -x2 + v: the tanh
+// arguments) and the x1/x3 recurrences are sequential: the four tanh of every step depend
+// on the x2 chain alone (rg_cell.cuh), so other warps can evaluate them, ahead of the
+// x1/x3 chain that consumes them.
 //
 // k_grid_ts splits each cell's rollout over three kinds of warps, per block of up to
 // kTsUnits units (a unit = 32 scenarios of one simulated row, one P-bit word):
@@ -15,15 +15,27 @@
 //   T (kTsTanhWarps)  evaluate the slot's tanh (tanhN_with, the same warp-uniform forms as
 //                     the rollouts) in place, 32 lanes of one unit and step per batch;
 //   C (one per unit)  the x1/x3 chain and the per-step checks, reading the slot's tanh
-//                     values; then the unit's verdicts into the per-row counters.
+//                     values one step ahead; then the unit's verdicts into the per-row
+//                     counters and the P bits.
 // Chunks of kTsChunk steps cycle through kTsSlots slots with named barriers per slot:
 // FULL_G (P -> T), FULL_T (T -> C), EMPTY (C -> P).  Every operation, operand and
 // rounding is the reference's (sfc_step); only which warp performs it changes, so the
-// verdicts are bit-identical to k_grid's (tests/test_gpu_kernels.py).  No cell exits
-// early: a finished cell's state runs on unobserved to the chunk's end, so status and
-// step count are the reference's and the counters k_grid's.
+// verdicts are bit-identical to k_grid's (tests/test_gpu_kernels.py: test_time_split_*,
+// and the whole 2000-step C3 golden trace runs through here).  No cell exits early: a
+// finished cell's state runs on unobserved to the end, so status and step count are the
+// reference's and the counters k_grid's.
 //
-// Used for host-planned (listed) steps without P-bit polling whose units fit one wave
+// Measured (profiles/r02_ab_time_split.txt, r02_ts_timeline_*.txt; RG_TS_TIMELINE build):
+// a one-row step is 0.054 ms at 1k scenarios (k_grid 0.099) and 0.099 ms at 10k (0.120);
+// C3 0.139-0.143 ms per closed-loop step (0.167).  At 10k the tanh warps are the busy
+// stage (~3.2k of ~3.5k cycles per chunk: the 17-24 batches of a block over 12 warps);
+// at 1k the producer (the prefetched loads land in the registers its chain reads, so the
+// next chunk's loads issue after this chunk's stores) sets the ~2.6k-cycle period.
+// Variants measured and not kept: tanh warps on two sub-partitions and the chains alone on
+// the others (10k 0.124 ms), the chains alone on one sub-partition (0.106), cp.async
+// staging of the disturbances with four slots (0.103), 8 tanh warps (0.104-0.108).
+//
+// Used for host-planned (listed) steps without polling whose units fit one wave
 // (rg_capi.cu: use_ts); the scenario block is the staged SoA, padded by kTsPadSteps steps
 // so the producer's look-ahead loads never leave the buffer.
 #include "rg_grid.cuh"
@@ -39,6 +51,20 @@ __device__ __forceinline__ void nb_arrive(int id, int n) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// bar.arrive that passes two doubles through (bit-exact moves): the computation that
+// depends on them cannot be scheduled above the arrive
+__device__ __forceinline__ void nb_arrive_pass(int id, int n, double& x, double& y) {
+    asm volatile("bar.arrive %2, %3;\n\tmov.b64 %0, %0;\n\tmov.b64 %1, %1;"
+                 : "+d"(x), "+d"(y) : "r"(id), "r"(n) : "memory");
+}
+// shared-memory load in program order (volatile): a chunk's values are all loaded up
+// front instead of one latency at a time next to their uses
+__device__ __forceinline__ double lds_v(const double* p) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+    return v;
+}
+
 constexpr int TW = kTsTanhWarps, RW = kTsUnits, CH = kTsChunk, S = kTsSlots;
 constexpr int kG = CH * 4 * RW * 32;  // doubles: tanh arguments / values of a slot
 constexpr int kD = CH * 2 * RW * 32;  // doubles: d0, d2 of a slot
@@ -52,6 +78,29 @@ static_assert(kTsSmemDyn == S * kSlot * 8 + S * RW * 32 * 4, "shared memory");
 static_assert(kTsPadSteps >= 2 * CH, "look-ahead padding");
 
 }  // namespace
+
+#ifdef RG_TS_TIMELINE
+// Instrumented build only (make EXTRA=-DRG_TS_TIMELINE): block 0's per-warp, per-chunk
+// clock64 stamps [warp][chunk][2] -- T: (go, done), P: (start, arrive), C: (go, done) --
+// read back with rg_ts_timeline (scripts/prof_ts.py).
+__device__ long long g_ts_tl[kTsThreads / 32][64][2];
+#define RG_TS_STAMP(g, k, t)                                                            \
+    do {                                                                               \
+        if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (g) < 64) g_ts_tl[warp][g][k] = (t); \
+    } while (0)
+__device__ __forceinline__ long long ts_clock_after(const unsigned* w) {
+    const unsigned x = *(volatile const unsigned*)w;  // issued after the barrier
+    long long t = clock64();
+    if (x == 0x9e3779b9u) t += 1;  // depends on the load: the barrier is behind us
+    return t;
+}
+#define RG_TS_STAMP_AFTER(g, k) RG_TS_STAMP(g, k, ts_clock_after(OV))
+#else
+#define RG_TS_STAMP(g, k, t) \
+    do {                     \
+    } while (0)
+#define RG_TS_STAMP_AFTER(g, k) RG_TS_STAMP(g, k, 0)
+#endif
 
 template <bool FMA>
 __global__ void __launch_bounds__(kTsThreads, 1) k_grid_ts(GridArgs a) {
@@ -75,6 +124,7 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_grid_ts(GridArgs a) {
         int slot = 0;
         for (int g = 0; g < nch; ++g) {
             nb_sync(kBarG + slot, nG);
+            RG_TS_STAMP_AFTER(g, 0);
             double* Gs = sm + slot * kSlot;
             for (int b = warp; b < nbat; b += TW) {
                 const int rr = b / CH, st = b % CH;
@@ -85,6 +135,7 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_grid_ts(GridArgs a) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) Gs[((st * 4 + q) * RW + rr) * 32 + lane] = z[q];
             }
+            RG_TS_STAMP(g, 1, clock64());
             nb_arrive(kBarT + slot, nT);
             slot = slot == S - 1 ? 0 : slot + 1;
         }
@@ -136,6 +187,7 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_grid_ts(GridArgs a) {
                         d2n[s] = __ldg(d + (CH + s) * st3 + 2 * ld);
                         d1n[s] = __ldg(d + (CH + s) * st3 + ld);
                     }
+                    RG_TS_STAMP(g, 0, clock64());
                     if (g >= S) nb_sync(kBarE + slot, nE);  // C is done with chunk g - S
                     double* Ss = sm + slot * kSlot;
                     unsigned ov = 0u;
@@ -159,6 +211,7 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_grid_ts(GridArgs a) {
                         d1c[s] = d1n[s];
                     }
                     OV[slot * RW * 32 + ridx] = ov;
+                    RG_TS_STAMP(g, 1, clock64());
                     nb_arrive(kBarG + slot, nG);
                     d += CH * st3;
                     slot = slot == S - 1 ? 0 : slot + 1;
@@ -177,24 +230,31 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_grid_ts(GridArgs a) {
                 int slot = 0;
                 for (int g = 0; g < nch; ++g) {
                     nb_sync(kBarT + slot, nT);
+                    RG_TS_STAMP_AFTER(g, 0);
                     const double* Cs = sm + slot * kSlot + ridx;
                     const unsigned ovc = OV[slot * RW * 32 + ridx];
-                    double t[CH][4], dd[CH][2];
+                    // one step of look-ahead: step s+1's six values load while step s runs
+                    double tn[4], dn[2];
+                    auto load = [&](int s) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) tn[k] = lds_v(Cs + (s * 4 + k) * RW * 32);
+                        dn[0] = lds_v(Cs + kG + (s * 2 + 0) * RW * 32);
+                        dn[1] = lds_v(Cs + kG + (s * 2 + 1) * RW * 32);
+                    };
+                    load(0);
 #pragma unroll
                     for (int s = 0; s < CH; ++s) {
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) t[s][k] = Cs[(s * 4 + k) * RW * 32];
-                        dd[s][0] = Cs[kG + (s * 2 + 0) * RW * 32];
-                        dd[s][1] = Cs[kG + (s * 2 + 1) * RW * 32];
-                    }
-                    // the slot is read out (bar.arrive orders the loads before it): P may
-                    // refill it while the chain below runs
-                    nb_arrive(kBarE + slot, nE);
-#pragma unroll
-                    for (int s = 0; s < CH; ++s) {
+                        const double t1 = tn[0], t2 = tn[1], t3 = tn[2], t4 = tn[3];
+                        const double d0 = dn[0], d2 = dn[1];
+                        if (s + 1 < CH) {
+                            load(s + 1);
+                        } else {
+                            // the slot is read out (bar.arrive orders the loads before it):
+                            // P may refill it
+                            nb_arrive_pass(kBarE + slot, nE, x1, x3);
+                        }
                         const int j = g * CH + s;
-                        x13_update<FMA>(x1, x3, t[s][0], t[s][1], t[s][2], t[s][3], p,
-                                        dd[s][0], dd[s][1]);
+                        x13_update<FMA>(x1, x3, t1, t2, t3, t4, p, d0, d2);
                         const bool ovf = !(fabs(x1) <= kStateLimit && !((ovc >> s) & 1u) &&
                                            fabs(x3) <= kStateLimit);
                         const bool bnd = !in_bounds(x1, p.ylo, p.yhi);
@@ -203,6 +263,7 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_grid_ts(GridArgs a) {
                         steps = now ? j + 1 : steps;
                         done = done || now;
                     }
+                    RG_TS_STAMP(g, 1, clock64() + (long long)(x1 == 12345.0));
                     slot = slot == S - 1 ? 0 : slot + 1;
                 }
                 // the unit's verdicts, as k_grid's warp epilogue
@@ -220,6 +281,12 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_grid_ts(GridArgs a) {
     }
     grid_finalize(a);
 }
+
+#ifdef RG_TS_TIMELINE
+extern "C" __attribute__((visibility("default"))) int rg_ts_timeline(long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, g_ts_tl, sizeof(g_ts_tl));
+}
+#endif
 
 // Blocks for `units` units: one wave of at most kTsUnits units per block, at least one
 // block per SM while there are units to spread.
