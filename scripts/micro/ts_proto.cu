@@ -26,6 +26,7 @@ struct TsArgs {
     int* status;
     int* steps;
     long long* prof;  // [block][warp][2]: cycles waiting, cycles total (k_ts3, if set)
+    long long* tl;    // block 0 timeline: [warp][chunk][2]
 };
 
 __device__ __forceinline__ void nb_sync(int id, int n) {
@@ -444,7 +445,8 @@ __global__ void __launch_bounds__((TW + 2 * RW) * 32, 1) k_ts3(TsArgs a) {
         const int nbat = rw * CH;
         int slot = 0;
         for (int g = 0; g < nch; ++g) {
-            { const long long t0 = clock64(); nb_sync(1 + slot, nG); t_wait += clock_after(OV) - t0; }
+            { const long long t0 = clock64(); nb_sync(1 + slot, nG); const long long t1 = clock_after(OV); t_wait += t1 - t0;
+              if (a.tl && blockIdx.x == 0 && lane == 0 && g < 64) a.tl[(warp * 64 + g) * 2] = t1; }
             double* Gs = sm + slot * kSlot;
             for (int b = warp; b < nbat; b += TW) {
                 const int rr = b / CH, st = b % CH;
@@ -455,6 +457,7 @@ __global__ void __launch_bounds__((TW + 2 * RW) * 32, 1) k_ts3(TsArgs a) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) Gs[((st * 4 + q) * RW + rr) * 32 + lane] = z[q];
             }
+            if (a.tl && blockIdx.x == 0 && lane == 0 && g < 64) a.tl[(warp * 64 + g) * 2 + 1] = clock64();
             nb_arrive(4 + slot, nT);
             slot = slot == S - 1 ? 0 : slot + 1;
         }
@@ -506,6 +509,7 @@ __global__ void __launch_bounds__((TW + 2 * RW) * 32, 1) k_ts3(TsArgs a) {
                 d2n[s] = __ldg(d + (CH + s) * st3 + 2 * ld);
                 d1n[s] = __ldg(d + (CH + s) * st3 + ld);
             }
+            if (a.tl && blockIdx.x == 0 && lane == 0 && g < 64) a.tl[(warp * 64 + g) * 2] = clock64();
             if (g >= S) { const long long t0 = clock64(); nb_sync(7 + slot, nE); t_wait += clock_after(OV) - t0; }
             double* Ss = sm + slot * kSlot;
             unsigned ov = 0u;
@@ -528,6 +532,7 @@ __global__ void __launch_bounds__((TW + 2 * RW) * 32, 1) k_ts3(TsArgs a) {
                 d1c[s] = d1n[s];
             }
             OV[slot * RW * 32 + ridx] = ov;
+            if (a.tl && blockIdx.x == 0 && lane == 0 && g < 64) a.tl[(warp * 64 + g) * 2 + 1] = clock64();
             nb_arrive(1 + slot, nG);
             d += CH * st3;
             slot = slot == S - 1 ? 0 : slot + 1;
@@ -549,7 +554,9 @@ __global__ void __launch_bounds__((TW + 2 * RW) * 32, 1) k_ts3(TsArgs a) {
     for (int g = 0; g < nch; ++g) {
         const long long t0 = clock64();
         const uint32_t tok = nb_sync_tok(4 + slot, nT);
-        t_wait += clock_after(OV) - t0;
+        const long long t1 = clock_after(OV);
+        t_wait += t1 - t0;
+        if (a.tl && blockIdx.x == 0 && lane == 0 && g < 64) a.tl[(warp * 64 + g) * 2] = t1;
         const uint32_t ca = sbase + 8u * (uint32_t)(slot * kSlot + ridx) + tok;
         const unsigned ovc = OV[slot * RW * 32 + ridx];
         double t[CH][4], dd[CH][2];
@@ -575,6 +582,7 @@ __global__ void __launch_bounds__((TW + 2 * RW) * 32, 1) k_ts3(TsArgs a) {
             steps = now ? j + 1 : steps;
             done = done || now;
         }
+        if (a.tl && blockIdx.x == 0 && lane == 0 && g < 64) a.tl[(warp * 64 + g) * 2 + 1] = clock64() + (long long)(x1 == 12345.0);
         slot = slot == S - 1 ? 0 : slot + 1;
     }
     prof_out();
@@ -675,6 +683,8 @@ int main(int argc, char** argv) {
     std::vector<double> vrow(M);
     for (int i = 0; i < M; ++i) vrow[i] = (transient ? 2.5 : 0.5) * (M > 1 ? i / (double)(M - 1) : 0.5);
     TsArgs a{};
+    a.tl = nullptr;
+    a.prof = nullptr;
     double *d_soa, *d_v;
     int *st_ref, *sp_ref, *st_ts, *sp_ts;
     CK(cudaMalloc(&d_soa, h_soa.size() * 8));
@@ -729,6 +739,23 @@ int main(int argc, char** argv) {
     CK(cudaMalloc(&d_prof, 4096 * 32 * 2 * 8));
     CK(cudaMemset(d_prof, 0, 4096 * 32 * 2 * 8));
     a.prof = d_prof;
+    long long* d_tl;
+    CK(cudaMalloc(&d_tl, 32 * 64 * 2 * 8));
+    CK(cudaMemset(d_tl, 0, 32 * 64 * 2 * 8));
+    a.tl = d_tl;
+    check("v3 TW12 RW3 CH8", run_ts3<12, 3, 8>(a, sms, 50));
+    {
+        std::vector<long long> tl(32 * 64 * 2);
+        CK(cudaMemcpy(tl.data(), d_tl, tl.size() * 8, cudaMemcpyDeviceToHost));
+        const long long base = tl[(12 * 64 + 0) * 2];
+        printf("  timeline (kcycles from P0 start): chunk: P0[start,arrive] T0[go,done] C0[go,done]\n");
+        for (int g = 0; g < 32; g += 1)
+            printf("   %2d: P %.2f %.2f | T %.2f %.2f | C %.2f %.2f\n", g,
+                   (tl[(12 * 64 + g) * 2] - base) / 1e3, (tl[(12 * 64 + g) * 2 + 1] - base) / 1e3,
+                   (tl[(0 * 64 + g) * 2] - base) / 1e3, (tl[(0 * 64 + g) * 2 + 1] - base) / 1e3,
+                   (tl[(15 * 64 + g) * 2] - base) / 1e3, (tl[(15 * 64 + g) * 2 + 1] - base) / 1e3);
+    }
+    a.tl = nullptr;
     check("v3 TW8 RW3 CH8", run_ts3<8, 3, 8>(a, sms, 50));
     {
         std::vector<long long> hp(32 * 2 * 2);
