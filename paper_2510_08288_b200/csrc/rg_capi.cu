@@ -134,6 +134,7 @@ struct Tuning {
     int64_t xchg_timeout_ms = 10000;  // fused exchange: give up on a missing peer after this
     int no_row_plan = 0;      // grid step: rows always derived on the device
     int no_ts = 0;            // grid step: never the time-split form (rg_ts.cu)
+    int ts_staged = 0;        // time-split step: staged scenario block instead of the fused RNG
     int64_t batch_chunk = 0;  // batched step: at most this many staged episodes per chunk
 };
 
@@ -324,6 +325,7 @@ Tuning env_tuning() {
     if (const char* e = getenv("RG_XCHG_TIMEOUT_MS")) t.xchg_timeout_ms = atoll(e);
     if (getenv("RG_NO_ROW_PLAN")) t.no_row_plan = 1;
     if (getenv("RG_NO_TS")) t.no_ts = 1;
+    if (getenv("RG_TS_STAGED")) t.ts_staged = 1;
     if (const char* e = getenv("RG_BATCH_CHUNK")) t.batch_chunk = atoll(e);
     if (!(t.force_tpb == 32 || t.force_tpb == 64 || t.force_tpb == 128)) t.force_tpb = 0;
     return t;
@@ -484,6 +486,8 @@ int32_t rg_set_option(rg_ctx* ctx, const char* name, int64_t value) {
         t.no_row_plan = value != 0;
     } else if (!strcmp(name, "no_ts")) {
         t.no_ts = value != 0;
+    } else if (!strcmp(name, "ts_staged")) {
+        t.ts_staged = value != 0;
     } else if (!strcmp(name, "xchg_timeout_ms")) {
         if (value < 1) return fail(RG_E_ARGS, "xchg_timeout_ms must be >= 1");
         t.xchg_timeout_ms = value;
@@ -506,6 +510,7 @@ int32_t rg_get_option(rg_ctx* ctx, const char* name, int64_t* value) {
     else if (!strcmp(name, "fused_gen")) *value = t.fused_gen;
     else if (!strcmp(name, "no_row_plan")) *value = t.no_row_plan;
     else if (!strcmp(name, "no_ts")) *value = t.no_ts;
+    else if (!strcmp(name, "ts_staged")) *value = t.ts_staged;
     else if (!strcmp(name, "xchg_timeout_ms")) *value = t.xchg_timeout_ms;
     else if (!strcmp(name, "batch_chunk")) *value = t.batch_chunk;
     else if (!strcmp(name, "last_grid_kernel")) *value = ctx->last_grid_kernel;
@@ -790,7 +795,18 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
     // ms: k_gen_soa behind programmatic dependent launch overlaps the step's prologue,
     // scripts/ab_fused_gen.py), so it is off by default.
     const bool single_wave_s2 = a.smem_dyn > 0 && a.tpb <= rg::kRing4Stride && !a.no_s2;
-    if (use_rng && want_stage(n_sim, prob->j_star, flags) && single_wave_s2 &&
+    // A host-planned step whose simulated cells fit one wave of the time-split form
+    // (rg_ts.cu: the x2 chain, the tanh and the x1/x3 chain on separate warps) runs that
+    // instead of one warp per 32 rollouts: a closed-loop step (about one row) is bound by
+    // the rollout's per-step latency, not by FP64 throughput.  With an RNG stream its
+    // producer warps generate the disturbances themselves (no generator kernel, no block).
+    const int64_t ts_units = (int64_t)grid_rows * ((n_sim + 31) / 32);
+    const bool ts_ok = a.listed && !((flags & RG_ABANDON) && !pbits) && !ctx->tune.no_ts &&
+                       ts_units <= (int64_t)rg::kTsUnits * ctx->sm_count;
+    if (ts_ok && use_rng && !ctx->tune.ts_staged && !(flags & RG_STAGE_RNG)) {
+        a.stream = make_stream(rng);
+        a.k0 = rng->k0;
+    } else if (use_rng && want_stage(n_sim, prob->j_star, flags) && single_wave_s2 &&
         ctx->tune.fused_gen) {
         a.ld = (n_sim + 31) / 32 * 32;
         RG_CUDA(ctx->soa.ensure((size_t)prob->j_star * 3 * a.ld * sizeof(double)));
@@ -854,17 +870,12 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
         if (zero_copy && pbits_in_block)
             a.pbits_host = reinterpret_cast<unsigned*>(blk + kOutHead + viol_bytes(m_grid));
     }
-    // A host-planned step whose simulated cells fit one wave of the time-split form
-    // (rg_ts.cu: the x2 chain, the tanh and the x1/x3 chain on separate warps) runs that
-    // instead of one warp per 32 rollouts: a closed-loop step (about one row) is bound by
-    // the rollout's per-step latency, not by FP64 throughput.
-    const int64_t ts_units = (int64_t)grid_rows * ((n_sim + 31) / 32);
-    const bool use_ts = a.listed && !use_rng && !a.gen && !abandon && !ctx->tune.no_ts &&
-                        ts_units <= (int64_t)rg::kTsUnits * ctx->sm_count;
+    const bool use_ts = ts_ok && !a.gen;
     const bool timed = !(flags & RG_NO_TIMING);
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
     if (use_ts)
-        RG_CUDA(rg::launch_grid_ts(a, ctx->variant == rg::kTanhFma, ctx->sm_count, ctx->stream));
+        RG_CUDA(rg::launch_grid_ts(a, ctx->variant == rg::kTanhFma, use_rng, ctx->sm_count,
+                                   ctx->stream));
     else
         RG_CUDA(rg::launch_grid(a, ctx->variant == rg::kTanhFma, use_rng, abandon, ctx->stream));
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));

@@ -102,7 +102,10 @@ __device__ __forceinline__ long long ts_clock_after(const unsigned* w) {
 #define RG_TS_STAMP_AFTER(g, k) RG_TS_STAMP(g, k, 0)
 #endif
 
-template <bool FMA>
+// RNG: the producer generates each step's disturbances with the counter RNG (the
+// reference's generator, rg_rng.cuh) instead of reading the staged block -- no generator
+// kernel before the step, no scenario block in memory.
+template <bool FMA, bool RNG>
 __global__ void __launch_bounds__(kTsThreads, 1) k_grid_ts(GridArgs a) {
     extern __shared__ double sm[];
     unsigned* OV = reinterpret_cast<unsigned*>(sm + S * kSlot);  // [S][RW][32]
@@ -164,7 +167,39 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_grid_ts(GridArgs a) {
             const bool live = sc < a.n_sim;
             const CellConst p = make_cell(a.p);
             const int64_t ld = a.ld, st3 = 3 * a.ld;
-            if (is_p) {
+            if (is_p && RNG) {
+                // P with the fused counter RNG: step j's three disturbances from the
+                // scenario key, off the x2 chain's dependencies
+                const double v =
+                    update_setpoint(a.v_prev, a.r, dvd((double)i, (double)(a.m_grid - 1)));
+                const uint64_t K = scenario_key(a.stream, (uint64_t)(a.k0 + (live ? sc : 0)));
+                double x2p = a.x0[1];
+                int slot = 0;
+                for (int g = 0; g < nch; ++g) {
+                    RG_TS_STAMP(g, 0, clock64());
+                    if (g >= S) nb_sync(kBarE + slot, nE);  // C is done with chunk g - S
+                    double* Ss = sm + slot * kSlot;
+                    unsigned ov = 0u;
+#pragma unroll
+                    for (int s = 0; s < CH; ++s) {
+                        double d0, d1, d2;
+                        disturbance_at(a.stream, K, (uint64_t)(g * CH + s), d0, d1, d2);
+                        const X2Stage st = x2_stage<FMA>(x2p, v, p);
+                        Ss[(s * 4 + 0) * RW * 32 + ridx] = x2p;
+                        Ss[(s * 4 + 1) * RW * 32 + ridx] = st.a2;
+                        Ss[(s * 4 + 2) * RW * 32 + ridx] = st.b2;
+                        Ss[(s * 4 + 3) * RW * 32 + ridx] = st.c2;
+                        Ss[kG + (s * 2 + 0) * RW * 32 + ridx] = d0;
+                        Ss[kG + (s * 2 + 1) * RW * 32 + ridx] = d2;
+                        x2p = add(add(x2p, mul(p.c, st.s2)), d1);
+                        ov |= (fabs(x2p) <= kStateLimit ? 0u : 1u) << s;
+                    }
+                    OV[slot * RW * 32 + ridx] = ov;
+                    RG_TS_STAMP(g, 1, clock64());
+                    nb_arrive(kBarG + slot, nG);
+                    slot = slot == S - 1 ? 0 : slot + 1;
+                }
+            } else if (is_p) {
                 // P: the x2 chain.  Registers one chunk ahead: this chunk's d1 (the chain)
                 // and d0/d2 (staged for C); the next chunk's load while this one runs.
                 const double v =
@@ -295,17 +330,27 @@ int ts_blocks(int64_t units, int sms) {
     return (int)std::max<int64_t>(std::min<int64_t>(sms, units), by_units);
 }
 
-cudaError_t launch_grid_ts(const GridArgs& a, bool fma, int sms, cudaStream_t s) {
+cudaError_t launch_grid_ts(const GridArgs& a, bool fma, bool rng, int sms, cudaStream_t s) {
     const int64_t units = (int64_t)(a.listed ? a.list_n : a.m_grid) * ((a.n_sim + 31) / 32);
     const int nblk = ts_blocks(units, sms);
-    const void* fn = fma ? (const void*)k_grid_ts<true> : (const void*)k_grid_ts<false>;
-    int dyn = 0;
-    // pin_smem takes the block's total: the static part (the finalize's) is well below 4 KB
-    cudaError_t e = pin_smem(fn, kTsSmemDyn + 4096, &dyn);
-    if (e != cudaSuccess) return e;
-    e = fma ? launch_ex(k_grid_ts<true>, dim3(nblk), kTsThreads, (size_t)dyn, s, a.pdl != 0, a)
-            : launch_ex(k_grid_ts<false>, dim3(nblk), kTsThreads, (size_t)dyn, s, a.pdl != 0, a);
-    if (e != cudaSuccess) return e;
+#define RG_TS_LAUNCH(F, R)                                                                 \
+    do {                                                                                   \
+        int dyn = 0;                                                                       \
+        /* pin_smem takes the block's total: the static part (the finalize's) is < 4 KB */ \
+        cudaError_t e = pin_smem((const void*)k_grid_ts<F, R>, kTsSmemDyn + 4096, &dyn);  \
+        if (e != cudaSuccess) return e;                                                    \
+        e = launch_ex(k_grid_ts<F, R>, dim3(nblk), kTsThreads, (size_t)dyn, s,             \
+                      !R && a.pdl != 0, a);                                                \
+        if (e != cudaSuccess) return e;                                                    \
+    } while (0)
+    if (fma) {
+        if (rng) RG_TS_LAUNCH(true, true);
+        else RG_TS_LAUNCH(true, false);
+    } else {
+        if (rng) RG_TS_LAUNCH(false, true);
+        else RG_TS_LAUNCH(false, false);
+    }
+#undef RG_TS_LAUNCH
     return cudaGetLastError();
 }
 

@@ -419,7 +419,9 @@ def robust_rg_parallel(plant, x_t, state, r_t, cset, scenarios, config, backend=
                                      abandon=not keep, timing=False, want_viol=False)
     keep = want_p
     n_dup = 0
-    if res.ss_pruned_rows or res.dedup_rows:
+    # Without P (a closed loop) nothing below needs the host's row list, and the device's
+    # gate/dedup counts came from the host's own plan (rg_capi.cu: episode_rows) anyway.
+    if keep and (res.ss_pruned_rows or res.dedup_rows):
         # rows the device gated or deduplicated: the host's loop (governor.py:302-317)
         # names them, and must agree with the device's counts
         _, ss_ok, dup_src, _ = _host_rows(float(state.v_prev), float(r_t), grid_list, interval)

@@ -17,12 +17,14 @@ prob = _capi.Problem(0.01, -0.9, 0.9, lo, hi, 256, 0)
 m = rg.DisturbanceModel.scaled(0.001, 3)
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 res = _capi.GridResult()
-SETS = {"plan+ts": dict(no_row_plan=0, no_step2=0, no_ts=0),
+SETS = {"plan+ts": dict(no_row_plan=0, no_step2=0, no_ts=0, ts_staged=0),
+        "plan+ts staged": dict(no_row_plan=0, no_step2=0, no_ts=0, ts_staged=1),
         "plan+s2 (no ts)": dict(no_row_plan=0, no_step2=0, no_ts=1),
-        "device rows": dict(no_row_plan=1, no_step2=0, no_ts=1)}
+        "device rows": dict(no_row_plan=1, no_step2=0, no_ts=1, ts_staged=0)}
 if len(sys.argv) > 1 and sys.argv[1] == "ts":  # the time-split A/B only, twice
-    SETS = {"plan+ts": SETS["plan+ts"], "plan+s2 (no ts)": SETS["plan+s2 (no ts)"],
-            "plan+ts again": SETS["plan+ts"], "plan+s2 again": SETS["plan+s2 (no ts)"]}
+    SETS = {"plan+ts": SETS["plan+ts"], "plan+ts staged": SETS["plan+ts staged"],
+            "plan+s2 (no ts)": SETS["plan+s2 (no ts)"], "plan+ts again": SETS["plan+ts"],
+            "plan+ts staged again": SETS["plan+ts staged"]}
 
 
 def step_time(n, vp, r, reps=30):

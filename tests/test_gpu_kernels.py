@@ -23,7 +23,7 @@ def ctx():
 
 
 _DEFAULTS = {"force_tpb": 0, "no_placement": 0, "no_pdl": 0, "no_step2": 0, "fused_gen": 0,
-             "batch_chunk": 0, "no_row_plan": 0, "no_ts": 0}
+             "batch_chunk": 0, "no_row_plan": 0, "no_ts": 0, "ts_staged": 0}
 
 
 @pytest.fixture
@@ -476,7 +476,8 @@ def test_host_row_plan_equals_device_rows(ctx, tuned, n):
 @pytest.mark.parametrize("n", [1, 33, 1000, 10_000, 13_000])
 def test_time_split_step_equals_k_grid(ctx, tuned, n, j_star):
     """Host-planned steps whose cells fit one wave run the time-split kernel (rg_ts.cu: the
-    x2 chain, the tanh and the x1/x3 chain on separate warps); against k_grid (no_ts):
+    x2 chain, the tanh and the x1/x3 chain on separate warps; generated scenarios by the
+    producer's fused RNG or through the staged block); against k_grid (no_ts):
     the same row, per-row violation counts, early-termination and overflow counts -- in
     transient cases (violations at every step count, out-of-bounds starts, overflowing
     states), from generated and from dense host scenarios, chunk-ragged horizons."""
@@ -509,8 +510,10 @@ def test_time_split_step_equals_k_grid(ctx, tuned, n, j_star):
                 kernels.append(ctx.get_option("last_grid_kernel"))
         return out
 
-    ts = run()
+    ts = run()  # generated scenarios: the producer's fused RNG; dense: the staged block
     assert 1 in kernels  # the time-split kernel ran (one wave holds <= 3 units per SM)
+    tuned(ts_staged=1)
+    assert run() == ts  # generated scenarios through the staged block
     tuned(no_ts=1)
     kernels.clear()
     ref = run()
