@@ -163,7 +163,8 @@ RG_API int32_t rg_get_tanh_variant(rg_ctx *ctx, int32_t *variant);
 RG_API int32_t rg_set_option(rg_ctx *ctx, const char *name, int64_t value);
 /* Read a knob of rg_set_option, or the read-only "last_grid_kernel": which kernel the
  * context's last grid step launched (0 = k_grid, one warp per 32 rollouts; 1 = k_grid_ts,
- * the time-split form). */
+ * the time-split form), or "grid_step_kernels": how many kernels the context's grid steps
+ * have launched so far (the scenario staging kernel, when used, and the step kernel). */
 RG_API int32_t rg_get_option(rg_ctx *ctx, const char *name, int64_t *value);
 /* The cudaStream_t the context launches on, as an opaque pointer. */
 RG_API int32_t rg_get_stream(rg_ctx *ctx, void **stream);

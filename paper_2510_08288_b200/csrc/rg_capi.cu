@@ -150,6 +150,7 @@ struct rg_ctx {
     int grid_cap = 0;
     int last_m = 0;
     int last_grid_kernel = 0;  // 0 k_grid, 1 k_grid_ts (rg_get_option)
+    int64_t grid_step_kernels = 0;  // kernels launched by rg_grid_step (staging + step)
     DevBuf g_viol, g_early, g_ovf, g_aband, g_src, g_ticket, g_t0, g_out, g_bar;
     // bisection accumulators and outputs
     DevBuf b_acc, b_out;
@@ -514,6 +515,7 @@ int32_t rg_get_option(rg_ctx* ctx, const char* name, int64_t* value) {
     else if (!strcmp(name, "xchg_timeout_ms")) *value = t.xchg_timeout_ms;
     else if (!strcmp(name, "batch_chunk")) *value = t.batch_chunk;
     else if (!strcmp(name, "last_grid_kernel")) *value = ctx->last_grid_kernel;
+    else if (!strcmp(name, "grid_step_kernels")) *value = ctx->grid_step_kernels;
     else return fail(RG_E_ARGS, "unknown option '%s'", name);
     return RG_OK;
 }
@@ -871,6 +873,8 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
             a.pbits_host = reinterpret_cast<unsigned*>(blk + kOutHead + viol_bytes(m_grid));
     }
     const bool use_ts = ts_ok && !a.gen;
+    // the staging kernel (k_gen_soa / k_to_soa) when the step reads a block it did not write
+    ctx->grid_step_kernels += 1 + ((a.soa != nullptr && !a.gen) ? 1 : 0);
     const bool timed = !(flags & RG_NO_TIMING);
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
     if (use_ts)

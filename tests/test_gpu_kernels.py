@@ -521,3 +521,25 @@ def test_time_split_step_equals_k_grid(ctx, tuned, n, j_star):
     assert ts == ref
     # the cases exercise the verdict paths: some violations, some overflow
     assert any(o[4] > 0 for o in ref) and any(o[5] > 0 for o in ref)
+
+
+def test_grid_step_kernel_count(ctx, tuned):
+    """rg_get_option("grid_step_kernels") counts what a grid step launched: a closed-loop
+    step (one live row) is one time-split kernel generating its own scenarios; the full
+    32-row step stages its block first (generator + step kernel); with ts_staged the
+    time-split step reads a staged block too."""
+    m = rg.DisturbanceModel.scaled(0.001, 3)
+    prob = _problem(-0.9, 0.9, 0.0, 0.05, 256)
+    vp = 0.4
+    x0 = np.array([np.tanh(vp), vp, np.tanh(vp) / 2])
+    sc = _capi.make_scenarios(5, 0, 10_000, m.lo, m.span)
+
+    def count(r, want_pbits=False):
+        k0 = ctx.get_option("grid_step_kernels")
+        ctx.grid_step(prob, x0, vp, r, 32, False, None, 10_000, sc, want_pbits)
+        return ctx.get_option("grid_step_kernels") - k0, ctx.get_option("last_grid_kernel")
+
+    assert count(vp) == (1, 1)             # one live row: k_grid_ts, fused RNG
+    assert count(vp, want_pbits=True) == (2, 0)  # P requested: device rows, staged k_grid
+    tuned(ts_staged=1)
+    assert count(vp) == (2, 1)
