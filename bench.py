@@ -898,8 +898,8 @@ def active_cells(V_prev, R, m_grid, interval):
 
 def run_c3(args, rank, world, local_rank, spec, backend, cpu_group):
     """C3: the reference's desk-scale closed loop (harness.py:138-224) at n_sim scenarios per
-    step through the public API (run_closed_loop: robust_rg_parallel on the device, the true
-    plant on the host).  W untimed closed-loop steps of another episode (seed + 1000), then
+    step through the public API (run_closed_loop: the native loop rg_closed_loop -- the
+    device grid step, then the true plant on the host in C with numpy's tanh restated).  W untimed closed-loop steps of another episode (seed + 1000), then
     the timed episode from t = 0 for K steps; host wall clock of the whole loop (it is the
     latency a controller sees: sampling descriptor, device step, result, plant update), the
     max over ranks.  Cell-steps = the reference's sims_run x j* summed over the timed steps."""
@@ -968,8 +968,9 @@ def run_c3(args, rank, world, local_rank, spec, backend, cpu_group):
         # reads P, so run_closed_loop asks for none (the reference's diagnostics stay).
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 5 * 8 + 112,
                 "d2h_bytes_per_step": 128 + 4 * M_GRID,
-                "note": "the timed loop is the public API end to end (run_closed_loop -> "
-                        "robust_rg_parallel without P: the loop never reads it)"},
+                "note": "the timed loop is the public API end to end: run_closed_loop, which "
+                        "runs the governed loop natively (rg_closed_loop: grid step without P, "
+                        "kappa, v_t, the true plant with the library's numpy tanh)"},
         "roofline": roof, "cpu_baseline": cb, "clocks": clocks, "gpu_launches": launches,
     }
 

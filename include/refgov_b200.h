@@ -321,6 +321,42 @@ RG_API int32_t rg_bisect_joint_sharded(rg_ctx *ctx, const rg_problem *prob, cons
 
 RG_API int32_t rg_fp64_peak(rg_ctx *ctx, double *flops_per_s);
 
+/* ---- the closed loop in native code (harness.py:138-224) ----------------------------
+ * run_closed_loop's governed loop without a Python round trip per step: per step t the
+ * grid step (rg_grid_step on the scenario set seed scen_seed + t, k0 = 0, ranges lo/span:
+ * derive_seed(seed, "scenarios") + t), kappa = row / (M - 1), v = update_setpoint, the
+ * true plant's RK4 step with numpy's tanh (rg_np_tanh), then x += d_true[t].  Per-step
+ * outputs (host arrays of `steps`, each may be NULL): v_t, kappa, y_t = x1 before the
+ * plant step, feasible, sims_run, early_terms, wall time of the governor step.  The loop
+ * stops early as the reference does (res->abort_kind): the plant's integration overflow
+ * (|x_i| > 1e6 or non-finite after the RK4 step; dynamics.py:125-130), the state leaving
+ * the box after the disturbance (harness.py:222-224), or -- with infeasible_error --
+ * the first step without a feasible row (InfeasibleError).  res->steps_done rows were
+ * written.  x_out (3 doubles, may be NULL): the final state. */
+#define RG_LOOP_OVERFLOW 1
+#define RG_LOOP_LEFT_BOX 2
+#define RG_LOOP_INFEASIBLE 3
+typedef struct {
+    int32_t steps_done;
+    int32_t abort_kind;  /* 0, or RG_LOOP_* */
+    int32_t abort_step;  /* -1, or the step the loop stopped at */
+    int32_t abort_index; /* the state component for RG_LOOP_OVERFLOW / LEFT_BOX */
+    double abort_value;
+} rg_loop_result;
+RG_API int32_t rg_closed_loop(rg_ctx *ctx, const rg_problem *prob, int32_t m_grid,
+                              int32_t prefix_mode, int32_t infeasible_error, const double *x0,
+                              double v0, int32_t steps, const double *r, const double *d_true,
+                              uint64_t scen_seed, int64_t n_sim, const double *lo,
+                              const double *span, double *v_out, double *kappa_out,
+                              double *y_out, uint8_t *feasible_out, int64_t *sims_out,
+                              int64_t *early_out, int32_t *wall_us_out, double *x_out,
+                              rg_loop_result *res);
+/* numpy's float64 tanh (numpy 2.3.5's SIMD kernel, rg_nptanh.h) on the host: y[i] =
+ * np.tanh(x[i]) bit for bit for finite x.  And the surrogate true plant's step with it
+ * (dynamics.py: SurrogateFuelCellPlant.step without the overflow check).  No device. */
+RG_API int32_t rg_np_tanh(const double *x, double *y, int64_t n);
+RG_API int32_t rg_plant_step(double step_size, const double *x, double v, double *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -70,6 +70,14 @@ class GridResult(ctypes.Structure):
                 ("reduce_us", ctypes.c_float)]
 
 
+class LoopResult(ctypes.Structure):
+    _fields_ = [("steps_done", _i32), ("abort_kind", _i32), ("abort_step", _i32),
+                ("abort_index", _i32), ("abort_value", _d)]
+
+
+RG_LOOP_OVERFLOW, RG_LOOP_LEFT_BOX, RG_LOOP_INFEASIBLE = 1, 2, 3
+
+
 class BisectResult(ctypes.Structure):
     _fields_ = [("kappa", _d), ("found", _i32), ("_pad", _i32), ("cells", _i64),
                 ("early", _i64), ("kernel_ms", ctypes.c_float), ("_pad2", _i32)]
@@ -122,6 +130,11 @@ SIGNATURES = {
     "rg_set_option": (_i32, [_vp, ctypes.c_char_p, _i64]),
     "rg_get_option": (_i32, [_vp, ctypes.c_char_p, ctypes.POINTER(_i64)]),
     "rg_get_stream": (_i32, [_vp, ctypes.POINTER(_vp)]),
+    "rg_closed_loop": (_i32, [_vp, ctypes.POINTER(Problem), _i32, _i32, _i32, _vp, _d, _i32,
+                              _vp, _vp, _u64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                              _vp, _vp, ctypes.POINTER(LoopResult)]),
+    "rg_np_tanh": (_i32, [_vp, _vp, _i64]),
+    "rg_plant_step": (_i32, [_d, _vp, _d, _vp]),
     "rg_synchronize": (_i32, [_vp]),
     "rg_tanh": (_i32, [_vp, _vp, _vp, _i64, _i32]),
     "rg_sample_scenarios": (_i32, [_vp, _u64, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _i32]),
@@ -202,6 +215,24 @@ def _p(a: np.ndarray | None):
     # the integer address: ctypes passes it for c_void_p arguments, and it is
     # several times cheaper to produce than a.ctypes.data_as(c_void_p)
     return None if a is None else a.ctypes.data
+
+
+def np_tanh(x) -> np.ndarray:
+    """numpy's float64 tanh restated in the library (rg_np_tanh, host code, no device)."""
+    lib = load_library()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty_like(x)
+    check(lib.rg_np_tanh(_p(x), _p(y), x.size))
+    return y
+
+
+def plant_step(step_size: float, x, v: float) -> np.ndarray:
+    """The surrogate true plant's RK4 step in the library (rg_plant_step, host code)."""
+    lib = load_library()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty(3)
+    check(lib.rg_plant_step(float(step_size), _p(x), float(v), _p(out)))
+    return out
 
 
 def device_count() -> int:
@@ -532,6 +563,33 @@ class Context:
         check(self.lib.rg_xchg_close(self.handle))
 
     @_locked
+    @_locked
+    def closed_loop(self, prob: Problem, m_grid: int, prefix_mode: bool, infeasible_error: bool,
+                    x0, v0: float, r, d_true, scen_seed: int, n_sim: int, lo, span):
+        """rg_closed_loop: the governed loop in native code.  Returns (LoopResult, dict of
+        per-step arrays over the steps done, final state)."""
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        steps = r.size
+        d_true = np.ascontiguousarray(d_true, dtype=np.float64).reshape(steps, 3)
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        lo3 = np.ascontiguousarray(np.asarray(lo, dtype=np.float64)[:3])
+        span3 = np.ascontiguousarray(np.asarray(span, dtype=np.float64)[:3])
+        out = {"v": np.empty(steps), "kappa": np.empty(steps), "y": np.empty(steps),
+               "feasible": np.empty(steps, dtype=np.uint8),
+               "sims_run": np.empty(steps, dtype=np.int64),
+               "early_terms": np.empty(steps, dtype=np.int64),
+               "wall_us": np.empty(steps, dtype=np.int32)}
+        xf = np.empty(3)
+        res = LoopResult()
+        check(self.lib.rg_closed_loop(
+            self.handle, prob, int(m_grid), 1 if prefix_mode else 0, 1 if infeasible_error else 0,
+            _p(x0), float(v0), steps, _p(r), _p(d_true), int(scen_seed) & (2**64 - 1), int(n_sim),
+            _p(lo3), _p(span3), _p(out["v"]), _p(out["kappa"]), _p(out["y"]),
+            _p(out["feasible"]), _p(out["sims_run"]), _p(out["early_terms"]), _p(out["wall_us"]),
+            _p(xf), ctypes.byref(res)))
+        n = res.steps_done
+        return res, {k: a[:n] for k, a in out.items()}, xf
+
     def fp64_peak(self) -> float:
         f = _d()
         check(self.lib.rg_fp64_peak(self.handle, ctypes.byref(f)))

@@ -14,12 +14,14 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <string>
 #include <vector>
 
 #include "../../include/refgov_b200.h"
 #include "rg_kernels.h"
 #include "rg_math.cuh"
+#include "rg_nptanh.h"
 
 namespace {
 
@@ -1720,6 +1722,152 @@ int32_t rg_fp64_peak(rg_ctx* ctx, double* flops_per_s) {
         best = std::min(best, ms);
     }
     *flops_per_s = (double)blocks * threads * iters * 8.0 * 2.0 / (best * 1e-3);
+    return RG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// the closed loop in native code (harness.py:138-224)
+// ---------------------------------------------------------------------------
+
+}  // extern "C"
+
+// SurrogateFuelCellPlant.step (dynamics.py:110-130, 228-231) in the reference's operation
+// order -- the scalar form of dynamics.py: _surrogate_rk4 -- with numpy's tanh
+// (rg_nptanh.h).  Host code is compiled with -ffp-contract=off: every operation rounds.
+static void surrogate_plant_step(double h, const double* x, double v, double* out) {
+    const double hh = 0.5 * h;
+    const double x0 = x[0], x1 = x[1], x2 = x[2];
+    const double k11 = -x1 + v;
+    const double b1 = x1 + hh * k11;
+    const double k21 = -b1 + v;
+    const double c1 = x1 + hh * k21;
+    const double k31 = -c1 + v;
+    const double d1 = x1 + h * k31;
+    const double k41 = -d1 + v;
+    const double t1 = rg::np_tanh(x1), t2 = rg::np_tanh(b1), t3 = rg::np_tanh(c1),
+                 t4 = rg::np_tanh(d1);
+    const double k10 = -x0 + t1;
+    const double k12 = -2.0 * x2 + x0;
+    const double a0 = x0 + hh * k10, a2 = x2 + hh * k12;
+    const double k20 = -a0 + t2;
+    const double k22 = -2.0 * a2 + a0;
+    const double b0 = x0 + hh * k20, b2 = x2 + hh * k22;
+    const double k30 = -b0 + t3;
+    const double k32 = -2.0 * b2 + b0;
+    const double c0 = x0 + h * k30, c2 = x2 + h * k32;
+    const double k40 = -c0 + t4;
+    const double k42 = -2.0 * c2 + c0;
+    const double c = h / 6.0;
+    out[0] = x0 + c * (((k10 + 2.0 * k20) + 2.0 * k30) + k40);
+    out[1] = x1 + c * (((k11 + 2.0 * k21) + 2.0 * k31) + k41);
+    out[2] = x2 + c * (((k12 + 2.0 * k22) + 2.0 * k32) + k42);
+}
+
+extern "C" {
+
+int32_t rg_np_tanh(const double* x, double* y, int64_t n) {
+    if ((!x || !y) && n > 0) return fail(RG_E_ARGS, "null array");
+    for (int64_t i = 0; i < n; ++i) y[i] = rg::np_tanh(x[i]);
+    return RG_OK;
+}
+
+int32_t rg_plant_step(double step_size, const double* x, double v, double* out) {
+    if (!x || !out) return fail(RG_E_ARGS, "null array");
+    surrogate_plant_step(step_size, x, v, out);
+    return RG_OK;
+}
+
+int32_t rg_closed_loop(rg_ctx* ctx, const rg_problem* prob, int32_t m_grid, int32_t prefix_mode,
+                       int32_t infeasible_error, const double* x0, double v0, int32_t steps,
+                       const double* r, const double* d_true, uint64_t scen_seed, int64_t n_sim,
+                       const double* lo, const double* span, double* v_out, double* kappa_out,
+                       double* y_out, uint8_t* feasible_out, int64_t* sims_out,
+                       int64_t* early_out, int32_t* wall_us_out, double* x_out,
+                       rg_loop_result* res) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    if (!prob || !x0 || !r || !d_true || !lo || !span || !res)
+        return fail(RG_E_ARGS, "null argument");
+    if (steps < 1) return fail(RG_E_ARGS, "steps must be >= 1, got %d", steps);
+    if (m_grid < 2) return fail(RG_E_ARGS, "m_grid must be >= 2, got %d", m_grid);
+    if (n_sim < 1) return fail(RG_E_ARGS, "n_sim must be >= 1");
+    double x[3] = {x0[0], x0[1], x0[2]};
+    if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2])) || !isfinite(v0))
+        return fail(RG_E_ARGS, "state entries must be finite");
+    *res = rg_loop_result{};
+    res->abort_step = -1;
+    double v_prev = v0;
+    const double h = prob->step_size;
+    const double den = (double)(m_grid - 1);
+    for (int32_t t = 0; t < steps; ++t) {
+        const double rt = r[t];
+        // the step's scenario set: seed derive_seed(seed, "scenarios") + t (harness.py:197)
+        rg_scenarios sc{};
+        sc.seed = scen_seed + (uint64_t)t;
+        sc.k0 = 0;
+        sc.n_sim = n_sim;
+        for (int i = 0; i < 3; ++i) {
+            sc.lo[i] = lo[i];
+            sc.span[i] = span[i];
+        }
+        rg_grid_result gr{};
+        const auto w0 = std::chrono::steady_clock::now();
+        if ((rc = rg_grid_step(ctx, prob, x, v_prev, rt, m_grid, prefix_mode, nullptr, n_sim, 0,
+                               &sc, nullptr, nullptr, &gr, RG_NO_TIMING)))
+            return rc;
+        const int32_t wall_us = (int32_t)std::chrono::duration_cast<std::chrono::microseconds>(
+                                    std::chrono::steady_clock::now() - w0)
+                                    .count();
+        double v, kappa;
+        bool feas;
+        if (gr.row < 0) {  // governor.py:562-569
+            if (infeasible_error) {
+                res->abort_kind = RG_LOOP_INFEASIBLE;
+                res->abort_step = t;
+                return RG_OK;
+            }
+            v = v_prev;
+            kappa = 0.0;
+            feas = false;
+        } else {  // kappa = grid[row] = row / (M - 1); governor.py:571-579
+            kappa = rg::dvd((double)gr.row, den);
+            v = rg::update_setpoint(v_prev, rt, kappa);
+            v_prev = v;
+            feas = true;
+        }
+        if (v_out) v_out[t] = v;
+        if (kappa_out) kappa_out[t] = kappa;
+        if (y_out) y_out[t] = x[0];  // plant.output(x, v) = x1 before the plant step
+        if (feasible_out) feasible_out[t] = feas ? 1 : 0;
+        if (sims_out) sims_out[t] = gr.sims_run;
+        if (early_out) early_out[t] = gr.early_terms;
+        if (wall_us_out) wall_us_out[t] = wall_us;
+        res->steps_done = t + 1;
+        // the true plant, then its disturbance (harness.py:215-224)
+        double nx[3];
+        surrogate_plant_step(h, x, v, nx);
+        for (int i = 0; i < 3; ++i) {
+            if (!isfinite(nx[i]) || fabs(nx[i]) > 1e6) {  // dynamics.py STATE_ABORT_LIMIT
+                res->abort_kind = RG_LOOP_OVERFLOW;
+                res->abort_step = t;
+                res->abort_index = i;
+                res->abort_value = nx[i];
+                return RG_OK;
+            }
+        }
+        for (int i = 0; i < 3; ++i) x[i] = nx[i] + d_true[(int64_t)t * 3 + i];
+        for (int i = 0; i < 3; ++i) {
+            if (!isfinite(x[i]) || fabs(x[i]) > 1e6) {  // harness.py STATE_LIMIT
+                res->abort_kind = RG_LOOP_LEFT_BOX;
+                res->abort_step = t;
+                res->abort_index = i;
+                res->abort_value = x[i];
+                if (x_out) memcpy(x_out, x, sizeof x);
+                return RG_OK;
+            }
+        }
+    }
+    if (x_out) memcpy(x_out, x, sizeof x);
     return RG_OK;
 }
 

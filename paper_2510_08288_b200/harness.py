@@ -7,6 +7,11 @@ governor picks v_t, and the true plant advances on the host with numpy's tanh
 plus its own disturbance stream ``derive_seed(seed, "plant")`` -- exactly the
 reference's arithmetic, so the v_t sequence is bit-identical.
 
+The governed loop runs in native code by default (``rg_closed_loop``: the grid step,
+kappa and v_t, and the true plant's RK4 step with the library's restatement of numpy's
+tanh, per step without a Python round trip); ``native=False`` keeps the per-step Python
+loop below, which the tests hold it to bit for bit.
+
 ``run_closed_loop_bisection`` substitutes the nominal ``bisection_rg`` at
 harness.py:200 (configuration C1 of BASELINE.md; the reference ships no such
 driver).
@@ -20,7 +25,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .disturbance import DisturbanceModel, ScenarioSet, derive_seed, sample_scenarios
-from .errors import ConfigError, IntegrationOverflowError
+from .errors import ConfigError, InfeasibleError, IntegrationOverflowError
 from .governor import GovernorState, bisection_rg, robust_rg_parallel, \
     robust_rg_parallel_batch
 
@@ -84,14 +89,78 @@ def _schedule(profile, steps):
     return np.asarray(profile, dtype=np.float64)[:steps]
 
 
+def _native_loop_ok(plant, config) -> bool:
+    from .dynamics import SurrogateFuelCellPlant
+
+    return (type(plant) is SurrogateFuelCellPlant and getattr(config, "backend", "cuda") == "cuda"
+            and bool(getattr(config, "m_grid", 0)))
+
+
+def _run_closed_loop_native(plant, cset, model, config, profile, steps, seed, x0, v0):
+    """run_closed_loop's governed loop through rg_closed_loop: the same scenario and plant
+    streams, the same device step, kappa, update_setpoint and true-plant arithmetic (numpy's
+    tanh restated, rg_nptanh.h), the same rows, diagnostics and abort reasons."""
+    from . import _capi
+    from .governor import _prepared, validate_epsilon
+
+    device = getattr(config, "device", 0)
+    x = plant.validate_state(np.zeros(plant.state_dim) if x0 is None else x0)
+    if config.tighten_mode == "scale":
+        validate_epsilon(config.epsilon)
+    prob = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor, config.epsilon,
+                     config.tighten_mode, config.j_star, config.m_grid)[0]
+    scen_seed = derive_seed(seed, "scenarios")
+    d_true = _true_disturbance(model, steps, seed, device)
+    r_sched = np.ascontiguousarray(_schedule(profile, steps), dtype=np.float64)
+    if r_sched.size < steps:
+        raise ConfigError(f"profile has {r_sched.size} entries, need {steps}")
+    ctx = _capi.context(device)
+    res, out, _ = ctx.closed_loop(prob, config.m_grid, config.prefix_mode,
+                                  config.infeasible_policy == "error", x, float(v0),
+                                  r_sched[:steps], d_true, scen_seed, config.n_sim, model.lo,
+                                  model.span)
+    rec = RunRecord(rows=[], config={"governor_on": True, "j_star": config.j_star,
+                                     "n_sim": config.n_sim, "m_grid": config.m_grid,
+                                     "steps": steps, "backend": "cuda"}, seed=seed)
+    r_l, v_l, y_l = r_sched.tolist(), out["v"].tolist(), out["y"].tolist()
+    k_l, f_l, w_l = out["kappa"].tolist(), out["feasible"].tolist(), out["wall_us"].tolist()
+    s_l, e_l = out["sims_run"].tolist(), out["early_terms"].tolist()
+    for t in range(res.steps_done):
+        feas = bool(f_l[t])
+        rec.rows.append((t, r_l[t], v_l[t], y_l[t], k_l[t], feas, w_l[t]))
+        rec.diag_rows.append(f"{t},{k_l[t]!r},{v_l[t]!r},{int(feas)},{s_l[t]},{e_l[t]},{w_l[t]}")
+    if res.abort_kind == _capi.RG_LOOP_INFEASIBLE:
+        raise InfeasibleError("no candidate feasible, including kappa=0 (hold current setpoint)")
+    if res.abort_kind == _capi.RG_LOOP_OVERFLOW:
+        # the Python plant reports the numpy scalar (dynamics.py: _surrogate_rk4)
+        e = IntegrationOverflowError(f"integration overflow in state {res.abort_index} "
+                                     f"(value {np.float64(res.abort_value)!r})",
+                                     state_index=res.abort_index)
+        rec.aborted, rec.abort_reason = True, f"step {res.abort_step}: {e}"
+    elif res.abort_kind == _capi.RG_LOOP_LEFT_BOX:
+        rec.aborted = True
+        rec.abort_reason = f"step {res.abort_step}: state left the operating box"
+    return rec
+
+
 def run_closed_loop(plant, cset, model, config, profile, steps, seed, governor_on=True,
-                    x0=None, v0=0.0) -> RunRecord:
-    """The governed closed loop of harness.py:138-224 with the device governor."""
+                    x0=None, v0=0.0, native=None) -> RunRecord:
+    """The governed closed loop of harness.py:138-224 with the device governor.
+
+    ``native`` (default: whenever the plant is the surrogate and the governor is on): the
+    loop runs in the library (rg_closed_loop) instead of step by step in Python.
+    """
     if steps < 1:
         raise ConfigError(f"steps must be >= 1, got {steps}")
     if model.state_dim != plant.state_dim:
         raise ConfigError(f"disturbance model has {model.state_dim} states, plant has "
                           f"{plant.state_dim}")
+    if native is None:
+        native = governor_on and _native_loop_ok(plant, config)
+    if native:
+        if not governor_on:
+            raise ConfigError("the native closed loop runs the governor")
+        return _run_closed_loop_native(plant, cset, model, config, profile, steps, seed, x0, v0)
     device = getattr(config, "device", 0)
     x = plant.validate_state(np.zeros(plant.state_dim) if x0 is None else x0)
     state = GovernorState(v_prev=float(v0))

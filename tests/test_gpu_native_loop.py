@@ -1,0 +1,87 @@
+"""The native closed loop (rg_closed_loop: grid step, kappa, v_t and the true plant with
+the library's numpy-tanh, per step in C) against the per-step Python loop
+(run_closed_loop(native=False)), which is pinned to the reference's golden traces: equal
+rows, diagnostics, abort reasons and errors."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2510_08288_b200 as rg
+from paper_2510_08288_b200.errors import InfeasibleError
+from paper_2510_08288_b200.harness import ReferenceProfile, run_closed_loop
+
+pytestmark = pytest.mark.gpu
+
+PLANT = rg.make_plant("surrogate-fc")
+BOX = rg.ConstraintSet(-0.9, 0.9, anchor=0.0)
+DESK = ReferenceProfile(((0, 0.4), (400, 2.5), (1000, -2.5), (1600, 0.2)))
+
+
+def _same(a, b):
+    assert a.rows == b.rows  # (t, r, v, y, kappa, feasible, wall_us): wall_us differs
+    assert a.diag_rows == b.diag_rows
+    assert (a.aborted, a.abort_reason) == (b.aborted, b.abort_reason)
+
+
+def _strip_wall(rec):
+    rec.rows = [r[:6] for r in rec.rows]
+    rec.diag_rows = [",".join(d.split(",")[:6]) for d in rec.diag_rows]
+    return rec
+
+
+@pytest.mark.parametrize("n_sim,steps,seed", [(1000, 700, 2024), (10_000, 450, 77),
+                                              (300, 1200, 5)])
+def test_native_loop_equals_python_loop(n_sim, steps, seed):
+    model = rg.DisturbanceModel.scaled(0.001, 3)
+    cfg = rg.GovernorConfig(j_star=256, m_grid=32, n_sim=n_sim)
+    prof = DESK if steps < 1000 else ReferenceProfile(((0, 0.4), (300, 2.5), (700, -2.5),
+                                                       (1000, 0.2)))
+    nat = _strip_wall(run_closed_loop(PLANT, BOX, model, cfg, prof, steps, seed))
+    py = _strip_wall(run_closed_loop(PLANT, BOX, model, cfg, prof, steps, seed, native=False))
+    _same(nat, py)
+    assert not nat.aborted and len(nat.rows) == steps
+
+
+def test_native_loop_transients_prefix_mode_and_start_state():
+    """Larger disturbances, prefix extraction, j* = 64, and a start outside the output
+    bounds with v0 != 0: the first steps have no feasible row and hold the setpoint."""
+    model = rg.DisturbanceModel.scaled(0.02, 3)
+    cfg = rg.GovernorConfig(j_star=64, m_grid=16, n_sim=2000, prefix_mode=True)
+    prof = np.concatenate([np.full(60, 2.0), np.full(60, -2.4), np.full(80, 0.7)])
+    x0 = np.array([0.95, -0.5, 0.1])
+    nat = _strip_wall(run_closed_loop(PLANT, BOX, model, cfg, prof, 200, 31, x0=x0, v0=-0.5))
+    py = _strip_wall(run_closed_loop(PLANT, BOX, model, cfg, prof, 200, 31, x0=x0, v0=-0.5,
+                                     native=False))
+    _same(nat, py)
+    assert not nat.rows[0][5] and any(r[5] for r in nat.rows)  # held, then feasible
+
+
+def test_native_loop_aborts_like_the_python_loop():
+    model = rg.DisturbanceModel.scaled(0.02, 3)
+    cfg = rg.GovernorConfig(j_star=32, m_grid=8, n_sim=64)
+    # the plant's integration overflow at step 0 (|x1| beyond 1e6 after the RK4 step)
+    x0 = np.array([1.5e6, 0.0, 0.0])
+    a = _strip_wall(run_closed_loop(PLANT, BOX, model, cfg, [0.4] * 5, 5, 3, x0=x0))
+    b = _strip_wall(run_closed_loop(PLANT, BOX, model, cfg, [0.4] * 5, 5, 3, x0=x0,
+                                    native=False))
+    _same(a, b)
+    assert a.aborted and "integration overflow in state 0" in a.abort_reason
+    # the state leaving the box after the disturbance: x2 at the edge, held setpoint 1e6
+    x0 = np.array([0.0, 1e6 - 1e-4, 0.0])
+    a = _strip_wall(run_closed_loop(PLANT, BOX, model, cfg, [1e6] * 20, 20, 4, x0=x0, v0=1e6))
+    b = _strip_wall(run_closed_loop(PLANT, BOX, model, cfg, [1e6] * 20, 20, 4, x0=x0, v0=1e6,
+                                    native=False))
+    _same(a, b)
+    assert a.aborted and "left the operating box" in a.abort_reason
+
+
+def test_native_loop_infeasible_error_policy():
+    model = rg.DisturbanceModel.scaled(0.001, 3)
+    cfg = rg.GovernorConfig(j_star=32, m_grid=8, n_sim=64, infeasible_policy="error")
+    x0 = np.array([0.95, 0.0, 0.0])  # out of the output bounds: nothing is feasible
+    with pytest.raises(InfeasibleError):
+        run_closed_loop(PLANT, BOX, model, cfg, [0.4] * 3, 3, 1, x0=x0)
+    with pytest.raises(InfeasibleError):
+        run_closed_loop(PLANT, BOX, model, cfg, [0.4] * 3, 3, 1, x0=x0, native=False)
