@@ -543,3 +543,20 @@ def test_grid_step_kernel_count(ctx, tuned):
     assert count(vp, want_pbits=True) == (2, 0)  # P requested: device rows, staged k_grid
     tuned(ts_staged=1)
     assert count(vp) == (2, 1)
+
+
+def test_options_round_trip(ctx, tuned):
+    """rg_get_option reads back every rg_set_option knob; unknown names are ConfigError."""
+    from paper_2510_08288_b200.errors import ConfigError
+
+    for name, value in (("force_tpb", 64), ("no_placement", 1), ("no_pdl", 1), ("no_step2", 1),
+                        ("fused_gen", 1), ("no_row_plan", 1), ("no_ts", 1), ("ts_staged", 1),
+                        ("batch_chunk", 7), ("xchg_timeout_ms", 1234)):
+        before = ctx.get_option(name)
+        ctx.set_option(name, value)
+        assert ctx.get_option(name) == value
+        ctx.set_option(name, before)
+    with pytest.raises(ConfigError):
+        ctx.get_option("no_such_knob")
+    with pytest.raises(ConfigError):
+        ctx.set_option("last_grid_kernel", 1)  # read-only
