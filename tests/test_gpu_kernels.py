@@ -560,3 +560,42 @@ def test_options_round_trip(ctx, tuned):
         ctx.get_option("no_such_knob")
     with pytest.raises(ConfigError):
         ctx.set_option("last_grid_kernel", 1)  # read-only
+
+
+def test_time_split_random_stress(ctx, tuned):
+    """150 random one- and few-row steps (scenario counts 1..13,000, horizons 1..300,
+    random starts, setpoints, disturbance scales and grid sizes): the time-split kernel
+    (fused RNG and staged) gives k_grid's row, per-row violation counts, early and overflow
+    counts on every one."""
+    rng = np.random.default_rng(20261019)
+    cases = []
+    for trial in range(150):
+        n = int(rng.choice([1, 7, 31, 32, 33, 500, 1000, 4097, 10_000, 13_000]))
+        j = int(rng.choice([1, 2, 7, 8, 9, 15, 16, 17, 64, 255, 256, 300]))
+        M = int(rng.choice([2, 5, 16, 32, 64]))
+        vp = float(rng.uniform(-1.3, 1.3))
+        r = vp if trial % 2 else vp + float(rng.choice([1e-9, 1e-3, 0.3])) * rng.choice([-1, 1])
+        x0 = np.array([np.tanh(vp), vp, np.tanh(vp) / 2]) + rng.uniform(-0.1, 0.1, 3)
+        amp = float(rng.choice([0.001, 0.02, 0.08]))
+        m = rg.DisturbanceModel.scaled(amp, 3)
+        cases.append((_problem(-0.9, 0.9, 0.0, 0.05, j), n, M, vp, r, x0,
+                      _capi.make_scenarios(1000 + trial, int(rng.integers(0, 1 << 20)), n, m.lo,
+                                           m.span), bool(trial % 5 == 0)))
+
+    def run():
+        out, ks = [], []
+        for prob, n, M, vp, r, x0, sc, prefix in cases:
+            res, viol, _ = ctx.grid_step(prob, x0, vp, r, M, prefix, None, n, sc, False)
+            out.append((res.row, res.n_active, res.sims_run, viol.tolist(), res.early_terms,
+                        res.overflows))
+            ks.append(ctx.get_option("last_grid_kernel"))
+        return out, ks
+
+    ts, ks = run()
+    assert sum(ks) > 50  # most cases fit the time-split form
+    tuned(ts_staged=1)
+    staged, _ = run()
+    tuned(ts_staged=0, no_ts=1)
+    ref, ks_ref = run()
+    assert set(ks_ref) == {0}
+    assert ts == ref and staged == ref
