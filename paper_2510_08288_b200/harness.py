@@ -89,11 +89,32 @@ def _schedule(profile, steps):
     return np.asarray(profile, dtype=np.float64)[:steps]
 
 
+_NP_TANH_PROBE: list = []
+
+
+def _np_tanh_matches() -> bool:
+    """Whether the library's restatement of numpy's tanh (rg_nptanh.h: numpy's AVX512/AVX2
+    kernel) is this process's np.tanh -- checked once on values across every interval and
+    its boundaries.  A numpy without that kernel (no AVX2 on the host: libm's tanh) keeps
+    the closed loop's true plant in Python, where it calls np.tanh itself."""
+    if not _NP_TANH_PROBE:
+        from . import _capi
+
+        rng = np.random.default_rng(1)
+        edges = np.array([0.1875 * 2.0 ** e * m for e in range(-3, 7) for m in (1.0, 1.5)])
+        near = (edges[:, None].view(np.int64) + np.arange(-8, 9)[None, :]).ravel()
+        x = np.concatenate([rng.uniform(-30, 30, 2048), rng.uniform(-1, 1, 2048),
+                            near.view(np.float64), -near.view(np.float64)])
+        ok = np.array_equal(_capi.np_tanh(x).view(np.uint64), np.tanh(x).view(np.uint64))
+        _NP_TANH_PROBE.append(bool(ok))
+    return _NP_TANH_PROBE[0]
+
+
 def _native_loop_ok(plant, config) -> bool:
     from .dynamics import SurrogateFuelCellPlant
 
     return (type(plant) is SurrogateFuelCellPlant and getattr(config, "backend", "cuda") == "cuda"
-            and bool(getattr(config, "m_grid", 0)))
+            and bool(getattr(config, "m_grid", 0)) and _np_tanh_matches())
 
 
 def _run_closed_loop_native(plant, cset, model, config, profile, steps, seed, x0, v0):
