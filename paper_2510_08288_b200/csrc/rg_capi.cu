@@ -770,13 +770,13 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
     a.prefix_mode = prefix_mode ? 1 : 0;
     a.n_sim = n_sim;
     bool use_rng = dist == nullptr;
-    // Host-planned rows: without P (the governor's decision, a closed loop) the host
-    // evaluates the candidates' setpoints, gate and dedup itself and launches grid rows for
-    // the simulated ones only -- a closed-loop step has about one, and
-    // the placement below then sees the real work.  With P, or when every row is simulated,
-    // the kernel derives the rows on the device (row_source).
+    // Host-planned rows: the host evaluates the candidates' setpoints, gate and dedup itself
+    // and launches grid rows for the simulated ones only -- a closed-loop step has about one
+    // (SURVEY.md §0 fact 6), and the placement below then sees the real work (with P the
+    // kernels zero the other rows' words: zero_unlisted_pbits).  When every row is
+    // simulated the kernel derives the rows on the device (row_source).
     int grid_rows = m_grid;
-    if (!pbits && m_grid <= rg::kListMax && !ctx->tune.no_row_plan) {
+    if (m_grid <= rg::kListMax && !ctx->tune.no_row_plan) {
         int src[rg::kListMax];
         double vv[rg::kListMax];
         const int32_t n_act = episode_rows(a.p, v_prev, r, m_grid, src, vv);

@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(256, RG_GRID_MINB) k_grid(GridArgs a) {
         // pruned or duplicate row: no simulated bits (the host expands duplicates)
         a.pbits[(int64_t)i * a.pwords + (k >> 5)] = 0u;
     }
+    zero_unlisted_pbits(a);
     grid_finalize(a);
 }
 

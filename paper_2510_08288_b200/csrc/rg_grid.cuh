@@ -117,6 +117,19 @@ __device__ __forceinline__ void grid_finalize_xchg(const GridArgs& a, unsigned l
     if (threadIdx.x == 0) *a.ticket = 0u;
 }
 
+// A host-planned step (listed) launches only the simulated rows; with P requested the
+// gated-out and duplicate rows' words must still read zero (the host expands duplicates from
+// their source rows).  Every block zeroes a grid-strided share of them before finalizing.
+__device__ __forceinline__ void zero_unlisted_pbits(const GridArgs& a) {
+    if (!a.listed || !a.pbits) return;
+    const int64_t nth = (int64_t)gridDim.x * gridDim.y * blockDim.x;
+    const int64_t t0 = ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+    for (int q = 0; q < a.m_grid; ++q) {
+        if (a.src_tab[q] == -1) continue;
+        for (int64_t w = t0; w < a.pwords; w += nth) a.pbits[(int64_t)q * a.pwords + w] = 0u;
+    }
+}
+
 // Last block out extracts the best row (governor.py:351-377) and resets the
 // accumulators for the next launch.  The first warp reads 32 rows at a time
 // (one per lane) and reduces with ballots and shuffles, so the step's tail is

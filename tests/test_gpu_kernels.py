@@ -525,9 +525,9 @@ def test_time_split_step_equals_k_grid(ctx, tuned, n, j_star):
 
 def test_grid_step_kernel_count(ctx, tuned):
     """rg_get_option("grid_step_kernels") counts what a grid step launched: a closed-loop
-    step (one live row) is one time-split kernel generating its own scenarios; the full
-    32-row step stages its block first (generator + step kernel); with ts_staged the
-    time-split step reads a staged block too."""
+    step (one live row; with or without P) is one time-split kernel generating its own
+    scenarios; a step with every row live stages its block first (generator + k_grid); with
+    ts_staged the time-split step reads a staged block too."""
     m = rg.DisturbanceModel.scaled(0.001, 3)
     prob = _problem(-0.9, 0.9, 0.0, 0.05, 256)
     vp = 0.4
@@ -540,7 +540,8 @@ def test_grid_step_kernel_count(ctx, tuned):
         return ctx.get_option("grid_step_kernels") - k0, ctx.get_option("last_grid_kernel")
 
     assert count(vp) == (1, 1)             # one live row: k_grid_ts, fused RNG
-    assert count(vp, want_pbits=True) == (2, 0)  # P requested: device rows, staged k_grid
+    assert count(vp, want_pbits=True) == (1, 1)  # with P too (the other rows' words zeroed)
+    assert count(vp + 0.3) == (2, 0)       # 32 distinct live rows: staged block + k_grid
     tuned(ts_staged=1)
     assert count(vp) == (2, 1)
 
@@ -599,3 +600,35 @@ def test_time_split_random_stress(ctx, tuned):
     ref, ks_ref = run()
     assert set(ks_ref) == {0}
     assert ts == ref and staged == ref
+
+
+@pytest.mark.parametrize("n", [33, 1000, 10_000])
+def test_row_plan_with_p_equals_device_rows(ctx, tuned, n):
+    """Steps that return P also launch only the host-planned rows (time-split or k_grid):
+    the gated-out and duplicate rows' words come back zero, so P, the per-row counts and
+    the row equal the device-derived rows' -- through robust_rg_parallel's expansion too."""
+    rng = np.random.default_rng(n + 3)
+    m = rg.DisturbanceModel.scaled(0.02, 3)
+    prob = _problem(-0.9, 0.9, 0.0, 0.05, 96)
+    cases = []
+    for trial in range(8):
+        vp = float(rng.uniform(-1.2, 1.2))
+        r = [vp, vp + 1e-3, float(rng.uniform(-3, 3)), 2.9][trial % 4]
+        x0 = np.array([np.tanh(vp), vp, np.tanh(vp) / 2]) + rng.uniform(-0.06, 0.06, 3)
+        cases.append((vp, r, x0, int(rng.choice([8, 32])), trial % 3 == 1,
+                      _capi.make_scenarios(70 + trial, 0, n, m.lo, m.span)))
+
+    def run():
+        out = []
+        for vp, r, x0, M, prefix, sc in cases:
+            res, viol, pb = ctx.grid_step(prob, x0, vp, r, M, prefix, None, n, sc, True)
+            out.append((res.row, res.n_active, res.ss_pruned_rows, res.dedup_rows,
+                        viol.tolist(), pb.copy()))
+        return out
+
+    planned = run()
+    tuned(no_row_plan=1)
+    device = run()
+    for a, b in zip(planned, device):
+        assert a[:5] == b[:5]
+        assert np.array_equal(a[5], b[5])
