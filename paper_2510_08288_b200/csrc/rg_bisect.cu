@@ -404,7 +404,13 @@ __global__ void __launch_bounds__(256, RG_GRID_MINB) k_bisect(BisectArgs a) {
             const bool run = !fin && ss_gate(v, a.p);
             bool ok = false;
             int32_t sr = 0;
-            if (run || U) {
+            if (it < 0 && a.probe_ok) {
+                // the kappa = 1 probe was rolled out ahead (rg_bisect: the time-split kernel,
+                // used only when v = r passes the gate): its verdict and early bit
+                const unsigned bit = 1u << (kk & 31);
+                ok = run && (a.probe_ok[kk >> 5] & bit) != 0u;
+                sr = run && (a.probe_early[kk >> 5] & bit) != 0u ? 0 : a.p.j_star;
+            } else if (run || U) {
                 int st;
                 if (SRC == 1)
                     st = rollout<FMA, false, RngSource, true>(c, a.x0[0], a.x0[1], a.x0[2], v,

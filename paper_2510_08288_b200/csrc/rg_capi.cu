@@ -137,6 +137,7 @@ struct Tuning {
     int no_row_plan = 0;      // grid step: rows always derived on the device
     int no_ts = 0;            // grid step: never the time-split form (rg_ts.cu)
     int ts_staged = 0;        // time-split step: staged scenario block instead of the fused RNG
+    int no_ts_probe = 0;      // Alg. 2: the kappa = 1 probe inside k_bisect, not time-split
     int64_t batch_chunk = 0;  // batched step: at most this many staged episodes per chunk
 };
 
@@ -169,6 +170,7 @@ struct rg_ctx {
     HostBuf h_stage;
     HostBuf h_out;                  // zero-copy grid result block (pinned, UVA-mapped)
     DevBuf j_state;                 // joint bisection state (rg::JointState)
+    DevBuf probe;                   // the bisection's kappa = 1 probe bits (ok, early)
     rg::JointArgs j_args{};         // the joint search in progress (rg_joint_begin)
     int j_src = -1;                 // its scenario source; -1 = none begun
     unsigned long long seq_ctr = 0; // grid-step publication tokens
@@ -329,6 +331,7 @@ Tuning env_tuning() {
     if (getenv("RG_NO_ROW_PLAN")) t.no_row_plan = 1;
     if (getenv("RG_NO_TS")) t.no_ts = 1;
     if (getenv("RG_TS_STAGED")) t.ts_staged = 1;
+    if (getenv("RG_NO_TS_PROBE")) t.no_ts_probe = 1;
     if (const char* e = getenv("RG_BATCH_CHUNK")) t.batch_chunk = atoll(e);
     if (!(t.force_tpb == 32 || t.force_tpb == 64 || t.force_tpb == 128)) t.force_tpb = 0;
     return t;
@@ -459,7 +462,7 @@ int32_t rg_destroy(rg_ctx* ctx) {
                       &ctx->vrows, &ctx->tmp_a, &ctx->tmp_b, &ctx->kap_k, &ctx->fnd_k,
                       &ctx->cel_k, &ctx->erl_k, &ctx->path_k, &ctx->path_o, &ctx->e_in,
                       &ctx->e_viol, &ctx->e_early, &ctx->e_ticket, &ctx->e_out,
-                      &ctx->e_violout};
+                      &ctx->e_violout, &ctx->probe};
     for (DevBuf* b : bufs) b->release();
     ctx->h_stage.release();
     ctx->h_out.release();
@@ -491,6 +494,8 @@ int32_t rg_set_option(rg_ctx* ctx, const char* name, int64_t value) {
         t.no_ts = value != 0;
     } else if (!strcmp(name, "ts_staged")) {
         t.ts_staged = value != 0;
+    } else if (!strcmp(name, "no_ts_probe")) {
+        t.no_ts_probe = value != 0;
     } else if (!strcmp(name, "xchg_timeout_ms")) {
         if (value < 1) return fail(RG_E_ARGS, "xchg_timeout_ms must be >= 1");
         t.xchg_timeout_ms = value;
@@ -514,6 +519,7 @@ int32_t rg_get_option(rg_ctx* ctx, const char* name, int64_t* value) {
     else if (!strcmp(name, "no_row_plan")) *value = t.no_row_plan;
     else if (!strcmp(name, "no_ts")) *value = t.no_ts;
     else if (!strcmp(name, "ts_staged")) *value = t.ts_staged;
+    else if (!strcmp(name, "no_ts_probe")) *value = t.no_ts_probe;
     else if (!strcmp(name, "xchg_timeout_ms")) *value = t.xchg_timeout_ms;
     else if (!strcmp(name, "batch_chunk")) *value = t.batch_chunk;
     else if (!strcmp(name, "last_grid_kernel")) *value = ctx->last_grid_kernel;
@@ -1025,11 +1031,25 @@ int32_t rg_bisect(rg_ctx* ctx, const rg_problem* prob, const double* x0, double 
     a.r = r;
     a.n_kappa = n_kappa;
     a.n_sim = n_sim;
+    // Every scenario's search starts with the kappa = 1 probe (v = r), one candidate over all
+    // scenarios -- the time-split kernel's regime (rg_ts.cu).  When v = r passes the gate
+    // and the scenarios fit one wave of it, the probe runs there first and k_bisect takes
+    // each scenario's verdict and early bit from its output instead of rolling it out; a
+    // closed loop's steady-state search is the probe alone.  With an RNG stream neither
+    // stages a block: the probe's producers and k_bisect's rollouts hash their own.
+    const int64_t probe_units = (n_sim + 31) / 32;
+    const bool probe = (dist || rng) && !ctx->tune.no_ts && !ctx->tune.no_ts_probe &&
+                       a.p.vlo <= r && r <= a.p.vhi &&
+                       probe_units <= (int64_t)rg::kTsUnits * ctx->sm_count;
     int src = 0;
     if (dist) {
         src = 2;
         if ((rc = stage_dist(ctx, dist, n_sim, horizon, prob->j_star, flags, &a.soa, &a.ld)))
             return rc;
+    } else if (rng && probe && !(flags & RG_STAGE_RNG)) {
+        src = 1;
+        a.stream = make_stream(rng);
+        a.k0 = rng->k0;
     } else if (rng && want_stage(n_sim, prob->j_star, flags, kStageMaxScenarioStepsBisect)) {
         src = 2;
         if ((rc = stage_rng(ctx, rng, n_sim, prob->j_star, &a.soa, &a.ld))) return rc;
@@ -1077,6 +1097,47 @@ int32_t rg_bisect(rg_ctx* ctx, const rg_problem* prob, const double* x0, double 
     grid_placement(ctx, n_sim, 1, &a.tpb, &a.smem_dyn);
     const bool timed = !(flags & RG_NO_TIMING);
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+    if (probe && (src == 1 || src == 2)) {  // the kappa = 1 probe on the time-split kernel
+        if ((rc = grow_grid(ctx, 2))) return rc;
+        rg::GridArgs g{};
+        g.p = a.p;
+        for (int i = 0; i < 3; ++i) g.x0[i] = a.x0[i];
+        g.v_prev = v_prev;
+        g.r = r;  // row 1 of 2: kappa = 1, v = r
+        g.m_grid = 2;
+        g.n_sim = n_sim;
+        g.listed = 1;
+        g.list_n = 1;
+        g.row_list[0] = 1;
+        g.src_tab[0] = -2;
+        g.src_tab[1] = -1;
+        if (src == 2) {
+            g.soa = a.soa;
+            g.ld = a.ld;
+        } else {
+            g.stream = a.stream;
+            g.k0 = a.k0;
+        }
+        g.viol = ctx->g_viol.as<unsigned>();
+        g.early = ctx->g_early.as<unsigned long long>();
+        g.ovf = ctx->g_ovf.as<unsigned long long>();
+        g.abandoned = ctx->g_aband.as<unsigned long long>();
+        g.row_src = ctx->g_src.as<int>();
+        g.ticket = ctx->g_ticket.as<unsigned>();
+        g.pwords = probe_units;
+        const size_t words = (size_t)2 * probe_units;
+        RG_CUDA(ctx->probe.ensure(2 * words * sizeof(unsigned)));
+        g.pbits = ctx->probe.as<unsigned>();
+        g.ebits = g.pbits + words;
+        RG_CUDA(ctx->g_out.ensure(kOutHead + viol_bytes(2)));
+        g.out = ctx->g_out.as<rg::GridOut>();
+        g.viol_out = reinterpret_cast<unsigned*>(ctx->g_out.as<char>() + kOutHead);
+        g.seq_token = ++ctx->seq_ctr;
+        RG_CUDA(rg::launch_grid_ts(g, ctx->variant == rg::kTanhFma, src == 1, ctx->sm_count,
+                                   ctx->stream));
+        a.probe_ok = g.pbits + probe_units;  // row 1
+        a.probe_early = g.ebits + probe_units;
+    }
     RG_CUDA(rg::launch_bisect(a, ctx->variant == rg::kTanhFma, src, ctx->stream));
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     if (!dev) {

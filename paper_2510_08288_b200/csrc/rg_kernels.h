@@ -106,6 +106,7 @@ struct GridArgs {
     // grid_placement); 0: no pin
     int smem_dyn;
     int no_s2;  // single-wave step without the two-step rollout (A/B and tests)
+    unsigned* ebits;  // optional [m][pwords]: cells that ended before j* (the time-split step)
     // single-wave staged step with the generator fused in (gen = 1): every block writes its
     // share of the SoA block to soa_w, then a grid barrier (bar[0] count, bar[1] generation;
     // cooperative launch, every block resident) before any rollout reads it
@@ -226,6 +227,10 @@ struct BisectArgs {
     BisectOut* out;
     int tpb;
     int smem_dyn;  // shared memory per block, static + dynamic (single-wave placement pin)
+    // the kappa = 1 probe already rolled out (by the time-split kernel, rg_capi.cu: rg_bisect):
+    // bit k of word k/32 -- the probe's verdict and whether it ended before j*
+    const unsigned* probe_ok;
+    const unsigned* probe_early;
 };
 
 // Joint bisection: one candidate kappa for every

@@ -23,7 +23,7 @@ def ctx():
 
 
 _DEFAULTS = {"force_tpb": 0, "no_placement": 0, "no_pdl": 0, "no_step2": 0, "fused_gen": 0,
-             "batch_chunk": 0, "no_row_plan": 0, "no_ts": 0, "ts_staged": 0}
+             "batch_chunk": 0, "no_row_plan": 0, "no_ts": 0, "ts_staged": 0, "no_ts_probe": 0}
 
 
 @pytest.fixture
@@ -552,6 +552,7 @@ def test_options_round_trip(ctx, tuned):
 
     for name, value in (("force_tpb", 64), ("no_placement", 1), ("no_pdl", 1), ("no_step2", 1),
                         ("fused_gen", 1), ("no_row_plan", 1), ("no_ts", 1), ("ts_staged", 1),
+                        ("no_ts_probe", 1),
                         ("batch_chunk", 7), ("xchg_timeout_ms", 1234)):
         before = ctx.get_option(name)
         ctx.set_option(name, value)
@@ -632,3 +633,43 @@ def test_row_plan_with_p_equals_device_rows(ctx, tuned, n):
     for a, b in zip(planned, device):
         assert a[:5] == b[:5]
         assert np.array_equal(a[5], b[5])
+
+
+@pytest.mark.parametrize("n", [1, 45, 1000, 10_000])
+def test_bisect_time_split_probe_equals_inline_probe(ctx, tuned, n):
+    """Alg. 2's kappa = 1 probe run ahead by the time-split kernel (its verdict and early bits
+    handed to k_bisect) against the probe rolled out inside k_bisect: the same kappa, found,
+    cells and early counts, per-scenario results and search paths -- steady states (the
+    probe alone), transients (probe failures, then bisection), out-of-bounds starts,
+    generated and dense scenarios."""
+    rng = np.random.default_rng(11 * n + 1)
+    m = rg.DisturbanceModel.scaled(0.02, 3)
+    prob = _problem(-0.9, 0.9, 0.0, 0.05, 128)
+    dense = rg.sample_scenarios(m, n, 129, seed=5).data
+    cases = []
+    for trial in range(8):
+        vp = float(rng.uniform(-1.1, 1.1))
+        r = [vp, float(rng.uniform(-1.2, 1.2)), 2.4, vp + 0.05][trial % 4]
+        x0 = np.array([np.tanh(vp), vp, np.tanh(vp) / 2]) + rng.uniform(-0.08, 0.08, 3)
+        if trial == 6:
+            x0[0] = 0.93  # out of bounds: every rollout fails at step 0
+        cases.append((vp, r, x0, _capi.make_scenarios(40 + trial, 3, n, m.lo, m.span)))
+
+    def run():
+        out = []
+        for vp, r, x0, sc in cases:
+            for dist, scen in ((None, sc), (dense, None)):
+                b, per, path = ctx.bisect(prob, x0, vp, r, 8, dist, n, scen, per_scenario=True,
+                                          paths=True)
+                out.append(((b.kappa, b.found, b.cells, b.early),
+                            [np.asarray(a).copy() for a in per],
+                            [np.asarray(a).copy() for a in path]))
+        return out
+
+    probe = run()
+    tuned(no_ts_probe=1)
+    inline = run()
+    for a, b in zip(probe, inline):
+        assert a[0] == b[0]
+        for x, y in zip(a[1] + a[2], b[1] + b[2]):
+            assert np.array_equal(x, y, equal_nan=True)
