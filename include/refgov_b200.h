@@ -157,8 +157,8 @@ RG_API int32_t rg_get_tanh_variant(rg_ctx *ctx, int32_t *variant);
  * launching only the host-planned simulated rows), "no_ts" (0/1: never the time-split
  * grid kernel for host-planned steps with few cells), "ts_staged" (0/1: the time-split
  * kernel reads a staged scenario block instead of generating the disturbances itself),
- * "no_ts_probe" (0/1: rg_bisect rolls its kappa = 1 probe out inside k_bisect instead of
- * on the time-split kernel first).  Defaults come from the
+ * "no_ts_probe" (0/1: rg_bisect and the persistent rg_bisect_joint roll their kappa = 1
+ * probe out inside their own kernels instead of on the time-split kernel first).  Defaults come from the
  * RG_FORCE_TPB, RG_NO_PLACEMENT, RG_NO_PDL, RG_NO_STEP2, RG_FUSED_GEN, RG_NO_ROW_PLAN,
  * RG_NO_TS and RG_BATCH_CHUNK environment variables, read once at rg_create.  Unknown
  * names give RG_E_ARGS. */

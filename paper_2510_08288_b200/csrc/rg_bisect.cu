@@ -193,6 +193,11 @@ __global__ void __launch_bounds__(256, 1) k_joint_spec(JointArgs a) {
         b.hi = 1.0;
         b.it = -1;
         bracket_advance(b, a);
+        if (a.probe_out && !b.done && b.it < 0) {  // the probe's verdict and early count
+            b.early += (unsigned long long)((const volatile GridOut*)a.probe_out)->early_terms;
+            bracket_apply(b, *(const volatile unsigned*)a.probe_viol == 0u, a);
+            bracket_advance(b, a);
+        }
         cur = b;
     }
     __syncthreads();

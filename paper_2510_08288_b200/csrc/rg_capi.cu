@@ -1006,6 +1006,65 @@ int32_t rg_grid_fetch(rg_ctx* ctx, uint32_t* row_viol, int32_t m_grid, rg_grid_r
     return read_grid(ctx, row_viol, m_grid, out, nullptr, 0, false);
 }
 
+}  // extern "C"
+
+// The kappa = 1 probe of the bisections (v = r for every scenario) on the time-split kernel:
+// a one-row step (row 1 of two, row 0 gated out) writing each scenario's verdict (ok) and
+// early bit, and the result block (the row's violation count, early terminations).  All
+// outputs are device pointers valid until the next grid step or probe.
+static int32_t ts_probe(rg_ctx* ctx, const rg::ProblemDev& p, const double* x0, double v_prev,
+                        double r, int64_t n_sim, int src, const double* soa, int64_t ld,
+                        const rg::ScenarioStream& stream, int64_t k0, const unsigned** ok,
+                        const unsigned** early, const rg::GridOut** out,
+                        const unsigned** viol) {
+    int32_t rc;
+    if ((rc = grow_grid(ctx, 2))) return rc;
+    rg::GridArgs g{};
+    g.p = p;
+    for (int i = 0; i < 3; ++i) g.x0[i] = x0[i];
+    g.v_prev = v_prev;
+    g.r = r;  // row 1 of 2: kappa = 1, v = r
+    g.m_grid = 2;
+    g.n_sim = n_sim;
+    g.listed = 1;
+    g.list_n = 1;
+    g.row_list[0] = 1;
+    g.src_tab[0] = -2;
+    g.src_tab[1] = -1;
+    if (src == 2) {
+        g.soa = soa;
+        g.ld = ld;
+    } else {
+        g.stream = stream;
+        g.k0 = k0;
+    }
+    g.viol = ctx->g_viol.as<unsigned>();
+    g.early = ctx->g_early.as<unsigned long long>();
+    g.ovf = ctx->g_ovf.as<unsigned long long>();
+    g.abandoned = ctx->g_aband.as<unsigned long long>();
+    g.row_src = ctx->g_src.as<int>();
+    g.ticket = ctx->g_ticket.as<unsigned>();
+    const int64_t pwords = (n_sim + 31) / 32;
+    g.pwords = pwords;
+    const size_t words = (size_t)2 * pwords;
+    RG_CUDA(ctx->probe.ensure(2 * words * sizeof(unsigned)));
+    g.pbits = ctx->probe.as<unsigned>();
+    g.ebits = g.pbits + words;
+    RG_CUDA(ctx->g_out.ensure(kOutHead + viol_bytes(2)));
+    g.out = ctx->g_out.as<rg::GridOut>();
+    g.viol_out = reinterpret_cast<unsigned*>(ctx->g_out.as<char>() + kOutHead);
+    g.seq_token = ++ctx->seq_ctr;
+    RG_CUDA(rg::launch_grid_ts(g, ctx->variant == rg::kTanhFma, src == 1, ctx->sm_count,
+                               ctx->stream));
+    *ok = g.pbits + pwords;  // row 1
+    *early = g.ebits + pwords;
+    *out = g.out;
+    *viol = g.viol_out + 1;
+    return RG_OK;
+}
+
+extern "C" {
+
 int32_t rg_bisect(rg_ctx* ctx, const rg_problem* prob, const double* x0, double v_prev,
                   double r, int32_t n_kappa, const double* dist, int64_t n_sim, int64_t horizon,
                   const rg_scenarios* rng, double* kappa_k, int32_t* found_k, int32_t* cells_k,
@@ -1098,45 +1157,11 @@ int32_t rg_bisect(rg_ctx* ctx, const rg_problem* prob, const double* x0, double 
     const bool timed = !(flags & RG_NO_TIMING);
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
     if (probe && (src == 1 || src == 2)) {  // the kappa = 1 probe on the time-split kernel
-        if ((rc = grow_grid(ctx, 2))) return rc;
-        rg::GridArgs g{};
-        g.p = a.p;
-        for (int i = 0; i < 3; ++i) g.x0[i] = a.x0[i];
-        g.v_prev = v_prev;
-        g.r = r;  // row 1 of 2: kappa = 1, v = r
-        g.m_grid = 2;
-        g.n_sim = n_sim;
-        g.listed = 1;
-        g.list_n = 1;
-        g.row_list[0] = 1;
-        g.src_tab[0] = -2;
-        g.src_tab[1] = -1;
-        if (src == 2) {
-            g.soa = a.soa;
-            g.ld = a.ld;
-        } else {
-            g.stream = a.stream;
-            g.k0 = a.k0;
-        }
-        g.viol = ctx->g_viol.as<unsigned>();
-        g.early = ctx->g_early.as<unsigned long long>();
-        g.ovf = ctx->g_ovf.as<unsigned long long>();
-        g.abandoned = ctx->g_aband.as<unsigned long long>();
-        g.row_src = ctx->g_src.as<int>();
-        g.ticket = ctx->g_ticket.as<unsigned>();
-        g.pwords = probe_units;
-        const size_t words = (size_t)2 * probe_units;
-        RG_CUDA(ctx->probe.ensure(2 * words * sizeof(unsigned)));
-        g.pbits = ctx->probe.as<unsigned>();
-        g.ebits = g.pbits + words;
-        RG_CUDA(ctx->g_out.ensure(kOutHead + viol_bytes(2)));
-        g.out = ctx->g_out.as<rg::GridOut>();
-        g.viol_out = reinterpret_cast<unsigned*>(ctx->g_out.as<char>() + kOutHead);
-        g.seq_token = ++ctx->seq_ctr;
-        RG_CUDA(rg::launch_grid_ts(g, ctx->variant == rg::kTanhFma, src == 1, ctx->sm_count,
-                                   ctx->stream));
-        a.probe_ok = g.pbits + probe_units;  // row 1
-        a.probe_early = g.ebits + probe_units;
+        const rg::GridOut* pout;
+        const unsigned* pviol;
+        if ((rc = ts_probe(ctx, a.p, a.x0, v_prev, r, n_sim, src, a.soa, a.ld, a.stream, a.k0,
+                           &a.probe_ok, &a.probe_early, &pout, &pviol)))
+            return rc;
     }
     RG_CUDA(rg::launch_bisect(a, ctx->variant == rg::kTanhFma, src, ctx->stream));
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
@@ -1332,7 +1357,23 @@ int32_t rg_bisect_joint(rg_ctx* ctx, const rg_problem* prob, const double* x0, d
     if (rc) return rc;
     const int depth = rg::joint_spec_depth(n_sim, ctx->sm_count);
     if (!(flags & RG_JOINT_ITER) && depth > 0 && n_kappa + 1 <= rg::kJointMaxRounds) {
-        // the whole search in one cooperative launch, speculating `depth` levels per round
+        // the whole search in one cooperative launch, speculating `depth` levels per round;
+        // its kappa = 1 probe first on the time-split kernel when v = r passes the gate (a
+        // steady-state search is the probe alone; the kernel starts after its verdict)
+        rg::JointArgs& ja = ctx->j_args;
+        ja.probe_out = nullptr;
+        ja.probe_viol = nullptr;
+        if ((ctx->j_src == 1 || ctx->j_src == 2) && !ctx->tune.no_ts && !ctx->tune.no_ts_probe &&
+            ja.p.vlo <= r && r <= ja.p.vhi &&
+            (n_sim + 31) / 32 <= (int64_t)rg::kTsUnits * ctx->sm_count) {
+            const unsigned *pok, *pearly;
+            if ((rc = ts_probe(ctx, ja.p, ja.x0, v_prev, r, n_sim, ctx->j_src, ja.soa, ja.ld,
+                               ja.stream, ja.k0, &pok, &pearly, &ja.probe_out,
+                               &ja.probe_viol))) {
+                ctx->j_src = -1;
+                return rc;
+            }
+        }
         ctx->j_args.depth = depth;
         const cudaError_t e = rg::launch_joint_spec(ctx->j_args, ctx->variant == rg::kTanhFma,
                                                     ctx->j_src, ctx->sm_count, ctx->stream);

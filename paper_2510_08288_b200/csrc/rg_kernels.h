@@ -274,6 +274,10 @@ struct JointArgs {
     int smem_dyn;  // shared memory per block, static + dynamic (single-wave placement pin)
     int fold;  // 1: the last block decides (single GPU); 0: k_joint_decide after the all-reduce
     int depth;  // persistent search: speculation depth (1..3): 2^depth - 1 candidates per round
+    // persistent search: the kappa = 1 probe already rolled out by the time-split kernel (its
+    // result block and violation count), applied before the first round
+    const GridOut* probe_out;
+    const unsigned* probe_viol;
     // scenario-sharded persistent search with the per-round exchange fused in (xchg = 1): after
     // the local grid barrier block 0 writes this shard's candidate verdicts into every rank's
     // window over NVLink (epoch xepoch0 + round), every block waits for every rank's verdicts

@@ -673,3 +673,30 @@ def test_bisect_time_split_probe_equals_inline_probe(ctx, tuned, n):
         assert a[0] == b[0]
         for x, y in zip(a[1] + a[2], b[1] + b[2]):
             assert np.array_equal(x, y, equal_nan=True)
+
+
+@pytest.mark.parametrize("n", [1, 500, 1000, 10_000])
+def test_joint_time_split_probe_equals_inline_probe(ctx, tuned, n):
+    """The persistent joint search's kappa = 1 probe rolled out first by the time-split
+    kernel against the probe inside the search: the same kappa, found and rollout count, in
+    steady states (the probe alone), gated-in transients and out-of-bounds starts."""
+    rng = np.random.default_rng(5 * n + 2)
+    m = rg.DisturbanceModel.scaled(0.02, 3)
+    prob = _problem(-0.9, 0.9, 0.0, 0.05, 128)
+    cases = []
+    for trial in range(10):
+        vp = float(rng.uniform(-1.1, 1.1))
+        r = [vp, float(rng.uniform(-1.2, 1.2)), vp + 0.05, 2.4][trial % 4]
+        x0 = np.array([np.tanh(vp), vp, np.tanh(vp) / 2]) + rng.uniform(-0.08, 0.08, 3)
+        if trial == 5:
+            x0[0] = 0.93
+        cases.append((vp, r, x0, _capi.make_scenarios(60 + trial, 0, n, m.lo, m.span)))
+
+    def run():
+        return [(lambda j: (j.kappa, j.found, j.cells))(
+            ctx.bisect_joint(prob, x0, vp, r, 8, None, n, sc)) for vp, r, x0, sc in cases]
+
+    probe = run()
+    tuned(no_ts_probe=1)
+    inline = run()
+    assert probe == inline
