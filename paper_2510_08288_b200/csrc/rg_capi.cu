@@ -886,8 +886,8 @@ int32_t rg_grid_step(rg_ctx* ctx, const rg_problem* prob, const double* x0, doub
     const bool timed = !(flags & RG_NO_TIMING);
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
     if (use_ts)
-        RG_CUDA(rg::launch_grid_ts(a, ctx->variant == rg::kTanhFma, use_rng, ctx->sm_count,
-                                   ctx->stream));
+        RG_CUDA(rg::launch_grid_ts(a, ctx->variant == rg::kTanhFma, use_rng ? 1 : 2,
+                                   ctx->sm_count, ctx->stream));
     else
         RG_CUDA(rg::launch_grid(a, ctx->variant == rg::kTanhFma, use_rng, abandon, ctx->stream));
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
@@ -1054,7 +1054,7 @@ static int32_t ts_probe(rg_ctx* ctx, const rg::ProblemDev& p, const double* x0, 
     g.out = ctx->g_out.as<rg::GridOut>();
     g.viol_out = reinterpret_cast<unsigned*>(ctx->g_out.as<char>() + kOutHead);
     g.seq_token = ++ctx->seq_ctr;
-    RG_CUDA(rg::launch_grid_ts(g, ctx->variant == rg::kTanhFma, src == 1, ctx->sm_count,
+    RG_CUDA(rg::launch_grid_ts(g, ctx->variant == rg::kTanhFma, src, ctx->sm_count,
                                ctx->stream));
     *ok = g.pbits + pwords;  // row 1
     *early = g.ebits + pwords;
@@ -1097,7 +1097,7 @@ int32_t rg_bisect(rg_ctx* ctx, const rg_problem* prob, const double* x0, double 
     // closed loop's steady-state search is the probe alone.  With an RNG stream neither
     // stages a block: the probe's producers and k_bisect's rollouts hash their own.
     const int64_t probe_units = (n_sim + 31) / 32;
-    const bool probe = (dist || rng) && !ctx->tune.no_ts && !ctx->tune.no_ts_probe &&
+    const bool probe = !ctx->tune.no_ts && !ctx->tune.no_ts_probe &&
                        a.p.vlo <= r && r <= a.p.vhi &&
                        probe_units <= (int64_t)rg::kTsUnits * ctx->sm_count;
     int src = 0;
@@ -1156,7 +1156,7 @@ int32_t rg_bisect(rg_ctx* ctx, const rg_problem* prob, const double* x0, double 
     grid_placement(ctx, n_sim, 1, &a.tpb, &a.smem_dyn);
     const bool timed = !(flags & RG_NO_TIMING);
     if (timed) RG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-    if (probe && (src == 1 || src == 2)) {  // the kappa = 1 probe on the time-split kernel
+    if (probe) {  // the kappa = 1 probe on the time-split kernel
         const rg::GridOut* pout;
         const unsigned* pviol;
         if ((rc = ts_probe(ctx, a.p, a.x0, v_prev, r, n_sim, src, a.soa, a.ld, a.stream, a.k0,
@@ -1363,7 +1363,7 @@ int32_t rg_bisect_joint(rg_ctx* ctx, const rg_problem* prob, const double* x0, d
         rg::JointArgs& ja = ctx->j_args;
         ja.probe_out = nullptr;
         ja.probe_viol = nullptr;
-        if ((ctx->j_src == 1 || ctx->j_src == 2) && !ctx->tune.no_ts && !ctx->tune.no_ts_probe &&
+        if (ctx->j_src >= 0 && !ctx->tune.no_ts && !ctx->tune.no_ts_probe &&
             ja.p.vlo <= r && r <= ja.p.vhi &&
             (n_sim + 31) / 32 <= (int64_t)rg::kTsUnits * ctx->sm_count) {
             const unsigned *pok, *pearly;

@@ -307,10 +307,10 @@ cudaError_t launch_gen_soa_batch(const uint64_t* hs, const double* lo, const dou
                                  int64_t k0, int64_t n_sim, int32_t j_star, int64_t ld,
                                  int32_t n_ep, int64_t ep_stride, double* dst, cudaStream_t s);
 cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, cudaStream_t s);
-// the time-split form (rg_ts.cu): staged scenarios or (rng) the fused counter RNG, no
-// polling; ts_blocks = its grid size
+// the time-split form (rg_ts.cu), no polling: src 1 the fused counter RNG, 2 the staged
+// scenarios, 0 no disturbance (the nominal prediction); ts_blocks = its grid size
 int ts_blocks(int64_t units, int sms);
-cudaError_t launch_grid_ts(const GridArgs& a, bool fma, bool rng, int sms, cudaStream_t s);
+cudaError_t launch_grid_ts(const GridArgs& a, bool fma, int src, int sms, cudaStream_t s);
 // Pairs [a.p0, a.p0 + n_pairs) of the compacted list, a.bpr blocks of a.tpb threads each.
 cudaError_t launch_grid_batch(const BatchArgs& a, int64_t n_pairs, bool fma, bool poll,
                               cudaStream_t s);

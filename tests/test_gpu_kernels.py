@@ -658,7 +658,8 @@ def test_bisect_time_split_probe_equals_inline_probe(ctx, tuned, n):
     def run():
         out = []
         for vp, r, x0, sc in cases:
-            for dist, scen in ((None, sc), (dense, None)):
+            # generated, dense, and no scenarios (bisection_rg's nominal prediction)
+            for dist, scen in ((None, sc), (dense, None), (None, None)):
                 b, per, path = ctx.bisect(prob, x0, vp, r, 8, dist, n, scen, per_scenario=True,
                                           paths=True)
                 out.append(((b.kappa, b.found, b.cells, b.early),
@@ -693,8 +694,12 @@ def test_joint_time_split_probe_equals_inline_probe(ctx, tuned, n):
         cases.append((vp, r, x0, _capi.make_scenarios(60 + trial, 0, n, m.lo, m.span)))
 
     def run():
-        return [(lambda j: (j.kappa, j.found, j.cells))(
-            ctx.bisect_joint(prob, x0, vp, r, 8, None, n, sc)) for vp, r, x0, sc in cases]
+        out = []
+        for vp, r, x0, sc in cases:
+            for scen in (sc, None):  # generated, and the nominal prediction
+                j = ctx.bisect_joint(prob, x0, vp, r, 8, None, n, scen)
+                out.append((j.kappa, j.found, j.cells))
+        return out
 
     probe = run()
     tuned(no_ts_probe=1)
