@@ -275,6 +275,8 @@ int32_t stage_rng(rg_ctx* ctx, const rg_scenarios* rng, int64_t n_sim, int32_t j
 // The bisections run each scenario only until it fails, often a few steps:
 // generating the whole block up front pays off only while it is L2-sized.
 constexpr int64_t kStageMaxScenarioStepsBisect = 4ll << 20;  // 96 MB of SoA
+// internal rg_joint_begin flag (not in the public header): an RNG stream is not staged
+constexpr int32_t kJointPreferFused = 0x40000000;
 
 bool want_stage(int64_t n_sim, int32_t j_star, int32_t flags,
                 int64_t max_steps = kStageMaxScenarioSteps) {
@@ -1232,7 +1234,8 @@ int32_t rg_joint_begin(rg_ctx* ctx, const rg_problem* prob, const double* x0, do
         src = 2;
         if ((rc = stage_dist(ctx, dist, n_sim, horizon, prob->j_star, flags, &a.soa, &a.ld)))
             return rc;
-    } else if (rng && want_stage(n_sim, prob->j_star, flags, kStageMaxScenarioStepsBisect)) {
+    } else if (rng && !(flags & kJointPreferFused) &&
+               want_stage(n_sim, prob->j_star, flags, kStageMaxScenarioStepsBisect)) {
         src = 2;
         if ((rc = stage_rng(ctx, rng, n_sim, prob->j_star, &a.soa, &a.ld))) return rc;
     } else if (rng) {
@@ -1352,10 +1355,17 @@ int32_t rg_bisect_joint(rg_ctx* ctx, const rg_problem* prob, const double* x0, d
                         double r, int32_t n_kappa, const double* dist, int64_t n_sim,
                         int64_t horizon, const rg_scenarios* rng, rg_bisect_result* out,
                         int32_t flags) {
-    int32_t rc = rg_joint_begin(ctx, prob, x0, v_prev, r, n_kappa, dist, n_sim, horizon, rng,
-                                flags);
-    if (rc) return rc;
+    if (!ctx || !prob) return fail(RG_E_ARGS, "null argument");
     const int depth = rg::joint_spec_depth(n_sim, ctx->sm_count);
+    // a persistent search whose kappa = 1 probe goes to the time-split kernel with the RNG
+    // generates its scenarios in the kernels (a steady-state search then stages nothing)
+    const bool probe_rng = rng && !dist && !(flags & (RG_JOINT_ITER | RG_STAGE_RNG)) &&
+                           depth > 0 && !ctx->tune.no_ts && !ctx->tune.no_ts_probe &&
+                           prob->ss_v_lower <= r && r <= prob->ss_v_upper &&
+                           (n_sim + 31) / 32 <= (int64_t)rg::kTsUnits * ctx->sm_count;
+    int32_t rc = rg_joint_begin(ctx, prob, x0, v_prev, r, n_kappa, dist, n_sim, horizon, rng,
+                                flags | (probe_rng ? kJointPreferFused : 0));
+    if (rc) return rc;
     if (!(flags & RG_JOINT_ITER) && depth > 0 && n_kappa + 1 <= rg::kJointMaxRounds) {
         // the whole search in one cooperative launch, speculating `depth` levels per round;
         // its kappa = 1 probe first on the time-split kernel when v = r passes the gate (a
