@@ -33,10 +33,16 @@ __global__ void k_gen_soa_batch(const uint64_t* __restrict__ hs, double3 lo, dou
 // batched grid step over the compacted (episode, row) pairs
 // ---------------------------------------------------------------------------
 
-// Launch bounds: at most 168 registers (3 blocks of 128 threads per SM), so the
-// 64-thread blocks keep 12 warps per SM (3 per SMSP) in this always multi-wave kernel.
+// Launch bounds: at most 80 registers (6 blocks of 128 threads per SM; ptxas needs 80,
+// no spills), so the 64-thread blocks keep up to 24 warps per SM in this always multi-wave
+// kernel.  C5 per closed-loop step (scripts/ab_pairs_regs.sh): 3 blocks (154 registers)
+// 179.7 ms, 4: 183.5, 5: 178.1, 6: 177.1-177.4, 8 (64 registers): 178.8 -- the FP64 pipe,
+// not latency, bounds it (ncu: 69.6% busy at 3 warps per scheduler).
+#ifndef RG_PAIRS_MINB
+#define RG_PAIRS_MINB 6
+#endif
 template <bool FMA, bool POLL, bool SOA>
-__global__ void __launch_bounds__(128, 3) k_grid_pairs(BatchArgs a) {
+__global__ void __launch_bounds__(128, RG_PAIRS_MINB) k_grid_pairs(BatchArgs a) {
     __shared__ bool s_last;
     const int64_t pair = a.p0 + blockIdx.x / (unsigned)a.bpr;
     const int64_t kb = blockIdx.x % (unsigned)a.bpr;
