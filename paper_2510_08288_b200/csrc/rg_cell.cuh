@@ -374,16 +374,20 @@ __device__ __forceinline__ int rollout(const CellConst& p, double x1, double x2,
 // cp.async copies of steps j+6, j+7; then the pairs swap roles.
 
 constexpr int kRing4Stride = 256;  // threads per block of the two-step rollout, at most
+#ifndef RG_RING_PAIRS
+#define RG_RING_PAIRS 2
+#endif
+constexpr int kRing4Pairs = RG_RING_PAIRS;  // slot pairs in flight (2: double buffering)
 
 struct Soa4Source {
     const double* d;  // already offset by k
     int64_t ld;
-    double* ring;     // &ring[0][0][0][threadIdx.x] of a [2][2][3][kRing4Stride] array
+    double* ring;     // &ring[0][0][0][threadIdx.x] of a [kRing4Pairs][2][3][kRing4Stride] array
     const double* nxt = nullptr;   // next step to issue (clamped walk)
     const double* last = nullptr;  // step J-1
     int64_t stride = 0;
     uint32_t base = 0;  // shared-memory address of this lane's pair 0, slot 0, component 0
-    uint32_t rd = 0;    // byte offset of the pair read in this iteration (0 or kPair)
+    uint32_t rd = 0;    // byte offset of the pair read in this iteration
     static constexpr uint32_t kComp = 8 * kRing4Stride, kSlot = 3 * kComp, kPair = 2 * kSlot;
     __device__ __forceinline__ void init(int32_t J) {
         stride = 3 * ld;
@@ -407,7 +411,10 @@ struct Soa4Source {
         issue_one(sa + kSlot);
         asm volatile("cp.async.commit_group;");
     }
-    __device__ __forceinline__ void wait() { asm volatile("cp.async.wait_group 0;"); }
+    // the oldest pair in flight has landed (kRing4Pairs - 2 younger groups may still fly)
+    __device__ __forceinline__ void wait() {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kRing4Pairs - 2));
+    }
     __device__ __forceinline__ static double lds(uint32_t a) {
         double v;
         asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
@@ -418,26 +425,31 @@ struct Soa4Source {
         o[1] = lds(a + kComp);
         o[2] = lds(a + 2 * kComp);
     }
-    // prologue: steps 0, 1 read; steps 2, 3 in flight into pair 1 (read by next(-2))
+    __device__ __forceinline__ uint32_t after(uint32_t off) const {
+        return off + kPair == kRing4Pairs * kPair ? 0u : off + kPair;
+    }
+    // prologue: step pairs 0 .. kRing4Pairs-1 issued, pair 0 (steps 0, 1) read; pair 1 is
+    // read by next(-2)
     __device__ __forceinline__ void start(double (&dd)[2][3]) {
-        issue_pair(0);
-        issue_pair(kPair);
-        asm volatile("cp.async.wait_group 1;");
+#pragma unroll
+        for (int q = 0; q < kRing4Pairs; ++q) issue_pair(q * kPair);
+        asm volatile("cp.async.wait_group %0;" ::"n"(kRing4Pairs - 1));
         read_slot(base, dd[0]);
         read_slot(base + kSlot, dd[1]);
         rd = kPair;
     }
-    // iteration j: steps j+4, j+5 (landed in pair rd) read, steps j+6, j+7 issued into
-    // the other pair (read, into registers, in iteration j-2); the pairs swap roles
+    // iteration j: pair (j+4)/2 (steps j+4, j+5) read from offset rd; the pair read in
+    // iteration j-2 (the one before rd, now free) receives steps j+2+2*kRing4Pairs, +1
     __device__ __forceinline__ void next(int32_t, double (&e4)[3], double (&e5)[3]) {
         wait();
         const uint32_t a = base + rd;
         read_slot(a, e4);
         read_slot(a + kSlot, e5);
-        rd = kPair - rd;
-        issue_pair(rd);
+        const uint32_t freed = rd == 0 ? (kRing4Pairs - 1) * kPair : rd - kPair;
+        rd = after(rd);
+        issue_pair(freed);
     }
-    __device__ __forceinline__ void finish() { wait(); }
+    __device__ __forceinline__ void finish() { asm volatile("cp.async.wait_group 0;"); }
 };
 
 struct Rng4Source {  // fused counter RNG (micro-benchmarks)

@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(256, RG_GRID_MINB) k_grid(GridArgs a) {
         int32_t steps = a.p.j_star;
         if constexpr (S2) {
             static_assert(!RNG, "the two-step rollout reads a staged block");
-            __shared__ double ring4[4 * 3 * kRing4Stride];
+            __shared__ double ring4[kRing4Pairs * 2 * 3 * kRing4Stride];
             Soa4Source src;
             src.d = a.soa + kk;
             src.ld = a.ld;
