@@ -898,8 +898,11 @@ def active_cells(V_prev, R, m_grid, interval):
 
 def run_c3(args, rank, world, local_rank, spec, backend, cpu_group):
     """C3: the reference's desk-scale closed loop (harness.py:138-224) at n_sim scenarios per
-    step through the public API (run_closed_loop: the native loop rg_closed_loop -- the
-    device grid step, then the true plant on the host in C with numpy's tanh restated).  W untimed closed-loop steps of another episode (seed + 1000), then
+    step through the public API (run_closed_loop: rg_closed_loop, which runs the whole trace
+    as one cooperative kernel, k_loop_ts -- every governor step on the time-split form, the
+    row, kappa, v_t and the true plant with numpy's tanh restated on the device between grid
+    barriers; with RG_NO_DEVICE_LOOP=1 one grid-step launch per closed-loop step and the
+    plant on the host).  W untimed closed-loop steps of another episode (seed + 1000), then
     the timed episode from t = 0 for K steps; host wall clock of the whole loop (it is the
     latency a controller sees: sampling descriptor, device step, result, plant update), the
     max over ranks.  Cell-steps = the reference's sims_run x j* summed over the timed steps."""
@@ -934,6 +937,7 @@ def run_c3(args, rank, world, local_rank, spec, backend, cpu_group):
     # counted by the library: the step kernel per step (the time-split step generates its
     # own scenarios), plus the generator where a step staged its block
     launches = ctx.get_option("grid_step_kernels") - launches0
+    device_loop = bool(ctx.get_option("last_loop_device"))
     assert not rec.aborted
     sims = sum(int(d.split(",")[4]) for d in rec.diag_rows)
     total = _max_over_ranks(wall, world, dev)
@@ -962,15 +966,23 @@ def run_c3(args, rank, world, local_rank, spec, backend, cpu_group):
                 "active_rows_mean": sims / (n * args.steps * world),
                 "timing": "host wall clock of the whole timed closed loop (device governor step, "
                           "host true-plant step, result readback), max over ranks"},
-        # per step: the state, v_prev and r travel as kernel parameters (5 doubles) beside the
-        # RNG descriptor and the host row plan (112 B); the result block (128 B header +
-        # M row words) is written by the kernel into pinned host memory.  The loop never
-        # reads P, so run_closed_loop asks for none (the reference's diagnostics stay).
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 5 * 8 + 112,
-                "d2h_bytes_per_step": 128 + 4 * M_GRID,
-                "note": "the timed loop is the public API end to end: run_closed_loop, which "
-                        "runs the governed loop natively (rg_closed_loop: grid step without P, "
-                        "kappa, v_t, the true plant with the library's numpy tanh)"},
+        # device loop: per step r_t and d_true[t] in (32 B) and v, kappa, y, sims, early,
+        # device ns and the feasible flag out (49 B), copied once around the one launch.
+        # Per-step loop: the state, v_prev and r travel as kernel parameters (5 doubles)
+        # beside the RNG descriptor and the host row plan (112 B); the result block (128 B
+        # header + M row words) is written by the kernel into pinned host memory.  The loop
+        # never reads P, so run_closed_loop asks for none (the reference's diagnostics stay).
+        "e2e": {"value": value, "unit": UNIT,
+                "h2d_bytes_per_step": 32 if device_loop else 5 * 8 + 112,
+                "d2h_bytes_per_step": 49 if device_loop else 128 + 4 * M_GRID,
+                "note": "the timed loop is the public API end to end: run_closed_loop -> "
+                        "rg_closed_loop, " + (
+                            "the whole trace as one cooperative kernel (k_loop_ts: grid step, "
+                            "row, kappa, v_t and the true plant with numpy's tanh restated, on "
+                            "the device)" if device_loop else
+                            "one grid step launch per closed-loop step, then kappa, v_t and "
+                            "the true plant on the host")},
+        "device_loop": device_loop,
         "roofline": roof, "cpu_baseline": cb, "clocks": clocks, "gpu_launches": launches,
     }
 

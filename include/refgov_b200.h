@@ -158,15 +158,19 @@ RG_API int32_t rg_get_tanh_variant(rg_ctx *ctx, int32_t *variant);
  * grid kernel for host-planned steps with few cells), "ts_staged" (0/1: the time-split
  * kernel reads a staged scenario block instead of generating the disturbances itself),
  * "no_ts_probe" (0/1: rg_bisect and the persistent rg_bisect_joint roll their kappa = 1
- * probe out inside their own kernels instead of on the time-split kernel first).  Defaults come from the
- * RG_FORCE_TPB, RG_NO_PLACEMENT, RG_NO_PDL, RG_NO_STEP2, RG_FUSED_GEN, RG_NO_ROW_PLAN,
- * RG_NO_TS and RG_BATCH_CHUNK environment variables, read once at rg_create.  Unknown
- * names give RG_E_ARGS. */
+ * probe out inside their own kernels instead of on the time-split kernel first),
+ * "no_device_loop" (0/1: rg_closed_loop launches one grid step per closed-loop step instead
+ * of running the whole trace in one kernel).  Defaults come from the RG_FORCE_TPB,
+ * RG_NO_PLACEMENT, RG_NO_PDL, RG_NO_STEP2, RG_FUSED_GEN, RG_NO_ROW_PLAN, RG_NO_TS,
+ * RG_TS_STAGED, RG_NO_TS_PROBE, RG_NO_DEVICE_LOOP and RG_BATCH_CHUNK environment variables,
+ * read once at rg_create.  Unknown names give RG_E_ARGS. */
 RG_API int32_t rg_set_option(rg_ctx *ctx, const char *name, int64_t value);
 /* Read a knob of rg_set_option, or the read-only "last_grid_kernel": which kernel the
  * context's last grid step launched (0 = k_grid, one warp per 32 rollouts; 1 = k_grid_ts,
- * the time-split form), or "grid_step_kernels": how many kernels the context's grid steps
- * have launched so far (the scenario staging kernel, when used, and the step kernel). */
+ * the time-split form), "grid_step_kernels": how many kernels the context's grid steps
+ * have launched so far (the scenario staging kernel, when used, and the step kernel; a
+ * device closed loop counts one), or "last_loop_device": 1 if the last rg_closed_loop ran
+ * on the device as one kernel. */
 RG_API int32_t rg_get_option(rg_ctx *ctx, const char *name, int64_t *value);
 /* The cudaStream_t the context launches on, as an opaque pointer. */
 RG_API int32_t rg_get_stream(rg_ctx *ctx, void **stream);
@@ -334,7 +338,14 @@ RG_API int32_t rg_fp64_peak(rg_ctx *ctx, double *flops_per_s);
  * (|x_i| > 1e6 or non-finite after the RK4 step; dynamics.py:125-130), the state leaving
  * the box after the disturbance (harness.py:222-224), or -- with infeasible_error --
  * the first step without a feasible row (InfeasibleError).  res->steps_done rows were
- * written.  x_out (3 doubles, may be NULL): the final state. */
+ * written.  x_out (3 doubles, may be NULL): the final state.
+ * With m_grid <= 64 and every r[t] finite the whole trace runs on the device as one
+ * cooperative kernel (k_loop_ts: the steps on the time-split form, and between them the
+ * row, kappa, v_t, the true plant with numpy's tanh and the next step's row plan, all on
+ * the device; wall_us_out then holds each governor step's device time); the "no_device_loop"
+ * option (or no_ts / no_row_plan) keeps one grid-step launch per closed-loop step with the
+ * plant on the host.  Both give the same rows bit for bit.  rg_get_option
+ * "last_loop_device" tells which ran last. */
 #define RG_LOOP_OVERFLOW 1
 #define RG_LOOP_LEFT_BOX 2
 #define RG_LOOP_INFEASIBLE 3

@@ -138,6 +138,7 @@ struct Tuning {
     int no_ts = 0;            // grid step: never the time-split form (rg_ts.cu)
     int ts_staged = 0;        // time-split step: staged scenario block instead of the fused RNG
     int no_ts_probe = 0;      // Alg. 2: the kappa = 1 probe inside k_bisect, not time-split
+    int no_device_loop = 0;   // rg_closed_loop: one launch per step instead of k_loop_ts
     int64_t batch_chunk = 0;  // batched step: at most this many staged episodes per chunk
 };
 
@@ -171,6 +172,8 @@ struct rg_ctx {
     HostBuf h_out;                  // zero-copy grid result block (pinned, UVA-mapped)
     DevBuf j_state;                 // joint bisection state (rg::JointState)
     DevBuf probe;                   // the bisection's kappa = 1 probe bits (ok, early)
+    DevBuf loop_buf;                // the device closed loop's inputs, outputs and state
+    int last_loop_device = 0;       // the last rg_closed_loop ran as k_loop_ts
     rg::JointArgs j_args{};         // the joint search in progress (rg_joint_begin)
     int j_src = -1;                 // its scenario source; -1 = none begun
     unsigned long long seq_ctr = 0; // grid-step publication tokens
@@ -334,6 +337,7 @@ Tuning env_tuning() {
     if (getenv("RG_NO_TS")) t.no_ts = 1;
     if (getenv("RG_TS_STAGED")) t.ts_staged = 1;
     if (getenv("RG_NO_TS_PROBE")) t.no_ts_probe = 1;
+    if (getenv("RG_NO_DEVICE_LOOP")) t.no_device_loop = 1;
     if (const char* e = getenv("RG_BATCH_CHUNK")) t.batch_chunk = atoll(e);
     if (!(t.force_tpb == 32 || t.force_tpb == 64 || t.force_tpb == 128)) t.force_tpb = 0;
     return t;
@@ -464,7 +468,7 @@ int32_t rg_destroy(rg_ctx* ctx) {
                       &ctx->vrows, &ctx->tmp_a, &ctx->tmp_b, &ctx->kap_k, &ctx->fnd_k,
                       &ctx->cel_k, &ctx->erl_k, &ctx->path_k, &ctx->path_o, &ctx->e_in,
                       &ctx->e_viol, &ctx->e_early, &ctx->e_ticket, &ctx->e_out,
-                      &ctx->e_violout, &ctx->probe};
+                      &ctx->e_violout, &ctx->probe, &ctx->loop_buf};
     for (DevBuf* b : bufs) b->release();
     ctx->h_stage.release();
     ctx->h_out.release();
@@ -498,6 +502,8 @@ int32_t rg_set_option(rg_ctx* ctx, const char* name, int64_t value) {
         t.ts_staged = value != 0;
     } else if (!strcmp(name, "no_ts_probe")) {
         t.no_ts_probe = value != 0;
+    } else if (!strcmp(name, "no_device_loop")) {
+        t.no_device_loop = value != 0;
     } else if (!strcmp(name, "xchg_timeout_ms")) {
         if (value < 1) return fail(RG_E_ARGS, "xchg_timeout_ms must be >= 1");
         t.xchg_timeout_ms = value;
@@ -522,10 +528,12 @@ int32_t rg_get_option(rg_ctx* ctx, const char* name, int64_t* value) {
     else if (!strcmp(name, "no_ts")) *value = t.no_ts;
     else if (!strcmp(name, "ts_staged")) *value = t.ts_staged;
     else if (!strcmp(name, "no_ts_probe")) *value = t.no_ts_probe;
+    else if (!strcmp(name, "no_device_loop")) *value = t.no_device_loop;
     else if (!strcmp(name, "xchg_timeout_ms")) *value = t.xchg_timeout_ms;
     else if (!strcmp(name, "batch_chunk")) *value = t.batch_chunk;
     else if (!strcmp(name, "last_grid_kernel")) *value = ctx->last_grid_kernel;
     else if (!strcmp(name, "grid_step_kernels")) *value = ctx->grid_step_kernels;
+    else if (!strcmp(name, "last_loop_device")) *value = ctx->last_loop_device;
     else return fail(RG_E_ARGS, "unknown option '%s'", name);
     return RG_OK;
 }
@@ -1875,6 +1883,123 @@ static void surrogate_plant_step(double h, const double* x, double v, double* ou
     out[2] = x2 + c * (((k12 + 2.0 * k22) + 2.0 * k32) + k42);
 }
 
+// rg_closed_loop on the device (rg_ts.cu: k_loop_ts): the whole trace in one cooperative
+// launch.  Inputs and outputs travel once; the plan of step 0 comes from the host (the
+// same episode_rows), every later one from the kernel.  Returns 1 (with nothing done) when
+// the device cannot co-schedule one block per SM, so the caller runs the per-step loop.
+static int32_t closed_loop_device(rg_ctx* ctx, const rg_problem* prob, int32_t m_grid,
+                                  int32_t prefix_mode, int32_t infeasible_error, const double* x,
+                                  double v0, int32_t steps, const double* r,
+                                  const double* d_true, uint64_t scen_seed, int64_t n_sim,
+                                  const double* lo, const double* span, double* v_out,
+                                  double* kappa_out, double* y_out, uint8_t* feasible_out,
+                                  int64_t* sims_out, int64_t* early_out, int32_t* wall_us_out,
+                                  double* x_out, rg_loop_result* res) {
+    int32_t rc;
+    rg::LoopArgs L{};
+    rg::GridArgs& g = L.g;
+    if ((rc = make_problem(prob, &g.p))) return rc;
+    if ((rc = grow_grid(ctx, m_grid))) return rc;
+    g.m_grid = m_grid;
+    g.prefix_mode = prefix_mode ? 1 : 0;
+    g.n_sim = n_sim;
+    g.k0 = 0;
+    g.listed = 1;
+    for (int i = 0; i < 3; ++i) {
+        g.stream.lo[i] = lo[i];
+        g.stream.span[i] = span[i];
+    }
+    g.viol = ctx->g_viol.as<unsigned>();
+    g.early = ctx->g_early.as<unsigned long long>();
+    g.ovf = ctx->g_ovf.as<unsigned long long>();
+    g.abandoned = ctx->g_aband.as<unsigned long long>();
+    g.row_src = ctx->g_src.as<int>();
+    g.ticket = ctx->g_ticket.as<unsigned>();
+    g.pwords = (n_sim + 31) / 32;
+    // one buffer: r, d_true | v, kappa, y, sims, early, ns | feasible | LoopCtl, barrier
+    const size_t n = (size_t)steps;
+    const size_t o_r = 0, o_d = o_r + 8 * n, o_v = o_d + 24 * n, o_k = o_v + 8 * n,
+                 o_y = o_k + 8 * n, o_s = o_y + 8 * n, o_e = o_s + 8 * n, o_ns = o_e + 8 * n,
+                 o_f = o_ns + 8 * n, o_c = (o_f + n + 255) / 256 * 256,
+                 o_b = o_c + (sizeof(rg::LoopCtl) + 255) / 256 * 256, total = o_b + 256;
+    RG_CUDA(ctx->loop_buf.ensure(total));
+    char* d = ctx->loop_buf.as<char>();
+    rg::LoopCtl c0{};
+    for (int i = 0; i < 3; ++i) c0.x[i] = x[i];
+    c0.v_prev = v0;
+    c0.r = r[0];
+    c0.hs = rg::splitmix64(scen_seed);
+    {
+        int src[rg::kListMax];
+        double vv[rg::kListMax];
+        episode_rows(g.p, v0, r[0], m_grid, src, vv);
+        c0.list_n = 0;
+        for (int32_t q = 0; q < m_grid; ++q) {
+            c0.src_tab[q] = src[q];
+            if (src[q] == -1) c0.row_list[c0.list_n++] = q;
+        }
+    }
+    c0.abort_step = -1;
+    cudaStream_t st = ctx->stream;
+    RG_CUDA(cudaMemcpyAsync(d + o_r, r, 8 * n, cudaMemcpyHostToDevice, st));
+    RG_CUDA(cudaMemcpyAsync(d + o_d, d_true, 24 * n, cudaMemcpyHostToDevice, st));
+    RG_CUDA(cudaMemcpyAsync(d + o_c, &c0, sizeof c0, cudaMemcpyHostToDevice, st));
+    RG_CUDA(cudaMemsetAsync(d + o_b, 0, 256, st));
+    L.ctl = reinterpret_cast<rg::LoopCtl*>(d + o_c);
+    L.bar = reinterpret_cast<unsigned*>(d + o_b);
+    L.r = reinterpret_cast<const double*>(d + o_r);
+    L.d_true = reinterpret_cast<const double*>(d + o_d);
+    L.scen_seed = scen_seed;
+    L.steps = steps;
+    L.infeasible_error = infeasible_error ? 1 : 0;
+    L.v_out = reinterpret_cast<double*>(d + o_v);
+    L.kappa_out = reinterpret_cast<double*>(d + o_k);
+    L.y_out = reinterpret_cast<double*>(d + o_y);
+    L.sims_out = reinterpret_cast<long long*>(d + o_s);
+    L.early_out = reinterpret_cast<long long*>(d + o_e);
+    L.ns_out = reinterpret_cast<long long*>(d + o_ns);
+    L.feas_out = reinterpret_cast<unsigned char*>(d + o_f);
+    const cudaError_t e = rg::launch_loop_ts(L, ctx->variant == rg::kTanhFma, ctx->sm_count, st);
+    if (e == cudaErrorCooperativeLaunchTooLarge) {
+        cudaGetLastError();
+        return 1;
+    }
+    RG_CUDA(e);
+    ctx->grid_step_kernels += 1;
+    rg::LoopCtl c{};
+    RG_CUDA(cudaMemcpyAsync(&c, d + o_c, sizeof c, cudaMemcpyDeviceToHost, st));
+    RG_CUDA(cudaStreamSynchronize(st));
+    const size_t done = (size_t)c.steps_done;
+    auto fetch = [&](void* dst, size_t off, size_t bytes) -> cudaError_t {
+        return dst && bytes ? cudaMemcpy(dst, d + off, bytes, cudaMemcpyDeviceToHost)
+                            : cudaSuccess;
+    };
+    RG_CUDA(fetch(v_out, o_v, 8 * done));
+    RG_CUDA(fetch(kappa_out, o_k, 8 * done));
+    RG_CUDA(fetch(y_out, o_y, 8 * done));
+    RG_CUDA(fetch(feasible_out, o_f, done));
+    static_assert(sizeof(int64_t) == sizeof(long long), "int64 outputs");
+    RG_CUDA(fetch(sims_out, o_s, 8 * done));
+    RG_CUDA(fetch(early_out, o_e, 8 * done));
+    if (wall_us_out && done) {  // the device time of each governor step
+        std::vector<long long> ns(done);
+        RG_CUDA(fetch(ns.data(), o_ns, 8 * done));
+        for (size_t t = 0; t < done; ++t) wall_us_out[t] = (int32_t)(ns[t] / 1000);
+    }
+    res->steps_done = c.steps_done;
+    res->abort_kind = c.abort_kind;
+    res->abort_step = c.abort_kind ? c.abort_step : -1;
+    res->abort_index = c.abort_index;
+    res->abort_value = c.abort_value;
+    // the final state, where the per-step loop reports it (the end, or leaving the box)
+    if (x_out && (c.abort_kind == 0 || c.abort_kind == RG_LOOP_LEFT_BOX))
+        memcpy(x_out, c.x_final, sizeof c.x_final);
+    ctx->last_grid_kernel = 1;
+    ctx->last_zero_copy = false;
+    ctx->last_m = -1;  // no grid step result to fetch
+    return RG_OK;
+}
+
 extern "C" {
 
 int32_t rg_np_tanh(const double* x, double* y, int64_t n) {
@@ -1908,6 +2033,23 @@ int32_t rg_closed_loop(rg_ctx* ctx, const rg_problem* prob, int32_t m_grid, int3
         return fail(RG_E_ARGS, "state entries must be finite");
     *res = rg_loop_result{};
     res->abort_step = -1;
+    // the whole trace on the device when it runs on the time-split form with host-planned rows
+    // (the options that disable those keep the per-step loop) and every reference is finite
+    ctx->last_loop_device = 0;
+    bool dev_ok = !ctx->tune.no_device_loop && !ctx->tune.no_ts && !ctx->tune.no_row_plan &&
+                  m_grid <= rg::kListMax && n_sim <= ((int64_t)1 << 40) && isfinite(v0);
+    for (int32_t t = 0; dev_ok && t < steps; ++t) dev_ok = isfinite(r[t]);
+    if (dev_ok) {
+        rc = closed_loop_device(ctx, prob, m_grid, prefix_mode, infeasible_error, x, v0, steps, r,
+                                d_true, scen_seed, n_sim, lo, span, v_out, kappa_out, y_out,
+                                feasible_out, sims_out, early_out, wall_us_out, x_out, res);
+        if (rc <= 0) {
+            if (rc == 0) ctx->last_loop_device = 1;
+            return rc;
+        }
+        *res = rg_loop_result{};
+        res->abort_step = -1;
+    }
     double v_prev = v0;
     const double h = prob->step_size;
     const double den = (double)(m_grid - 1);

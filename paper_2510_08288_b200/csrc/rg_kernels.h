@@ -130,6 +130,39 @@ struct GridArgs {
     int src_tab[kListMax];
 };
 
+// The closed loop on the device (k_loop_ts, rg_closed_loop): one persistent cooperative
+// kernel runs every governor step of the trace on the time-split form, and between steps
+// block 0 extracts the row, applies kappa, steps the true plant (numpy's tanh restated,
+// rg_nptanh.h) and plans the next step's rows.  LoopCtl is the state it carries between
+// steps, in device memory.
+struct LoopCtl {
+    double x[3];                  // the plant state before the next step
+    double v_prev, r;             // the next step's previous setpoint and reference
+    unsigned long long hs;        // its scenario stream key splitmix64(seed + t)
+    int32_t list_n, stop;         // simulated rows; 1 once the loop is over
+    int32_t row_list[kListMax];
+    int32_t src_tab[kListMax];
+    int32_t steps_done, abort_kind, abort_step, abort_index;  // abort_kind: RG_LOOP_*
+    double abort_value;
+    double x_final[3];
+};
+struct LoopArgs {
+    GridArgs g;             // the constant part of every step (listed, fused RNG, no P)
+    LoopCtl* ctl;
+    unsigned* bar;          // grid barrier (count, generation), zeroed
+    const double* r;        // [steps] references
+    const double* d_true;   // [steps][3] true-plant disturbances
+    uint64_t scen_seed;     // step t's scenarios: seed scen_seed + t
+    int32_t steps, infeasible_error;
+    double* v_out;          // [steps] outputs, as rg_closed_loop's
+    double* kappa_out;
+    double* y_out;
+    unsigned char* feas_out;
+    long long* sims_out;
+    long long* early_out;
+    long long* ns_out;      // device time of each governor step (globaltimer)
+};
+
 // Batch of independent governor instances (episodes).  The host evaluates every
 // episode's candidate rows (setpoint, steady-state gate, dedup -- the reference's
 // governor.py:286-317, same arithmetic as the device) and hands the kernel a compacted
@@ -311,6 +344,8 @@ cudaError_t launch_grid(const GridArgs& a, bool fma, bool rng, bool poll, cudaSt
 // scenarios, 0 no disturbance (the nominal prediction); ts_blocks = its grid size
 int ts_blocks(int64_t units, int sms);
 cudaError_t launch_grid_ts(const GridArgs& a, bool fma, int src, int sms, cudaStream_t s);
+// the device closed loop: one cooperative block per SM (kTsThreads threads)
+cudaError_t launch_loop_ts(const LoopArgs& L, bool fma, int sms, cudaStream_t s);
 // Pairs [a.p0, a.p0 + n_pairs) of the compacted list, a.bpr blocks of a.tpb threads each.
 cudaError_t launch_grid_batch(const BatchArgs& a, int64_t n_pairs, bool fma, bool poll,
                               cudaStream_t s);

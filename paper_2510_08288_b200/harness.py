@@ -7,10 +7,12 @@ governor picks v_t, and the true plant advances on the host with numpy's tanh
 plus its own disturbance stream ``derive_seed(seed, "plant")`` -- exactly the
 reference's arithmetic, so the v_t sequence is bit-identical.
 
-The governed loop runs in native code by default (``rg_closed_loop``: the grid step,
+The governed loop runs in the library by default (``rg_closed_loop``: the grid step,
 kappa and v_t, and the true plant's RK4 step with the library's restatement of numpy's
-tanh, per step without a Python round trip); ``native=False`` keeps the per-step Python
-loop below, which the tests hold it to bit for bit.
+tanh, without a Python round trip; the whole trace as one device kernel, k_loop_ts, or
+with the "no_device_loop" option one grid-step launch per step and the plant in C on the
+host); ``native=False`` keeps the per-step Python loop below, which the tests hold both to
+bit for bit.
 
 ``run_closed_loop_bisection`` substitutes the nominal ``bisection_rg`` at
 harness.py:200 (configuration C1 of BASELINE.md; the reference ships no such

@@ -23,7 +23,8 @@ def ctx():
 
 
 _DEFAULTS = {"force_tpb": 0, "no_placement": 0, "no_pdl": 0, "no_step2": 0, "fused_gen": 0,
-             "batch_chunk": 0, "no_row_plan": 0, "no_ts": 0, "ts_staged": 0, "no_ts_probe": 0}
+             "batch_chunk": 0, "no_row_plan": 0, "no_ts": 0, "ts_staged": 0, "no_ts_probe": 0,
+             "no_device_loop": 0}
 
 
 @pytest.fixture
@@ -552,7 +553,7 @@ def test_options_round_trip(ctx, tuned):
 
     for name, value in (("force_tpb", 64), ("no_placement", 1), ("no_pdl", 1), ("no_step2", 1),
                         ("fused_gen", 1), ("no_row_plan", 1), ("no_ts", 1), ("ts_staged", 1),
-                        ("no_ts_probe", 1),
+                        ("no_ts_probe", 1), ("no_device_loop", 1),
                         ("batch_chunk", 7), ("xchg_timeout_ms", 1234)):
         before = ctx.get_option(name)
         ctx.set_option(name, value)

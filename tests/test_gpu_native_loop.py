@@ -85,3 +85,49 @@ def test_native_loop_infeasible_error_policy():
         run_closed_loop(PLANT, BOX, model, cfg, [0.4] * 3, 3, 1, x0=x0)
     with pytest.raises(InfeasibleError):
         run_closed_loop(PLANT, BOX, model, cfg, [0.4] * 3, 3, 1, x0=x0, native=False)
+
+
+@pytest.mark.parametrize("case", ["desk_10k", "transient_prefix", "held_start", "small_grid"])
+def test_device_loop_equals_per_step_loop(case):
+    """rg_closed_loop runs the whole trace as one cooperative kernel (k_loop_ts: block 0
+    extracts the row, steps the true plant with numpy's tanh on the device and plans the
+    next rows between grid barriers); with "no_device_loop" it launches one grid step per
+    closed-loop step from the host.  Same rows, diagnostics and aborts.  The desk case at 10k
+    crosses the profile's jumps, where many rows are live and a step takes several passes of
+    three units per block."""
+    from paper_2510_08288_b200 import _capi
+
+    ctx = _capi.context(0)
+    x0, v0, prefix = None, 0.0, False
+    if case == "desk_10k":
+        model = rg.DisturbanceModel.scaled(0.001, 3)
+        cfg = rg.GovernorConfig(j_star=256, m_grid=32, n_sim=10_000)
+        prof = ReferenceProfile(((0, 0.4), (40, 2.5), (120, -2.5), (200, 0.2)))
+        steps, seed = 260, 2024
+    elif case == "transient_prefix":
+        model = rg.DisturbanceModel.scaled(0.02, 3)
+        cfg = rg.GovernorConfig(j_star=64, m_grid=16, n_sim=3000, prefix_mode=True)
+        prof = np.concatenate([np.full(50, 2.0), np.full(50, -2.4), np.full(60, 0.7)])
+        steps, seed = 160, 31
+    elif case == "held_start":
+        model = rg.DisturbanceModel.scaled(0.02, 3)
+        cfg = rg.GovernorConfig(j_star=64, m_grid=64, n_sim=700)
+        prof = np.concatenate([np.full(60, 2.0), np.full(60, -0.4)])
+        steps, seed = 120, 5
+        x0, v0 = np.array([0.95, -0.5, 0.1]), -0.5
+    else:
+        model = rg.DisturbanceModel.scaled(0.005, 3)
+        cfg = rg.GovernorConfig(j_star=1, m_grid=2, n_sim=1)
+        prof = np.concatenate([np.full(30, 1.5), np.full(30, -1.5)])
+        steps, seed = 60, 9
+    kw = {} if x0 is None else {"x0": x0, "v0": v0}
+    dev = _strip_wall(run_closed_loop(PLANT, BOX, model, cfg, prof, steps, seed, **kw))
+    assert ctx.get_option("last_loop_device") == 1
+    ctx.set_option("no_device_loop", 1)
+    try:
+        host = _strip_wall(run_closed_loop(PLANT, BOX, model, cfg, prof, steps, seed, **kw))
+        assert ctx.get_option("last_loop_device") == 0
+    finally:
+        ctx.set_option("no_device_loop", 0)
+    _same(dev, host)
+    assert len(dev.rows) == steps
