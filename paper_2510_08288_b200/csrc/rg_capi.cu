@@ -1909,21 +1909,23 @@ static int32_t closed_loop_device(rg_ctx* ctx, const rg_problem* prob, int32_t m
         g.stream.lo[i] = lo[i];
         g.stream.span[i] = span[i];
     }
-    g.viol = ctx->g_viol.as<unsigned>();
-    g.early = ctx->g_early.as<unsigned long long>();
-    g.ovf = ctx->g_ovf.as<unsigned long long>();
     g.abandoned = ctx->g_aband.as<unsigned long long>();
     g.row_src = ctx->g_src.as<int>();
     g.ticket = ctx->g_ticket.as<unsigned>();
     g.pwords = (n_sim + 31) / 32;
-    // one buffer: r, d_true | v, kappa, y, sims, early, ns | feasible | LoopCtl, barrier
+    // one buffer: r, d_true | v, kappa, y, sims, early, ns | feasible | LoopCtl, barrier |
+    // three accumulator sets (violations, early, overflows per row; zeroed)
     const size_t n = (size_t)steps;
     const size_t o_r = 0, o_d = o_r + 8 * n, o_v = o_d + 24 * n, o_k = o_v + 8 * n,
                  o_y = o_k + 8 * n, o_s = o_y + 8 * n, o_e = o_s + 8 * n, o_ns = o_e + 8 * n,
                  o_f = o_ns + 8 * n, o_c = (o_f + n + 255) / 256 * 256,
-                 o_b = o_c + (sizeof(rg::LoopCtl) + 255) / 256 * 256, total = o_b + 256;
+                 o_b = o_c + (sizeof(rg::LoopCtl) + 255) / 256 * 256, o_acc = o_b + 256,
+                 acc_bytes = 3 * (size_t)m_grid * (4 + 8 + 8), total = o_acc + acc_bytes;
     RG_CUDA(ctx->loop_buf.ensure(total));
     char* d = ctx->loop_buf.as<char>();
+    g.early = reinterpret_cast<unsigned long long*>(d + o_acc);
+    g.ovf = g.early + 3 * m_grid;
+    g.viol = reinterpret_cast<unsigned*>(g.ovf + 3 * m_grid);
     rg::LoopCtl c0{};
     for (int i = 0; i < 3; ++i) c0.x[i] = x[i];
     c0.v_prev = v0;
@@ -1944,7 +1946,7 @@ static int32_t closed_loop_device(rg_ctx* ctx, const rg_problem* prob, int32_t m
     RG_CUDA(cudaMemcpyAsync(d + o_r, r, 8 * n, cudaMemcpyHostToDevice, st));
     RG_CUDA(cudaMemcpyAsync(d + o_d, d_true, 24 * n, cudaMemcpyHostToDevice, st));
     RG_CUDA(cudaMemcpyAsync(d + o_c, &c0, sizeof c0, cudaMemcpyHostToDevice, st));
-    RG_CUDA(cudaMemsetAsync(d + o_b, 0, 256, st));
+    RG_CUDA(cudaMemsetAsync(d + o_b, 0, 256 + acc_bytes, st));
     L.ctl = reinterpret_cast<rg::LoopCtl*>(d + o_c);
     L.bar = reinterpret_cast<unsigned*>(d + o_b);
     L.r = reinterpret_cast<const double*>(d + o_r);

@@ -132,9 +132,9 @@ struct GridArgs {
 
 // The closed loop on the device (k_loop_ts, rg_closed_loop): one persistent cooperative
 // kernel runs every governor step of the trace on the time-split form, and between steps
-// block 0 extracts the row, applies kappa, steps the true plant (numpy's tanh restated,
-// rg_nptanh.h) and plans the next step's rows.  LoopCtl is the state it carries between
-// steps, in device memory.
+// every block extracts the row, applies kappa, steps the true plant (numpy's tanh
+// restated, rg_nptanh.h) and plans the next step's rows (the same bits everywhere; block 0
+// writes the outputs).  LoopCtl carries step 0's inputs and plan in and the end state out.
 struct LoopCtl {
     double x[3];                  // the plant state before the next step
     double v_prev, r;             // the next step's previous setpoint and reference
@@ -147,7 +147,8 @@ struct LoopCtl {
     double x_final[3];
 };
 struct LoopArgs {
-    GridArgs g;             // the constant part of every step (listed, fused RNG, no P)
+    GridArgs g;             // the constant part of every step (listed, fused RNG, no P);
+                            // viol / early / ovf: three zeroed sets of m_grid counters
     LoopCtl* ctl;
     unsigned* bar;          // grid barrier (count, generation), zeroed
     const double* r;        // [steps] references
