@@ -162,6 +162,7 @@ struct LoopArgs {
     long long* sims_out;
     long long* early_out;
     long long* ns_out;      // device time of each governor step (globaltimer)
+    unsigned spin_cap_ns;   // the barrier's longest poll interval
 };
 
 // Batch of independent governor instances (episodes).  The host evaluates every
