@@ -364,6 +364,21 @@ RG_API int32_t rg_closed_loop(rg_ctx *ctx, const rg_problem *prob, int32_t m_gri
                               double *y_out, uint8_t *feasible_out, int64_t *sims_out,
                               int64_t *early_out, int32_t *wall_us_out, double *x_out,
                               rg_loop_result *res);
+/* The nominal bisection governor's closed loop (BASELINE C1: harness.py:138-224 with
+ * bisection_rg, governor.py:433-466, at harness.py:200) on the device as one kernel: per
+ * step t the kappa = 1 probe and n_kappa midpoint candidates of the one nominal cell (no
+ * disturbance; governor.py:380-430), v = update_setpoint, then the true plant with numpy's
+ * tanh and x += d_true[t].  Per-step outputs (host arrays of `steps`, each may be NULL):
+ * kappa, v_t, y_t = x1 before the step, found, cells (rollouts incl. gated-out candidates),
+ * early terminations, the step's device time.  Stops at the plant's integration overflow
+ * (RG_LOOP_OVERFLOW, as plant.step raises); x_out: the final state of a completed run. */
+RG_API int32_t rg_closed_loop_bisection(rg_ctx *ctx, const rg_problem *prob, int32_t n_kappa,
+                                        const double *x0, double v0, int32_t steps,
+                                        const double *r, const double *d_true,
+                                        double *kappa_out, double *v_out, double *y_out,
+                                        uint8_t *feasible_out, int64_t *cells_out,
+                                        int64_t *early_out, int32_t *wall_us_out, double *x_out,
+                                        rg_loop_result *res);
 /* numpy's float64 tanh (numpy 2.3.5's SIMD kernel, rg_nptanh.h) on the host: y[i] =
  * np.tanh(x[i]) bit for bit for finite x.  And the surrogate true plant's step with it
  * (dynamics.py: SurrogateFuelCellPlant.step without the overflow check).  No device. */

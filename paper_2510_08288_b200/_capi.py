@@ -133,6 +133,9 @@ SIGNATURES = {
     "rg_closed_loop": (_i32, [_vp, ctypes.POINTER(Problem), _i32, _i32, _i32, _vp, _d, _i32,
                               _vp, _vp, _u64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                               _vp, _vp, ctypes.POINTER(LoopResult)]),
+    "rg_closed_loop_bisection": (_i32, [_vp, ctypes.POINTER(Problem), _i32, _vp, _d, _i32, _vp,
+                                        _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                        ctypes.POINTER(LoopResult)]),
     "rg_np_tanh": (_i32, [_vp, _vp, _i64]),
     "rg_plant_step": (_i32, [_d, _vp, _d, _vp]),
     "rg_synchronize": (_i32, [_vp]),
@@ -587,6 +590,28 @@ class Context:
             _p(lo3), _p(span3), _p(out["v"]), _p(out["kappa"]), _p(out["y"]),
             _p(out["feasible"]), _p(out["sims_run"]), _p(out["early_terms"]), _p(out["wall_us"]),
             _p(xf), ctypes.byref(res)))
+        n = res.steps_done
+        return res, {k: a[:n] for k, a in out.items()}, xf
+
+    @_locked
+    def closed_loop_bisection(self, prob: Problem, n_kappa: int, x0, v0: float, r, d_true):
+        """rg_closed_loop_bisection: the nominal bisection governor's loop (C1) on the device.
+        Returns (LoopResult, dict of per-step arrays over the steps done, final state)."""
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        steps = r.size
+        d_true = np.ascontiguousarray(d_true, dtype=np.float64).reshape(steps, 3)
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        out = {"kappa": np.empty(steps), "v": np.empty(steps), "y": np.empty(steps),
+               "found": np.empty(steps, dtype=np.uint8),
+               "cells": np.empty(steps, dtype=np.int64),
+               "early": np.empty(steps, dtype=np.int64),
+               "wall_us": np.empty(steps, dtype=np.int32)}
+        xf = np.empty(3)
+        res = LoopResult()
+        check(self.lib.rg_closed_loop_bisection(
+            self.handle, prob, int(n_kappa), _p(x0), float(v0), steps, _p(r), _p(d_true),
+            _p(out["kappa"]), _p(out["v"]), _p(out["y"]), _p(out["found"]), _p(out["cells"]),
+            _p(out["early"]), _p(out["wall_us"]), _p(xf), ctypes.byref(res)))
         n = res.steps_done
         return res, {k: a[:n] for k, a in out.items()}, xf
 

@@ -2019,6 +2019,92 @@ int32_t rg_plant_step(double step_size, const double* x, double v, double* out) 
     return RG_OK;
 }
 
+int32_t rg_closed_loop_bisection(rg_ctx* ctx, const rg_problem* prob, int32_t n_kappa,
+                                 const double* x0, double v0, int32_t steps, const double* r,
+                                 const double* d_true, double* kappa_out, double* v_out,
+                                 double* y_out, uint8_t* feasible_out, int64_t* cells_out,
+                                 int64_t* early_out, int32_t* wall_us_out, double* x_out,
+                                 rg_loop_result* res) {
+    int32_t rc = enter(ctx);
+    if (rc) return rc;
+    if (!prob || !x0 || !r || !d_true || !res) return fail(RG_E_ARGS, "null argument");
+    if (steps < 1) return fail(RG_E_ARGS, "steps must be >= 1, got %d", steps);
+    if (n_kappa < 1) return fail(RG_E_ARGS, "n_kappa must be >= 1, got %d", n_kappa);
+    if (!(isfinite(x0[0]) && isfinite(x0[1]) && isfinite(x0[2])) || !isfinite(v0))
+        return fail(RG_E_ARGS, "state entries must be finite");
+    for (int32_t t = 0; t < steps; ++t)
+        if (!isfinite(r[t])) return fail(RG_E_ARGS, "v_prev and r must be finite");
+    rg::LoopBisArgs B{};
+    rg::GridArgs& g = B.g;
+    if ((rc = make_problem(prob, &g.p))) return rc;
+    g.m_grid = 2;  // unused: every unit takes its kappa from the bisection
+    g.n_sim = 1;
+    g.k0 = 0;
+    g.pwords = 1;
+    *res = rg_loop_result{};
+    res->abort_step = -1;
+    // one buffer: r, d_true | kappa, v, y, cells, early, ns | feasible | LoopCtl | counters
+    const size_t n = (size_t)steps;
+    const size_t o_r = 0, o_d = o_r + 8 * n, o_k = o_d + 24 * n, o_v = o_k + 8 * n,
+                 o_y = o_v + 8 * n, o_c = o_y + 8 * n, o_e = o_c + 8 * n, o_ns = o_e + 8 * n,
+                 o_f = o_ns + 8 * n, o_ctl = (o_f + n + 255) / 256 * 256,
+                 o_acc = o_ctl + (sizeof(rg::LoopCtl) + 255) / 256 * 256, total = o_acc + 256;
+    RG_CUDA(ctx->loop_buf.ensure(total));
+    char* d = ctx->loop_buf.as<char>();
+    g.early = reinterpret_cast<unsigned long long*>(d + o_acc);
+    g.ovf = g.early + 1;
+    g.viol = reinterpret_cast<unsigned*>(g.ovf + 1);
+    rg::LoopCtl c0{};
+    for (int i = 0; i < 3; ++i) c0.x[i] = x0[i];
+    c0.v_prev = v0;
+    c0.abort_step = -1;
+    cudaStream_t st = ctx->stream;
+    RG_CUDA(cudaMemcpyAsync(d + o_r, r, 8 * n, cudaMemcpyHostToDevice, st));
+    RG_CUDA(cudaMemcpyAsync(d + o_d, d_true, 24 * n, cudaMemcpyHostToDevice, st));
+    RG_CUDA(cudaMemcpyAsync(d + o_ctl, &c0, sizeof c0, cudaMemcpyHostToDevice, st));
+    RG_CUDA(cudaMemsetAsync(d + o_acc, 0, 256, st));
+    B.ctl = reinterpret_cast<rg::LoopCtl*>(d + o_ctl);
+    B.r = reinterpret_cast<const double*>(d + o_r);
+    B.d_true = reinterpret_cast<const double*>(d + o_d);
+    B.steps = steps;
+    B.n_kappa = n_kappa;
+    B.kappa_out = reinterpret_cast<double*>(d + o_k);
+    B.v_out = reinterpret_cast<double*>(d + o_v);
+    B.y_out = reinterpret_cast<double*>(d + o_y);
+    B.cells_out = reinterpret_cast<long long*>(d + o_c);
+    B.early_out = reinterpret_cast<long long*>(d + o_e);
+    B.ns_out = reinterpret_cast<long long*>(d + o_ns);
+    B.feas_out = reinterpret_cast<unsigned char*>(d + o_f);
+    RG_CUDA(rg::launch_loop_bisect(B, ctx->variant == rg::kTanhFma, st));
+    rg::LoopCtl c{};
+    RG_CUDA(cudaMemcpyAsync(&c, d + o_ctl, sizeof c, cudaMemcpyDeviceToHost, st));
+    RG_CUDA(cudaStreamSynchronize(st));
+    const size_t done = (size_t)c.steps_done;
+    auto fetch = [&](void* dst, size_t off, size_t bytes) -> cudaError_t {
+        return dst && bytes ? cudaMemcpy(dst, d + off, bytes, cudaMemcpyDeviceToHost)
+                            : cudaSuccess;
+    };
+    RG_CUDA(fetch(kappa_out, o_k, 8 * done));
+    RG_CUDA(fetch(v_out, o_v, 8 * done));
+    RG_CUDA(fetch(y_out, o_y, 8 * done));
+    RG_CUDA(fetch(feasible_out, o_f, done));
+    RG_CUDA(fetch(cells_out, o_c, 8 * done));
+    RG_CUDA(fetch(early_out, o_e, 8 * done));
+    if (wall_us_out && done) {
+        std::vector<long long> ns(done);
+        RG_CUDA(fetch(ns.data(), o_ns, 8 * done));
+        for (size_t t = 0; t < done; ++t) wall_us_out[t] = (int32_t)(ns[t] / 1000);
+    }
+    res->steps_done = c.steps_done;
+    res->abort_kind = c.abort_kind;
+    res->abort_step = c.abort_kind ? c.abort_step : -1;
+    res->abort_index = c.abort_index;
+    res->abort_value = c.abort_value;
+    if (x_out && c.abort_kind == 0) memcpy(x_out, c.x_final, sizeof c.x_final);
+    ctx->last_m = -1;
+    return RG_OK;
+}
+
 int32_t rg_closed_loop(rg_ctx* ctx, const rg_problem* prob, int32_t m_grid, int32_t prefix_mode,
                        int32_t infeasible_error, const double* x0, double v0, int32_t steps,
                        const double* r, const double* d_true, uint64_t scen_seed, int64_t n_sim,

@@ -165,6 +165,26 @@ struct LoopArgs {
     unsigned spin_cap_ns;   // the barrier's longest poll interval
 };
 
+// The nominal bisection governor's closed loop on the device (k_loop_bisect, BASELINE C1:
+// bisection_rg at harness.py:200): one block; per step the kappa = 1 probe and the
+// n_kappa midpoint candidates (governor.py:380-430) each roll out the one nominal cell on
+// the time-split passes, then kappa, v_t and the true plant (the driver checks only the
+// plant's integration overflow).  g: n_sim 1, no disturbances, one counter of each kind.
+struct LoopBisArgs {
+    GridArgs g;
+    LoopCtl* ctl;           // x / v_prev in (step 0); steps_done, abort_*, x_final out
+    const double* r;        // [steps]
+    const double* d_true;   // [steps][3]
+    int32_t steps, n_kappa;
+    double* kappa_out;
+    double* v_out;
+    double* y_out;
+    unsigned char* feas_out;
+    long long* cells_out;
+    long long* early_out;
+    long long* ns_out;
+};
+
 // Batch of independent governor instances (episodes).  The host evaluates every
 // episode's candidate rows (setpoint, steady-state gate, dedup -- the reference's
 // governor.py:286-317, same arithmetic as the device) and hands the kernel a compacted
@@ -348,6 +368,7 @@ int ts_blocks(int64_t units, int sms);
 cudaError_t launch_grid_ts(const GridArgs& a, bool fma, int src, int sms, cudaStream_t s);
 // the device closed loop: one cooperative block per SM (kTsThreads threads)
 cudaError_t launch_loop_ts(const LoopArgs& L, bool fma, int sms, cudaStream_t s);
+cudaError_t launch_loop_bisect(const LoopBisArgs& B, bool fma, cudaStream_t s);
 // Pairs [a.p0, a.p0 + n_pairs) of the compacted list, a.bpr blocks of a.tpb threads each.
 cudaError_t launch_grid_batch(const BatchArgs& a, int64_t n_pairs, bool fma, bool poll,
                               cudaStream_t s);

@@ -112,11 +112,46 @@ def _np_tanh_matches() -> bool:
     return _NP_TANH_PROBE[0]
 
 
-def _native_loop_ok(plant, config) -> bool:
+def _native_loop_ok(plant, config, grid=True) -> bool:
     from .dynamics import SurrogateFuelCellPlant
 
     return (type(plant) is SurrogateFuelCellPlant and getattr(config, "backend", "cuda") == "cuda"
-            and bool(getattr(config, "m_grid", 0)) and _np_tanh_matches())
+            and (not grid or bool(getattr(config, "m_grid", 0))) and _np_tanh_matches())
+
+
+def _run_closed_loop_bisection_native(plant, cset, model, config, profile, steps, seed, x0, v0):
+    """run_closed_loop_bisection through rg_closed_loop_bisection: the same plant stream,
+    the same bisection (governor.py:380-430 with zero disturbance), update_setpoint and
+    true-plant arithmetic, the same KappaResults; the plant's integration overflow raises as
+    plant.step does."""
+    from . import _capi
+    from .governor import KappaResult, _prepared
+
+    if steps < 1:
+        raise ConfigError(f"steps must be >= 1, got {steps}")
+    device = getattr(config, "device", 0)
+    x = plant.validate_state(np.zeros(plant.state_dim) if x0 is None else x0)
+    prob = _prepared(plant.step_size, cset.lower, cset.upper, cset.anchor, config.epsilon,
+                     config.tighten_mode, config.j_star, 0)[0]
+    d_true = _true_disturbance(model, steps, seed, device)
+    r_sched = np.ascontiguousarray(_schedule(profile, steps), dtype=np.float64)
+    if r_sched.size < steps:
+        raise ConfigError(f"profile has {r_sched.size} entries, need {steps}")
+    ctx = _capi.context(device)
+    res, out, _ = ctx.closed_loop_bisection(prob, config.n_kappa, x, float(v0), r_sched[:steps],
+                                            d_true)
+    if res.abort_kind == _capi.RG_LOOP_OVERFLOW:
+        raise IntegrationOverflowError(f"integration overflow in state {res.abort_index} "
+                                       f"(value {np.float64(res.abort_value)!r})",
+                                       state_index=res.abort_index)
+    k_l, v_l, y_l = out["kappa"].tolist(), out["v"].tolist(), out["y"].tolist()
+    f_l, c_l, e_l, w_l = (out["found"].tolist(), out["cells"].tolist(), out["early"].tolist(),
+                          out["wall_us"].tolist())
+    return [(KappaResult(kappa_opt=k_l[t], v_applied=v_l[t], feasible=bool(f_l[t]),
+                         diagnostics={"method": "bisection", "sims_run": c_l[t],
+                                      "early_terms": e_l[t], "kernel_us": w_l[t],
+                                      "wall_us": w_l[t]}), y_l[t])
+            for t in range(res.steps_done)]
 
 
 def _run_closed_loop_native(plant, cset, model, config, profile, steps, seed, x0, v0):
@@ -221,9 +256,21 @@ def run_closed_loop(plant, cset, model, config, profile, steps, seed, governor_o
 
 
 def run_closed_loop_bisection(plant, cset, model, config, profile, steps, seed, x0=None,
-                              v0=0.0):
+                              v0=0.0, native=None):
     """C1: the same loop with the nominal bisection governor; returns
-    [(KappaResult, y_t)] per step."""
+    [(KappaResult, y_t)] per step.
+
+    ``native`` (default: for the surrogate plant when the library's numpy tanh is this
+    process's): the whole loop runs on the device as one kernel (rg_closed_loop_bisection:
+    the bisection's candidates on the time-split passes, the true plant with numpy's tanh
+    restated); ``native=False`` keeps the per-step loop over bisection_rg below, which the
+    tests hold it to bit for bit.  ``wall_us`` is then each step's device time.
+    """
+    if native is None:
+        native = _native_loop_ok(plant, config, grid=False)
+    if native:
+        return _run_closed_loop_bisection_native(plant, cset, model, config, profile, steps,
+                                                 seed, x0, v0)
     device = getattr(config, "device", 0)
     x = plant.validate_state(np.zeros(plant.state_dim) if x0 is None else x0)
     state = GovernorState(v_prev=float(v0))

@@ -14,7 +14,11 @@ prof = ReferenceProfile(((0, 0.4), (400, 2.5), (1000, -2.5), (1600, 0.2)))
 run_closed_loop_bisection(plant, box, model, cfg, prof, 50, 2025)
 t0 = time.perf_counter()
 out = run_closed_loop_bisection(plant, box, model, cfg, prof, 2000, 2024)
-print("device C1: %.4f ms/step" % ((time.perf_counter() - t0) / 2000 * 1e3))
+print("device C1 (one kernel): %.4f ms/step" % ((time.perf_counter() - t0) / 2000 * 1e3))
+run_closed_loop_bisection(plant, box, model, cfg, prof, 50, 2025, native=False)
+t0 = time.perf_counter()
+run_closed_loop_bisection(plant, box, model, cfg, prof, 2000, 2024, native=False)
+print("device C1 (per-step bisection_rg): %.4f ms/step" % ((time.perf_counter() - t0) / 2000 * 1e3))
 try:
     sys.path.insert(0, "oracle/_ref")
     import refgov  # noqa

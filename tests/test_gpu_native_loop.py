@@ -131,3 +131,59 @@ def test_device_loop_equals_per_step_loop(case):
         ctx.set_option("no_device_loop", 0)
     _same(dev, host)
     assert len(dev.rows) == steps
+
+
+def _c1_rows(rows):
+    return [(r.kappa_opt, r.v_applied, r.feasible, y, r.diagnostics["sims_run"],
+             r.diagnostics["early_terms"]) for r, y in rows]
+
+
+@pytest.mark.parametrize("case", ["desk", "transient", "held_start", "deep"])
+def test_device_bisection_loop_equals_per_step_loop(case):
+    """C1's nominal bisection loop as one device kernel (rg_closed_loop_bisection: every
+    candidate's rollout on the time-split passes of one block, the true plant with numpy's
+    tanh on the device) against the per-step loop over bisection_rg: the same kappa, v_t,
+    found, y_t, rollout and early counts every step."""
+    from paper_2510_08288_b200.harness import run_closed_loop_bisection
+
+    model = rg.DisturbanceModel.scaled(0.001, 3)
+    x0, v0 = None, 0.0
+    if case == "desk":
+        cfg = rg.GovernorConfig()
+        prof = ReferenceProfile(((0, 0.4), (40, 2.5), (140, -2.5), (240, 0.2)))
+        steps, seed = 300, 2024
+    elif case == "transient":
+        model = rg.DisturbanceModel.scaled(0.02, 3)
+        cfg = rg.GovernorConfig(j_star=64, n_kappa=5)
+        prof = np.concatenate([np.full(40, 2.0), np.full(40, -2.4), np.full(40, 0.7)])
+        steps, seed = 120, 31
+    elif case == "held_start":
+        cfg = rg.GovernorConfig(j_star=32, n_kappa=3)
+        prof = np.concatenate([np.full(30, 2.0), np.full(30, -0.4)])
+        steps, seed = 60, 5
+        x0, v0 = np.array([0.95, -0.5, 0.1]), -0.5
+    else:
+        cfg = rg.GovernorConfig(j_star=1, n_kappa=20)
+        prof = np.concatenate([np.full(20, 1.5), np.full(20, -1.5)])
+        steps, seed = 40, 9
+    kw = {} if x0 is None else {"x0": x0, "v0": v0}
+    dev = run_closed_loop_bisection(PLANT, BOX, model, cfg, prof, steps, seed, **kw)
+    host = run_closed_loop_bisection(PLANT, BOX, model, cfg, prof, steps, seed, native=False,
+                                     **kw)
+    assert _c1_rows(dev) == _c1_rows(host)
+    assert len(dev) == steps
+
+
+def test_device_bisection_loop_overflow_raises_like_the_plant():
+    from paper_2510_08288_b200.errors import IntegrationOverflowError
+    from paper_2510_08288_b200.harness import run_closed_loop_bisection
+
+    cfg = rg.GovernorConfig(j_star=16, n_kappa=3)
+    x0 = np.array([1.5e6, 0.0, 0.0])
+    msgs = []
+    for native in (None, False):
+        with pytest.raises(IntegrationOverflowError) as e:
+            run_closed_loop_bisection(PLANT, BOX, rg.DisturbanceModel.scaled(0.001, 3), cfg,
+                                      [0.4] * 5, 5, 3, x0=x0, native=native)
+        msgs.append((str(e.value), e.value.state_index))
+    assert msgs[0] == msgs[1]
