@@ -445,9 +445,14 @@ struct Soa4Source {
         const uint32_t a = base + rd;
         read_slot(a, e4);
         read_slot(a + kSlot, e5);
-        const uint32_t freed = rd == 0 ? (kRing4Pairs - 1) * kPair : rd - kPair;
-        rd = after(rd);
-        issue_pair(freed);
+        if constexpr (kRing4Pairs == 2) {  // double buffering: the pairs swap roles
+            rd = kPair - rd;
+            issue_pair(rd);
+        } else {
+            const uint32_t freed = rd == 0 ? (kRing4Pairs - 1) * kPair : rd - kPair;
+            rd = after(rd);
+            issue_pair(freed);
+        }
     }
     __device__ __forceinline__ void finish() { asm volatile("cp.async.wait_group 0;"); }
 };
