@@ -54,8 +54,11 @@ __device__ int row_source_warp(const GridArgs& a, int i, double* v_out) {
 // issue-bound multi-wave steps; the single-wave (latency-bound) step keeps MOD off.
 // S2: the two-steps-per-iteration rollout (rollout2) for the latency-bound
 // single-wave step over a staged block (blocks of at most 256 threads).
+#ifndef RG_GRID_MW_MINB
+#define RG_GRID_MW_MINB RG_GRID_MINB
+#endif
 template <bool FMA, bool RNG, bool POLL, bool MOD = false, bool S2 = false>
-__global__ void __launch_bounds__(256, RG_GRID_MINB) k_grid(GridArgs a) {
+__global__ void __launch_bounds__(256, S2 ? RG_GRID_MINB : RG_GRID_MW_MINB) k_grid(GridArgs a) {
     __shared__ int s_src;
     __shared__ double s_v;
     const int i = a.listed ? a.row_list[blockIdx.y] : (int)blockIdx.y;
