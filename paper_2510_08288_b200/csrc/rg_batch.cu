@@ -38,11 +38,12 @@ __global__ void k_gen_soa_batch(const uint64_t* __restrict__ hs, double3 lo, dou
 // kernel.  C5 per closed-loop step (scripts/ab_pairs_regs.sh): 3 blocks (154 registers)
 // 179.7 ms, 4: 183.5, 5: 178.1, 6: 177.1-177.4, 8 (64 registers): 178.8 -- the FP64 pipe,
 // not latency, bounds it (ncu: 69.6% busy at 3 warps per scheduler).
+// The staged-block form (SOA) keeps 3 blocks: at 80 registers its ring addressing spills.
 #ifndef RG_PAIRS_MINB
 #define RG_PAIRS_MINB 6
 #endif
 template <bool FMA, bool POLL, bool SOA>
-__global__ void __launch_bounds__(128, RG_PAIRS_MINB) k_grid_pairs(BatchArgs a) {
+__global__ void __launch_bounds__(128, SOA ? 3 : RG_PAIRS_MINB) k_grid_pairs(BatchArgs a) {
     __shared__ bool s_last;
     const int64_t pair = a.p0 + blockIdx.x / (unsigned)a.bpr;
     const int64_t kb = blockIdx.x % (unsigned)a.bpr;
