@@ -229,6 +229,41 @@ def test_closed_loop_c3_truncated(golden):
     assert np.array_equal(got, golden["c3_trace40"])
 
 
+@pytest.mark.parametrize("case", ["lit", "prefix"])
+@pytest.mark.parametrize("device_loop", [1, 0])
+def test_closed_loop_transient_golden(case, device_loop):
+    """Closed loops with transients against the real reference (tests/golden/
+    make_loop_transient_golden.py): references jumping every 60 steps under larger
+    disturbances, so up to every row is live (literal mode: 2.6 live rows per step on
+    average at 2000 scenarios, up to 32; prefix mode at M = 16).  The rows (v, y, kappa,
+    feasible) and the diagnostics (sims_run, early_terms) equal the reference's every step,
+    through the device loop (k_loop_ts, several time-split passes per step) and through one
+    grid-step launch per step."""
+    from paper_2510_08288_b200 import _capi
+    from paper_2510_08288_b200.harness import ReferenceProfile, run_closed_loop
+
+    with np.load(GOLDEN.with_name("loop_transient.npz")) as z:
+        g = {k: z[k] for k in z.files}
+    c = lambda k: g[f"{case}_{k}"].item()
+    cfg = rg.GovernorConfig(j_star=c("j_star"), m_grid=c("m_grid"), n_sim=c("n_sim"),
+                            prefix_mode=bool(c("prefix_mode")))
+    prof = ReferenceProfile(tuple((int(t), float(r)) for t, r in g["profile"]))
+    ctx = _capi.context(0)
+    ctx.set_option("no_device_loop", 1 - device_loop)
+    try:
+        rec = run_closed_loop(PLANT, rg.ConstraintSet(-0.9, 0.9, anchor=0.0),
+                              rg.DisturbanceModel.scaled(c("scale"), 3), cfg, prof,
+                              int(g["steps"]), c("seed"))
+        assert ctx.get_option("last_loop_device") == device_loop
+    finally:
+        ctx.set_option("no_device_loop", 0)
+    assert not rec.aborted
+    got = np.array([[row[2], row[3], row[4], float(row[5])] for row in rec.rows])
+    diag = np.array([[int(d.split(",")[4]), int(d.split(",")[5])] for d in rec.diag_rows])
+    assert np.array_equal(got, g[f"{case}_trace"])
+    assert np.array_equal(diag, g[f"{case}_diag"])
+
+
 def test_closed_loop_c3_10k_full_trace():
     """C3 at its named size: 10,000 scenarios per step, the whole 2000-step desk trace
     (rise to r = 0.4, r = 2.5 at t = 400, r = -2.5 at t = 1000, r = 0.2 at t = 1600;
