@@ -358,6 +358,17 @@ __global__ void __launch_bounds__(256, 1) k_joint_spec(JointArgs a) {
         vs->rounds = round;
         vs->exit_ticket = 0u;
         vs->seq = vs->seq + 1;
+        if (a.hout) {
+            volatile JointOut* ho = a.hout;
+            ho->kopt = cur.kopt;
+            ho->found = cur.found;
+            ho->cells = cur.cells;
+            ho->early = cur.early;
+            ho->rounds = round;
+            ho->xfail = vs->xfail;
+            __threadfence_system();
+            ho->seq = a.seq_token;
+        }
     }
 }
 
@@ -497,7 +508,8 @@ __global__ void __launch_bounds__(256, RG_GRID_MINB) k_bisect(BisectArgs a) {
     a.out->found = acc->found;
     a.out->cells = (long long)acc->cells;
     a.out->early = (long long)acc->early;
-    a.out->seq += 1;
+    if (a.host_out) __threadfence_system();  // the fields before the token
+    *(volatile unsigned long long*)&a.out->seq = a.seq_token;
     acc->kappa_bits = 0x3ff0000000000000ull;  // 1.0
     acc->found = 1;
     acc->cells = 0ull;

@@ -170,6 +170,8 @@ struct rg_ctx {
         erl_k, path_k, path_o;
     HostBuf h_stage;
     HostBuf h_out;                  // zero-copy grid result block (pinned, UVA-mapped)
+    HostBuf h_bout;                 // zero-copy bisection result (pinned, UVA-mapped)
+    HostBuf h_jout;                 // zero-copy persistent joint search result
     DevBuf j_state;                 // joint bisection state (rg::JointState)
     DevBuf probe;                   // the bisection's kappa = 1 probe bits (ok, early)
     DevBuf loop_buf;                // the device closed loop's inputs, outputs and state
@@ -472,6 +474,8 @@ int32_t rg_destroy(rg_ctx* ctx) {
     for (DevBuf* b : bufs) b->release();
     ctx->h_stage.release();
     ctx->h_out.release();
+    ctx->h_bout.release();
+    ctx->h_jout.release();
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -695,13 +699,14 @@ int32_t rg_fill(rg_ctx* ctx, const rg_problem* prob, const double* x0, const dou
 // Spin until the grid step publishes `token` in the pinned result block.  The
 // stream is polled now and then so a failed launch surfaces as an error
 // instead of a hang.
-static cudaError_t wait_token(rg_ctx* ctx, volatile rg::GridOut* ho, unsigned long long token) {
+static cudaError_t wait_seq(rg_ctx* ctx, volatile unsigned long long* seq,
+                            unsigned long long token) {
     for (unsigned long n = 1;; ++n) {
-        if (ho->seq == token) break;
+        if (*seq == token) break;
         if ((n & 1023u) == 0) {
             const cudaError_t q = cudaStreamQuery(ctx->stream);
             if (q == cudaSuccess) {  // stream drained: the token must be there now
-                if (ho->seq == token) break;
+                if (*seq == token) break;
                 return cudaErrorUnknown;
             }
             if (q != cudaErrorNotReady) return q;
@@ -712,6 +717,10 @@ static cudaError_t wait_token(rg_ctx* ctx, volatile rg::GridOut* ho, unsigned lo
     }
     std::atomic_thread_fence(std::memory_order_acquire);
     return cudaSuccess;
+}
+
+static cudaError_t wait_token(rg_ctx* ctx, volatile rg::GridOut* ho, unsigned long long token) {
+    return wait_seq(ctx, &ho->seq, token);
 }
 
 static int32_t unpack_grid(rg_ctx* ctx, const char* h, uint32_t* row_viol, int32_t m_grid,
@@ -1161,7 +1170,17 @@ int32_t rg_bisect(rg_ctx* ctx, const rg_problem* prob, const double* x0, double 
         }
     }
     a.acc = ctx->b_acc.as<rg::BisectAcc>();
-    a.out = ctx->b_out.as<rg::BisectOut>();
+    // a synchronous call without per-scenario outputs: the last block writes the result into
+    // pinned host memory and the call spins on its token (no copy, no stream sync)
+    const bool zero_copy = !(flags & RG_ASYNC) && !kappa_k && !path_kappa;
+    if (zero_copy) {
+        RG_CUDA(ctx->h_bout.ensure(sizeof(rg::BisectOut)));
+        a.out = ctx->h_bout.as<rg::BisectOut>();
+        a.host_out = 1;
+    } else {
+        a.out = ctx->b_out.as<rg::BisectOut>();
+    }
+    a.seq_token = ++ctx->seq_ctr;
     a.tpb = tpb_for(ctx, n_sim, 1);
     grid_placement(ctx, n_sim, 1, &a.tpb, &a.smem_dyn);
     const bool timed = !(flags & RG_NO_TIMING);
@@ -1194,11 +1213,18 @@ int32_t rg_bisect(rg_ctx* ctx, const rg_problem* prob, const double* x0, double 
         }
     }
     if (flags & RG_ASYNC) return RG_OK;
-    RG_CUDA(ctx->h_stage.ensure(sizeof(rg::BisectOut)));
-    rg::BisectOut* ho = ctx->h_stage.as<rg::BisectOut>();
-    RG_CUDA(cudaMemcpyAsync(ho, ctx->b_out.p, sizeof(rg::BisectOut), cudaMemcpyDeviceToHost,
-                            ctx->stream));
-    RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    rg::BisectOut* ho;
+    if (zero_copy) {
+        ho = ctx->h_bout.as<rg::BisectOut>();
+        RG_CUDA(wait_seq(ctx, &ho->seq, a.seq_token));
+        if (timed) RG_CUDA(cudaEventSynchronize(ctx->ev1));
+    } else {
+        RG_CUDA(ctx->h_stage.ensure(sizeof(rg::BisectOut)));
+        ho = ctx->h_stage.as<rg::BisectOut>();
+        RG_CUDA(cudaMemcpyAsync(ho, ctx->b_out.p, sizeof(rg::BisectOut), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+        RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
     if (out) {
         out->kappa = ho->kappa;
         out->found = ho->found;
@@ -1393,13 +1419,44 @@ int32_t rg_bisect_joint(rg_ctx* ctx, const rg_problem* prob, const double* x0, d
             }
         }
         ctx->j_args.depth = depth;
+        // the result lands in pinned host memory; the call spins on its token
+        RG_CUDA(ctx->h_jout.ensure(sizeof(rg::JointOut)));
+        rg::JointOut* jo = ctx->h_jout.as<rg::JointOut>();
+        ctx->j_args.hout = jo;
+        ctx->j_args.seq_token = ++ctx->seq_ctr;
         const cudaError_t e = rg::launch_joint_spec(ctx->j_args, ctx->variant == rg::kTanhFma,
                                                     ctx->j_src, ctx->sm_count, ctx->stream);
+        ctx->j_args.hout = nullptr;
         if (e != cudaSuccess) {
             ctx->j_src = -1;
             return fail(RG_E_CUDA, "joint search launch failed: %s", cudaGetErrorString(e));
         }
-        return rg_joint_end(ctx, out);
+        RG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+        const cudaError_t w = wait_seq(ctx, &jo->seq, ctx->j_args.seq_token);
+        if (w != cudaSuccess) {
+            ctx->j_src = -1;
+            RG_CUDA(w);
+        }
+        const bool xchg = ctx->j_args.xchg != 0;
+        if (xchg) ctx->x_epoch += (unsigned long long)jo->rounds;  // one epoch per round
+        ctx->j_src = -1;
+        if (xchg && jo->xfail)
+            return fail(RG_E_CUDA, "fused exchange: a peer's verdicts did not arrive within %lld "
+                        "ms (every rank must run the same searches)",
+                        (long long)ctx->tune.xchg_timeout_ms);
+        if (out) {
+            out->kappa = jo->kopt;
+            out->found = jo->found;
+            out->cells = (int64_t)jo->cells;
+            out->early = (int64_t)jo->early;
+            float ms = 0.f;
+            out->kernel_ms = cudaEventSynchronize(ctx->ev1) == cudaSuccess &&
+                                     cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) == cudaSuccess
+                                 ? ms
+                                 : 0.f;
+            cudaGetLastError();
+        }
+        return RG_OK;
     }
     for (int32_t it = -1; it < n_kappa; ++it)
         if ((rc = rg_joint_iter(ctx, it, 1))) return rc;

@@ -286,6 +286,10 @@ struct BisectArgs {
     // bit k of word k/32 -- the probe's verdict and whether it ended before j*
     const unsigned* probe_ok;
     const unsigned* probe_early;
+    // the result's publication: out->seq = seq_token after the fields; host_out: *out is
+    // pinned host memory (zero copy), written behind a system-scope fence
+    unsigned long long seq_token;
+    int host_out;
 };
 
 // Joint bisection: one candidate kappa for every
@@ -341,6 +345,17 @@ struct JointArgs {
     unsigned long long xepoch0, xtimeout_ns;
     XWin* xlocal;
     XWin* const* xpeers;
+    // persistent search: the result also into pinned host memory (zero copy), published by
+    // hout->seq = seq_token behind a system-scope fence; null: device state only
+    struct JointOut* hout;
+    unsigned long long seq_token;
+};
+
+struct JointOut {
+    double kopt;
+    int found, rounds, xfail;
+    unsigned long long cells, early;
+    unsigned long long seq;
 };
 
 cudaError_t launch_joint_roll(const JointArgs& a, int it, bool fma, int src, cudaStream_t s);
