@@ -74,6 +74,9 @@ WORKLOADS = {
            "n_per_gpu": 1000, "scaling": "weak", "steps": 3000, "warmup": 20},
     "c4": {"name": "C4: robust grid step (Alg. 3) over 2^20 scenarios sharded across the GPUs",
            "n_total": 1 << 20, "scaling": "strong", "steps": 20, "warmup": 3},
+    "c1": {"name": "C1: desk-scale closed loop with the nominal bisection governor "
+                   "(bisection_rg, one scenario), the whole 2000-step trace",
+           "n_sim": 1, "scaling": "weak", "steps": 2000, "warmup": 200},
     "c3": {"name": "C3: desk-scale closed loop, 10k scenarios per step, the whole 2000-step trace",
            "n_sim": 10_000, "scaling": "weak", "steps": 2000, "warmup": 200},
     "c5": {"name": "C5: 4096 desk-scale closed-loop episodes x 10k scenarios, episodes as "
@@ -88,7 +91,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=None)
     ap.add_argument("--impl", default="own", choices=["own", "reference"])
-    ap.add_argument("--workload", default="auto", choices=["auto", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="auto", choices=["auto", "c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--n-sim", type=int, default=None,
                     help="c2: scenarios per GPU; c4: total scenarios; c5: scenarios per episode")
     ap.add_argument("--episodes", type=int, default=None, help="c5: total episodes")
@@ -117,13 +120,15 @@ def resolve(args, world):
     args.steps = spec["steps"] if args.steps is None else args.steps
     args.warmup = spec["warmup"] if args.warmup is None else args.warmup
     if args.e2e_steps is None:
-        args.e2e_steps = {"c2": 300, "c3": 0, "c4": 5, "c5": 0}[wl]
+        args.e2e_steps = {"c1": 0, "c2": 300, "c3": 0, "c4": 5, "c5": 0}[wl]
     if wl == "c2":
         spec["n_per_gpu"] = args.n_sim or spec["n_per_gpu"]
     elif wl == "c4":
         spec["n_total"] = args.n_sim or spec["n_total"]
     elif wl == "c3":
         spec["n_sim"] = args.n_sim or spec["n_sim"]
+    elif wl == "c1":
+        pass
     else:
         spec["n_sim"] = args.n_sim or spec["n_sim"]
         spec["episodes"] = args.episodes or spec["episodes"]
@@ -139,6 +144,12 @@ def config_of(wl, spec, world, j_star):
     if wl == "c4":
         return {"workload": spec["name"], "n_sim": spec["n_total"], "disturbance": "U(+-0.001)",
                 "r": R_REF, **base}
+    if wl == "c1":
+        return {"workload": spec["name"], "n_sim": 1, "n_kappa": 8,
+                "disturbance": "none in the prediction; the true plant's U(+-0.001) (desk-scale "
+                "preset)", "profile": "desk-scale [[0,0.4],[400,2.5],[1000,-2.5],[1600,0.2]]",
+                "seed": "2024 (+ rank at N>1)", "plant": "surrogate-fc", "j_star": j_star,
+                "l2": L2_NOTE}
     if wl == "c3":
         return {"workload": spec["name"], "n_sim": spec["n_sim"],
                 "disturbance": "U(+-0.001) (desk-scale preset)", "profile": "desk-scale "
@@ -308,6 +319,8 @@ def grid_sample_size(wl, spec, world):
 def cpu_baseline(cpu: RefCPU, wl, spec, world, j_star, seconds):
     """Bounded CPU baseline on rank 0 (about `seconds` of timed work): the grid step on
     every core (best rep), one serial rep, and the sequential entry point."""
+    if wl == "c1":
+        return c1_cpu_baseline(cpu, j_star, seconds)
     if wl in ("c3", "c5"):
         return closed_loop_cpu_baseline(cpu, spec, j_star, seconds)
     n = grid_sample_size(wl, spec, world)
@@ -339,6 +352,45 @@ def cpu_baseline(cpu: RefCPU, wl, spec, world, j_star, seconds):
         "sequential_alg2_1core": {"ms_per_step": t_seq * 1e3, "n_sim": n_seq,
                                   "sample": "robust_rg_sequential on the step's scenarios, 1 core"},
     }
+
+
+def c1_cpu_baseline(cpu: RefCPU, j_star, seconds):
+    """C1 on the host: the reference's own functions in run_closed_loop's loop with
+    bisection_rg at harness.py:200 (y_t, the governor step, plant.step + d_true from the
+    reference's derive_seed(seed, "plant") stream), seed 2024, as many steps from t = 0 as
+    fit in `seconds` (min 50), after 10 untimed steps (numba JIT)."""
+    if cpu.ref is None:
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "port",
+                "sample": "the C port has no closed-loop driver; c1 needs the reference"}
+    rf = cpu.ref
+    import refgov.disturbance as rdist
+    setup = rf.load_config({})
+    plant, cset, cfg = setup.plant, setup.cset, setup.governor
+    lo = np.array([a for a, _ in setup.model.ranges])
+    span = np.array([b - a for a, b in setup.model.ranges])
+
+    def loop(steps):
+        d_true = lo + span * rdist._uniform_grid(rdist.derive_seed(setup.seed, "plant"), 1, steps,
+                                                 setup.model.state_dim)[0]
+        r_sched = setup.profile.schedule(steps)
+        x, state, cells = np.zeros(plant.state_dim), rf.GovernorState(v_prev=0.0), 0
+        t0 = time.perf_counter()
+        for t in range(steps):
+            plant.output(x, state.v_prev)
+            res = rf.bisection_rg(plant, x, state, float(r_sched[t]), cset, cfg)
+            cells += int(res.diagnostics.get("sims_run", 0))
+            x = plant.step(x, res.v_applied) + d_true[t]
+        return time.perf_counter() - t0, cells
+
+    loop(10)
+    t_probe, _ = loop(50)
+    steps = max(50, min(2000, int(seconds / max(t_probe / 50, 1e-6))))
+    dt, cells = loop(steps)
+    return {"value": cells * j_star / dt, "unit": UNIT, "cores": 1, "kind": cpu.kind,
+            "steps": steps, "ms_per_closed_loop_step": dt * 1e3 / steps,
+            "sample": f"1 episode (seed {setup.seed}) x {steps} closed-loop steps from t = 0: "
+                      "refgov.bisection_rg + plant.step per step (the reference's Python loop, one "
+                      "core)", "impl": cpu.info()}
 
 
 def closed_loop_cpu_baseline(cpu: RefCPU, spec, j_star, seconds):
@@ -383,8 +435,9 @@ def run_reference(args, rank, world, wl, spec):
     cpu = RefCPU()
     j_star = args.j_star
     config = config_of(wl, spec, world, j_star)
-    if wl in ("c3", "c5"):
-        cb = closed_loop_cpu_baseline(cpu, spec, j_star, min(REF_BUDGET_S, 40.0))
+    if wl in ("c1", "c3", "c5"):
+        cb = c1_cpu_baseline(cpu, j_star, min(REF_BUDGET_S, 20.0)) if wl == "c1" else \
+            closed_loop_cpu_baseline(cpu, spec, j_star, min(REF_BUDGET_S, 40.0))
         value = cb["value"]
         line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
                 "n_gpus": world, "steps": cb.get("steps"), "warmup": 1, "higher_is_better": True,
@@ -471,6 +524,8 @@ def run_own(args, rank, world, local_rank, wl, spec):
         line = run_c5(args, rank, world, local_rank, spec, backend, cpu_group)
     elif wl == "c3":
         line = run_c3(args, rank, world, local_rank, spec, backend, cpu_group)
+    elif wl == "c1":
+        line = run_c1(args, rank, world, local_rank, spec, backend, cpu_group)
     else:
         line = run_grid(args, rank, world, local_rank, wl, spec, backend, cpu_group)
     if rank == 0:
@@ -894,6 +949,74 @@ def active_cells(V_prev, R, m_grid, interval):
     distinct = np.isfinite(Vs) & np.concatenate(
         [np.ones((Vs.shape[0], 1), bool), Vs[:, 1:] != Vs[:, :-1]], axis=1)
     return distinct.sum(axis=1)
+
+
+def run_c1(args, rank, world, local_rank, spec, backend, cpu_group):
+    """C1 (configs[0]): the desk-scale closed loop with the nominal bisection governor through
+    the public API (run_closed_loop_bisection -> rg_closed_loop_bisection: the whole trace as
+    one device kernel, k_loop_bisect).  W untimed steps of another episode, then the timed
+    episode from t = 0 for K steps; host wall clock of the whole loop, the max over ranks.
+    Cell-steps = the rollouts (sims_run) x j* summed over the timed steps."""
+    import torch
+
+    import paper_2510_08288_b200 as rg
+    from paper_2510_08288_b200.harness import ReferenceProfile, run_closed_loop_bisection
+
+    dev = f"cuda:{local_rank}"
+    j_star = args.j_star
+    plant = rg.make_plant("surrogate-fc")
+    box = rg.ConstraintSet(-0.9, 0.9, anchor=0.0)
+    model = rg.DisturbanceModel.scaled(0.001, 3)
+    cfg = rg.GovernorConfig(j_star=j_star, n_kappa=8, device=local_rank)
+    prof = ReferenceProfile(((0, 0.4), (400, 2.5), (1000, -2.5), (1600, 0.2)))
+    seed = 2024 + rank
+    if args.warmup > 0:
+        run_closed_loop_bisection(plant, box, model, cfg, prof, args.warmup, seed + 1000)
+    torch.cuda.synchronize()
+    if MULTI:
+        torch.distributed.barrier()
+    from paper_2510_08288_b200 import _capi
+
+    ctx = _capi.context(local_rank)
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    t0 = time.perf_counter()
+    out = run_closed_loop_bisection(plant, box, model, cfg, prof, args.steps, seed)
+    wall = time.perf_counter() - t0
+    clocks = sampler.stop()
+    cells = sum(int(r.diagnostics["sims_run"]) for r, _ in out)
+    total = _max_over_ranks(wall, world, dev)
+    if MULTI:
+        t = torch.tensor([cells], dtype=torch.int64, device=dev)
+        torch.distributed.all_reduce(t)
+        cells = int(t.item())
+    value = cells * j_star / total
+    roof = wall_roofline(value / world, local_rank,
+                         "host wall clock of the closed loop per GPU (one device kernel for the "
+                         "trace): a lower bound on the kernel's rate")
+    cb = None
+    if MULTI:
+        torch.distributed.barrier()
+    if rank == 0 and not args.no_cpu_baseline:
+        cb = c1_cpu_baseline(RefCPU(), j_star, min(args.cpu_seconds, 20.0))
+    if MULTI:
+        torch.distributed.barrier(group=cpu_group)
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": spec["scaling"], "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": config_of("c1", spec, world, j_star),
+        "parallelism": f"one closed-loop episode per GPU x{world} (replicas)",
+        "run": {"found_steps": sum(1 for r, _ in out if r.feasible),
+                "rollouts_total": cells,
+                "timing": "host wall clock of the whole timed closed loop, max over ranks"},
+        # per step r_t and d_true[t] in (32 B); kappa, v, y, cells, early, device ns and the
+        # found flag out (49 B), copied once around the one launch
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 32, "d2h_bytes_per_step": 49,
+                "note": "the timed loop is the public API end to end: run_closed_loop_bisection "
+                        "-> rg_closed_loop_bisection (one device kernel for the whole trace)"},
+        "roofline": roof, "cpu_baseline": cb, "clocks": clocks, "gpu_launches": 1,
+    }
 
 
 def run_c3(args, rank, world, local_rank, spec, backend, cpu_group):
