@@ -14,8 +14,12 @@ scenario-steps/sec vs FP64 roofline", unit cell-steps/s):
       [r*n/N, (r+1)*n/N) of one stream (no scenario traffic); the per-row violation
       counts go through one all-reduce (MAX, int32) per step and every rank extracts
       the same row on its device.
+  c1  (configs[0])  the desk-scale closed loop with the nominal bisection governor
+      (bisection_rg, one scenario, n_kappa 8), the whole 2000-step trace, as one device
+      kernel (rg_closed_loop_bisection); the reference arm runs the reference's own loop.
   c3  (configs[2])  the desk-scale closed loop at 10k scenarios per step, the whole
-      2000-step setpoint trace (seed 2024), governor on the device, true plant on the host;
+      2000-step setpoint trace (seed 2024): the whole loop as one device kernel
+      (rg_closed_loop: governor, kappa, v_t and the true plant on the device);
       at N>1 every rank runs its own episode (seed 2024 + rank, replicas).
   c5  (configs[4])  4096 independent desk-scale closed-loop episodes x 10k scenarios
       (episode seeds 2024 + e), episodes spread over the N GPUs as replicas; K timed
