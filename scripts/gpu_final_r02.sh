@@ -24,3 +24,9 @@ print(f, "value %.4g" % (d.get("value") or 0), "ms/step", d.get("ms_per_step"),
       "e2e", (d.get("e2e") or {}).get("ms_per_step"), "frac", (d.get("roofline") or {}).get("frac"))
 PY
 done
+timeout 300 python bench.py --workload c1 > gpurun_out/final_c1.jsonl 2>&1; echo "c1 rc=$?"
+timeout 300 python bench.py --impl reference --workload c1 > gpurun_out/final_c1_reference.jsonl 2>&1; echo "c1 ref rc=$?"
+for f in gpurun_out/final_c1*.jsonl; do
+  python -c "
+import json; d=json.loads([l for l in open('$f') if l.startswith('{')][-1]); print('$f', 'ms/step', d.get('ms_per_step'))"
+done
