@@ -36,7 +36,7 @@ def test_config_is_shared_by_both_arms():
     sys.path.insert(0, str(ROOT))
     import bench
 
-    for wl in ("c2", "c3", "c4", "c5"):
+    for wl in ("c1", "c2", "c3", "c4", "c5"):
         spec = dict(bench.WORKLOADS[wl])
         a = bench.config_of(wl, spec, 4, 256)
         b = bench.config_of(wl, dict(spec), 4, 256)
@@ -88,3 +88,19 @@ def test_issue_model_arithmetic():
     ncu10k = bench._ncu_summary("k_grid_ncu_10k.json")
     assert abs(big["cycles_per_warp_step"] - (ncu10k["fp64_instr_per_cell_step"]
                                               + ncu10k["instr_per_cell_step"])) < 1e-9
+
+
+def test_reference_arm_c1_line():
+    """C1's reference arm: the reference's own bisection loop on one host core (when the
+    reference is staged; the C port has no closed-loop driver and reports value None)."""
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
+                          "--workload", "c1", "--cpu-seconds", "2"],
+                         capture_output=True, text=True, check=True, timeout=600)
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["config"]["workload"].startswith("C1")
+    cb = d["cpu_baseline"]
+    assert cb["kind"] in ("reference", "port") and cb["cores"] == 1
+    if cb["kind"] == "reference":
+        assert d["value"] == cb["value"] > 0 and d["ms_per_step"] > 0
