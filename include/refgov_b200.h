@@ -339,7 +339,9 @@ RG_API int32_t rg_fp64_peak(rg_ctx *ctx, double *flops_per_s);
  * the box after the disturbance (harness.py:222-224), or -- with infeasible_error --
  * the first step without a feasible row (InfeasibleError).  res->steps_done rows were
  * written.  x_out (3 doubles, may be NULL): the final state.
- * With m_grid <= 64 and every r[t] finite the whole trace runs on the device as one
+ * With m_grid <= 64, every r[t] finite and one row's scenarios within one wave of the time-split
+ * form (ceil(n_sim / 32) <= 3 x the SM count: 14,208 scenarios on a B200) the whole trace runs on
+ * the device as one
  * cooperative kernel (k_loop_ts: the steps on the time-split form, and between them the
  * row, kappa, v_t, the true plant with numpy's tanh and the next step's row plan, all on
  * the device; wall_us_out then holds each governor step's device time); the "no_device_loop"

@@ -2183,10 +2183,11 @@ int32_t rg_closed_loop(rg_ctx* ctx, const rg_problem* prob, int32_t m_grid, int3
     res->abort_step = -1;
     // the whole trace on the device when it runs on the time-split form with host-planned rows
     // (the options that disable those keep the per-step loop), every reference is finite and
-    // a step's units (rows x scenario words) index as int
+    // a one-row step fits one pass (above that a step's k_grid launch beats many passes)
     ctx->last_loop_device = 0;
     bool dev_ok = !ctx->tune.no_device_loop && !ctx->tune.no_ts && !ctx->tune.no_row_plan &&
-                  m_grid <= rg::kListMax && n_sim <= ((int64_t)1 << 30) && isfinite(v0);
+                  m_grid <= rg::kListMax &&
+                  (n_sim + 31) / 32 <= (int64_t)rg::kTsUnits * ctx->sm_count && isfinite(v0);
     for (int32_t t = 0; dev_ok && t < steps; ++t) dev_ok = isfinite(r[t]);
     if (dev_ok) {
         rc = closed_loop_device(ctx, prob, m_grid, prefix_mode, infeasible_error, x, v0, steps, r,

@@ -187,3 +187,22 @@ def test_device_bisection_loop_overflow_raises_like_the_plant():
                                       [0.4] * 5, 5, 3, x0=x0, native=native)
         msgs.append((str(e.value), e.value.state_index))
     assert msgs[0] == msgs[1]
+
+
+def test_large_scenario_sets_keep_the_per_step_loop():
+    """Above one wave of the time-split form for a single row (ceil(n_sim / 32) > 3 x SMs)
+    rg_closed_loop launches a grid step per closed-loop step (k_grid for the big steps) rather
+    than many passes per step; the rows still equal the Python loop's."""
+    from paper_2510_08288_b200 import _capi
+
+    import torch
+
+    ctx = _capi.context(0)
+    n = 32 * 3 * torch.cuda.get_device_properties(0).multi_processor_count + 64
+    cfg = rg.GovernorConfig(j_star=64, m_grid=16, n_sim=n)
+    prof = np.concatenate([np.full(15, 0.4), np.full(15, 2.0)])
+    model = rg.DisturbanceModel.scaled(0.001, 3)
+    nat = _strip_wall(run_closed_loop(PLANT, BOX, model, cfg, prof, 30, 12))
+    assert ctx.get_option("last_loop_device") == 0
+    py = _strip_wall(run_closed_loop(PLANT, BOX, model, cfg, prof, 30, 12, native=False))
+    _same(nat, py)
