@@ -67,7 +67,13 @@ constexpr int kListMax = 64;  // host-planned grid steps: at most this many cand
 // and one x1/x3-chain warp for each of up to kTsUnits units (32 scenarios of a row), chunks
 // of kTsChunk steps through kTsSlots shared-memory slots.  The staged scenario block carries
 // kTsPadSteps steps of padding past j* for the producer's look-ahead loads.
-constexpr int kTsTanhWarps = 12, kTsUnits = 3, kTsChunk = 8, kTsSlots = 3;
+#ifndef RG_TS_CHUNK
+#define RG_TS_CHUNK 8
+#endif
+#ifndef RG_TS_SLOTS
+#define RG_TS_SLOTS 3
+#endif
+constexpr int kTsTanhWarps = 12, kTsUnits = 3, kTsChunk = RG_TS_CHUNK, kTsSlots = RG_TS_SLOTS;
 constexpr int kTsThreads = (kTsTanhWarps + 2 * kTsUnits) * 32;
 constexpr int kTsSmemDyn =
     kTsSlots * kTsChunk * 6 * kTsUnits * 32 * 8 + kTsSlots * kTsUnits * 32 * 4;
